@@ -1,0 +1,217 @@
+"""Sparse-pattern, value and dense-operand generators (seeded, synthetic).
+
+Every generator returns CSR in the boundary layout of include/accspmm.h:
+``rowptr`` int64[M+1], ``colidx`` int32[nnz] strictly ascending within a row.
+Recipes follow SURVEY.md §8(d) "Generator recipes"; shapes follow PAPER.md
+Table 1 and BASELINE.json ``configs``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "_native.so")
+_SRC = os.path.join(_HERE, "_native.c")
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """gcc -fopenmp the plumbing helpers (pairs -> CSR, DC-SBM draws)."""
+    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
+        tmp = _SO + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O3", "-fopenmp", "-fPIC", "-shared", "-std=c11", _SRC, "-o", tmp])
+        os.replace(tmp, _SO)
+    return _SO
+
+
+def _native():
+    global _lib
+    if _lib is None:
+        build()
+        lib = ctypes.CDLL(_SO)
+        P, I = ctypes.c_void_p, ctypes.c_int64
+        lib.gen_pairs_to_csr.argtypes = [I, P, P, I, I, ctypes.c_int, ctypes.c_int, P, P]
+        lib.gen_pairs_to_csr.restype = I
+        lib.gen_dcsbm_draw.argtypes = [I, I, P, P, P, P, P, P, P, P, ctypes.c_double, ctypes.c_uint64, P, P]
+        lib.gen_dcsbm_draw.restype = None
+        _lib = lib
+    return _lib
+
+
+def _p(a):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+@dataclass
+class Csr:
+    M: int
+    K: int
+    rowptr: np.ndarray  # int64[M+1]
+    colidx: np.ndarray  # int32[nnz]
+
+    @property
+    def nnz(self) -> int:
+        return int(self.rowptr[-1]) if self.M > 0 else 0
+
+    def row_ids(self) -> np.ndarray:
+        return np.repeat(np.arange(self.M, dtype=np.int64), np.diff(self.rowptr))
+
+
+def csr_from_pairs(rows, cols, M: int, K: int, symmetric: bool = False, drop_diag: bool = False) -> Csr:
+    """Canonical CSR (sorted, unique columns per row) from (row, col) pairs.
+
+    ``symmetric`` also inserts (col, row); ``drop_diag`` drops (i, i)."""
+    rows = np.ascontiguousarray(rows, dtype=np.int64).ravel()
+    cols = np.ascontiguousarray(cols, dtype=np.int64).ravel()
+    rowptr = np.zeros(M + 1, dtype=np.int64)
+    colidx = np.empty(rows.size * (2 if symmetric else 1), dtype=np.int32)
+    nnz = _native().gen_pairs_to_csr(rows.size, _p(rows), _p(cols), M, K, int(symmetric),
+                                     int(drop_diag), _p(rowptr), _p(colidx))
+    if nnz < 0:
+        raise ValueError("pair index out of range")
+    return Csr(M, K, rowptr, colidx[:nnz].copy())
+
+
+# --------------------------------------------------------------------------- patterns
+
+def uniform_random(M: int, K: int, nnz: int, seed: int) -> Csr:
+    """Config T: nnz distinct positions sampled without replacement."""
+    rng = np.random.default_rng(seed)
+    k = rng.choice(M * K, size=nnz, replace=False)
+    r, c = np.divmod(np.sort(k), K)
+    return csr_from_pairs(r, c, M, K)
+
+
+def stencil27(nx: int) -> Csr:
+    """Config S(i): 27-point stencil on an nx^3 grid, row id = x + nx*y + nx^2*z."""
+    n = nx ** 3
+    idx = np.arange(n, dtype=np.int64)
+    x, y, z = idx % nx, (idx // nx) % nx, idx // (nx * nx)
+    rows, cols = [], []
+    for dz in (-1, 0, 1):
+        for dy in (-1, 0, 1):
+            for dx in (-1, 0, 1):
+                ok = ((x + dx >= 0) & (x + dx < nx) & (y + dy >= 0) & (y + dy < nx)
+                      & (z + dz >= 0) & (z + dz < nx))
+                rows.append(idx[ok])
+                cols.append(idx[ok] + dx + nx * dy + nx * nx * dz)
+    return csr_from_pairs(np.concatenate(rows), np.concatenate(cols), n, n)
+
+
+def banded_random(M: int, per_row: int, halfwidth: int, seed: int) -> Csr:
+    """Config S(ii): per_row uniform draws within +-halfwidth of the diagonal, deduplicated."""
+    rng = np.random.default_rng(seed)
+    r = np.repeat(np.arange(M, dtype=np.int64), per_row)
+    c = np.clip(r + rng.integers(-halfwidth, halfwidth + 1, size=r.size), 0, M - 1)
+    return csr_from_pairs(r, c, M, M)
+
+
+def dcsbm(n: int, target_nnz: int, communities: int, alpha: float, mu: float,
+          dmax: float, seed: int, oversample: float = 1.0) -> Csr:
+    """Configs R / P: symmetric degree-corrected SBM, labels uncorrelated with ids.
+
+    1. comm ~ U{0..C-1}; 2. theta = 1 + Lomax(alpha-1), rescaled to mean
+    target_nnz/n and capped at dmax; 3. E = oversample*target_nnz/2 edges,
+    src ~ Cat(theta), dst ~ Cat(theta) with prob. mu else Cat(theta | comm[src]);
+    4. drop self-loops, symmetrise, deduplicate.
+    """
+    rng = np.random.default_rng(seed)
+    comm = rng.integers(0, communities, size=n)
+    theta = 1.0 + rng.pareto(alpha - 1.0, size=n)
+    theta *= (target_nnz / n) / theta.mean()
+    theta = np.minimum(theta, dmax)
+    E = int(oversample * target_nnz / 2)
+    cum = np.cumsum(theta)
+    # within-community draws: vertices sorted by community, per-community cumulative weights
+    order = np.argsort(comm, kind="stable").astype(np.int64)
+    cum_sorted = np.cumsum(theta[order])
+    starts = np.searchsorted(comm[order], np.arange(communities), side="left").astype(np.int64)
+    ends = np.searchsorted(comm[order], np.arange(communities), side="right").astype(np.int64)
+    base = np.where(starts > 0, cum_sorted[np.maximum(starts - 1, 0)], 0.0)
+    tot = np.where(ends > starts, cum_sorted[np.maximum(ends - 1, 0)] - base, 0.0)
+    comm32 = comm.astype(np.int32)
+    src = np.empty(E, dtype=np.int64)
+    dst = np.empty(E, dtype=np.int64)
+    _native().gen_dcsbm_draw(E, n, _p(cum), _p(comm32), _p(order), _p(cum_sorted), _p(starts), _p(ends),
+                             _p(base), _p(tot), float(mu), int(seed) & 0xFFFFFFFFFFFFFFFF, _p(src), _p(dst))
+    return csr_from_pairs(src, dst, n, n, symmetric=True, drop_diag=True)
+
+
+def sbm(n: int, blocks: int, p_in: float, p_out: float, seed: int, shuffle: bool = True) -> Csr:
+    """Symmetric 0/1 stochastic block model, no self-loops, optional label shuffle."""
+    rng = np.random.default_rng(seed)
+    b = np.arange(n) // (n // blocks)
+    iu, ju = np.triu_indices(n, 1)
+    p = np.where(b[iu] == b[ju], p_in, p_out)
+    keep = rng.random(iu.size) < p
+    r, c = iu[keep], ju[keep]
+    if shuffle:
+        lab = rng.permutation(n)
+        r, c = lab[r], lab[c]
+    return csr_from_pairs(r, c, n, n, symmetric=True)
+
+
+def identity(n: int) -> Csr:
+    i = np.arange(n)
+    return csr_from_pairs(i, i, n, n)
+
+
+def permutation_matrix(n: int, seed: int) -> Csr:
+    """A = P with one 1 per row at column sigma(i) (SURVEY §8(c) C-4, a7/a10 fixture)."""
+    rng = np.random.default_rng(seed)
+    return csr_from_pairs(np.arange(n), rng.permutation(n), n, n)
+
+
+def two_cliques(k: int, seed: int | None = None, bridge: bool = True) -> Csr:
+    """Two k-cliques (optionally joined by one edge), labels optionally shuffled."""
+    rows, cols = [], []
+    for off in (0, k):
+        for i in range(k):
+            for j in range(k):
+                if i != j:
+                    rows.append(off + i)
+                    cols.append(off + j)
+    if bridge:
+        rows += [k - 1, k]
+        cols += [k, k - 1]
+    rows, cols = np.array(rows, dtype=np.int64), np.array(cols, dtype=np.int64)
+    if seed is not None:
+        lab = np.random.default_rng(seed).permutation(2 * k)
+        rows, cols = lab[rows], lab[cols]
+    return csr_from_pairs(rows, cols, 2 * k, 2 * k)
+
+
+def star(leaves: int) -> Csr:
+    """K_{1,leaves}: centre 0 joined to 1..leaves."""
+    r = np.concatenate([np.zeros(leaves, int), np.arange(1, leaves + 1)])
+    c = np.concatenate([np.arange(1, leaves + 1), np.zeros(leaves, int)])
+    return csr_from_pairs(r, c, leaves + 1, leaves + 1)
+
+
+# --------------------------------------------------------------------------- values
+
+def values_uniform(nnz: int, seed: int) -> np.ndarray:
+    """A values ~ U[-1, 1) float32 (SURVEY §8(d) 'Values and B')."""
+    return np.random.default_rng(seed).uniform(-1.0, 1.0, nnz).astype(np.float32)
+
+
+def values_int(nnz: int, seed: int) -> np.ndarray:
+    """Integer variant: A in {-3..3} \\ {0} (bit-exact in TF32/FP16 x FP32 accumulate)."""
+    rng = np.random.default_rng(seed)
+    mag = rng.integers(1, 4, size=nnz)
+    sgn = np.where(rng.random(nnz) < 0.5, -1, 1)
+    return (mag * sgn).astype(np.float32)
+
+
+def dense_normal(K: int, N: int, seed: int) -> np.ndarray:
+    return np.random.default_rng(seed).standard_normal((K, N), dtype=np.float32)
+
+
+def dense_int(K: int, N: int, seed: int) -> np.ndarray:
+    """Integer variant: B in {-8..8}."""
+    return np.random.default_rng(seed).integers(-8, 9, size=(K, N)).astype(np.float32)

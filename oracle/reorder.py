@@ -1,0 +1,159 @@
+"""Data-affinity-based reordering, Algorithm 1 (TEST INFRASTRUCTURE ONLY; small graphs).
+
+PAPER.md §3.2, Algorithm 1, Eq. (1).
+The reordering is a heuristic: many orderings are valid, so the exact ordering
+is "parity unpinned" -- it is pinned only by invariants
+(bijection, Q/dQ closed forms, clique contiguity, MeanNNZTC gain).
+
+Readings:
+  * graph: pattern(A or A^T) without the diagonal, weight 1 per edge;
+  * Eq. (1) is global Q; the merge gain is dQ(u,v) = 2*(w_uv/2m - a_u*a_v/(2m)^2) (Q9);
+  * Step I is ONE pass over vertices in ascending degree, ties by id (Alg. 1 l.2-8,
+    Q11); argmax-dQ ties go to the smallest community id; merge iff dQ > 0;
+  * the dendrogram DFS visits roots in ascending id, each node before its children,
+    children in merge order -- the leaf (vertex) sequence;
+  * Step II (Alg. 1 l.9-27): the candidate set of "u in DFS that has most common
+    nbrs with v" is the next L unvisited vertices in DFS order, neighbour lists
+    capped at their first H entries (ascending id); ties by DFS order;
+    no candidate with >= 1 common neighbour -> continue with the next DFS vertex.
+  * non-square A -> identity (Q14).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+CAND_WINDOW = 64   # L
+HUB_CAP = 128      # H
+
+
+def affinity_graph(n: int, rowptr, colidx):
+    """Sorted adjacency lists of pattern(A or A^T) minus self-loops."""
+    rowptr = np.asarray(rowptr, dtype=np.int64)
+    colidx = np.asarray(colidx, dtype=np.int64)
+    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(rowptr))
+    keep = rows != colidx
+    r, c = rows[keep], colidx[keep]
+    keys = np.unique(np.concatenate([r * n + c, c * n + r]))
+    src, dst = keys // n, keys % n
+    adj = [[] for _ in range(n)]
+    for s, d in zip(src.tolist(), dst.tolist()):
+        adj[s].append(d)
+    return adj
+
+
+def modularity(adj, comm) -> float:
+    """Eq. (1) as the global Q = (1/2m) sum_{i,j} (A_ij - k_i k_j / 2m) delta(s_i, s_j)."""
+    n = len(adj)
+    k = [len(a) for a in adj]
+    m2 = sum(k)
+    if m2 == 0:
+        raise ValueError("empty graph")
+    q = 0.0
+    for i in range(n):
+        nb = set(adj[i])
+        for j in range(n):
+            if comm[i] == comm[j]:
+                q += (1.0 if j in nb else 0.0) - k[i] * k[j] / m2
+    return q / m2
+
+
+def delta_q(w_uv: float, a_u: float, a_v: float, m2: float) -> float:
+    """Merge gain of joining communities u and v."""
+    return 2.0 * (w_uv / m2 - a_u * a_v / (m2 * m2))
+
+
+def dendrogram(adj):
+    """Alg. 1 Step I (l.1-8): returns (parent, children, roots) of the merge forest."""
+    n = len(adj)
+    deg = [len(a) for a in adj]
+    m2 = float(sum(deg))
+    parent = list(range(n))
+    a = [float(d) for d in deg]
+    children = [[] for _ in range(n)]
+    edges = [dict((x, 1) for x in adj[v]) for v in range(n)]
+
+    def find(x):
+        root = x
+        while parent[root] != root:
+            root = parent[root]
+        while parent[x] != root:
+            parent[x], x = root, parent[x]
+        return root
+
+    for v in sorted(range(n), key=lambda u: (deg[u], u)):   # l.2 ascending degree
+        if deg[v] == 0 or m2 == 0:
+            continue
+        acc = {}
+        for x, w in edges[v].items():
+            r = find(x)
+            if r != v:
+                acc[r] = acc.get(r, 0) + w
+        edges[v] = acc
+        best, best_dq = -1, 0.0
+        for r in sorted(acc):                                # l.4 argmax dQ, smallest id on ties
+            dq = delta_q(acc[r], a[r], a[v], m2)
+            if best < 0 or dq > best_dq:
+                best, best_dq = r, dq
+        if best >= 0 and best_dq > 0.0:                      # l.5-7 merge v into u
+            u = best
+            parent[v] = u
+            a[u] += a[v]
+            eu = edges[u]
+            for x, w in acc.items():
+                eu[x] = eu.get(x, 0) + w
+            edges[v] = {}
+            children[u].append(v)
+    roots = [v for v in range(n) if parent[v] == v]
+    return parent, children, roots
+
+
+def dfs_sequence(children, roots):
+    seq = []
+    for r in roots:
+        stack = [r]
+        while stack:
+            x = stack.pop()
+            seq.append(x)
+            stack.extend(reversed(children[x]))
+    return seq
+
+
+def ordering(adj, children, roots, L: int = CAND_WINDOW, H: int = HUB_CAP):
+    """Alg. 1 Step II (l.9-27): returns perm new -> old."""
+    n = len(adj)
+    seq = dfs_sequence(children, roots)
+    capped = [a[:H] for a in adj]
+    visited = [False] * n
+    perm = []
+    alive = list(seq)  # unvisited vertices in DFS order (small graphs: a plain list)
+
+    def assign(x):
+        visited[x] = True
+        perm.append(x)
+        alive.remove(x)
+
+    for v in seq:
+        if visited[v]:
+            continue
+        assign(v)                                            # l.15-17
+        while alive:                                         # l.18 while-loop
+            nv = set(capped[v])
+            best, best_c = -1, 0
+            for u in alive[:L]:
+                c = sum(1 for x in capped[u] if x in nv)
+                if c > best_c:
+                    best, best_c = u, c
+            if best < 0:
+                break
+            assign(best)                                     # l.22-24
+            v = best                                         # l.25
+    return np.asarray(perm, dtype=np.int64)
+
+
+def reorder(M: int, K: int, rowptr, colidx, L: int = CAND_WINDOW, H: int = HUB_CAP):
+    """Algorithm 1 end to end: perm new->old (identity when M != K, Q14)."""
+    if M != K:
+        return np.arange(M, dtype=np.int64)
+    adj = affinity_graph(M, rowptr, colidx)
+    _, children, roots = dendrogram(adj)
+    return ordering(adj, children, roots, L, H)

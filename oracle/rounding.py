@@ -1,0 +1,42 @@
+"""rho: the input rounding both sides apply before the product (TEST INFRASTRUCTURE ONLY).
+
+PAPER.md P:308 fixes the arithmetic type ("we mainly focus on tf32 datatype")
+but never the rounding mode; SURVEY §8(c) Q1 adopts round-to-nearest, ties
+away from zero (the semantics of PTX ``cvt.rna.tf32.f32``), applied
+unconditionally on the float32 bit pattern:
+
+    u = bits(x);  u = (u + 0x1000) & 0xFFFFE000
+
+This is written out here as that definition.  Consequences kept on purpose
+("Rounding rho"): Inf stays Inf, a NaN with payload >= 0x1000
+stays NaN, values with |bits| >= 0x7F7FF000 overflow to +-Inf.
+
+FP16 path: IEEE round-to-nearest-even, i.e. numpy's
+float32 -> float16 cast.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def tf32_rna(x) -> np.ndarray:
+    """TF32 round-to-nearest, ties away from zero, kept in float32 bits."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    u = x.view(np.uint32).astype(np.uint64)
+    u = (u + np.uint64(0x1000)) & np.uint64(0xFFFFE000)
+    return u.astype(np.uint32).view(np.float32).reshape(x.shape)
+
+
+def fp16_rne(x) -> np.ndarray:
+    """IEEE binary16 round-to-nearest-even."""
+    with np.errstate(over="ignore"):
+        return np.asarray(x, dtype=np.float32).astype(np.float16)
+
+
+def rho(x, precision: str) -> np.ndarray:
+    """Rounded operand as float32 (exactly representable), for the FP64 oracle."""
+    if precision == "tf32":
+        return tf32_rna(x)
+    if precision == "fp16":
+        return fp16_rne(x).astype(np.float32)
+    raise ValueError(precision)

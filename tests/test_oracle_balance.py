@@ -1,0 +1,92 @@
+"""Pins for oracle/balance.py -- Eq. (3), Eq. (4)."""
+import numpy as np
+import pytest
+
+from oracle import balance as ob
+
+
+def test_ibd_worked_values():
+    assert ob.ibd([2, 2, 2, 2]) == 0.0
+    assert ob.ibd([1, 3, 8, 4]) == 2.0                  # avg 4, (3+1+4+0)/4
+    assert ob.ibd([0, 16]) == 8.0                       # exactly at threshold: not "exceeds" (Q24)
+    with pytest.raises(ValueError):
+        ob.ibd([])
+
+
+def test_ibd_permutation_invariant_and_zero_iff_equal():
+    rng = np.random.default_rng(0)
+    for _ in range(50):
+        x = rng.integers(0, 50, size=int(rng.integers(1, 40)))
+        assert ob.ibd(x) == pytest.approx(ob.ibd(rng.permutation(x)), rel=1e-12, abs=0)
+        assert (ob.ibd(x) == 0.0) == bool(np.all(x == x[0]))
+
+
+def test_eq4_worked_value():
+    # A800, FeatureDim 128, 4 blocks: Load = WB = 8*128*4*4 / 1935e9, MMA = 8*15*128 / 156e12
+    load = 16384 / 1935e9
+    mma = 15360 / 156e12
+    assert ob.eq4_time("A800", 128, 4) == pytest.approx(2 * load + mma, rel=1e-12)
+    assert ob.eq4_time("A800", 128, 4) == pytest.approx(1.7033e-8, rel=1e-4)
+
+
+def test_eq4_linearity_and_monotonicity():
+    rng = np.random.default_rng(1)
+    for _ in range(1000):
+        p = ["RTX4090", "A800", "H100"][int(rng.integers(0, 3))]
+        fd, tb = int(rng.integers(1, 1024)), int(rng.integers(1, 64))
+        t = ob.eq4_time(p, fd, tb)
+        assert ob.eq4_time(p, fd, tb + 1) > t and ob.eq4_time(p, fd + 1, tb) > t
+        mma = ob.eq4_time(p, fd, 0)
+        assert ob.eq4_time(p, fd, 2 * tb) - mma == pytest.approx(2 * (t - mma), rel=1e-9)
+
+
+def _powerlaw_rwo(rng, W):
+    nb = np.minimum((rng.pareto(1.2, W) * 3).astype(np.int64), 400)
+    nb[rng.random(W) < 0.1] = 0
+    return np.concatenate([[0], np.cumsum(nb)])
+
+
+@pytest.mark.parametrize("seed", range(20))
+@pytest.mark.parametrize("cap", [32, 100])
+@pytest.mark.parametrize("precision", ["tf32", "fp16"])
+def test_schedule_coverage_and_cap(seed, cap, precision):
+    rng = np.random.default_rng(seed)
+    rwo = _powerlaw_rwo(rng, int(rng.integers(1, 500)))
+    units = ob.build_units(rwo, cap, True, precision)
+    ob.check_coverage(units, rwo)
+    wb = ob.wb_cost(precision)
+    for (w0, nw, b0, b1, split, seg, nseg, slot) in units:
+        assert b1 - b0 <= cap and nw <= ob.WMAX
+        if split == ob.NO_SPLIT:
+            cost = sum(int(rwo[w + 1] - rwo[w]) + wb for w in range(w0, w0 + nw))
+            assert nw == 1 or cost <= cap + wb
+        else:
+            assert nseg == -(-int(rwo[w0 + 1] - rwo[w0]) // cap) and 0 <= seg < nseg
+    # identity schedule: one unit per window, one write-back each
+    ident = ob.build_units(rwo, cap, False, precision)
+    assert len(ident) == rwo.size - 1
+    ob.check_coverage(ident, rwo)
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_balanced_max_over_mean_not_worse(seed):
+    """S:575 acceptance 6: balanced max/mean predicted time <= identity schedule's on power-law plans."""
+    rng = np.random.default_rng(100 + seed)
+    rwo = _powerlaw_rwo(rng, 300)
+    nonempty = [(w, 1, int(rwo[w]), int(rwo[w + 1]), 0, 0, 1, 0) for w in range(rwo.size - 1)
+                if rwo[w + 1] > rwo[w]]
+    bal = [u for u in ob.build_units(rwo, 32, True) if u[3] > u[2]]
+    assert ob.mean_ratio(ob.unit_times(bal, rwo)) <= ob.mean_ratio(ob.unit_times(nonempty, rwo))
+
+
+def test_split_segments_even():
+    rwo = np.array([0, 100])
+    units = ob.build_units(rwo, 32, True)
+    assert [(u[2], u[3]) for u in units] == [(0, 25), (25, 50), (50, 75), (75, 100)]
+    assert [u[7] for u in units] == [0, 1, 2, 3]
+
+
+def test_auto_cap():
+    assert ob.auto_cap(0) == 32 and ob.auto_cap(10) == 32
+    assert ob.auto_cap(14_000_000) == 1504
+    assert ob.auto_cap(10 ** 10) == 4096

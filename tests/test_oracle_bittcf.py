@@ -1,0 +1,157 @@
+"""Pins for the reference BitTCF encoder/decoder (oracle/bittcf.py) -- P:250-273."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import gen
+from oracle import bittcf as bt
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _enc(A, vals=None):
+    return bt.encode(A.M, A.K, A.rowptr, A.colidx, vals)
+
+
+def _brute_encode(A):
+    """Pure-Python, window-by-window encoder (small inputs) for cross-checking the vectorised one."""
+    W = (A.M + 7) // 8
+    rwo, tco, a2b, bits = [0], [0], [], []
+    for w in range(W):
+        rows = range(8 * w, min(8 * w + 8, A.M))
+        U = sorted({int(A.colidx[p]) for i in rows for p in range(A.rowptr[i], A.rowptr[i + 1])})
+        nb = (len(U) + 7) // 8
+        for t in range(nb):
+            lanes = U[8 * t:8 * t + 8]
+            a2b += lanes + [0] * (8 - len(lanes))
+            m = 0
+            for i in rows:
+                for p in range(A.rowptr[i], A.rowptr[i + 1]):
+                    c = int(A.colidx[p])
+                    if c in lanes:
+                        m |= 1 << ((i - 8 * w) * 8 + lanes.index(c))
+            bits.append(m)
+            tco.append(tco[-1] + bin(m).count("1"))
+        rwo.append(rwo[-1] + nb)
+    return rwo, tco, a2b, bits
+
+
+def test_golden_fixtures():
+    with open(os.path.join(GOLDEN, "bittcf_fixtures.json")) as f:
+        fx = json.load(f)
+    for case in fx["cases"]:
+        A = gen.csr_from_pairs(case["rows"], case["cols"], case["M"], case["K"])
+        F = _enc(A)
+        assert F["RowWindowOffset"].tolist() == case["RowWindowOffset"], case["name"]
+        assert F["TCOffset"].tolist() == case["TCOffset"], case["name"]
+        assert F["SparseAToB"].tolist() == case["SparseAToB"], case["name"]
+        assert [int(x) for x in F["TCLocalBit"]] == [int(x, 16) for x in case["TCLocalBit"]], case["name"]
+        assert bt.bittcf_index_bytes(case["M"], F["NB"]) == case["index_bytes"], case["name"]
+
+
+def test_byte_formula_worked_values():
+    # substitution into P:253
+    assert bt.bittcf_index_bytes(8, 1) == 56
+    assert bt.bittcf_index_bytes(16, 3) == 148
+    assert bt.bittcf_index_bytes(8, 0) == 12
+    # S:309-312 ME-TCF: tie at 8 nnz, BitTCF wins at 64, ME-TCF wins at 1
+    assert bt.metcf_index_bytes(8, 1, 8) == 56
+    assert bt.metcf_index_bytes(8, 1, 64) == 112
+    assert bt.metcf_index_bytes(8, 1, 1) == 49
+
+
+def test_single_bit_probes_pin_bit_order():
+    """64 probes: target nnz at (r, lane c); lanes 0..c-1 filled in row r'=(r+1)%8 (SURVEY C-4 a8(ii))."""
+    for r in range(8):
+        for c in range(8):
+            rp = (r + 1) % 8
+            rows = [rp] * c + [r]
+            cols = list(range(c)) + [c]
+            A = gen.csr_from_pairs(rows, cols, 8, 8)
+            F = _enc(A)
+            expect = (((1 << c) - 1) << (8 * rp)) | (1 << (8 * r + c))
+            assert int(F["TCLocalBit"][0]) == expect
+
+
+def test_value_order_and_decode_offset():
+    # mask bits {0,5,9} -> offset of bit 9 = 2
+    assert bt.value_index((1 << 0) | (1 << 5) | (1 << 9), 9) == 2
+    A = gen.csr_from_pairs([0, 0, 1], [10, 20, 10], 8, 32)
+    F = _enc(A, np.float32([1.0, 2.0, 3.0]))
+    # bits: (r0,l0)=0, (r0,l1)=1, (r1,l0)=8 -> values ascending by bit
+    assert int(F["TCLocalBit"][0]) == 0x103
+    assert F["values"].tolist() == [1.0, 2.0, 3.0]
+
+
+@pytest.mark.parametrize("seed", range(200))
+def test_roundtrip_random(seed):
+    """S:568 acceptance 1: decode(encode(A)) == A bit-exactly on 200 random matrices."""
+    rng = np.random.default_rng(1000 + seed)
+    M = int(rng.integers(1, 513))
+    K = int(rng.integers(1, 513))
+    dens = float(10 ** rng.uniform(-3, np.log10(0.3)))
+    nnz = max(0, min(M * K, int(dens * M * K)))
+    A = gen.uniform_random(M, K, nnz, seed=seed)
+    v = gen.values_uniform(A.nnz, seed)
+    F = _enc(A, v)
+    rp, ci, vv = bt.decode(F)
+    assert np.array_equal(rp, A.rowptr) and np.array_equal(ci, A.colidx) and np.array_equal(vv, v)
+    # invariants S:275
+    tco = F["TCOffset"].astype(np.int64)
+    assert np.array_equal(np.diff(tco), np.bitwise_count(F["TCLocalBit"]).astype(np.int64))
+    assert int(tco[-1]) == A.nnz
+    assert bt.array_bytes(F) == bt.bittcf_index_bytes(M, F["NB"])
+    assert bt.bittcf_index_bytes(M, F["NB"]) - bt.metcf_index_bytes(M, F["NB"], A.nnz) == 8 * F["NB"] - A.nnz
+    # padding lanes never carry bits
+    lanes_used = np.zeros((F["NB"], 8), bool)
+    for k in range(64):
+        lanes_used[:, k % 8] |= ((F["TCLocalBit"] >> np.uint64(k)) & np.uint64(1)).astype(bool)
+    U = F["U"]
+    valid = np.zeros((F["NB"], 8), bool)
+    b = 0
+    for u in U:
+        for t in range((int(u) + 7) // 8):
+            valid[b, :min(8, int(u) - 8 * t)] = True
+            b += 1
+    assert np.array_equal(lanes_used, valid)
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_vectorised_equals_brute_force(seed):
+    rng = np.random.default_rng(seed)
+    M, K = int(rng.integers(1, 70)), int(rng.integers(1, 90))
+    A = gen.uniform_random(M, K, int(rng.integers(0, M * K // 3 + 1)), seed=seed)
+    F = _enc(A)
+    rwo, tco, a2b, bits = _brute_encode(A)
+    assert F["RowWindowOffset"].tolist() == rwo and F["TCOffset"].tolist() == tco
+    assert F["SparseAToB"].tolist() == a2b and [int(x) for x in F["TCLocalBit"]] == bits
+
+
+def test_mean_nnz_tc():
+    dense = gen.csr_from_pairs(np.repeat(np.arange(8), 8), np.tile(np.arange(8), 8), 8, 8)
+    assert bt.mean_nnz_tc(_enc(dense)) == 64.0
+    assert bt.mean_nnz_tc(_enc(gen.identity(16))) == 8.0
+
+
+def test_empty_and_ragged():
+    E = gen.Csr(13, 9, np.zeros(14, np.int64), np.zeros(0, np.int32))
+    F = _enc(E)
+    assert F["NB"] == 0 and F["RowWindowOffset"].tolist() == [0, 0, 0]
+    assert bt.decode(F)[0].tolist() == [0] * 14
+    R = gen.csr_from_pairs([12, 12], [0, 8], 13, 9)   # last window holds only rows 8..12
+    F = _enc(R)
+    assert F["RowWindowOffset"].tolist() == [0, 0, 1]
+    assert int(F["TCLocalBit"][0]) == (1 << 32) | (1 << 33)
+
+
+def test_permute_rows():
+    A = gen.uniform_random(40, 30, 200, seed=3)
+    v = gen.values_uniform(A.nnz, 4)
+    perm = np.random.default_rng(5).permutation(40)
+    rp, ci, vv = bt.permute_rows(40, A.rowptr, A.colidx, v, perm)
+    for r in range(40):
+        o = perm[r]
+        assert np.array_equal(ci[rp[r]:rp[r + 1]], A.colidx[A.rowptr[o]:A.rowptr[o + 1]])
+        assert np.array_equal(vv[rp[r]:rp[r + 1]], v[A.rowptr[o]:A.rowptr[o + 1]])
