@@ -1,0 +1,190 @@
+/*
+ * accspmm.h -- C ABI of the B200-native Acc-SpMM hot path (arXiv 2501.09251).
+ *
+ * Operation (§5): "Given an m-by-k sparse matrix A and a
+ * k-by-n dense matrix B, SpMM computes A multiply B and obtains an m-by-n dense
+ * matrix C."  A is held in the paper's BitTCF format (§3.3): RowWindows
+ * of 8 rows whose non-empty columns are condensed into 8x8 TC blocks, each with a
+ * uint64 occupancy bitmap.  Work is balanced over SMs by the
+ * sparsity-aware scheduler of §3.5.  Inputs are rounded once with
+ * rho = TF32 round-to-nearest-away ("tf32"; reading SURVEY §8(c) Q1) or
+ * FP16 round-to-nearest-even (BASELINE north_star "plus an FP16 variant"), and
+ * products accumulate in FP32.
+ *
+ * Conventions (all functions):
+ *   - Sparse A is canonical CSR on the HOST: rowptr int64[M+1] (rowptr[0] = 0,
+ *     non-decreasing), colidx int32[nnz] strictly ascending within each row and
+ *     in [0, K), vals float32[nnz].  The arrays are borrowed for the duration of
+ *     plan creation only; the caller may free them afterwards.
+ *   - Dense B is K x N row-major, contiguous (leading dimension N), on the
+ *     plan's device: float32 for ACCSPMM_TF32, IEEE binary16 for ACCSPMM_FP16;
+ *     16-byte aligned.  C is float32, row-major, leading dimension N, 16-byte
+ *     aligned, caller-owned, on the plan's device.
+ *   - N must be a positive multiple of 16 (ACCSPMM_ERR_UNSUPPORTED otherwise).
+ *   - Streams are CUDA runtime streams passed as `void*` (cudaStream_t); NULL
+ *     is the legacy default stream.
+ *   - Every function returns a status; on failure a thread-local message is
+ *     available from accspmm_last_error().  No function calls exit/abort.
+ *   - There is no CPU fallback: a plan created for a device executes only with
+ *     the CUDA kernels of this library; a host-only plan (device = -1) can be
+ *     inspected (info, export) but refuses to execute.
+ */
+#ifndef ACCSPMM_H
+#define ACCSPMM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ACCSPMM_ABI_VERSION 1
+
+typedef struct accspmm_plan accspmm_plan; /* opaque */
+
+typedef enum {
+    ACCSPMM_OK = 0,
+    ACCSPMM_ERR_INVALID_VALUE = 1,  /* null pointer, bad size, bad option, misaligned pointer     */
+    ACCSPMM_ERR_INVALID_CSR = 2,    /* rowptr not monotone / colidx unsorted, duplicate, out of range */
+    ACCSPMM_ERR_UNSUPPORTED = 3,    /* N not a multiple of 16, u32 offset overflow, host-only plan  */
+    ACCSPMM_ERR_OUT_OF_MEMORY = 4,  /* host or device allocation failed                           */
+    ACCSPMM_ERR_CUDA = 5,           /* a CUDA runtime call or kernel launch failed                 */
+    ACCSPMM_ERR_INTERNAL = 6
+} accspmm_status;
+
+typedef enum { ACCSPMM_TF32 = 0, ACCSPMM_FP16 = 1 } accspmm_precision;
+
+typedef enum {
+    ACCSPMM_REORDER_OFF = 0,
+    ACCSPMM_REORDER_ON = 1,   /* Algorithm 1, rows only (reading SURVEY Q12)      */
+    ACCSPMM_REORDER_AUTO = 2  /* keep the permutation only if it reduces the TC-block count   */
+} accspmm_reorder_mode;
+
+typedef enum {
+    ACCSPMM_BALANCE_OFF = 0,  /* one work unit per RowWindow ("each TB processes all the TC blocks of a single RowWindow") */
+    ACCSPMM_BALANCE_ON = 1,   /* TC blocks redistributed into units of <= unit_cap blocks   */
+    ACCSPMM_BALANCE_AUTO = 2  /* balance iff IBD (Eq. 3) > 8                                 */
+} accspmm_balance_mode;
+
+typedef struct {
+    int32_t precision;  /* accspmm_precision; default ACCSPMM_TF32                                   */
+    int32_t reorder;    /* accspmm_reorder_mode; default ACCSPMM_REORDER_OFF                         */
+    int32_t balance;    /* accspmm_balance_mode; default ACCSPMM_BALANCE_AUTO                        */
+    int32_t unit_cap;   /* max TC blocks per work unit; 0 = automatic (>= 32, the P:446 threshold)   */
+    int32_t part;       /* this rank's part in [0, nparts)                                          */
+    int32_t nparts;     /* number of nnz-balanced RowWindow ranges (multi-GPU); 1 = whole matrix    */
+    int32_t device;     /* CUDA device ordinal; -1 = host-only plan (format + schedule, no upload)  */
+    int32_t reserved[9];
+} accspmm_options;
+
+typedef struct {
+    int64_t M, K, nnz;          /* the input matrix                                                 */
+    int64_t rows;               /* rows this plan writes (= M when nparts == 1)                     */
+    int64_t row_begin;          /* first (reordered) row of this plan's slab                        */
+    int64_t window_begin;       /* first RowWindow of the slab (global index)                       */
+    int64_t W, NB;              /* RowWindows and TC blocks in this plan                            */
+    int64_t plan_nnz;           /* nnz held by this plan                                            */
+    int64_t sum_U;              /* sum over windows of unique columns = B rows gathered (bytes model) */
+    int64_t n_units, n_split_windows, n_segments;
+    int64_t nb_unreordered;     /* TC blocks of the matrix without reordering (AUTO decision)        */
+    int32_t precision, reorder_applied, balanced, unit_cap, perm_present, part, nparts, device;
+    double mean_nnz_tc;         /* plan_nnz / NB                                             */
+    double ibd;                 /* Eq. (3) over this plan's windows                                  */
+    int64_t index_bytes;        /* (ceil(rows/8) + 11*NB + 2)*4                               */
+    int64_t metcf_index_bytes;  /* ME-TCF equivalent                                     */
+    int64_t csr_index_bytes;    /* (rows+1)*4 + nnz*4                                                */
+    int64_t value_bytes;        /* es_A * plan_nnz                                                   */
+    int64_t device_bytes;       /* bytes resident on the device for this plan (excl. workspace)      */
+    double ms_validate, ms_reorder, ms_build, ms_schedule, ms_upload;
+    int64_t reserved[8];
+} accspmm_plan_info;
+
+/* Fills *opt with the defaults listed above.  Never fails for a non-null opt. */
+accspmm_status accspmm_options_default(accspmm_options *opt);
+
+/* Builds a plan with default options on the current CUDA device.
+ * Steps (all host-side, timed into accspmm_plan_info): validate CSR, round vals
+ * with rho, optional Algorithm-1 reordering, BitTCF build, IBD +
+ * schedule (Eq. 3/4), device upload.  *out receives a plan owned by the caller
+ * (free with accspmm_plan_destroy).  M = 0 or nnz = 0 are valid.
+ * Errors: INVALID_VALUE (null out, negative sizes, null arrays with nnz > 0),
+ * INVALID_CSR, UNSUPPORTED (a u32 offset would overflow), OUT_OF_MEMORY, CUDA. */
+accspmm_status accspmm_plan_create(int64_t M, int64_t K, const int64_t *rowptr, const int32_t *colidx,
+                                   const float *vals, accspmm_plan **out);
+
+/* As accspmm_plan_create with explicit options (opt may be NULL = defaults).
+ * With nparts > 1 the plan covers only RowWindows [b_part, b_part+1) of the
+ * nnz-balanced partition b_k = min{w : nparts*pre(w) >= k*nnz} (pre = nnz of
+ * windows before w, in reordered order). */
+accspmm_status accspmm_plan_create_ex(int64_t M, int64_t K, const int64_t *rowptr, const int32_t *colidx,
+                                      const float *vals, const accspmm_options *opt, accspmm_plan **out);
+
+/* C = A . B on `stream`, asynchronously (never synchronises the host).
+ * nparts == 1: C is M x N in ORIGINAL row order (reordered rows are scattered
+ * back through the permutation).  nparts > 1: C is the slab, info.rows x N, in
+ * reordered row order (accspmm_plan_export_rows gives each slab row's original id).
+ * Every element of C is written (empty rows get 0); there is no beta.
+ * B and C are device pointers (see conventions).  The first call for a given
+ * N may allocate a split-window workspace (cudaMalloc).  Concurrent executes of
+ * one plan on different streams are not allowed (they share the workspace).
+ * Errors: INVALID_VALUE (null/misaligned pointers, N <= 0), UNSUPPORTED
+ * (N % 16 != 0, host-only plan), OUT_OF_MEMORY, CUDA (launch failure). */
+accspmm_status accspmm_execute(const accspmm_plan *plan, const void *B, int64_t N, void *C, void *stream);
+
+/* End-to-end variant with HOST buffers: copies B (K x N, host) to the device,
+ * executes, copies C (host, same shape as accspmm_execute's C) back and
+ * synchronises `stream`.  Pinned host memory gives full PCIe bandwidth. */
+accspmm_status accspmm_execute_host(const accspmm_plan *plan, const void *B_host, int64_t N, void *C_host,
+                                    void *stream);
+
+/* Frees every host and device resource of the plan.  NULL is a no-op.  The
+ * caller must ensure no execute on this plan is still in flight. */
+void accspmm_plan_destroy(accspmm_plan *plan);
+
+/* Copies plan statistics into *info. */
+accspmm_status accspmm_plan_get_info(const accspmm_plan *plan, accspmm_plan_info *info);
+
+/* Copies the plan's BitTCF arrays to HOST buffers sized from accspmm_plan_info:
+ * rwo u32[W+1], tco u32[NB+1], a2b u32[8*NB], bits u64[NB], vals (float32[plan_nnz]
+ * for TF32, uint16 bit patterns for FP16).  Any pointer may be NULL (skipped).
+ * Window/block offsets are relative to this plan's slab.  Blocks the host thread. */
+accspmm_status accspmm_plan_export_format(const accspmm_plan *plan, uint32_t *rwo, uint32_t *tco, uint32_t *a2b,
+                                          uint64_t *bits, void *vals);
+
+/* Copies the n_units work units as u32[n_units][8] = {w0, nw, b0, b1, split_id
+ * (0xFFFFFFFF = whole windows), seg, nseg, workspace slot}. */
+accspmm_status accspmm_plan_export_units(const accspmm_plan *plan, uint32_t *units);
+
+/* Copies, for each of the plan's info.rows rows, its ORIGINAL row index
+ * (u32[rows]); identity when no reordering was applied. */
+accspmm_status accspmm_plan_export_rows(const accspmm_plan *plan, uint32_t *orig_row);
+
+/* Algorithm 1 alone (host): perm_new2old u32[n] for the square n x n CSR.
+ * Returns INVALID_CSR / INVALID_VALUE as plan creation does. */
+accspmm_status accspmm_reorder(int64_t n, const int64_t *rowptr, const int32_t *colidx, uint32_t *perm_new2old);
+
+/* nnz-balanced partition bounds (host): bounds int64[nparts+1] over the
+ * ceil(M/8) windows of the given CSR (already in the order to be partitioned). */
+accspmm_status accspmm_partition_bounds(int64_t M, const int64_t *rowptr, int32_t nparts, int64_t *bounds);
+
+/* Multi-GPU helper (device): C[orig_row[i]][:] = G[i][:] for i < n_rows where
+ * orig_row[i] != 0xFFFFFFFF (padding of an all-gathered slab set).  G and C are
+ * float32 row-major with leading dimension N (multiple of 4). */
+accspmm_status accspmm_unpermute(const float *G, const uint32_t *orig_row, int64_t n_rows, int64_t N, float *C,
+                                 void *stream);
+
+/* Test hooks (device).  accspmm_debug_round_tf32: out[i] = cvt.rna.tf32.f32(in[i])
+ * -- the instruction the kernel applies to B.  accspmm_debug_decode: tiles
+ * float32[NB][64], tile[b][r*8+c] = value of (row r, lane c) of TC block b or 0,
+ * decoded on the device with the kernel's popcount rule. */
+accspmm_status accspmm_debug_round_tf32(const float *in, float *out, int64_t n, void *stream);
+accspmm_status accspmm_debug_decode(const accspmm_plan *plan, float *tiles, void *stream);
+
+const char *accspmm_status_string(accspmm_status s);
+const char *accspmm_last_error(void);
+int32_t accspmm_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ACCSPMM_H */

@@ -1,0 +1,328 @@
+"""paper_2501_09251_b200 -- B200-native Acc-SpMM (arXiv 2501.09251) hot path.
+
+Thin ctypes binding of ``libaccspmm.so`` (C ABI declared in include/accspmm.h).
+Every function here only marshals arguments: all of the SpMM path (format
+build, schedule, decode, MMA, epilogue) runs in the library's C++ and CUDA code.
+There is no CPU fallback -- if the library is missing, importing the binding
+raises, and a host-only plan refuses to execute.
+
+The functions keep the C names (``accspmm_plan_create`` ...); ``Plan`` is a
+small convenience wrapper taking numpy arrays and torch CUDA tensors.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libaccspmm.so")
+
+TF32, FP16 = 0, 1
+REORDER = {"off": 0, "on": 1, "auto": 2}
+BALANCE = {"off": 0, "on": 1, "auto": 2}
+PRECISION = {"tf32": TF32, "fp16": FP16}
+NO_SPLIT = 0xFFFFFFFF
+
+
+class AccSpmmError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        super().__init__(f"{_status_name(status)}: {message}")
+        self.status = status
+
+
+class accspmm_options(ctypes.Structure):
+    _fields_ = [("precision", ctypes.c_int32), ("reorder", ctypes.c_int32), ("balance", ctypes.c_int32),
+                ("unit_cap", ctypes.c_int32), ("part", ctypes.c_int32), ("nparts", ctypes.c_int32),
+                ("device", ctypes.c_int32), ("reserved", ctypes.c_int32 * 9)]
+
+
+_I64 = ["M", "K", "nnz", "rows", "row_begin", "window_begin", "W", "NB", "plan_nnz", "sum_U", "n_units",
+        "n_split_windows", "n_segments", "nb_unreordered"]
+_I32 = ["precision", "reorder_applied", "balanced", "unit_cap", "perm_present", "part", "nparts", "device"]
+
+
+class accspmm_plan_info(ctypes.Structure):
+    _fields_ = ([(n, ctypes.c_int64) for n in _I64] + [(n, ctypes.c_int32) for n in _I32]
+                + [("mean_nnz_tc", ctypes.c_double), ("ibd", ctypes.c_double)]
+                + [(n, ctypes.c_int64) for n in ("index_bytes", "metcf_index_bytes", "csr_index_bytes",
+                                                  "value_bytes", "device_bytes")]
+                + [(n, ctypes.c_double) for n in ("ms_validate", "ms_reorder", "ms_build", "ms_schedule",
+                                                   "ms_upload")]
+                + [("reserved", ctypes.c_int64 * 8)])
+
+    def as_dict(self) -> dict:
+        return {n: getattr(self, n) for n, _ in self._fields_ if n != "reserved"}
+
+
+_lib = None
+EXPORTED = [
+    "accspmm_options_default", "accspmm_plan_create", "accspmm_plan_create_ex", "accspmm_execute",
+    "accspmm_execute_host", "accspmm_plan_destroy", "accspmm_plan_get_info", "accspmm_plan_export_format",
+    "accspmm_plan_export_units", "accspmm_plan_export_rows", "accspmm_reorder", "accspmm_partition_bounds",
+    "accspmm_unpermute", "accspmm_debug_round_tf32", "accspmm_debug_decode", "accspmm_status_string",
+    "accspmm_last_error", "accspmm_abi_version",
+]
+
+
+def load_library(path: str = LIB_PATH):
+    """Loads libaccspmm.so (raises if it has not been built: no fallback exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} not found: build it with `python -m paper_2501_09251_b200._build` "
+                          "(the CUDA path has no CPU fallback)")
+    lib = ctypes.CDLL(path)
+    P, I64, I32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32
+    S = ctypes.c_int
+    sig = {
+        "accspmm_options_default": ([ctypes.POINTER(accspmm_options)], S),
+        "accspmm_plan_create": ([I64, I64, P, P, P, ctypes.POINTER(P)], S),
+        "accspmm_plan_create_ex": ([I64, I64, P, P, P, ctypes.POINTER(accspmm_options), ctypes.POINTER(P)], S),
+        "accspmm_execute": ([P, P, I64, P, P], S),
+        "accspmm_execute_host": ([P, P, I64, P, P], S),
+        "accspmm_plan_destroy": ([P], None),
+        "accspmm_plan_get_info": ([P, ctypes.POINTER(accspmm_plan_info)], S),
+        "accspmm_plan_export_format": ([P, P, P, P, P, P], S),
+        "accspmm_plan_export_units": ([P, P], S),
+        "accspmm_plan_export_rows": ([P, P], S),
+        "accspmm_reorder": ([I64, P, P, P], S),
+        "accspmm_partition_bounds": ([I64, P, I32, P], S),
+        "accspmm_unpermute": ([P, P, I64, I64, P, P], S),
+        "accspmm_debug_round_tf32": ([P, P, I64, P], S),
+        "accspmm_debug_decode": ([P, P, P], S),
+        "accspmm_status_string": ([S], ctypes.c_char_p),
+        "accspmm_last_error": ([], ctypes.c_char_p),
+        "accspmm_abi_version": ([], I32),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = res
+    _lib = lib
+    return lib
+
+
+def _status_name(s: int) -> str:
+    try:
+        return load_library().accspmm_status_string(s).decode()
+    except Exception:  # pragma: no cover
+        return f"status {s}"
+
+
+def _check(status: int):
+    if status != 0:
+        raise AccSpmmError(status, load_library().accspmm_last_error().decode())
+
+
+def _ptr(a) -> int | None:
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data
+    if hasattr(a, "data_ptr"):
+        return a.data_ptr()
+    return int(a)
+
+
+# ------------------------------------------------------------------ C-named functions
+
+def accspmm_options_default() -> accspmm_options:
+    opt = accspmm_options()
+    _check(load_library().accspmm_options_default(ctypes.byref(opt)))
+    return opt
+
+
+def accspmm_plan_create(M, K, rowptr, colidx, vals):
+    return accspmm_plan_create_ex(M, K, rowptr, colidx, vals, None)
+
+
+def accspmm_plan_create_ex(M, K, rowptr, colidx, vals, opt: accspmm_options | None):
+    rowptr = np.ascontiguousarray(rowptr, dtype=np.int64)
+    colidx = np.ascontiguousarray(colidx, dtype=np.int32)
+    vals = np.ascontiguousarray(vals, dtype=np.float32)
+    out = ctypes.c_void_p()
+    _check(load_library().accspmm_plan_create_ex(int(M), int(K), _ptr(rowptr), _ptr(colidx), _ptr(vals),
+                                                 ctypes.byref(opt) if opt is not None else None, ctypes.byref(out)))
+    return out.value
+
+
+def accspmm_execute(plan, B_ptr, N, C_ptr, stream_ptr=None):
+    _check(load_library().accspmm_execute(plan, B_ptr, int(N), C_ptr, stream_ptr))
+
+
+def accspmm_execute_host(plan, B_host_ptr, N, C_host_ptr, stream_ptr=None):
+    _check(load_library().accspmm_execute_host(plan, B_host_ptr, int(N), C_host_ptr, stream_ptr))
+
+
+def accspmm_plan_destroy(plan):
+    if plan:
+        load_library().accspmm_plan_destroy(plan)
+
+
+def accspmm_plan_get_info(plan) -> dict:
+    info = accspmm_plan_info()
+    _check(load_library().accspmm_plan_get_info(plan, ctypes.byref(info)))
+    return info.as_dict()
+
+
+def accspmm_plan_export_format(plan) -> dict:
+    info = accspmm_plan_get_info(plan)
+    W, NB, nnz = info["W"], info["NB"], info["plan_nnz"]
+    rwo = np.empty(W + 1, np.uint32)
+    tco = np.empty(NB + 1, np.uint32)
+    a2b = np.empty(8 * NB, np.uint32)
+    bits = np.empty(NB, np.uint64)
+    vals = np.empty(nnz, np.uint16 if info["precision"] == FP16 else np.float32)
+    _check(load_library().accspmm_plan_export_format(plan, _ptr(rwo), _ptr(tco), _ptr(a2b), _ptr(bits), _ptr(vals)))
+    if info["precision"] == FP16:
+        vals = vals.view(np.float16)
+    return {"RowWindowOffset": rwo, "TCOffset": tco, "SparseAToB": a2b, "TCLocalBit": bits, "values": vals,
+            "W": W, "NB": NB, "nnz": nnz}
+
+
+def accspmm_plan_export_units(plan) -> np.ndarray:
+    n = accspmm_plan_get_info(plan)["n_units"]
+    u = np.empty((n, 8), np.uint32)
+    _check(load_library().accspmm_plan_export_units(plan, _ptr(u)))
+    return u
+
+
+def accspmm_plan_export_rows(plan) -> np.ndarray:
+    n = accspmm_plan_get_info(plan)["rows"]
+    r = np.empty(n, np.uint32)
+    if n:
+        _check(load_library().accspmm_plan_export_rows(plan, _ptr(r)))
+    return r
+
+
+def accspmm_reorder(n, rowptr, colidx) -> np.ndarray:
+    rowptr = np.ascontiguousarray(rowptr, dtype=np.int64)
+    colidx = np.ascontiguousarray(colidx, dtype=np.int32)
+    perm = np.empty(n, np.uint32)
+    _check(load_library().accspmm_reorder(int(n), _ptr(rowptr), _ptr(colidx), _ptr(perm)))
+    return perm
+
+
+def accspmm_partition_bounds(M, rowptr, nparts) -> np.ndarray:
+    rowptr = np.ascontiguousarray(rowptr, dtype=np.int64)
+    b = np.empty(nparts + 1, np.int64)
+    _check(load_library().accspmm_partition_bounds(int(M), _ptr(rowptr), int(nparts), _ptr(b)))
+    return b
+
+
+def accspmm_unpermute(G_ptr, orig_row_ptr, n_rows, N, C_ptr, stream_ptr=None):
+    _check(load_library().accspmm_unpermute(G_ptr, orig_row_ptr, int(n_rows), int(N), C_ptr, stream_ptr))
+
+
+def accspmm_debug_round_tf32(in_ptr, out_ptr, n, stream_ptr=None):
+    _check(load_library().accspmm_debug_round_tf32(in_ptr, out_ptr, int(n), stream_ptr))
+
+
+def accspmm_debug_decode(plan, tiles_ptr, stream_ptr=None):
+    _check(load_library().accspmm_debug_decode(plan, tiles_ptr, stream_ptr))
+
+
+def accspmm_status_string(s: int) -> str:
+    return load_library().accspmm_status_string(s).decode()
+
+
+def accspmm_last_error() -> str:
+    return load_library().accspmm_last_error().decode()
+
+
+def accspmm_abi_version() -> int:
+    return load_library().accspmm_abi_version()
+
+
+# ------------------------------------------------------------------ convenience wrapper
+
+def _stream_ptr(stream):
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    return getattr(stream, "cuda_stream", stream)
+
+
+class Plan:
+    """Owns one accspmm_plan.  ``execute`` takes torch CUDA tensors (B: K x N, float32 for
+    TF32 / float16 for FP16) and returns / fills C (float32)."""
+
+    def __init__(self, M, K, rowptr, colidx, vals, precision="tf32", reorder="off", balance="auto",
+                 unit_cap=0, part=0, nparts=1, device=None):
+        opt = accspmm_options_default()
+        opt.precision = PRECISION[precision]
+        opt.reorder = REORDER[reorder]
+        opt.balance = BALANCE[balance]
+        opt.unit_cap = int(unit_cap)
+        opt.part, opt.nparts = int(part), int(nparts)
+        if device is not None:
+            opt.device = int(device)
+        self.precision = precision
+        self.handle = accspmm_plan_create_ex(M, K, rowptr, colidx, vals, opt)
+        self.info = accspmm_plan_get_info(self.handle)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            accspmm_plan_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    @property
+    def out_rows(self) -> int:
+        return self.info["M"] if self.info["nparts"] == 1 else self.info["rows"]
+
+    def execute(self, B, C=None, stream=None):
+        import torch
+        N = B.shape[1]
+        if C is None:
+            C = torch.empty((self.out_rows, N), dtype=torch.float32, device=B.device)
+        accspmm_execute(self.handle, B.data_ptr(), N, C.data_ptr(), _stream_ptr(stream))
+        return C
+
+    def execute_host(self, B_host, C_host, stream=None):
+        """End to end with host buffers (numpy or pinned torch CPU tensors)."""
+        N = B_host.shape[1]
+        accspmm_execute_host(self.handle, _ptr(B_host), N, _ptr(C_host), _stream_ptr(stream))
+        return C_host
+
+    def export_format(self) -> dict:
+        return accspmm_plan_export_format(self.handle)
+
+    def export_units(self) -> np.ndarray:
+        return accspmm_plan_export_units(self.handle)
+
+    def export_rows(self) -> np.ndarray:
+        return accspmm_plan_export_rows(self.handle)
+
+    def debug_decode(self, stream=None):
+        import torch
+        tiles = torch.empty((self.info["NB"], 64), dtype=torch.float32, device="cuda")
+        accspmm_debug_decode(self.handle, tiles.data_ptr(), _stream_ptr(stream))
+        return tiles
+
+
+def bytes_model(info: dict, N: int) -> dict:
+    """SURVEY §8(d) stated bytes model for one execute: A-format + unique B rows per window + C."""
+    es_a = 2 if info["precision"] == FP16 else 4
+    es_b = es_a
+    W, NB = info["W"], info["NB"]
+    a_fmt = (4 * (W + 1) + 4 * (NB + 1) + 32 * NB + 8 * NB + es_a * info["plan_nnz"]
+             + 32 * info["n_units"] + (4 * info["rows"] if info["perm_present"] and info["nparts"] == 1 else 0))
+    b_model = es_b * N * info["sum_U"]
+    c = 4 * info["rows"] * N
+    return {"A_fmt": a_fmt, "B_model": b_model, "C": c, "total": a_fmt + b_model + c,
+            "flops": 2 * info["plan_nnz"] * N}

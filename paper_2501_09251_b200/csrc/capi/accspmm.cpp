@@ -1,0 +1,433 @@
+// C ABI of libaccspmm (include/accspmm.h): plan lifecycle, device upload, execute.
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cstring>
+#include <mutex>
+#include <new>
+
+#include "../internal.hpp"
+
+struct accspmm_plan {
+    accspmm_plan_info info{};
+    accspmm_options opt{};
+    accspmm::HostFormat host;           // kept only for host-only plans
+    std::vector<uint32_t> units_host;   // [n_units][8]
+    std::vector<uint32_t> orig_rows;    // slab row -> original row
+    accspmm::DevicePlan dev{};
+    // split-window workspace (grown on demand by execute)
+    mutable float *ws = nullptr;
+    mutable size_t ws_bytes = 0;
+    mutable uint32_t *counters = nullptr;
+    mutable size_t counters_n = 0;
+    // e2e staging buffers (grown on demand by execute_host)
+    mutable void *dB = nullptr;
+    mutable size_t dB_bytes = 0;
+    mutable float *dC = nullptr;
+    mutable size_t dC_bytes = 0;
+    mutable std::mutex mu;
+};
+
+namespace accspmm {
+
+static thread_local std::string g_last_error;
+
+accspmm_status fail(accspmm_status s, const std::string &msg)
+{
+    g_last_error = msg;
+    return s;
+}
+
+static accspmm_status cuda_fail(cudaError_t e, const char *what)
+{
+    return fail(ACCSPMM_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+static double ms_since(std::chrono::steady_clock::time_point t0)
+{
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
+template <class T>
+static accspmm_status upload(T **dst, const std::vector<T> &src, int64_t &bytes)
+{
+    size_t n = src.size() ? src.size() : 1;
+    cudaError_t e = cudaMalloc((void **)dst, n * sizeof(T));
+    if (e != cudaSuccess) return e == cudaErrorMemoryAllocation ? fail(ACCSPMM_ERR_OUT_OF_MEMORY, "cudaMalloc")
+                                                                : cuda_fail(e, "cudaMalloc");
+    bytes += (int64_t)(n * sizeof(T));
+    if (!src.empty()) {
+        e = cudaMemcpy(*dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy H2D");
+    }
+    return ACCSPMM_OK;
+}
+
+static void free_device(accspmm_plan *p)
+{
+    auto &d = p->dev;
+    cudaFree(d.rwo); cudaFree(d.tco); cudaFree(d.a2b); cudaFree(d.bits); cudaFree(d.vals);
+    cudaFree(d.units); cudaFree(d.row_map);
+    cudaFree(p->ws); cudaFree(p->counters); cudaFree(p->dB); cudaFree(p->dC);
+    d = DevicePlan();
+    p->ws = nullptr; p->counters = nullptr; p->dB = nullptr; p->dC = nullptr;
+}
+
+}  // namespace accspmm
+
+using namespace accspmm;
+
+template <class T>
+static accspmm_status export_array(T *dst, const std::vector<T> &host, const T *dev, size_t n)
+{
+    if (!dst || n == 0) return ACCSPMM_OK;
+    if (dev) {
+        cudaError_t e = cudaMemcpy(dst, dev, n * sizeof(T), cudaMemcpyDeviceToHost);
+        return e == cudaSuccess ? ACCSPMM_OK : cuda_fail(e, "cudaMemcpy D2H");
+    }
+    std::memcpy(dst, host.data(), n * sizeof(T));
+    return ACCSPMM_OK;
+}
+
+extern "C" {
+
+accspmm_status accspmm_options_default(accspmm_options *opt)
+{
+    if (!opt) return fail(ACCSPMM_ERR_INVALID_VALUE, "opt is NULL");
+    std::memset(opt, 0, sizeof(*opt));
+    opt->precision = ACCSPMM_TF32;
+    opt->reorder = ACCSPMM_REORDER_OFF;
+    opt->balance = ACCSPMM_BALANCE_AUTO;
+    opt->unit_cap = 0;
+    opt->part = 0;
+    opt->nparts = 1;
+    int dev = 0;
+    opt->device = cudaGetDevice(&dev) == cudaSuccess ? dev : 0;
+    cudaGetLastError();
+    return ACCSPMM_OK;
+}
+
+accspmm_status accspmm_plan_create(int64_t M, int64_t K, const int64_t *rowptr, const int32_t *colidx,
+                                   const float *vals, accspmm_plan **out)
+{
+    return accspmm_plan_create_ex(M, K, rowptr, colidx, vals, nullptr, out);
+}
+
+accspmm_status accspmm_plan_create_ex(int64_t M, int64_t K, const int64_t *rowptr, const int32_t *colidx,
+                                      const float *vals, const accspmm_options *opt_in, accspmm_plan **out)
+{
+    if (!out) return fail(ACCSPMM_ERR_INVALID_VALUE, "out is NULL");
+    *out = nullptr;
+    accspmm_options opt;
+    if (opt_in) opt = *opt_in; else accspmm_options_default(&opt);
+    if (opt.precision != ACCSPMM_TF32 && opt.precision != ACCSPMM_FP16)
+        return fail(ACCSPMM_ERR_INVALID_VALUE, "unknown precision");
+    if (opt.reorder < 0 || opt.reorder > 2 || opt.balance < 0 || opt.balance > 2)
+        return fail(ACCSPMM_ERR_INVALID_VALUE, "unknown reorder/balance mode");
+    if (opt.nparts < 1 || opt.part < 0 || opt.part >= opt.nparts)
+        return fail(ACCSPMM_ERR_INVALID_VALUE, "part must be in [0, nparts)");
+    if (opt.unit_cap < 0) return fail(ACCSPMM_ERR_INVALID_VALUE, "unit_cap < 0");
+    if (M < 0 || K < 0) return fail(ACCSPMM_ERR_INVALID_VALUE, "negative matrix dimension");
+    if (M >= (int64_t)UINT32_MAX || K >= (int64_t)INT32_MAX)
+        return fail(ACCSPMM_ERR_UNSUPPORTED, "M or K too large for 32-bit indices");
+
+    auto t0 = std::chrono::steady_clock::now();
+    Csr a{M, K, rowptr, colidx};
+    accspmm_status st = validate_csr(a);
+    if (st != ACCSPMM_OK) return st;
+    const int64_t nnz = M ? rowptr[M] : 0;
+    if (nnz > 0 && !vals) return fail(ACCSPMM_ERR_INVALID_VALUE, "vals is NULL");
+
+    accspmm_plan *p = new (std::nothrow) accspmm_plan();
+    if (!p) return fail(ACCSPMM_ERR_OUT_OF_MEMORY, "plan allocation");
+    p->opt = opt;
+    accspmm_plan_info &I = p->info;
+    I.M = M; I.K = K; I.nnz = nnz;
+    I.precision = opt.precision; I.part = opt.part; I.nparts = opt.nparts; I.device = opt.device;
+    I.ms_validate = ms_since(t0);
+
+    // ---- reordering (Algorithm 1), rows only ----
+    t0 = std::chrono::steady_clock::now();
+    std::vector<uint32_t> perm;
+    I.nb_unreordered = -1;
+    if (opt.reorder != ACCSPMM_REORDER_OFF && M == K && M > 0) {
+        try {
+            perm = reorder_alg1(a);
+        } catch (const std::bad_alloc &) {
+            delete p;
+            return fail(ACCSPMM_ERR_OUT_OF_MEMORY, "reordering");
+        }
+        if (opt.reorder == ACCSPMM_REORDER_AUTO) {
+            int64_t nb0 = count_blocks(a, {});
+            int64_t nb1 = count_blocks(a, perm);
+            I.nb_unreordered = nb0;
+            if (nb1 >= nb0) perm.clear();
+        }
+    }
+    I.reorder_applied = perm.empty() ? 0 : 1;
+    I.ms_reorder = ms_since(t0);
+
+    // ---- partition + BitTCF build ----
+    t0 = std::chrono::steady_clock::now();
+    int64_t wb0 = 0, wb1 = (M + kWindow - 1) / kWindow;
+    if (opt.nparts > 1) {
+        std::vector<int64_t> b = partition_bounds(a, perm, opt.nparts);
+        wb0 = b[(size_t)opt.part];
+        wb1 = b[(size_t)opt.part + 1];
+    }
+    const int64_t r0 = wb0 * kWindow, r1 = std::min<int64_t>(M, wb1 * kWindow);
+    HostFormat &F = p->host;
+    st = build_format(a, vals, perm, r0, std::max(r0, r1), opt.precision, F);
+    if (st != ACCSPMM_OK) { delete p; return st; }
+    if (I.nb_unreordered < 0 && opt.nparts == 1 && perm.empty()) I.nb_unreordered = F.NB;
+    I.rows = F.rows; I.row_begin = r0; I.window_begin = wb0;
+    I.W = F.W; I.NB = F.NB; I.plan_nnz = F.nnz; I.sum_U = F.sum_U;
+    I.mean_nnz_tc = F.NB ? (double)F.nnz / (double)F.NB : 0.0;
+    I.index_bytes = ((F.rows + 7) / 8 + 11 * F.NB + 2) * 4;
+    I.metcf_index_bytes = ((F.rows + 7) / 8 + 1 + F.NB + 1 + 8 * F.NB) * 4 + F.nnz;
+    I.csr_index_bytes = (F.rows + 1) * 4 + F.nnz * 4;
+    I.value_bytes = F.nnz * (opt.precision == ACCSPMM_FP16 ? 2 : 4);
+    p->orig_rows.resize((size_t)F.rows);
+    for (int64_t r = 0; r < F.rows; ++r)
+        p->orig_rows[(size_t)r] = perm.empty() ? (uint32_t)(r0 + r) : perm[(size_t)(r0 + r)];
+    I.perm_present = perm.empty() ? 0 : 1;
+    I.ms_build = ms_since(t0);
+
+    // ---- IBD + schedule ----
+    t0 = std::chrono::steady_clock::now();
+    const double ibd = compute_ibd(F.rwo);
+    const bool balance = opt.balance == ACCSPMM_BALANCE_ON ||
+                         (opt.balance == ACCSPMM_BALANCE_AUTO && ibd > kIbdThreshold);
+    const int cap = opt.unit_cap > 0 ? opt.unit_cap : auto_cap(F.NB);
+    Schedule S = build_schedule(F.rwo, cap, balance, opt.precision);
+    I.ibd = ibd; I.balanced = balance ? 1 : 0; I.unit_cap = cap;
+    I.n_units = (int64_t)S.units.size(); I.n_split_windows = S.n_split; I.n_segments = S.n_segments;
+    p->units_host.resize(S.units.size() * 8);
+    std::memcpy(p->units_host.data(), S.units.data(), S.units.size() * sizeof(Unit));
+    I.ms_schedule = ms_since(t0);
+
+    // ---- device upload ----
+    t0 = std::chrono::steady_clock::now();
+    if (opt.device >= 0) {
+        cudaError_t e = cudaSetDevice(opt.device);
+        if (e != cudaSuccess) { delete p; return cuda_fail(e, "cudaSetDevice"); }
+        DevicePlan &d = p->dev;
+        d.W = F.W; d.NB = F.NB; d.nnz = F.nnz; d.rows = F.rows; d.n_units = I.n_units;
+        d.n_split = S.n_split; d.n_segments = S.n_segments; d.precision = opt.precision;
+        int64_t bytes = 0;
+        st = upload(&d.rwo, F.rwo, bytes);
+        if (st == ACCSPMM_OK) st = upload(&d.tco, F.tco, bytes);
+        if (st == ACCSPMM_OK) st = upload(&d.a2b, F.a2b, bytes);
+        if (st == ACCSPMM_OK) st = upload(&d.bits, F.bits, bytes);
+        if (st == ACCSPMM_OK) {
+            if (opt.precision == ACCSPMM_FP16) st = upload((uint16_t **)&d.vals, F.v16, bytes);
+            else st = upload((float **)&d.vals, F.v32, bytes);
+        }
+        if (st == ACCSPMM_OK) st = upload(&d.units, p->units_host, bytes);
+        if (st == ACCSPMM_OK && opt.nparts == 1 && !perm.empty()) st = upload(&d.row_map, p->orig_rows, bytes);
+        if (st != ACCSPMM_OK) { free_device(p); delete p; return st; }
+        I.device_bytes = bytes;
+        // the device holds the format now; drop the host copy
+        HostFormat empty;
+        empty.W = F.W; empty.NB = F.NB; empty.nnz = F.nnz; empty.rows = F.rows; empty.sum_U = F.sum_U;
+        F = std::move(empty);
+    }
+    I.ms_upload = ms_since(t0);
+    *out = p;
+    return ACCSPMM_OK;
+}
+
+static accspmm_status ensure_workspace(const accspmm_plan *p, int64_t N)
+{
+    const auto &d = p->dev;
+    if (d.n_split == 0) return ACCSPMM_OK;
+    size_t need_ws = (size_t)d.n_segments * (size_t)N * 8 * sizeof(float);
+    int64_t fw = N % 128 == 0 ? 128 : N % 64 == 0 ? 64 : N % 32 == 0 ? 32 : 16;
+    size_t need_cnt = (size_t)d.n_split * (size_t)(N / fw);
+    if (need_ws > p->ws_bytes) {
+        cudaFree(p->ws);
+        p->ws = nullptr;
+        p->ws_bytes = 0;
+        cudaError_t e = cudaMalloc((void **)&p->ws, need_ws);
+        if (e != cudaSuccess) return fail(ACCSPMM_ERR_OUT_OF_MEMORY, "split-window workspace");
+        p->ws_bytes = need_ws;
+    }
+    if (need_cnt > p->counters_n) {
+        cudaFree(p->counters);
+        p->counters = nullptr;
+        p->counters_n = 0;
+        cudaError_t e = cudaMalloc((void **)&p->counters, need_cnt * sizeof(uint32_t));
+        if (e != cudaSuccess) return fail(ACCSPMM_ERR_OUT_OF_MEMORY, "split-window counters");
+        e = cudaMemset(p->counters, 0, need_cnt * sizeof(uint32_t));
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMemset counters");
+        p->counters_n = need_cnt;
+    }
+    return ACCSPMM_OK;
+}
+
+accspmm_status accspmm_execute(const accspmm_plan *p, const void *B, int64_t N, void *C, void *stream)
+{
+    if (!p) return fail(ACCSPMM_ERR_INVALID_VALUE, "plan is NULL");
+    if (p->opt.device < 0) return fail(ACCSPMM_ERR_UNSUPPORTED, "host-only plan cannot execute (no CPU fallback)");
+    if (N <= 0) return fail(ACCSPMM_ERR_INVALID_VALUE, "N <= 0");
+    if (N % 16 != 0) return fail(ACCSPMM_ERR_UNSUPPORTED, "N must be a multiple of 16");
+    if (p->info.rows == 0) return ACCSPMM_OK;
+    if (!C || (!B && p->info.K > 0)) return fail(ACCSPMM_ERR_INVALID_VALUE, "B or C is NULL");
+    if (((uintptr_t)B & 15) || ((uintptr_t)C & 15)) return fail(ACCSPMM_ERR_INVALID_VALUE, "B and C must be 16-byte aligned");
+    std::lock_guard<std::mutex> lk(p->mu);
+    accspmm_status st = ensure_workspace(p, N);
+    if (st != ACCSPMM_OK) return st;
+    return launch_spmm(p->dev, B, N, (float *)C, p->ws, p->counters, stream);
+}
+
+accspmm_status accspmm_execute_host(const accspmm_plan *p, const void *B_host, int64_t N, void *C_host, void *stream)
+{
+    if (!p) return fail(ACCSPMM_ERR_INVALID_VALUE, "plan is NULL");
+    if (p->opt.device < 0) return fail(ACCSPMM_ERR_UNSUPPORTED, "host-only plan cannot execute (no CPU fallback)");
+    if (N <= 0 || N % 16 != 0) return fail(N <= 0 ? ACCSPMM_ERR_INVALID_VALUE : ACCSPMM_ERR_UNSUPPORTED, "bad N");
+    if (!C_host || (!B_host && p->info.K > 0)) return fail(ACCSPMM_ERR_INVALID_VALUE, "B or C is NULL");
+    const size_t es = p->opt.precision == ACCSPMM_FP16 ? 2 : 4;
+    const size_t bB = (size_t)p->info.K * (size_t)N * es;
+    const size_t bC = (size_t)p->info.rows * (size_t)N * sizeof(float);
+    cudaStream_t s = (cudaStream_t)stream;
+    {
+        std::lock_guard<std::mutex> lk(p->mu);
+        if (bB > p->dB_bytes) {
+            cudaFree(p->dB); p->dB = nullptr; p->dB_bytes = 0;
+            if (cudaMalloc(&p->dB, bB) != cudaSuccess) return fail(ACCSPMM_ERR_OUT_OF_MEMORY, "e2e B buffer");
+            p->dB_bytes = bB;
+        }
+        if (bC > p->dC_bytes) {
+            cudaFree(p->dC); p->dC = nullptr; p->dC_bytes = 0;
+            if (cudaMalloc((void **)&p->dC, bC) != cudaSuccess) return fail(ACCSPMM_ERR_OUT_OF_MEMORY, "e2e C buffer");
+            p->dC_bytes = bC;
+        }
+    }
+    cudaError_t e = cudaMemcpyAsync(p->dB, B_host, bB, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return cuda_fail(e, "H2D B");
+    accspmm_status st = accspmm_execute(p, p->dB, N, p->dC, stream);
+    if (st != ACCSPMM_OK) return st;
+    e = cudaMemcpyAsync(C_host, p->dC, bC, cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) return cuda_fail(e, "D2H C");
+    e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
+    return ACCSPMM_OK;
+}
+
+void accspmm_plan_destroy(accspmm_plan *p)
+{
+    if (!p) return;
+    if (p->opt.device >= 0) free_device(p);
+    delete p;
+}
+
+accspmm_status accspmm_plan_get_info(const accspmm_plan *p, accspmm_plan_info *info)
+{
+    if (!p || !info) return fail(ACCSPMM_ERR_INVALID_VALUE, "NULL argument");
+    *info = p->info;
+    return ACCSPMM_OK;
+}
+
+accspmm_status accspmm_plan_export_format(const accspmm_plan *p, uint32_t *rwo, uint32_t *tco, uint32_t *a2b,
+                                          uint64_t *bits, void *vals)
+{
+    if (!p) return fail(ACCSPMM_ERR_INVALID_VALUE, "plan is NULL");
+    const auto &I = p->info;
+    const bool dev = p->opt.device >= 0;
+    accspmm_status st = export_array(rwo, p->host.rwo, dev ? p->dev.rwo : nullptr, (size_t)I.W + 1);
+    if (st == ACCSPMM_OK) st = export_array(tco, p->host.tco, dev ? p->dev.tco : nullptr, (size_t)I.NB + 1);
+    if (st == ACCSPMM_OK) st = export_array(a2b, p->host.a2b, dev ? p->dev.a2b : nullptr, (size_t)I.NB * 8);
+    if (st == ACCSPMM_OK) st = export_array(bits, p->host.bits, dev ? p->dev.bits : nullptr, (size_t)I.NB);
+    if (st == ACCSPMM_OK) {
+        if (p->opt.precision == ACCSPMM_FP16)
+            st = export_array((uint16_t *)vals, p->host.v16, dev ? (const uint16_t *)p->dev.vals : nullptr,
+                              (size_t)I.plan_nnz);
+        else
+            st = export_array((float *)vals, p->host.v32, dev ? (const float *)p->dev.vals : nullptr,
+                              (size_t)I.plan_nnz);
+    }
+    return st;
+}
+
+accspmm_status accspmm_plan_export_units(const accspmm_plan *p, uint32_t *units)
+{
+    if (!p || !units) return fail(ACCSPMM_ERR_INVALID_VALUE, "NULL argument");
+    std::memcpy(units, p->units_host.data(), p->units_host.size() * sizeof(uint32_t));
+    return ACCSPMM_OK;
+}
+
+accspmm_status accspmm_plan_export_rows(const accspmm_plan *p, uint32_t *orig_row)
+{
+    if (!p || !orig_row) return fail(ACCSPMM_ERR_INVALID_VALUE, "NULL argument");
+    std::memcpy(orig_row, p->orig_rows.data(), p->orig_rows.size() * sizeof(uint32_t));
+    return ACCSPMM_OK;
+}
+
+accspmm_status accspmm_reorder(int64_t n, const int64_t *rowptr, const int32_t *colidx, uint32_t *perm_new2old)
+{
+    if (n < 0 || !perm_new2old) return fail(ACCSPMM_ERR_INVALID_VALUE, "bad argument");
+    Csr a{n, n, rowptr, colidx};
+    accspmm_status st = validate_csr(a);
+    if (st != ACCSPMM_OK) return st;
+    try {
+        std::vector<uint32_t> perm = reorder_alg1(a);
+        std::memcpy(perm_new2old, perm.data(), perm.size() * sizeof(uint32_t));
+    } catch (const std::bad_alloc &) {
+        return fail(ACCSPMM_ERR_OUT_OF_MEMORY, "reordering");
+    }
+    return ACCSPMM_OK;
+}
+
+accspmm_status accspmm_partition_bounds(int64_t M, const int64_t *rowptr, int32_t nparts, int64_t *bounds)
+{
+    if (M < 0 || nparts < 1 || !bounds || (M > 0 && !rowptr)) return fail(ACCSPMM_ERR_INVALID_VALUE, "bad argument");
+    Csr a{M, 0, rowptr, nullptr};
+    std::vector<int64_t> b = partition_bounds(a, {}, nparts);
+    std::memcpy(bounds, b.data(), b.size() * sizeof(int64_t));
+    return ACCSPMM_OK;
+}
+
+accspmm_status accspmm_unpermute(const float *G, const uint32_t *orig_row, int64_t n_rows, int64_t N, float *C,
+                                 void *stream)
+{
+    if (n_rows < 0 || N <= 0 || N % 4 != 0) return fail(ACCSPMM_ERR_INVALID_VALUE, "bad size");
+    if (n_rows == 0) return ACCSPMM_OK;
+    if (!G || !orig_row || !C) return fail(ACCSPMM_ERR_INVALID_VALUE, "NULL pointer");
+    return launch_unpermute(G, orig_row, n_rows, N, C, stream);
+}
+
+accspmm_status accspmm_debug_round_tf32(const float *in, float *out, int64_t n, void *stream)
+{
+    if (n < 0 || (n > 0 && (!in || !out))) return fail(ACCSPMM_ERR_INVALID_VALUE, "bad argument");
+    if (n == 0) return ACCSPMM_OK;
+    return launch_round_tf32(in, out, n, stream);
+}
+
+accspmm_status accspmm_debug_decode(const accspmm_plan *p, float *tiles, void *stream)
+{
+    if (!p) return fail(ACCSPMM_ERR_INVALID_VALUE, "plan is NULL");
+    if (p->opt.device < 0) return fail(ACCSPMM_ERR_UNSUPPORTED, "host-only plan");
+    if (p->info.NB == 0) return ACCSPMM_OK;
+    if (!tiles) return fail(ACCSPMM_ERR_INVALID_VALUE, "tiles is NULL");
+    return launch_decode(p->dev, tiles, stream);
+}
+
+const char *accspmm_status_string(accspmm_status s)
+{
+    switch (s) {
+    case ACCSPMM_OK: return "ACCSPMM_OK";
+    case ACCSPMM_ERR_INVALID_VALUE: return "ACCSPMM_ERR_INVALID_VALUE";
+    case ACCSPMM_ERR_INVALID_CSR: return "ACCSPMM_ERR_INVALID_CSR";
+    case ACCSPMM_ERR_UNSUPPORTED: return "ACCSPMM_ERR_UNSUPPORTED";
+    case ACCSPMM_ERR_OUT_OF_MEMORY: return "ACCSPMM_ERR_OUT_OF_MEMORY";
+    case ACCSPMM_ERR_CUDA: return "ACCSPMM_ERR_CUDA";
+    case ACCSPMM_ERR_INTERNAL: return "ACCSPMM_ERR_INTERNAL";
+    }
+    return "ACCSPMM_UNKNOWN_STATUS";
+}
+
+const char *accspmm_last_error(void) { return g_last_error.c_str(); }
+
+int32_t accspmm_abi_version(void) { return ACCSPMM_ABI_VERSION; }
+
+}  // extern "C"

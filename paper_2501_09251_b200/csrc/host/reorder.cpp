@@ -1,0 +1,208 @@
+// Data-affinity-based reordering, Algorithm 1 (§3.2).
+//
+// Step I (Alg. 1 l.1-8): vertices of the affinity graph G = pattern(A or A^T)
+// minus the diagonal are visited once in ascending degree (ties by
+// id); each is merged into the neighbouring community u maximising the merge
+// gain dQ(u,v) = 2*(w_uv/2m - a_u*a_v/(2m)^2) (Eq. 1 read as a merge
+// differential) if dQ > 0 (ties: smallest community id).  Community
+// edge lists are aggregated lazily (coarsening) and compacted when a community
+// is visited.  Step II (l.9-27): DFS over the merge forest (roots ascending,
+// node before children, children in merge order) gives the leaf sequence; each
+// unvisited vertex v gets the next id, then the walk repeatedly jumps to the
+// vertex with the most common neighbours among the next L = 64 unvisited
+// vertices in DFS order (neighbour lists capped at H = 128 entries), ties by DFS
+// order; with no common neighbour it resumes the DFS sequence (Q13).
+#include <algorithm>
+#include <numeric>
+
+#include "../internal.hpp"
+
+namespace accspmm {
+
+namespace {
+constexpr int kCandWindow = 64;  // L
+constexpr int kHubCap = 128;     // H
+
+struct Graph {
+    std::vector<int64_t> ptr;
+    std::vector<uint32_t> adj;
+};
+
+Graph affinity_graph(const Csr &a)
+{
+    const int64_t n = a.M;
+    std::vector<int64_t> cnt((size_t)n + 1, 0);
+    for (int64_t i = 0; i < n; ++i)
+        for (int64_t p = a.rowptr[i]; p < a.rowptr[i + 1]; ++p) {
+            int64_t j = a.colidx[p];
+            if (j == i) continue;
+            cnt[(size_t)i + 1]++;
+            cnt[(size_t)j + 1]++;
+        }
+    for (int64_t i = 0; i < n; ++i) cnt[(size_t)i + 1] += cnt[(size_t)i];
+    std::vector<uint32_t> tmp((size_t)cnt[(size_t)n]);
+    std::vector<int64_t> fill(cnt.begin(), cnt.end() - 1);
+    for (int64_t i = 0; i < n; ++i)
+        for (int64_t p = a.rowptr[i]; p < a.rowptr[i + 1]; ++p) {
+            int64_t j = a.colidx[p];
+            if (j == i) continue;
+            tmp[(size_t)fill[(size_t)i]++] = (uint32_t)j;
+            tmp[(size_t)fill[(size_t)j]++] = (uint32_t)i;
+        }
+    Graph g;
+    g.ptr.assign((size_t)n + 1, 0);
+    std::vector<int64_t> uniq((size_t)n, 0);
+#pragma omp parallel for schedule(dynamic, 256)
+    for (int64_t i = 0; i < n; ++i) {
+        auto b = tmp.begin() + cnt[(size_t)i], e = tmp.begin() + cnt[(size_t)i + 1];
+        std::sort(b, e);
+        uniq[(size_t)i] = std::unique(b, e) - b;
+    }
+    for (int64_t i = 0; i < n; ++i) g.ptr[(size_t)i + 1] = g.ptr[(size_t)i] + uniq[(size_t)i];
+    g.adj.resize((size_t)g.ptr[(size_t)n]);
+#pragma omp parallel for schedule(dynamic, 256)
+    for (int64_t i = 0; i < n; ++i)
+        std::copy(tmp.begin() + cnt[(size_t)i], tmp.begin() + cnt[(size_t)i] + uniq[(size_t)i],
+                  g.adj.begin() + g.ptr[(size_t)i]);
+    return g;
+}
+
+}  // namespace
+
+std::vector<uint32_t> reorder_alg1(const Csr &a)
+{
+    const int64_t n = a.M;
+    std::vector<uint32_t> perm((size_t)n);
+    std::iota(perm.begin(), perm.end(), 0u);
+    if (n == 0 || a.M != a.K) return perm;  // Q14: non-square -> identity
+    Graph g = affinity_graph(a);
+    const double m2 = (double)g.ptr[(size_t)n];
+
+    // ---------------- Step I: dendrogram construction (one pass) ----------------
+    std::vector<uint32_t> parent((size_t)n);
+    std::iota(parent.begin(), parent.end(), 0u);
+    std::vector<double> acomm((size_t)n);
+    std::vector<uint32_t> first_child((size_t)n, UINT32_MAX), last_child((size_t)n, UINT32_MAX),
+        next_sib((size_t)n, UINT32_MAX);
+    std::vector<std::vector<std::pair<uint32_t, uint32_t>>> E((size_t)n);
+    std::vector<uint32_t> order((size_t)n);
+    std::iota(order.begin(), order.end(), 0u);
+    for (int64_t v = 0; v < n; ++v) acomm[(size_t)v] = (double)(g.ptr[(size_t)v + 1] - g.ptr[(size_t)v]);
+    std::stable_sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) {
+        return g.ptr[x + 1] - g.ptr[x] < g.ptr[y + 1] - g.ptr[y];
+    });
+    auto find = [&](uint32_t x) {
+        uint32_t r = x;
+        while (parent[r] != r) r = parent[r];
+        while (parent[x] != r) { uint32_t nx = parent[x]; parent[x] = r; x = nx; }
+        return r;
+    };
+    std::vector<uint64_t> accw((size_t)n, 0);
+    std::vector<uint32_t> touched;
+    for (uint32_t v : order) {
+        const int64_t deg = g.ptr[v + 1] - g.ptr[v];
+        if (deg == 0 || m2 == 0.0) continue;
+        touched.clear();
+        auto add = [&](uint32_t x, uint32_t w) {
+            uint32_t r = find(x);
+            if (r == v) return;
+            if (accw[r] == 0) touched.push_back(r);
+            accw[r] += w;
+        };
+        for (int64_t p = g.ptr[v]; p < g.ptr[v + 1]; ++p) add(g.adj[(size_t)p], 1u);
+        for (auto &e : E[v]) add(e.first, e.second);
+        std::sort(touched.begin(), touched.end());
+        std::vector<std::pair<uint32_t, uint32_t>> comp;
+        comp.reserve(touched.size());
+        uint32_t best = UINT32_MAX;
+        double best_dq = 0.0;
+        for (uint32_t r : touched) {
+            double dq = 2.0 * ((double)accw[r] / m2 - acomm[r] * acomm[v] / (m2 * m2));
+            if (best == UINT32_MAX || dq > best_dq) { best = r; best_dq = dq; }
+            comp.emplace_back(r, (uint32_t)accw[r]);
+            accw[r] = 0;
+        }
+        E[v].clear();
+        E[v].shrink_to_fit();
+        if (best != UINT32_MAX && best_dq > 0.0) {
+            const uint32_t u = best;
+            parent[v] = u;
+            acomm[u] += acomm[v];
+            // v's original edges were consumed into comp; u inherits the aggregated list
+            E[u].insert(E[u].end(), comp.begin(), comp.end());
+            if (first_child[u] == UINT32_MAX) first_child[u] = v; else next_sib[last_child[u]] = v;
+            last_child[u] = v;
+        } else {
+            // v stays a root: keep its compacted list for communities merging into it later
+            E[v] = std::move(comp);
+        }
+    }
+    // A vertex is visited exactly once; its graph adjacency is read only on that
+    // visit, and afterwards its aggregated edges live in E[] of itself or its parent.
+
+    // ---------------- Step II: ordering generation ----------------
+    std::vector<uint32_t> seq;
+    seq.reserve((size_t)n);
+    std::vector<uint32_t> stack;
+    for (int64_t r = 0; r < n; ++r) {
+        if (parent[(size_t)r] != (uint32_t)r) continue;
+        stack.push_back((uint32_t)r);
+        while (!stack.empty()) {
+            uint32_t x = stack.back();
+            stack.pop_back();
+            seq.push_back(x);
+            // push children in reverse merge order so they pop in merge order
+            std::vector<uint32_t> ch;
+            for (uint32_t c = first_child[x]; c != UINT32_MAX; c = next_sib[c]) ch.push_back(c);
+            for (auto it = ch.rbegin(); it != ch.rend(); ++it) stack.push_back(*it);
+        }
+    }
+    // doubly linked list of unvisited positions in seq
+    std::vector<int64_t> nxt((size_t)n + 1), prv((size_t)n + 1);
+    std::vector<int64_t> pos_of((size_t)n);
+    for (int64_t i = 0; i < n; ++i) pos_of[seq[(size_t)i]] = i;
+    // sentinel at index n
+    for (int64_t i = 0; i <= n; ++i) { nxt[(size_t)i] = i + 1; prv[(size_t)i] = i - 1; }
+    nxt[(size_t)n] = 0;
+    prv[0] = n;
+    prv[(size_t)n] = n - 1;
+    if (n > 0) nxt[(size_t)n - 1] = n;
+    std::vector<char> visited((size_t)n, 0);
+    std::vector<uint32_t> mark((size_t)n, 0);
+    uint32_t stamp = 0;
+    int64_t next_id = 0;
+    auto assign = [&](uint32_t x) {
+        visited[x] = 1;
+        perm[(size_t)next_id++] = x;
+        int64_t p = pos_of[x];
+        nxt[(size_t)prv[(size_t)p]] = nxt[(size_t)p];
+        prv[(size_t)nxt[(size_t)p]] = prv[(size_t)p];
+    };
+    for (int64_t i = 0; i < n; ++i) {
+        uint32_t v = seq[(size_t)i];
+        if (visited[v]) continue;
+        assign(v);
+        while (nxt[(size_t)n] != n) {
+            ++stamp;
+            if (stamp == 0) { std::fill(mark.begin(), mark.end(), 0u); stamp = 1; }
+            const int64_t dv = std::min<int64_t>(kHubCap, g.ptr[v + 1] - g.ptr[v]);
+            for (int64_t q = 0; q < dv; ++q) mark[g.adj[(size_t)(g.ptr[v] + q)]] = stamp;
+            uint32_t best = UINT32_MAX;
+            int64_t best_c = 0;
+            int cand = 0;
+            for (int64_t p = nxt[(size_t)n]; p != n && cand < kCandWindow; p = nxt[(size_t)p], ++cand) {
+                uint32_t u = seq[(size_t)p];
+                const int64_t du = std::min<int64_t>(kHubCap, g.ptr[u + 1] - g.ptr[u]);
+                int64_t c = 0;
+                for (int64_t q = 0; q < du; ++q) c += mark[g.adj[(size_t)(g.ptr[u] + q)]] == stamp;
+                if (c > best_c) { best_c = c; best = u; }
+            }
+            if (best == UINT32_MAX) break;
+            assign(best);
+            v = best;
+        }
+    }
+    return perm;
+}
+
+}  // namespace accspmm

@@ -1,0 +1,116 @@
+// Adaptive sparsity-aware load balancing (§3.5) and the
+// nnz-balanced multi-GPU partition (BASELINE north_star).
+//
+// IBD (Eq. 3) decides whether to balance (> 8).  Balanced
+// schedules cut the TC-block stream into work units of <= cap blocks
+// with near-uniform cost.  Cost per unit follows Eq. (4) with the
+// B200 reading of SURVEY Q15: B-row loads scale with the blocks, and the
+// write-back of one 8-row window of C costs `wb` block loads (4 B of C vs es_B
+// bytes of B per feature: 1 for TF32, 2 for FP16).  Windows longer than the cap
+// are split evenly (cross-row write-back); shorter windows are
+// concatenated while sum(blocks + wb) <= cap + wb (Fig. 7(b)).
+#include <algorithm>
+#include <cmath>
+
+#include "../internal.hpp"
+
+namespace accspmm {
+
+double compute_ibd(const std::vector<uint32_t> &rwo)
+{
+    const size_t W = rwo.size() ? rwo.size() - 1 : 0;
+    if (W == 0) return 0.0;
+    const double avg = (double)rwo[W] / (double)W;
+    double s = 0.0;
+    for (size_t w = 0; w < W; ++w) s += std::fabs((double)(rwo[w + 1] - rwo[w]) - avg);
+    return s / (double)W;
+}
+
+// B200 default: about 64 units per SM (148 SMs), a multiple of 32, in [32, 4096].
+int auto_cap(int64_t NB)
+{
+    int64_t c = (NB + 148 * 64 - 1) / (148 * 64);
+    c = (c + 31) / 32 * 32;
+    return (int)std::max<int64_t>(kPaperCap, std::min<int64_t>(4096, c));
+}
+
+Schedule build_schedule(const std::vector<uint32_t> &rwo, int cap, bool balance, int precision)
+{
+    Schedule s;
+    s.cap = cap;
+    s.balanced = balance;
+    s.ibd = compute_ibd(rwo);
+    const int64_t W = rwo.size() ? (int64_t)rwo.size() - 1 : 0;
+    if (!balance) {
+        s.units.reserve((size_t)W);
+        for (int64_t w = 0; w < W; ++w)
+            s.units.push_back({(uint32_t)w, 1u, rwo[(size_t)w], rwo[(size_t)w + 1], kNoSplit, 0u, 1u, 0u});
+        return s;
+    }
+    const int64_t wb = precision == ACCSPMM_FP16 ? 2 : 1;
+    bool open = false;
+    Unit cur{};
+    int64_t cost = 0;
+    auto close = [&]() {
+        if (open) s.units.push_back(cur);
+        open = false;
+    };
+    for (int64_t w = 0; w < W; ++w) {
+        const int64_t nb = (int64_t)rwo[(size_t)w + 1] - (int64_t)rwo[(size_t)w];
+        if (nb > cap) {
+            close();
+            const int64_t nseg = (nb + cap - 1) / cap;
+            for (int64_t k = 0; k < nseg; ++k) {
+                uint32_t b0 = rwo[(size_t)w] + (uint32_t)((k * nb) / nseg);
+                uint32_t b1 = rwo[(size_t)w] + (uint32_t)(((k + 1) * nb) / nseg);
+                s.units.push_back({(uint32_t)w, 1u, b0, b1, (uint32_t)s.n_split, (uint32_t)k, (uint32_t)nseg,
+                                   (uint32_t)(s.n_segments + k)});
+            }
+            s.n_split += 1;
+            s.n_segments += nseg;
+        } else {
+            const int64_t c = nb + wb;
+            if (open && (int64_t)cur.nw < kWmax && cost + c <= cap + wb) {
+                cur.nw += 1;
+                cur.b1 = rwo[(size_t)w + 1];
+                cost += c;
+            } else {
+                close();
+                cur = {(uint32_t)w, 1u, rwo[(size_t)w], rwo[(size_t)w + 1], kNoSplit, 0u, 1u, 0u};
+                cost = c;
+                open = true;
+            }
+        }
+    }
+    close();
+    return s;
+}
+
+std::vector<int64_t> partition_bounds(const Csr &a, const std::vector<uint32_t> &perm, int nparts)
+{
+    const int64_t W = (a.M + kWindow - 1) / kWindow;
+    std::vector<int64_t> pre((size_t)W + 1, 0);
+    for (int64_t w = 0; w < W; ++w) {
+        int64_t s = 0;
+        for (int64_t r = w * kWindow; r < std::min<int64_t>(a.M, (w + 1) * kWindow); ++r) {
+            int64_t o = perm.empty() ? r : (int64_t)perm[(size_t)r];
+            s += a.rowptr[o + 1] - a.rowptr[o];
+        }
+        pre[(size_t)w + 1] = pre[(size_t)w] + s;
+    }
+    const int64_t nnz = pre[(size_t)W];
+    std::vector<int64_t> b((size_t)nparts + 1, 0);
+    for (int k = 1; k < nparts; ++k) {
+        // b_k = min{ w : nparts * pre(w) >= k * nnz }  (exact integers)
+        int64_t lo = 0, hi = W;
+        while (lo < hi) {
+            int64_t mid = (lo + hi) / 2;
+            if ((int64_t)nparts * pre[(size_t)mid] >= (int64_t)k * nnz) hi = mid; else lo = mid + 1;
+        }
+        b[(size_t)k] = lo;
+    }
+    b[(size_t)nparts] = W;
+    return b;
+}
+
+}  // namespace accspmm

@@ -1,0 +1,88 @@
+// Internal declarations shared by the host (C++) and device (CUDA) halves of libaccspmm.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "accspmm.h"
+
+namespace accspmm {
+
+constexpr int kWindow = 8;            // P:250 "8 x 8" TC blocks, P:251 ceil(M/8) windows
+constexpr uint32_t kNoSplit = 0xFFFFFFFFu;
+constexpr int kWmax = 31;             // windows per concatenated unit (one per lane of the window table)
+constexpr double kIbdThreshold = 8.0; // P:417 "When IBD exceeds 8"
+constexpr int kPaperCap = 32;         // P:446 "maximum threshold of 32 TC blocks per TB"
+
+// Error plumbing (thread-local message returned by accspmm_last_error).
+accspmm_status fail(accspmm_status s, const std::string &msg);
+
+struct Csr {
+    int64_t M = 0, K = 0;
+    const int64_t *rowptr = nullptr;
+    const int32_t *colidx = nullptr;
+};
+
+// Host-side BitTCF of one plan (a contiguous range of RowWindows of the
+// reordered matrix); offsets relative to the slab.
+struct HostFormat {
+    int64_t W = 0, NB = 0, nnz = 0, rows = 0, sum_U = 0;
+    std::vector<uint32_t> rwo;   // RowWindowOffset u32[W+1]
+    std::vector<uint32_t> tco;   // TCOffset        u32[NB+1]
+    std::vector<uint32_t> a2b;   // SparseAToB      u32[8 NB]
+    std::vector<uint64_t> bits;  // TCLocalBit      u64[NB]
+    std::vector<float> v32;      // values (TF32-rounded) when precision == TF32
+    std::vector<uint16_t> v16;   // values (FP16 bits) when precision == FP16
+};
+
+struct Unit { uint32_t w0, nw, b0, b1, split, seg, nseg, slot; };
+
+struct Schedule {
+    std::vector<Unit> units;
+    int64_t n_split = 0, n_segments = 0;
+    int cap = 0;
+    bool balanced = false;
+    double ibd = 0.0;
+};
+
+// host/csr.cpp
+accspmm_status validate_csr(const Csr &a);
+float round_tf32_rna(float x);        // (bits + 0x1000) & 0xFFFFE000
+uint16_t round_fp16_rne(float x);     // IEEE binary16, ties to even
+
+// host/bittcf.cpp -- rows [row_begin, row_end) of the row-permuted matrix
+// (perm new->old may be empty = identity); row_begin is a multiple of 8.
+accspmm_status build_format(const Csr &a, const float *vals, const std::vector<uint32_t> &perm,
+                            int64_t row_begin, int64_t row_end, int precision, HostFormat &out);
+int64_t count_blocks(const Csr &a, const std::vector<uint32_t> &perm);
+
+// host/schedule.cpp
+double compute_ibd(const std::vector<uint32_t> &rwo);
+int auto_cap(int64_t NB);
+Schedule build_schedule(const std::vector<uint32_t> &rwo, int cap, bool balance, int precision);
+
+// host/partition.cpp
+std::vector<int64_t> partition_bounds(const Csr &a, const std::vector<uint32_t> &perm, int nparts);
+
+// host/reorder.cpp -- Algorithm 1; returns perm new->old (identity for an edgeless graph)
+std::vector<uint32_t> reorder_alg1(const Csr &a);
+
+// kernels (device side, kernels/*.cu)
+struct DevicePlan {
+    int64_t W = 0, NB = 0, nnz = 0, rows = 0, n_units = 0, n_split = 0, n_segments = 0;
+    int precision = 0;
+    uint32_t *rwo = nullptr, *tco = nullptr, *a2b = nullptr;
+    uint64_t *bits = nullptr;
+    void *vals = nullptr;
+    uint32_t *units = nullptr;     // [n_units][8]
+    uint32_t *row_map = nullptr;   // slab row -> C row (nparts == 1 with a permutation), else null
+};
+
+accspmm_status launch_spmm(const DevicePlan &p, const void *B, int64_t N, float *C, float *ws,
+                           uint32_t *counters, void *stream);
+accspmm_status launch_unpermute(const float *G, const uint32_t *orig_row, int64_t n_rows, int64_t N,
+                                float *C, void *stream);
+accspmm_status launch_round_tf32(const float *in, float *out, int64_t n, void *stream);
+accspmm_status launch_decode(const DevicePlan &p, float *tiles, void *stream);
+
+}  // namespace accspmm

@@ -1,0 +1,92 @@
+// Auxiliary device kernels: multi-GPU un-permute (K6), TF32 rounding and BitTCF
+// decode test hooks.
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../internal.hpp"
+
+namespace accspmm {
+namespace {
+
+// C[orig_row[i]][:] = G[i][:]  (padding rows carry 0xFFFFFFFF and are skipped)
+__global__ void unpermute_kernel(const float4 *__restrict__ G, const uint32_t *__restrict__ orig_row, int64_t n_rows,
+                                 int64_t n4, float4 *__restrict__ C)
+{
+    const int64_t total = n_rows * n4;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e / n4, j = e - i * n4;
+        const uint32_t o = __ldg(orig_row + i);
+        if (o != 0xFFFFFFFFu) C[(int64_t)o * n4 + j] = __ldg(G + e);
+    }
+}
+
+__global__ void round_tf32_kernel(const float *__restrict__ in, float *__restrict__ out, int64_t n)
+{
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t r;
+        asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(in[e]));
+        out[e] = __uint_as_float(r);
+    }
+}
+
+// tile[b][k] = value at bit k of TC block b: TCOffset[b] + popc(mask & (2^k - 1)), else 0
+template <bool F16>
+__global__ void decode_kernel(const uint64_t *__restrict__ bits, const uint32_t *__restrict__ tco,
+                              const void *__restrict__ vals, int64_t NB, float *__restrict__ tiles)
+{
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < NB * 64; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = e >> 6;
+        const int k = (int)(e & 63);
+        const uint64_t m = __ldg(bits + b);
+        float v = 0.f;
+        if ((m >> k) & 1ull) {
+            const uint32_t idx = __ldg(tco + b) + (uint32_t)__popcll(m & ((1ull << k) - 1ull));
+            if (F16) v = __half2float(reinterpret_cast<const __half *>(vals)[idx]);
+            else v = reinterpret_cast<const float *>(vals)[idx];
+        }
+        tiles[e] = v;
+    }
+}
+
+int grid_for(int64_t n, int threads)
+{
+    int64_t g = (n + threads - 1) / threads;
+    return (int)(g < 148 * 32 ? (g < 1 ? 1 : g) : 148 * 32);
+}
+
+accspmm_status check_launch(const char *what)
+{
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? ACCSPMM_OK : fail(ACCSPMM_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+}  // namespace
+
+accspmm_status launch_unpermute(const float *G, const uint32_t *orig_row, int64_t n_rows, int64_t N, float *C,
+                                void *stream)
+{
+    const int64_t n4 = N / 4;
+    unpermute_kernel<<<grid_for(n_rows * n4, 256), 256, 0, (cudaStream_t)stream>>>(
+        reinterpret_cast<const float4 *>(G), orig_row, n_rows, n4, reinterpret_cast<float4 *>(C));
+    return check_launch("unpermute launch");
+}
+
+accspmm_status launch_round_tf32(const float *in, float *out, int64_t n, void *stream)
+{
+    round_tf32_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(in, out, n);
+    return check_launch("round_tf32 launch");
+}
+
+accspmm_status launch_decode(const DevicePlan &p, float *tiles, void *stream)
+{
+    const int64_t n = p.NB * 64;
+    if (p.precision == ACCSPMM_FP16)
+        decode_kernel<true><<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(p.bits, p.tco, p.vals, p.NB, tiles);
+    else
+        decode_kernel<false><<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(p.bits, p.tco, p.vals, p.NB, tiles);
+    return check_launch("decode launch");
+}
+
+}  // namespace accspmm

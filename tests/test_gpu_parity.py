@@ -1,0 +1,336 @@
+"""GPU parity: the sm_100a CUDA path (through the C ABI) vs the FP64 oracle.
+
+Tolerance (BASELINE north_star): |C_gpu - C_ref| <= tau*S + 1e-6, tau = 1e-3 TF32 / 4e-3 FP16.
+Integer-valued inputs (A in {-3..3}\\{0}, B in {-8..8}) must be bit-exact.
+Fixtures follow SURVEY §8(c) C-4; every output starts as a NaN canary.
+"""
+import numpy as np
+import pytest
+
+import gen
+import paper_2501_09251_b200 as acc
+from gpu_util import assert_bit_exact, assert_within, oracle, run, to_dev_B
+
+pytestmark = pytest.mark.gpu
+
+PRECISIONS = ["tf32", "fp16"]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    torch.cuda.init()
+    from paper_2501_09251_b200 import _build
+    _build.build()
+
+
+def _ragged(seed=0, M=1003, K=777, nnz=20000):
+    return gen.uniform_random(M, K, nnz, seed=seed)
+
+
+def test_tiny_config():
+    cfg, A = gen.make_config("tiny")
+    v = gen.values_uniform(A.nnz, cfg.seed_A + 1)
+    B = gen.dense_normal(A.K, 16, cfg.seed_B)
+    C, _ = run(A, v, B, "tf32")
+    assert_within(C, A, v, B, "tf32")
+
+
+@pytest.mark.parametrize("precision", PRECISIONS)
+@pytest.mark.parametrize("N", [16, 32, 48, 64, 96, 128, 256])
+@pytest.mark.parametrize("balance", ["off", "on"])
+def test_random_ragged_float(precision, N, balance):
+    A = _ragged(seed=N)
+    v = gen.values_uniform(A.nnz, 5)
+    B = gen.dense_normal(A.K, N, 6)
+    C, p = run(A, v, B, precision, balance=balance, unit_cap=8)
+    assert_within(C, A, v, B, precision)
+
+
+@pytest.mark.parametrize("precision", PRECISIONS)
+@pytest.mark.parametrize("N", [16, 32, 64, 128])
+def test_integer_bit_exact_and_balance_invariant(precision, N):
+    A = gen.dcsbm(3000, 150_000, 5, 2.2, 0.2, 2000, seed=N, oversample=1.3)
+    v = gen.values_int(A.nnz, 1)
+    B = gen.dense_int(A.K, N, 2)
+    C_off, _ = run(A, v, B, precision, balance="off")
+    C_on, p = run(A, v, B, precision, balance="on", unit_cap=32)
+    assert p.info["n_split_windows"] > 0
+    assert_bit_exact(C_off, A, v, B, precision)
+    assert np.array_equal(C_on, C_off)
+
+
+@pytest.mark.parametrize("precision", PRECISIONS)
+def test_permutation_matrix_exact(precision):
+    A = gen.permutation_matrix(1000, seed=3)
+    v = np.ones(A.nnz, np.float32)
+    B = gen.dense_normal(1000, 64, 4)
+    C, _ = run(A, v, B, precision)
+    assert_bit_exact(C, A, v, B, precision)
+
+
+@pytest.mark.parametrize("precision", PRECISIONS)
+def test_padding_lanes_do_not_leak_inf(precision):
+    # windows with 1..7 unique columns (partial last block), column 0 unused, B[0,:] = +Inf
+    rows, cols = [], []
+    for w in range(7):
+        for u in range(1, w + 2):
+            rows.append(8 * w + (u % 8))
+            cols.append(10 * w + u)
+    A = gen.csr_from_pairs(rows, cols, 64, 128)
+    v = gen.values_int(A.nnz, 0)
+    B = gen.dense_int(128, 32, 1)
+    B[0, :] = np.inf
+    C, _ = run(A, v, B, precision)
+    assert np.isfinite(C).all()
+    assert_bit_exact(C, A, v, B, precision)
+
+
+@pytest.mark.parametrize("precision", PRECISIONS)
+def test_single_bit_probes(precision):
+    # 64 windows, window (8r+c) holds the probe for position (r, c) (SURVEY C-4 a8(ii))
+    rows, cols = [], []
+    for r in range(8):
+        for c in range(8):
+            w = 8 * r + c
+            rp = (r + 1) % 8
+            for l in range(c):
+                rows.append(8 * w + rp)
+                cols.append(l)
+            rows.append(8 * w + r)
+            cols.append(c)
+    A = gen.csr_from_pairs(rows, cols, 512, 8)
+    v = gen.values_int(A.nnz, 3)
+    B = gen.dense_int(8, 16, 4)
+    C, _ = run(A, v, B, precision)
+    assert_bit_exact(C, A, v, B, precision)
+
+
+@pytest.mark.parametrize("precision", PRECISIONS)
+def test_dense_band_and_dense_windows(precision):
+    r = np.repeat(np.arange(64), 40)
+    c = np.tile(np.arange(40), 64) + (np.repeat(np.arange(64), 40) // 8) * 3
+    A = gen.csr_from_pairs(r, c, 64, 300)
+    v = gen.values_int(A.nnz, 5)
+    B = gen.dense_int(300, 128, 6)
+    C, _ = run(A, v, B, precision)
+    assert_bit_exact(C, A, v, B, precision)
+
+
+@pytest.mark.parametrize("precision", PRECISIONS)
+def test_empty_windows_ragged_and_degenerate(precision):
+    # M = 8k+3, rows 0..63 empty, K not a multiple of 8
+    base = gen.uniform_random(8 * 50 + 3, 45, 600, seed=9)
+    keep = base.row_ids() >= 64
+    A = gen.csr_from_pairs(base.row_ids()[keep], base.colidx[keep], base.M, base.K)
+    v = gen.values_int(A.nnz, 7)
+    B = gen.dense_int(45, 32, 8)
+    for bal in ("off", "on"):
+        C, _ = run(A, v, B, precision, balance=bal, unit_cap=4)
+        assert_bit_exact(C, A, v, B, precision)
+        assert np.all(C[:64] == 0)
+    # nnz = 0
+    Z = gen.Csr(37, 20, np.zeros(38, np.int64), np.zeros(0, np.int32))
+    C, _ = run(Z, np.zeros(0, np.float32), gen.dense_int(20, 16, 1), precision)
+    assert np.all(C == 0)
+    # M = 0
+    E = gen.Csr(0, 20, np.zeros(1, np.int64), np.zeros(0, np.int32))
+    C, _ = run(E, np.zeros(0, np.float32), gen.dense_int(20, 16, 1), precision)
+    assert C.shape == (0, 16)
+
+
+@pytest.mark.parametrize("precision", PRECISIONS)
+def test_split_window_hub(precision):
+    # one window of 8 rows x 4000 distinct columns = 500 blocks > cap 32
+    rng = np.random.default_rng(1)
+    rows = np.repeat(np.arange(8), 1500)
+    cols = np.concatenate([rng.choice(4000, 1500, replace=False) for _ in range(8)])
+    A = gen.csr_from_pairs(np.concatenate([rows, [20]]), np.concatenate([cols, [5]]), 24, 4000)
+    v = gen.values_int(A.nnz, 2)
+    B = gen.dense_int(4000, 64, 3)
+    C_on, p = run(A, v, B, precision, balance="on", unit_cap=32)
+    assert p.info["n_split_windows"] == 1 and p.info["n_segments"] >= 16
+    C_off, _ = run(A, v, B, precision, balance="off")
+    assert_bit_exact(C_on, A, v, B, precision)
+    assert np.array_equal(C_on, C_off)
+    vf = gen.values_uniform(A.nnz, 4)
+    Bf = gen.dense_normal(4000, 64, 5)
+    C, _ = run(A, vf, Bf, precision, balance="on", unit_cap=32)
+    assert_within(C, A, vf, Bf, precision)
+
+
+def test_concatenated_windows_exact():
+    # 1000 windows with one block each, balance forced on (concatenation) vs off
+    A = gen.uniform_random(8000, 8000, 8000, seed=12)
+    v = gen.values_int(A.nnz, 1)
+    B = gen.dense_int(8000, 32, 2)
+    C_on, p = run(A, v, B, "tf32", balance="on", unit_cap=32)
+    assert p.info["n_units"] < 1000
+    C_off, _ = run(A, v, B, "tf32", balance="off")
+    assert np.array_equal(C_on, C_off)
+    assert_bit_exact(C_on, A, v, B, "tf32")
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 8])
+def test_partitions_concatenate_to_whole(P):
+    A = gen.dcsbm(5000, 200_000, 6, 2.2, 0.2, 3000, seed=4, oversample=1.3)
+    v = gen.values_uniform(A.nnz, 3)
+    B = gen.dense_normal(A.K, 64, 4)
+    C1, _ = run(A, v, B, "tf32", balance="on", unit_cap=32)
+    slabs = []
+    for k in range(P):
+        Ck, pk = run(A, v, B, "tf32", balance="on", unit_cap=32, part=k, nparts=P)
+        assert np.array_equal(pk.export_rows(), np.arange(pk.info["row_begin"], pk.info["row_begin"] + pk.info["rows"]))
+        slabs.append(Ck)
+    assert np.array_equal(np.concatenate(slabs), C1)
+
+
+@pytest.mark.parametrize("mode", ["on", "auto"])
+@pytest.mark.parametrize("precision", PRECISIONS)
+def test_reordered_product_equals_unreordered_oracle(mode, precision):
+    A = gen.sbm(2048, 32, 0.1, 0.002, seed=7)
+    vi = gen.values_int(A.nnz, 1)
+    Bi = gen.dense_int(A.K, 32, 2)
+    C, p = run(A, vi, Bi, precision, reorder=mode)
+    if mode == "on":
+        assert p.info["reorder_applied"] == 1
+    assert_bit_exact(C, A, vi, Bi, precision)
+    vf = gen.values_uniform(A.nnz, 3)
+    Bf = gen.dense_normal(A.K, 64, 4)
+    C, _ = run(A, vf, Bf, precision, reorder=mode)
+    assert_within(C, A, vf, Bf, precision)
+
+
+def test_reordered_partitions_and_unpermute():
+    import torch
+    A = gen.sbm(1024, 16, 0.1, 0.004, seed=8)
+    v = gen.values_int(A.nnz, 1)
+    B = gen.dense_int(A.K, 32, 2)
+    C1, _ = run(A, v, B, "tf32", reorder="on")
+    P = 3
+    slabs, ids = [], []
+    for k in range(P):
+        Ck, pk = run(A, v, B, "tf32", reorder="on", part=k, nparts=P)
+        slabs.append(Ck)
+        ids.append(pk.export_rows())
+    # emulate the all-gather of padded slabs + device un-permute (K6)
+    mx = max(s.shape[0] for s in slabs)
+    G = np.zeros((P * mx, 32), np.float32)
+    rid = np.full(P * mx, 0xFFFFFFFF, np.uint32)
+    for k in range(P):
+        G[k * mx:k * mx + slabs[k].shape[0]] = slabs[k]
+        rid[k * mx:k * mx + slabs[k].shape[0]] = ids[k]
+    Gd = torch.from_numpy(G).cuda()
+    rd = torch.from_numpy(rid.view(np.int32)).cuda()
+    Cd = torch.full((A.M, 32), float("nan"), device="cuda")
+    acc.accspmm_unpermute(Gd.data_ptr(), rd.data_ptr(), P * mx, 32, Cd.data_ptr(),
+                          torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert np.array_equal(Cd.cpu().numpy(), C1)
+
+
+def test_repeat_runs_bitwise_deterministic():
+    import torch
+    A = gen.dcsbm(4000, 300_000, 5, 2.2, 0.2, 3000, seed=5, oversample=1.3)
+    v = gen.values_uniform(A.nnz, 1)
+    B = gen.dense_normal(A.K, 128, 2)
+    p = acc.Plan(A.M, A.K, A.rowptr, A.colidx, v, balance="on", unit_cap=32)
+    Bd = to_dev_B(B, "tf32")
+    outs = [p.execute(Bd).cpu().numpy() for _ in range(3)]
+    torch.cuda.synchronize()
+    assert p.info["n_split_windows"] > 0
+    assert all(np.array_equal(outs[0], o) for o in outs[1:])
+
+
+@pytest.mark.parametrize("precision", PRECISIONS)
+def test_device_decode_matches_oracle_tiles(precision):
+    from oracle import bittcf as bt
+    from oracle.rounding import rho
+    A = _ragged(seed=2, M=300, K=200, nnz=6000)
+    v = gen.values_uniform(A.nnz, 1)
+    p = acc.Plan(A.M, A.K, A.rowptr, A.colidx, v, precision=precision)
+    tiles = p.debug_decode().cpu().numpy()
+    F = bt.encode(A.M, A.K, A.rowptr, A.colidx, rho(v, precision))
+    ref = np.zeros((F["NB"], 64), np.float32)
+    tco = F["TCOffset"].astype(np.int64)
+    for b in range(F["NB"]):
+        m = int(F["TCLocalBit"][b])
+        for k in range(64):
+            if (m >> k) & 1:
+                ref[b, k] = F["values"][tco[b] + bin(m & ((1 << k) - 1)).count("1")]
+    assert np.array_equal(tiles, ref)
+
+
+def test_e2e_host_path_matches_device_path():
+    A = _ragged(seed=3)
+    v = gen.values_uniform(A.nnz, 1)
+    B = gen.dense_normal(A.K, 128, 2)
+    C, p = run(A, v, B, "tf32")
+    Ch = np.full((A.M, 128), np.nan, np.float32)
+    p.execute_host(np.ascontiguousarray(B), Ch)
+    assert np.array_equal(Ch, C)
+
+
+def test_execute_errors():
+    import torch
+    A = _ragged(seed=4, M=100, K=100, nnz=500)
+    p = acc.Plan(A.M, A.K, A.rowptr, A.colidx, gen.values_uniform(A.nnz, 1))
+    B = torch.zeros((100, 24), device="cuda")
+    C = torch.zeros((100, 24), device="cuda")
+    with pytest.raises(acc.AccSpmmError) as ei:
+        p.execute(B, C)
+    assert ei.value.status == 3
+    B = torch.zeros((100, 32), device="cuda")
+    with pytest.raises(acc.AccSpmmError) as ei:
+        acc.accspmm_execute(p.handle, B.data_ptr() + 4, 32, C.data_ptr())
+    assert ei.value.status == 1
+
+
+def test_tf32_rounding_exhaustive_vs_oracle():
+    """Pins oracle/rounding.tf32_rna to the hardware cvt.rna.tf32.f32 over all 2^32 patterns."""
+    import torch
+    from oracle.rounding import tf32_rna
+    chunk = 1 << 28
+    inp = torch.empty(chunk, dtype=torch.int32, device="cuda")
+    out = torch.empty(chunk, dtype=torch.float32, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    for c in range(1 << 32 >> 28):
+        base = c * chunk
+        host = (np.arange(chunk, dtype=np.uint64) + base).astype(np.uint32)
+        inp.copy_(torch.from_numpy(host.view(np.int32)))
+        acc.accspmm_debug_round_tf32(inp.data_ptr(), out.data_ptr(), chunk, s)
+        dev = out.cpu().numpy().view(np.uint32)
+        ref = tf32_rna(host.view(np.float32)).view(np.uint32)
+        assert np.array_equal(dev, ref), f"chunk {c}"
+
+
+# --------------------------------------------------------------- full-size configs, sampled rows
+
+def _sample_rows(M, n, seed):
+    rng = np.random.default_rng(seed)
+    return np.unique(np.concatenate([rng.integers(0, M, n), [0, M - 1]]))
+
+
+@pytest.mark.parametrize("name,N,precision", [
+    ("reddit", 128, "tf32"), ("reddit", 128, "fp16"), ("reddit", 32, "tf32"), ("reddit", 64, "tf32"),
+    ("stencil", 128, "tf32"), ("products", 128, "tf32"),
+])
+def test_full_size_config_sampled(name, N, precision):
+    cfg, A = gen.make_config(name)
+    v = gen.values_uniform(A.nnz, cfg.seed_A + 1)
+    B = gen.dense_normal(A.K, N, cfg.seed_B)
+    C, p = run(A, v, B, precision)
+    rows = _sample_rows(A.M, 3000, 1)
+    assert np.isfinite(C).all()
+    assert_within(C, A, v, B, precision, rows=rows)
+
+
+def test_full_size_reddit_integer_sampled_bit_exact():
+    cfg, A = gen.make_config("reddit")
+    v = gen.values_int(A.nnz, cfg.seed_A + 1)
+    B = gen.dense_int(A.K, 128, cfg.seed_B)
+    C, p = run(A, v, B, "tf32")
+    assert p.info["balanced"] == 1
+    rows = _sample_rows(A.M, 2000, 2)
+    Cr, _ = oracle(A, v, B, "tf32", rows=rows)
+    assert np.array_equal(C[rows].astype(np.float64), Cr)

@@ -1,0 +1,218 @@
+"""CPU tests of libaccspmm through its C ABI (host-only plans, device = -1): symbols,
+error paths, and BitTCF / schedule / partition / reorder bit-exact against the oracle."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import gen
+import paper_2501_09251_b200 as acc
+from oracle import balance as ob
+from oracle import bittcf as bt
+from oracle import partition as op
+from oracle import reorder as orr
+from oracle.rounding import fp16_rne, tf32_rna
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    from paper_2501_09251_b200 import _build
+    _build.build()
+
+
+def host_plan(A, vals, **kw):
+    kw.setdefault("device", -1)
+    return acc.Plan(A.M, A.K, A.rowptr, A.colidx, vals, **kw)
+
+
+def test_exports_every_declared_symbol():
+    with open(os.path.join(ROOT, "include", "accspmm.h")) as f:
+        hdr = f.read()
+    declared = set(re.findall(r"\b(accspmm_[a-z0-9_]+)\s*\(", hdr))
+    assert declared == set(acc.EXPORTED)
+    lib = ctypes.CDLL(acc.LIB_PATH)
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert acc.accspmm_abi_version() == 1
+
+
+def test_status_strings():
+    assert acc.accspmm_status_string(0) == "ACCSPMM_OK"
+    assert acc.accspmm_status_string(2) == "ACCSPMM_ERR_INVALID_CSR"
+
+
+@pytest.mark.parametrize("case", ["unsorted", "duplicate", "range", "rowptr", "rowptr0"])
+def test_invalid_csr_rejected(case):
+    rowptr = np.array([0, 2, 3], np.int64)
+    colidx = np.array([1, 3, 0], np.int32)
+    if case == "unsorted":
+        colidx = np.array([3, 1, 0], np.int32)
+    elif case == "duplicate":
+        colidx = np.array([1, 1, 0], np.int32)
+    elif case == "range":
+        colidx = np.array([1, 9, 0], np.int32)
+    elif case == "rowptr":
+        rowptr = np.array([0, 3, 2], np.int64)
+    elif case == "rowptr0":
+        rowptr = np.array([1, 2, 3], np.int64)
+    opt = acc.accspmm_options_default()
+    opt.device = -1
+    with pytest.raises(acc.AccSpmmError) as ei:
+        acc.accspmm_plan_create_ex(2, 4, rowptr, colidx, np.ones(3, np.float32), opt)
+    assert ei.value.status == 2
+
+
+def test_bad_options_and_host_only_execute():
+    A = gen.identity(8)
+    opt = acc.accspmm_options_default()
+    opt.device = -1
+    opt.nparts, opt.part = 2, 2
+    with pytest.raises(acc.AccSpmmError) as ei:
+        acc.accspmm_plan_create_ex(8, 8, A.rowptr, A.colidx, np.ones(8, np.float32), opt)
+    assert ei.value.status == 1
+    p = host_plan(A, np.ones(8, np.float32))
+    with pytest.raises(acc.AccSpmmError) as ei:   # no CPU fallback: host-only plans cannot execute
+        acc.accspmm_execute(p.handle, 16, 16, 16)
+    assert ei.value.status == 3
+
+
+def _check_format(F, ref, precision):
+    assert np.array_equal(F["RowWindowOffset"], ref["RowWindowOffset"])
+    assert np.array_equal(F["TCOffset"], ref["TCOffset"])
+    assert np.array_equal(F["SparseAToB"], ref["SparseAToB"])
+    assert np.array_equal(F["TCLocalBit"], ref["TCLocalBit"])
+    if precision == "tf32":
+        assert np.array_equal(F["values"].view(np.uint32), ref["values"].view(np.uint32))
+    else:
+        assert np.array_equal(F["values"].view(np.uint16), ref["values"].view(np.uint16))
+
+
+def _rho_vals(v, precision):
+    return tf32_rna(v) if precision == "tf32" else fp16_rne(v)
+
+
+@pytest.mark.parametrize("precision", ["tf32", "fp16"])
+@pytest.mark.parametrize("seed", range(30))
+def test_format_bit_exact_vs_oracle(seed, precision):
+    rng = np.random.default_rng(seed)
+    M, K = int(rng.integers(1, 700)), int(rng.integers(1, 700))
+    dens = float(10 ** rng.uniform(-3, np.log10(0.2)))
+    A = gen.uniform_random(M, K, int(dens * M * K), seed=seed)
+    v = gen.values_uniform(A.nnz, seed + 1)
+    p = host_plan(A, v, precision=precision)
+    ref = bt.encode(A.M, A.K, A.rowptr, A.colidx, _rho_vals(v, precision))
+    _check_format(p.export_format(), ref, precision)
+    I = p.info
+    assert I["NB"] == ref["NB"] and I["W"] == ref["W"] and I["sum_U"] == int(ref["U"].sum())
+    assert I["index_bytes"] == bt.bittcf_index_bytes(M, ref["NB"])
+    assert I["metcf_index_bytes"] == bt.metcf_index_bytes(M, ref["NB"], A.nnz)
+    assert I["mean_nnz_tc"] == pytest.approx(bt.mean_nnz_tc(ref), rel=1e-12)
+
+
+def test_golden_fixtures_through_library():
+    import json
+    with open(os.path.join(ROOT, "tests", "golden", "bittcf_fixtures.json")) as f:
+        fx = json.load(f)
+    for case in fx["cases"]:
+        A = gen.csr_from_pairs(case["rows"], case["cols"], case["M"], case["K"])
+        F = host_plan(A, np.ones(A.nnz, np.float32)).export_format()
+        assert F["RowWindowOffset"].tolist() == case["RowWindowOffset"], case["name"]
+        assert F["TCOffset"].tolist() == case["TCOffset"], case["name"]
+        assert F["SparseAToB"].tolist() == case["SparseAToB"], case["name"]
+        assert [int(x) for x in F["TCLocalBit"]] == [int(x, 16) for x in case["TCLocalBit"]], case["name"]
+
+
+def test_empty_matrices():
+    for M, K in [(0, 0), (0, 5), (13, 9)]:
+        A = gen.Csr(M, K, np.zeros(M + 1, np.int64), np.zeros(0, np.int32))
+        p = host_plan(A, np.zeros(0, np.float32))
+        assert p.info["NB"] == 0 and p.info["W"] == (M + 7) // 8
+        assert p.export_units().shape[0] == p.info["W"]
+
+
+@pytest.mark.parametrize("balance", ["off", "on", "auto"])
+@pytest.mark.parametrize("cap", [0, 32, 100])
+@pytest.mark.parametrize("precision", ["tf32", "fp16"])
+def test_schedule_bit_exact_vs_oracle(balance, cap, precision):
+    A = gen.dcsbm(4000, 160_000, 7, 2.3, 0.25, 2500, seed=11, oversample=1.3)
+    p = host_plan(A, gen.values_uniform(A.nnz, 1), balance=balance, unit_cap=cap, precision=precision)
+    I = p.info
+    F = p.export_format()
+    rwo = F["RowWindowOffset"].astype(np.int64)
+    ibd = ob.ibd(np.diff(rwo))
+    assert I["ibd"] == pytest.approx(ibd, rel=1e-12)
+    on = balance == "on" or (balance == "auto" and ibd > ob.IBD_THRESHOLD)
+    assert I["balanced"] == int(on)
+    expect_cap = cap if cap > 0 else ob.auto_cap(I["NB"])
+    assert I["unit_cap"] == expect_cap
+    ref = np.array(ob.build_units(rwo, expect_cap, on, precision), dtype=np.uint64).astype(np.uint32)
+    got = p.export_units()
+    assert got.shape == ref.shape and np.array_equal(got, ref)
+    ob.check_coverage([tuple(int(x) for x in u) for u in got], rwo)
+    assert I["n_split_windows"] == len({int(u[4]) for u in got if u[4] != ob.NO_SPLIT})
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 8])
+def test_partition_bounds_and_slabs(P):
+    A = gen.dcsbm(3000, 60_000, 5, 2.2, 0.2, 1500, seed=3, oversample=1.3)
+    v = gen.values_uniform(A.nnz, 2)
+    b = acc.accspmm_partition_bounds(A.M, A.rowptr, P)
+    assert b.tolist() == op.bounds(A.M, A.rowptr, P)
+    rows = []
+    for k in range(P):
+        p = host_plan(A, v, part=k, nparts=P)
+        I = p.info
+        assert I["window_begin"] == b[k] and I["row_begin"] == 8 * b[k]
+        r0, r1 = 8 * b[k], min(A.M, 8 * b[k + 1])
+        assert I["rows"] == max(0, r1 - r0)
+        sub_ptr = A.rowptr[r0:r1 + 1] - A.rowptr[r0] if r1 > r0 else np.zeros(1, np.int64)
+        sub_col = A.colidx[A.rowptr[r0]:A.rowptr[r1]] if r1 > r0 else np.zeros(0, np.int32)
+        ref = bt.encode(max(0, r1 - r0), A.K, sub_ptr, sub_col, tf32_rna(v[A.rowptr[r0]:A.rowptr[max(r0, r1)]]))
+        _check_format(p.export_format(), ref, "tf32")
+        rows.append(p.export_rows())
+    assert np.array_equal(np.concatenate(rows), np.arange(A.M, dtype=np.uint32))
+
+
+def _graphs():
+    out = []
+    for seed in range(6):
+        rng = np.random.default_rng(seed)
+        n = int(rng.integers(20, 200))
+        iu, ju = np.triu_indices(n, 1)
+        keep = rng.random(iu.size) < 0.05
+        out.append(gen.csr_from_pairs(iu[keep], ju[keep], n, n, symmetric=True))
+    out.append(gen.sbm(256, 8, 0.3, 0.01, seed=1))
+    out.append(gen.two_cliques(6, seed=2))
+    out.append(gen.star(9))
+    out.append(gen.uniform_random(150, 150, 900, seed=4))   # asymmetric pattern
+    out.append(gen.identity(10))
+    return out
+
+
+@pytest.mark.parametrize("idx", range(11))
+def test_reorder_matches_oracle_algorithm1(idx):
+    A = _graphs()[idx]
+    got = acc.accspmm_reorder(A.M, A.rowptr, A.colidx)
+    ref = orr.reorder(A.M, A.K, A.rowptr, A.colidx)
+    assert np.array_equal(got.astype(np.int64), ref)
+
+
+@pytest.mark.parametrize("mode", ["on", "auto"])
+def test_reordered_plan_format(mode):
+    A = gen.sbm(512, 16, 0.3, 0.005, seed=5)
+    v = gen.values_uniform(A.nnz, 6)
+    p = host_plan(A, v, reorder=mode)
+    perm = p.export_rows().astype(np.int64)
+    assert sorted(perm.tolist()) == list(range(A.M))
+    rp, ci, vv = bt.permute_rows(A.M, A.rowptr, A.colidx, v, perm)
+    ref = bt.encode(A.M, A.K, rp, ci, tf32_rna(vv))
+    _check_format(p.export_format(), ref, "tf32")
+    base = bt.encode(A.M, A.K, A.rowptr, A.colidx)
+    if mode == "auto":
+        assert p.info["nb_unreordered"] == base["NB"]
+        assert (p.info["reorder_applied"] == 1) == (ref["NB"] < base["NB"]) or p.info["reorder_applied"] == 0
+    assert p.info["NB"] <= base["NB"] or mode == "on"
