@@ -7,9 +7,13 @@ unconditionally on the float32 bit pattern:
 
     u = bits(x);  u = (u + 0x1000) & 0xFFFFE000
 
-This is written out here as that definition.  Consequences kept on purpose
-("Rounding rho"): Inf stays Inf, a NaN with payload >= 0x1000
-stays NaN, values with |bits| >= 0x7F7FF000 overflow to +-Inf.
+This is written out here as that definition for every non-NaN input: Inf stays
+Inf and values with |bits| >= 0x7F7FF000 overflow to +-Inf.  NaN inputs are not
+rounded but truncated, u & 0xFFFFE000 (so a NaN whose payload lives only in the
+low 13 bits becomes +-Inf): that is what cvt.rna.tf32.f32 does on sm_100a, as
+pinned by the exhaustive 2^32-pattern test (tests/test_gpu_parity.py) and
+recorded as DESIGN.md reading R1.  The bit trick alone would wrap large NaN
+payloads into the sign bit, which no hardware does.
 
 FP16 path: IEEE round-to-nearest-even, i.e. numpy's
 float32 -> float16 cast.
@@ -23,7 +27,9 @@ def tf32_rna(x) -> np.ndarray:
     """TF32 round-to-nearest, ties away from zero, kept in float32 bits."""
     x = np.ascontiguousarray(x, dtype=np.float32)
     u = x.view(np.uint32).astype(np.uint64)
-    u = (u + np.uint64(0x1000)) & np.uint64(0xFFFFE000)
+    rounded = (u + np.uint64(0x1000)) & np.uint64(0xFFFFE000)
+    truncated = u & np.uint64(0xFFFFE000)
+    u = np.where(np.isnan(x).ravel().reshape(u.shape), truncated, rounded)
     return u.astype(np.uint32).view(np.float32).reshape(x.shape)
 
 

@@ -37,12 +37,14 @@ accspmm_status validate_csr(const Csr &a)
 }
 
 // TF32 round-to-nearest, ties away from zero, on the float32 bit pattern
-// (SURVEY §8(c) Q1 -- the semantics of PTX cvt.rna.tf32.f32).
+// (SURVEY §8(c) Q1 -- the semantics of PTX cvt.rna.tf32.f32 on sm_100a, which
+// truncates NaN payloads instead of rounding them; reading R1).
 float round_tf32_rna(float x)
 {
     uint32_t u;
     std::memcpy(&u, &x, 4);
-    u = (u + 0x1000u) & 0xFFFFE000u;
+    const bool nan = (u & 0x7F800000u) == 0x7F800000u && (u & 0x007FFFFFu) != 0u;
+    u = nan ? (u & 0xFFFFE000u) : ((u + 0x1000u) & 0xFFFFE000u);
     float y;
     std::memcpy(&y, &u, 4);
     return y;

@@ -62,6 +62,13 @@ def test_tf32_low_bits_cleared_and_specials():
     assert y[0] == np.inf and y[1] == -np.inf and np.isnan(y[2]) and y[3] == np.inf
 
 
+def test_tf32_nan_truncated_not_rounded():
+    """DESIGN.md reading R1: NaNs keep their sign and top payload bits, low 13 bits cleared."""
+    u = np.array([0x7FC00000, 0x7FFFFFFF, 0x7F801FFF, 0x7F800001, 0xFFFFF000], dtype=np.uint32)
+    y = tf32_rna(u.view(np.float32)).view(np.uint32)
+    assert y.tolist() == [0x7FC00000, 0x7FFFE000, 0x7F800000, 0x7F800000, 0xFFFFE000]
+
+
 def test_fp16_rne_ties_to_even():
     x = np.array([1 + 2 ** -11, 1 + 3 * 2 ** -11, 65520.0, 2 ** -25, -2.5], dtype=np.float32)
     y = fp16_rne(x).astype(np.float64)
