@@ -124,8 +124,11 @@ accspmm_status accspmm_plan_create_ex(int64_t M, int64_t K, const int64_t *rowpt
  * back through the permutation).  nparts > 1: C is the slab, info.rows x N, in
  * reordered row order (accspmm_plan_export_rows gives each slab row's original id).
  * Every element of C is written (empty rows get 0); there is no beta.
- * B and C are device pointers (see conventions).  The first call for a given
- * N may allocate a split-window workspace (cudaMalloc).  Concurrent executes of
+ * B and C are device pointers (see conventions).  For TF32 plans the call
+ * launches two kernels: rho(B) into a plan-owned K x N scratch (one elementwise
+ * pass; every B row is then gathered by many windows), then the SpMM kernel.
+ * The first call for a given N may allocate the scratch and a split-window
+ * workspace (cudaMalloc).  Concurrent executes of
  * one plan on different streams are not allowed (they share the workspace).
  * Errors: INVALID_VALUE (null/misaligned pointers, N <= 0), UNSUPPORTED
  * (N % 16 != 0, host-only plan), OUT_OF_MEMORY, CUDA (launch failure). */
@@ -166,6 +169,14 @@ accspmm_status accspmm_reorder(int64_t n, const int64_t *rowptr, const int32_t *
 /* nnz-balanced partition bounds (host): bounds int64[nparts+1] over the
  * ceil(M/8) windows of the given CSR (already in the order to be partitioned). */
 accspmm_status accspmm_partition_bounds(int64_t M, const int64_t *rowptr, int32_t nparts, int64_t *bounds);
+
+/* Kernel timing (measurement hook).  While enabled, every execute records CUDA
+ * events on its stream around the SpMM kernel launch only (not the B rounding
+ * pass).  accspmm_plan_kernel_times synchronises on the recorded events, writes
+ * up to max_n elapsed times in ms (oldest first) and clears the record; *n_out
+ * receives the number written.  At most 4096 launches are kept. */
+accspmm_status accspmm_plan_set_timing(accspmm_plan *plan, int32_t enable);
+accspmm_status accspmm_plan_kernel_times(accspmm_plan *plan, float *ms_out, int32_t max_n, int32_t *n_out);
 
 /* Multi-GPU helper (device): C[orig_row[i]][:] = G[i][:] for i < n_rows where
  * orig_row[i] != 0xFFFFFFFF (padding of an all-gathered slab set).  G and C are

@@ -62,7 +62,7 @@ EXPORTED = [
     "accspmm_execute_host", "accspmm_plan_destroy", "accspmm_plan_get_info", "accspmm_plan_export_format",
     "accspmm_plan_export_units", "accspmm_plan_export_rows", "accspmm_reorder", "accspmm_partition_bounds",
     "accspmm_unpermute", "accspmm_debug_round_tf32", "accspmm_debug_decode", "accspmm_status_string",
-    "accspmm_last_error", "accspmm_abi_version",
+    "accspmm_last_error", "accspmm_abi_version", "accspmm_plan_set_timing", "accspmm_plan_kernel_times",
 ]
 
 
@@ -96,6 +96,8 @@ def load_library(path: str = LIB_PATH):
         "accspmm_status_string": ([S], ctypes.c_char_p),
         "accspmm_last_error": ([], ctypes.c_char_p),
         "accspmm_abi_version": ([], I32),
+        "accspmm_plan_set_timing": ([P, I32], S),
+        "accspmm_plan_kernel_times": ([P, P, I32, ctypes.POINTER(I32)], S),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -225,6 +227,17 @@ def accspmm_debug_decode(plan, tiles_ptr, stream_ptr=None):
     _check(load_library().accspmm_debug_decode(plan, tiles_ptr, stream_ptr))
 
 
+def accspmm_plan_set_timing(plan, enable: bool):
+    _check(load_library().accspmm_plan_set_timing(plan, int(bool(enable))))
+
+
+def accspmm_plan_kernel_times(plan, max_n: int = 4096) -> np.ndarray:
+    out = np.empty(max_n, np.float32)
+    n = ctypes.c_int32()
+    _check(load_library().accspmm_plan_kernel_times(plan, _ptr(out), int(max_n), ctypes.byref(n)))
+    return out[:n.value].copy()
+
+
 def accspmm_status_string(s: int) -> str:
     return load_library().accspmm_status_string(s).decode()
 
@@ -307,6 +320,16 @@ class Plan:
 
     def export_rows(self) -> np.ndarray:
         return accspmm_plan_export_rows(self.handle)
+
+    def set_timing(self, enable=True):
+        accspmm_plan_set_timing(self.handle, enable)
+
+    def kernel_times(self) -> np.ndarray:
+        return accspmm_plan_kernel_times(self.handle)
+
+    @property
+    def launches_per_execute(self) -> int:
+        return 2 if self.precision == "tf32" else 1
 
     def debug_decode(self, stream=None):
         import torch

@@ -25,6 +25,15 @@ struct accspmm_plan {
     mutable size_t dB_bytes = 0;
     mutable float *dC = nullptr;
     mutable size_t dC_bytes = 0;
+    // TF32: rounded copy of B (K x N) produced by the pre-pass of each execute
+    mutable float *Br = nullptr;
+    mutable size_t Br_bytes = 0;
+    // zero row read by padding lanes (>= 128 features x 4 B)
+    void *zrow = nullptr;
+    // kernel timing ring
+    mutable bool timing = false;
+    mutable std::vector<cudaEvent_t> ev;
+    mutable size_t ev_n = 0;
     mutable std::mutex mu;
 };
 
@@ -68,9 +77,11 @@ static void free_device(accspmm_plan *p)
     auto &d = p->dev;
     cudaFree(d.rwo); cudaFree(d.tco); cudaFree(d.a2b); cudaFree(d.bits); cudaFree(d.vals);
     cudaFree(d.units); cudaFree(d.row_map);
-    cudaFree(p->ws); cudaFree(p->counters); cudaFree(p->dB); cudaFree(p->dC);
+    cudaFree(p->ws); cudaFree(p->counters); cudaFree(p->dB); cudaFree(p->dC); cudaFree(p->Br); cudaFree(p->zrow);
+    for (auto e : p->ev) cudaEventDestroy(e);
+    p->ev.clear();
     d = DevicePlan();
-    p->ws = nullptr; p->counters = nullptr; p->dB = nullptr; p->dC = nullptr;
+    p->ws = nullptr; p->counters = nullptr; p->dB = nullptr; p->dC = nullptr; p->Br = nullptr; p->zrow = nullptr;
 }
 
 }  // namespace accspmm
@@ -225,6 +236,10 @@ accspmm_status accspmm_plan_create_ex(int64_t M, int64_t K, const int64_t *rowpt
         }
         if (st == ACCSPMM_OK) st = upload(&d.units, p->units_host, bytes);
         if (st == ACCSPMM_OK && opt.nparts == 1 && !perm.empty()) st = upload(&d.row_map, p->orig_rows, bytes);
+        if (st == ACCSPMM_OK) {
+            std::vector<uint32_t> zeros(256, 0u);  // 1 KB: covers a 128-wide FP32 feature slice
+            st = upload((uint32_t **)&p->zrow, zeros, bytes);
+        }
         if (st != ACCSPMM_OK) { free_device(p); delete p; return st; }
         I.device_bytes = bytes;
         // the device holds the format now; drop the host copy
@@ -277,7 +292,28 @@ accspmm_status accspmm_execute(const accspmm_plan *p, const void *B, int64_t N, 
     std::lock_guard<std::mutex> lk(p->mu);
     accspmm_status st = ensure_workspace(p, N);
     if (st != ACCSPMM_OK) return st;
-    return launch_spmm(p->dev, B, N, (float *)C, p->ws, p->counters, stream);
+    const void *Bk = B;
+    if (p->opt.precision == ACCSPMM_TF32 && p->info.K > 0) {
+        const size_t need = (size_t)p->info.K * (size_t)N * sizeof(float);
+        if (need > p->Br_bytes) {
+            cudaFree(p->Br);
+            p->Br = nullptr;
+            p->Br_bytes = 0;
+            if (cudaMalloc((void **)&p->Br, need) != cudaSuccess) return fail(ACCSPMM_ERR_OUT_OF_MEMORY, "B scratch");
+            p->Br_bytes = need;
+        }
+        st = launch_round_b((const float *)B, p->Br, p->info.K * N, stream);
+        if (st != ACCSPMM_OK) return st;
+        Bk = p->Br;
+    }
+    const bool timed = p->timing && p->ev_n + 2 <= p->ev.size();
+    if (timed) cudaEventRecord(p->ev[p->ev_n], (cudaStream_t)stream);
+    st = launch_spmm(p->dev, Bk, p->zrow, N, (float *)C, p->ws, p->counters, stream);
+    if (timed) {
+        cudaEventRecord(p->ev[p->ev_n + 1], (cudaStream_t)stream);
+        p->ev_n += 2;
+    }
+    return st;
 }
 
 accspmm_status accspmm_execute_host(const accspmm_plan *p, const void *B_host, int64_t N, void *C_host, void *stream)
@@ -384,6 +420,39 @@ accspmm_status accspmm_partition_bounds(int64_t M, const int64_t *rowptr, int32_
     Csr a{M, 0, rowptr, nullptr};
     std::vector<int64_t> b = partition_bounds(a, {}, nparts);
     std::memcpy(bounds, b.data(), b.size() * sizeof(int64_t));
+    return ACCSPMM_OK;
+}
+
+accspmm_status accspmm_plan_set_timing(accspmm_plan *p, int32_t enable)
+{
+    if (!p) return fail(ACCSPMM_ERR_INVALID_VALUE, "plan is NULL");
+    if (p->opt.device < 0) return fail(ACCSPMM_ERR_UNSUPPORTED, "host-only plan");
+    std::lock_guard<std::mutex> lk(p->mu);
+    if (enable && p->ev.empty()) {
+        p->ev.resize(8192);
+        for (auto &e : p->ev)
+            if (cudaEventCreate(&e) != cudaSuccess) return cuda_fail(cudaGetLastError(), "cudaEventCreate");
+    }
+    p->timing = enable != 0;
+    p->ev_n = 0;
+    return ACCSPMM_OK;
+}
+
+accspmm_status accspmm_plan_kernel_times(accspmm_plan *p, float *ms_out, int32_t max_n, int32_t *n_out)
+{
+    if (!p || !n_out || (max_n > 0 && !ms_out)) return fail(ACCSPMM_ERR_INVALID_VALUE, "NULL argument");
+    std::lock_guard<std::mutex> lk(p->mu);
+    int32_t n = 0;
+    for (size_t k = 0; k + 1 < p->ev_n && n < max_n; k += 2) {
+        cudaError_t e = cudaEventSynchronize(p->ev[k + 1]);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaEventSynchronize");
+        float ms = 0.f;
+        e = cudaEventElapsedTime(&ms, p->ev[k], p->ev[k + 1]);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaEventElapsedTime");
+        ms_out[n++] = ms;
+    }
+    p->ev_n = 0;
+    *n_out = n;
     return ACCSPMM_OK;
 }
 

@@ -78,8 +78,9 @@ struct DevicePlan {
     uint32_t *row_map = nullptr;   // slab row -> C row (nparts == 1 with a permutation), else null
 };
 
-accspmm_status launch_spmm(const DevicePlan &p, const void *B, int64_t N, float *C, float *ws,
+accspmm_status launch_spmm(const DevicePlan &p, const void *B, const void *zrow, int64_t N, float *C, float *ws,
                            uint32_t *counters, void *stream);
+accspmm_status launch_round_b(const float *B, float *Br, int64_t n, void *stream);
 accspmm_status launch_unpermute(const float *G, const uint32_t *orig_row, int64_t n_rows, int64_t N,
                                 float *C, void *stream);
 accspmm_status launch_round_tf32(const float *in, float *out, int64_t n, void *stream);

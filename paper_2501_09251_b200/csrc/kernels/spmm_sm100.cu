@@ -7,27 +7,30 @@
 // sparse tile the right operand of m16n8k8.  TF32 inputs with
 // FP32 accumulation; an FP16 variant uses m16n8k8.f16 (BASELINE north_star).
 //
-// How it does it is designed for B200, not translated from Alg. 2 (P:334-383):
-//   * one warp owns one work unit of the sparsity-aware schedule:
-//     a run of whole windows, or an even segment of one long window;
-//   * the unit's compressed A stream (TCLocalBit, TCOffset, SparseAToB) is read
-//     in 32-block chunks with coalesced 64/128-bit loads and staged in shared
-//     memory; each block's values are cp.async'ed next to its B rows;
-//   * B rows of each block are gathered with 16-byte cp.async (LDGSTS) into a
-//     per-warp STAGES-deep shared-memory ring (the paper's double buffer, P:325-331,
-//     generalised to an S-stage ring); padding lanes are zero-filled by the copy
-//     engine (src-size 0) so B[0, :] never leaks;
-//   * rows are XOR-swizzled at 16-byte granularity so the fragment loads are
-//     bank-conflict free;
-//   * B elements are rounded with cvt.rna.tf32.f32 at fragment load;
-//   * the accumulator tile (8 window rows x FW features) lives in registers;
-//     the epilogue stores C rows with st.global.cs (streaming, the .wt intent of
-//     P:282) through the row permutation of the reordering;
-//   * split windows write partial tiles to a workspace; the last-arriving
-//     segment (atomic counter) sums them in segment order -- deterministic
-//     cross-row write-back.
-#include <cuda_runtime.h>
+// How it does it is designed for B200 (DESIGN.md §6), not translated from Alg. 2:
+//   * one warp owns one work unit of the sparsity-aware schedule and
+//     one FW-wide feature slice: a run of whole RowWindows or an even segment of a
+//     long window;
+//   * the unit's compressed A stream (TCLocalBit, TCOffset, SparseAToB) is streamed
+//     in 32-block chunks by cp.async into a double-buffered per-warp shared-memory
+//     chunk (coalesced 8/4/16-byte copies, L2 evict_first);
+//   * each lane loads its part of the block's gathered B rows straight from
+//     L2/HBM into the MMA fragment registers (the paper's "B tile to registers
+//     directly") with 128-bit non-caching loads and an L2 evict_last
+//     policy; the features of the 16x8 operand are permuted so that 8 lanes read
+//     128 contiguous bytes of a B row and write 128 contiguous bytes of C;
+//     an A/B register double buffer keeps two blocks in flight per warp (the
+//     paper's least-bubble prefetch);
+//   * padding lanes of a block read a zero row instead of B[0,:];
+//   * B was rounded to TF32 (RNA) once per execute by a separate
+//     elementwise pass -- each B row is gathered by hundreds of windows, so the
+//     rounding is hoisted out of the gather instead of being repeated per block;
+//   * accumulators (8 window rows x FW features) live in registers; the epilogue
+//     stores C rows with st.global.cs through the reordering permutation (Q12);
+//   * split windows: partial tile -> workspace, the last-arriving segment (atomic
+//     counter) sums all partials in segment order (deterministic, Q18).
 #include <cuda_fp16.h>
+#include <cuda_runtime.h>
 
 #include <cstdint>
 #include <cstdlib>
@@ -39,34 +42,58 @@ namespace {
 
 // ------------------------------------------------------------------ PTX helpers
 
-__device__ __forceinline__ uint32_t smem_u32(const void *p)
-{
-    return (uint32_t)__cvta_generic_to_shared(p);
-}
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src, uint32_t src_bytes)
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src, uint64_t pol)
 {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "l"(pol)
+                 : "memory");
 }
-
-__device__ __forceinline__ void cp_async4(uint32_t dst, const void *src, uint32_t src_bytes)
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void *src, uint64_t pol)
 {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "l"(pol)
+                 : "memory");
 }
-
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void *src, uint64_t pol)
+{
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2;\n" ::"r"(dst), "l"(src), "l"(pol)
+                 : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
-template <int N>
-__device__ __forceinline__ void cp_async_wait()
+__device__ __forceinline__ uint64_t policy_evict_last()
 {
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first()
+{
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+    return p;
 }
 
-__device__ __forceinline__ uint32_t tf32_rna(float x)
+template <int BYTES>
+struct Vec;
+template <> struct Vec<16> { using T = uint4; };
+template <> struct Vec<8> { using T = uint2; };
+template <> struct Vec<4> { using T = uint32_t; };
+
+__device__ __forceinline__ void ldg_nc(uint4 &v, const void *p, uint64_t pol)
 {
-    uint32_t r;
-    asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
-    return r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;\n"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(pol));
+}
+__device__ __forceinline__ void ldg_nc(uint2 &v, const void *p, uint64_t pol)
+{
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;\n"
+                 : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(pol));
+}
+__device__ __forceinline__ void ldg_nc(uint32_t &v, const void *p, uint64_t pol)
+{
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;\n" : "=r"(v) : "l"(p), "l"(pol));
 }
 
 __device__ __forceinline__ void mma_tf32(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
@@ -87,61 +114,44 @@ __device__ __forceinline__ void mma_f16(float (&d)[4], uint32_t a0, uint32_t a1,
         : "r"(a0), "r"(a1), "r"(b0));
 }
 
-__device__ __forceinline__ void st_cs_v4(float *p, float a, float b, float c, float d)
+__device__ __forceinline__ void st_cs(float *p, float a, float b, float c, float d)
 {
     asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};\n" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
 }
-
-__device__ __forceinline__ void st_cs_v2(float *p, float a, float b)
+__device__ __forceinline__ void st_cs(float *p, float a, float b)
 {
     asm volatile("st.global.cs.v2.f32 [%0], {%1,%2};\n" ::"l"(p), "f"(a), "f"(b) : "memory");
 }
 
 // ------------------------------------------------------------------ configuration
 
+// Fragment geometry.  A lane (g = lane/4, t = lane%4) owns, for each of its two
+// gathered rows (TF32: t and t+4; FP16: 2t and 2t+1), NV vectors of VW features;
+// vector j covers features VW*(8j+g) .. +VW of the slice, so the 8 lanes sharing
+// a row read (and later write) 8*VW contiguous features.  Feature slot f = VW*j+e
+// of the lane is row (f&1 ? g+8 : g) of m16 tile mt = f>>1 (any bijection works
+// for a product; this one makes both the loads and the stores coalesced).
 template <int FW, bool F16>
 struct Cfg {
-    static constexpr int ES = F16 ? 2 : 4;              // bytes per B element
-    static constexpr int MT = FW / 16;                  // m16 tiles per warp tile
-    static constexpr int ROW_BYTES = FW * ES;           // one gathered B row slice
-    static constexpr int ROW_CHUNKS = ROW_BYTES / 16;   // 16-byte chunks per row
-    static constexpr int CHUNKS = 8 * ROW_CHUNKS;       // chunks per TC block
-    static constexpr int CP_ITERS = (CHUNKS + 31) / 32; // cp.async per lane per block
-    static constexpr int LANE_BYTES = FW * ES / 8;      // bytes of one row a lane consumes
-    static constexpr int VAL_WORDS = F16 ? 34 : 64;     // staged value words per block
-    // XOR mask on the 16-byte chunk index of row r: makes the fragment loads
-    // conflict-free (lanes of one 8-lane phase hit 8 distinct bank groups).
-    __device__ static __forceinline__ int swz(int r)
-    {
-        if (!F16) {
-            if (FW == 128) return r & 3;
-            if (FW == 64) return (r & 1) | ((r & 2) << 1);
-            if (FW == 32) return (r & 3) << 1;
-            return r & 2;                                  // FW == 16
-        } else {
-            const int t = r >> 1;
-            if (FW == 128) return (t & 1) | ((t & 2) << 1);
-            if (FW == 64) return (t & 3) << 1;
-            if (FW == 32) return (t & 1) << 1;
-            return 0;                                      // FW == 16
-        }
-    }
+    static constexpr int ES = F16 ? 2 : 4;
+    static constexpr int MT = FW / 16;
+    static constexpr int LPR = FW / 8;                                    // features per lane per row
+    static constexpr int VB = LPR * ES >= 16 ? 16 : LPR * ES;             // vector bytes
+    static constexpr int VW = VB / ES;                                    // features per vector
+    static constexpr int NV = LPR / VW;                                   // vectors per row per lane
+    using V = typename Vec<VB>::T;
 };
 
-template <int FW, bool F16, int STAGES>
+constexpr int kChunk = 32;  // TC blocks per staged A-stream chunk
+
+struct ChunkSmem {
+    uint32_t a2b[kChunk * 8];
+    uint64_t mask[kChunk];
+    uint32_t tco[kChunk];
+};
+
 struct WarpSmem {
-    using C = Cfg<FW, F16>;
-    struct Stage {
-        alignas(16) uint8_t b[8 * C::ROW_BYTES];
-        uint32_t val[C::VAL_WORDS];
-        uint64_t mask;
-        uint32_t voff;
-        uint32_t pad;
-    };
-    uint32_t a2b[256];
-    uint64_t mask[32];
-    uint32_t tco[32];
-    Stage st[STAGES];
+    ChunkSmem ch[2];
 };
 
 struct KParams {
@@ -153,6 +163,7 @@ struct KParams {
     const uint4 *__restrict__ units;
     const uint32_t *__restrict__ row_map;
     const void *__restrict__ B;
+    const void *__restrict__ zrow;   // N zeros (the row padding lanes read)
     float *__restrict__ C;
     float *__restrict__ ws;
     uint32_t *__restrict__ counters;
@@ -162,22 +173,67 @@ struct KParams {
     int32_t nslices;
 };
 
+template <int FW, bool F16>
+struct Frag {
+    using CF = Cfg<FW, F16>;
+    typename CF::V x[CF::NV];   // row rA (TF32: t, FP16: 2t)
+    typename CF::V y[CF::NV];   // row rB (TF32: t+4, FP16: 2t+1)
+    uint32_t b0, b1;            // decoded sparse-operand registers
+};
+
+template <int FW, bool F16>
+__device__ __forceinline__ void mma_block(float (&acc)[Cfg<FW, F16>::MT][4], const Frag<FW, F16> &fr)
+{
+    using CF = Cfg<FW, F16>;
+#pragma unroll
+    for (int j = 0; j < CF::NV; ++j) {
+        if constexpr (!F16) {
+            if constexpr (CF::VW == 4) {
+                const uint4 x = fr.x[j], y = fr.y[j];
+                mma_tf32(acc[2 * j], x.x, x.y, y.x, y.y, fr.b0, fr.b1);
+                mma_tf32(acc[2 * j + 1], x.z, x.w, y.z, y.w, fr.b0, fr.b1);
+            } else {  // VW == 2 (FW == 16)
+                const uint2 x = fr.x[j], y = fr.y[j];
+                mma_tf32(acc[j], x.x, x.y, y.x, y.y, fr.b0, fr.b1);
+            }
+        } else {
+            if constexpr (CF::VW == 8) {
+                const uint4 x = fr.x[j], y = fr.y[j];
+                const uint32_t xs[4] = {x.x, x.y, x.z, x.w}, ys[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    mma_f16(acc[4 * j + e], __byte_perm(xs[e], ys[e], 0x5410), __byte_perm(xs[e], ys[e], 0x7632),
+                            fr.b0);
+            } else if constexpr (CF::VW == 4) {
+                const uint2 x = fr.x[j], y = fr.y[j];
+                mma_f16(acc[2 * j], __byte_perm(x.x, y.x, 0x5410), __byte_perm(x.x, y.x, 0x7632), fr.b0);
+                mma_f16(acc[2 * j + 1], __byte_perm(x.y, y.y, 0x5410), __byte_perm(x.y, y.y, 0x7632), fr.b0);
+            } else {  // VW == 2
+                const uint32_t x = fr.x[j], y = fr.y[j];
+                mma_f16(acc[j], __byte_perm(x, y, 0x5410), __byte_perm(x, y, 0x7632), fr.b0);
+            }
+        }
+    }
+}
+
 // ------------------------------------------------------------------ the kernel
 
-template <int FW, bool F16, int WARPS, int STAGES>
+template <int FW, bool F16, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32) spmm_bittcf_kernel(const KParams p)
 {
     using CF = Cfg<FW, F16>;
-    using SM = WarpSmem<FW, F16, STAGES>;
-    constexpr int MT = CF::MT;
-    extern __shared__ __align__(128) uint8_t smem_raw[];
+    using V = typename CF::V;
+    constexpr int MT = CF::MT, NV = CF::NV, VW = CF::VW;
+    __shared__ WarpSmem smem_all[WARPS];
 
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int slice = (int)(blockIdx.x % (unsigned)p.nslices);
     const int64_t u = (int64_t)(blockIdx.x / (unsigned)p.nslices) * WARPS + warp;
     if (u >= p.n_units) return;  // warp-uniform; no CTA-wide barrier is used below
-    SM &sm = reinterpret_cast<SM *>(smem_raw)[warp];
+    WarpSmem &sm = smem_all[warp];
+    const uint64_t pol_keep = policy_evict_last();
+    const uint64_t pol_stream = policy_evict_first();
 
     const uint4 ua = __ldg(p.units + 2 * u);
     const uint4 ub = __ldg(p.units + 2 * u + 1);
@@ -185,222 +241,144 @@ __global__ void __launch_bounds__(WARPS * 32) spmm_bittcf_kernel(const KParams p
     const bool split = ub.x != kNoSplit;
     const int64_t f0 = (int64_t)slice * FW;
     const uint32_t my_rwo = (uint32_t)lane <= nw ? __ldg(p.rwo + w0 + lane) : 0u;
+    const uint32_t nblk = b1 - b0;
 
     const int g = lane >> 2, t = lane & 3;
+    const int rA = F16 ? 2 * t : t, rB = F16 ? 2 * t + 1 : t + 4;
+    // byte offset of this lane's vector j inside a gathered row slice
+    const char *Bbase = reinterpret_cast<const char *>(p.B) + f0 * CF::ES + (int64_t)(VW * g) * CF::ES;
+    const char *Zbase = reinterpret_cast<const char *>(p.zrow) + (int64_t)(VW * g) * CF::ES;
+    const int64_t row_stride = p.N * CF::ES;
+
+    // ---- A-stream chunk staging (cp.async, double buffered)
+    auto issue_chunk = [&](uint32_t i) {  // blocks [b0+i, b0+i+32) -> buffer (i/32)&1
+        if (i < nblk) {
+            ChunkSmem &c = sm.ch[(i >> 5) & 1];
+            const uint32_t b = b0 + i;
+            const uint32_t cnt = min((uint32_t)kChunk, nblk - i);
+            if ((uint32_t)lane < cnt) {
+                cp_async8(smem_u32(&c.mask[lane]), p.bits + b + lane, pol_stream);
+                cp_async4(smem_u32(&c.tco[lane]), p.tco + b + lane, pol_stream);
+            }
+            const uint4 *src4 = reinterpret_cast<const uint4 *>(p.a2b + (size_t)b * 8);
+            if ((uint32_t)lane < 2 * cnt) cp_async16(smem_u32(&c.a2b[4 * lane]), src4 + lane, pol_stream);
+            if ((uint32_t)lane + 32 < 2 * cnt) cp_async16(smem_u32(&c.a2b[4 * (lane + 32)]), src4 + lane + 32, pol_stream);
+        }
+        cp_async_commit();
+    };
+
+    // ---- gather + decode of block i (relative to b0) into a register fragment
+    auto load_block = [&](Frag<FW, F16> &fr, uint32_t i) {
+        if ((i & 31u) == 0) {  // chunk boundary: chunk i/32 must have landed; prefetch the next one
+            cp_async_wait_all();
+            __syncwarp();
+            issue_chunk(i + kChunk);
+        }
+        const ChunkSmem &c = sm.ch[(i >> 5) & 1];
+        const uint32_t cs = i & 31u;
+        const uint64_t mask = c.mask[cs];
+        const uint32_t t0 = c.tco[cs];
+        uint64_t cm = mask | (mask >> 32);
+        cm |= cm >> 16;
+        cm |= cm >> 8;  // low byte: condensed lanes present in the block
+        const bool va = (cm >> rA) & 1u, vb = (cm >> rB) & 1u;
+        const char *pa = va ? Bbase + (int64_t)c.a2b[cs * 8 + rA] * row_stride : Zbase;
+        const char *pb = vb ? Bbase + (int64_t)c.a2b[cs * 8 + rB] * row_stride : Zbase;
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+            ldg_nc(fr.x[j], pa + j * 8 * CF::VB, pol_keep);
+            ldg_nc(fr.y[j], pb + j * 8 * CF::VB, pol_keep);
+        }
+        // sparse operand: value index = TCOffset + popc(mask & (2^k - 1))
+        const uint64_t one = 1ull;
+        if constexpr (!F16) {
+            const int k0 = g * 8 + t, k1 = k0 + 4;
+            const float *vp = reinterpret_cast<const float *>(p.vals) + t0;
+            fr.b0 = ((mask >> k0) & one) ? __float_as_uint(__ldg(vp + __popcll(mask & ((one << k0) - one)))) : 0u;
+            fr.b1 = ((mask >> k1) & one) ? __float_as_uint(__ldg(vp + __popcll(mask & ((one << k1) - one)))) : 0u;
+        } else {
+            const int k0 = g * 8 + 2 * t;
+            const unsigned short *vp = reinterpret_cast<const unsigned short *>(p.vals) + t0;
+            const uint32_t lo = ((mask >> k0) & one) ? (uint32_t)__ldg(vp + __popcll(mask & ((one << k0) - one))) : 0u;
+            const uint32_t hi =
+                ((mask >> (k0 + 1)) & one) ? (uint32_t)__ldg(vp + __popcll(mask & ((one << (k0 + 1)) - one))) : 0u;
+            fr.b0 = lo | (hi << 16);
+            fr.b1 = 0u;
+        }
+    };
+
     float acc[MT][4];
 #pragma unroll
     for (int m = 0; m < MT; ++m) acc[m][0] = acc[m][1] = acc[m][2] = acc[m][3] = 0.f;
 
     // ---- epilogue: whole window -> C rows 2t, 2t+1 of window (w0 + wi)
-    auto store_window = [&](uint32_t wi) {
+    auto store_rows = [&](float *base, int64_t ld, int64_t lr0, bool remap) {
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
-            const int64_t lr = (int64_t)(w0 + wi) * 8 + 2 * t + s;
-            if (lr < p.rows) {
-                const int64_t orow = p.row_map ? (int64_t)__ldg(p.row_map + lr) : lr;
-                float *dst = p.C + orow * p.N + f0 + g * (FW / 8);
-                if constexpr (MT >= 2) {
+            const int64_t lr = lr0 + 2 * t + s;
+            if (!remap || lr < p.rows) {
+                const int64_t orow = remap ? (p.row_map ? (int64_t)__ldg(p.row_map + lr) : lr) : (2 * t + s);
+                float *dst = base + orow * ld + VW * g;
 #pragma unroll
-                    for (int q = 0; q < MT / 2; ++q)
-                        st_cs_v4(dst + 4 * q, acc[2 * q][s], acc[2 * q][2 + s], acc[2 * q + 1][s],
-                                 acc[2 * q + 1][2 + s]);
-                } else {
-                    st_cs_v2(dst, acc[0][s], acc[0][2 + s]);
+                for (int j = 0; j < NV; ++j) {
+                    float *d = dst + 8 * VW * j;
+                    if constexpr (VW == 2) {
+                        st_cs(d, acc[j][s], acc[j][2 + s]);
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < VW / 4; ++q) {
+                            const int m0 = (VW / 2) * j + 2 * q;
+                            st_cs(d + 4 * q, acc[m0][s], acc[m0][2 + s], acc[m0 + 1][s], acc[m0 + 1][2 + s]);
+                        }
+                    }
                 }
             }
         }
+    };
+    auto store_window = [&](uint32_t wi) {
+        store_rows(p.C + f0, p.N, (int64_t)(w0 + wi) * 8, true);
 #pragma unroll
         for (int m = 0; m < MT; ++m) acc[m][0] = acc[m][1] = acc[m][2] = acc[m][3] = 0.f;
     };
 
     uint32_t wi = 0;
     uint32_t wend = split ? b1 : __shfl_sync(0xffffffffu, my_rwo, 1);
-    auto flush_empty = [&](uint32_t j) {
-        while (!split && wi < nw && wend == j) {
+    auto after_block = [&](uint32_t jnext) {  // jnext = absolute index of the next block
+        while (!split && wi < nw && wend == jnext) {
             store_window(wi);
             ++wi;
             wend = __shfl_sync(0xffffffffu, my_rwo, (int)(wi < nw ? wi + 1 : nw));
         }
     };
 
-    // ---- producer side of the ring: stage block i (relative to b0)
-    const uint32_t nblk = b1 - b0;
-    const char *Bbase = reinterpret_cast<const char *>(p.B);
-    auto issue = [&](uint32_t i) {
-        if (i < nblk) {
-            const uint32_t b = b0 + i;
-            const uint32_t cs = i & 31u;
-            if (cs == 0) {  // stage the next 32 blocks of the compressed A stream (coalesced loads)
-                const uint32_t cnt = min(32u, nblk - i);
-                uint64_t m = 0;
-                uint32_t o = 0;
-                if ((uint32_t)lane < cnt) {
-                    m = __ldg(p.bits + b + lane);
-                    o = __ldg(p.tco + b + lane);
-                }
-                const uint4 *src4 = reinterpret_cast<const uint4 *>(p.a2b + (size_t)b * 8);
-                uint4 x0 = make_uint4(0, 0, 0, 0), x1 = x0;
-                if ((uint32_t)lane < 2 * cnt) x0 = __ldg(src4 + lane);
-                if ((uint32_t)lane + 32 < 2 * cnt) x1 = __ldg(src4 + lane + 32);
-                __syncwarp();
-                sm.mask[lane] = m;
-                sm.tco[lane] = o;
-                reinterpret_cast<uint4 *>(sm.a2b)[lane] = x0;
-                reinterpret_cast<uint4 *>(sm.a2b)[lane + 32] = x1;
-                __syncwarp();
-            }
-            const uint64_t mask = sm.mask[cs];
-            const uint32_t t0 = sm.tco[cs];
-            const int cnt = __popcll(mask);
-            uint64_t cm = mask | (mask >> 32);
-            cm |= cm >> 16;
-            cm |= cm >> 8;
-            const uint32_t colmask = (uint32_t)cm & 0xFFu;  // condensed lanes present in the block
-            auto &st = sm.st[i % STAGES];
-            const uint32_t sb = smem_u32(st.b);
-#pragma unroll
-            for (int k = 0; k < CF::CP_ITERS; ++k) {
-                const int q = lane + 32 * k;
-                if (q < CF::CHUNKS) {
-                    const int r = q / CF::ROW_CHUNKS, c = q % CF::ROW_CHUNKS;
-                    const uint32_t col = sm.a2b[cs * 8 + r];
-                    const bool v = (colmask >> r) & 1u;
-                    const char *src = v ? Bbase + ((int64_t)col * p.N + f0) * CF::ES + c * 16 : Bbase;
-                    cp_async16(sb + r * CF::ROW_BYTES + ((c ^ CF::swz(r)) * 16), src, v ? 16u : 0u);
-                }
-            }
-            const uint32_t sv = smem_u32(st.val);
-            if constexpr (!F16) {
-                const float *vp = reinterpret_cast<const float *>(p.vals) + t0;
-#pragma unroll
-                for (int k = 0; k < 2; ++k) {
-                    const int e = lane + 32 * k;
-                    cp_async4(sv + 4 * e, e < cnt ? (const void *)(vp + e) : p.vals, e < cnt ? 4u : 0u);
-                }
-            } else {
-                const uint32_t ws0 = t0 >> 1;
-                const int nwords = (int)(((t0 + (uint32_t)cnt + 1u) >> 1) - ws0);
-                const uint32_t *vp = reinterpret_cast<const uint32_t *>(p.vals) + ws0;
-#pragma unroll
-                for (int k = 0; k < 2; ++k) {
-                    const int e = lane + 32 * k;
-                    if (e < CF::VAL_WORDS)
-                        cp_async4(sv + 4 * e, e < nwords ? (const void *)(vp + e) : p.vals, e < nwords ? 4u : 0u);
-                }
-            }
-            if (lane == 0) {
-                st.mask = mask;
-                st.voff = t0 & 1u;
-            }
-        }
-        cp_async_commit();
-    };
-
-    // ---- consumer side: decode + tensor-core MMA of block i
-    auto consume = [&](uint32_t i) {
-        auto &st = sm.st[i % STAGES];
-        const uint64_t mask = st.mask;
-        const uint8_t *sb = st.b;
-        if constexpr (!F16) {
-            // sparse operand (mma B fragment): b0 = A[g][t], b1 = A[g][t+4]
-            const int k0 = g * 8 + t, k1 = k0 + 4;
-            const uint64_t one = 1ull;
-            const float *sv = reinterpret_cast<const float *>(st.val);
-            const uint32_t bb0 = ((mask >> k0) & one) ? __float_as_uint(sv[__popcll(mask & ((one << k0) - one))]) : 0u;
-            const uint32_t bb1 = ((mask >> k1) & one) ? __float_as_uint(sv[__popcll(mask & ((one << k1) - one))]) : 0u;
-            const uint8_t *r0 = sb + t * CF::ROW_BYTES;
-            const uint8_t *r1 = sb + (t + 4) * CF::ROW_BYTES;
-            if constexpr (FW >= 32) {
-#pragma unroll
-                for (int j = 0; j < FW / 32; ++j) {
-                    const int c = g * (FW / 32) + j;
-                    const float4 x = *reinterpret_cast<const float4 *>(r0 + ((c ^ CF::swz(t)) * 16));
-                    const float4 y = *reinterpret_cast<const float4 *>(r1 + ((c ^ CF::swz(t + 4)) * 16));
-                    mma_tf32(acc[2 * j], tf32_rna(x.x), tf32_rna(x.y), tf32_rna(y.x), tf32_rna(y.y), bb0, bb1);
-                    mma_tf32(acc[2 * j + 1], tf32_rna(x.z), tf32_rna(x.w), tf32_rna(y.z), tf32_rna(y.w), bb0, bb1);
-                }
-            } else {  // FW == 16: 2 floats per lane per row
-                const int c = g >> 1, h = (g & 1) * 8;
-                const float2 x = *reinterpret_cast<const float2 *>(r0 + ((c ^ CF::swz(t)) * 16) + h);
-                const float2 y = *reinterpret_cast<const float2 *>(r1 + ((c ^ CF::swz(t + 4)) * 16) + h);
-                mma_tf32(acc[0], tf32_rna(x.x), tf32_rna(x.y), tf32_rna(y.x), tf32_rna(y.y), bb0, bb1);
-            }
-        } else {
-            // sparse operand: b0 = {A[g][2t], A[g][2t+1]} (adjacent bits)
-            const int k0 = g * 8 + 2 * t;
-            const uint64_t one = 1ull;
-            const uint16_t *sv = reinterpret_cast<const uint16_t *>(st.val) + st.voff;
-            const uint32_t lo = ((mask >> k0) & one) ? sv[__popcll(mask & ((one << k0) - one))] : 0u;
-            const uint32_t hi = ((mask >> (k0 + 1)) & one) ? sv[__popcll(mask & ((one << (k0 + 1)) - one))] : 0u;
-            const uint32_t bb0 = lo | (hi << 16);
-            const int ra = 2 * t, rb = 2 * t + 1;
-            const uint8_t *r0 = sb + ra * CF::ROW_BYTES;
-            const uint8_t *r1 = sb + rb * CF::ROW_BYTES;
-            if constexpr (FW >= 64) {
-#pragma unroll
-                for (int j = 0; j < FW / 64; ++j) {
-                    const int c = g * (FW / 64) + j;
-                    const uint4 x = *reinterpret_cast<const uint4 *>(r0 + ((c ^ CF::swz(ra)) * 16));
-                    const uint4 y = *reinterpret_cast<const uint4 *>(r1 + ((c ^ CF::swz(rb)) * 16));
-                    const uint32_t xs[4] = {x.x, x.y, x.z, x.w}, ys[4] = {y.x, y.y, y.z, y.w};
-#pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                        mma_f16(acc[4 * j + e], __byte_perm(xs[e], ys[e], 0x5410), __byte_perm(xs[e], ys[e], 0x7632),
-                                bb0);
-                }
-            } else if constexpr (FW == 32) {
-                const int c = g >> 1, h = (g & 1) * 8;
-                const uint2 x = *reinterpret_cast<const uint2 *>(r0 + ((c ^ CF::swz(ra)) * 16) + h);
-                const uint2 y = *reinterpret_cast<const uint2 *>(r1 + ((c ^ CF::swz(rb)) * 16) + h);
-                mma_f16(acc[0], __byte_perm(x.x, y.x, 0x5410), __byte_perm(x.x, y.x, 0x7632), bb0);
-                mma_f16(acc[1], __byte_perm(x.y, y.y, 0x5410), __byte_perm(x.y, y.y, 0x7632), bb0);
-            } else {  // FW == 16
-                const int c = g >> 2, h = (g & 3) * 4;
-                const uint32_t x = *reinterpret_cast<const uint32_t *>(r0 + ((c ^ CF::swz(ra)) * 16) + h);
-                const uint32_t y = *reinterpret_cast<const uint32_t *>(r1 + ((c ^ CF::swz(rb)) * 16) + h);
-                mma_f16(acc[0], __byte_perm(x, y, 0x5410), __byte_perm(x, y, 0x7632), bb0);
-            }
-        }
-    };
-
-    // ---- the pipelined block loop
-#pragma unroll
-    for (int i = 0; i < STAGES - 1; ++i) issue((uint32_t)i);
-    flush_empty(b0);
-    for (uint32_t i = 0; i < nblk; ++i) {
-        issue(i + STAGES - 1);
-        cp_async_wait<STAGES - 1>();
-        __syncwarp();
-        consume(i);
-        __syncwarp();
-        if (!split && b0 + i + 1 == wend) {
-            store_window(wi);
-            ++wi;
-            wend = __shfl_sync(0xffffffffu, my_rwo, (int)(wi < nw ? wi + 1 : nw));
-            flush_empty(b0 + i + 1);
+    // ---- pipelined block loop: two register fragments in flight per warp
+    issue_chunk(0);
+    after_block(b0);  // leading empty windows
+    Frag<FW, F16> fa, fb;
+    if (nblk > 0) load_block(fa, 0);
+    if (nblk > 1) load_block(fb, 1);
+    for (uint32_t i = 0; i < nblk; i += 2) {
+        mma_block<FW, F16>(acc, fa);
+        after_block(b0 + i + 1);
+        if (i + 2 < nblk) load_block(fa, i + 2);
+        if (i + 1 < nblk) {
+            mma_block<FW, F16>(acc, fb);
+            after_block(b0 + i + 2);
+            if (i + 3 < nblk) load_block(fb, i + 3);
         }
     }
-    cp_async_wait<0>();
+    cp_async_wait_all();
 
     if (split) {
         // ---- cross-row write-back of a split window: partial -> workspace, last arriver reduces
         const uint32_t sid = ub.x, seg = ub.y, nseg = ub.z, slot = ub.w;
         float *tile = p.ws + ((int64_t)slot * p.nslices + slice) * (8 * FW);
-#pragma unroll
-        for (int s = 0; s < 2; ++s) {
-            float *dst = tile + (2 * t + s) * FW + g * (FW / 8);
-#pragma unroll
-            for (int m = 0; m < MT; ++m) {
-                dst[2 * m] = acc[m][s];
-                dst[2 * m + 1] = acc[m][2 + s];
-            }
-        }
+        store_rows(tile, FW, 0, false);
         __threadfence();
         __syncwarp();
         uint32_t prev = 0;
         if (lane == 0) prev = atomicAdd(p.counters + (int64_t)sid * p.nslices + slice, 1u);
         prev = __shfl_sync(0xffffffffu, prev, 0);
-        (void)seg;
         if (prev == nseg - 1) {
             __threadfence();
             const float *first = p.ws + ((int64_t)(slot - seg) * p.nslices + slice) * (8 * FW);
@@ -410,11 +388,16 @@ __global__ void __launch_bounds__(WARPS * 32) spmm_bittcf_kernel(const KParams p
                 const float *src = first + (int64_t)k * p.nslices * (8 * FW);
 #pragma unroll
                 for (int s = 0; s < 2; ++s) {
-                    const float *row = src + (2 * t + s) * FW + g * (FW / 8);
+                    const float *row = src + (2 * t + s) * FW + VW * g;
 #pragma unroll
-                    for (int m = 0; m < MT; ++m) {
-                        acc[m][s] += __ldcg(row + 2 * m);
-                        acc[m][2 + s] += __ldcg(row + 2 * m + 1);
+                    for (int j = 0; j < NV; ++j) {
+#pragma unroll
+                        for (int e = 0; e < VW; e += 2) {
+                            const int m = (VW / 2) * j + (e >> 1);
+                            const float2 v = __ldcg(reinterpret_cast<const float2 *>(row + 8 * VW * j + e));
+                            acc[m][s] += v.x;
+                            acc[m][2 + s] += v.y;
+                        }
                     }
                 }
             }
@@ -424,24 +407,30 @@ __global__ void __launch_bounds__(WARPS * 32) spmm_bittcf_kernel(const KParams p
     }
 }
 
+// B -> TF32 (RNA) once per execute; each B row is then gathered by many windows.
+__global__ void round_b_tf32_kernel(const float4 *__restrict__ in, float4 *__restrict__ out, int64_t n4)
+{
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n4; e += (int64_t)gridDim.x * blockDim.x) {
+        float4 v = __ldcs(in + e);
+        uint32_t a, b, c, d;
+        asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(a) : "f"(v.x));
+        asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(b) : "f"(v.y));
+        asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(c) : "f"(v.z));
+        asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(d) : "f"(v.w));
+        out[e] = make_float4(__uint_as_float(a), __uint_as_float(b), __uint_as_float(c), __uint_as_float(d));
+    }
+}
+
 // ------------------------------------------------------------------ launch
 
-template <int FW, bool F16, int WARPS, int STAGES>
+template <int FW, bool F16, int WARPS>
 accspmm_status launch_cfg(const KParams &kp, int64_t n_units, cudaStream_t stream)
 {
-    using SM = WarpSmem<FW, F16, STAGES>;
-    const size_t smem = sizeof(SM) * WARPS;
-    auto kern = spmm_bittcf_kernel<FW, F16, WARPS, STAGES>;
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return fail(ACCSPMM_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
-        configured = true;
-    }
+    auto kern = spmm_bittcf_kernel<FW, F16, WARPS>;
     const int64_t groups = (n_units + WARPS - 1) / WARPS;
     const int64_t grid = groups * kp.nslices;
     if (grid > 0x7FFFFFFFll) return fail(ACCSPMM_ERR_UNSUPPORTED, "grid too large");
-    kern<<<(unsigned)grid, WARPS * 32, smem, stream>>>(kp);
+    kern<<<(unsigned)grid, WARPS * 32, 0, stream>>>(kp);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(ACCSPMM_ERR_CUDA, std::string("spmm launch: ") + cudaGetErrorString(e));
     return ACCSPMM_OK;
@@ -456,19 +445,31 @@ int env_int(const char *name, int dflt)
 template <int FW, bool F16>
 accspmm_status launch_fw(const KParams &kp, int64_t n_units, cudaStream_t stream)
 {
-    // (warps per CTA, stages) variants; ACCSPMM_KCFG selects one for tuning.
+    // warps per CTA; ACCSPMM_KCFG selects a variant for tuning
     switch (env_int("ACCSPMM_KCFG", 0)) {
-    case 1: return launch_cfg<FW, F16, 4, 3>(kp, n_units, stream);
-    case 2: return launch_cfg<FW, F16, 4, 2>(kp, n_units, stream);
-    case 3: return launch_cfg<FW, F16, 8, 2>(kp, n_units, stream);
-    default: return launch_cfg<FW, F16, 4, 4>(kp, n_units, stream);
+    case 1: return launch_cfg<FW, F16, 2>(kp, n_units, stream);
+    case 2: return launch_cfg<FW, F16, 8>(kp, n_units, stream);
+    default: return launch_cfg<FW, F16, 4>(kp, n_units, stream);
     }
 }
 
 }  // namespace
 
-accspmm_status launch_spmm(const DevicePlan &d, const void *B, int64_t N, float *C, float *ws, uint32_t *counters,
-                           void *stream)
+accspmm_status launch_round_b(const float *B, float *Br, int64_t n, void *stream)
+{
+    const int64_t n4 = n / 4;
+    int64_t grid = (n4 + 255) / 256;
+    if (grid > 148 * 16) grid = 148 * 16;
+    if (grid < 1) grid = 1;
+    round_b_tf32_kernel<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const float4 *>(B),
+                                                                        reinterpret_cast<float4 *>(Br), n4);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(ACCSPMM_ERR_CUDA, std::string("round launch: ") + cudaGetErrorString(e));
+    return ACCSPMM_OK;
+}
+
+accspmm_status launch_spmm(const DevicePlan &d, const void *B, const void *zrow, int64_t N, float *C, float *ws,
+                           uint32_t *counters, void *stream)
 {
     if (d.rows == 0) return ACCSPMM_OK;
     const int FW = N % 128 == 0 ? 128 : N % 64 == 0 ? 64 : N % 32 == 0 ? 32 : 16;
@@ -481,6 +482,7 @@ accspmm_status launch_spmm(const DevicePlan &d, const void *B, int64_t N, float 
     kp.units = reinterpret_cast<const uint4 *>(d.units);
     kp.row_map = d.row_map;
     kp.B = B;
+    kp.zrow = zrow;
     kp.C = C;
     kp.ws = ws;
     kp.counters = counters;

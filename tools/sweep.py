@@ -1,0 +1,78 @@
+"""Tuning sweep (GPU box): one matrix, many plan/kernel variants, CUDA-event timing per variant.
+
+usage: python tools/sweep.py --config reddit --N 128 --variants 'kcfg=0' 'kcfg=1,cap=256' ...
+variant keys: kcfg (ACCSPMM_KCFG), cap, balance, reorder, precision, N
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+import gen
+import paper_2501_09251_b200 as acc
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="reddit")
+    ap.add_argument("--N", type=int, default=128)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--variants", nargs="+", default=["kcfg=0"])
+    ap.add_argument("--out", default=None)
+    a = ap.parse_args()
+    cfg, A = gen.make_config(a.config)
+    vals = gen.values_uniform(A.nnz, cfg.seed_A + 1)
+    Bs = {}
+    flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
+    plans = {}
+    res = []
+    for v in a.variants:
+        kv = dict(x.split("=") for x in v.split(",") if x)
+        N = int(kv.get("N", a.N))
+        prec = kv.get("precision", "tf32")
+        os.environ["ACCSPMM_KCFG"] = kv.get("kcfg", "0")
+        key = (prec, kv.get("balance", "auto"), int(kv.get("cap", 0)), kv.get("reorder", "off"))
+        if key not in plans:
+            t0 = time.perf_counter()
+            plans[key] = acc.Plan(A.M, A.K, A.rowptr, A.colidx, vals, precision=prec, balance=key[1],
+                                  unit_cap=key[2], reorder=key[3])
+            plans[key].create_s = time.perf_counter() - t0
+        p = plans[key]
+        if (prec, N) not in Bs:
+            B = gen.dense_normal(A.K, N, cfg.seed_B)
+            Bs[(prec, N)] = torch.from_numpy(B).cuda().to(torch.float16 if prec == "fp16" else torch.float32)
+        Bd = Bs[(prec, N)]
+        C = torch.empty((A.M, N), device="cuda")
+        for _ in range(3):
+            p.execute(Bd, C)
+        ts = []
+        for _ in range(a.steps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            p.execute(Bd, C)
+            e1.record()
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        ms = float(np.median(ts))
+        bm = acc.bytes_model(p.info, N)
+        r = {"variant": v, "ms": ms, "ms_min": float(min(ts)), "GFLOPs": bm["flops"] / ms / 1e6,
+             "model_GBs": bm["total"] / ms / 1e6, "NB": p.info["NB"], "sum_U": p.info["sum_U"],
+             "units": p.info["n_units"], "cap": p.info["unit_cap"], "balanced": p.info["balanced"],
+             "split": p.info["n_split_windows"], "reorder_ms": p.info["ms_reorder"],
+             "create_s": round(p.create_s, 2), "reorder_applied": p.info["reorder_applied"]}
+        print(json.dumps(r), flush=True)
+        res.append(r)
+    if a.out:
+        with open(a.out, "w") as f:
+            for r in res:
+                f.write(json.dumps(r) + "\n")
+
+
+if __name__ == "__main__":
+    main()
