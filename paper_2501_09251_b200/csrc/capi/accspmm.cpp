@@ -57,14 +57,17 @@ static double ms_since(std::chrono::steady_clock::time_point t0)
     return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
 }
 
+// pad = extra zeroed elements after the data (the TMA value window may read up to
+// 16 bytes past the last value of a block)
 template <class T>
-static accspmm_status upload(T **dst, const std::vector<T> &src, int64_t &bytes)
+static accspmm_status upload(T **dst, const std::vector<T> &src, int64_t &bytes, size_t pad = 0)
 {
-    size_t n = src.size() ? src.size() : 1;
+    size_t n = (src.size() ? src.size() : 1) + pad;
     cudaError_t e = cudaMalloc((void **)dst, n * sizeof(T));
     if (e != cudaSuccess) return e == cudaErrorMemoryAllocation ? fail(ACCSPMM_ERR_OUT_OF_MEMORY, "cudaMalloc")
                                                                 : cuda_fail(e, "cudaMalloc");
     bytes += (int64_t)(n * sizeof(T));
+    if (pad || src.empty()) cudaMemset(*dst, 0, n * sizeof(T));
     if (!src.empty()) {
         e = cudaMemcpy(*dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice);
         if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy H2D");
@@ -231,8 +234,8 @@ accspmm_status accspmm_plan_create_ex(int64_t M, int64_t K, const int64_t *rowpt
         if (st == ACCSPMM_OK) st = upload(&d.a2b, F.a2b, bytes);
         if (st == ACCSPMM_OK) st = upload(&d.bits, F.bits, bytes);
         if (st == ACCSPMM_OK) {
-            if (opt.precision == ACCSPMM_FP16) st = upload((uint16_t **)&d.vals, F.v16, bytes);
-            else st = upload((float **)&d.vals, F.v32, bytes);
+            if (opt.precision == ACCSPMM_FP16) st = upload((uint16_t **)&d.vals, F.v16, bytes, 16);
+            else st = upload((float **)&d.vals, F.v32, bytes, 16);
         }
         if (st == ACCSPMM_OK) st = upload(&d.units, p->units_host, bytes);
         if (st == ACCSPMM_OK && opt.nparts == 1 && !perm.empty()) st = upload(&d.row_map, p->orig_rows, bytes);
