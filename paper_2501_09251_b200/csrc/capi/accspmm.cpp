@@ -227,7 +227,7 @@ accspmm_status accspmm_plan_create_ex(int64_t M, int64_t K, const int64_t *rowpt
         if (e != cudaSuccess) { delete p; return cuda_fail(e, "cudaSetDevice"); }
         DevicePlan &d = p->dev;
         d.W = F.W; d.NB = F.NB; d.nnz = F.nnz; d.rows = F.rows; d.n_units = I.n_units;
-        d.n_split = S.n_split; d.n_segments = S.n_segments; d.precision = opt.precision;
+        d.n_split = S.n_split; d.n_segments = S.n_segments; d.precision = opt.precision; d.K = K;
         int64_t bytes = 0;
         st = upload(&d.rwo, F.rwo, bytes);
         if (st == ACCSPMM_OK) st = upload(&d.tco, F.tco, bytes);

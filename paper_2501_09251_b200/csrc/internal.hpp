@@ -76,6 +76,10 @@ struct DevicePlan {
     void *vals = nullptr;
     uint32_t *units = nullptr;     // [n_units][8]
     uint32_t *row_map = nullptr;   // slab row -> C row (nparts == 1 with a permutation), else null
+    int64_t K = 0;                 // rows of B (padding lanes gather row K -> TMA zero fill)
+    // cached TMA tensor map of the last B operand (key: ptr, N, FW, dtype)
+    mutable uint64_t tmap_key[4] = {0, 0, 0, 0};
+    alignas(64) mutable unsigned char tmap[128] = {};
 };
 
 accspmm_status launch_spmm(const DevicePlan &p, const void *B, const void *zrow, int64_t N, float *C, float *ws,

@@ -29,6 +29,8 @@
 //     stores C rows with st.global.cs through the reordering permutation (Q12);
 //   * split windows: partial tile -> workspace, the last-arriving segment (atomic
 //     counter) sums all partials in segment order (deterministic, Q18).
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -171,6 +173,7 @@ struct KParams {
     int64_t rows;
     int64_t n_units;
     int32_t nslices;
+    int32_t Krows;
 };
 
 template <int FW, bool F16>
@@ -680,6 +683,270 @@ __global__ void __launch_bounds__(WARPS * 32) spmm_bittcf_tma_kernel(const KPara
     }
 }
 
+
+// ================================================================== v4: TMA gather4
+//
+// v3 issues 9 bulk copies per TC block and becomes TMA-request bound (~10 SM
+// cycles per request).  v4 uses the sm_100 tensor gather:
+// cp.async.bulk.tensor.2d.tile::gather4 brings 4 arbitrary B rows (box FW+8
+// elements wide) per instruction, so a block costs 2 gathers + 1 bulk copy of its
+// values.  Padding lanes ask for row K, which the TMA zero-fills.
+// The box is 8 elements wider than the slice so consecutive gathered rows land
+// 32 B (TF32) / 16 B (FP16) off a 128-byte bank period: the fragment LDS of each
+// 8-lane phase then touches 8 distinct bank groups.  Gather 1 carries the rows of
+// fragment x (TF32 rows 0-3, FP16 rows 0,2,4,6), gather 2 those of fragment y.
+
+template <int FW, bool F16>
+struct G4Cfg {
+    using CF = Cfg<FW, F16>;
+    static constexpr int BOXE = FW + 8;                      // box width in elements
+    static constexpr int RS = BOXE * CF::ES;                 // gathered row stride in smem
+    static constexpr int GRP = (4 * RS + 127) / 128 * 128;   // one gather4 (4 rows), 128-aligned
+    static constexpr int VALB = F16 ? 144 : 272;
+    static constexpr int STAGE = 2 * GRP + VALB + 16;        // + mask/voff stash
+    static constexpr int STAGE_AL = (STAGE + 127) / 128 * 128;
+};
+
+template <int FW, bool F16, int STAGES>
+struct G4WarpSmem {
+    alignas(128) uint8_t stage[STAGES][G4Cfg<FW, F16>::STAGE_AL];
+    ChunkSmem ch[2];
+    uint64_t bar[STAGES];
+};
+
+__device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap *map, int32_t col, int32_t r0, int32_t r1,
+                                            int32_t r2, int32_t r3, uint32_t bar, uint64_t pol)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;\n"
+        ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar),
+          "l"(pol)
+        : "memory");
+}
+
+template <int FW, bool F16, int WARPS, int STAGES>
+__global__ void __launch_bounds__(WARPS * 32)
+    spmm_bittcf_g4_kernel(const KParams p, const __grid_constant__ CUtensorMap tmap)
+{
+    using CF = Cfg<FW, F16>;
+    using GC = G4Cfg<FW, F16>;
+    using SM = G4WarpSmem<FW, F16, STAGES>;
+    using V = typename CF::V;
+    constexpr int MT = CF::MT, NV = CF::NV, VW = CF::VW;
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int slice = (int)(blockIdx.x % (unsigned)p.nslices);
+    const int64_t u = (int64_t)(blockIdx.x / (unsigned)p.nslices) * WARPS + warp;
+    if (u >= p.n_units) return;  // warp-uniform; only warp-scoped synchronisation below
+    SM &sm = reinterpret_cast<SM *>(smem_raw)[warp];
+    const uint64_t pol_keep = policy_evict_last();
+    const uint64_t pol_stream = policy_evict_first();
+    if (lane == 0) {
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+#pragma unroll
+        for (int s = 0; s < STAGES; ++s) mbar_init(smem_u32(&sm.bar[s]), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncwarp();
+
+    const uint4 ua = __ldg(p.units + 2 * u);
+    const uint4 ub = __ldg(p.units + 2 * u + 1);
+    const uint32_t w0 = ua.x, nw = ua.y, b0 = ua.z, b1 = ua.w;
+    const bool split = ub.x != kNoSplit;
+    const int64_t f0 = (int64_t)slice * FW;
+    const uint32_t my_rwo = (uint32_t)lane <= nw ? __ldg(p.rwo + w0 + lane) : 0u;
+    const uint32_t nblk = b1 - b0;
+    const int g = lane >> 2, t = lane & 3;
+
+    auto issue_chunk = [&](uint32_t i) {
+        if (i < nblk) {
+            ChunkSmem &c = sm.ch[(i >> 5) & 1];
+            const uint32_t b = b0 + i;
+            const uint32_t cnt = min((uint32_t)kChunk, nblk - i);
+            if ((uint32_t)lane < cnt) {
+                cp_async8(smem_u32(&c.mask[lane]), p.bits + b + lane, pol_stream);
+                cp_async4(smem_u32(&c.tco[lane]), p.tco + b + lane, pol_stream);
+            }
+            const uint4 *src4 = reinterpret_cast<const uint4 *>(p.a2b + (size_t)b * 8);
+            if ((uint32_t)lane < 2 * cnt) cp_async16(smem_u32(&c.a2b[4 * lane]), src4 + lane, pol_stream);
+            if ((uint32_t)lane + 32 < 2 * cnt) cp_async16(smem_u32(&c.a2b[4 * (lane + 32)]), src4 + lane + 32, pol_stream);
+        }
+        cp_async_commit();
+    };
+
+    // ---- producer (lane 0): two gather4 of the block's B rows + one bulk copy of its values
+    auto issue = [&](uint32_t i) {
+        if (i >= nblk) return;
+        if ((i & 31u) == 0) {
+            cp_async_wait_all();
+            __syncwarp();
+            issue_chunk(i + kChunk);
+        }
+        if (lane == 0) {
+            const ChunkSmem &c = sm.ch[(i >> 5) & 1];
+            const uint32_t cs = i & 31u;
+            const uint64_t mask = c.mask[cs];
+            const uint32_t t0 = c.tco[cs];
+            const int cnt = __popcll(mask);
+            uint64_t cm = mask | (mask >> 32);
+            cm |= cm >> 16;
+            cm |= cm >> 8;
+            const uint4 ca = *reinterpret_cast<const uint4 *>(&c.a2b[cs * 8]);
+            const uint4 cb = *reinterpret_cast<const uint4 *>(&c.a2b[cs * 8 + 4]);
+            const int32_t K = p.Krows;
+            const int32_t r[8] = {(cm & 1u) ? (int32_t)ca.x : K,   (cm & 2u) ? (int32_t)ca.y : K,
+                                  (cm & 4u) ? (int32_t)ca.z : K,   (cm & 8u) ? (int32_t)ca.w : K,
+                                  (cm & 16u) ? (int32_t)cb.x : K,  (cm & 32u) ? (int32_t)cb.y : K,
+                                  (cm & 64u) ? (int32_t)cb.z : K,  (cm & 128u) ? (int32_t)cb.w : K};
+            constexpr uint32_t VA = F16 ? 8u : 4u;
+            const uint32_t vs = t0 & ~(VA - 1u);
+            const uint32_t vbytes = ((t0 + (uint32_t)cnt - vs + VA - 1u) & ~(VA - 1u)) * CF::ES;
+            const int s = (int)(i % STAGES);
+            const uint32_t bar = smem_u32(&sm.bar[s]);
+            uint8_t *st = sm.stage[s];
+            fence_proxy_async();
+            mbar_arrive_expect_tx(bar, 8u * GC::RS + vbytes);
+            const int32_t col = (int32_t)(slice * FW);
+            if constexpr (!F16) {
+                tma_gather4(smem_u32(st), &tmap, col, r[0], r[1], r[2], r[3], bar, pol_keep);
+                tma_gather4(smem_u32(st + GC::GRP), &tmap, col, r[4], r[5], r[6], r[7], bar, pol_keep);
+            } else {
+                tma_gather4(smem_u32(st), &tmap, col, r[0], r[2], r[4], r[6], bar, pol_keep);
+                tma_gather4(smem_u32(st + GC::GRP), &tmap, col, r[1], r[3], r[5], r[7], bar, pol_keep);
+            }
+            bulk_g2s(smem_u32(st + 2 * GC::GRP), reinterpret_cast<const char *>(p.vals) + (int64_t)vs * CF::ES, vbytes,
+                     bar, pol_stream);
+            *reinterpret_cast<uint64_t *>(st + 2 * GC::GRP + GC::VALB) = mask;
+            *reinterpret_cast<uint32_t *>(st + 2 * GC::GRP + GC::VALB + 8) = t0 - vs;
+        }
+    };
+
+    float acc[MT][4];
+#pragma unroll
+    for (int m = 0; m < MT; ++m) acc[m][0] = acc[m][1] = acc[m][2] = acc[m][3] = 0.f;
+
+    auto consume = [&](uint32_t i) {
+        const int s = (int)(i % STAGES);
+        mbar_wait(smem_u32(&sm.bar[s]), (i / STAGES) & 1u);
+        const uint8_t *st = sm.stage[s];
+        const uint64_t mask = *reinterpret_cast<const uint64_t *>(st + 2 * GC::GRP + GC::VALB);
+        const uint32_t voff = *reinterpret_cast<const uint32_t *>(st + 2 * GC::GRP + GC::VALB + 8);
+        Frag<FW, F16> fr;
+        const uint8_t *ra = st + t * GC::RS + CF::VB * g;
+        const uint8_t *rb = st + GC::GRP + t * GC::RS + CF::VB * g;
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+            fr.x[j] = *reinterpret_cast<const V *>(ra + 8 * CF::VB * j);
+            fr.y[j] = *reinterpret_cast<const V *>(rb + 8 * CF::VB * j);
+        }
+        const uint64_t one = 1ull;
+        if constexpr (!F16) {
+            const float *sv = reinterpret_cast<const float *>(st + 2 * GC::GRP) + voff;
+            const int k0 = g * 8 + t, k1 = k0 + 4;
+            fr.b0 = ((mask >> k0) & one) ? __float_as_uint(sv[__popcll(mask & ((one << k0) - one))]) : 0u;
+            fr.b1 = ((mask >> k1) & one) ? __float_as_uint(sv[__popcll(mask & ((one << k1) - one))]) : 0u;
+        } else {
+            const unsigned short *sv = reinterpret_cast<const unsigned short *>(st + 2 * GC::GRP) + voff;
+            const int k0 = g * 8 + 2 * t;
+            const uint32_t lo = ((mask >> k0) & one) ? (uint32_t)sv[__popcll(mask & ((one << k0) - one))] : 0u;
+            const uint32_t hi =
+                ((mask >> (k0 + 1)) & one) ? (uint32_t)sv[__popcll(mask & ((one << (k0 + 1)) - one))] : 0u;
+            fr.b0 = lo | (hi << 16);
+            fr.b1 = 0u;
+        }
+        __syncwarp();
+        mma_block<FW, F16>(acc, fr);
+    };
+
+    auto store_rows = [&](float *base, int64_t ld, int64_t lr0, bool remap) {
+#pragma unroll
+        for (int s2 = 0; s2 < 2; ++s2) {
+            const int64_t lr = lr0 + 2 * t + s2;
+            if (!remap || lr < p.rows) {
+                const int64_t orow = remap ? (p.row_map ? (int64_t)__ldg(p.row_map + lr) : lr) : (2 * t + s2);
+                float *dst = base + orow * ld + VW * g;
+#pragma unroll
+                for (int j = 0; j < NV; ++j) {
+                    float *d = dst + 8 * VW * j;
+                    if constexpr (VW == 2) {
+                        st_cs(d, acc[j][s2], acc[j][2 + s2]);
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < VW / 4; ++q) {
+                            const int m0 = (VW / 2) * j + 2 * q;
+                            st_cs(d + 4 * q, acc[m0][s2], acc[m0][2 + s2], acc[m0 + 1][s2], acc[m0 + 1][2 + s2]);
+                        }
+                    }
+                }
+            }
+        }
+    };
+    auto store_window = [&](uint32_t wi) {
+        store_rows(p.C + f0, p.N, (int64_t)(w0 + wi) * 8, true);
+#pragma unroll
+        for (int m = 0; m < MT; ++m) acc[m][0] = acc[m][1] = acc[m][2] = acc[m][3] = 0.f;
+    };
+    uint32_t wi = 0;
+    uint32_t wend = split ? b1 : __shfl_sync(0xffffffffu, my_rwo, 1);
+    auto after_block = [&](uint32_t jnext) {
+        while (!split && wi < nw && wend == jnext) {
+            store_window(wi);
+            ++wi;
+            wend = __shfl_sync(0xffffffffu, my_rwo, (int)(wi < nw ? wi + 1 : nw));
+        }
+    };
+
+    issue_chunk(0);
+    after_block(b0);
+#pragma unroll
+    for (int i = 0; i < STAGES - 1; ++i) issue((uint32_t)i);
+    for (uint32_t i = 0; i < nblk; ++i) {
+        issue(i + STAGES - 1);
+        consume(i);
+        after_block(b0 + i + 1);
+    }
+    cp_async_wait_all();
+
+    if (split) {
+        const uint32_t sid = ub.x, seg = ub.y, nseg = ub.z, slot = ub.w;
+        float *tile = p.ws + ((int64_t)slot * p.nslices + slice) * (8 * FW);
+        store_rows(tile, FW, 0, false);
+        __threadfence();
+        __syncwarp();
+        uint32_t prev = 0;
+        if (lane == 0) prev = atomicAdd(p.counters + (int64_t)sid * p.nslices + slice, 1u);
+        prev = __shfl_sync(0xffffffffu, prev, 0);
+        if (prev == nseg - 1) {
+            __threadfence();
+            const float *first = p.ws + ((int64_t)(slot - seg) * p.nslices + slice) * (8 * FW);
+#pragma unroll
+            for (int m = 0; m < MT; ++m) acc[m][0] = acc[m][1] = acc[m][2] = acc[m][3] = 0.f;
+            for (uint32_t k = 0; k < nseg; ++k) {
+                const float *src = first + (int64_t)k * p.nslices * (8 * FW);
+#pragma unroll
+                for (int s2 = 0; s2 < 2; ++s2) {
+                    const float *row = src + (2 * t + s2) * FW + VW * g;
+#pragma unroll
+                    for (int j = 0; j < NV; ++j) {
+#pragma unroll
+                        for (int e = 0; e < VW; e += 2) {
+                            const int m = (VW / 2) * j + (e >> 1);
+                            const float2 v = __ldcg(reinterpret_cast<const float2 *>(row + 8 * VW * j + e));
+                            acc[m][s2] += v.x;
+                            acc[m][2 + s2] += v.y;
+                        }
+                    }
+                }
+            }
+            store_window(0);
+            if (lane == 0) p.counters[(int64_t)sid * p.nslices + slice] = 0u;
+        }
+    }
+}
+
 // B -> TF32 (RNA) once per execute; each B row is then gathered by many windows.
 __global__ void round_b_tf32_kernel(const float4 *__restrict__ in, float4 *__restrict__ out, int64_t n4)
 {
@@ -738,9 +1005,77 @@ accspmm_status launch_tma(const KParams &kp, int64_t n_units, cudaStream_t strea
     return ACCSPMM_OK;
 }
 
-template <int FW, bool F16>
-accspmm_status launch_fw(const KParams &kp, int64_t n_units, cudaStream_t stream)
+template <int FW, bool F16, int WARPS, int STAGES>
+accspmm_status launch_g4(const KParams &kp, const CUtensorMap *map, int64_t n_units, cudaStream_t stream)
 {
+    using SM = G4WarpSmem<FW, F16, STAGES>;
+    const size_t smem = sizeof(SM) * WARPS;
+    auto kern = spmm_bittcf_g4_kernel<FW, F16, WARPS, STAGES>;
+    static int configured_device = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (configured_device != dev) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return fail(ACCSPMM_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+        configured_device = dev;
+    }
+    const int64_t groups = (n_units + WARPS - 1) / WARPS;
+    const int64_t grid = groups * kp.nslices;
+    if (grid > 0x7FFFFFFFll) return fail(ACCSPMM_ERR_UNSUPPORTED, "grid too large");
+    kern<<<(unsigned)grid, WARPS * 32, smem, stream>>>(kp, *map);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(ACCSPMM_ERR_CUDA, std::string("spmm launch: ") + cudaGetErrorString(e));
+    return ACCSPMM_OK;
+}
+
+// TMA tensor map of B (2D: K rows x N columns, box = (FW+8) x 1 for gather4), cached in the plan
+accspmm_status tensor_map(const DevicePlan &d, const void *B, int64_t N, int FW, const CUtensorMap **out)
+{
+    const uint64_t key[4] = {(uint64_t)(uintptr_t)B, (uint64_t)N, (uint64_t)FW, (uint64_t)d.precision + 1};
+    CUtensorMap *m = reinterpret_cast<CUtensorMap *>(d.tmap);
+    if (!(key[0] == d.tmap_key[0] && key[1] == d.tmap_key[1] && key[2] == d.tmap_key[2] && key[3] == d.tmap_key[3])) {
+        static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+        if (!encode) {
+            cudaDriverEntryPointQueryResult q;
+            void *fn = nullptr;
+            cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+            if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn)
+                return fail(ACCSPMM_ERR_CUDA, "cuTensorMapEncodeTiled entry point not available");
+            encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+        }
+        const bool f16 = d.precision == ACCSPMM_FP16;
+        const cuuint64_t es = f16 ? 2 : 4;
+        cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)d.K};
+        cuuint64_t strides[1] = {(cuuint64_t)N * es};
+        cuuint32_t box[2] = {(cuuint32_t)(FW + 8), 1u};
+        cuuint32_t estr[2] = {1u, 1u};
+        CUresult r = encode(m, f16 ? CU_TENSOR_MAP_DATA_TYPE_UINT16 : CU_TENSOR_MAP_DATA_TYPE_UINT32, 2,
+                            const_cast<void *>(B), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(ACCSPMM_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+        for (int k = 0; k < 4; ++k) d.tmap_key[k] = key[k];
+    }
+    *out = m;
+    return ACCSPMM_OK;
+}
+
+template <int FW, bool F16>
+accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, int64_t n_units, cudaStream_t stream)
+{
+    const int kcfg = env_int("ACCSPMM_KCFG", -1);
+    if (kcfg < 0 || kcfg >= 20) {  // TMA gather4 (v4): default
+        const CUtensorMap *map = nullptr;
+        accspmm_status st = tensor_map(d, B, kp.N, FW, &map);
+        if (st != ACCSPMM_OK) return st;
+        switch (kcfg) {
+        case 21: return launch_g4<FW, F16, 4, 2>(kp, map, n_units, stream);
+        case 22: return launch_g4<FW, F16, 2, 3>(kp, map, n_units, stream);
+        case 23: return launch_g4<FW, F16, 4, 3>(kp, map, n_units, stream);
+        case 24: return launch_g4<FW, F16, 2, 4>(kp, map, n_units, stream);
+        default: return launch_g4<FW, F16, 2, 2>(kp, map, n_units, stream);
+        }
+    }
     // ACCSPMM_KCFG selects a kernel variant for tuning: 0-2 TMA-staged (v3), 10-12 register-direct (v2)
     switch (env_int("ACCSPMM_KCFG", 0)) {
     case 1: return launch_tma<FW, F16, 2, 2>(kp, n_units, stream);
@@ -790,13 +1125,14 @@ accspmm_status launch_spmm(const DevicePlan &d, const void *B, const void *zrow,
     kp.rows = d.rows;
     kp.n_units = d.n_units;
     kp.nslices = (int32_t)(N / FW);
+    kp.Krows = (int32_t)d.K;
     cudaStream_t s = (cudaStream_t)stream;
     const bool f16 = d.precision == ACCSPMM_FP16;
     switch (FW) {
-    case 128: return f16 ? launch_fw<128, true>(kp, d.n_units, s) : launch_fw<128, false>(kp, d.n_units, s);
-    case 64: return f16 ? launch_fw<64, true>(kp, d.n_units, s) : launch_fw<64, false>(kp, d.n_units, s);
-    case 32: return f16 ? launch_fw<32, true>(kp, d.n_units, s) : launch_fw<32, false>(kp, d.n_units, s);
-    default: return f16 ? launch_fw<16, true>(kp, d.n_units, s) : launch_fw<16, false>(kp, d.n_units, s);
+    case 128: return f16 ? launch_fw<128, true>(kp, d, B, d.n_units, s) : launch_fw<128, false>(kp, d, B, d.n_units, s);
+    case 64: return f16 ? launch_fw<64, true>(kp, d, B, d.n_units, s) : launch_fw<64, false>(kp, d, B, d.n_units, s);
+    case 32: return f16 ? launch_fw<32, true>(kp, d, B, d.n_units, s) : launch_fw<32, false>(kp, d, B, d.n_units, s);
+    default: return f16 ? launch_fw<16, true>(kp, d, B, d.n_units, s) : launch_fw<16, false>(kp, d, B, d.n_units, s);
     }
 }
 

@@ -35,7 +35,7 @@ def main():
         kv = dict(x.split("=") for x in v.split(",") if x)
         N = int(kv.get("N", a.N))
         prec = kv.get("precision", "tf32")
-        os.environ["ACCSPMM_KCFG"] = kv.get("kcfg", "0")
+        os.environ["ACCSPMM_KCFG"] = kv.get("kcfg", "-1")
         key = (prec, kv.get("balance", "auto"), int(kv.get("cap", 0)), kv.get("reorder", "off"))
         if key not in plans:
             t0 = time.perf_counter()
