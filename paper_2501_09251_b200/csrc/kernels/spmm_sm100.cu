@@ -702,9 +702,7 @@ struct G4Cfg {
     static constexpr int BOXE = FW + 8;                      // box width in elements
     static constexpr int RS = BOXE * CF::ES;                 // gathered row stride in smem
     static constexpr int GRP = (4 * RS + 127) / 128 * 128;   // one gather4 (4 rows), 128-aligned
-    static constexpr int VALB = F16 ? 144 : 272;
-    static constexpr int STAGE = 2 * GRP + VALB + 16;        // + mask/voff stash
-    static constexpr int STAGE_AL = (STAGE + 127) / 128 * 128;
+    static constexpr int STAGE_AL = 2 * GRP;
 };
 
 template <int FW, bool F16, int STAGES>
@@ -760,6 +758,10 @@ __global__ void __launch_bounds__(WARPS * 32)
     const uint32_t my_rwo = (uint32_t)lane <= nw ? __ldg(p.rwo + w0 + lane) : 0u;
     const uint32_t nblk = b1 - b0;
     const int g = lane >> 2, t = lane & 3;
+    // this lane's two positions of the 8x8 tile (the mma B fragment) and their low-bit masks
+    const int k0 = F16 ? g * 8 + 2 * t : g * 8 + t;
+    const int k1 = F16 ? k0 + 1 : k0 + 4;
+    const uint64_t below0 = (1ull << k0) - 1ull, below1 = (1ull << k1) - 1ull;
 
     auto issue_chunk = [&](uint32_t i) {
         if (i < nblk) {
@@ -777,50 +779,56 @@ __global__ void __launch_bounds__(WARPS * 32)
         cp_async_commit();
     };
 
-    // ---- producer (lane 0): two gather4 of the block's B rows + one bulk copy of its values
-    auto issue = [&](uint32_t i) {
+    // value registers of the blocks in flight (decoded at issue time, one per stage)
+    uint32_t vb0[STAGES], vb1[STAGES];
+
+    // ---- producer: lane 0 issues two gather4 of block i's B rows into stage s;
+    //      every lane decodes its two tile entries and loads their values
+    auto issue = [&](uint32_t i, int s) {
         if (i >= nblk) return;
         if ((i & 31u) == 0) {
             cp_async_wait_all();
             __syncwarp();
             issue_chunk(i + kChunk);
         }
+        const ChunkSmem &c = sm.ch[(i >> 5) & 1];
+        const uint32_t cs = i & 31u;
+        const uint64_t mask = c.mask[cs];
+        const uint32_t t0 = c.tco[cs];
+        if constexpr (!F16) {
+            const float *vp = reinterpret_cast<const float *>(p.vals) + t0;
+            vb0[s] = ((mask >> k0) & 1ull) ? __float_as_uint(__ldg(vp + __popcll(mask & below0))) : 0u;
+            vb1[s] = ((mask >> k1) & 1ull) ? __float_as_uint(__ldg(vp + __popcll(mask & below1))) : 0u;
+        } else {
+            const unsigned short *vp = reinterpret_cast<const unsigned short *>(p.vals) + t0;
+            const uint32_t lo = ((mask >> k0) & 1ull) ? (uint32_t)__ldg(vp + __popcll(mask & below0)) : 0u;
+            const uint32_t hi = ((mask >> k1) & 1ull) ? (uint32_t)__ldg(vp + __popcll(mask & below1)) : 0u;
+            vb0[s] = lo | (hi << 16);
+            vb1[s] = 0u;
+        }
         if (lane == 0) {
-            const ChunkSmem &c = sm.ch[(i >> 5) & 1];
-            const uint32_t cs = i & 31u;
-            const uint64_t mask = c.mask[cs];
-            const uint32_t t0 = c.tco[cs];
-            const int cnt = __popcll(mask);
             uint64_t cm = mask | (mask >> 32);
             cm |= cm >> 16;
             cm |= cm >> 8;
             const uint4 ca = *reinterpret_cast<const uint4 *>(&c.a2b[cs * 8]);
             const uint4 cb = *reinterpret_cast<const uint4 *>(&c.a2b[cs * 8 + 4]);
             const int32_t K = p.Krows;
-            const int32_t r[8] = {(cm & 1u) ? (int32_t)ca.x : K,   (cm & 2u) ? (int32_t)ca.y : K,
-                                  (cm & 4u) ? (int32_t)ca.z : K,   (cm & 8u) ? (int32_t)ca.w : K,
-                                  (cm & 16u) ? (int32_t)cb.x : K,  (cm & 32u) ? (int32_t)cb.y : K,
-                                  (cm & 64u) ? (int32_t)cb.z : K,  (cm & 128u) ? (int32_t)cb.w : K};
-            constexpr uint32_t VA = F16 ? 8u : 4u;
-            const uint32_t vs = t0 & ~(VA - 1u);
-            const uint32_t vbytes = ((t0 + (uint32_t)cnt - vs + VA - 1u) & ~(VA - 1u)) * CF::ES;
-            const int s = (int)(i % STAGES);
+            const int32_t r0 = (cm & 1u) ? (int32_t)ca.x : K, r1 = (cm & 2u) ? (int32_t)ca.y : K;
+            const int32_t r2 = (cm & 4u) ? (int32_t)ca.z : K, r3 = (cm & 8u) ? (int32_t)ca.w : K;
+            const int32_t r4 = (cm & 16u) ? (int32_t)cb.x : K, r5 = (cm & 32u) ? (int32_t)cb.y : K;
+            const int32_t r6 = (cm & 64u) ? (int32_t)cb.z : K, r7 = (cm & 128u) ? (int32_t)cb.w : K;
             const uint32_t bar = smem_u32(&sm.bar[s]);
-            uint8_t *st = sm.stage[s];
+            const uint32_t st = smem_u32(sm.stage[s]);
             fence_proxy_async();
-            mbar_arrive_expect_tx(bar, 8u * GC::RS + vbytes);
+            mbar_arrive_expect_tx(bar, 8u * GC::RS);
             const int32_t col = (int32_t)(slice * FW);
             if constexpr (!F16) {
-                tma_gather4(smem_u32(st), &tmap, col, r[0], r[1], r[2], r[3], bar, pol_keep);
-                tma_gather4(smem_u32(st + GC::GRP), &tmap, col, r[4], r[5], r[6], r[7], bar, pol_keep);
+                tma_gather4(st, &tmap, col, r0, r1, r2, r3, bar, pol_keep);
+                tma_gather4(st + GC::GRP, &tmap, col, r4, r5, r6, r7, bar, pol_keep);
             } else {
-                tma_gather4(smem_u32(st), &tmap, col, r[0], r[2], r[4], r[6], bar, pol_keep);
-                tma_gather4(smem_u32(st + GC::GRP), &tmap, col, r[1], r[3], r[5], r[7], bar, pol_keep);
+                tma_gather4(st, &tmap, col, r0, r2, r4, r6, bar, pol_keep);
+                tma_gather4(st + GC::GRP, &tmap, col, r1, r3, r5, r7, bar, pol_keep);
             }
-            bulk_g2s(smem_u32(st + 2 * GC::GRP), reinterpret_cast<const char *>(p.vals) + (int64_t)vs * CF::ES, vbytes,
-                     bar, pol_stream);
-            *reinterpret_cast<uint64_t *>(st + 2 * GC::GRP + GC::VALB) = mask;
-            *reinterpret_cast<uint32_t *>(st + 2 * GC::GRP + GC::VALB + 8) = t0 - vs;
         }
     };
 
@@ -828,12 +836,10 @@ __global__ void __launch_bounds__(WARPS * 32)
 #pragma unroll
     for (int m = 0; m < MT; ++m) acc[m][0] = acc[m][1] = acc[m][2] = acc[m][3] = 0.f;
 
-    auto consume = [&](uint32_t i) {
-        const int s = (int)(i % STAGES);
+    // ---- consumer: wait for stage s, load the gathered-row fragments, tensor-core MMA
+    auto consume = [&](uint32_t i, int s) {
         mbar_wait(smem_u32(&sm.bar[s]), (i / STAGES) & 1u);
         const uint8_t *st = sm.stage[s];
-        const uint64_t mask = *reinterpret_cast<const uint64_t *>(st + 2 * GC::GRP + GC::VALB);
-        const uint32_t voff = *reinterpret_cast<const uint32_t *>(st + 2 * GC::GRP + GC::VALB + 8);
         Frag<FW, F16> fr;
         const uint8_t *ra = st + t * GC::RS + CF::VB * g;
         const uint8_t *rb = st + GC::GRP + t * GC::RS + CF::VB * g;
@@ -842,22 +848,9 @@ __global__ void __launch_bounds__(WARPS * 32)
             fr.x[j] = *reinterpret_cast<const V *>(ra + 8 * CF::VB * j);
             fr.y[j] = *reinterpret_cast<const V *>(rb + 8 * CF::VB * j);
         }
-        const uint64_t one = 1ull;
-        if constexpr (!F16) {
-            const float *sv = reinterpret_cast<const float *>(st + 2 * GC::GRP) + voff;
-            const int k0 = g * 8 + t, k1 = k0 + 4;
-            fr.b0 = ((mask >> k0) & one) ? __float_as_uint(sv[__popcll(mask & ((one << k0) - one))]) : 0u;
-            fr.b1 = ((mask >> k1) & one) ? __float_as_uint(sv[__popcll(mask & ((one << k1) - one))]) : 0u;
-        } else {
-            const unsigned short *sv = reinterpret_cast<const unsigned short *>(st + 2 * GC::GRP) + voff;
-            const int k0 = g * 8 + 2 * t;
-            const uint32_t lo = ((mask >> k0) & one) ? (uint32_t)sv[__popcll(mask & ((one << k0) - one))] : 0u;
-            const uint32_t hi =
-                ((mask >> (k0 + 1)) & one) ? (uint32_t)sv[__popcll(mask & ((one << (k0 + 1)) - one))] : 0u;
-            fr.b0 = lo | (hi << 16);
-            fr.b1 = 0u;
-        }
-        __syncwarp();
+        fr.b0 = vb0[s];
+        fr.b1 = vb1[s];
+        __syncwarp();  // every lane has read the stage before it is refilled
         mma_block<FW, F16>(acc, fr);
     };
 
@@ -902,11 +895,17 @@ __global__ void __launch_bounds__(WARPS * 32)
     issue_chunk(0);
     after_block(b0);
 #pragma unroll
-    for (int i = 0; i < STAGES - 1; ++i) issue((uint32_t)i);
-    for (uint32_t i = 0; i < nblk; ++i) {
-        issue(i + STAGES - 1);
-        consume(i);
-        after_block(b0 + i + 1);
+    for (int s = 0; s < STAGES - 1; ++s) issue((uint32_t)s, s);
+    for (uint32_t i = 0; i < nblk; i += STAGES) {
+#pragma unroll
+        for (int s = 0; s < STAGES; ++s) {
+            const uint32_t ii = i + (uint32_t)s;
+            if (ii < nblk) {
+                issue(ii + STAGES - 1, (s + STAGES - 1) % STAGES);
+                consume(ii, s);
+                after_block(b0 + ii + 1);
+            }
+        }
     }
     cp_async_wait_all();
 
