@@ -108,6 +108,15 @@ __device__ __forceinline__ void mma_tf32(float (&d)[4], uint32_t a0, uint32_t a1
         : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
+// m16n8k4 TF32: A fragment = (row g, k t), (row g+8, k t) -> both come from one gathered row
+__device__ __forceinline__ void mma_tf32_k4(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t b0)
+{
+    asm volatile(
+        "mma.sync.aligned.m16n8k4.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a0), "r"(a1), "r"(b0));
+}
+
 __device__ __forceinline__ void mma_f16(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t b0)
 {
     asm volatile(
@@ -758,10 +767,14 @@ __global__ void __launch_bounds__(WARPS * 32)
     const uint32_t my_rwo = (uint32_t)lane <= nw ? __ldg(p.rwo + w0 + lane) : 0u;
     const uint32_t nblk = b1 - b0;
     const int g = lane >> 2, t = lane & 3;
-    // this lane's two positions of the 8x8 tile (the mma B fragment) and their low-bit masks
+    // this lane's two positions of the 8x8 tile (the mma B fragment): bit k sits in word k/32;
+    // popc(mask & (2^k - 1)) = popc(lo & below_lo) + popc(hi & below_hi) with lane-constant masks
     const int k0 = F16 ? g * 8 + 2 * t : g * 8 + t;
     const int k1 = F16 ? k0 + 1 : k0 + 4;
-    const uint64_t below0 = (1ull << k0) - 1ull, below1 = (1ull << k1) - 1ull;
+    const uint32_t bit0 = 1u << (k0 & 31), bit1 = 1u << (k1 & 31);
+    const bool hi0 = k0 >= 32, hi1 = k1 >= 32;
+    const uint32_t bl0_lo = hi0 ? 0xFFFFFFFFu : bit0 - 1u, bl0_hi = hi0 ? bit0 - 1u : 0u;
+    const uint32_t bl1_lo = hi1 ? 0xFFFFFFFFu : bit1 - 1u, bl1_hi = hi1 ? bit1 - 1u : 0u;
 
     auto issue_chunk = [&](uint32_t i) {
         if (i < nblk) {
@@ -795,14 +808,18 @@ __global__ void __launch_bounds__(WARPS * 32)
         const uint32_t cs = i & 31u;
         const uint64_t mask = c.mask[cs];
         const uint32_t t0 = c.tco[cs];
+        const uint32_t mlo = (uint32_t)mask, mhi = (uint32_t)(mask >> 32);
+        const bool p0 = ((hi0 ? mhi : mlo) & bit0) != 0u, p1 = ((hi1 ? mhi : mlo) & bit1) != 0u;
+        const uint32_t i0 = t0 + __popc(mlo & bl0_lo) + __popc(mhi & bl0_hi);
+        const uint32_t i1 = t0 + __popc(mlo & bl1_lo) + __popc(mhi & bl1_hi);
         if constexpr (!F16) {
-            const float *vp = reinterpret_cast<const float *>(p.vals) + t0;
-            vb0[s] = ((mask >> k0) & 1ull) ? __float_as_uint(__ldg(vp + __popcll(mask & below0))) : 0u;
-            vb1[s] = ((mask >> k1) & 1ull) ? __float_as_uint(__ldg(vp + __popcll(mask & below1))) : 0u;
+            const float *vp = reinterpret_cast<const float *>(p.vals);
+            vb0[s] = p0 ? __float_as_uint(__ldg(vp + i0)) : 0u;
+            vb1[s] = p1 ? __float_as_uint(__ldg(vp + i1)) : 0u;
         } else {
-            const unsigned short *vp = reinterpret_cast<const unsigned short *>(p.vals) + t0;
-            const uint32_t lo = ((mask >> k0) & 1ull) ? (uint32_t)__ldg(vp + __popcll(mask & below0)) : 0u;
-            const uint32_t hi = ((mask >> k1) & 1ull) ? (uint32_t)__ldg(vp + __popcll(mask & below1)) : 0u;
+            const unsigned short *vp = reinterpret_cast<const unsigned short *>(p.vals);
+            const uint32_t lo = p0 ? (uint32_t)__ldg(vp + i0) : 0u;
+            const uint32_t hi = p1 ? (uint32_t)__ldg(vp + i1) : 0u;
             vb0[s] = lo | (hi << 16);
             vb1[s] = 0u;
         }
@@ -819,7 +836,8 @@ __global__ void __launch_bounds__(WARPS * 32)
             const int32_t r6 = (cm & 64u) ? (int32_t)cb.z : K, r7 = (cm & 128u) ? (int32_t)cb.w : K;
             const uint32_t bar = smem_u32(&sm.bar[s]);
             const uint32_t st = smem_u32(sm.stage[s]);
-            fence_proxy_async();
+            // no proxy fence: the stage's previous generic reads fed this warp's mma.sync,
+            // which cannot issue before every lane's LDS has returned
             mbar_arrive_expect_tx(bar, 8u * GC::RS);
             const int32_t col = (int32_t)(slice * FW);
             if constexpr (!F16) {
@@ -840,18 +858,31 @@ __global__ void __launch_bounds__(WARPS * 32)
     auto consume = [&](uint32_t i, int s) {
         mbar_wait(smem_u32(&sm.bar[s]), (i / STAGES) & 1u);
         const uint8_t *st = sm.stage[s];
-        Frag<FW, F16> fr;
         const uint8_t *ra = st + t * GC::RS + CF::VB * g;
         const uint8_t *rb = st + GC::GRP + t * GC::RS + CF::VB * g;
+        if constexpr (!F16 && CF::VW == 4) {
+            // two k=4 halves of the 8x8 tile: rows t (k = 0..3) and t+4 (k = 4..7); each
+            // LDS.128 of one row feeds the A operands of two m16 tiles directly
 #pragma unroll
-        for (int j = 0; j < NV; ++j) {
-            fr.x[j] = *reinterpret_cast<const V *>(ra + 8 * CF::VB * j);
-            fr.y[j] = *reinterpret_cast<const V *>(rb + 8 * CF::VB * j);
+            for (int j = 0; j < NV; ++j) {
+                const uint4 x = *reinterpret_cast<const uint4 *>(ra + 8 * CF::VB * j);
+                const uint4 y = *reinterpret_cast<const uint4 *>(rb + 8 * CF::VB * j);
+                mma_tf32_k4(acc[2 * j], x.x, x.y, vb0[s]);
+                mma_tf32_k4(acc[2 * j + 1], x.z, x.w, vb0[s]);
+                mma_tf32_k4(acc[2 * j], y.x, y.y, vb1[s]);
+                mma_tf32_k4(acc[2 * j + 1], y.z, y.w, vb1[s]);
+            }
+        } else {
+            Frag<FW, F16> fr;
+#pragma unroll
+            for (int j = 0; j < NV; ++j) {
+                fr.x[j] = *reinterpret_cast<const V *>(ra + 8 * CF::VB * j);
+                fr.y[j] = *reinterpret_cast<const V *>(rb + 8 * CF::VB * j);
+            }
+            fr.b0 = vb0[s];
+            fr.b1 = vb1[s];
+            mma_block<FW, F16>(acc, fr);
         }
-        fr.b0 = vb0[s];
-        fr.b1 = vb1[s];
-        __syncwarp();  // every lane has read the stage before it is refilled
-        mma_block<FW, F16>(acc, fr);
     };
 
     auto store_rows = [&](float *base, int64_t ld, int64_t lr0, bool remap) {
