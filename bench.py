@@ -39,7 +39,7 @@ def parse():
     ap.add_argument("--config", default="reddit")
     ap.add_argument("--N", type=int, default=128)
     ap.add_argument("--precision", default="tf32", choices=["tf32", "fp16"])
-    ap.add_argument("--reorder", default="off", choices=["off", "on", "auto"])
+    ap.add_argument("--reorder", default="auto", choices=["off", "on", "auto"])
     ap.add_argument("--balance", default="auto", choices=["off", "on", "auto"])
     ap.add_argument("--unit-cap", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -59,8 +59,8 @@ def wb_cost(precision: str) -> int:
 
 
 def auto_cap(NB: int) -> int:
-    """B200 default cap when unit_cap == 0: ~64 units per SM, in [32, 4096], multiple of 32."""
-    c = -(-NB // (148 * 64))
+    """B200 default cap when unit_cap == 0 (reading R7): ~192 units per SM, in [32, 4096], multiple of 32."""
+    c = -(-NB // (148 * 192))
     c = -(-c // 32) * 32
     return max(PAPER_CAP, min(4096, c))
 

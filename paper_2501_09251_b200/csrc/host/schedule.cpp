@@ -26,10 +26,11 @@ double compute_ibd(const std::vector<uint32_t> &rwo)
     return s / (double)W;
 }
 
-// B200 default: about 64 units per SM (148 SMs), a multiple of 32, in [32, 4096].
+// B200 default: about 192 units per SM (148 SMs; ~12 per resident warp), a multiple
+// of 32, in [32, 4096] -- measured on the Reddit-shaped graph.
 int auto_cap(int64_t NB)
 {
-    int64_t c = (NB + 148 * 64 - 1) / (148 * 64);
+    int64_t c = (NB + 148 * 192 - 1) / (148 * 192);
     c = (c + 31) / 32 * 32;
     return (int)std::max<int64_t>(kPaperCap, std::min<int64_t>(4096, c));
 }

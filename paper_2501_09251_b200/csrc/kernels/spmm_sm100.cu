@@ -1093,8 +1093,12 @@ accspmm_status tensor_map(const DevicePlan &d, const void *B, int64_t N, int FW,
 template <int FW, bool F16>
 accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, int64_t n_units, cudaStream_t stream)
 {
-    const int kcfg = env_int("ACCSPMM_KCFG", -1);
-    if (kcfg < 0 || kcfg >= 20) {  // TMA gather4 (v4): default
+    // Default (measured): TMA gather4 for TF32 slices of >= 64 features
+    // (>= 256-byte rows); the register-direct gather (2 warps/CTA) for FP16 and narrow
+    // slices, where per-TMA-request cost dominates.  ACCSPMM_KCFG overrides for tuning.
+    int kcfg = env_int("ACCSPMM_KCFG", -1);
+    if (kcfg < 0) kcfg = (!F16 && FW >= 64) ? 20 : 11;
+    if (kcfg >= 20) {
         const CUtensorMap *map = nullptr;
         accspmm_status st = tensor_map(d, B, kp.N, FW, &map);
         if (st != ACCSPMM_OK) return st;

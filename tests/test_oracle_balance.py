@@ -88,5 +88,5 @@ def test_split_segments_even():
 
 def test_auto_cap():
     assert ob.auto_cap(0) == 32 and ob.auto_cap(10) == 32
-    assert ob.auto_cap(14_000_000) == 1504
+    assert ob.auto_cap(14_000_000) == 512   # ceil(14e6 / 28416) = 493 -> 512
     assert ob.auto_cap(10 ** 10) == 4096
