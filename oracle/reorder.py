@@ -16,6 +16,9 @@ Readings:
     nbrs with v" is the next L unvisited vertices in DFS order, neighbour lists
     capped at their first H entries (ascending id); ties by DFS order (P:241);
     no candidate with >= 1 common neighbour -> continue with the next DFS vertex.
+  * R6b: after a visit (whose merge decision uses all of its edges), a community
+    carries on only its EDGE_CAP heaviest community edges (ties: smaller id) --
+    a bound on the coarsening work; graphs whose lists stay short are unaffected;
   * non-square A -> identity (Q14).
 """
 from __future__ import annotations
@@ -24,6 +27,7 @@ import numpy as np
 
 CAND_WINDOW = 64   # L
 HUB_CAP = 128      # H
+EDGE_CAP = 256     # community edges carried up a merge (reading R6b)
 
 
 def affinity_graph(n: int, rowptr, colidx):
@@ -88,12 +92,15 @@ def dendrogram(adj):
             r = find(x)
             if r != v:
                 acc[r] = acc.get(r, 0) + w
-        edges[v] = acc
         best, best_dq = -1, 0.0
         for r in sorted(acc):                                # l.4 argmax dQ, smallest id on ties
             dq = delta_q(acc[r], a[r], a[v], m2)
             if best < 0 or dq > best_dq:
                 best, best_dq = r, dq
+        if len(acc) > EDGE_CAP:                              # R6b
+            keep = sorted(acc.items(), key=lambda kv: (-kv[1], kv[0]))[:EDGE_CAP]
+            acc = dict(keep)
+        edges[v] = acc
         if best >= 0 and best_dq > 0.0:                      # l.5-7 merge v into u
             u = best
             parent[v] = u

@@ -329,7 +329,10 @@ class Plan:
 
     @property
     def launches_per_execute(self) -> int:
-        return 2 if self.precision == "tf32" else 1
+        """SpMM kernel + (TF32, high B-row reuse) the rho(B) pre-pass -- mirrors accspmm_execute."""
+        i = self.info
+        pre = self.precision == "tf32" and i["K"] > 0 and i["sum_U"] >= 32 * i["K"]
+        return 2 if pre else 1
 
     def debug_decode(self, stream=None):
         import torch

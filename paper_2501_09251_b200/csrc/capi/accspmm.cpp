@@ -296,7 +296,11 @@ accspmm_status accspmm_execute(const accspmm_plan *p, const void *B, int64_t N, 
     accspmm_status st = ensure_workspace(p, N);
     if (st != ACCSPMM_OK) return st;
     const void *Bk = B;
-    if (p->opt.precision == ACCSPMM_TF32 && p->info.K > 0) {
+    // rho(B) for TF32: one elementwise pass when each B row is gathered many times
+    // (reuse = sum_w |U_w| / K >= 32), else in the kernel's registers.
+    const bool tf32 = p->opt.precision == ACCSPMM_TF32;
+    const bool in_kernel_round = tf32 && p->info.K > 0 && p->info.sum_U < 32 * p->info.K;
+    if (tf32 && !in_kernel_round && p->info.K > 0) {
         const size_t need = (size_t)p->info.K * (size_t)N * sizeof(float);
         if (need > p->Br_bytes) {
             cudaFree(p->Br);
@@ -311,7 +315,7 @@ accspmm_status accspmm_execute(const accspmm_plan *p, const void *B, int64_t N, 
     }
     const bool timed = p->timing && p->ev_n + 2 <= p->ev.size();
     if (timed) cudaEventRecord(p->ev[p->ev_n], (cudaStream_t)stream);
-    st = launch_spmm(p->dev, Bk, p->zrow, N, (float *)C, p->ws, p->counters, stream);
+    st = launch_spmm(p->dev, Bk, p->zrow, N, (float *)C, p->ws, p->counters, stream, in_kernel_round);
     if (timed) {
         cudaEventRecord(p->ev[p->ev_n + 1], (cudaStream_t)stream);
         p->ev_n += 2;

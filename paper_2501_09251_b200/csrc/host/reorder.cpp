@@ -12,6 +12,8 @@
 // vertex with the most common neighbours among the next L = 64 unvisited
 // vertices in DFS order (neighbour lists capped at H = 128 entries), ties by DFS
 // order; with no common neighbour it resumes the DFS sequence (Q13).
+// Reading R6b: after a visit, a community passes on at most its 256
+// heaviest neighbour-community edges, so chains of merges on meshes stay O(m).
 #include <algorithm>
 #include <numeric>
 
@@ -22,6 +24,7 @@ namespace accspmm {
 namespace {
 constexpr int kCandWindow = 64;  // L
 constexpr int kHubCap = 128;     // H
+constexpr size_t kEdgeCap = 256;  // community edges carried up a merge (reading R6b)
 
 struct Graph {
     std::vector<int64_t> ptr;
@@ -124,6 +127,16 @@ std::vector<uint32_t> reorder_alg1(const Csr &a)
         }
         E[v].clear();
         E[v].shrink_to_fit();
+        // R6b: only the kEdgeCap heaviest community edges (ties: smaller id) are carried on,
+        // which bounds the coarsening work on meshes; the merge decision above is exact.
+        if (comp.size() > kEdgeCap) {
+            std::partial_sort(comp.begin(), comp.begin() + kEdgeCap, comp.end(),
+                              [](const std::pair<uint32_t, uint32_t> &x, const std::pair<uint32_t, uint32_t> &y) {
+                                  return x.second != y.second ? x.second > y.second : x.first < y.first;
+                              });
+            comp.resize(kEdgeCap);
+            std::sort(comp.begin(), comp.end());
+        }
         if (best != UINT32_MAX && best_dq > 0.0) {
             const uint32_t u = best;
             parent[v] = u;

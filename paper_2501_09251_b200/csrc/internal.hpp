@@ -82,8 +82,9 @@ struct DevicePlan {
     alignas(64) mutable unsigned char tmap[128] = {};
 };
 
+// round_b: the kernel applies rho(B) in registers (B not pre-rounded)
 accspmm_status launch_spmm(const DevicePlan &p, const void *B, const void *zrow, int64_t N, float *C, float *ws,
-                           uint32_t *counters, void *stream);
+                           uint32_t *counters, void *stream, bool round_b);
 accspmm_status launch_round_b(const float *B, float *Br, int64_t n, void *stream);
 accspmm_status launch_unpermute(const float *G, const uint32_t *orig_row, int64_t n_rows, int64_t N,
                                 float *C, void *stream);

@@ -228,9 +228,37 @@ __device__ __forceinline__ void mma_block(float (&acc)[Cfg<FW, F16>::MT][4], con
     }
 }
 
+__device__ __forceinline__ uint32_t tf32_rna_bits(uint32_t x)
+{
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(__uint_as_float(x)));
+    return r;
+}
+
+// rho(B) applied to a loaded fragment (TF32 only; FP16 operands arrive already rounded)
+template <int FW, bool F16>
+__device__ __forceinline__ void round_frag(Frag<FW, F16> &fr)
+{
+    using CF = Cfg<FW, F16>;
+    if constexpr (!F16) {
+#pragma unroll
+        for (int j = 0; j < CF::NV; ++j) {
+            if constexpr (CF::VW == 4) {
+                fr.x[j] = make_uint4(tf32_rna_bits(fr.x[j].x), tf32_rna_bits(fr.x[j].y), tf32_rna_bits(fr.x[j].z),
+                                     tf32_rna_bits(fr.x[j].w));
+                fr.y[j] = make_uint4(tf32_rna_bits(fr.y[j].x), tf32_rna_bits(fr.y[j].y), tf32_rna_bits(fr.y[j].z),
+                                     tf32_rna_bits(fr.y[j].w));
+            } else {
+                fr.x[j] = make_uint2(tf32_rna_bits(fr.x[j].x), tf32_rna_bits(fr.x[j].y));
+                fr.y[j] = make_uint2(tf32_rna_bits(fr.y[j].x), tf32_rna_bits(fr.y[j].y));
+            }
+        }
+    }
+}
+
 // ------------------------------------------------------------------ the kernel
 
-template <int FW, bool F16, int WARPS>
+template <int FW, bool F16, int WARPS, bool RND>
 __global__ void __launch_bounds__(WARPS * 32) spmm_bittcf_kernel(const KParams p)
 {
     using CF = Cfg<FW, F16>;
@@ -370,10 +398,12 @@ __global__ void __launch_bounds__(WARPS * 32) spmm_bittcf_kernel(const KParams p
     if (nblk > 0) load_block(fa, 0);
     if (nblk > 1) load_block(fb, 1);
     for (uint32_t i = 0; i < nblk; i += 2) {
+        if constexpr (RND) round_frag<FW, F16>(fa);
         mma_block<FW, F16>(acc, fa);
         after_block(b0 + i + 1);
         if (i + 2 < nblk) load_block(fa, i + 2);
         if (i + 1 < nblk) {
+            if constexpr (RND) round_frag<FW, F16>(fb);
             mma_block<FW, F16>(acc, fb);
             after_block(b0 + i + 2);
             if (i + 3 < nblk) load_block(fb, i + 3);
@@ -732,7 +762,7 @@ __device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap *map
         : "memory");
 }
 
-template <int FW, bool F16, int WARPS, int STAGES>
+template <int FW, bool F16, int WARPS, int STAGES, bool RND>
 __global__ void __launch_bounds__(WARPS * 32)
     spmm_bittcf_g4_kernel(const KParams p, const __grid_constant__ CUtensorMap tmap)
 {
@@ -865,8 +895,12 @@ __global__ void __launch_bounds__(WARPS * 32)
             // LDS.128 of one row feeds the A operands of two m16 tiles directly
 #pragma unroll
             for (int j = 0; j < NV; ++j) {
-                const uint4 x = *reinterpret_cast<const uint4 *>(ra + 8 * CF::VB * j);
-                const uint4 y = *reinterpret_cast<const uint4 *>(rb + 8 * CF::VB * j);
+                uint4 x = *reinterpret_cast<const uint4 *>(ra + 8 * CF::VB * j);
+                uint4 y = *reinterpret_cast<const uint4 *>(rb + 8 * CF::VB * j);
+                if constexpr (RND) {  // rho(B) in registers (low-reuse plans skip the pre-round pass)
+                    x = make_uint4(tf32_rna_bits(x.x), tf32_rna_bits(x.y), tf32_rna_bits(x.z), tf32_rna_bits(x.w));
+                    y = make_uint4(tf32_rna_bits(y.x), tf32_rna_bits(y.y), tf32_rna_bits(y.z), tf32_rna_bits(y.w));
+                }
                 mma_tf32_k4(acc[2 * j], x.x, x.y, vb0[s]);
                 mma_tf32_k4(acc[2 * j + 1], x.z, x.w, vb0[s]);
                 mma_tf32_k4(acc[2 * j], y.x, y.y, vb1[s]);
@@ -879,6 +913,7 @@ __global__ void __launch_bounds__(WARPS * 32)
                 fr.x[j] = *reinterpret_cast<const V *>(ra + 8 * CF::VB * j);
                 fr.y[j] = *reinterpret_cast<const V *>(rb + 8 * CF::VB * j);
             }
+            if constexpr (RND) round_frag<FW, F16>(fr);
             fr.b0 = vb0[s];
             fr.b1 = vb1[s];
             mma_block<FW, F16>(acc, fr);
@@ -993,10 +1028,10 @@ __global__ void round_b_tf32_kernel(const float4 *__restrict__ in, float4 *__res
 
 // ------------------------------------------------------------------ launch
 
-template <int FW, bool F16, int WARPS>
+template <int FW, bool F16, int WARPS, bool RND = false>
 accspmm_status launch_cfg(const KParams &kp, int64_t n_units, cudaStream_t stream)
 {
-    auto kern = spmm_bittcf_kernel<FW, F16, WARPS>;
+    auto kern = spmm_bittcf_kernel<FW, F16, WARPS, RND>;
     const int64_t groups = (n_units + WARPS - 1) / WARPS;
     const int64_t grid = groups * kp.nslices;
     if (grid > 0x7FFFFFFFll) return fail(ACCSPMM_ERR_UNSUPPORTED, "grid too large");
@@ -1035,12 +1070,12 @@ accspmm_status launch_tma(const KParams &kp, int64_t n_units, cudaStream_t strea
     return ACCSPMM_OK;
 }
 
-template <int FW, bool F16, int WARPS, int STAGES>
+template <int FW, bool F16, int WARPS, int STAGES, bool RND = false>
 accspmm_status launch_g4(const KParams &kp, const CUtensorMap *map, int64_t n_units, cudaStream_t stream)
 {
     using SM = G4WarpSmem<FW, F16, STAGES>;
     const size_t smem = sizeof(SM) * WARPS;
-    auto kern = spmm_bittcf_g4_kernel<FW, F16, WARPS, STAGES>;
+    auto kern = spmm_bittcf_g4_kernel<FW, F16, WARPS, STAGES, RND>;
     static int configured_device = -1;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -1091,13 +1126,25 @@ accspmm_status tensor_map(const DevicePlan &d, const void *B, int64_t N, int FW,
 }
 
 template <int FW, bool F16>
-accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, int64_t n_units, cudaStream_t stream)
+accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, int64_t n_units, cudaStream_t stream,
+                         bool rnd)
 {
     // Default (measured): TMA gather4 for TF32 slices of >= 64 features
     // (>= 256-byte rows); the register-direct gather (2 warps/CTA) for FP16 and narrow
     // slices, where per-TMA-request cost dominates.  ACCSPMM_KCFG overrides for tuning.
     int kcfg = env_int("ACCSPMM_KCFG", -1);
     if (kcfg < 0) kcfg = (!F16 && FW >= 64) ? 20 : 11;
+    if constexpr (!F16) {
+        if (rnd) {  // B not pre-rounded: rho(B) applied in registers (default configurations only)
+            if (kcfg >= 20) {
+                const CUtensorMap *map = nullptr;
+                accspmm_status st = tensor_map(d, B, kp.N, FW, &map);
+                if (st != ACCSPMM_OK) return st;
+                return launch_g4<FW, F16, 2, 2, true>(kp, map, n_units, stream);
+            }
+            return launch_cfg<FW, F16, 2, true>(kp, n_units, stream);
+        }
+    }
     if (kcfg >= 20) {
         const CUtensorMap *map = nullptr;
         accspmm_status st = tensor_map(d, B, kp.N, FW, &map);
@@ -1138,7 +1185,7 @@ accspmm_status launch_round_b(const float *B, float *Br, int64_t n, void *stream
 }
 
 accspmm_status launch_spmm(const DevicePlan &d, const void *B, const void *zrow, int64_t N, float *C, float *ws,
-                           uint32_t *counters, void *stream)
+                           uint32_t *counters, void *stream, bool round_b)
 {
     if (d.rows == 0) return ACCSPMM_OK;
     const int FW = N % 128 == 0 ? 128 : N % 64 == 0 ? 64 : N % 32 == 0 ? 32 : 16;
@@ -1162,11 +1209,12 @@ accspmm_status launch_spmm(const DevicePlan &d, const void *B, const void *zrow,
     kp.Krows = (int32_t)d.K;
     cudaStream_t s = (cudaStream_t)stream;
     const bool f16 = d.precision == ACCSPMM_FP16;
+    const bool r = round_b;
     switch (FW) {
-    case 128: return f16 ? launch_fw<128, true>(kp, d, B, d.n_units, s) : launch_fw<128, false>(kp, d, B, d.n_units, s);
-    case 64: return f16 ? launch_fw<64, true>(kp, d, B, d.n_units, s) : launch_fw<64, false>(kp, d, B, d.n_units, s);
-    case 32: return f16 ? launch_fw<32, true>(kp, d, B, d.n_units, s) : launch_fw<32, false>(kp, d, B, d.n_units, s);
-    default: return f16 ? launch_fw<16, true>(kp, d, B, d.n_units, s) : launch_fw<16, false>(kp, d, B, d.n_units, s);
+    case 128: return f16 ? launch_fw<128, true>(kp, d, B, d.n_units, s, r) : launch_fw<128, false>(kp, d, B, d.n_units, s, r);
+    case 64: return f16 ? launch_fw<64, true>(kp, d, B, d.n_units, s, r) : launch_fw<64, false>(kp, d, B, d.n_units, s, r);
+    case 32: return f16 ? launch_fw<32, true>(kp, d, B, d.n_units, s, r) : launch_fw<32, false>(kp, d, B, d.n_units, s, r);
+    default: return f16 ? launch_fw<16, true>(kp, d, B, d.n_units, s, r) : launch_fw<16, false>(kp, d, B, d.n_units, s, r);
     }
 }
 

@@ -70,6 +70,19 @@ def test_permutation_matrix_exact(precision):
 
 
 @pytest.mark.parametrize("precision", PRECISIONS)
+def test_rho_b_bit_exact_both_rounding_paths(precision):
+    """C = A.rho(B) with one unit nnz per row is rho(B) itself: pins the B rounding on the
+    in-kernel path (low B-row reuse) and on the pre-round pass (high reuse) bit-exactly."""
+    low = gen.permutation_matrix(2048, seed=5)                        # reuse 1
+    high = gen.csr_from_pairs(np.arange(4096), np.arange(4096) % 8, 4096, 8)   # reuse 512
+    for A in (low, high):
+        v = np.ones(A.nnz, np.float32)
+        B = gen.dense_normal(A.K, 128, 9)
+        C, p = run(A, v, B, precision)
+        assert_bit_exact(C, A, v, B, precision)
+
+
+@pytest.mark.parametrize("precision", PRECISIONS)
 def test_padding_lanes_do_not_leak_inf(precision):
     # windows with 1..7 unique columns (partial last block), column 0 unused, B[0,:] = +Inf
     rows, cols = [], []
