@@ -450,17 +450,7 @@ __global__ void __launch_bounds__(WARPS * 32) spmm_bittcf_kernel(const KParams p
 }
 
 
-// ================================================================== v3: TMA-staged B rows
-//
-// The register-direct gather of v2 is bound by the LSU data pipe of L1TEX (one
-// 32-byte sector per wavefront for uncached global loads; ncu: 93% of
-// l1tex__data_pipe_lsu_wavefronts at 33% L2 throughput).  v3 moves the gather off
-// the LSU: per TC block, 8 lanes each issue one TMA bulk copy
-// (cp.async.bulk ... mbarrier::complete_tx) of one B row slice into a per-warp
-// STAGES-deep shared-memory ring, plus one bulk copy of the block's values;
-// padding lanes copy a zero row.  Fragments are then read with conflict-free
-// LDS (row stride padded so the 8 lanes of a phase hit 8 bank groups), which
-// return 128 bytes per wavefront instead of 32.
+// ================================================================== mbarrier / TMA helpers
 
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count)
 {
@@ -488,240 +478,6 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t
         ::"r"(dst), "l"(src), "r"(bytes), "r"(bar), "l"(pol) : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
-
-template <int FW, bool F16>
-struct TmaCfg {
-    using CF = Cfg<FW, F16>;
-    static constexpr int ROW = FW * CF::ES;                 // bytes copied per gathered row
-    static constexpr int RS = ROW + (F16 ? 16 : 32);        // padded smem row stride (bank-conflict free)
-    static constexpr int VALB = F16 ? 144 : 272;            // values window (16-byte aligned superset)
-    static constexpr int STAGE = 8 * RS + VALB;
-};
-
-template <int FW, bool F16, int STAGES>
-struct TmaWarpSmem {
-    ChunkSmem ch[2];
-    alignas(16) uint8_t stage[STAGES][TmaCfg<FW, F16>::STAGE];
-    uint64_t bar[STAGES];
-};
-
-template <int FW, bool F16, int WARPS, int STAGES>
-__global__ void __launch_bounds__(WARPS * 32) spmm_bittcf_tma_kernel(const KParams p)
-{
-    using CF = Cfg<FW, F16>;
-    using TC = TmaCfg<FW, F16>;
-    using SM = TmaWarpSmem<FW, F16, STAGES>;
-    using V = typename CF::V;
-    constexpr int MT = CF::MT, NV = CF::NV, VW = CF::VW;
-    extern __shared__ __align__(128) uint8_t smem_raw[];
-
-    const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
-    const int slice = (int)(blockIdx.x % (unsigned)p.nslices);
-    const int64_t u = (int64_t)(blockIdx.x / (unsigned)p.nslices) * WARPS + warp;
-    if (u >= p.n_units) return;  // warp-uniform; only warp-scoped synchronisation below
-    SM &sm = reinterpret_cast<SM *>(smem_raw)[warp];
-    const uint64_t pol_keep = policy_evict_last();
-    const uint64_t pol_stream = policy_evict_first();
-    if (lane == 0) {
-#pragma unroll
-        for (int s = 0; s < STAGES; ++s) mbar_init(smem_u32(&sm.bar[s]), 1);
-        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    }
-    __syncwarp();
-
-    const uint4 ua = __ldg(p.units + 2 * u);
-    const uint4 ub = __ldg(p.units + 2 * u + 1);
-    const uint32_t w0 = ua.x, nw = ua.y, b0 = ua.z, b1 = ua.w;
-    const bool split = ub.x != kNoSplit;
-    const int64_t f0 = (int64_t)slice * FW;
-    const uint32_t my_rwo = (uint32_t)lane <= nw ? __ldg(p.rwo + w0 + lane) : 0u;
-    const uint32_t nblk = b1 - b0;
-    const int g = lane >> 2, t = lane & 3;
-    const int rA = F16 ? 2 * t : t, rB = F16 ? 2 * t + 1 : t + 4;
-    const char *Bslice = reinterpret_cast<const char *>(p.B) + f0 * CF::ES;
-    const int64_t row_stride = p.N * CF::ES;
-
-    auto issue_chunk = [&](uint32_t i) {
-        if (i < nblk) {
-            ChunkSmem &c = sm.ch[(i >> 5) & 1];
-            const uint32_t b = b0 + i;
-            const uint32_t cnt = min((uint32_t)kChunk, nblk - i);
-            if ((uint32_t)lane < cnt) {
-                cp_async8(smem_u32(&c.mask[lane]), p.bits + b + lane, pol_stream);
-                cp_async4(smem_u32(&c.tco[lane]), p.tco + b + lane, pol_stream);
-            }
-            const uint4 *src4 = reinterpret_cast<const uint4 *>(p.a2b + (size_t)b * 8);
-            if ((uint32_t)lane < 2 * cnt) cp_async16(smem_u32(&c.a2b[4 * lane]), src4 + lane, pol_stream);
-            if ((uint32_t)lane + 32 < 2 * cnt) cp_async16(smem_u32(&c.a2b[4 * (lane + 32)]), src4 + lane + 32, pol_stream);
-        }
-        cp_async_commit();
-    };
-
-    // ---- producer: TMA the 8 row slices + the value window of block i into stage i % STAGES
-    auto issue = [&](uint32_t i) {
-        if (i >= nblk) return;
-        if ((i & 31u) == 0) {
-            cp_async_wait_all();
-            __syncwarp();
-            issue_chunk(i + kChunk);
-        }
-        const ChunkSmem &c = sm.ch[(i >> 5) & 1];
-        const uint32_t cs = i & 31u;
-        const uint64_t mask = c.mask[cs];
-        const uint32_t t0 = c.tco[cs];
-        const int cnt = __popcll(mask);
-        constexpr uint32_t VA = F16 ? 8u : 4u;             // elements per 16 bytes
-        const uint32_t vs = t0 & ~(VA - 1u);
-        const uint32_t vbytes = ((t0 + (uint32_t)cnt - vs + VA - 1u) & ~(VA - 1u)) * CF::ES;
-        const int s = (int)(i % STAGES);
-        const uint32_t bar = smem_u32(&sm.bar[s]);
-        uint8_t *st = sm.stage[s];
-        fence_proxy_async();  // order this warp's earlier generic reads of the stage before the async writes
-        if (lane == 0) mbar_arrive_expect_tx(bar, 8u * TC::ROW + vbytes);
-        if (lane < 8) {
-            uint64_t cm = mask | (mask >> 32);
-            cm |= cm >> 16;
-            cm |= cm >> 8;
-            const bool v = (cm >> lane) & 1u;
-            const char *src = v ? Bslice + (int64_t)c.a2b[cs * 8 + lane] * row_stride
-                                : reinterpret_cast<const char *>(p.zrow);
-            bulk_g2s(smem_u32(st + lane * TC::RS), src, TC::ROW, bar, pol_keep);
-        } else if (lane == 8) {
-            bulk_g2s(smem_u32(st + 8 * TC::RS), reinterpret_cast<const char *>(p.vals) + (int64_t)vs * CF::ES, vbytes,
-                     bar, pol_stream);
-        }
-        if (lane == 0) {
-            // stash mask and the value offset inside the block's value window in the stage's pad bytes
-            *reinterpret_cast<uint64_t *>(st + TC::ROW) = mask;
-            *reinterpret_cast<uint32_t *>(st + TC::ROW + 8) = t0 - vs;
-        }
-    };
-
-    float acc[MT][4];
-#pragma unroll
-    for (int m = 0; m < MT; ++m) acc[m][0] = acc[m][1] = acc[m][2] = acc[m][3] = 0.f;
-
-    // ---- consumer: wait for the stage, decode the 8x8 tile, tensor-core MMA
-    auto consume = [&](uint32_t i) {
-        const int s = (int)(i % STAGES);
-        mbar_wait(smem_u32(&sm.bar[s]), (i / STAGES) & 1u);
-        const uint8_t *st = sm.stage[s];
-        const uint64_t mask = *reinterpret_cast<const uint64_t *>(st + TC::ROW);
-        const uint32_t voff = *reinterpret_cast<const uint32_t *>(st + TC::ROW + 8);
-        Frag<FW, F16> fr;
-        const uint8_t *ra = st + rA * TC::RS + CF::VB * g;
-        const uint8_t *rb = st + rB * TC::RS + CF::VB * g;
-#pragma unroll
-        for (int j = 0; j < NV; ++j) {
-            fr.x[j] = *reinterpret_cast<const V *>(ra + 8 * CF::VB * j);
-            fr.y[j] = *reinterpret_cast<const V *>(rb + 8 * CF::VB * j);
-        }
-        const uint64_t one = 1ull;
-        if constexpr (!F16) {
-            const float *sv = reinterpret_cast<const float *>(st + 8 * TC::RS) + voff;
-            const int k0 = g * 8 + t, k1 = k0 + 4;
-            fr.b0 = ((mask >> k0) & one) ? __float_as_uint(sv[__popcll(mask & ((one << k0) - one))]) : 0u;
-            fr.b1 = ((mask >> k1) & one) ? __float_as_uint(sv[__popcll(mask & ((one << k1) - one))]) : 0u;
-        } else {
-            const unsigned short *sv = reinterpret_cast<const unsigned short *>(st + 8 * TC::RS) + voff;
-            const int k0 = g * 8 + 2 * t;
-            const uint32_t lo = ((mask >> k0) & one) ? (uint32_t)sv[__popcll(mask & ((one << k0) - one))] : 0u;
-            const uint32_t hi =
-                ((mask >> (k0 + 1)) & one) ? (uint32_t)sv[__popcll(mask & ((one << (k0 + 1)) - one))] : 0u;
-            fr.b0 = lo | (hi << 16);
-            fr.b1 = 0u;
-        }
-        __syncwarp();  // every lane has read the stage before it is refilled
-        mma_block<FW, F16>(acc, fr);
-    };
-
-    auto store_rows = [&](float *base, int64_t ld, int64_t lr0, bool remap) {
-#pragma unroll
-        for (int s2 = 0; s2 < 2; ++s2) {
-            const int64_t lr = lr0 + 2 * t + s2;
-            if (!remap || lr < p.rows) {
-                const int64_t orow = remap ? (p.row_map ? (int64_t)__ldg(p.row_map + lr) : lr) : (2 * t + s2);
-                float *dst = base + orow * ld + VW * g;
-#pragma unroll
-                for (int j = 0; j < NV; ++j) {
-                    float *d = dst + 8 * VW * j;
-                    if constexpr (VW == 2) {
-                        st_cs(d, acc[j][s2], acc[j][2 + s2]);
-                    } else {
-#pragma unroll
-                        for (int q = 0; q < VW / 4; ++q) {
-                            const int m0 = (VW / 2) * j + 2 * q;
-                            st_cs(d + 4 * q, acc[m0][s2], acc[m0][2 + s2], acc[m0 + 1][s2], acc[m0 + 1][2 + s2]);
-                        }
-                    }
-                }
-            }
-        }
-    };
-    auto store_window = [&](uint32_t wi) {
-        store_rows(p.C + f0, p.N, (int64_t)(w0 + wi) * 8, true);
-#pragma unroll
-        for (int m = 0; m < MT; ++m) acc[m][0] = acc[m][1] = acc[m][2] = acc[m][3] = 0.f;
-    };
-    uint32_t wi = 0;
-    uint32_t wend = split ? b1 : __shfl_sync(0xffffffffu, my_rwo, 1);
-    auto after_block = [&](uint32_t jnext) {
-        while (!split && wi < nw && wend == jnext) {
-            store_window(wi);
-            ++wi;
-            wend = __shfl_sync(0xffffffffu, my_rwo, (int)(wi < nw ? wi + 1 : nw));
-        }
-    };
-
-    issue_chunk(0);
-    after_block(b0);
-#pragma unroll
-    for (int i = 0; i < STAGES - 1; ++i) issue((uint32_t)i);
-    for (uint32_t i = 0; i < nblk; ++i) {
-        issue(i + STAGES - 1);
-        consume(i);
-        after_block(b0 + i + 1);
-    }
-    cp_async_wait_all();
-
-    if (split) {
-        const uint32_t sid = ub.x, seg = ub.y, nseg = ub.z, slot = ub.w;
-        float *tile = p.ws + ((int64_t)slot * p.nslices + slice) * (8 * FW);
-        store_rows(tile, FW, 0, false);
-        __threadfence();
-        __syncwarp();
-        uint32_t prev = 0;
-        if (lane == 0) prev = atomicAdd(p.counters + (int64_t)sid * p.nslices + slice, 1u);
-        prev = __shfl_sync(0xffffffffu, prev, 0);
-        if (prev == nseg - 1) {
-            __threadfence();
-            const float *first = p.ws + ((int64_t)(slot - seg) * p.nslices + slice) * (8 * FW);
-#pragma unroll
-            for (int m = 0; m < MT; ++m) acc[m][0] = acc[m][1] = acc[m][2] = acc[m][3] = 0.f;
-            for (uint32_t k = 0; k < nseg; ++k) {
-                const float *src = first + (int64_t)k * p.nslices * (8 * FW);
-#pragma unroll
-                for (int s2 = 0; s2 < 2; ++s2) {
-                    const float *row = src + (2 * t + s2) * FW + VW * g;
-#pragma unroll
-                    for (int j = 0; j < NV; ++j) {
-#pragma unroll
-                        for (int e = 0; e < VW; e += 2) {
-                            const int m = (VW / 2) * j + (e >> 1);
-                            const float2 v = __ldcg(reinterpret_cast<const float2 *>(row + 8 * VW * j + e));
-                            acc[m][s2] += v.x;
-                            acc[m][2 + s2] += v.y;
-                        }
-                    }
-                }
-            }
-            store_window(0);
-            if (lane == 0) p.counters[(int64_t)sid * p.nslices + slice] = 0u;
-        }
-    }
-}
-
 
 // ================================================================== v4: TMA gather4
 //
@@ -1047,29 +803,6 @@ int env_int(const char *name, int dflt)
     return s ? std::atoi(s) : dflt;
 }
 
-template <int FW, bool F16, int WARPS, int STAGES>
-accspmm_status launch_tma(const KParams &kp, int64_t n_units, cudaStream_t stream)
-{
-    using SM = TmaWarpSmem<FW, F16, STAGES>;
-    const size_t smem = sizeof(SM) * WARPS;
-    auto kern = spmm_bittcf_tma_kernel<FW, F16, WARPS, STAGES>;
-    static int configured_device = -1;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (configured_device != dev) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return fail(ACCSPMM_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
-        configured_device = dev;
-    }
-    const int64_t groups = (n_units + WARPS - 1) / WARPS;
-    const int64_t grid = groups * kp.nslices;
-    if (grid > 0x7FFFFFFFll) return fail(ACCSPMM_ERR_UNSUPPORTED, "grid too large");
-    kern<<<(unsigned)grid, WARPS * 32, smem, stream>>>(kp);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return fail(ACCSPMM_ERR_CUDA, std::string("spmm launch: ") + cudaGetErrorString(e));
-    return ACCSPMM_OK;
-}
-
 template <int FW, bool F16, int WARPS, int STAGES, bool RND = false>
 accspmm_status launch_g4(const KParams &kp, const CUtensorMap *map, int64_t n_units, cudaStream_t stream)
 {
@@ -1157,15 +890,11 @@ accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, 
         default: return launch_g4<FW, F16, 2, 2>(kp, map, n_units, stream);
         }
     }
-    // ACCSPMM_KCFG selects a kernel variant for tuning: 0-2 TMA-staged (v3), 10-12 register-direct (v2)
-    switch (env_int("ACCSPMM_KCFG", 0)) {
-    case 1: return launch_tma<FW, F16, 2, 2>(kp, n_units, stream);
-    case 2: return launch_tma<FW, F16, 4, 3>(kp, n_units, stream);
-    case 3: return launch_tma<FW, F16, 2, 3>(kp, n_units, stream);
+    // register-direct flavour (kcfg 10-12: 4, 2 or 8 warps per CTA)
+    switch (kcfg) {
     case 10: return launch_cfg<FW, F16, 4>(kp, n_units, stream);
-    case 11: return launch_cfg<FW, F16, 2>(kp, n_units, stream);
     case 12: return launch_cfg<FW, F16, 8>(kp, n_units, stream);
-    default: return launch_tma<FW, F16, 4, 2>(kp, n_units, stream);
+    default: return launch_cfg<FW, F16, 2>(kp, n_units, stream);
     }
 }
 
