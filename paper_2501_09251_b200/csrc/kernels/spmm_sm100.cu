@@ -228,6 +228,15 @@ __device__ __forceinline__ void mma_block(float (&acc)[Cfg<FW, F16>::MT][4], con
     }
 }
 
+// Decode of one tile position: shifting the mask left by 63-k puts bit k on top;
+// the popcount of the shifted word minus that top bit is popc(mask & (2^k - 1)).
+__device__ __forceinline__ uint32_t tile_rank(uint64_t mask, uint32_t sh, bool &present)
+{
+    const uint64_t x = mask << sh;
+    present = (int64_t)x < 0;
+    return (uint32_t)__popcll(x) - (present ? 1u : 0u);
+}
+
 __device__ __forceinline__ uint32_t tf32_rna_bits(uint32_t x)
 {
     uint32_t r;
@@ -285,6 +294,8 @@ __global__ void __launch_bounds__(WARPS * 32) spmm_bittcf_kernel(const KParams p
 
     const int g = lane >> 2, t = lane & 3;
     const int rA = F16 ? 2 * t : t, rB = F16 ? 2 * t + 1 : t + 4;
+    const uint32_t sh0 = 63u - (uint32_t)(F16 ? g * 8 + 2 * t : g * 8 + t);
+    const uint32_t sh1 = F16 ? sh0 - 1u : sh0 - 4u;
     // byte offset of this lane's vector j inside a gathered row slice
     const char *Bbase = reinterpret_cast<const char *>(p.B) + f0 * CF::ES + (int64_t)(VW * g) * CF::ES;
     const char *Zbase = reinterpret_cast<const char *>(p.zrow) + (int64_t)(VW * g) * CF::ES;
@@ -330,18 +341,17 @@ __global__ void __launch_bounds__(WARPS * 32) spmm_bittcf_kernel(const KParams p
             ldg_nc(fr.y[j], pb + j * 8 * CF::VB, pol_keep);
         }
         // sparse operand: value index = TCOffset + popc(mask & (2^k - 1))
-        const uint64_t one = 1ull;
+        bool p0, p1;
+        const uint32_t i0 = t0 + tile_rank(mask, sh0, p0);
+        const uint32_t i1 = t0 + tile_rank(mask, sh1, p1);
         if constexpr (!F16) {
-            const int k0 = g * 8 + t, k1 = k0 + 4;
-            const float *vp = reinterpret_cast<const float *>(p.vals) + t0;
-            fr.b0 = ((mask >> k0) & one) ? __float_as_uint(__ldg(vp + __popcll(mask & ((one << k0) - one)))) : 0u;
-            fr.b1 = ((mask >> k1) & one) ? __float_as_uint(__ldg(vp + __popcll(mask & ((one << k1) - one)))) : 0u;
+            const float *vp = reinterpret_cast<const float *>(p.vals);
+            fr.b0 = p0 ? __float_as_uint(__ldg(vp + i0)) : 0u;
+            fr.b1 = p1 ? __float_as_uint(__ldg(vp + i1)) : 0u;
         } else {
-            const int k0 = g * 8 + 2 * t;
-            const unsigned short *vp = reinterpret_cast<const unsigned short *>(p.vals) + t0;
-            const uint32_t lo = ((mask >> k0) & one) ? (uint32_t)__ldg(vp + __popcll(mask & ((one << k0) - one))) : 0u;
-            const uint32_t hi =
-                ((mask >> (k0 + 1)) & one) ? (uint32_t)__ldg(vp + __popcll(mask & ((one << (k0 + 1)) - one))) : 0u;
+            const unsigned short *vp = reinterpret_cast<const unsigned short *>(p.vals);
+            const uint32_t lo = p0 ? (uint32_t)__ldg(vp + i0) : 0u;
+            const uint32_t hi = p1 ? (uint32_t)__ldg(vp + i1) : 0u;
             fr.b0 = lo | (hi << 16);
             fr.b1 = 0u;
         }
@@ -553,14 +563,10 @@ __global__ void __launch_bounds__(WARPS * 32)
     const uint32_t my_rwo = (uint32_t)lane <= nw ? __ldg(p.rwo + w0 + lane) : 0u;
     const uint32_t nblk = b1 - b0;
     const int g = lane >> 2, t = lane & 3;
-    // this lane's two positions of the 8x8 tile (the mma B fragment): bit k sits in word k/32;
-    // popc(mask & (2^k - 1)) = popc(lo & below_lo) + popc(hi & below_hi) with lane-constant masks
+    // this lane's two positions of the 8x8 tile (the mma B fragment), as shift amounts 63-k
     const int k0 = F16 ? g * 8 + 2 * t : g * 8 + t;
     const int k1 = F16 ? k0 + 1 : k0 + 4;
-    const uint32_t bit0 = 1u << (k0 & 31), bit1 = 1u << (k1 & 31);
-    const bool hi0 = k0 >= 32, hi1 = k1 >= 32;
-    const uint32_t bl0_lo = hi0 ? 0xFFFFFFFFu : bit0 - 1u, bl0_hi = hi0 ? bit0 - 1u : 0u;
-    const uint32_t bl1_lo = hi1 ? 0xFFFFFFFFu : bit1 - 1u, bl1_hi = hi1 ? bit1 - 1u : 0u;
+    const uint32_t sh0 = 63u - (uint32_t)k0, sh1 = 63u - (uint32_t)k1;
 
     auto issue_chunk = [&](uint32_t i) {
         if (i < nblk) {
@@ -594,10 +600,9 @@ __global__ void __launch_bounds__(WARPS * 32)
         const uint32_t cs = i & 31u;
         const uint64_t mask = c.mask[cs];
         const uint32_t t0 = c.tco[cs];
-        const uint32_t mlo = (uint32_t)mask, mhi = (uint32_t)(mask >> 32);
-        const bool p0 = ((hi0 ? mhi : mlo) & bit0) != 0u, p1 = ((hi1 ? mhi : mlo) & bit1) != 0u;
-        const uint32_t i0 = t0 + __popc(mlo & bl0_lo) + __popc(mhi & bl0_hi);
-        const uint32_t i1 = t0 + __popc(mlo & bl1_lo) + __popc(mhi & bl1_hi);
+        bool p0, p1;
+        const uint32_t i0 = t0 + tile_rank(mask, sh0, p0);
+        const uint32_t i1 = t0 + tile_rank(mask, sh1, p1);
         if constexpr (!F16) {
             const float *vp = reinterpret_cast<const float *>(p.vals);
             vb0[s] = p0 ? __float_as_uint(__ldg(vp + i0)) : 0u;
