@@ -481,13 +481,6 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase)
         "DONE_%=:\n\t}\n" ::"r"(bar), "r"(phase), "r"(0x989680)
         : "memory");
 }
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar, uint64_t pol)
-{
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n"
-        ::"r"(dst), "l"(src), "r"(bytes), "r"(bar), "l"(pol) : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 
 // ================================================================== v4: TMA gather4
 //
@@ -867,11 +860,11 @@ template <int FW, bool F16>
 accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, int64_t n_units, cudaStream_t stream,
                          bool rnd)
 {
-    // Default (measured): TMA gather4 for TF32 slices of >= 64 features
-    // (>= 256-byte rows); the register-direct gather (2 warps/CTA) for FP16 and narrow
+    // Default (measured): TMA gather4 for slices of >= 256-byte rows (TF32
+    // FW >= 64, FP16 FW = 128); the register-direct gather (2 warps/CTA) for narrower
     // slices, where per-TMA-request cost dominates.  ACCSPMM_KCFG overrides for tuning.
     int kcfg = env_int("ACCSPMM_KCFG", -1);
-    if (kcfg < 0) kcfg = (!F16 && FW >= 64) ? 20 : 11;
+    if (kcfg < 0) kcfg = ((!F16 && FW >= 64) || (F16 && FW == 128)) ? 20 : 11;
     if constexpr (!F16) {
         if (rnd) {  // B not pre-rounded: rho(B) applied in registers (default configurations only)
             if (kcfg >= 20) {
