@@ -12,6 +12,7 @@ from .matrices import (  # noqa: F401
     stencil27,
     banded_random,
     dcsbm,
+    powerlaw_directed,
     sbm,
     identity,
     permutation_matrix,

@@ -132,3 +132,92 @@ int64_t gen_pairs_to_csr(int64_t npairs, const int64_t *rows, const int64_t *col
     free(cnt); free(fill); free(uniq);
     return nnz;
 }
+
+/* ------------------------------------------------------------------------
+ * Config X (papers100M-shaped): directed graph, out-degree
+ * round(lognormal(mu, sigma)) rescaled to mean `mean_deg` and capped at dmax,
+ * columns ~ Cat(p) with p_j = 1 + Lomax(alpha) (alias method), deduplicated per
+ * row.  Row i's draws use counters derived from (seed, i) only, so the output
+ * does not depend on the thread count.
+ * ---------------------------------------------------------------------- */
+#include <math.h>
+
+static inline double normal01(uint64_t seed, uint64_t ctr)
+{
+    double u1 = u01(seed, ctr), u2 = u01(seed, ctr + 1);
+    if (u1 < 1e-300) u1 = 1e-300;
+    return sqrt(-2.0 * log(u1)) * cos(6.283185307179586 * u2);
+}
+
+void gen_x_degrees(int64_t n, double mean_deg, double mu, double sigma, int64_t dmax, uint64_t seed, int64_t *deg)
+{
+    const double scale = mean_deg / exp(mu + 0.5 * sigma * sigma);
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) {
+        double x = exp(mu + sigma * normal01(seed, 2ull * (uint64_t)i)) * scale;
+        int64_t d = (int64_t)llround(x);
+        if (d < 1) d = 1;
+        if (d > dmax) d = dmax;
+        if (d > n) d = n;
+        deg[i] = d;
+    }
+}
+
+/* Vose alias table over weights w[0..n): prob[], alias[] (caller-allocated). */
+void gen_alias_build(int64_t n, const double *w, double *prob, int64_t *alias)
+{
+    double total = 0.0;
+    for (int64_t i = 0; i < n; ++i) total += w[i];
+    int64_t *small = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
+    int64_t *large = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
+    int64_t ns = 0, nl = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        prob[i] = w[i] * (double)n / total;
+        if (prob[i] < 1.0) small[ns++] = i; else large[nl++] = i;
+    }
+    while (ns > 0 && nl > 0) {
+        int64_t s = small[--ns], l = large[--nl];
+        alias[s] = l;
+        prob[l] = (prob[l] + prob[s]) - 1.0;
+        if (prob[l] < 1.0) small[ns++] = l; else large[nl++] = l;
+    }
+    while (nl > 0) { int64_t l = large[--nl]; prob[l] = 1.0; alias[l] = l; }
+    while (ns > 0) { int64_t s = small[--ns]; prob[s] = 1.0; alias[s] = s; }
+    free(small);
+    free(large);
+}
+
+/* Fills row i's draws at colidx[off[i] .. off[i]+deg_i), sorts and deduplicates each
+ * row in place; uniq[i] receives the unique count.  Then compacts into CSR:
+ * rowptr (n+1) and colidx[0 .. rowptr[n]).  Returns rowptr[n]. */
+int64_t gen_x_fill(int64_t n, int64_t ncols, const int64_t *off, const double *prob, const int64_t *alias,
+                   uint64_t seed, int32_t *colidx, int64_t *rowptr)
+{
+    int64_t *uniq = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
+#pragma omp parallel for schedule(dynamic, 4096)
+    for (int64_t i = 0; i < n; ++i) {
+        int64_t d = off[i + 1] - off[i];
+        int32_t *a = colidx + off[i];
+        uint64_t base = 0x5851F42D4C957F2Dull ^ ((uint64_t)i << 20);
+        for (int64_t k = 0; k < d; ++k) {
+            double u = u01(seed, base + 2ull * (uint64_t)k) * (double)ncols;
+            int64_t j = (int64_t)u;
+            if (j >= ncols) j = ncols - 1;
+            double f = u - (double)j;
+            a[k] = (int32_t)(f < prob[j] ? j : alias[j]);
+        }
+        if (d > 1) qsort(a, (size_t)d, sizeof(int32_t), cmp_i32);
+        int64_t u = 0;
+        for (int64_t k = 0; k < d; ++k)
+            if (k == 0 || a[k] != a[k - 1]) a[u++] = a[k];
+        uniq[i] = u;
+    }
+    rowptr[0] = 0;
+    for (int64_t i = 0; i < n; ++i) rowptr[i + 1] = rowptr[i] + uniq[i];
+    for (int64_t i = 0; i < n; ++i)
+        if (rowptr[i] != off[i] && uniq[i] > 0)
+            memmove(colidx + rowptr[i], colidx + off[i], sizeof(int32_t) * (size_t)uniq[i]);
+    int64_t nnz = rowptr[n];
+    free(uniq);
+    return nnz;
+}

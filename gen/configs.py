@@ -48,6 +48,16 @@ def _products():
     return mx.dcsbm(2_449_029, 123_718_280, 47, 2.1, 0.10, 17_481, seed=9, oversample=1.22)
 
 
+def _papers100m():
+    # directed, out-degree lognormal(2.3, 0.8) rescaled to mean 14.55, popularity Pareto(1.2)
+    return mx.powerlaw_directed(111_059_956, 14.55, seed=11)
+
+
+def _papers100m_small():
+    # 1/64 scale of config X with the same per-row statistics (CPU-checkable, multi-GPU tests)
+    return mx.powerlaw_directed(111_059_956 // 64, 14.55, seed=11)
+
+
 CONFIGS = {
     "tiny": Config("tiny", 0, (16,), 1, 2, _tiny, "uniform random 512x512, 5120 nnz"),
     "stencil": Config("stencil", 1, (128,), 3, 4, _stencil, "27-point stencil on 100^3 grid, 26.46M nnz"),
@@ -56,6 +66,10 @@ CONFIGS = {
                      "Reddit-shaped DC-SBM 232,965 nodes ~115M nnz, labels shuffled"),
     "products": Config("products", 3, (128,), 9, 10, _products,
                        "ogbn-products-shaped DC-SBM 2,449,029 nodes ~124M nnz"),
+    "papers100m": Config("papers100m", 4, (64,), 11, 12, _papers100m,
+                         "ogbn-papers100M-shaped directed power-law 111,059,956 nodes ~1.6B nnz"),
+    "papers100m_small": Config("papers100m_small", 4, (64,), 11, 12, _papers100m_small,
+                               "papers100M-shaped at 1/64 scale (1,735,311 nodes ~25M nnz)"),
 }
 
 

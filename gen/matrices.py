@@ -39,6 +39,13 @@ def _native():
         lib.gen_pairs_to_csr.restype = I
         lib.gen_dcsbm_draw.argtypes = [I, I, P, P, P, P, P, P, P, P, ctypes.c_double, ctypes.c_uint64, P, P]
         lib.gen_dcsbm_draw.restype = None
+        D = ctypes.c_double
+        lib.gen_x_degrees.argtypes = [I, D, D, D, I, ctypes.c_uint64, P]
+        lib.gen_x_degrees.restype = None
+        lib.gen_alias_build.argtypes = [I, P, P, P]
+        lib.gen_alias_build.restype = None
+        lib.gen_x_fill.argtypes = [I, I, P, P, P, ctypes.c_uint64, P, P]
+        lib.gen_x_fill.restype = I
         _lib = lib
     return _lib
 
@@ -140,6 +147,32 @@ def dcsbm(n: int, target_nnz: int, communities: int, alpha: float, mu: float,
     _native().gen_dcsbm_draw(E, n, _p(cum), _p(comm32), _p(order), _p(cum_sorted), _p(starts), _p(ends),
                              _p(base), _p(tot), float(mu), int(seed) & 0xFFFFFFFFFFFFFFFF, _p(src), _p(dst))
     return csr_from_pairs(src, dst, n, n, symmetric=True, drop_diag=True)
+
+
+def powerlaw_directed(n: int, mean_deg: float, seed: int, mu: float = 2.3, sigma: float = 0.8,
+                      dmax: int = 2000, alpha: float = 1.2) -> Csr:
+    """Config X (papers100M-shaped): out-degree round(lognormal(mu, sigma)) rescaled to mean
+    ``mean_deg``, capped at dmax; columns ~ Cat(p), p_j = 1 + Lomax(alpha); dedup per row."""
+    lib = _native()
+    rng = np.random.default_rng(seed)
+    w = 1.0 + rng.pareto(alpha, size=n)
+    prob = np.empty(n, dtype=np.float64)
+    alias = np.empty(n, dtype=np.int64)
+    lib.gen_alias_build(n, _p(w), _p(prob), _p(alias))
+    del w
+    deg = np.empty(n, dtype=np.int64)
+    lib.gen_x_degrees(n, float(mean_deg), float(mu), float(sigma), int(dmax), int(seed) & 0xFFFFFFFFFFFFFFFF, _p(deg))
+    off = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(deg, out=off[1:])
+    del deg
+    colidx = np.empty(int(off[-1]), dtype=np.int32)
+    rowptr = np.empty(n + 1, dtype=np.int64)
+    nnz = lib.gen_x_fill(n, n, _p(off), _p(prob), _p(alias), (int(seed) * 7919 + 1) & 0xFFFFFFFFFFFFFFFF,
+                         _p(colidx), _p(rowptr))
+    del off, prob, alias
+    if nnz < colidx.size:
+        colidx = colidx[:nnz].copy()
+    return Csr(n, n, rowptr, colidx)
 
 
 def sbm(n: int, blocks: int, p_in: float, p_out: float, seed: int, shuffle: bool = True) -> Csr:

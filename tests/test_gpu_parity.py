@@ -326,7 +326,7 @@ def _sample_rows(M, n, seed):
 
 @pytest.mark.parametrize("name,N,precision", [
     ("reddit", 128, "tf32"), ("reddit", 128, "fp16"), ("reddit", 32, "tf32"), ("reddit", 64, "tf32"),
-    ("stencil", 128, "tf32"), ("products", 128, "tf32"),
+    ("stencil", 128, "tf32"), ("products", 128, "tf32"), ("papers100m_small", 64, "tf32"),
 ])
 def test_full_size_config_sampled(name, N, precision):
     cfg, A = gen.make_config(name)
@@ -336,6 +336,17 @@ def test_full_size_config_sampled(name, N, precision):
     rows = _sample_rows(A.M, 3000, 1)
     assert np.isfinite(C).all()
     assert_within(C, A, v, B, precision, rows=rows)
+
+
+@pytest.mark.parametrize("name,N,reorder", [("reddit", 128, "auto"), ("papers100m_small", 64, "off")])
+def test_bench_configuration_sampled(name, N, reorder):
+    """The launch configuration bench.py times (reorder/balance auto), sampled rows vs the oracle."""
+    cfg, A = gen.make_config(name)
+    v = gen.values_uniform(A.nnz, cfg.seed_A + 1)
+    B = gen.dense_normal(A.K, N, cfg.seed_B)
+    C, p = run(A, v, B, "tf32", reorder=reorder, balance="auto")
+    assert np.isfinite(C).all()
+    assert_within(C, A, v, B, "tf32", rows=_sample_rows(A.M, 3000, 3))
 
 
 def test_full_size_reddit_integer_sampled_bit_exact():
