@@ -228,9 +228,15 @@ def star(leaves: int) -> Csr:
 
 # --------------------------------------------------------------------------- values
 
-def values_uniform(nnz: int, seed: int) -> np.ndarray:
-    """A values ~ U[-1, 1) float32 (SURVEY §8(d) 'Values and B')."""
-    return np.random.default_rng(seed).uniform(-1.0, 1.0, nnz).astype(np.float32)
+def values_uniform(nnz: int, seed: int, chunk: int = 1 << 24) -> np.ndarray:
+    """A values ~ U[-1, 1) float32 (SURVEY §8(d) 'Values and B'); drawn in chunks from one
+    stream (identical to a single draw) so 1.6B values need no float64 temporary."""
+    rng = np.random.default_rng(seed)
+    out = np.empty(nnz, dtype=np.float32)
+    for a in range(0, nnz, chunk):
+        n = min(chunk, nnz - a)
+        out[a:a + n] = rng.uniform(-1.0, 1.0, n)
+    return out
 
 
 def values_int(nnz: int, seed: int) -> np.ndarray:
