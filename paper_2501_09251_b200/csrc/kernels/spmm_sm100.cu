@@ -153,7 +153,7 @@ struct Cfg {
     using V = typename Vec<VB>::T;
 };
 
-constexpr int kChunk = 32;  // TC blocks per staged A-stream chunk
+constexpr int kChunk = 16;  // TC blocks per staged A-stream chunk
 
 struct ChunkSmem {
     uint32_t a2b[kChunk * 8];
@@ -304,7 +304,7 @@ __global__ void __launch_bounds__(WARPS * 32) spmm_bittcf_kernel(const KParams p
     // ---- A-stream chunk staging (cp.async, double buffered)
     auto issue_chunk = [&](uint32_t i) {  // blocks [b0+i, b0+i+32) -> buffer (i/32)&1
         if (i < nblk) {
-            ChunkSmem &c = sm.ch[(i >> 5) & 1];
+            ChunkSmem &c = sm.ch[(i / kChunk) & 1];
             const uint32_t b = b0 + i;
             const uint32_t cnt = min((uint32_t)kChunk, nblk - i);
             if ((uint32_t)lane < cnt) {
@@ -320,13 +320,13 @@ __global__ void __launch_bounds__(WARPS * 32) spmm_bittcf_kernel(const KParams p
 
     // ---- gather + decode of block i (relative to b0) into a register fragment
     auto load_block = [&](Frag<FW, F16> &fr, uint32_t i) {
-        if ((i & 31u) == 0) {  // chunk boundary: chunk i/32 must have landed; prefetch the next one
+        if ((i & (kChunk - 1u)) == 0) {  // chunk boundary: this chunk must have landed; prefetch the next one
             cp_async_wait_all();
             __syncwarp();
             issue_chunk(i + kChunk);
         }
-        const ChunkSmem &c = sm.ch[(i >> 5) & 1];
-        const uint32_t cs = i & 31u;
+        const ChunkSmem &c = sm.ch[(i / kChunk) & 1];
+        const uint32_t cs = i & (kChunk - 1u);
         const uint64_t mask = c.mask[cs];
         const uint32_t t0 = c.tco[cs];
         uint64_t cm = mask | (mask >> 32);
@@ -563,7 +563,7 @@ __global__ void __launch_bounds__(WARPS * 32)
 
     auto issue_chunk = [&](uint32_t i) {
         if (i < nblk) {
-            ChunkSmem &c = sm.ch[(i >> 5) & 1];
+            ChunkSmem &c = sm.ch[(i / kChunk) & 1];
             const uint32_t b = b0 + i;
             const uint32_t cnt = min((uint32_t)kChunk, nblk - i);
             if ((uint32_t)lane < cnt) {
@@ -584,13 +584,13 @@ __global__ void __launch_bounds__(WARPS * 32)
     //      every lane decodes its two tile entries and loads their values
     auto issue = [&](uint32_t i, int s) {
         if (i >= nblk) return;
-        if ((i & 31u) == 0) {
+        if ((i & (kChunk - 1u)) == 0) {
             cp_async_wait_all();
             __syncwarp();
             issue_chunk(i + kChunk);
         }
-        const ChunkSmem &c = sm.ch[(i >> 5) & 1];
-        const uint32_t cs = i & 31u;
+        const ChunkSmem &c = sm.ch[(i / kChunk) & 1];
+        const uint32_t cs = i & (kChunk - 1u);
         const uint64_t mask = c.mask[cs];
         const uint32_t t0 = c.tco[cs];
         bool p0, p1;
@@ -646,19 +646,29 @@ __global__ void __launch_bounds__(WARPS * 32)
         const uint8_t *rb = st + GC::GRP + t * GC::RS + CF::VB * g;
         if constexpr (!F16 && CF::VW == 4) {
             // two k=4 halves of the 8x8 tile: rows t (k = 0..3) and t+4 (k = 4..7); each
-            // LDS.128 of one row feeds the A operands of two m16 tiles directly
+            // LDS.128 of one row feeds the A operands of two m16 tiles directly.  All k = 0..3
+            // MMAs go first so dependent accumulations sit NV*2 instructions apart.
+            uint4 x[NV], y[NV];
 #pragma unroll
             for (int j = 0; j < NV; ++j) {
-                uint4 x = *reinterpret_cast<const uint4 *>(ra + 8 * CF::VB * j);
-                uint4 y = *reinterpret_cast<const uint4 *>(rb + 8 * CF::VB * j);
+                x[j] = *reinterpret_cast<const uint4 *>(ra + 8 * CF::VB * j);
+                y[j] = *reinterpret_cast<const uint4 *>(rb + 8 * CF::VB * j);
                 if constexpr (RND) {  // rho(B) in registers (low-reuse plans skip the pre-round pass)
-                    x = make_uint4(tf32_rna_bits(x.x), tf32_rna_bits(x.y), tf32_rna_bits(x.z), tf32_rna_bits(x.w));
-                    y = make_uint4(tf32_rna_bits(y.x), tf32_rna_bits(y.y), tf32_rna_bits(y.z), tf32_rna_bits(y.w));
+                    x[j] = make_uint4(tf32_rna_bits(x[j].x), tf32_rna_bits(x[j].y), tf32_rna_bits(x[j].z),
+                                      tf32_rna_bits(x[j].w));
+                    y[j] = make_uint4(tf32_rna_bits(y[j].x), tf32_rna_bits(y[j].y), tf32_rna_bits(y[j].z),
+                                      tf32_rna_bits(y[j].w));
                 }
-                mma_tf32_k4(acc[2 * j], x.x, x.y, vb0[s]);
-                mma_tf32_k4(acc[2 * j + 1], x.z, x.w, vb0[s]);
-                mma_tf32_k4(acc[2 * j], y.x, y.y, vb1[s]);
-                mma_tf32_k4(acc[2 * j + 1], y.z, y.w, vb1[s]);
+            }
+#pragma unroll
+            for (int j = 0; j < NV; ++j) {
+                mma_tf32_k4(acc[2 * j], x[j].x, x[j].y, vb0[s]);
+                mma_tf32_k4(acc[2 * j + 1], x[j].z, x[j].w, vb0[s]);
+            }
+#pragma unroll
+            for (int j = 0; j < NV; ++j) {
+                mma_tf32_k4(acc[2 * j], y[j].x, y[j].y, vb1[s]);
+                mma_tf32_k4(acc[2 * j + 1], y[j].z, y[j].w, vb1[s]);
             }
         } else {
             Frag<FW, F16> fr;
