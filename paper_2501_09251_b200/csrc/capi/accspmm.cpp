@@ -231,7 +231,21 @@ accspmm_status accspmm_plan_create_ex(int64_t M, int64_t K, const int64_t *rowpt
         int64_t bytes = 0;
         st = upload(&d.rwo, F.rwo, bytes);
         if (st == ACCSPMM_OK) st = upload(&d.tco, F.tco, bytes);
-        if (st == ACCSPMM_OK) st = upload(&d.a2b, F.a2b, bytes);
+        if (st == ACCSPMM_OK) {
+            // device copy: padding lanes (no bit in the block's column-OR) hold 0xFFFFFFFF, an
+            // out-of-bounds row the TMA zero-fills; the exported paper format keeps 0
+            std::vector<uint32_t> a2b_dev(F.a2b);
+#pragma omp parallel for schedule(static)
+            for (int64_t b = 0; b < F.NB; ++b) {
+                uint64_t m = F.bits[(size_t)b];
+                m |= m >> 32;
+                m |= m >> 16;
+                m |= m >> 8;
+                for (int l = 0; l < kWindow; ++l)
+                    if (!((m >> l) & 1u)) a2b_dev[(size_t)b * kWindow + (size_t)l] = kPadLane;
+            }
+            st = upload(&d.a2b, a2b_dev, bytes);
+        }
         if (st == ACCSPMM_OK) st = upload(&d.bits, F.bits, bytes);
         if (st == ACCSPMM_OK) {
             if (opt.precision == ACCSPMM_FP16) st = upload((uint16_t **)&d.vals, F.v16, bytes, 16);
@@ -379,7 +393,12 @@ accspmm_status accspmm_plan_export_format(const accspmm_plan *p, uint32_t *rwo, 
     const bool dev = p->opt.device >= 0;
     accspmm_status st = export_array(rwo, p->host.rwo, dev ? p->dev.rwo : nullptr, (size_t)I.W + 1);
     if (st == ACCSPMM_OK) st = export_array(tco, p->host.tco, dev ? p->dev.tco : nullptr, (size_t)I.NB + 1);
-    if (st == ACCSPMM_OK) st = export_array(a2b, p->host.a2b, dev ? p->dev.a2b : nullptr, (size_t)I.NB * 8);
+    if (st == ACCSPMM_OK) {
+        st = export_array(a2b, p->host.a2b, dev ? p->dev.a2b : nullptr, (size_t)I.NB * 8);
+        if (st == ACCSPMM_OK && a2b && dev)  // device padding marker -> the paper format's 0
+            for (size_t q = 0; q < (size_t)I.NB * 8; ++q)
+                if (a2b[q] == kPadLane) a2b[q] = 0u;
+    }
     if (st == ACCSPMM_OK) st = export_array(bits, p->host.bits, dev ? p->dev.bits : nullptr, (size_t)I.NB);
     if (st == ACCSPMM_OK) {
         if (p->opt.precision == ACCSPMM_FP16)

@@ -10,6 +10,7 @@ namespace accspmm {
 
 constexpr int kWindow = 8;            // P:250 "8 x 8" TC blocks, P:251 ceil(M/8) windows
 constexpr uint32_t kNoSplit = 0xFFFFFFFFu;
+constexpr uint32_t kPadLane = 0xFFFFFFFFu;  // device SparseAToB padding lane (row -1: TMA zero fill)
 constexpr int kWmax = 31;             // windows per concatenated unit (one per lane of the window table)
 constexpr double kIbdThreshold = 8.0; // P:417 "When IBD exceeds 8"
 constexpr int kPaperCap = 32;         // P:446 "maximum threshold of 32 TC blocks per TB"

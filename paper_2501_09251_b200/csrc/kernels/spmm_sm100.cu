@@ -608,16 +608,11 @@ __global__ void __launch_bounds__(WARPS * 32)
             vb1[s] = 0u;
         }
         if (lane == 0) {
-            uint64_t cm = mask | (mask >> 32);
-            cm |= cm >> 16;
-            cm |= cm >> 8;
+            // padding lanes hold 0xFFFFFFFF on the device (row -1): the TMA zero-fills them
             const uint4 ca = *reinterpret_cast<const uint4 *>(&c.a2b[cs * 8]);
             const uint4 cb = *reinterpret_cast<const uint4 *>(&c.a2b[cs * 8 + 4]);
-            const int32_t K = p.Krows;
-            const int32_t r0 = (cm & 1u) ? (int32_t)ca.x : K, r1 = (cm & 2u) ? (int32_t)ca.y : K;
-            const int32_t r2 = (cm & 4u) ? (int32_t)ca.z : K, r3 = (cm & 8u) ? (int32_t)ca.w : K;
-            const int32_t r4 = (cm & 16u) ? (int32_t)cb.x : K, r5 = (cm & 32u) ? (int32_t)cb.y : K;
-            const int32_t r6 = (cm & 64u) ? (int32_t)cb.z : K, r7 = (cm & 128u) ? (int32_t)cb.w : K;
+            const int32_t r0 = (int32_t)ca.x, r1 = (int32_t)ca.y, r2 = (int32_t)ca.z, r3 = (int32_t)ca.w;
+            const int32_t r4 = (int32_t)cb.x, r5 = (int32_t)cb.y, r6 = (int32_t)cb.z, r7 = (int32_t)cb.w;
             const uint32_t bar = smem_u32(&sm.bar[s]);
             const uint32_t st = smem_u32(sm.stage[s]);
             // no proxy fence: the stage's previous generic reads fed this warp's mma.sync,

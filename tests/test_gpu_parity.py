@@ -274,6 +274,21 @@ def test_device_decode_matches_oracle_tiles(precision):
     assert np.array_equal(tiles, ref)
 
 
+@pytest.mark.parametrize("precision", PRECISIONS)
+def test_device_plan_exports_paper_format(precision):
+    """The device copy of the format (padding lanes re-marked for the TMA) exports as BitTCF."""
+    from oracle import bittcf as bt
+    from oracle.rounding import rho
+    A = _ragged(seed=6, M=700, K=900, nnz=9000)
+    v = gen.values_uniform(A.nnz, 2)
+    p = acc.Plan(A.M, A.K, A.rowptr, A.colidx, v, precision=precision)
+    F = p.export_format()
+    ref = bt.encode(A.M, A.K, A.rowptr, A.colidx, rho(v, precision))
+    for k in ("RowWindowOffset", "TCOffset", "SparseAToB", "TCLocalBit"):
+        assert np.array_equal(F[k], ref[k]), k
+    assert np.array_equal(F["values"].astype(np.float32), ref["values"].astype(np.float32))
+
+
 def test_e2e_host_path_matches_device_path():
     A = _ragged(seed=3)
     v = gen.values_uniform(A.nnz, 1)
