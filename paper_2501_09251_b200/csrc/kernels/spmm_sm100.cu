@@ -582,8 +582,8 @@ __global__ void __launch_bounds__(WARPS * 32)
 
     // ---- producer: lane 0 issues two gather4 of block i's B rows into stage s;
     //      every lane decodes its two tile entries and loads their values
-    auto issue = [&](uint32_t i, int s) {
-        if (i >= nblk) return;
+    auto issue = [&](uint32_t i, int s, bool checked) {
+        if (checked && i >= nblk) return;
         if ((i & (kChunk - 1u)) == 0) {
             cp_async_wait_all();
             __syncwarp();
@@ -720,13 +720,25 @@ __global__ void __launch_bounds__(WARPS * 32)
     issue_chunk(0);
     after_block(b0);
 #pragma unroll
-    for (int s = 0; s < STAGES - 1; ++s) issue((uint32_t)s, s);
-    for (uint32_t i = 0; i < nblk; i += STAGES) {
+    for (int s = 0; s < STAGES - 1; ++s) issue((uint32_t)s, s, true);
+    // steady state: every look-ahead issue is in range (no bound checks); then the tail
+    const uint32_t nmain = nblk >= (uint32_t)STAGES ? ((nblk - (STAGES - 1)) / STAGES) * STAGES : 0u;
+    uint32_t i = 0;
+    for (; i < nmain; i += STAGES) {
+#pragma unroll
+        for (int s = 0; s < STAGES; ++s) {
+            const uint32_t ii = i + (uint32_t)s;
+            issue(ii + STAGES - 1, (s + STAGES - 1) % STAGES, false);
+            consume(ii, s);
+            after_block(b0 + ii + 1);
+        }
+    }
+    for (; i < nblk; i += STAGES) {
 #pragma unroll
         for (int s = 0; s < STAGES; ++s) {
             const uint32_t ii = i + (uint32_t)s;
             if (ii < nblk) {
-                issue(ii + STAGES - 1, (s + STAGES - 1) % STAGES);
+                issue(ii + STAGES - 1, (s + STAGES - 1) % STAGES, true);
                 consume(ii, s);
                 after_block(b0 + ii + 1);
             }
