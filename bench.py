@@ -185,6 +185,14 @@ def workload_config(args, cfg, A, world):
             "parallelism": f"rowwindow-nnz-partition x{world}"}
 
 
+def kernel_name(args):
+    """The SpMM kernel flavour the library's default dispatch picks."""
+    N = args.N
+    fw = 128 if N % 128 == 0 else 64 if N % 64 == 0 else 32 if N % 32 == 0 else 16
+    g4 = (args.precision == "tf32" and fw >= 64) or (args.precision == "fp16" and fw == 128)
+    return "spmm_bittcf_g4_kernel (TMA gather4)" if g4 else "spmm_bittcf_kernel (register-direct gather)"
+
+
 def emit(out, args):
     line = json.dumps(out)
     print(line, flush=True)
@@ -320,7 +328,7 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                          "bytes_model_per_launch": bm, "frac_of_8TBps_spec": achieved / 8000.0,
-                         "kernel": "spmm_bittcf_kernel", "launch_ms": avg_s * 1e3,
+                         "kernel": kernel_name(args), "launch_ms": avg_s * 1e3,
                          "kernel_share_of_step": avg_s * args.steps / t_local},
             "cpu_baseline": cpu,
             "clocks": clk,
