@@ -214,9 +214,17 @@ def main():
 
     import paper_2501_09251_b200 as acc
 
+    # ACCSPMM_BENCH_SHARED_GPU=1: every rank on cuda:0 over gloo (exercises the multi-rank
+    # path on a one-GPU box; NCCL refuses two ranks per device).  Default: one GPU per rank, NCCL.
+    shared = os.environ.get("ACCSPMM_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     cfg, A, vals, B = make_inputs(args)
     t0 = time.perf_counter()
@@ -233,7 +241,12 @@ def main():
     if world > 1:
         torch.cuda.synchronize()
         tb = time.perf_counter()
-        dist.broadcast(Bd, src=0)
+        if shared:
+            Bh = Bd.cpu()
+            dist.broadcast(Bh, src=0)
+            Bd.copy_(Bh)
+        else:
+            dist.broadcast(Bd, src=0)
         torch.cuda.synchronize()
         bcast_ms = (time.perf_counter() - tb) * 1e3
     C = torch.empty((plan.out_rows, args.N), dtype=torch.float32, device="cuda")
@@ -270,7 +283,7 @@ def main():
     t_local = sum(step_ms) / 1e3
     t_max = t_local
     if world > 1:
-        tt = torch.tensor([t_local], dtype=torch.float64, device="cuda")
+        tt = torch.tensor([t_local], dtype=torch.float64, device="cpu" if shared else "cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_max = float(tt.item())
     flops_total = 2.0 * A.nnz * args.N * args.steps
@@ -307,7 +320,7 @@ def main():
         torch.cuda.synchronize()
         te = s0.elapsed_time(s1) / 1e3
         if world > 1:
-            tt = torch.tensor([te], dtype=torch.float64, device="cuda")
+            tt = torch.tensor([te], dtype=torch.float64, device="cpu" if shared else "cuda")
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             te = float(tt.item())
         e2e = {"value": 2.0 * A.nnz * args.N * e_steps / te / 1e9, "unit": "GFLOP/s",

@@ -373,3 +373,29 @@ def test_full_size_reddit_integer_sampled_bit_exact():
     rows = _sample_rows(A.M, 2000, 2)
     Cr, _ = oracle(A, v, B, "tf32", rows=rows)
     assert np.array_equal(C[rows].astype(np.float64), Cr)
+
+
+# --------------------------------------------------------------- randomized sweep
+
+@pytest.mark.parametrize("seed", range(24))
+def test_random_shapes_and_options(seed):
+    """Seeded random shapes, densities, N, precision and plan options vs the oracle."""
+    rng = np.random.default_rng(seed)
+    M, K = int(rng.integers(1, 3000)), int(rng.integers(1, 3000))
+    nnz = int(min(M * K, 10 ** rng.uniform(0, 5)))
+    A = gen.uniform_random(M, K, nnz, seed=seed)
+    N = int(rng.choice([16, 32, 48, 64, 80, 128, 192, 256, 384]))
+    precision = PRECISIONS[seed % 2]
+    balance = ["off", "on", "auto"][seed % 3]
+    cap = int(rng.choice([0, 8, 32, 100]))
+    reorder = "on" if (M == K and seed % 4 == 0) else "off"
+    if seed % 5 == 0:
+        v = gen.values_int(A.nnz, seed)
+        B = gen.dense_int(K, N, seed + 1)
+        C, _ = run(A, v, B, precision, balance=balance, unit_cap=cap, reorder=reorder)
+        assert_bit_exact(C, A, v, B, precision)
+    else:
+        v = gen.values_uniform(A.nnz, seed)
+        B = gen.dense_normal(K, N, seed + 1)
+        C, _ = run(A, v, B, precision, balance=balance, unit_cap=cap, reorder=reorder)
+        assert_within(C, A, v, B, precision)
