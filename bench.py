@@ -187,9 +187,8 @@ def workload_config(args, cfg, A, world):
 
 def kernel_name(args):
     """The SpMM kernel flavour the library's default dispatch picks."""
-    N = args.N
-    fw = 128 if N % 128 == 0 else 64 if N % 64 == 0 else 32 if N % 32 == 0 else 16
-    g4 = (args.precision == "tf32" and fw >= 64) or (args.precision == "fp16" and fw == 128)
+    kcfg = int(os.environ.get("ACCSPMM_KCFG", "-1"))
+    g4 = kcfg < 0 or kcfg >= 20
     return "spmm_bittcf_g4_kernel (TMA gather4)" if g4 else "spmm_bittcf_kernel (register-direct gather)"
 
 

@@ -877,11 +877,11 @@ template <int FW, bool F16>
 accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, int64_t n_units, cudaStream_t stream,
                          bool rnd)
 {
-    // Default (measured): TMA gather4 for slices of >= 256-byte rows (TF32
-    // FW >= 64, FP16 FW = 128); the register-direct gather (2 warps/CTA) for narrower
-    // slices, where per-TMA-request cost dominates.  ACCSPMM_KCFG overrides for tuning.
+    // Default (measured): TMA gather4, 2 warps x 2 stages per CTA, at every
+    // width and precision.  ACCSPMM_KCFG selects other variants for A/B measurements
+    // (21-24: gather4 warps/stages, 10-12: register-direct gather).
     int kcfg = env_int("ACCSPMM_KCFG", -1);
-    if (kcfg < 0) kcfg = ((!F16 && FW >= 64) || (F16 && FW == 128)) ? 20 : 11;
+    if (kcfg < 0) kcfg = 20;
     if constexpr (!F16) {
         if (rnd) {  // B not pre-rounded: rho(B) applied in registers (default configurations only)
             if (kcfg >= 20) {
