@@ -15,6 +15,7 @@
 // Reading R6b: after a visit, a community passes on at most its 256
 // heaviest neighbour-community edges, so chains of merges on meshes stay O(m).
 #include <algorithm>
+#include <cstdlib>
 #include <numeric>
 
 #include "../internal.hpp"
@@ -22,8 +23,14 @@
 namespace accspmm {
 
 namespace {
-constexpr int kCandWindow = 64;  // L
-constexpr int kHubCap = 128;     // H
+constexpr int kCandWindow = 64;  // L (default; ACCSPMM_REORDER_L overrides for experiments)
+constexpr int kHubCap = 128;     // H (default; ACCSPMM_REORDER_H overrides for experiments)
+
+int env_or(const char *name, int dflt)
+{
+    const char *s = std::getenv(name);
+    return s ? std::atoi(s) : dflt;
+}
 constexpr size_t kEdgeCap = 256;  // community edges carried up a merge (reading R6b)
 
 struct Graph {
@@ -180,6 +187,7 @@ std::vector<uint32_t> reorder_alg1(const Csr &a)
     prv[0] = n;
     prv[(size_t)n] = n - 1;
     if (n > 0) nxt[(size_t)n - 1] = n;
+    const int L = env_or("ACCSPMM_REORDER_L", kCandWindow), H = env_or("ACCSPMM_REORDER_H", kHubCap);
     std::vector<char> visited((size_t)n, 0);
     std::vector<uint32_t> mark((size_t)n, 0);
     uint32_t stamp = 0;
@@ -198,14 +206,14 @@ std::vector<uint32_t> reorder_alg1(const Csr &a)
         while (nxt[(size_t)n] != n) {
             ++stamp;
             if (stamp == 0) { std::fill(mark.begin(), mark.end(), 0u); stamp = 1; }
-            const int64_t dv = std::min<int64_t>(kHubCap, g.ptr[v + 1] - g.ptr[v]);
+            const int64_t dv = std::min<int64_t>(H, g.ptr[v + 1] - g.ptr[v]);
             for (int64_t q = 0; q < dv; ++q) mark[g.adj[(size_t)(g.ptr[v] + q)]] = stamp;
             uint32_t best = UINT32_MAX;
             int64_t best_c = 0;
             int cand = 0;
-            for (int64_t p = nxt[(size_t)n]; p != n && cand < kCandWindow; p = nxt[(size_t)p], ++cand) {
+            for (int64_t p = nxt[(size_t)n]; p != n && cand < L; p = nxt[(size_t)p], ++cand) {
                 uint32_t u = seq[(size_t)p];
-                const int64_t du = std::min<int64_t>(kHubCap, g.ptr[u + 1] - g.ptr[u]);
+                const int64_t du = std::min<int64_t>(H, g.ptr[u + 1] - g.ptr[u]);
                 int64_t c = 0;
                 for (int64_t q = 0; q < du; ++q) c += mark[g.adj[(size_t)(g.ptr[u] + q)]] == stamp;
                 if (c > best_c) { best_c = c; best = u; }

@@ -577,20 +577,15 @@ __global__ void __launch_bounds__(WARPS * 32)
         cp_async_commit();
     };
 
-    // value registers of the blocks in flight (decoded at issue time, one per stage)
-    uint32_t vb0[STAGES], vb1[STAGES];
+    // Value registers of the blocks in flight: decoded and loaded 2 blocks ahead of use
+    // (a 4-slot ring), so their L2 latency hides behind two block steps.
+    constexpr int VR = 4;
+    uint32_t vb0[VR], vb1[VR];
 
-    // ---- producer: lane 0 issues two gather4 of block i's B rows into stage s;
-    //      every lane decodes its two tile entries and loads their values
-    auto issue = [&](uint32_t i, int s, bool checked) {
-        if (checked && i >= nblk) return;
-        if ((i & (kChunk - 1u)) == 0) {
-            cp_async_wait_all();
-            __syncwarp();
-            issue_chunk(i + kChunk);
-        }
-        const ChunkSmem &c = sm.ch[(i / kChunk) & 1];
-        const uint32_t cs = i & (kChunk - 1u);
+    // ---- every lane: decode this lane's two tile entries of block j, load values
+    auto value_load = [&](uint32_t j, int slot) {
+        const ChunkSmem &c = sm.ch[(j / kChunk) & 1];
+        const uint32_t cs = j & (kChunk - 1u);
         const uint64_t mask = c.mask[cs];
         const uint32_t t0 = c.tco[cs];
         bool p0, p1;
@@ -598,16 +593,22 @@ __global__ void __launch_bounds__(WARPS * 32)
         const uint32_t i1 = t0 + tile_rank(mask, sh1, p1);
         if constexpr (!F16) {
             const float *vp = reinterpret_cast<const float *>(p.vals);
-            vb0[s] = p0 ? __float_as_uint(__ldg(vp + i0)) : 0u;
-            vb1[s] = p1 ? __float_as_uint(__ldg(vp + i1)) : 0u;
+            vb0[slot] = p0 ? __float_as_uint(__ldg(vp + i0)) : 0u;
+            vb1[slot] = p1 ? __float_as_uint(__ldg(vp + i1)) : 0u;
         } else {
             const unsigned short *vp = reinterpret_cast<const unsigned short *>(p.vals);
             const uint32_t lo = p0 ? (uint32_t)__ldg(vp + i0) : 0u;
             const uint32_t hi = p1 ? (uint32_t)__ldg(vp + i1) : 0u;
-            vb0[s] = lo | (hi << 16);
-            vb1[s] = 0u;
+            vb0[slot] = lo | (hi << 16);
+            vb1[slot] = 0u;
         }
+    };
+
+    // ---- lane 0: two gather4 of block j's B rows into stage s
+    auto issue_tma = [&](uint32_t j, int s) {
         if (lane == 0) {
+            const ChunkSmem &c = sm.ch[(j / kChunk) & 1];
+            const uint32_t cs = j & (kChunk - 1u);
             // padding lanes hold 0xFFFFFFFF on the device (row -1): the TMA zero-fills them
             const uint4 ca = *reinterpret_cast<const uint4 *>(&c.a2b[cs * 8]);
             const uint4 cb = *reinterpret_cast<const uint4 *>(&c.a2b[cs * 8 + 4]);
@@ -634,7 +635,7 @@ __global__ void __launch_bounds__(WARPS * 32)
     for (int m = 0; m < MT; ++m) acc[m][0] = acc[m][1] = acc[m][2] = acc[m][3] = 0.f;
 
     // ---- consumer: wait for stage s, load the gathered-row fragments, tensor-core MMA
-    auto consume = [&](uint32_t i, int s) {
+    auto consume = [&](uint32_t i, int s, int slot) {
         mbar_wait(smem_u32(&sm.bar[s]), (i / STAGES) & 1u);
         const uint8_t *st = sm.stage[s];
         const uint8_t *ra = st + t * GC::RS + CF::VB * g;
@@ -657,13 +658,13 @@ __global__ void __launch_bounds__(WARPS * 32)
             }
 #pragma unroll
             for (int j = 0; j < NV; ++j) {
-                mma_tf32_k4(acc[2 * j], x[j].x, x[j].y, vb0[s]);
-                mma_tf32_k4(acc[2 * j + 1], x[j].z, x[j].w, vb0[s]);
+                mma_tf32_k4(acc[2 * j], x[j].x, x[j].y, vb0[slot]);
+                mma_tf32_k4(acc[2 * j + 1], x[j].z, x[j].w, vb0[slot]);
             }
 #pragma unroll
             for (int j = 0; j < NV; ++j) {
-                mma_tf32_k4(acc[2 * j], y[j].x, y[j].y, vb1[s]);
-                mma_tf32_k4(acc[2 * j + 1], y[j].z, y[j].w, vb1[s]);
+                mma_tf32_k4(acc[2 * j], y[j].x, y[j].y, vb1[slot]);
+                mma_tf32_k4(acc[2 * j + 1], y[j].z, y[j].w, vb1[slot]);
             }
         } else {
             Frag<FW, F16> fr;
@@ -673,8 +674,8 @@ __global__ void __launch_bounds__(WARPS * 32)
                 fr.y[j] = *reinterpret_cast<const V *>(rb + 8 * CF::VB * j);
             }
             if constexpr (RND) round_frag<FW, F16>(fr);
-            fr.b0 = vb0[s];
-            fr.b1 = vb1[s];
+            fr.b0 = vb0[slot];
+            fr.b1 = vb1[slot];
             mma_block<FW, F16>(acc, fr);
         }
     };
@@ -717,32 +718,40 @@ __global__ void __launch_bounds__(WARPS * 32)
         }
     };
 
+    // Prologue: chunk 0 (wait) and chunk 1 in flight; values of blocks 0, 1; TMA of block 0.
     issue_chunk(0);
+    cp_async_wait_all();
+    __syncwarp();
+    issue_chunk(kChunk);
     after_block(b0);
-#pragma unroll
-    for (int s = 0; s < STAGES - 1; ++s) issue((uint32_t)s, s, true);
-    // steady state: every look-ahead issue is in range (no bound checks); then the tail
-    const uint32_t nmain = nblk >= (uint32_t)STAGES ? ((nblk - (STAGES - 1)) / STAGES) * STAGES : 0u;
-    uint32_t i = 0;
-    for (; i < nmain; i += STAGES) {
-#pragma unroll
-        for (int s = 0; s < STAGES; ++s) {
-            const uint32_t ii = i + (uint32_t)s;
-            issue(ii + STAGES - 1, (s + STAGES - 1) % STAGES, false);
-            consume(ii, s);
-            after_block(b0 + ii + 1);
+    if (nblk > 0) value_load(0, 0);
+    if (nblk > 1) value_load(1, 1);
+    if (nblk > 0) issue_tma(0, 0);
+    // Block step j: TMA for j+1 (chunk boundary: wait for the next chunk, prefetch the one
+    // after), values for j+2, then decode-free MMA of block j.  STAGES == 2 TMA stages.
+    static_assert(STAGES == 2, "the block step below is written for a 2-stage TMA ring");
+    auto step = [&](uint32_t j, int u, bool checked) {
+        const uint32_t jt = j + 1, jv = j + 2;
+        if (!checked || jt < nblk) issue_tma(jt, (u + 1) & 1);
+        if ((jv & (kChunk - 1u)) == 0) {  // chunk (jv / kChunk) must have landed
+            cp_async_wait_all();
+            __syncwarp();
+            issue_chunk(jv + kChunk);
         }
+        if (!checked || jv < nblk) value_load(jv, (u + 2) & (VR - 1));
+        consume(j, u & 1, u & (VR - 1));
+        after_block(b0 + j + 1);
+    };
+    const uint32_t nmain = nblk >= 2u ? ((nblk - 2u) / VR) * VR : 0u;
+    uint32_t j = 0;
+    for (; j < nmain; j += VR) {
+#pragma unroll
+        for (int u = 0; u < VR; ++u) step(j + (uint32_t)u, u, false);
     }
-    for (; i < nblk; i += STAGES) {
+    for (; j < nblk; j += VR) {
 #pragma unroll
-        for (int s = 0; s < STAGES; ++s) {
-            const uint32_t ii = i + (uint32_t)s;
-            if (ii < nblk) {
-                issue(ii + STAGES - 1, (s + STAGES - 1) % STAGES, true);
-                consume(ii, s);
-                after_block(b0 + ii + 1);
-            }
-        }
+        for (int u = 0; u < VR; ++u)
+            if (j + (uint32_t)u < nblk) step(j + (uint32_t)u, u, true);
     }
     cp_async_wait_all();
 
@@ -879,7 +888,8 @@ accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, 
 {
     // Default (measured): TMA gather4, 2 warps x 2 stages per CTA, at every
     // width and precision.  ACCSPMM_KCFG selects other variants for A/B measurements
-    // (21-24: gather4 warps/stages, 10-12: register-direct gather).
+    // (21, 22: gather4 with 4 / 1 warps per CTA; 10-12: register-direct gather).  Deeper
+    // gather4 rings (3, 4 stages) measured slower (smem per warp limits occupancy).
     int kcfg = env_int("ACCSPMM_KCFG", -1);
     if (kcfg < 0) kcfg = 20;
     if constexpr (!F16) {
@@ -899,9 +909,7 @@ accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, 
         if (st != ACCSPMM_OK) return st;
         switch (kcfg) {
         case 21: return launch_g4<FW, F16, 4, 2>(kp, map, n_units, stream);
-        case 22: return launch_g4<FW, F16, 2, 3>(kp, map, n_units, stream);
-        case 23: return launch_g4<FW, F16, 4, 3>(kp, map, n_units, stream);
-        case 24: return launch_g4<FW, F16, 2, 4>(kp, map, n_units, stream);
+        case 22: return launch_g4<FW, F16, 1, 2>(kp, map, n_units, stream);
         default: return launch_g4<FW, F16, 2, 2>(kp, map, n_units, stream);
         }
     }
