@@ -888,7 +888,7 @@ accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, 
 {
     // Default (measured): TMA gather4, 2 warps x 2 stages per CTA, at every
     // width and precision.  ACCSPMM_KCFG selects other variants for A/B measurements
-    // (21, 22: gather4 with 4 / 1 warps per CTA; 10-12: register-direct gather).  Deeper
+    // (21: gather4 with 4 warps per CTA; 10-12: register-direct gather).  Deeper
     // gather4 rings (3, 4 stages) measured slower (smem per warp limits occupancy).
     int kcfg = env_int("ACCSPMM_KCFG", -1);
     if (kcfg < 0) kcfg = 20;
@@ -909,7 +909,6 @@ accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, 
         if (st != ACCSPMM_OK) return st;
         switch (kcfg) {
         case 21: return launch_g4<FW, F16, 4, 2>(kp, map, n_units, stream);
-        case 22: return launch_g4<FW, F16, 1, 2>(kp, map, n_units, stream);
         default: return launch_g4<FW, F16, 2, 2>(kp, map, n_units, stream);
         }
     }
