@@ -596,11 +596,10 @@ __global__ void __launch_bounds__(WARPS * 32)
             vb0[slot] = p0 ? __float_as_uint(__ldg(vp + i0)) : 0u;
             vb1[slot] = p1 ? __float_as_uint(__ldg(vp + i1)) : 0u;
         } else {
+            // keep the two halves apart until the MMA: packing here would stall on the loads
             const unsigned short *vp = reinterpret_cast<const unsigned short *>(p.vals);
-            const uint32_t lo = p0 ? (uint32_t)__ldg(vp + i0) : 0u;
-            const uint32_t hi = p1 ? (uint32_t)__ldg(vp + i1) : 0u;
-            vb0[slot] = lo | (hi << 16);
-            vb1[slot] = 0u;
+            vb0[slot] = p0 ? (uint32_t)__ldg(vp + i0) : 0u;
+            vb1[slot] = p1 ? (uint32_t)__ldg(vp + i1) : 0u;
         }
     };
 
@@ -674,8 +673,13 @@ __global__ void __launch_bounds__(WARPS * 32)
                 fr.y[j] = *reinterpret_cast<const V *>(rb + 8 * CF::VB * j);
             }
             if constexpr (RND) round_frag<FW, F16>(fr);
-            fr.b0 = vb0[slot];
-            fr.b1 = vb1[slot];
+            if constexpr (F16) {
+                fr.b0 = vb0[slot] | (vb1[slot] << 16);
+                fr.b1 = 0u;
+            } else {
+                fr.b0 = vb0[slot];
+                fr.b1 = vb1[slot];
+            }
             mma_block<FW, F16>(acc, fr);
         }
     };
