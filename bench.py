@@ -28,12 +28,13 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 L2_FLUSH_BYTES = 256 << 20
+METRIC = "SpMM GFLOP/s (2\u00b7nnz\u00b7N/t) and achieved HBM GB/s vs peak at N=128, 1/2/4/8 B200"
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="reddit")
@@ -129,12 +130,12 @@ def make_inputs(args):
     return cfg, A, vals, B
 
 
-def cpu_oracle_sample(A, vals, B, precision, seconds, seed=0):
-    """The FP64 oracle as it stands, on the host cores, over a bounded random row sample."""
+def cpu_oracle_sample(A, vals, B, precision, seconds, seed=0, rounded=None):
+    """The FP64 oracle as it stands, on the host cores, over a bounded random row sample
+    (rho(A), rho(B) are computed once, outside the timed sample)."""
     from oracle import spmm as osp
     from oracle.rounding import rho
-    a = rho(vals, precision)
-    b = rho(B, precision)
+    a, b = rounded if rounded is not None else (rho(vals, precision), rho(B, precision))
     rng = np.random.default_rng(seed)
     nnz_row = np.diff(A.rowptr)
     N = B.shape[1]
@@ -155,18 +156,20 @@ def cpu_oracle_sample(A, vals, B, precision, seconds, seed=0):
 def run_reference(args, rank, world):
     if rank != 0:
         return
+    from oracle.rounding import rho
     cfg, A, vals, B = make_inputs(args)
+    rounded = (rho(vals, args.precision), rho(B, args.precision))
     steps = []
     info = None
-    per_step_seconds = max(0.5, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    per_step_seconds = max(0.25, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
     for i in range(args.warmup + args.steps):
-        cb, t = cpu_oracle_sample(A, vals, B, args.precision, per_step_seconds, seed=i)
+        cb, t = cpu_oracle_sample(A, vals, B, args.precision, per_step_seconds, seed=i, rounded=rounded)
         if i >= args.warmup:
             steps.append(cb["value"])
             info = cb
     value = statistics.median(steps)
     out = {
-        "impl": "reference", "metric": "SpMM GFLOP/s (2*nnz*N/t)", "value": value, "unit": "GFLOP/s",
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GFLOP/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(args, cfg, A, world),
@@ -294,6 +297,16 @@ def main():
             print(json.dumps({"profile_run": True, "ms_per_step": ms_per_step, "value": value}))
         return
 
+    # warm regime: the same steps back to back, no L2 flush in between
+    w0, w1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    w0.record(stream)
+    for _ in range(args.steps):
+        plan.execute(Bd, C, stream)
+    w1.record(stream)
+    torch.cuda.synchronize()
+    warm_ms = w0.elapsed_time(w1) / args.steps
+
     bm = acc.bytes_model(info, args.N)
     avg_s = float(np.mean(kernel_ms)) / 1e3 if len(kernel_ms) else t_local / args.steps
     peak, peak_kind = load_peaks()
@@ -333,7 +346,7 @@ def main():
 
     if rank == 0:
         out = {
-            "metric": "SpMM GFLOP/s (2*nnz*N/t)", "value": value, "unit": "GFLOP/s", "n_gpus": world,
+            "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
             "config": workload_config(args, cfg, A, world),
@@ -349,6 +362,8 @@ def main():
             "plan": {k: info[k] for k in ("W", "NB", "sum_U", "mean_nnz_tc", "ibd", "balanced", "unit_cap", "n_units",
                                           "n_split_windows", "n_segments", "reorder_applied", "ms_reorder",
                                           "ms_build", "ms_schedule", "ms_upload", "device_bytes")},
+            "warm": {"ms_per_step": warm_ms, "value": 2.0 * A.nnz * args.N / (warm_ms / 1e3) / 1e9 * world,
+                     "note": "back-to-back steps without the L2 flush (rank-local)"},
             "plan_create_s": plan_s, "broadcast_ms": bcast_ms, "wall_s_timed_loop": wall,
             "step_ms_min": min(step_ms), "step_ms_max": max(step_ms),
         }
