@@ -362,7 +362,7 @@ def main():
             "plan": {k: info[k] for k in ("W", "NB", "sum_U", "mean_nnz_tc", "ibd", "balanced", "unit_cap", "n_units",
                                           "n_split_windows", "n_segments", "reorder_applied", "ms_reorder",
                                           "ms_build", "ms_schedule", "ms_upload", "device_bytes")},
-            "warm": {"ms_per_step": warm_ms, "value": 2.0 * A.nnz * args.N / (warm_ms / 1e3) / 1e9 * world,
+            "warm": {"ms_per_step": warm_ms, "value": 2.0 * A.nnz * args.N / (warm_ms / 1e3) / 1e9,
                      "note": "back-to-back steps without the L2 flush (rank-local)"},
             "plan_create_s": plan_s, "broadcast_ms": bcast_ms, "wall_s_timed_loop": wall,
             "step_ms_min": min(step_ms), "step_ms_max": max(step_ms),
