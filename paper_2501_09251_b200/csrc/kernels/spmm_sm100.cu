@@ -521,8 +521,8 @@ __device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap *map
         : "memory");
 }
 
-template <int FW, bool F16, int WARPS, int STAGES, bool RND>
-__global__ void __launch_bounds__(WARPS * 32)
+template <int FW, bool F16, int WARPS, int STAGES, bool RND, int MINB = 1>
+__global__ void __launch_bounds__(WARPS * 32, MINB)
     spmm_bittcf_g4_kernel(const KParams p, const __grid_constant__ CUtensorMap tmap)
 {
     using CF = Cfg<FW, F16>;
@@ -831,12 +831,12 @@ int env_int(const char *name, int dflt)
     return s ? std::atoi(s) : dflt;
 }
 
-template <int FW, bool F16, int WARPS, int STAGES, bool RND = false>
+template <int FW, bool F16, int WARPS, int STAGES, bool RND = false, int MINB = 1>
 accspmm_status launch_g4(const KParams &kp, const CUtensorMap *map, int64_t n_units, cudaStream_t stream)
 {
     using SM = G4WarpSmem<FW, F16, STAGES>;
     const size_t smem = sizeof(SM) * WARPS;
-    auto kern = spmm_bittcf_g4_kernel<FW, F16, WARPS, STAGES, RND>;
+    auto kern = spmm_bittcf_g4_kernel<FW, F16, WARPS, STAGES, RND, MINB>;
     static int configured_device = -1;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -913,6 +913,7 @@ accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, 
         if (st != ACCSPMM_OK) return st;
         switch (kcfg) {
         case 21: return launch_g4<FW, F16, 4, 2>(kp, map, n_units, stream);
+        case 23: return launch_g4<FW, F16, 2, 2, false, 11>(kp, map, n_units, stream);
         default: return launch_g4<FW, F16, 2, 2>(kp, map, n_units, stream);
         }
     }
