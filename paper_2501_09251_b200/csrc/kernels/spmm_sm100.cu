@@ -521,7 +521,7 @@ __device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap *map
         : "memory");
 }
 
-template <int FW, bool F16, int WARPS, int STAGES, bool RND, int MINB = 1>
+template <int FW, bool F16, int WARPS, int STAGES, bool RND, int MINB = 1, int DIST = 1>
 __global__ void __launch_bounds__(WARPS * 32, MINB)
     spmm_bittcf_g4_kernel(const KParams p, const __grid_constant__ CUtensorMap tmap)
 {
@@ -577,9 +577,10 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
         cp_async_commit();
     };
 
-    // Value registers of the blocks in flight: decoded and loaded 2 blocks ahead of use
-    // (a 4-slot ring), so their L2 latency hides behind two block steps.
-    constexpr int VR = 4;
+    // Value registers of the blocks in flight: decoded and loaded DIST blocks ahead of use
+    // (a VR-slot register ring), so their L2 latency hides behind DIST block steps.
+    static_assert(DIST == 1 || DIST == 2, "value prefetch distance");
+    constexpr int VR = DIST == 1 ? 2 : 4;
     uint32_t vb0[VR], vb1[VR];
 
     // ---- every lane: decode this lane's two tile entries of block j, load values
@@ -722,31 +723,37 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
         }
     };
 
-    // Prologue: chunk 0 (wait) and chunk 1 in flight; values of blocks 0, 1; TMA of block 0.
+    // Prologue: chunk 0 (wait) and chunk 1 in flight; values of blocks 0..DIST-1; TMA of block 0.
     issue_chunk(0);
     cp_async_wait_all();
     __syncwarp();
     issue_chunk(kChunk);
     after_block(b0);
-    if (nblk > 0) value_load(0, 0);
-    if (nblk > 1) value_load(1, 1);
+#pragma unroll
+    for (int d = 0; d < DIST; ++d)
+        if ((uint32_t)d < nblk) value_load((uint32_t)d, d);
     if (nblk > 0) issue_tma(0, 0);
-    // Block step j: TMA for j+1 (chunk boundary: wait for the next chunk, prefetch the one
-    // after), values for j+2, then decode-free MMA of block j.  STAGES == 2 TMA stages.
+    // Block step j: TMA for j+1, values for j+DIST (at a chunk boundary first wait for that
+    // chunk and prefetch the one after), then the decode-free MMA of block j.
     static_assert(STAGES == 2, "the block step below is written for a 2-stage TMA ring");
     auto step = [&](uint32_t j, int u, bool checked) {
-        const uint32_t jt = j + 1, jv = j + 2;
-        if (!checked || jt < nblk) issue_tma(jt, (u + 1) & 1);
-        if ((jv & (kChunk - 1u)) == 0) {  // chunk (jv / kChunk) must have landed
+        const uint32_t jt = j + 1, jv = j + DIST;
+        if (DIST == 1 && (jv & (kChunk - 1u)) == 0) {  // chunk (jv / kChunk) must have landed
             cp_async_wait_all();
             __syncwarp();
             issue_chunk(jv + kChunk);
         }
-        if (!checked || jv < nblk) value_load(jv, (u + 2) & (VR - 1));
+        if (!checked || jt < nblk) issue_tma(jt, (u + 1) & 1);
+        if (DIST == 2 && (jv & (kChunk - 1u)) == 0) {
+            cp_async_wait_all();
+            __syncwarp();
+            issue_chunk(jv + kChunk);
+        }
+        if (!checked || jv < nblk) value_load(jv, (u + DIST) & (VR - 1));
         consume(j, u & 1, u & (VR - 1));
         after_block(b0 + j + 1);
     };
-    const uint32_t nmain = nblk >= 2u ? ((nblk - 2u) / VR) * VR : 0u;
+    const uint32_t nmain = nblk >= (uint32_t)DIST ? ((nblk - DIST) / VR) * VR : 0u;
     uint32_t j = 0;
     for (; j < nmain; j += VR) {
 #pragma unroll
@@ -831,12 +838,12 @@ int env_int(const char *name, int dflt)
     return s ? std::atoi(s) : dflt;
 }
 
-template <int FW, bool F16, int WARPS, int STAGES, bool RND = false, int MINB = 1>
+template <int FW, bool F16, int WARPS, int STAGES, bool RND = false, int MINB = 1, int DIST = 1>
 accspmm_status launch_g4(const KParams &kp, const CUtensorMap *map, int64_t n_units, cudaStream_t stream)
 {
     using SM = G4WarpSmem<FW, F16, STAGES>;
     const size_t smem = sizeof(SM) * WARPS;
-    auto kern = spmm_bittcf_g4_kernel<FW, F16, WARPS, STAGES, RND, MINB>;
+    auto kern = spmm_bittcf_g4_kernel<FW, F16, WARPS, STAGES, RND, MINB, DIST>;
     static int configured_device = -1;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -913,7 +920,9 @@ accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, 
         if (st != ACCSPMM_OK) return st;
         switch (kcfg) {
         case 21: return launch_g4<FW, F16, 4, 2>(kp, map, n_units, stream);
-        case 23: return launch_g4<FW, F16, 2, 2, false, 11>(kp, map, n_units, stream);
+        case 23: return launch_g4<FW, F16, 2, 2, false, 1, 2>(kp, map, n_units, stream);
+        case 24: return launch_g4<FW, F16, 2, 2, false, 10, 1>(kp, map, n_units, stream);
+        case 25: return launch_g4<FW, F16, 2, 2, false, 10, 2>(kp, map, n_units, stream);
         default: return launch_g4<FW, F16, 2, 2>(kp, map, n_units, stream);
         }
     }
