@@ -66,6 +66,12 @@ typedef enum {
     ACCSPMM_BALANCE_AUTO = 2  /* balance iff IBD (Eq. 3) > 8                                 */
 } accspmm_balance_mode;
 
+typedef enum {
+    ACCSPMM_BUILD_HOST = 0,   /* BitTCF built by the host builder (OpenMP over RowWindows), then uploaded */
+    ACCSPMM_BUILD_DEVICE = 1  /* CSR uploaded, BitTCF built by data-parallel device passes (sort + scans);
+                                 bit-identical arrays; needs device >= 0                             */
+} accspmm_build_mode;
+
 typedef struct {
     int32_t precision;  /* accspmm_precision; default ACCSPMM_TF32                                   */
     int32_t reorder;    /* accspmm_reorder_mode; default ACCSPMM_REORDER_OFF                         */
@@ -74,7 +80,8 @@ typedef struct {
     int32_t part;       /* this rank's part in [0, nparts)                                          */
     int32_t nparts;     /* number of nnz-balanced RowWindow ranges (multi-GPU); 1 = whole matrix    */
     int32_t device;     /* CUDA device ordinal; -1 = host-only plan (format + schedule, no upload)  */
-    int32_t reserved[9];
+    int32_t build;      /* accspmm_build_mode; default ACCSPMM_BUILD_HOST                            */
+    int32_t reserved[8];
 } accspmm_options;
 
 typedef struct {

@@ -23,6 +23,7 @@ TF32, FP16 = 0, 1
 REORDER = {"off": 0, "on": 1, "auto": 2}
 BALANCE = {"off": 0, "on": 1, "auto": 2}
 PRECISION = {"tf32": TF32, "fp16": FP16}
+BUILD = {"host": 0, "device": 1}
 NO_SPLIT = 0xFFFFFFFF
 
 
@@ -35,7 +36,7 @@ class AccSpmmError(RuntimeError):
 class accspmm_options(ctypes.Structure):
     _fields_ = [("precision", ctypes.c_int32), ("reorder", ctypes.c_int32), ("balance", ctypes.c_int32),
                 ("unit_cap", ctypes.c_int32), ("part", ctypes.c_int32), ("nparts", ctypes.c_int32),
-                ("device", ctypes.c_int32), ("reserved", ctypes.c_int32 * 9)]
+                ("device", ctypes.c_int32), ("build", ctypes.c_int32), ("reserved", ctypes.c_int32 * 8)]
 
 
 _I64 = ["M", "K", "nnz", "rows", "row_begin", "window_begin", "W", "NB", "plan_nnz", "sum_U", "n_units",
@@ -264,8 +265,9 @@ class Plan:
     TF32 / float16 for FP16) and returns / fills C (float32)."""
 
     def __init__(self, M, K, rowptr, colidx, vals, precision="tf32", reorder="off", balance="auto",
-                 unit_cap=0, part=0, nparts=1, device=None):
+                 unit_cap=0, part=0, nparts=1, device=None, build="host"):
         opt = accspmm_options_default()
+        opt.build = BUILD[build]
         opt.precision = PRECISION[precision]
         opt.reorder = REORDER[reorder]
         opt.balance = BALANCE[balance]

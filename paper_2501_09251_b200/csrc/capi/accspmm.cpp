@@ -141,6 +141,10 @@ accspmm_status accspmm_plan_create_ex(int64_t M, int64_t K, const int64_t *rowpt
     if (opt.nparts < 1 || opt.part < 0 || opt.part >= opt.nparts)
         return fail(ACCSPMM_ERR_INVALID_VALUE, "part must be in [0, nparts)");
     if (opt.unit_cap < 0) return fail(ACCSPMM_ERR_INVALID_VALUE, "unit_cap < 0");
+    if (opt.build != ACCSPMM_BUILD_HOST && opt.build != ACCSPMM_BUILD_DEVICE)
+        return fail(ACCSPMM_ERR_INVALID_VALUE, "unknown build mode");
+    if (opt.build == ACCSPMM_BUILD_DEVICE && opt.device < 0)
+        return fail(ACCSPMM_ERR_UNSUPPORTED, "device build needs a device (device >= 0)");
     if (M < 0 || K < 0) return fail(ACCSPMM_ERR_INVALID_VALUE, "negative matrix dimension");
     if (M >= (int64_t)UINT32_MAX || K >= (int64_t)INT32_MAX)
         return fail(ACCSPMM_ERR_UNSUPPORTED, "M or K too large for 32-bit indices");
@@ -191,8 +195,20 @@ accspmm_status accspmm_plan_create_ex(int64_t M, int64_t K, const int64_t *rowpt
     }
     const int64_t r0 = wb0 * kWindow, r1 = std::min<int64_t>(M, wb1 * kWindow);
     HostFormat &F = p->host;
-    st = build_format(a, vals, perm, r0, std::max(r0, r1), opt.precision, F);
-    if (st != ACCSPMM_OK) { delete p; return st; }
+    DeviceFormat DF;
+    double ms_csr_upload = 0.0;
+    if (opt.build == ACCSPMM_BUILD_DEVICE) {
+        cudaError_t e = cudaSetDevice(opt.device);
+        if (e != cudaSuccess) { delete p; return cuda_fail(e, "cudaSetDevice"); }
+        st = build_format_device(a, vals, perm, r0, std::max(r0, r1), opt.precision, DF);
+        if (st != ACCSPMM_OK) { free_device_format(DF); delete p; return st; }
+        F.W = DF.W; F.NB = DF.NB; F.nnz = DF.nnz; F.rows = DF.rows; F.sum_U = DF.sum_U;
+        F.rwo = DF.rwo_host;
+        ms_csr_upload = DF.ms_upload;
+    } else {
+        st = build_format(a, vals, perm, r0, std::max(r0, r1), opt.precision, F);
+        if (st != ACCSPMM_OK) { delete p; return st; }
+    }
     if (I.nb_unreordered < 0 && opt.nparts == 1 && perm.empty()) I.nb_unreordered = F.NB;
     I.rows = F.rows; I.row_begin = r0; I.window_begin = wb0;
     I.W = F.W; I.NB = F.NB; I.plan_nnz = F.nnz; I.sum_U = F.sum_U;
@@ -205,7 +221,7 @@ accspmm_status accspmm_plan_create_ex(int64_t M, int64_t K, const int64_t *rowpt
     for (int64_t r = 0; r < F.rows; ++r)
         p->orig_rows[(size_t)r] = perm.empty() ? (uint32_t)(r0 + r) : perm[(size_t)(r0 + r)];
     I.perm_present = perm.empty() ? 0 : 1;
-    I.ms_build = ms_since(t0);
+    I.ms_build = opt.build == ACCSPMM_BUILD_DEVICE ? DF.ms_build : ms_since(t0);
 
     // ---- IBD + schedule ----
     t0 = std::chrono::steady_clock::now();
@@ -229,9 +245,17 @@ accspmm_status accspmm_plan_create_ex(int64_t M, int64_t K, const int64_t *rowpt
         d.W = F.W; d.NB = F.NB; d.nnz = F.nnz; d.rows = F.rows; d.n_units = I.n_units;
         d.n_split = S.n_split; d.n_segments = S.n_segments; d.precision = opt.precision; d.K = K;
         int64_t bytes = 0;
-        st = upload(&d.rwo, F.rwo, bytes);
-        if (st == ACCSPMM_OK) st = upload(&d.tco, F.tco, bytes);
-        if (st == ACCSPMM_OK) {
+        if (opt.build == ACCSPMM_BUILD_DEVICE) {  // format already resident: take ownership
+            d.rwo = DF.rwo; d.tco = DF.tco; d.a2b = DF.a2b; d.bits = DF.bits; d.vals = DF.vals;
+            DF.rwo = DF.tco = DF.a2b = nullptr; DF.bits = nullptr; DF.vals = nullptr;
+            const int64_t es = opt.precision == ACCSPMM_FP16 ? 2 : 4;
+            bytes += 4 * (F.W + 1) + 4 * (F.NB + 1) + 32 * std::max<int64_t>(F.NB, 1) + 8 * std::max<int64_t>(F.NB, 1) +
+                     es * (F.nnz + 16);
+        } else {
+            st = upload(&d.rwo, F.rwo, bytes);
+            if (st == ACCSPMM_OK) st = upload(&d.tco, F.tco, bytes);
+        }
+        if (st == ACCSPMM_OK && opt.build != ACCSPMM_BUILD_DEVICE) {
             // device copy: padding lanes (no bit in the block's column-OR) hold 0xFFFFFFFF, an
             // out-of-bounds row the TMA zero-fills; the exported paper format keeps 0
             std::vector<uint32_t> a2b_dev(F.a2b);
@@ -246,8 +270,8 @@ accspmm_status accspmm_plan_create_ex(int64_t M, int64_t K, const int64_t *rowpt
             }
             st = upload(&d.a2b, a2b_dev, bytes);
         }
-        if (st == ACCSPMM_OK) st = upload(&d.bits, F.bits, bytes);
-        if (st == ACCSPMM_OK) {
+        if (st == ACCSPMM_OK && opt.build != ACCSPMM_BUILD_DEVICE) st = upload(&d.bits, F.bits, bytes);
+        if (st == ACCSPMM_OK && opt.build != ACCSPMM_BUILD_DEVICE) {
             if (opt.precision == ACCSPMM_FP16) st = upload((uint16_t **)&d.vals, F.v16, bytes, 16);
             else st = upload((float **)&d.vals, F.v32, bytes, 16);
         }
@@ -264,7 +288,7 @@ accspmm_status accspmm_plan_create_ex(int64_t M, int64_t K, const int64_t *rowpt
         empty.W = F.W; empty.NB = F.NB; empty.nnz = F.nnz; empty.rows = F.rows; empty.sum_U = F.sum_U;
         F = std::move(empty);
     }
-    I.ms_upload = ms_since(t0);
+    I.ms_upload = ms_since(t0) + ms_csr_upload;
     *out = p;
     return ACCSPMM_OK;
 }
@@ -274,7 +298,7 @@ static accspmm_status ensure_workspace(const accspmm_plan *p, int64_t N)
     const auto &d = p->dev;
     if (d.n_split == 0) return ACCSPMM_OK;
     size_t need_ws = (size_t)d.n_segments * (size_t)N * 8 * sizeof(float);
-    int64_t fw = N % 128 == 0 ? 128 : N % 64 == 0 ? 64 : N % 32 == 0 ? 32 : 16;
+    const int64_t fw = pick_fw(N);
     size_t need_cnt = (size_t)d.n_split * (size_t)(N / fw);
     if (need_ws > p->ws_bytes) {
         cudaFree(p->ws);

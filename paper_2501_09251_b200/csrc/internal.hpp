@@ -83,6 +83,25 @@ struct DevicePlan {
     alignas(64) mutable unsigned char tmap[128] = {};
 };
 
+// kernels/build_sm100.cu -- the same BitTCF arrays built by data-parallel device passes
+// (SparseAToB padding lanes already hold kPadLane); rwo_host = RowWindowOffset for the
+// host-side schedule.  On failure the caller frees what was allocated (free_device_format).
+struct DeviceFormat {
+    int64_t W = 0, NB = 0, nnz = 0, rows = 0, sum_U = 0;
+    uint32_t *rwo = nullptr, *tco = nullptr, *a2b = nullptr;
+    uint64_t *bits = nullptr;
+    void *vals = nullptr;
+    std::vector<uint32_t> rwo_host;
+    double ms_upload = 0.0, ms_build = 0.0;
+};
+accspmm_status build_format_device(const Csr &a, const float *vals, const std::vector<uint32_t> &perm,
+                                   int64_t row_begin, int64_t row_end, int precision, DeviceFormat &out);
+void free_device_format(DeviceFormat &f);
+
+// Feature-slice width of one warp for a given N (N % 16 == 0): the widest of 128/64/32/16
+// dividing N.  ACCSPMM_FW (16/32/64/128, must divide N) overrides it for A/B measurements.
+int pick_fw(int64_t N);
+
 // round_b: the kernel applies rho(B) in registers (B not pre-rounded)
 accspmm_status launch_spmm(const DevicePlan &p, const void *B, const void *zrow, int64_t N, float *C, float *ws,
                            uint32_t *counters, void *stream, bool round_b);

@@ -63,6 +63,11 @@ __device__ __forceinline__ void cp_async4(uint32_t dst, const void *src, uint64_
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+// bulk L2 prefetch of [p, p+bytes) (p and bytes multiples of 16)
+__device__ __forceinline__ void prefetch_l2_bulk(const void *p, uint32_t bytes)
+{
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
+}
 
 __device__ __forceinline__ uint64_t policy_evict_last()
 {
@@ -158,7 +163,7 @@ constexpr int kChunk = 16;  // TC blocks per staged A-stream chunk
 struct ChunkSmem {
     uint32_t a2b[kChunk * 8];
     uint64_t mask[kChunk];
-    uint32_t tco[kChunk];
+    uint32_t tco[kChunk + 4];   // TCOffset of the chunk's blocks plus the end offset (value range)
 };
 
 struct WarpSmem {
@@ -497,7 +502,9 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase)
 template <int FW, bool F16>
 struct G4Cfg {
     using CF = Cfg<FW, F16>;
-    static constexpr int BOXE = FW + 8;                      // box width in elements
+    // box width in elements: gathered rows then sit 32 B off a 128-byte bank period, so the
+    // fragment LDS.128 of one 8-lane phase (4 rows x 2 column groups) hits 8 distinct bank groups
+    static constexpr int BOXE = FW + 32 / CF::ES;
     static constexpr int RS = BOXE * CF::ES;                 // gathered row stride in smem
     static constexpr int GRP = (4 * RS + 127) / 128 * 128;   // one gather4 (4 rows), 128-aligned
     static constexpr int STAGE_AL = 2 * GRP;
@@ -521,7 +528,7 @@ __device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap *map
         : "memory");
 }
 
-template <int FW, bool F16, int WARPS, int STAGES, bool RND, int MINB = 1, int DIST = 1>
+template <int FW, bool F16, int WARPS, int STAGES, bool RND, int MINB = 1, int DIST = 1, bool PF = false>
 __global__ void __launch_bounds__(WARPS * 32, MINB)
     spmm_bittcf_g4_kernel(const KParams p, const __grid_constant__ CUtensorMap tmap)
 {
@@ -566,15 +573,24 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
             ChunkSmem &c = sm.ch[(i / kChunk) & 1];
             const uint32_t b = b0 + i;
             const uint32_t cnt = min((uint32_t)kChunk, nblk - i);
-            if ((uint32_t)lane < cnt) {
-                cp_async8(smem_u32(&c.mask[lane]), p.bits + b + lane, pol_stream);
-                cp_async4(smem_u32(&c.tco[lane]), p.tco + b + lane, pol_stream);
-            }
+            if ((uint32_t)lane < cnt) cp_async8(smem_u32(&c.mask[lane]), p.bits + b + lane, pol_stream);
+            if ((uint32_t)lane <= cnt) cp_async4(smem_u32(&c.tco[lane]), p.tco + b + lane, pol_stream);
             const uint4 *src4 = reinterpret_cast<const uint4 *>(p.a2b + (size_t)b * 8);
             if ((uint32_t)lane < 2 * cnt) cp_async16(smem_u32(&c.a2b[4 * lane]), src4 + lane, pol_stream);
             if ((uint32_t)lane + 32 < 2 * cnt) cp_async16(smem_u32(&c.a2b[4 * (lane + 32)]), src4 + lane + 32, pol_stream);
         }
         cp_async_commit();
+    };
+    // Lane 0: bulk L2 prefetch of the values of the staged chunk starting at block i (its
+    // TCOffset range is contiguous), so the per-lane value loads of its blocks hit L2.
+    auto prefetch_values = [&](uint32_t i) {
+        if (lane == 0 && i < nblk) {
+            const ChunkSmem &c = sm.ch[(i / kChunk) & 1];
+            const uint32_t cnt = min((uint32_t)kChunk, nblk - i);
+            constexpr uint32_t ES = CF::ES;
+            const uint32_t lo = (c.tco[0] * ES) & ~15u, hi = (c.tco[cnt] * ES + 15u) & ~15u;
+            if (hi > lo) prefetch_l2_bulk(reinterpret_cast<const char *>(p.vals) + lo, hi - lo);
+        }
     };
 
     // Value registers of the blocks in flight: decoded and loaded DIST blocks ahead of use
@@ -728,6 +744,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     cp_async_wait_all();
     __syncwarp();
     issue_chunk(kChunk);
+    if constexpr (PF) prefetch_values(0);
     after_block(b0);
 #pragma unroll
     for (int d = 0; d < DIST; ++d)
@@ -742,6 +759,11 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
             cp_async_wait_all();
             __syncwarp();
             issue_chunk(jv + kChunk);
+        }
+        if (PF && (jv & (kChunk - 1u)) == kChunk / 2) {  // mid-chunk: the next chunk has landed
+            cp_async_wait_all();
+            __syncwarp();
+            prefetch_values((jv | (kChunk - 1u)) + 1u);
         }
         if (!checked || jt < nblk) issue_tma(jt, (u + 1) & 1);
         if (DIST == 2 && (jv & (kChunk - 1u)) == 0) {
@@ -838,17 +860,20 @@ int env_int(const char *name, int dflt)
     return s ? std::atoi(s) : dflt;
 }
 
-template <int FW, bool F16, int WARPS, int STAGES, bool RND = false, int MINB = 1, int DIST = 1>
+template <int FW, bool F16, int WARPS, int STAGES, bool RND = false, int MINB = 1, int DIST = 1, bool PF = false>
 accspmm_status launch_g4(const KParams &kp, const CUtensorMap *map, int64_t n_units, cudaStream_t stream)
 {
     using SM = G4WarpSmem<FW, F16, STAGES>;
     const size_t smem = sizeof(SM) * WARPS;
-    auto kern = spmm_bittcf_g4_kernel<FW, F16, WARPS, STAGES, RND, MINB, DIST>;
+    auto kern = spmm_bittcf_g4_kernel<FW, F16, WARPS, STAGES, RND, MINB, DIST, PF>;
     static int configured_device = -1;
     int dev = 0;
     cudaGetDevice(&dev);
     if (configured_device != dev) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return fail(ACCSPMM_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+        // the whole unified L1/shared array as shared memory: occupancy is smem-limited
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         if (e != cudaSuccess) return fail(ACCSPMM_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
         configured_device = dev;
     }
@@ -880,7 +905,7 @@ accspmm_status tensor_map(const DevicePlan &d, const void *B, int64_t N, int FW,
         const cuuint64_t es = f16 ? 2 : 4;
         cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)d.K};
         cuuint64_t strides[1] = {(cuuint64_t)N * es};
-        cuuint32_t box[2] = {(cuuint32_t)(FW + 8), 1u};
+        cuuint32_t box[2] = {(cuuint32_t)(FW + (f16 ? 16 : 8)), 1u};  // G4Cfg::BOXE
         cuuint32_t estr[2] = {1u, 1u};
         CUresult r = encode(m, f16 ? CU_TENSOR_MAP_DATA_TYPE_UINT16 : CU_TENSOR_MAP_DATA_TYPE_UINT32, 2,
                             const_cast<void *>(B), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -909,7 +934,12 @@ accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, 
                 const CUtensorMap *map = nullptr;
                 accspmm_status st = tensor_map(d, B, kp.N, FW, &map);
                 if (st != ACCSPMM_OK) return st;
-                return launch_g4<FW, F16, 2, 2, true>(kp, map, n_units, stream);
+                switch (kcfg) {
+                case 24: return launch_g4<FW, F16, 2, 2, true, 10>(kp, map, n_units, stream);
+                case 31: return launch_g4<FW, F16, 2, 2, true, 12>(kp, map, n_units, stream);
+                case 33: return launch_g4<FW, F16, 2, 2, true, 16>(kp, map, n_units, stream);
+                default: return launch_g4<FW, F16, 2, 2, true>(kp, map, n_units, stream);
+                }
             }
             return launch_cfg<FW, F16, 2, true>(kp, n_units, stream);
         }
@@ -923,6 +953,12 @@ accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, 
         case 23: return launch_g4<FW, F16, 2, 2, false, 1, 2>(kp, map, n_units, stream);
         case 24: return launch_g4<FW, F16, 2, 2, false, 10, 1>(kp, map, n_units, stream);
         case 25: return launch_g4<FW, F16, 2, 2, false, 10, 2>(kp, map, n_units, stream);
+        case 26: return launch_g4<FW, F16, 2, 2, false, 1, 1, true>(kp, map, n_units, stream);
+        case 27: return launch_g4<FW, F16, 2, 2, false, 10, 1, true>(kp, map, n_units, stream);
+        case 28: return launch_g4<FW, F16, 2, 2, false, 10, 2, true>(kp, map, n_units, stream);
+        case 31: return launch_g4<FW, F16, 2, 2, false, 12, 1>(kp, map, n_units, stream);
+        case 32: return launch_g4<FW, F16, 2, 2, false, 14, 1>(kp, map, n_units, stream);
+        case 33: return launch_g4<FW, F16, 2, 2, false, 16, 1>(kp, map, n_units, stream);
         default: return launch_g4<FW, F16, 2, 2>(kp, map, n_units, stream);
         }
     }
@@ -935,6 +971,13 @@ accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, 
 }
 
 }  // namespace
+
+int pick_fw(int64_t N)
+{
+    const int f = env_int("ACCSPMM_FW", 0);
+    if ((f == 16 || f == 32 || f == 64 || f == 128) && N % f == 0) return f;
+    return N % 128 == 0 ? 128 : N % 64 == 0 ? 64 : N % 32 == 0 ? 32 : 16;
+}
 
 accspmm_status launch_round_b(const float *B, float *Br, int64_t n, void *stream)
 {
@@ -953,7 +996,7 @@ accspmm_status launch_spmm(const DevicePlan &d, const void *B, const void *zrow,
                            uint32_t *counters, void *stream, bool round_b)
 {
     if (d.rows == 0) return ACCSPMM_OK;
-    const int FW = N % 128 == 0 ? 128 : N % 64 == 0 ? 64 : N % 32 == 0 ? 32 : 16;
+    const int FW = pick_fw(N);
     KParams kp;
     kp.rwo = d.rwo;
     kp.tco = d.tco;

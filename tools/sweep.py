@@ -1,7 +1,7 @@
 """Tuning sweep (GPU box): one matrix, many plan/kernel variants, CUDA-event timing per variant.
 
 usage: python tools/sweep.py --config reddit --N 128 --variants 'kcfg=0' 'kcfg=1,cap=256' ...
-variant keys: kcfg (ACCSPMM_KCFG), cap, balance, reorder, precision, N
+variant keys: kcfg (ACCSPMM_KCFG), fw (ACCSPMM_FW), cap, balance, reorder, precision, N
 """
 import argparse
 import json
@@ -36,6 +36,7 @@ def main():
         N = int(kv.get("N", a.N))
         prec = kv.get("precision", "tf32")
         os.environ["ACCSPMM_KCFG"] = kv.get("kcfg", "-1")
+        os.environ["ACCSPMM_FW"] = kv.get("fw", "0")
         key = (prec, kv.get("balance", "auto"), int(kv.get("cap", 0)), kv.get("reorder", "off"))
         if key not in plans:
             t0 = time.perf_counter()
