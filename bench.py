@@ -312,6 +312,9 @@ def main():
     peak, peak_kind = load_peaks()
     achieved = bm["total"] / avg_s / 1e9
     traffic = load_traffic(f"{args.config}-N{args.N}-{args.precision}-{args.reorder}-{args.balance}-p{world}")
+    # L2 roofline: every model byte (gathered B rows, A stream, C) passes through L2, and on
+    # graphs whose B fits L2 the gather is served from there -- the binding resource
+    l2_peak = acc.accspmm_probe_l2_bandwidth(64 << 20, 40)
 
     # ---- end to end through the public API with pinned host buffers (H2D B + execute + D2H C)
     e2e = None
@@ -354,7 +357,9 @@ def main():
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                          "bytes_model_per_launch": bm, "frac_of_8TBps_spec": achieved / 8000.0,
                          "kernel": kernel_name(args), "launch_ms": avg_s * 1e3,
-                         "kernel_share_of_step": avg_s * args.steps / t_local},
+                         "kernel_share_of_step": avg_s * args.steps / t_local,
+                         "l2": {"achieved": achieved, "peak": l2_peak, "unit": "GB/s", "frac": achieved / l2_peak,
+                                "peak_kind": "measured live: accspmm_probe_l2_bandwidth (64 MiB, ld.global.cg)"}},
             "cpu_baseline": cpu,
             "clocks": clk,
             "e2e": e2e,

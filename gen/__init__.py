@@ -13,6 +13,9 @@ from .matrices import (  # noqa: F401
     banded_random,
     dcsbm,
     powerlaw_directed,
+    road_grid,
+    molecules,
+    web_hosts,
     sbm,
     identity,
     permutation_matrix,

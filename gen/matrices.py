@@ -175,6 +175,80 @@ def powerlaw_directed(n: int, mean_deg: float, seed: int, mu: float = 2.3, sigma
     return Csr(n, n, rowptr, colidx)
 
 
+def road_grid(side: int, keep: float, seed: int, shuffle: bool = True) -> Csr:
+    """roadNet-shaped (PAPER Table 1 type-1, rCA/rPA, AvgL ~2.8): the side x side 4-neighbour
+    grid, each undirected edge kept with probability ``keep`` (grid degree 4 -> AvgL ~4*keep),
+    symmetric, no self-loops; labels shuffled unless ``shuffle`` is False."""
+    rng = np.random.default_rng(seed)
+    n = side * side
+    idx = np.arange(n, dtype=np.int64)
+    x, y = idx % side, idx // side
+    right = idx[x + 1 < side]
+    down = idx[y + 1 < side]
+    src = np.concatenate([right, down])
+    dst = np.concatenate([right + 1, down + side])
+    k = rng.random(src.size) < keep
+    src, dst = src[k], dst[k]
+    if shuffle:
+        lab = rng.permutation(n).astype(np.int64)
+        src, dst = lab[src], lab[dst]
+    return csr_from_pairs(src, dst, n, n, symmetric=True, drop_diag=True)
+
+
+def molecules(n_graphs: int, mean_nodes: float, extra_edge_frac: float, seed: int, window: int = 0) -> Csr:
+    """Graph-classification-shaped (PAPER Table 1 type-1: YeastH/OVCAR-8H/Yeast AvgL ~2.1, DD
+    AvgL ~5): a block-diagonal union of ``n_graphs`` small graphs with consecutive ids (as in
+    the TU datasets).  Each graph: a random recursive tree (node i joins a random earlier node,
+    within the previous ``window`` nodes if window > 0) plus extra_edge_frac * size random
+    chords (rings / contacts); symmetric, no self-loops."""
+    rng = np.random.default_rng(seed)
+    sizes = np.maximum(2, rng.poisson(mean_nodes - 2, n_graphs) + 2).astype(np.int64)
+    off = np.concatenate([[0], np.cumsum(sizes)])
+    n = int(off[-1])
+    g = np.repeat(np.arange(n_graphs), sizes)
+    local = np.arange(n, dtype=np.int64) - off[g]
+    child = np.nonzero(local > 0)[0]
+    lo = np.zeros(child.size, np.int64) if window <= 0 else np.maximum(0, local[child] - window)
+    parent_local = lo + np.floor(rng.random(child.size) * (local[child] - lo)).astype(np.int64)
+    src = [child, off[g[child]] + parent_local]
+    n_extra = int(extra_edge_frac * n)
+    eg = rng.integers(0, n_graphs, n_extra)
+    a = off[eg] + np.floor(rng.random(n_extra) * sizes[eg]).astype(np.int64)
+    if window > 0:
+        b = np.clip(a + rng.integers(-window, window + 1, n_extra), off[eg], off[eg + 1] - 1)
+    else:
+        b = off[eg] + np.floor(rng.random(n_extra) * sizes[eg]).astype(np.int64)
+    rows = np.concatenate([src[0], a])
+    cols = np.concatenate([src[1], b])
+    return csr_from_pairs(rows, cols, n, n, symmetric=True, drop_diag=True)
+
+
+def web_hosts(n: int, mean_deg: float, local_frac: float, seed: int, mean_host: float = 2000.0) -> Csr:
+    """web-BerkStan-shaped (PAPER Table 1 type-1, AvgL 11.09): directed; pages in host blocks of
+    consecutive ids (sizes 1 + Lomax(1.5) scaled to ``mean_host``); out-degree lognormal
+    rescaled to ``mean_deg``; a link stays in its host with probability ``local_frac``
+    (uniform there), else goes to a global page ~ Cat(1 + Lomax(1.2)); dedup per row."""
+    rng = np.random.default_rng(seed)
+    hs = 1.0 + rng.pareto(1.5, size=max(1, int(2 * n / mean_host)))
+    hs = np.maximum(1, np.round(hs * mean_host / hs.mean())).astype(np.int64)
+    hs = hs[np.cumsum(hs) <= n]
+    hs = np.append(hs, n - hs.sum()) if hs.sum() < n else hs
+    hoff = np.concatenate([[0], np.cumsum(hs)])
+    host = np.repeat(np.arange(hs.size), hs)
+    d = rng.lognormal(1.8, 1.0, n)
+    deg = np.minimum(np.round(d * mean_deg / d.mean()).astype(np.int64), 5000)
+    src = np.repeat(np.arange(n, dtype=np.int64), deg)
+    loc = rng.random(src.size) < local_frac
+    h = host[src]
+    dst = np.empty(src.size, np.int64)
+    dst[loc] = hoff[h[loc]] + np.floor(rng.random(int(loc.sum())) * hs[h[loc]]).astype(np.int64)
+    pop = 1.0 + rng.pareto(1.2, size=n)
+    cdf = np.cumsum(pop)
+    cdf /= cdf[-1]
+    dst[~loc] = np.minimum(np.searchsorted(cdf, rng.random(int((~loc).sum()))), n - 1)
+    return csr_from_pairs(src, dst, n, n)
+
+
 def sbm(n: int, blocks: int, p_in: float, p_out: float, seed: int, shuffle: bool = True) -> Csr:
     """Symmetric 0/1 stochastic block model, no self-loops, optional label shuffle."""
     rng = np.random.default_rng(seed)

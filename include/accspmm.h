@@ -198,6 +198,13 @@ accspmm_status accspmm_unpermute(const float *G, const uint32_t *orig_row, int64
 accspmm_status accspmm_debug_round_tf32(const float *in, float *out, int64_t n, void *stream);
 accspmm_status accspmm_debug_decode(const accspmm_plan *plan, float *tiles, void *stream);
 
+/* Measurement hook (device, synchronous): L2 read bandwidth of the current device in
+ * GB/s.  Allocates an L2-resident buffer of `bytes` (>= 1 MiB; well under the 126 MB L2),
+ * warms it, then times `iters` full passes of 128-bit L2-only loads (ld.global.cg) by all
+ * SMs with CUDA events.  The SpMM kernel's B-row gathers are served from L2 on graphs
+ * whose B fits there, so this is the roofline denominator of its L2 bytes (bench.py). */
+accspmm_status accspmm_probe_l2_bandwidth(int64_t bytes, int32_t iters, double *gbs);
+
 const char *accspmm_status_string(accspmm_status s);
 const char *accspmm_last_error(void);
 int32_t accspmm_abi_version(void);

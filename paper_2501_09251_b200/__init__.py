@@ -64,6 +64,7 @@ EXPORTED = [
     "accspmm_plan_export_units", "accspmm_plan_export_rows", "accspmm_reorder", "accspmm_partition_bounds",
     "accspmm_unpermute", "accspmm_debug_round_tf32", "accspmm_debug_decode", "accspmm_status_string",
     "accspmm_last_error", "accspmm_abi_version", "accspmm_plan_set_timing", "accspmm_plan_kernel_times",
+    "accspmm_probe_l2_bandwidth",
 ]
 
 
@@ -99,6 +100,7 @@ def load_library(path: str = LIB_PATH):
         "accspmm_abi_version": ([], I32),
         "accspmm_plan_set_timing": ([P, I32], S),
         "accspmm_plan_kernel_times": ([P, P, I32, ctypes.POINTER(I32)], S),
+        "accspmm_probe_l2_bandwidth": ([I64, I32, ctypes.POINTER(ctypes.c_double)], S),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -237,6 +239,12 @@ def accspmm_plan_kernel_times(plan, max_n: int = 4096) -> np.ndarray:
     n = ctypes.c_int32()
     _check(load_library().accspmm_plan_kernel_times(plan, _ptr(out), int(max_n), ctypes.byref(n)))
     return out[:n.value].copy()
+
+
+def accspmm_probe_l2_bandwidth(nbytes: int = 64 << 20, iters: int = 50) -> float:
+    g = ctypes.c_double()
+    _check(load_library().accspmm_probe_l2_bandwidth(int(nbytes), int(iters), ctypes.byref(g)))
+    return g.value
 
 
 def accspmm_status_string(s: int) -> str:

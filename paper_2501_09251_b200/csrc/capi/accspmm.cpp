@@ -531,6 +531,12 @@ accspmm_status accspmm_debug_decode(const accspmm_plan *p, float *tiles, void *s
     return launch_decode(p->dev, tiles, stream);
 }
 
+accspmm_status accspmm_probe_l2_bandwidth(int64_t bytes, int32_t iters, double *gbs)
+{
+    if (bytes < (1 << 20) || iters < 1 || !gbs) return fail(ACCSPMM_ERR_INVALID_VALUE, "bad argument");
+    return probe_l2_read(bytes & ~(int64_t)15, iters, gbs);
+}
+
 const char *accspmm_status_string(accspmm_status s)
 {
     switch (s) {

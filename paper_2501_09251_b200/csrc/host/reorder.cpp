@@ -15,6 +15,8 @@
 // Reading R6b: after a visit, a community passes on at most its 256
 // heaviest neighbour-community edges, so chains of merges on meshes stay O(m).
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <numeric>
 
@@ -31,6 +33,20 @@ int env_or(const char *name, int dflt)
     const char *s = std::getenv(name);
     return s ? std::atoi(s) : dflt;
 }
+
+// ACCSPMM_TRACE=1: phase times of the reordering on stderr
+struct Trace {
+    bool on = env_or("ACCSPMM_TRACE", 0) != 0;
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    void mark(const char *what)
+    {
+        if (!on) return;
+        auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[accspmm reorder] %-28s %9.1f ms\n", what,
+                     std::chrono::duration<double, std::milli>(now - t).count());
+        t = now;
+    }
+};
 constexpr size_t kEdgeCap = 256;  // community edges carried up a merge (reading R6b)
 
 struct Graph {
@@ -38,9 +54,42 @@ struct Graph {
     std::vector<uint32_t> adj;
 };
 
+// pattern(A or A^T) without the diagonal, as sorted unique adjacency lists.  A
+// structurally symmetric A (the graph workloads) is its own affinity graph: checked in
+// parallel by binary search, then copied without the diagonal.  Otherwise A and A^T are
+// merged by a counting scatter and every list is sorted and deduplicated.
 Graph affinity_graph(const Csr &a)
 {
     const int64_t n = a.M;
+    bool sym = true;
+#pragma omp parallel for schedule(dynamic, 1024) reduction(&& : sym)
+    for (int64_t i = 0; i < n; ++i) {
+        if (!sym) continue;
+        for (int64_t p = a.rowptr[i]; p < a.rowptr[i + 1] && sym; ++p) {
+            const int64_t j = a.colidx[p];
+            if (j == i) continue;
+            const int32_t *b = a.colidx + a.rowptr[j], *e = a.colidx + a.rowptr[j + 1];
+            sym = std::binary_search(b, e, (int32_t)i);
+        }
+    }
+    Graph g;
+    g.ptr.assign((size_t)n + 1, 0);
+    if (sym) {
+#pragma omp parallel for schedule(static)
+        for (int64_t i = 0; i < n; ++i) {
+            const int32_t *b = a.colidx + a.rowptr[i], *e = a.colidx + a.rowptr[i + 1];
+            g.ptr[(size_t)i + 1] = (e - b) - (std::binary_search(b, e, (int32_t)i) ? 1 : 0);
+        }
+        for (int64_t i = 0; i < n; ++i) g.ptr[(size_t)i + 1] += g.ptr[(size_t)i];
+        g.adj.resize((size_t)g.ptr[(size_t)n]);
+#pragma omp parallel for schedule(dynamic, 1024)
+        for (int64_t i = 0; i < n; ++i) {
+            size_t q = (size_t)g.ptr[(size_t)i];
+            for (int64_t p = a.rowptr[i]; p < a.rowptr[i + 1]; ++p)
+                if (a.colidx[p] != i) g.adj[q++] = (uint32_t)a.colidx[p];
+        }
+        return g;
+    }
     std::vector<int64_t> cnt((size_t)n + 1, 0);
     for (int64_t i = 0; i < n; ++i)
         for (int64_t p = a.rowptr[i]; p < a.rowptr[i + 1]; ++p) {
@@ -59,8 +108,6 @@ Graph affinity_graph(const Csr &a)
             tmp[(size_t)fill[(size_t)i]++] = (uint32_t)j;
             tmp[(size_t)fill[(size_t)j]++] = (uint32_t)i;
         }
-    Graph g;
-    g.ptr.assign((size_t)n + 1, 0);
     std::vector<int64_t> uniq((size_t)n, 0);
 #pragma omp parallel for schedule(dynamic, 256)
     for (int64_t i = 0; i < n; ++i) {
@@ -85,7 +132,9 @@ std::vector<uint32_t> reorder_alg1(const Csr &a)
     std::vector<uint32_t> perm((size_t)n);
     std::iota(perm.begin(), perm.end(), 0u);
     if (n == 0 || a.M != a.K) return perm;  // Q14: non-square -> identity
+    Trace tr;
     Graph g = affinity_graph(a);
+    tr.mark("affinity graph");
     const double m2 = (double)g.ptr[(size_t)n];
 
     // ---------------- Step I: dendrogram construction (one pass) ----------------
@@ -119,16 +168,27 @@ std::vector<uint32_t> reorder_alg1(const Csr &a)
             if (accw[r] == 0) touched.push_back(r);
             accw[r] += w;
         };
-        for (int64_t p = g.ptr[v]; p < g.ptr[v + 1]; ++p) add(g.adj[(size_t)p], 1u);
-        for (auto &e : E[v]) add(e.first, e.second);
-        std::sort(touched.begin(), touched.end());
+        for (int64_t p = g.ptr[v]; p < g.ptr[v + 1]; ++p) {
+            if (p + 16 < g.ptr[v + 1]) {  // the walk is bound by random accesses: prefetch ahead
+                const uint32_t x = g.adj[(size_t)p + 16];
+                __builtin_prefetch(&parent[x]);
+                __builtin_prefetch(&accw[x], 1);
+            }
+            add(g.adj[(size_t)p], 1u);
+        }
+        for (size_t q = 0; q < E[v].size(); ++q) {
+            if (q + 16 < E[v].size()) __builtin_prefetch(&parent[E[v][q + 16].first]);
+            add(E[v][q].first, E[v][q].second);
+        }
+        // touched is in first-touch order: the argmax breaks ties by the smallest id explicitly,
+        // and every later use of comp is order-independent (integer sums, a total-order cut)
         std::vector<std::pair<uint32_t, uint32_t>> comp;
         comp.reserve(touched.size());
         uint32_t best = UINT32_MAX;
         double best_dq = 0.0;
         for (uint32_t r : touched) {
             double dq = 2.0 * ((double)accw[r] / m2 - acomm[r] * acomm[v] / (m2 * m2));
-            if (best == UINT32_MAX || dq > best_dq) { best = r; best_dq = dq; }
+            if (best == UINT32_MAX || dq > best_dq || (dq == best_dq && r < best)) { best = r; best_dq = dq; }
             comp.emplace_back(r, (uint32_t)accw[r]);
             accw[r] = 0;
         }
@@ -142,7 +202,6 @@ std::vector<uint32_t> reorder_alg1(const Csr &a)
                                   return x.second != y.second ? x.second > y.second : x.first < y.first;
                               });
             comp.resize(kEdgeCap);
-            std::sort(comp.begin(), comp.end());
         }
         if (best != UINT32_MAX && best_dq > 0.0) {
             const uint32_t u = best;
@@ -159,6 +218,7 @@ std::vector<uint32_t> reorder_alg1(const Csr &a)
     }
     // A vertex is visited exactly once; its graph adjacency is read only on that
     // visit, and afterwards its aggregated edges live in E[] of itself or its parent.
+    tr.mark("step I (dendrogram)");
 
     // ---------------- Step II: ordering generation ----------------
     std::vector<uint32_t> seq;
@@ -223,6 +283,7 @@ std::vector<uint32_t> reorder_alg1(const Csr &a)
             v = best;
         }
     }
+    tr.mark("step II (ordering)");
     return perm;
 }
 

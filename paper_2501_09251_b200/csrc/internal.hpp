@@ -78,9 +78,10 @@ struct DevicePlan {
     uint32_t *units = nullptr;     // [n_units][8]
     uint32_t *row_map = nullptr;   // slab row -> C row (nparts == 1 with a permutation), else null
     int64_t K = 0;                 // rows of B (padding lanes gather row K -> TMA zero fill)
-    // cached TMA tensor map of the last B operand (key: ptr, N, FW, dtype)
+    // cached TMA tensor maps of the last B operand (key: ptr, N, FW, dtype): one per feature
+    // slice (kMaxSliceMaps at most), else one map over all N columns
     mutable uint64_t tmap_key[4] = {0, 0, 0, 0};
-    alignas(64) mutable unsigned char tmap[128] = {};
+    alignas(64) mutable unsigned char tmap[128 * 8] = {};
 };
 
 // kernels/build_sm100.cu -- the same BitTCF arrays built by data-parallel device passes
@@ -110,5 +111,6 @@ accspmm_status launch_unpermute(const float *G, const uint32_t *orig_row, int64_
                                 float *C, void *stream);
 accspmm_status launch_round_tf32(const float *in, float *out, int64_t n, void *stream);
 accspmm_status launch_decode(const DevicePlan &p, float *tiles, void *stream);
+accspmm_status probe_l2_read(int64_t bytes, int iters, double *gbs);
 
 }  // namespace accspmm

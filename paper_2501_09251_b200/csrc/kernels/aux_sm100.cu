@@ -3,6 +3,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "../internal.hpp"
@@ -50,6 +51,34 @@ __global__ void decode_kernel(const uint64_t *__restrict__ bits, const uint32_t 
     }
 }
 
+// L2 read-bandwidth probe: every thread streams 128-bit L2-only loads (ld.global.cg) over
+// an L2-resident buffer; the XOR of everything read is stored so nothing is elided.
+template <int U>
+__global__ void l2_read_kernel(const uint4 *__restrict__ buf, int64_t n16, int iters, uint32_t *__restrict__ sink)
+{
+    uint32_t acc = 0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int it = 0; it < iters; ++it) {
+        int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+        for (; e + (U - 1) * stride < n16; e += U * stride) {
+            uint4 v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];\n"
+                             : "=r"(v[u].x), "=r"(v[u].y), "=r"(v[u].z), "=r"(v[u].w) : "l"(buf + e + u * stride));
+#pragma unroll
+            for (int u = 0; u < U; ++u) acc ^= v[u].x ^ v[u].y ^ v[u].z ^ v[u].w;
+        }
+        for (; e < n16; e += stride) {
+            uint4 v;
+            asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];\n"
+                         : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(buf + e));
+            acc ^= v.x ^ v.y ^ v.z ^ v.w;
+        }
+    }
+    if (acc == 0x9E3779B9u) sink[0] = acc;  // practically never taken; keeps the loads live
+}
+
 int grid_for(int64_t n, int threads)
 {
     int64_t g = (n + threads - 1) / threads;
@@ -71,6 +100,45 @@ accspmm_status launch_unpermute(const float *G, const uint32_t *orig_row, int64_
     unpermute_kernel<<<grid_for(n_rows * n4, 256), 256, 0, (cudaStream_t)stream>>>(
         reinterpret_cast<const float4 *>(G), orig_row, n_rows, n4, reinterpret_cast<float4 *>(C));
     return check_launch("unpermute launch");
+}
+
+accspmm_status probe_l2_read(int64_t bytes, int iters, double *gbs)
+{
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    void *buf = nullptr;
+    uint32_t *sink = nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    cudaError_t e = cudaMalloc(&buf, (size_t)bytes);
+    if (e == cudaSuccess) e = cudaMalloc((void **)&sink, 4);
+    if (e == cudaSuccess) e = cudaMemset(buf, 0x5A, (size_t)bytes);
+    if (e == cudaSuccess) e = cudaEventCreate(&e0);
+    if (e == cudaSuccess) e = cudaEventCreate(&e1);
+    const int64_t n16 = bytes / 16;
+    const uint4 *b16 = reinterpret_cast<const uint4 *>(buf);
+    double best = 0.0;
+    // the best of a few launch shapes / load depths (the probe must not under-state the peak)
+    for (int cfg = 0; cfg < 4 && e == cudaSuccess; ++cfg) {
+        const unsigned grid = (unsigned)sms * (cfg & 1 ? 8 : 4);
+        const int threads = cfg & 1 ? 256 : 512;
+        auto kern = cfg < 2 ? l2_read_kernel<4> : l2_read_kernel<8>;
+        kern<<<grid, threads>>>(b16, n16, 2, sink);  // warm L2
+        cudaEventRecord(e0);
+        kern<<<grid, threads>>>(b16, n16, iters, sink);
+        cudaEventRecord(e1);
+        float ms = 0.f;
+        e = cudaEventSynchronize(e1);
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, e0, e1);
+        if (e == cudaSuccess && ms > 0.f) best = std::max(best, (double)n16 * 16.0 * iters / (ms * 1e-3) / 1e9);
+    }
+    cudaFree(buf);
+    cudaFree(sink);
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+    if (e != cudaSuccess) return fail(ACCSPMM_ERR_CUDA, std::string("L2 probe: ") + cudaGetErrorString(e));
+    *gbs = best;
+    return ACCSPMM_OK;
 }
 
 accspmm_status launch_round_tf32(const float *in, float *out, int64_t n, void *stream)

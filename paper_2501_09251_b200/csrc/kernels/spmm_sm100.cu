@@ -63,11 +63,6 @@ __device__ __forceinline__ void cp_async4(uint32_t dst, const void *src, uint64_
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
-// bulk L2 prefetch of [p, p+bytes) (p and bytes multiples of 16)
-__device__ __forceinline__ void prefetch_l2_bulk(const void *p, uint32_t bytes)
-{
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
-}
 
 __device__ __forceinline__ uint64_t policy_evict_last()
 {
@@ -163,7 +158,7 @@ constexpr int kChunk = 16;  // TC blocks per staged A-stream chunk
 struct ChunkSmem {
     uint32_t a2b[kChunk * 8];
     uint64_t mask[kChunk];
-    uint32_t tco[kChunk + 4];   // TCOffset of the chunk's blocks plus the end offset (value range)
+    uint32_t tco[kChunk];
 };
 
 struct WarpSmem {
@@ -528,9 +523,21 @@ __device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap *map
         : "memory");
 }
 
-template <int FW, bool F16, int WARPS, int STAGES, bool RND, int MINB = 1, int DIST = 1, bool PF = false>
+// Tensor maps of B: with nmaps > 1, map s covers exactly feature slice s (base B + s*FW,
+// width FW), so the box's extra columns fall outside the tensor and are zero-filled
+// without L2 traffic; with nmaps == 1 one map spans all N columns (N == FW, or more
+// slices than maps: the extra columns of a box are then real reads of the next slice).
+constexpr int kMaxSliceMaps = 8;
+template <int NM>
+struct G4MapsT {
+    CUtensorMap m[NM];
+};
+using G4Maps = G4MapsT<kMaxSliceMaps>;
+inline int map_count(const KParams &kp) { return kp.nslices > 1 && kp.nslices <= kMaxSliceMaps ? kp.nslices : 1; }
+
+template <int FW, bool F16, int WARPS, int STAGES, bool RND, int MINB = 1, int DIST = 1, int NM = 1>
 __global__ void __launch_bounds__(WARPS * 32, MINB)
-    spmm_bittcf_g4_kernel(const KParams p, const __grid_constant__ CUtensorMap tmap)
+    spmm_bittcf_g4_kernel(const KParams p, const __grid_constant__ G4MapsT<NM> maps)
 {
     using CF = Cfg<FW, F16>;
     using GC = G4Cfg<FW, F16>;
@@ -548,7 +555,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     const uint64_t pol_keep = policy_evict_last();
     const uint64_t pol_stream = policy_evict_first();
     if (lane == 0) {
-        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&maps.m[NM > 1 ? slice : 0]))
+                     : "memory");
 #pragma unroll
         for (int s = 0; s < STAGES; ++s) mbar_init(smem_u32(&sm.bar[s]), 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -573,24 +581,15 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
             ChunkSmem &c = sm.ch[(i / kChunk) & 1];
             const uint32_t b = b0 + i;
             const uint32_t cnt = min((uint32_t)kChunk, nblk - i);
-            if ((uint32_t)lane < cnt) cp_async8(smem_u32(&c.mask[lane]), p.bits + b + lane, pol_stream);
-            if ((uint32_t)lane <= cnt) cp_async4(smem_u32(&c.tco[lane]), p.tco + b + lane, pol_stream);
+            if ((uint32_t)lane < cnt) {
+                cp_async8(smem_u32(&c.mask[lane]), p.bits + b + lane, pol_stream);
+                cp_async4(smem_u32(&c.tco[lane]), p.tco + b + lane, pol_stream);
+            }
             const uint4 *src4 = reinterpret_cast<const uint4 *>(p.a2b + (size_t)b * 8);
             if ((uint32_t)lane < 2 * cnt) cp_async16(smem_u32(&c.a2b[4 * lane]), src4 + lane, pol_stream);
             if ((uint32_t)lane + 32 < 2 * cnt) cp_async16(smem_u32(&c.a2b[4 * (lane + 32)]), src4 + lane + 32, pol_stream);
         }
         cp_async_commit();
-    };
-    // Lane 0: bulk L2 prefetch of the values of the staged chunk starting at block i (its
-    // TCOffset range is contiguous), so the per-lane value loads of its blocks hit L2.
-    auto prefetch_values = [&](uint32_t i) {
-        if (lane == 0 && i < nblk) {
-            const ChunkSmem &c = sm.ch[(i / kChunk) & 1];
-            const uint32_t cnt = min((uint32_t)kChunk, nblk - i);
-            constexpr uint32_t ES = CF::ES;
-            const uint32_t lo = (c.tco[0] * ES) & ~15u, hi = (c.tco[cnt] * ES + 15u) & ~15u;
-            if (hi > lo) prefetch_l2_bulk(reinterpret_cast<const char *>(p.vals) + lo, hi - lo);
-        }
     };
 
     // Value registers of the blocks in flight: decoded and loaded DIST blocks ahead of use
@@ -635,13 +634,15 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
             // no proxy fence: the stage's previous generic reads fed this warp's mma.sync,
             // which cannot issue before every lane's LDS has returned
             mbar_arrive_expect_tx(bar, 8u * GC::RS);
-            const int32_t col = (int32_t)(slice * FW);
+            // derived here, not held across the loop (registers are the occupancy limit)
+            const CUtensorMap *tmap = &maps.m[NM > 1 ? slice : 0];
+            const int32_t tcol = NM > 1 ? 0 : slice * FW;
             if constexpr (!F16) {
-                tma_gather4(st, &tmap, col, r0, r1, r2, r3, bar, pol_keep);
-                tma_gather4(st + GC::GRP, &tmap, col, r4, r5, r6, r7, bar, pol_keep);
+                tma_gather4(st, tmap, tcol, r0, r1, r2, r3, bar, pol_keep);
+                tma_gather4(st + GC::GRP, tmap, tcol, r4, r5, r6, r7, bar, pol_keep);
             } else {
-                tma_gather4(st, &tmap, col, r0, r2, r4, r6, bar, pol_keep);
-                tma_gather4(st + GC::GRP, &tmap, col, r1, r3, r5, r7, bar, pol_keep);
+                tma_gather4(st, tmap, tcol, r0, r2, r4, r6, bar, pol_keep);
+                tma_gather4(st + GC::GRP, tmap, tcol, r1, r3, r5, r7, bar, pol_keep);
             }
         }
     };
@@ -744,7 +745,6 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     cp_async_wait_all();
     __syncwarp();
     issue_chunk(kChunk);
-    if constexpr (PF) prefetch_values(0);
     after_block(b0);
 #pragma unroll
     for (int d = 0; d < DIST; ++d)
@@ -759,11 +759,6 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
             cp_async_wait_all();
             __syncwarp();
             issue_chunk(jv + kChunk);
-        }
-        if (PF && (jv & (kChunk - 1u)) == kChunk / 2) {  // mid-chunk: the next chunk has landed
-            cp_async_wait_all();
-            __syncwarp();
-            prefetch_values((jv | (kChunk - 1u)) + 1u);
         }
         if (!checked || jt < nblk) issue_tma(jt, (u + 1) & 1);
         if (DIST == 2 && (jv & (kChunk - 1u)) == 0) {
@@ -860,12 +855,14 @@ int env_int(const char *name, int dflt)
     return s ? std::atoi(s) : dflt;
 }
 
-template <int FW, bool F16, int WARPS, int STAGES, bool RND = false, int MINB = 1, int DIST = 1, bool PF = false>
-accspmm_status launch_g4(const KParams &kp, const CUtensorMap *map, int64_t n_units, cudaStream_t stream)
+// NM = 1: one tensor map (the full-width map when several slices exist); NM = kMaxSliceMaps:
+// one map per slice (tensor_map decides; only the default configurations instantiate it)
+template <int FW, bool F16, int WARPS, int STAGES, bool RND = false, int MINB = 1, int DIST = 1, int NM = 1>
+accspmm_status launch_g4(const KParams &kp, const G4Maps *map, int64_t n_units, cudaStream_t stream)
 {
     using SM = G4WarpSmem<FW, F16, STAGES>;
     const size_t smem = sizeof(SM) * WARPS;
-    auto kern = spmm_bittcf_g4_kernel<FW, F16, WARPS, STAGES, RND, MINB, DIST, PF>;
+    auto kern = spmm_bittcf_g4_kernel<FW, F16, WARPS, STAGES, RND, MINB, DIST, NM>;
     static int configured_device = -1;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -880,17 +877,23 @@ accspmm_status launch_g4(const KParams &kp, const CUtensorMap *map, int64_t n_un
     const int64_t groups = (n_units + WARPS - 1) / WARPS;
     const int64_t grid = groups * kp.nslices;
     if (grid > 0x7FFFFFFFll) return fail(ACCSPMM_ERR_UNSUPPORTED, "grid too large");
-    kern<<<(unsigned)grid, WARPS * 32, smem, stream>>>(kp, *map);
+    kern<<<(unsigned)grid, WARPS * 32, smem, stream>>>(kp, *reinterpret_cast<const G4MapsT<NM> *>(map));
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(ACCSPMM_ERR_CUDA, std::string("spmm launch: ") + cudaGetErrorString(e));
     return ACCSPMM_OK;
 }
 
-// TMA tensor map of B (2D: K rows x N columns, box = (FW+8) x 1 for gather4), cached in the plan
-accspmm_status tensor_map(const DevicePlan &d, const void *B, int64_t N, int FW, const CUtensorMap **out)
+// TMA tensor maps of B (2D: K rows x width columns, box = BOXE x 1 for gather4), cached in
+// the plan; one per feature slice when the slices fit G4Maps (see G4Maps)
+accspmm_status tensor_map(const DevicePlan &d, const KParams &kp, int FW, bool multi, const G4Maps **out)
 {
-    const uint64_t key[4] = {(uint64_t)(uintptr_t)B, (uint64_t)N, (uint64_t)FW, (uint64_t)d.precision + 1};
-    CUtensorMap *m = reinterpret_cast<CUtensorMap *>(d.tmap);
+    const void *B = kp.B;
+    const int64_t N = kp.N;
+    const int nm = multi ? map_count(kp) : 1;
+    const uint64_t key[4] = {(uint64_t)(uintptr_t)B, (uint64_t)N, (uint64_t)FW,
+                             (uint64_t)(d.precision + 1) | ((uint64_t)nm << 8)};
+    G4Maps *maps = reinterpret_cast<G4Maps *>(d.tmap);
+    static_assert(sizeof(G4Maps) <= sizeof(d.tmap), "tensor-map cache too small");
     if (!(key[0] == d.tmap_key[0] && key[1] == d.tmap_key[1] && key[2] == d.tmap_key[2] && key[3] == d.tmap_key[3])) {
         static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
         if (!encode) {
@@ -903,65 +906,69 @@ accspmm_status tensor_map(const DevicePlan &d, const void *B, int64_t N, int FW,
         }
         const bool f16 = d.precision == ACCSPMM_FP16;
         const cuuint64_t es = f16 ? 2 : 4;
-        cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)d.K};
-        cuuint64_t strides[1] = {(cuuint64_t)N * es};
-        cuuint32_t box[2] = {(cuuint32_t)(FW + (f16 ? 16 : 8)), 1u};  // G4Cfg::BOXE
-        cuuint32_t estr[2] = {1u, 1u};
-        CUresult r = encode(m, f16 ? CU_TENSOR_MAP_DATA_TYPE_UINT16 : CU_TENSOR_MAP_DATA_TYPE_UINT32, 2,
-                            const_cast<void *>(B), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        if (r != CUDA_SUCCESS) return fail(ACCSPMM_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+        for (int m = 0; m < nm; ++m) {
+            cuuint64_t dims[2] = {(cuuint64_t)(nm > 1 ? FW : N), (cuuint64_t)d.K};
+            cuuint64_t strides[1] = {(cuuint64_t)N * es};
+            cuuint32_t box[2] = {(cuuint32_t)(FW + (f16 ? 16 : 8)), 1u};  // G4Cfg::BOXE
+            cuuint32_t estr[2] = {1u, 1u};
+            void *base = const_cast<char *>(reinterpret_cast<const char *>(B)) + (size_t)m * FW * es;
+            CUresult r = encode(&maps->m[m], f16 ? CU_TENSOR_MAP_DATA_TYPE_UINT16 : CU_TENSOR_MAP_DATA_TYPE_UINT32, 2,
+                                base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS)
+                return fail(ACCSPMM_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+        }
         for (int k = 0; k < 4; ++k) d.tmap_key[k] = key[k];
     }
-    *out = m;
+    *out = maps;
     return ACCSPMM_OK;
+}
+
+// Minimum resident CTAs per SM for __launch_bounds__ (caps registers per thread): the
+// kernel is latency-bound, so occupancy pays until the register cap starts to serialise
+// the gather/decode pipeline.  Measured on the Reddit-shaped and stencil matrices
+// (DESIGN.md §7): FW 128 10 (TF32 is then smem-bound; FP16 spills above); FW 64/32 12;
+// FW 16 16.
+template <int FW, bool F16>
+constexpr int tuned_minb()
+{
+    return FW == 128 ? 10 : FW == 16 ? 16 : 12;
 }
 
 template <int FW, bool F16>
 accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, int64_t n_units, cudaStream_t stream,
                          bool rnd)
 {
-    // Default (measured): TMA gather4, 2 warps x 2 stages per CTA, at every
-    // width and precision.  ACCSPMM_KCFG selects other variants for A/B measurements
-    // (21: gather4 with 4 warps per CTA; 10-12: register-direct gather).  Deeper
-    // gather4 rings (3, 4 stages) measured slower (smem per warp limits occupancy).
-    int kcfg = env_int("ACCSPMM_KCFG", -1);
-    if (kcfg < 0) kcfg = 20;
-    if constexpr (!F16) {
-        if (rnd) {  // B not pre-rounded: rho(B) applied in registers (default configurations only)
-            if (kcfg >= 20) {
-                const CUtensorMap *map = nullptr;
-                accspmm_status st = tensor_map(d, B, kp.N, FW, &map);
-                if (st != ACCSPMM_OK) return st;
-                switch (kcfg) {
-                case 24: return launch_g4<FW, F16, 2, 2, true, 10>(kp, map, n_units, stream);
-                case 31: return launch_g4<FW, F16, 2, 2, true, 12>(kp, map, n_units, stream);
-                case 33: return launch_g4<FW, F16, 2, 2, true, 16>(kp, map, n_units, stream);
-                default: return launch_g4<FW, F16, 2, 2, true>(kp, map, n_units, stream);
-                }
-            }
-            return launch_cfg<FW, F16, 2, true>(kp, n_units, stream);
-        }
-    }
-    if (kcfg >= 20) {
-        const CUtensorMap *map = nullptr;
-        accspmm_status st = tensor_map(d, B, kp.N, FW, &map);
+    // Default (measured): TMA gather4, 2 warps x 2 stages per CTA, tuned launch
+    // bounds, at every width and precision.  ACCSPMM_KCFG selects other variants for A/B
+    // measurements: 20 = no launch-bounds minimum, 21 = 4 warps per CTA, 24/31/33 = minimum
+    // 10/12/16 CTAs per SM, 10-12 = register-direct gather (4, 2, 8 warps per CTA).
+    constexpr int MB = tuned_minb<FW, F16>();
+    const int kcfg = env_int("ACCSPMM_KCFG", -1);
+    if (kcfg < 0 || kcfg >= 20) {
+        const G4Maps *map = nullptr;
+        const bool multi = kcfg < 0 && map_count(kp) > 1;
+        accspmm_status st = tensor_map(d, kp, FW, multi, &map);
         if (st != ACCSPMM_OK) return st;
+        constexpr int NM = kMaxSliceMaps;
+        if (!F16 && rnd) {  // B not pre-rounded: rho(B) applied in registers
+            if (multi) return launch_g4<FW, F16, 2, 2, true, MB, 1, NM>(kp, map, n_units, stream);
+            switch (kcfg) {
+            case 20: return launch_g4<FW, F16, 2, 2, true, 1>(kp, map, n_units, stream);
+            default: return launch_g4<FW, F16, 2, 2, true, MB>(kp, map, n_units, stream);
+            }
+        }
+        if (multi) return launch_g4<FW, F16, 2, 2, false, MB, 1, NM>(kp, map, n_units, stream);
         switch (kcfg) {
+        case 20: return launch_g4<FW, F16, 2, 2, false, 1>(kp, map, n_units, stream);
         case 21: return launch_g4<FW, F16, 4, 2>(kp, map, n_units, stream);
-        case 23: return launch_g4<FW, F16, 2, 2, false, 1, 2>(kp, map, n_units, stream);
-        case 24: return launch_g4<FW, F16, 2, 2, false, 10, 1>(kp, map, n_units, stream);
-        case 25: return launch_g4<FW, F16, 2, 2, false, 10, 2>(kp, map, n_units, stream);
-        case 26: return launch_g4<FW, F16, 2, 2, false, 1, 1, true>(kp, map, n_units, stream);
-        case 27: return launch_g4<FW, F16, 2, 2, false, 10, 1, true>(kp, map, n_units, stream);
-        case 28: return launch_g4<FW, F16, 2, 2, false, 10, 2, true>(kp, map, n_units, stream);
-        case 31: return launch_g4<FW, F16, 2, 2, false, 12, 1>(kp, map, n_units, stream);
-        case 32: return launch_g4<FW, F16, 2, 2, false, 14, 1>(kp, map, n_units, stream);
-        case 33: return launch_g4<FW, F16, 2, 2, false, 16, 1>(kp, map, n_units, stream);
-        default: return launch_g4<FW, F16, 2, 2>(kp, map, n_units, stream);
+        case 24: return launch_g4<FW, F16, 2, 2, false, 10>(kp, map, n_units, stream);
+        case 31: return launch_g4<FW, F16, 2, 2, false, 12>(kp, map, n_units, stream);
+        case 33: return launch_g4<FW, F16, 2, 2, false, 16>(kp, map, n_units, stream);
+        default: return launch_g4<FW, F16, 2, 2, false, MB>(kp, map, n_units, stream);
         }
     }
+    if (!F16 && rnd) return launch_cfg<FW, F16, 2, true>(kp, n_units, stream);
     // register-direct flavour (kcfg 10-12: 4, 2 or 8 warps per CTA)
     switch (kcfg) {
     case 10: return launch_cfg<FW, F16, 4>(kp, n_units, stream);

@@ -37,9 +37,11 @@ def test_tiny_config():
 
 
 @pytest.mark.parametrize("precision", PRECISIONS)
-@pytest.mark.parametrize("N", [16, 32, 48, 64, 96, 128, 256])
+@pytest.mark.parametrize("N", [16, 32, 48, 64, 96, 128, 256, 384, 512, 1152])
 @pytest.mark.parametrize("balance", ["off", "on"])
 def test_random_ragged_float(precision, N, balance):
+    """N up to 512 (the paper's widest feature dimension) uses one TMA map per 128-wide
+    slice; N = 1152 (9 slices) exercises the single full-width map."""
     A = _ragged(seed=N)
     v = gen.values_uniform(A.nnz, 5)
     B = gen.dense_normal(A.K, N, 6)
@@ -48,7 +50,7 @@ def test_random_ragged_float(precision, N, balance):
 
 
 @pytest.mark.parametrize("precision", PRECISIONS)
-@pytest.mark.parametrize("N", [16, 32, 64, 128])
+@pytest.mark.parametrize("N", [16, 32, 64, 128, 256, 512])
 def test_integer_bit_exact_and_balance_invariant(precision, N):
     A = gen.dcsbm(3000, 150_000, 5, 2.2, 0.2, 2000, seed=N, oversample=1.3)
     v = gen.values_int(A.nnz, 1)
