@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--reorder", default="auto", choices=["off", "on", "auto"])
     ap.add_argument("--balance", default="auto", choices=["off", "on", "auto"])
     ap.add_argument("--unit-cap", type=int, default=0)
+    ap.add_argument("--permute-cols", action="store_true", help="symmetric reordering: relabel columns too")
+    ap.add_argument("--build", default="host", choices=["host", "device"], help="BitTCF builder")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-flush", action="store_true")
@@ -184,6 +186,7 @@ def workload_config(args, cfg, A, world):
     return {"workload": f"{cfg.name}: {cfg.note}; N={args.N}, {args.precision}",
             "matrix": cfg.name, "baseline_config_index": cfg.baseline_index, "M": A.M, "K": A.K, "nnz": A.nnz,
             "N": args.N, "precision": args.precision, "reorder": args.reorder, "balance": args.balance,
+            "permute_cols": bool(getattr(args, "permute_cols", False)),
             "l2": "none" if args.no_flush else f"flushed between timed steps ({L2_FLUSH_BYTES >> 20} MiB write)",
             "parallelism": f"rowwindow-nnz-partition x{world}"}
 
@@ -231,7 +234,8 @@ def main():
     cfg, A, vals, B = make_inputs(args)
     t0 = time.perf_counter()
     plan = acc.Plan(A.M, A.K, A.rowptr, A.colidx, vals, precision=args.precision, reorder=args.reorder,
-                    balance=args.balance, unit_cap=args.unit_cap, part=rank, nparts=world, device=local)
+                    balance=args.balance, unit_cap=args.unit_cap, part=rank, nparts=world, device=local,
+                    permute_cols=args.permute_cols, build=args.build)
     plan_s = time.perf_counter() - t0
     info = plan.info
     tdt = torch.float16 if args.precision == "fp16" else torch.float32
@@ -260,6 +264,7 @@ def main():
             flush.zero_()
     torch.cuda.synchronize()
 
+    l2_peak_before = acc.accspmm_probe_l2_bandwidth(96 << 20, 100)  # again after the loop: max of both
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     plan.set_timing(True)   # in-library CUDA events around the SpMM kernel launch (dominant kernel)
     clocks = ClockSampler(local)
@@ -314,34 +319,53 @@ def main():
     traffic = load_traffic(f"{args.config}-N{args.N}-{args.precision}-{args.reorder}-{args.balance}-p{world}")
     # L2 roofline: every model byte (gathered B rows, A stream, C) passes through L2, and on
     # graphs whose B fits L2 the gather is served from there -- the binding resource
-    l2_peak = acc.accspmm_probe_l2_bandwidth(64 << 20, 40)
+    l2_peak = max(acc.accspmm_probe_l2_bandwidth(96 << 20, 100), l2_peak_before)
 
     # ---- end to end through the public API with pinned host buffers (H2D B + execute + D2H C)
+    # Every step copies its own B from pinned host memory and its C back (separate host buffers
+    # per ring slot).  Headline: accspmm_execute_host_batch, which overlaps H2D(i+1) and D2H(i-1)
+    # with the SpMM of step i; beside it the one-call-per-step synchronous accspmm_execute_host.
     e2e = None
     if not args.no_e2e:
-        Bh = torch.from_numpy(B).to(tdt).pin_memory()
-        Ch = torch.empty((plan.out_rows, args.N), dtype=torch.float32).pin_memory()
+        ring = 3
+        Bh = [torch.from_numpy(B).to(tdt).pin_memory() for _ in range(ring)]
+        Ch = [torch.empty((plan.out_rows, args.N), dtype=torch.float32).pin_memory() for _ in range(ring)]
+        e_steps = max(3, min(args.steps, 30))
+        Bb = [Bh[i % ring] for i in range(e_steps)]
+        Cb = [Ch[i % ring] for i in range(e_steps)]
+
+        def timed(fn):
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            fn()
+            s1.record(stream)
+            torch.cuda.synchronize()
+            te = s0.elapsed_time(s1) / 1e3
+            if world > 1:
+                tt = torch.tensor([te], dtype=torch.float64, device="cpu" if shared else "cuda")
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                te = float(tt.item())
+            return te
+
+        plan.execute_host_batch(Bb[:4], Cb[:4], stream)  # warm-up (staging buffers, streams)
+        te = timed(lambda: plan.execute_host_batch(Bb, Cb, stream))
         for _ in range(2):
-            plan.execute_host(Bh, Ch, stream)
-        e_steps = max(3, min(args.steps, 20))
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s0.record(stream)
-        for _ in range(e_steps):
-            plan.execute_host(Bh, Ch, stream)
-        s1.record(stream)
-        torch.cuda.synchronize()
-        te = s0.elapsed_time(s1) / 1e3
-        if world > 1:
-            tt = torch.tensor([te], dtype=torch.float64, device="cpu" if shared else "cuda")
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            te = float(tt.item())
+            plan.execute_host(Bh[0], Ch[0], stream)
+
+        def sync_steps():
+            for i in range(e_steps):
+                plan.execute_host(Bb[i], Cb[i], stream)
+        ts = timed(sync_steps)
         e2e = {"value": 2.0 * A.nnz * args.N * e_steps / te / 1e9, "unit": "GFLOP/s",
-               "h2d_bytes_per_step": int(Bh.numel() * Bh.element_size()),
-               "d2h_bytes_per_step": int(Ch.numel() * Ch.element_size()), "steps": e_steps,
-               "ms_per_step": te / e_steps * 1e3}
+               "h2d_bytes_per_step": int(Bh[0].numel() * Bh[0].element_size()),
+               "d2h_bytes_per_step": int(Ch[0].numel() * Ch[0].element_size()), "steps": e_steps,
+               "ms_per_step": te / e_steps * 1e3,
+               "api": "accspmm_execute_host_batch (H2D/SpMM/D2H pipelined over 2 device slots)",
+               "sync_per_step": {"value": 2.0 * A.nnz * args.N * e_steps / ts / 1e9,
+                                 "ms_per_step": ts / e_steps * 1e3, "api": "accspmm_execute_host"}}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -359,14 +383,17 @@ def main():
                          "kernel": kernel_name(args), "launch_ms": avg_s * 1e3,
                          "kernel_share_of_step": avg_s * args.steps / t_local,
                          "l2": {"achieved": achieved, "peak": l2_peak, "unit": "GB/s", "frac": achieved / l2_peak,
-                                "peak_kind": "measured live: accspmm_probe_l2_bandwidth (64 MiB, ld.global.cg)"}},
+                                "peak_kind": "measured live: accspmm_probe_l2_bandwidth (96 MiB, ld.global.cg, best "
+                                             "of 4 launch shapes, before and after the timed loop)"}},
             "cpu_baseline": cpu,
             "clocks": clk,
             "e2e": e2e,
             "gpu_launches": args.steps * plan.launches_per_execute,
-            "plan": {k: info[k] for k in ("W", "NB", "sum_U", "mean_nnz_tc", "ibd", "balanced", "unit_cap", "n_units",
-                                          "n_split_windows", "n_segments", "reorder_applied", "ms_reorder",
-                                          "ms_build", "ms_schedule", "ms_upload", "device_bytes")},
+            "plan": {k: info[k] for k in ("W", "NB", "sum_U", "mean_nnz_tc", "ibd", "balanced", "grouped", "unit_cap",
+                                          "n_units", "n_split_windows", "n_segments", "reorder_applied",
+                                          "cols_permuted", "ms_reorder", "ms_build", "ms_schedule", "ms_upload",
+                                          "device_bytes")},
+            "plan_build": args.build,
             "warm": {"ms_per_step": warm_ms, "value": 2.0 * A.nnz * args.N / (warm_ms / 1e3) / 1e9,
                      "note": "back-to-back steps without the L2 flush (rank-local)"},
             "plan_create_s": plan_s, "broadcast_ms": bcast_ms, "wall_s_timed_loop": wall,

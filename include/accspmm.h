@@ -63,7 +63,8 @@ typedef enum {
 typedef enum {
     ACCSPMM_BALANCE_OFF = 0,  /* one work unit per RowWindow ("each TB processes all the TC blocks of a single RowWindow") */
     ACCSPMM_BALANCE_ON = 1,   /* TC blocks redistributed into units of <= unit_cap blocks   */
-    ACCSPMM_BALANCE_AUTO = 2  /* balance iff IBD (Eq. 3) > 8                                 */
+    ACCSPMM_BALANCE_AUTO = 2  /* balance iff IBD (Eq. 3) > 8; otherwise windows stay whole but
+                                 consecutive ones are grouped into one warp's unit (B200)        */
 } accspmm_balance_mode;
 
 typedef enum {
@@ -81,7 +82,11 @@ typedef struct {
     int32_t nparts;     /* number of nnz-balanced RowWindow ranges (multi-GPU); 1 = whole matrix    */
     int32_t device;     /* CUDA device ordinal; -1 = host-only plan (format + schedule, no upload)  */
     int32_t build;      /* accspmm_build_mode; default ACCSPMM_BUILD_HOST                            */
-    int32_t reserved[8];
+    int32_t permute_cols; /* 1: when a row permutation is applied (square A), relabel the columns with
+                             it too (A' = P A P^T); every execute then gathers
+                             B' = P B on the device before the SpMM (fused with the TF32 rounding
+                             pass).  C is unchanged.  Default 0 (rows only, reading Q12).          */
+    int32_t reserved[7];
 } accspmm_options;
 
 typedef struct {
@@ -103,7 +108,9 @@ typedef struct {
     int64_t value_bytes;        /* es_A * plan_nnz                                                   */
     int64_t device_bytes;       /* bytes resident on the device for this plan (excl. workspace)      */
     double ms_validate, ms_reorder, ms_build, ms_schedule, ms_upload;
-    int64_t reserved[8];
+    int64_t grouped;            /* 1: unbalanced plan whose whole windows are grouped per unit (AUTO) */
+    int64_t cols_permuted;      /* 1: columns relabelled with the row permutation (permute_cols)      */
+    int64_t reserved[6];
 } accspmm_plan_info;
 
 /* Fills *opt with the defaults listed above.  Never fails for a non-null opt. */
@@ -147,6 +154,16 @@ accspmm_status accspmm_execute(const accspmm_plan *plan, const void *B, int64_t 
 accspmm_status accspmm_execute_host(const accspmm_plan *plan, const void *B_host, int64_t N, void *C_host,
                                     void *stream);
 
+/* Pipelined end-to-end batch: for i < count, C_hosts[i] = A . B_hosts[i] (shapes and
+ * types as accspmm_execute_host).  Two device staging slots and two copy streams
+ * overlap the H2D copy of B_{i+1} and the D2H copy of C_{i-1} with the SpMM of step i
+ * (PCIe is full duplex), so the steady-state step costs max(H2D, SpMM, D2H) instead of
+ * their sum.  Host buffers must be pinned for the copies to overlap (pageable memory is
+ * still correct, only serialised).  The SpMM runs on `stream`; returns after every C_i
+ * has landed (synchronises).  Errors as accspmm_execute_host. */
+accspmm_status accspmm_execute_host_batch(const accspmm_plan *plan, const void *const *B_hosts, void *const *C_hosts,
+                                          int32_t count, int64_t N, void *stream);
+
 /* Frees every host and device resource of the plan.  NULL is a no-op.  The
  * caller must ensure no execute on this plan is still in flight. */
 void accspmm_plan_destroy(accspmm_plan *plan);
@@ -172,6 +189,13 @@ accspmm_status accspmm_plan_export_rows(const accspmm_plan *plan, uint32_t *orig
 /* Algorithm 1 alone (host): perm_new2old u32[n] for the square n x n CSR.
  * Returns INVALID_CSR / INVALID_VALUE as plan creation does. */
 accspmm_status accspmm_reorder(int64_t n, const int64_t *rowptr, const int32_t *colidx, uint32_t *perm_new2old);
+
+/* A^T (host): the K x M transpose of the canonical CSR A as canonical CSR -- the operand
+ * of the backward pass dB = A^T . dC of C = A . B.  t_rowptr int64[K+1], t_colidx
+ * int32[nnz], t_vals float32[nnz] (t_vals and vals may be NULL: pattern only), caller-owned.
+ * Errors: INVALID_VALUE, INVALID_CSR (as plan creation), UNSUPPORTED (M >= 2^31). */
+accspmm_status accspmm_csr_transpose(int64_t M, int64_t K, const int64_t *rowptr, const int32_t *colidx,
+                                    const float *vals, int64_t *t_rowptr, int32_t *t_colidx, float *t_vals);
 
 /* nnz-balanced partition bounds (host): bounds int64[nparts+1] over the
  * ceil(M/8) windows of the given CSR (already in the order to be partitioned). */

@@ -65,12 +65,16 @@ def auto_cap(NB: int) -> int:
     return max(PAPER_CAP, min(4096, c))
 
 
-def build_units(rwo, cap: int, balance: bool, precision: str = "tf32"):
-    """Work units (w0, nw, b0, b1, split_id, seg, nseg, slot) covering every block once."""
+def build_units(rwo, cap: int, balance: bool, precision: str = "tf32", group: bool = False):
+    """Work units (w0, nw, b0, b1, split_id, seg, nseg, slot) covering every block once.
+
+    Not balanced: one unit per RowWindow, or with ``group`` (the B200 reading R7b,
+    DESIGN.md: balance AUTO below the IBD threshold) consecutive WHOLE windows packed into
+    one unit by the same concatenation rule, never split."""
     rwo = np.asarray(rwo, dtype=np.int64)
     W = rwo.size - 1
     units = []
-    if not balance:
+    if not balance and not group:
         for w in range(W):
             units.append((w, 1, int(rwo[w]), int(rwo[w + 1]), NO_SPLIT, 0, 1, 0))
         return units
@@ -80,7 +84,7 @@ def build_units(rwo, cap: int, balance: bool, precision: str = "tf32"):
     cur = None  # [w0, nw, b0, b1, cost]
     for w in range(W):
         nb = int(rwo[w + 1] - rwo[w])
-        if nb > cap:
+        if nb > cap and balance:
             if cur is not None:
                 units.append((cur[0], cur[1], cur[2], cur[3], NO_SPLIT, 0, 1, 0))
                 cur = None

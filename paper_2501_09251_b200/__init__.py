@@ -36,7 +36,8 @@ class AccSpmmError(RuntimeError):
 class accspmm_options(ctypes.Structure):
     _fields_ = [("precision", ctypes.c_int32), ("reorder", ctypes.c_int32), ("balance", ctypes.c_int32),
                 ("unit_cap", ctypes.c_int32), ("part", ctypes.c_int32), ("nparts", ctypes.c_int32),
-                ("device", ctypes.c_int32), ("build", ctypes.c_int32), ("reserved", ctypes.c_int32 * 8)]
+                ("device", ctypes.c_int32), ("build", ctypes.c_int32), ("permute_cols", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 7)]
 
 
 _I64 = ["M", "K", "nnz", "rows", "row_begin", "window_begin", "W", "NB", "plan_nnz", "sum_U", "n_units",
@@ -51,7 +52,7 @@ class accspmm_plan_info(ctypes.Structure):
                                                   "value_bytes", "device_bytes")]
                 + [(n, ctypes.c_double) for n in ("ms_validate", "ms_reorder", "ms_build", "ms_schedule",
                                                    "ms_upload")]
-                + [("reserved", ctypes.c_int64 * 8)])
+                + [("grouped", ctypes.c_int64), ("cols_permuted", ctypes.c_int64), ("reserved", ctypes.c_int64 * 6)])
 
     def as_dict(self) -> dict:
         return {n: getattr(self, n) for n, _ in self._fields_ if n != "reserved"}
@@ -64,7 +65,7 @@ EXPORTED = [
     "accspmm_plan_export_units", "accspmm_plan_export_rows", "accspmm_reorder", "accspmm_partition_bounds",
     "accspmm_unpermute", "accspmm_debug_round_tf32", "accspmm_debug_decode", "accspmm_status_string",
     "accspmm_last_error", "accspmm_abi_version", "accspmm_plan_set_timing", "accspmm_plan_kernel_times",
-    "accspmm_probe_l2_bandwidth",
+    "accspmm_probe_l2_bandwidth", "accspmm_execute_host_batch", "accspmm_csr_transpose",
 ]
 
 
@@ -101,6 +102,8 @@ def load_library(path: str = LIB_PATH):
         "accspmm_plan_set_timing": ([P, I32], S),
         "accspmm_plan_kernel_times": ([P, P, I32, ctypes.POINTER(I32)], S),
         "accspmm_probe_l2_bandwidth": ([I64, I32, ctypes.POINTER(ctypes.c_double)], S),
+        "accspmm_execute_host_batch": ([P, P, P, I32, I64, P], S),
+        "accspmm_csr_transpose": ([I64, I64, P, P, P, P, P, P], S),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -162,6 +165,15 @@ def accspmm_execute_host(plan, B_host_ptr, N, C_host_ptr, stream_ptr=None):
     _check(load_library().accspmm_execute_host(plan, B_host_ptr, int(N), C_host_ptr, stream_ptr))
 
 
+def accspmm_execute_host_batch(plan, B_host_ptrs, C_host_ptrs, N, stream_ptr=None):
+    n = len(B_host_ptrs)
+    if len(C_host_ptrs) != n:
+        raise ValueError("B and C batches differ in length")
+    Bs = (ctypes.c_void_p * max(n, 1))(*B_host_ptrs)
+    Cs = (ctypes.c_void_p * max(n, 1))(*C_host_ptrs)
+    _check(load_library().accspmm_execute_host_batch(plan, Bs, Cs, n, int(N), stream_ptr))
+
+
 def accspmm_plan_destroy(plan):
     if plan:
         load_library().accspmm_plan_destroy(plan)
@@ -209,6 +221,21 @@ def accspmm_reorder(n, rowptr, colidx) -> np.ndarray:
     perm = np.empty(n, np.uint32)
     _check(load_library().accspmm_reorder(int(n), _ptr(rowptr), _ptr(colidx), _ptr(perm)))
     return perm
+
+
+def accspmm_csr_transpose(M, K, rowptr, colidx, vals=None):
+    rowptr = np.ascontiguousarray(rowptr, dtype=np.int64)
+    colidx = np.ascontiguousarray(colidx, dtype=np.int32)
+    nnz = int(rowptr[-1]) if M > 0 else 0
+    t_rowptr = np.empty(K + 1, np.int64)
+    t_colidx = np.empty(nnz, np.int32)
+    t_vals = None
+    if vals is not None:
+        vals = np.ascontiguousarray(vals, dtype=np.float32)
+        t_vals = np.empty(nnz, np.float32)
+    _check(load_library().accspmm_csr_transpose(int(M), int(K), _ptr(rowptr), _ptr(colidx), _ptr(vals),
+                                                _ptr(t_rowptr), _ptr(t_colidx), _ptr(t_vals)))
+    return t_rowptr, t_colidx, t_vals
 
 
 def accspmm_partition_bounds(M, rowptr, nparts) -> np.ndarray:
@@ -273,9 +300,10 @@ class Plan:
     TF32 / float16 for FP16) and returns / fills C (float32)."""
 
     def __init__(self, M, K, rowptr, colidx, vals, precision="tf32", reorder="off", balance="auto",
-                 unit_cap=0, part=0, nparts=1, device=None, build="host"):
+                 unit_cap=0, part=0, nparts=1, device=None, build="host", permute_cols=False):
         opt = accspmm_options_default()
         opt.build = BUILD[build]
+        opt.permute_cols = int(bool(permute_cols))
         opt.precision = PRECISION[precision]
         opt.reorder = REORDER[reorder]
         opt.balance = BALANCE[balance]
@@ -322,6 +350,13 @@ class Plan:
         accspmm_execute_host(self.handle, _ptr(B_host), N, _ptr(C_host), _stream_ptr(stream))
         return C_host
 
+    def execute_host_batch(self, B_hosts, C_hosts, stream=None):
+        """Pipelined end to end over a batch of host B / C buffers (pinned for overlap)."""
+        N = B_hosts[0].shape[1]
+        accspmm_execute_host_batch(self.handle, [_ptr(b) for b in B_hosts], [_ptr(c) for c in C_hosts], N,
+                                   _stream_ptr(stream))
+        return C_hosts
+
     def export_format(self) -> dict:
         return accspmm_plan_export_format(self.handle)
 
@@ -339,9 +374,11 @@ class Plan:
 
     @property
     def launches_per_execute(self) -> int:
-        """SpMM kernel + (TF32, high B-row reuse) the rho(B) pre-pass -- mirrors accspmm_execute."""
+        """SpMM kernel + (TF32 with high B-row reuse, or permuted columns) the B pre-pass --
+        mirrors accspmm_execute."""
         i = self.info
-        pre = self.precision == "tf32" and i["K"] > 0 and i["sum_U"] >= 32 * i["K"]
+        pre = (self.precision == "tf32" and i["K"] > 0 and i["sum_U"] >= 32 * i["K"]) or \
+            (i["cols_permuted"] and i["K"] > 0)
         return 2 if pre else 1
 
     def debug_decode(self, stream=None):

@@ -20,11 +20,16 @@ struct accspmm_plan {
     mutable size_t ws_bytes = 0;
     mutable uint32_t *counters = nullptr;
     mutable size_t counters_n = 0;
-    // e2e staging buffers (grown on demand by execute_host)
+    // e2e staging buffers (grown on demand by execute_host / execute_host_batch: two slots)
     mutable void *dB = nullptr;
     mutable size_t dB_bytes = 0;
     mutable float *dC = nullptr;
     mutable size_t dC_bytes = 0;
+    mutable void *dB2 = nullptr;
+    mutable float *dC2 = nullptr;
+    // copy-engine streams and slot events of the pipelined batch path
+    mutable cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+    mutable cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_k[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
     // TF32: rounded copy of B (K x N) produced by the pre-pass of each execute
     mutable float *Br = nullptr;
     mutable size_t Br_bytes = 0;
@@ -79,8 +84,19 @@ static void free_device(accspmm_plan *p)
 {
     auto &d = p->dev;
     cudaFree(d.rwo); cudaFree(d.tco); cudaFree(d.a2b); cudaFree(d.bits); cudaFree(d.vals);
-    cudaFree(d.units); cudaFree(d.row_map);
+    cudaFree(d.units); cudaFree(d.row_map); cudaFree(d.col_perm);
     cudaFree(p->ws); cudaFree(p->counters); cudaFree(p->dB); cudaFree(p->dC); cudaFree(p->Br); cudaFree(p->zrow);
+    cudaFree(p->dB2); cudaFree(p->dC2);
+    p->dB2 = nullptr; p->dC2 = nullptr;
+    if (p->s_h2d) cudaStreamDestroy(p->s_h2d);
+    if (p->s_d2h) cudaStreamDestroy(p->s_d2h);
+    p->s_h2d = p->s_d2h = nullptr;
+    for (int k = 0; k < 2; ++k) {
+        if (p->ev_in[k]) cudaEventDestroy(p->ev_in[k]);
+        if (p->ev_k[k]) cudaEventDestroy(p->ev_k[k]);
+        if (p->ev_out[k]) cudaEventDestroy(p->ev_out[k]);
+        p->ev_in[k] = p->ev_k[k] = p->ev_out[k] = nullptr;
+    }
     for (auto e : p->ev) cudaEventDestroy(e);
     p->ev.clear();
     d = DevicePlan();
@@ -194,19 +210,27 @@ accspmm_status accspmm_plan_create_ex(int64_t M, int64_t K, const int64_t *rowpt
         wb1 = b[(size_t)opt.part + 1];
     }
     const int64_t r0 = wb0 * kWindow, r1 = std::min<int64_t>(M, wb1 * kWindow);
+    // symmetric reordering (NEXT-2): column c becomes inv_perm[c]; B is gathered as B[perm]
+    std::vector<uint32_t> colmap;
+    if (opt.permute_cols && !perm.empty()) {
+        colmap.resize((size_t)M);
+        for (int64_t r = 0; r < M; ++r) colmap[perm[(size_t)r]] = (uint32_t)r;
+    }
+    const uint32_t *cm = colmap.empty() ? nullptr : colmap.data();
+    I.cols_permuted = cm ? 1 : 0;
     HostFormat &F = p->host;
     DeviceFormat DF;
     double ms_csr_upload = 0.0;
     if (opt.build == ACCSPMM_BUILD_DEVICE) {
         cudaError_t e = cudaSetDevice(opt.device);
         if (e != cudaSuccess) { delete p; return cuda_fail(e, "cudaSetDevice"); }
-        st = build_format_device(a, vals, perm, r0, std::max(r0, r1), opt.precision, DF);
+        st = build_format_device(a, vals, perm, r0, std::max(r0, r1), opt.precision, DF, cm);
         if (st != ACCSPMM_OK) { free_device_format(DF); delete p; return st; }
         F.W = DF.W; F.NB = DF.NB; F.nnz = DF.nnz; F.rows = DF.rows; F.sum_U = DF.sum_U;
         F.rwo = DF.rwo_host;
         ms_csr_upload = DF.ms_upload;
     } else {
-        st = build_format(a, vals, perm, r0, std::max(r0, r1), opt.precision, F);
+        st = build_format(a, vals, perm, r0, std::max(r0, r1), opt.precision, F, cm);
         if (st != ACCSPMM_OK) { delete p; return st; }
     }
     if (I.nb_unreordered < 0 && opt.nparts == 1 && perm.empty()) I.nb_unreordered = F.NB;
@@ -229,8 +253,11 @@ accspmm_status accspmm_plan_create_ex(int64_t M, int64_t K, const int64_t *rowpt
     const bool balance = opt.balance == ACCSPMM_BALANCE_ON ||
                          (opt.balance == ACCSPMM_BALANCE_AUTO && ibd > kIbdThreshold);
     const int cap = opt.unit_cap > 0 ? opt.unit_cap : auto_cap(F.NB);
-    Schedule S = build_schedule(F.rwo, cap, balance, opt.precision);
-    I.ibd = ibd; I.balanced = balance ? 1 : 0; I.unit_cap = cap;
+    // AUTO below the IBD threshold keeps windows whole but groups consecutive ones
+    // into a warp's unit (reading R7b); OFF is the paper's one window per unit
+    const bool group = !balance && opt.balance == ACCSPMM_BALANCE_AUTO;
+    Schedule S = build_schedule(F.rwo, cap, balance, opt.precision, group);
+    I.ibd = ibd; I.balanced = balance ? 1 : 0; I.unit_cap = cap; I.grouped = group ? 1 : 0;
     I.n_units = (int64_t)S.units.size(); I.n_split_windows = S.n_split; I.n_segments = S.n_segments;
     p->units_host.resize(S.units.size() * 8);
     std::memcpy(p->units_host.data(), S.units.data(), S.units.size() * sizeof(Unit));
@@ -277,6 +304,7 @@ accspmm_status accspmm_plan_create_ex(int64_t M, int64_t K, const int64_t *rowpt
         }
         if (st == ACCSPMM_OK) st = upload(&d.units, p->units_host, bytes);
         if (st == ACCSPMM_OK && opt.nparts == 1 && !perm.empty()) st = upload(&d.row_map, p->orig_rows, bytes);
+        if (st == ACCSPMM_OK && cm) st = upload(&d.col_perm, perm, bytes);
         if (st == ACCSPMM_OK) {
             std::vector<uint32_t> zeros(256, 0u);  // 1 KB: covers a 128-wide FP32 feature slice
             st = upload((uint32_t **)&p->zrow, zeros, bytes);
@@ -335,11 +363,14 @@ accspmm_status accspmm_execute(const accspmm_plan *p, const void *B, int64_t N, 
     if (st != ACCSPMM_OK) return st;
     const void *Bk = B;
     // rho(B) for TF32: one elementwise pass when each B row is gathered many times
-    // (reuse = sum_w |U_w| / K >= 32), else in the kernel's registers.
+    // (reuse = sum_w |U_w| / K >= 32), else in the kernel's registers.  With permuted
+    // columns the pass is a row gather B' = B[perm] (rounding fused for the TF32 pre-pass).
     const bool tf32 = p->opt.precision == ACCSPMM_TF32;
     const bool in_kernel_round = tf32 && p->info.K > 0 && p->info.sum_U < 32 * p->info.K;
-    if (tf32 && !in_kernel_round && p->info.K > 0) {
-        const size_t need = (size_t)p->info.K * (size_t)N * sizeof(float);
+    const bool permute = p->dev.col_perm != nullptr && p->info.K > 0;
+    if (((tf32 && !in_kernel_round) || permute) && p->info.K > 0) {
+        const size_t es = tf32 ? 4 : 2;
+        const size_t need = (size_t)p->info.K * (size_t)N * es;
         if (need > p->Br_bytes) {
             cudaFree(p->Br);
             p->Br = nullptr;
@@ -347,7 +378,10 @@ accspmm_status accspmm_execute(const accspmm_plan *p, const void *B, int64_t N, 
             if (cudaMalloc((void **)&p->Br, need) != cudaSuccess) return fail(ACCSPMM_ERR_OUT_OF_MEMORY, "B scratch");
             p->Br_bytes = need;
         }
-        st = launch_round_b((const float *)B, p->Br, p->info.K * N, stream);
+        if (permute)
+            st = launch_permute_b(B, p->Br, p->dev.col_perm, p->info.K, N * (int64_t)es, tf32 && !in_kernel_round, stream);
+        else
+            st = launch_round_b((const float *)B, p->Br, p->info.K * N, stream);
         if (st != ACCSPMM_OK) return st;
         Bk = p->Br;
     }
@@ -391,6 +425,79 @@ accspmm_status accspmm_execute_host(const accspmm_plan *p, const void *B_host, i
     e = cudaMemcpyAsync(C_host, p->dC, bC, cudaMemcpyDeviceToHost, s);
     if (e != cudaSuccess) return cuda_fail(e, "D2H C");
     e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
+    return ACCSPMM_OK;
+}
+
+accspmm_status accspmm_execute_host_batch(const accspmm_plan *p, const void *const *B_hosts, void *const *C_hosts,
+                                          int32_t count, int64_t N, void *stream)
+{
+    if (!p) return fail(ACCSPMM_ERR_INVALID_VALUE, "plan is NULL");
+    if (p->opt.device < 0) return fail(ACCSPMM_ERR_UNSUPPORTED, "host-only plan cannot execute (no CPU fallback)");
+    if (N <= 0 || N % 16 != 0) return fail(N <= 0 ? ACCSPMM_ERR_INVALID_VALUE : ACCSPMM_ERR_UNSUPPORTED, "bad N");
+    if (count < 0 || (count > 0 && (!B_hosts || !C_hosts))) return fail(ACCSPMM_ERR_INVALID_VALUE, "bad batch");
+    for (int32_t i = 0; i < count; ++i)
+        if (!C_hosts[i] || (!B_hosts[i] && p->info.K > 0)) return fail(ACCSPMM_ERR_INVALID_VALUE, "B or C is NULL");
+    if (count == 0) return ACCSPMM_OK;
+    const size_t es = p->opt.precision == ACCSPMM_FP16 ? 2 : 4;
+    const size_t bB = (size_t)p->info.K * (size_t)N * es;
+    const size_t bC = (size_t)p->info.rows * (size_t)N * sizeof(float);
+    cudaStream_t s = (cudaStream_t)stream;
+    {
+        std::lock_guard<std::mutex> lk(p->mu);
+        auto grow = [&](void **a, void **b, size_t &have, size_t need) -> bool {
+            if (need <= have && *a && *b) return true;
+            cudaFree(*a); cudaFree(*b);
+            *a = *b = nullptr;
+            have = 0;
+            if (cudaMalloc(a, need ? need : 16) != cudaSuccess || cudaMalloc(b, need ? need : 16) != cudaSuccess) {
+                cudaFree(*a); cudaFree(*b);
+                *a = *b = nullptr;
+                return false;
+            }
+            have = need;
+            return true;
+        };
+        if (!grow(&p->dB, &p->dB2, p->dB_bytes, bB)) return fail(ACCSPMM_ERR_OUT_OF_MEMORY, "e2e B buffers");
+        if (!grow((void **)&p->dC, (void **)&p->dC2, p->dC_bytes, bC)) return fail(ACCSPMM_ERR_OUT_OF_MEMORY, "e2e C buffers");
+        if (!p->s_h2d) {
+            cudaError_t e = cudaStreamCreateWithFlags(&p->s_h2d, cudaStreamNonBlocking);
+            if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->s_d2h, cudaStreamNonBlocking);
+            for (int k = 0; k < 2 && e == cudaSuccess; ++k) {
+                e = cudaEventCreateWithFlags(&p->ev_in[k], cudaEventDisableTiming);
+                if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_k[k], cudaEventDisableTiming);
+                if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ev_out[k], cudaEventDisableTiming);
+            }
+            if (e != cudaSuccess) return cuda_fail(e, "batch streams/events");
+        }
+    }
+    void *dB[2] = {p->dB, p->dB2};
+    float *dC[2] = {p->dC, p->dC2};
+    // start after the caller's prior work on `stream`
+    cudaError_t e = cudaEventRecord(p->ev_k[0], s);
+    if (e == cudaSuccess) e = cudaEventRecord(p->ev_k[1], s);
+    if (e == cudaSuccess) e = cudaEventRecord(p->ev_out[0], s);
+    if (e == cudaSuccess) e = cudaEventRecord(p->ev_out[1], s);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord");
+    // three-stage pipeline over two slots: H2D(i+1) and D2H(i-1) overlap the SpMM of step i
+    for (int32_t i = 0; i < count; ++i) {
+        const int k = i & 1;
+        e = cudaStreamWaitEvent(p->s_h2d, p->ev_k[k], 0);  // the SpMM of step i-2 has read dB[k]
+        if (e == cudaSuccess) e = cudaMemcpyAsync(dB[k], B_hosts[i], bB, cudaMemcpyHostToDevice, p->s_h2d);
+        if (e == cudaSuccess) e = cudaEventRecord(p->ev_in[k], p->s_h2d);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(s, p->ev_in[k], 0);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(s, p->ev_out[k], 0);  // D2H of step i-2 has read dC[k]
+        if (e != cudaSuccess) return cuda_fail(e, "batch H2D");
+        accspmm_status st = accspmm_execute(p, dB[k], N, dC[k], stream);
+        if (st != ACCSPMM_OK) return st;
+        e = cudaEventRecord(p->ev_k[k], s);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(p->s_d2h, p->ev_k[k], 0);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(C_hosts[i], dC[k], bC, cudaMemcpyDeviceToHost, p->s_d2h);
+        if (e == cudaSuccess) e = cudaEventRecord(p->ev_out[k], p->s_d2h);
+        if (e != cudaSuccess) return cuda_fail(e, "batch D2H");
+    }
+    e = cudaStreamSynchronize(p->s_d2h);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
     return ACCSPMM_OK;
 }
@@ -461,6 +568,20 @@ accspmm_status accspmm_reorder(int64_t n, const int64_t *rowptr, const int32_t *
     } catch (const std::bad_alloc &) {
         return fail(ACCSPMM_ERR_OUT_OF_MEMORY, "reordering");
     }
+    return ACCSPMM_OK;
+}
+
+accspmm_status accspmm_csr_transpose(int64_t M, int64_t K, const int64_t *rowptr, const int32_t *colidx,
+                                    const float *vals, int64_t *t_rowptr, int32_t *t_colidx, float *t_vals)
+{
+    if (M < 0 || K < 0 || !t_rowptr) return fail(ACCSPMM_ERR_INVALID_VALUE, "bad argument");
+    if (K >= (int64_t)INT32_MAX || M >= (int64_t)INT32_MAX) return fail(ACCSPMM_ERR_UNSUPPORTED, "too large");
+    Csr a{M, K, rowptr, colidx};
+    accspmm_status st = validate_csr(a);
+    if (st != ACCSPMM_OK) return st;
+    const int64_t nnz = M ? rowptr[M] : 0;
+    if (nnz > 0 && !t_colidx) return fail(ACCSPMM_ERR_INVALID_VALUE, "t_colidx is NULL");
+    csr_transpose(a, vals, t_rowptr, t_colidx, t_vals);
     return ACCSPMM_OK;
 }
 

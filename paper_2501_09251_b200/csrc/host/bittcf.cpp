@@ -7,7 +7,9 @@
 // each condensed lane, 0 for padding (Q5), TCLocalBit = u64 occupancy with
 // bit k = r*8 + lane (Q3).  Values are placed at TCOffset[b] + popc(mask & (2^k-1)),
 // i.e. ascending bit order inside a block -- the decode rule of P:273 used in
-// reverse.  Windows are independent, so every pass is an OpenMP loop over windows.
+// reverse.  With a column map (symmetric reordering, NEXT-2) columns are relabelled
+// c -> colmap[c] before the window's condensed set is formed.  Windows are
+// independent, so every pass is an OpenMP loop over windows.
 #include <algorithm>
 #include <cstring>
 
@@ -22,14 +24,19 @@ inline int64_t orig_row(const std::vector<uint32_t> &perm, int64_t r)
     return perm.empty() ? r : (int64_t)perm[(size_t)r];
 }
 
-// sorted unique columns of reordered rows [r0, r1)
+inline int32_t col_of(const uint32_t *colmap, int32_t c) { return colmap ? (int32_t)colmap[c] : c; }
+
+// sorted unique (relabelled) columns of reordered rows [r0, r1)
 inline void window_columns(const Csr &a, const std::vector<uint32_t> &perm, int64_t r0, int64_t r1,
-                           std::vector<int32_t> &buf)
+                           std::vector<int32_t> &buf, const uint32_t *colmap = nullptr)
 {
     buf.clear();
     for (int64_t r = r0; r < r1; ++r) {
         int64_t o = orig_row(perm, r);
-        buf.insert(buf.end(), a.colidx + a.rowptr[o], a.colidx + a.rowptr[o + 1]);
+        if (colmap)
+            for (int64_t p = a.rowptr[o]; p < a.rowptr[o + 1]; ++p) buf.push_back(col_of(colmap, a.colidx[p]));
+        else
+            buf.insert(buf.end(), a.colidx + a.rowptr[o], a.colidx + a.rowptr[o + 1]);
     }
     std::sort(buf.begin(), buf.end());
     buf.erase(std::unique(buf.begin(), buf.end()), buf.end());
@@ -54,7 +61,8 @@ int64_t count_blocks(const Csr &a, const std::vector<uint32_t> &perm)
 }
 
 accspmm_status build_format(const Csr &a, const float *vals, const std::vector<uint32_t> &perm,
-                            int64_t row_begin, int64_t row_end, int precision, HostFormat &out)
+                            int64_t row_begin, int64_t row_end, int precision, HostFormat &out,
+                            const uint32_t *colmap)
 {
     const int64_t rows = row_end - row_begin;
     const int64_t W = (rows + kWindow - 1) / kWindow;
@@ -69,7 +77,7 @@ accspmm_status build_format(const Csr &a, const float *vals, const std::vector<u
 #pragma omp for schedule(dynamic, 64)
         for (int64_t w = 0; w < W; ++w) {
             int64_t r0 = row_begin + w * kWindow, r1 = std::min(row_end, r0 + kWindow);
-            window_columns(a, perm, r0, r1, buf);
+            window_columns(a, perm, r0, r1, buf, colmap);
             U[(size_t)w] = (int64_t)buf.size();
         }
     }
@@ -107,14 +115,14 @@ accspmm_status build_format(const Csr &a, const float *vals, const std::vector<u
 #pragma omp for schedule(dynamic, 64)
         for (int64_t w = 0; w < W; ++w) {
             int64_t r0 = row_begin + w * kWindow, r1 = std::min(row_end, r0 + kWindow);
-            window_columns(a, perm, r0, r1, buf);
+            window_columns(a, perm, r0, r1, buf, colmap);
             const int64_t base = rwo64[(size_t)w];
             for (size_t q = 0; q < buf.size(); ++q) out.a2b[(size_t)base * kWindow + q] = (uint32_t)buf[q];
             for (int64_t r = r0; r < r1; ++r) {
                 int64_t o = orig_row(perm, r);
                 const int lr = (int)(r - r0);
                 for (int64_t p = a.rowptr[o]; p < a.rowptr[o + 1]; ++p) {
-                    size_t pos = (size_t)(std::lower_bound(buf.begin(), buf.end(), a.colidx[p]) - buf.begin());
+                    size_t pos = (size_t)(std::lower_bound(buf.begin(), buf.end(), col_of(colmap, a.colidx[p])) - buf.begin());
                     out.bits[(size_t)base + pos / kWindow] |= 1ull << (lr * kWindow + (int)(pos % kWindow));
                 }
             }
@@ -131,13 +139,13 @@ accspmm_status build_format(const Csr &a, const float *vals, const std::vector<u
 #pragma omp for schedule(dynamic, 64)
         for (int64_t w = 0; w < W; ++w) {
             int64_t r0 = row_begin + w * kWindow, r1 = std::min(row_end, r0 + kWindow);
-            window_columns(a, perm, r0, r1, buf);
+            window_columns(a, perm, r0, r1, buf, colmap);
             const int64_t base = rwo64[(size_t)w];
             for (int64_t r = r0; r < r1; ++r) {
                 int64_t o = orig_row(perm, r);
                 const int lr = (int)(r - r0);
                 for (int64_t p = a.rowptr[o]; p < a.rowptr[o + 1]; ++p) {
-                    size_t pos = (size_t)(std::lower_bound(buf.begin(), buf.end(), a.colidx[p]) - buf.begin());
+                    size_t pos = (size_t)(std::lower_bound(buf.begin(), buf.end(), col_of(colmap, a.colidx[p])) - buf.begin());
                     size_t b = (size_t)base + pos / kWindow;
                     int k = lr * kWindow + (int)(pos % kWindow);
                     uint64_t below = out.bits[b] & ((1ull << k) - 1ull);

@@ -1,4 +1,6 @@
 // CSR validation and input rounding rho (host side of plan creation, SURVEY §3 call stack step 1-2).
+#include <algorithm>
+#include <vector>
 #include <cstring>
 
 #include "../internal.hpp"
@@ -57,6 +59,23 @@ uint16_t round_fp16_rne(float x)
     uint16_t b;
     std::memcpy(&b, &h, 2);
     return b;
+}
+
+// A^T in canonical CSR (the operand of the backward pass dB = A^T . dC).  Counting sort
+// by column; rows are visited in ascending order, so each transposed row comes out sorted.
+void csr_transpose(const Csr &a, const float *vals, int64_t *t_rowptr, int32_t *t_colidx, float *t_vals)
+{
+    const int64_t nnz = a.M ? a.rowptr[a.M] : 0;
+    std::fill(t_rowptr, t_rowptr + a.K + 1, 0);
+    for (int64_t p = 0; p < nnz; ++p) t_rowptr[a.colidx[p] + 1]++;
+    for (int64_t j = 0; j < a.K; ++j) t_rowptr[j + 1] += t_rowptr[j];
+    std::vector<int64_t> fill(t_rowptr, t_rowptr + a.K);
+    for (int64_t i = 0; i < a.M; ++i)
+        for (int64_t p = a.rowptr[i]; p < a.rowptr[i + 1]; ++p) {
+            const int64_t q = fill[(size_t)a.colidx[p]]++;
+            t_colidx[q] = (int32_t)i;
+            if (t_vals) t_vals[q] = vals ? vals[p] : 0.0f;
+        }
 }
 
 }  // namespace accspmm

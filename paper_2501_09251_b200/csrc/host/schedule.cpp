@@ -9,6 +9,9 @@
 // bytes of B per feature: 1 for TF32, 2 for FP16).  Windows longer than the cap
 // are split evenly (cross-row write-back); shorter windows are
 // concatenated while sum(blocks + wb) <= cap + wb (Fig. 7(b)).
+// Unbalanced plans (IBD <= 8 under ACCSPMM_BALANCE_AUTO) may still be `group`ed:
+// whole windows concatenated by the same rule, none split (reading R7b: a warp's
+// fixed per-unit cost is amortised over short windows).
 #include <algorithm>
 #include <cmath>
 
@@ -35,14 +38,14 @@ int auto_cap(int64_t NB)
     return (int)std::max<int64_t>(kPaperCap, std::min<int64_t>(4096, c));
 }
 
-Schedule build_schedule(const std::vector<uint32_t> &rwo, int cap, bool balance, int precision)
+Schedule build_schedule(const std::vector<uint32_t> &rwo, int cap, bool balance, int precision, bool group)
 {
     Schedule s;
     s.cap = cap;
     s.balanced = balance;
     s.ibd = compute_ibd(rwo);
     const int64_t W = rwo.size() ? (int64_t)rwo.size() - 1 : 0;
-    if (!balance) {
+    if (!balance && !group) {
         s.units.reserve((size_t)W);
         for (int64_t w = 0; w < W; ++w)
             s.units.push_back({(uint32_t)w, 1u, rwo[(size_t)w], rwo[(size_t)w + 1], kNoSplit, 0u, 1u, 0u});
@@ -58,7 +61,7 @@ Schedule build_schedule(const std::vector<uint32_t> &rwo, int cap, bool balance,
     };
     for (int64_t w = 0; w < W; ++w) {
         const int64_t nb = (int64_t)rwo[(size_t)w + 1] - (int64_t)rwo[(size_t)w];
-        if (nb > cap) {
+        if (nb > cap && balance) {
             close();
             const int64_t nseg = (nb + cap - 1) / cap;
             for (int64_t k = 0; k < nseg; ++k) {

@@ -50,17 +50,21 @@ struct Schedule {
 accspmm_status validate_csr(const Csr &a);
 float round_tf32_rna(float x);        // (bits + 0x1000) & 0xFFFFE000
 uint16_t round_fp16_rne(float x);     // IEEE binary16, ties to even
+void csr_transpose(const Csr &a, const float *vals, int64_t *t_rowptr, int32_t *t_colidx, float *t_vals);
 
 // host/bittcf.cpp -- rows [row_begin, row_end) of the row-permuted matrix
 // (perm new->old may be empty = identity); row_begin is a multiple of 8.
+// colmap (may be null): column relabelling old -> new (the inverse row permutation when
+// columns are reordered with the rows, accspmm_options.permute_cols)
 accspmm_status build_format(const Csr &a, const float *vals, const std::vector<uint32_t> &perm,
-                            int64_t row_begin, int64_t row_end, int precision, HostFormat &out);
+                            int64_t row_begin, int64_t row_end, int precision, HostFormat &out,
+                            const uint32_t *colmap = nullptr);
 int64_t count_blocks(const Csr &a, const std::vector<uint32_t> &perm);
 
 // host/schedule.cpp
 double compute_ibd(const std::vector<uint32_t> &rwo);
 int auto_cap(int64_t NB);
-Schedule build_schedule(const std::vector<uint32_t> &rwo, int cap, bool balance, int precision);
+Schedule build_schedule(const std::vector<uint32_t> &rwo, int cap, bool balance, int precision, bool group);
 
 // host/partition.cpp
 std::vector<int64_t> partition_bounds(const Csr &a, const std::vector<uint32_t> &perm, int nparts);
@@ -77,6 +81,7 @@ struct DevicePlan {
     void *vals = nullptr;
     uint32_t *units = nullptr;     // [n_units][8]
     uint32_t *row_map = nullptr;   // slab row -> C row (nparts == 1 with a permutation), else null
+    uint32_t *col_perm = nullptr;  // permute_cols: B'[i] = B[col_perm[i]] is gathered each execute
     int64_t K = 0;                 // rows of B (padding lanes gather row K -> TMA zero fill)
     // cached TMA tensor maps of the last B operand (key: ptr, N, FW, dtype): one per feature
     // slice (kMaxSliceMaps at most), else one map over all N columns
@@ -96,7 +101,8 @@ struct DeviceFormat {
     double ms_upload = 0.0, ms_build = 0.0;
 };
 accspmm_status build_format_device(const Csr &a, const float *vals, const std::vector<uint32_t> &perm,
-                                   int64_t row_begin, int64_t row_end, int precision, DeviceFormat &out);
+                                   int64_t row_begin, int64_t row_end, int precision, DeviceFormat &out,
+                                   const uint32_t *colmap = nullptr);
 void free_device_format(DeviceFormat &f);
 
 // Feature-slice width of one warp for a given N (N % 16 == 0): the widest of 128/64/32/16
@@ -107,6 +113,9 @@ int pick_fw(int64_t N);
 accspmm_status launch_spmm(const DevicePlan &p, const void *B, const void *zrow, int64_t N, float *C, float *ws,
                            uint32_t *counters, void *stream, bool round_b);
 accspmm_status launch_round_b(const float *B, float *Br, int64_t n, void *stream);
+// B' = B[perm] row gather (K rows of row_bytes), optionally with rho = TF32 RNA (f32 rows)
+accspmm_status launch_permute_b(const void *B, void *Bp, const uint32_t *perm, int64_t K, int64_t row_bytes,
+                                bool round_tf32, void *stream);
 accspmm_status launch_unpermute(const float *G, const uint32_t *orig_row, int64_t n_rows, int64_t N,
                                 float *C, void *stream);
 accspmm_status launch_round_tf32(const float *in, float *out, int64_t n, void *stream);

@@ -74,8 +74,8 @@ __global__ void row_len_kernel(const int64_t *__restrict__ rowptr, const uint32_
 // one warp per slab row: key = window << (cbits + 3) | col << 3 | row-in-window
 __global__ void keys_kernel(const int64_t *__restrict__ rowptr, const int32_t *__restrict__ colidx,
                             const float *__restrict__ vals, const uint32_t *__restrict__ perm, int64_t r0, int64_t rows,
-                            const int64_t *__restrict__ sptr, int cbits, bool f16, uint64_t *__restrict__ keys,
-                            uint32_t *__restrict__ vbits)
+                            const int64_t *__restrict__ sptr, int cbits, bool f16, const uint32_t *__restrict__ colmap,
+                            uint64_t *__restrict__ keys, uint32_t *__restrict__ vbits)
 {
     const int lane = threadIdx.x & 31;
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -84,7 +84,8 @@ __global__ void keys_kernel(const int64_t *__restrict__ rowptr, const int32_t *_
         const int64_t p0 = rowptr[o], n = rowptr[o + 1] - p0, q0 = sptr[r];
         const uint64_t hi = ((uint64_t)(r >> 3) << (cbits + 3)) | (uint64_t)(r & 7);
         for (int64_t i = lane; i < n; i += 32) {
-            keys[q0 + i] = hi | ((uint64_t)(uint32_t)colidx[p0 + i] << 3);
+            const uint32_t c = (uint32_t)colidx[p0 + i];
+            keys[q0 + i] = hi | ((uint64_t)(colmap ? colmap[c] : c) << 3);
             vbits[q0 + i] = rho_bits(vals[p0 + i], f16);
         }
     }
@@ -184,7 +185,7 @@ struct Builder {
 }  // namespace
 
 accspmm_status build_format_device(const Csr &a, const float *vals, const std::vector<uint32_t> &perm, int64_t row_begin,
-                                   int64_t row_end, int precision, DeviceFormat &out)
+                                   int64_t row_end, int precision, DeviceFormat &out, const uint32_t *colmap)
 {
     using clk = std::chrono::steady_clock;
     const auto t_start = clk::now();
@@ -214,6 +215,12 @@ accspmm_status build_format_device(const Csr &a, const float *vals, const std::v
     if (!perm.empty()) {
         if (!B.alloc(d_perm, perm.size() * 4, "perm") ||
             !B.ok(cudaMemcpyAsync(d_perm.p, perm.data(), perm.size() * 4, cudaMemcpyHostToDevice, B.s), "H2D"))
+            return B.st;
+    }
+    Scratch d_colmap;
+    if (colmap) {
+        if (!B.alloc(d_colmap, (size_t)a.K * 4, "colmap") ||
+            !B.ok(cudaMemcpyAsync(d_colmap.p, colmap, (size_t)a.K * 4, cudaMemcpyHostToDevice, B.s), "H2D"))
             return B.st;
     }
     if (!B.ok(cudaStreamSynchronize(B.s), "upload")) return B.st;
@@ -252,8 +259,9 @@ accspmm_status build_format_device(const Csr &a, const float *vals, const std::v
     if (rows > 0 && nnz > 0)
         keys_kernel<<<grid_for(rows * 32), kThreads, 0, B.s>>>(d_rowptr.get<int64_t>(), d_colidx.get<int32_t>(),
                                                                d_vals.get<float>(), permp, row_begin, rows,
-                                                               d_sptr.get<int64_t>(), cbits, f16, d_k0.get<uint64_t>(),
-                                                               d_v0.get<uint32_t>());
+                                                               d_sptr.get<int64_t>(), cbits, f16,
+                                                               colmap ? d_colmap.get<uint32_t>() : nullptr,
+                                                               d_k0.get<uint64_t>(), d_v0.get<uint32_t>());
     cub::DoubleBuffer<uint64_t> kb(d_k0.get<uint64_t>(), d_k1.get<uint64_t>());
     cub::DoubleBuffer<uint32_t> vb(d_v0.get<uint32_t>(), d_v1.get<uint32_t>());
     size_t sort_bytes = 0;

@@ -834,6 +834,30 @@ __global__ void round_b_tf32_kernel(const float4 *__restrict__ in, float4 *__res
     }
 }
 
+// B'[i] = B[perm[i]] row gather (symmetric reordering: the plan's columns are relabelled, so
+// B is permuted once per execute), optionally fused with rho = TF32 RNA.  One warp per row,
+// 16-byte vectors (row_bytes is a multiple of 32: N % 16 == 0).
+__global__ void permute_b_kernel(const uint4 *__restrict__ in, uint4 *__restrict__ out, const uint32_t *__restrict__ perm,
+                                 int64_t K, int64_t row16, bool rnd)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < K; r += warps) {
+        const uint4 *src = in + (int64_t)__ldg(perm + r) * row16;
+        uint4 *dst = out + r * row16;
+        for (int64_t e = lane; e < row16; e += 32) {
+            uint4 v = __ldcs(src + e);
+            if (rnd) {
+                v.x = tf32_rna_bits(v.x);
+                v.y = tf32_rna_bits(v.y);
+                v.z = tf32_rna_bits(v.z);
+                v.w = tf32_rna_bits(v.w);
+            }
+            dst[e] = v;
+        }
+    }
+}
+
 // ------------------------------------------------------------------ launch
 
 template <int FW, bool F16, int WARPS, bool RND = false>
@@ -996,6 +1020,20 @@ accspmm_status launch_round_b(const float *B, float *Br, int64_t n, void *stream
                                                                         reinterpret_cast<float4 *>(Br), n4);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(ACCSPMM_ERR_CUDA, std::string("round launch: ") + cudaGetErrorString(e));
+    return ACCSPMM_OK;
+}
+
+accspmm_status launch_permute_b(const void *B, void *Bp, const uint32_t *perm, int64_t K, int64_t row_bytes,
+                                bool round_tf32, void *stream)
+{
+    if (K == 0) return ACCSPMM_OK;
+    int64_t grid = (K + 7) / 8;
+    if (grid > 148 * 16) grid = 148 * 16;
+    permute_b_kernel<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const uint4 *>(B),
+                                                                     reinterpret_cast<uint4 *>(Bp), perm, K,
+                                                                     row_bytes / 16, round_tf32);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(ACCSPMM_ERR_CUDA, std::string("permute launch: ") + cudaGetErrorString(e));
     return ACCSPMM_OK;
 }
 

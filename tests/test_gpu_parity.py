@@ -301,6 +301,30 @@ def test_e2e_host_path_matches_device_path():
     assert np.array_equal(Ch, C)
 
 
+@pytest.mark.parametrize("precision", PRECISIONS)
+def test_e2e_host_batch_pipeline_matches_device_path(precision):
+    """accspmm_execute_host_batch: 5 different B (pinned and pageable) through the two-slot
+    pipeline; every C equals the device-path C of its own B bitwise."""
+    import torch
+    A = _ragged(seed=4)
+    v = gen.values_uniform(A.nnz, 1)
+    Bs = [gen.dense_normal(A.K, 64, 10 + i) for i in range(5)]
+    p = acc.Plan(A.M, A.K, A.rowptr, A.colidx, v, precision=precision)
+    ref = []
+    for B in Bs:
+        C = torch.full((A.M, 64), float("nan"), device="cuda")
+        p.execute(to_dev_B(B, precision), C)
+        ref.append(C.cpu().numpy())
+    hdt = torch.float16 if precision == "fp16" else torch.float32
+    Bh = [torch.from_numpy(B).to(hdt).pin_memory() if i % 2 == 0 else torch.from_numpy(B).to(hdt)
+          for i, B in enumerate(Bs)]
+    Ch = [torch.full((A.M, 64), float("nan")).pin_memory() for _ in Bs]
+    p.execute_host_batch(Bh, Ch)
+    for c, r in zip(Ch, ref):
+        assert np.array_equal(c.numpy(), r)
+    acc.accspmm_execute_host_batch(p.handle, [], [], 64)  # empty batch is a no-op
+
+
 def test_execute_errors():
     import torch
     A = _ragged(seed=4, M=100, K=100, nnz=500)
@@ -344,6 +368,8 @@ def _sample_rows(M, n, seed):
 @pytest.mark.parametrize("name,N,precision", [
     ("reddit", 128, "tf32"), ("reddit", 128, "fp16"), ("reddit", 32, "tf32"), ("reddit", 64, "tf32"),
     ("stencil", 128, "tf32"), ("products", 128, "tf32"), ("papers100m_small", 64, "tf32"),
+    ("reddit", 256, "tf32"), ("reddit", 512, "fp16"),
+    ("roadnet", 128, "tf32"), ("yeasth", 512, "tf32"), ("dd", 256, "fp16"), ("webberkstan", 128, "tf32"),
 ])
 def test_full_size_config_sampled(name, N, precision):
     cfg, A = gen.make_config(name)
@@ -353,6 +379,20 @@ def test_full_size_config_sampled(name, N, precision):
     rows = _sample_rows(A.M, 3000, 1)
     assert np.isfinite(C).all()
     assert_within(C, A, v, B, precision, rows=rows)
+
+
+@pytest.mark.parametrize("precision", PRECISIONS)
+def test_grouped_whole_windows_equal_one_window_per_unit(precision):
+    """Balance AUTO below the IBD threshold groups whole windows per unit (reading R7b); on
+    integer data the result equals the paper's one-window-per-unit schedule bitwise."""
+    A = gen.road_grid(300, 0.7, seed=4)
+    v = gen.values_int(A.nnz, 3)
+    B = gen.dense_int(A.K, 128, 4)
+    C_auto, pa = run(A, v, B, precision, balance="auto")
+    C_off, po = run(A, v, B, precision, balance="off")
+    assert pa.info["grouped"] == 1 and pa.info["n_units"] < po.info["n_units"] == po.info["W"]
+    assert_bit_exact(C_auto, A, v, B, precision)
+    assert np.array_equal(C_auto, C_off)
 
 
 @pytest.mark.parametrize("name,N,reorder", [("reddit", 128, "auto"), ("papers100m_small", 64, "off")])
@@ -401,3 +441,42 @@ def test_random_shapes_and_options(seed):
         B = gen.dense_normal(K, N, seed + 1)
         C, _ = run(A, v, B, precision, balance=balance, unit_cap=cap, reorder=reorder)
         assert_within(C, A, v, B, precision)
+
+
+@pytest.mark.parametrize("precision", PRECISIONS)
+@pytest.mark.parametrize("shape", ["graph", "road"])
+def test_permute_cols_exact(precision, shape):
+    """Symmetric reordering (permute_cols): B' = B[perm] is gathered on the
+    device (fused with the TF32 pre-round on high-reuse graphs, without it on the road grid
+    where rho(B) stays in the kernel); integer data bit-exact, floats within tolerance."""
+    if shape == "graph":
+        A = gen.dcsbm(5000, 250_000, 6, 2.2, 0.15, 3000, seed=8, oversample=1.3)
+    else:
+        A = gen.road_grid(200, 0.7, seed=8)
+    v = gen.values_int(A.nnz, 1)
+    B = gen.dense_int(A.K, 128, 2)
+    C, p = run(A, v, B, precision, reorder="on", permute_cols=True)
+    assert p.info["cols_permuted"] == 1 and p.launches_per_execute == 2
+    assert_bit_exact(C, A, v, B, precision)
+    vf = gen.values_uniform(A.nnz, 3)
+    Bf = gen.dense_normal(A.K, 256, 4)
+    Cf, _ = run(A, vf, Bf, precision, reorder="on", permute_cols=True)
+    assert_within(Cf, A, vf, Bf, precision)
+
+
+def test_permute_cols_partitions_and_device_build():
+    import torch
+    A = gen.dcsbm(4000, 200_000, 6, 2.2, 0.2, 2500, seed=6, oversample=1.3)
+    v = gen.values_int(A.nnz, 1)
+    B = gen.dense_int(A.K, 64, 2)
+    Cfull, _ = run(A, v, B, "tf32", reorder="on", permute_cols=True)
+    out = torch.full((A.M, 64), float("nan"), device="cuda")
+    for part in range(3):
+        for build in ("host", "device"):
+            p = acc.Plan(A.M, A.K, A.rowptr, A.colidx, v, reorder="on", permute_cols=True, part=part, nparts=3,
+                         build=build)
+            G = p.execute(to_dev_B(B, "tf32"))
+            rows = torch.from_numpy(p.export_rows().astype(np.int64)).cuda()
+            out[rows] = G
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), Cfull)

@@ -131,14 +131,24 @@ def test_empty_matrices():
         A = gen.Csr(M, K, np.zeros(M + 1, np.int64), np.zeros(0, np.int32))
         p = host_plan(A, np.zeros(0, np.float32))
         assert p.info["NB"] == 0 and p.info["W"] == (M + 7) // 8
-        assert p.export_units().shape[0] == p.info["W"]
+        u = p.export_units()
+        assert u.shape[0] == (0 if M == 0 else 1)  # AUTO groups the empty windows into one unit
+        ob.check_coverage([tuple(int(x) for x in r) for r in u], np.zeros(p.info["W"] + 1, np.int64))
+        off = host_plan(A, np.zeros(0, np.float32), balance="off")
+        assert off.export_units().shape[0] == p.info["W"]
 
 
 @pytest.mark.parametrize("balance", ["off", "on", "auto"])
 @pytest.mark.parametrize("cap", [0, 32, 100])
 @pytest.mark.parametrize("precision", ["tf32", "fp16"])
-def test_schedule_bit_exact_vs_oracle(balance, cap, precision):
-    A = gen.dcsbm(4000, 160_000, 7, 2.3, 0.25, 2500, seed=11, oversample=1.3)
+@pytest.mark.parametrize("shape", ["powerlaw", "road"])
+def test_schedule_bit_exact_vs_oracle(balance, cap, precision, shape):
+    """Units equal the oracle's, for a high-IBD graph (AUTO balances) and a low-IBD road grid
+    (AUTO keeps windows whole but groups them, reading R7b)."""
+    if shape == "powerlaw":
+        A = gen.dcsbm(4000, 160_000, 7, 2.3, 0.25, 2500, seed=11, oversample=1.3)
+    else:
+        A = gen.road_grid(120, 0.7, seed=2)
     p = host_plan(A, gen.values_uniform(A.nnz, 1), balance=balance, unit_cap=cap, precision=precision)
     I = p.info
     F = p.export_format()
@@ -149,7 +159,11 @@ def test_schedule_bit_exact_vs_oracle(balance, cap, precision):
     assert I["balanced"] == int(on)
     expect_cap = cap if cap > 0 else ob.auto_cap(I["NB"])
     assert I["unit_cap"] == expect_cap
-    ref = np.array(ob.build_units(rwo, expect_cap, on, precision), dtype=np.uint64).astype(np.uint32)
+    group = balance == "auto" and not on
+    assert I["grouped"] == int(group)
+    if shape == "road":
+        assert not on or balance == "on"
+    ref = np.array(ob.build_units(rwo, expect_cap, on, precision, group=group), dtype=np.uint64).astype(np.uint32)
     got = p.export_units()
     assert got.shape == ref.shape and np.array_equal(got, ref)
     ob.check_coverage([tuple(int(x) for x in u) for u in got], rwo)
@@ -216,3 +230,61 @@ def test_reordered_plan_format(mode):
         assert p.info["nb_unreordered"] == base["NB"]
         assert (p.info["reorder_applied"] == 1) == (ref["NB"] < base["NB"]) or p.info["reorder_applied"] == 0
     assert p.info["NB"] <= base["NB"] or mode == "on"
+
+
+@pytest.mark.parametrize("shape", [(300, 170, 4000), (1, 9, 3), (40, 1, 12), (0, 5, 0), (13, 9, 0)])
+def test_csr_transpose_vs_scipy(shape):
+    """accspmm_csr_transpose (the backward-pass operand A^T) equals scipy's transpose exactly."""
+    import scipy.sparse as sp
+    M, K, nnz = shape
+    A = gen.uniform_random(M, K, nnz, seed=M + K) if nnz else gen.Csr(M, K, np.zeros(M + 1, np.int64),
+                                                                      np.zeros(0, np.int32))
+    v = gen.values_uniform(A.nnz, 3)
+    tr, tc, tv = acc.accspmm_csr_transpose(A.M, A.K, A.rowptr, A.colidx, v)
+    ref = sp.csr_matrix((v, A.colidx, A.rowptr), shape=(M, K)).T.tocsr()
+    ref.sort_indices()
+    assert np.array_equal(tr, ref.indptr.astype(np.int64))
+    assert np.array_equal(tc, ref.indices.astype(np.int32))
+    assert np.array_equal(tv, ref.data.astype(np.float32))
+    if A.nnz:
+        t2 = acc.accspmm_csr_transpose(K, M, tr, tc, tv)
+        assert np.array_equal(t2[0], A.rowptr) and np.array_equal(t2[1], A.colidx) and np.array_equal(t2[2], v)
+
+
+def test_csr_transpose_rejects_invalid():
+    with pytest.raises(acc.AccSpmmError) as ei:
+        acc.accspmm_csr_transpose(2, 4, np.array([0, 2, 3]), np.array([3, 1, 0]), np.ones(3, np.float32))
+    assert ei.value.status == 2
+
+
+@pytest.mark.parametrize("precision", ["tf32", "fp16"])
+@pytest.mark.parametrize("nparts", [1, 3])
+def test_permute_cols_format_is_symmetric_permutation(precision, nparts):
+    """permute_cols: the plan holds BitTCF of A' = P A P^T (rows and columns relabelled by the
+    same Alg. 1 permutation) -- encoded independently by the oracle."""
+    A = gen.dcsbm(2000, 60_000, 6, 2.2, 0.1, 800, seed=5, oversample=1.3)
+    v = gen.values_uniform(A.nnz, 2)
+    full = host_plan(A, v, precision=precision, reorder="on", permute_cols=True)
+    assert full.info["cols_permuted"] == 1 and full.info["reorder_applied"] == 1
+    perm = full.export_rows().astype(np.int64)            # new -> old
+    inv = np.empty_like(perm)
+    inv[perm] = np.arange(A.M)
+    r, c = inv[A.row_ids()], inv[A.colidx.astype(np.int64)]
+    order = np.lexsort((c, r))
+    Ap = gen.csr_from_pairs(r[order], c[order], A.M, A.K)
+    vp = v[order]
+    rows_seen = 0
+    for part in range(nparts):
+        p = host_plan(A, v, precision=precision, reorder="on", permute_cols=True, part=part, nparts=nparts)
+        I = p.info
+        lo, hi = I["row_begin"], I["row_begin"] + I["rows"]
+        sl = gen.csr_from_pairs(Ap.row_ids()[(Ap.row_ids() >= lo) & (Ap.row_ids() < hi)] - lo,
+                                Ap.colidx[(Ap.row_ids() >= lo) & (Ap.row_ids() < hi)], hi - lo, A.K)
+        vs = vp[(Ap.row_ids() >= lo) & (Ap.row_ids() < hi)]
+        ref = bt.encode(sl.M, sl.K, sl.rowptr, sl.colidx, _rho_vals(vs, precision))
+        _check_format(p.export_format(), ref, precision)
+        rows_seen += I["rows"]
+    assert rows_seen == A.M
+    # without a permutation (reorder off) the option changes nothing
+    off = host_plan(A, v, precision=precision, reorder="off", permute_cols=True)
+    assert off.info["cols_permuted"] == 0
