@@ -44,7 +44,7 @@ def parse():
     ap.add_argument("--balance", default="auto", choices=["off", "on", "auto"])
     ap.add_argument("--unit-cap", type=int, default=0)
     ap.add_argument("--permute-cols", action="store_true", help="symmetric reordering: relabel columns too")
-    ap.add_argument("--build", default="host", choices=["host", "device"], help="BitTCF builder")
+    ap.add_argument("--build", default="device", choices=["host", "device"], help="BitTCF builder")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-flush", action="store_true")

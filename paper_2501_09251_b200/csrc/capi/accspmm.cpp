@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -366,7 +367,11 @@ accspmm_status accspmm_execute(const accspmm_plan *p, const void *B, int64_t N, 
     // (reuse = sum_w |U_w| / K >= 32), else in the kernel's registers.  With permuted
     // columns the pass is a row gather B' = B[perm] (rounding fused for the TF32 pre-pass).
     const bool tf32 = p->opt.precision == ACCSPMM_TF32;
-    const bool in_kernel_round = tf32 && p->info.K > 0 && p->info.sum_U < 32 * p->info.K;
+    // ACCSPMM_ROUND_B = 1 (pass) / 2 (kernel) overrides the reuse rule for A/B measurements
+    const char *rb = std::getenv("ACCSPMM_ROUND_B");
+    const int rmode = rb ? std::atoi(rb) : 0;
+    const bool in_kernel_round = tf32 && p->info.K > 0 &&
+                                 (rmode == 2 || (rmode != 1 && p->info.sum_U < kRoundReuse * p->info.K));
     const bool permute = p->dev.col_perm != nullptr && p->info.K > 0;
     if (((tf32 && !in_kernel_round) || permute) && p->info.K > 0) {
         const size_t es = tf32 ? 4 : 2;

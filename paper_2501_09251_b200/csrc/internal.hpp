@@ -14,6 +14,9 @@ constexpr uint32_t kPadLane = 0xFFFFFFFFu;  // device SparseAToB padding lane (r
 constexpr int kWmax = 31;             // windows per concatenated unit (one per lane of the window table)
 constexpr double kIbdThreshold = 8.0; // P:417 "When IBD exceeds 8"
 constexpr int kPaperCap = 32;         // P:446 "maximum threshold of 32 TC blocks per TB"
+// TF32 rho(B): a separate rounding pass over B when every B row is gathered at least this
+// many times on average (sum_w |U_w| >= kRoundReuse * K), else cvt.rna in the kernel
+constexpr int64_t kRoundReuse = 32;
 
 // Error plumbing (thread-local message returned by accspmm_last_error).
 accspmm_status fail(accspmm_status s, const std::string &msg);
