@@ -505,12 +505,35 @@ struct G4Cfg {
     static constexpr int STAGE_AL = 2 * GRP;
 };
 
-template <int FW, bool F16, int STAGES>
+// A-stream chunk of the gather4 kernel: CH blocks of SparseAToB / TCLocalBit / TCOffset (plus
+// the end offset), and with VST the chunk's value range staged by cp.async (kVBytes at most;
+// values beyond it are read from global memory)
+constexpr uint32_t kVBytes = 512;
+template <int CH, bool VST>
+struct alignas(16) ChunkG4 {  // 16-byte aligned: cp.async 16 B into a2b
+    uint32_t a2b[CH * 8];
+    uint64_t mask[CH];
+    uint32_t tco[CH + 4];
+    uint32_t vbuf[VST ? kVBytes / 4 : 1];
+};
+
+template <int FW, bool F16, int STAGES, int CH = kChunk, bool VST = false>
 struct G4WarpSmem {
     alignas(128) uint8_t stage[STAGES][G4Cfg<FW, F16>::STAGE_AL];
-    ChunkSmem ch[2];
+    ChunkG4<CH, VST> ch[2];
     uint64_t bar[STAGES];
 };
+static_assert(sizeof(ChunkG4<16, false>) % 16 == 0 && sizeof(ChunkG4<8, true>) % 16 == 0, "chunk alignment");
+
+__device__ __forceinline__ void tma_gather4_nohint(uint32_t dst, const CUtensorMap *map, int32_t col, int32_t r0,
+                                                   int32_t r1, int32_t r2, int32_t r3, uint32_t bar)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n"
+        ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar)
+        : "memory");
+}
 
 __device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap *map, int32_t col, int32_t r0, int32_t r1,
                                             int32_t r2, int32_t r3, uint32_t bar, uint64_t pol)
@@ -535,13 +558,15 @@ struct G4MapsT {
 using G4Maps = G4MapsT<kMaxSliceMaps>;
 inline int map_count(const KParams &kp) { return kp.nslices > 1 && kp.nslices <= kMaxSliceMaps ? kp.nslices : 1; }
 
-template <int FW, bool F16, int WARPS, int STAGES, bool RND, int MINB = 1, int DIST = 1, int NM = 1>
+template <int FW, bool F16, int WARPS, int STAGES, bool RND, int MINB = 1, int DIST = 1, int NM = 1, bool VST = false,
+          bool HINT = true>
 __global__ void __launch_bounds__(WARPS * 32, MINB)
     spmm_bittcf_g4_kernel(const KParams p, const __grid_constant__ G4MapsT<NM> maps)
 {
+    constexpr int CH = VST ? 8 : kChunk;  // blocks per staged chunk
     using CF = Cfg<FW, F16>;
     using GC = G4Cfg<FW, F16>;
-    using SM = G4WarpSmem<FW, F16, STAGES>;
+    using SM = G4WarpSmem<FW, F16, STAGES, CH, VST>;
     using V = typename CF::V;
     constexpr int MT = CF::MT, NV = CF::NV, VW = CF::VW;
     extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -578,18 +603,33 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
 
     auto issue_chunk = [&](uint32_t i) {
         if (i < nblk) {
-            ChunkSmem &c = sm.ch[(i / kChunk) & 1];
+            auto &c = sm.ch[(i / CH) & 1];
             const uint32_t b = b0 + i;
-            const uint32_t cnt = min((uint32_t)kChunk, nblk - i);
-            if ((uint32_t)lane < cnt) {
-                cp_async8(smem_u32(&c.mask[lane]), p.bits + b + lane, pol_stream);
-                cp_async4(smem_u32(&c.tco[lane]), p.tco + b + lane, pol_stream);
-            }
+            const uint32_t cnt = min((uint32_t)CH, nblk - i);
+            if ((uint32_t)lane < cnt) cp_async8(smem_u32(&c.mask[lane]), p.bits + b + lane, pol_stream);
+            // VST also needs the end offset TCOffset[b + cnt] (the chunk's value range)
+            if ((uint32_t)lane < cnt + (VST ? 1u : 0u)) cp_async4(smem_u32(&c.tco[lane]), p.tco + b + lane, pol_stream);
             const uint4 *src4 = reinterpret_cast<const uint4 *>(p.a2b + (size_t)b * 8);
             if ((uint32_t)lane < 2 * cnt) cp_async16(smem_u32(&c.a2b[4 * lane]), src4 + lane, pol_stream);
-            if ((uint32_t)lane + 32 < 2 * cnt) cp_async16(smem_u32(&c.a2b[4 * (lane + 32)]), src4 + lane + 32, pol_stream);
+            if (2 * CH > 32 && (uint32_t)lane + 32 < 2 * cnt)
+                cp_async16(smem_u32(&c.a2b[4 * (lane + 32)]), src4 + lane + 32, pol_stream);
         }
         cp_async_commit();
+    };
+    // VST: stage the value range of the chunk starting at block i (its TCOffsets have landed)
+    auto issue_values = [&](uint32_t i) {
+        if constexpr (VST) {
+            if (i < nblk) {
+                auto &c = sm.ch[(i / CH) & 1];
+                const uint32_t cnt = min((uint32_t)CH, nblk - i);
+                const uint32_t lo = (c.tco[0] * CF::ES) & ~3u;
+                const uint32_t hi = min(lo + kVBytes, (c.tco[cnt] * CF::ES + 3u) & ~3u);
+                const char *src = reinterpret_cast<const char *>(p.vals);
+                for (uint32_t o = lo + 4u * (uint32_t)lane; o < hi; o += 128u)
+                    cp_async4(smem_u32(reinterpret_cast<const char *>(c.vbuf) + (o - lo)), src + o, pol_stream);
+            }
+            cp_async_commit();
+        }
     };
 
     // Value registers of the blocks in flight: decoded and loaded DIST blocks ahead of use
@@ -600,14 +640,31 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
 
     // ---- every lane: decode this lane's two tile entries of block j, load values
     auto value_load = [&](uint32_t j, int slot) {
-        const ChunkSmem &c = sm.ch[(j / kChunk) & 1];
-        const uint32_t cs = j & (kChunk - 1u);
+        const auto &c = sm.ch[(j / CH) & 1];
+        const uint32_t cs = j & (CH - 1u);
         const uint64_t mask = c.mask[cs];
         const uint32_t t0 = c.tco[cs];
         bool p0, p1;
         const uint32_t i0 = t0 + tile_rank(mask, sh0, p0);
         const uint32_t i1 = t0 + tile_rank(mask, sh1, p1);
-        if constexpr (!F16) {
+        if constexpr (VST) {  // staged range first, global memory beyond it
+            const uint32_t lo = (c.tco[0] * CF::ES) & ~3u;
+            const uint32_t o0 = i0 * CF::ES - lo, o1 = i1 * CF::ES - lo;
+            const char *vb = reinterpret_cast<const char *>(c.vbuf);
+            if constexpr (!F16) {
+                const float *vp = reinterpret_cast<const float *>(p.vals);
+                vb0[slot] = p0 ? (o0 < kVBytes ? *reinterpret_cast<const uint32_t *>(vb + o0)
+                                               : __float_as_uint(__ldg(vp + i0))) : 0u;
+                vb1[slot] = p1 ? (o1 < kVBytes ? *reinterpret_cast<const uint32_t *>(vb + o1)
+                                               : __float_as_uint(__ldg(vp + i1))) : 0u;
+            } else {
+                const unsigned short *vp = reinterpret_cast<const unsigned short *>(p.vals);
+                vb0[slot] = p0 ? (o0 < kVBytes ? (uint32_t)*reinterpret_cast<const uint16_t *>(vb + o0)
+                                               : (uint32_t)__ldg(vp + i0)) : 0u;
+                vb1[slot] = p1 ? (o1 < kVBytes ? (uint32_t)*reinterpret_cast<const uint16_t *>(vb + o1)
+                                               : (uint32_t)__ldg(vp + i1)) : 0u;
+            }
+        } else if constexpr (!F16) {
             const float *vp = reinterpret_cast<const float *>(p.vals);
             vb0[slot] = p0 ? __float_as_uint(__ldg(vp + i0)) : 0u;
             vb1[slot] = p1 ? __float_as_uint(__ldg(vp + i1)) : 0u;
@@ -622,8 +679,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     // ---- lane 0: two gather4 of block j's B rows into stage s
     auto issue_tma = [&](uint32_t j, int s) {
         if (lane == 0) {
-            const ChunkSmem &c = sm.ch[(j / kChunk) & 1];
-            const uint32_t cs = j & (kChunk - 1u);
+            const auto &c = sm.ch[(j / CH) & 1];
+            const uint32_t cs = j & (CH - 1u);
             // padding lanes hold 0xFFFFFFFF on the device (row -1): the TMA zero-fills them
             const uint4 ca = *reinterpret_cast<const uint4 *>(&c.a2b[cs * 8]);
             const uint4 cb = *reinterpret_cast<const uint4 *>(&c.a2b[cs * 8 + 4]);
@@ -637,7 +694,15 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
             // derived here, not held across the loop (registers are the occupancy limit)
             const CUtensorMap *tmap = &maps.m[NM > 1 ? slice : 0];
             const int32_t tcol = NM > 1 ? 0 : slice * FW;
-            if constexpr (!F16) {
+            if constexpr (!HINT) {
+                if constexpr (!F16) {
+                    tma_gather4_nohint(st, tmap, tcol, r0, r1, r2, r3, bar);
+                    tma_gather4_nohint(st + GC::GRP, tmap, tcol, r4, r5, r6, r7, bar);
+                } else {
+                    tma_gather4_nohint(st, tmap, tcol, r0, r2, r4, r6, bar);
+                    tma_gather4_nohint(st + GC::GRP, tmap, tcol, r1, r3, r5, r7, bar);
+                }
+            } else if constexpr (!F16) {
                 tma_gather4(st, tmap, tcol, r0, r1, r2, r3, bar, pol_keep);
                 tma_gather4(st + GC::GRP, tmap, tcol, r4, r5, r6, r7, bar, pol_keep);
             } else {
@@ -744,7 +809,12 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     issue_chunk(0);
     cp_async_wait_all();
     __syncwarp();
-    issue_chunk(kChunk);
+    if constexpr (VST) {
+        issue_values(0);
+        cp_async_wait_all();
+        __syncwarp();
+    }
+    issue_chunk(CH);
     after_block(b0);
 #pragma unroll
     for (int d = 0; d < DIST; ++d)
@@ -755,16 +825,21 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     static_assert(STAGES == 2, "the block step below is written for a 2-stage TMA ring");
     auto step = [&](uint32_t j, int u, bool checked) {
         const uint32_t jt = j + 1, jv = j + DIST;
-        if (DIST == 1 && (jv & (kChunk - 1u)) == 0) {  // chunk (jv / kChunk) must have landed
+        if (DIST == 1 && (jv & (CH - 1u)) == 0) {  // chunk (jv / CH) must have landed
             cp_async_wait_all();
             __syncwarp();
-            issue_chunk(jv + kChunk);
+            issue_chunk(jv + CH);
+        }
+        if (VST && (jv & (CH - 1u)) == CH / 2) {  // mid-chunk: the next chunk's offsets have landed
+            cp_async_wait_all();
+            __syncwarp();
+            issue_values((jv | (CH - 1u)) + 1u);
         }
         if (!checked || jt < nblk) issue_tma(jt, (u + 1) & 1);
-        if (DIST == 2 && (jv & (kChunk - 1u)) == 0) {
+        if (DIST == 2 && (jv & (CH - 1u)) == 0) {
             cp_async_wait_all();
             __syncwarp();
-            issue_chunk(jv + kChunk);
+            issue_chunk(jv + CH);
         }
         if (!checked || jv < nblk) value_load(jv, (u + DIST) & (VR - 1));
         consume(j, u & 1, u & (VR - 1));
@@ -881,12 +956,13 @@ int env_int(const char *name, int dflt)
 
 // NM = 1: one tensor map (the full-width map when several slices exist); NM = kMaxSliceMaps:
 // one map per slice (tensor_map decides; only the default configurations instantiate it)
-template <int FW, bool F16, int WARPS, int STAGES, bool RND = false, int MINB = 1, int DIST = 1, int NM = 1>
+template <int FW, bool F16, int WARPS, int STAGES, bool RND = false, int MINB = 1, int DIST = 1, int NM = 1,
+          bool VST = false, bool HINT = true>
 accspmm_status launch_g4(const KParams &kp, const G4Maps *map, int64_t n_units, cudaStream_t stream)
 {
-    using SM = G4WarpSmem<FW, F16, STAGES>;
+    using SM = G4WarpSmem<FW, F16, STAGES, VST ? 8 : kChunk, VST>;
     const size_t smem = sizeof(SM) * WARPS;
-    auto kern = spmm_bittcf_g4_kernel<FW, F16, WARPS, STAGES, RND, MINB, DIST, NM>;
+    auto kern = spmm_bittcf_g4_kernel<FW, F16, WARPS, STAGES, RND, MINB, DIST, NM, VST, HINT>;
     static int configured_device = -1;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -979,6 +1055,7 @@ accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, 
             if (multi) return launch_g4<FW, F16, 2, 2, true, MB, 1, NM>(kp, map, n_units, stream);
             switch (kcfg) {
             case 20: return launch_g4<FW, F16, 2, 2, true, 1>(kp, map, n_units, stream);
+            case 42: return launch_g4<FW, F16, 1, 2, true, 2 * MB>(kp, map, n_units, stream);
             default: return launch_g4<FW, F16, 2, 2, true, MB>(kp, map, n_units, stream);
             }
         }
@@ -989,6 +1066,9 @@ accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, 
         case 24: return launch_g4<FW, F16, 2, 2, false, 10>(kp, map, n_units, stream);
         case 31: return launch_g4<FW, F16, 2, 2, false, 12>(kp, map, n_units, stream);
         case 33: return launch_g4<FW, F16, 2, 2, false, 16>(kp, map, n_units, stream);
+        case 40: return launch_g4<FW, F16, 2, 2, false, MB, 1, 1, true>(kp, map, n_units, stream);
+        case 42: return launch_g4<FW, F16, 1, 2, false, 2 * MB>(kp, map, n_units, stream);
+        case 43: return launch_g4<FW, F16, 2, 2, false, MB, 1, 1, false, false>(kp, map, n_units, stream);
         default: return launch_g4<FW, F16, 2, 2, false, MB>(kp, map, n_units, stream);
         }
     }

@@ -24,6 +24,9 @@ def main():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--variants", nargs="+", default=["kcfg=0"])
     ap.add_argument("--out", default=None)
+    ap.add_argument("--rounds", type=int, default=1,
+                    help="interleave the variants this many times (A B A B ...) and pool the samples: "
+                         "clock/power drift over the run then hits every variant alike")
     a = ap.parse_args()
     cfg, A = gen.make_config(a.config)
     vals = gen.values_uniform(A.nnz, cfg.seed_A + 1)
@@ -31,7 +34,8 @@ def main():
     flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
     plans = {}
     res = []
-    for v in a.variants:
+    samples = {}
+    for rnd, v in [(r, v) for r in range(a.rounds) for v in a.variants]:
         kv = dict(x.split("=") for x in v.split(",") if x)
         N = int(kv.get("N", a.N))
         prec = kv.get("precision", "tf32")
@@ -60,9 +64,13 @@ def main():
             e1.record()
             e1.synchronize()
             ts.append(e0.elapsed_time(e1))
+        samples.setdefault(v, []).extend(ts)
+        if rnd < a.rounds - 1:
+            continue
+        ts = samples[v]
         ms = float(np.median(ts))
         bm = acc.bytes_model(p.info, N)
-        r = {"variant": v, "ms": ms, "ms_min": float(min(ts)), "GFLOPs": bm["flops"] / ms / 1e6,
+        r = {"variant": v, "ms": ms, "ms_min": float(min(ts)), "samples": len(ts), "GFLOPs": bm["flops"] / ms / 1e6,
              "model_GBs": bm["total"] / ms / 1e6, "NB": p.info["NB"], "sum_U": p.info["sum_U"],
              "units": p.info["n_units"], "cap": p.info["unit_cap"], "balanced": p.info["balanced"],
              "split": p.info["n_split_windows"], "reorder_ms": p.info["ms_reorder"],
