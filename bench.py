@@ -195,7 +195,9 @@ def kernel_name(args):
     """The SpMM kernel flavour the library's default dispatch picks."""
     kcfg = int(os.environ.get("ACCSPMM_KCFG", "-1"))
     g4 = kcfg < 0 or kcfg >= 20
-    return "spmm_bittcf_g4_kernel (TMA gather4)" if g4 else "spmm_bittcf_kernel (register-direct gather)"
+    if not g4:
+        return "spmm_bittcf_kernel (register-direct gather)"
+    return "spmm_bittcf_g4_kernel (TMA gather4, " + ("1 warp/CTA)" if kcfg < 0 else "variant %d)" % kcfg)
 
 
 def emit(out, args):

@@ -125,6 +125,22 @@ __device__ __forceinline__ void mma_f16(float (&d)[4], uint32_t a0, uint32_t a1,
         : "r"(a0), "r"(a1), "r"(b0));
 }
 
+// ldmatrix .trans: the stored 8x8 b16 matrices are (gathered row k) x (8 consecutive features);
+// thread (g, t) receives (k = 2t, 2t+1) of feature g packed -- the m16n8k8 A fragment
+__device__ __forceinline__ void ldsm_x4_trans(uint32_t &r0, uint32_t &r1, uint32_t &r2, uint32_t &r3, uint32_t addr)
+{
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x2_trans(uint32_t &r0, uint32_t &r1, uint32_t addr)
+{
+    asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0,%1}, [%2];\n" : "=r"(r0), "=r"(r1) : "r"(addr));
+}
+__device__ __forceinline__ void st_cs1(float *p, float a)
+{
+    asm volatile("st.global.cs.f32 [%0], %1;\n" ::"l"(p), "f"(a) : "memory");
+}
+
 __device__ __forceinline__ void st_cs(float *p, float a, float b, float c, float d)
 {
     asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};\n" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
@@ -559,10 +575,15 @@ using G4Maps = G4MapsT<kMaxSliceMaps>;
 inline int map_count(const KParams &kp) { return kp.nslices > 1 && kp.nslices <= kMaxSliceMaps ? kp.nslices : 1; }
 
 template <int FW, bool F16, int WARPS, int STAGES, bool RND, int MINB = 1, int DIST = 1, int NM = 1, bool VST = false,
-          bool HINT = true>
+          bool HINT = true, bool LDSM_ = false>
 __global__ void __launch_bounds__(WARPS * 32, MINB)
     spmm_bittcf_g4_kernel(const KParams p, const __grid_constant__ G4MapsT<NM> maps)
 {
+    // LDSM (FP16 only): A fragments by ldmatrix.trans straight from the gathered rows (no
+    // PRMT packing); gather y is fetched 8 columns early so its rows sit 16 B off gather x's
+    // and the 8 row addresses of every ldmatrix phase hit 8 distinct bank groups.  The
+    // accumulator layout is then m16 tile mt = features 16mt .. 16mt+15 (epilogue below).
+    constexpr bool LDSM = LDSM_ && F16;
     constexpr int CH = VST ? 8 : kChunk;  // blocks per staged chunk
     using CF = Cfg<FW, F16>;
     using GC = G4Cfg<FW, F16>;
@@ -694,20 +715,21 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
             // derived here, not held across the loop (registers are the occupancy limit)
             const CUtensorMap *tmap = &maps.m[NM > 1 ? slice : 0];
             const int32_t tcol = NM > 1 ? 0 : slice * FW;
+            const int32_t tcol_y = LDSM ? tcol - 8 : tcol;
             if constexpr (!HINT) {
                 if constexpr (!F16) {
                     tma_gather4_nohint(st, tmap, tcol, r0, r1, r2, r3, bar);
                     tma_gather4_nohint(st + GC::GRP, tmap, tcol, r4, r5, r6, r7, bar);
                 } else {
                     tma_gather4_nohint(st, tmap, tcol, r0, r2, r4, r6, bar);
-                    tma_gather4_nohint(st + GC::GRP, tmap, tcol, r1, r3, r5, r7, bar);
+                    tma_gather4_nohint(st + GC::GRP, tmap, tcol_y, r1, r3, r5, r7, bar);
                 }
             } else if constexpr (!F16) {
                 tma_gather4(st, tmap, tcol, r0, r1, r2, r3, bar, pol_keep);
                 tma_gather4(st + GC::GRP, tmap, tcol, r4, r5, r6, r7, bar, pol_keep);
             } else {
                 tma_gather4(st, tmap, tcol, r0, r2, r4, r6, bar, pol_keep);
-                tma_gather4(st + GC::GRP, tmap, tcol, r1, r3, r5, r7, bar, pol_keep);
+                tma_gather4(st + GC::GRP, tmap, tcol_y, r1, r3, r5, r7, bar, pol_keep);
             }
         }
     };
@@ -722,7 +744,26 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
         const uint8_t *st = sm.stage[s];
         const uint8_t *ra = st + t * GC::RS + CF::VB * g;
         const uint8_t *rb = st + GC::GRP + t * GC::RS + CF::VB * g;
-        if constexpr (!F16 && CF::VW == 4) {
+        if constexpr (LDSM) {
+            // lane L addresses row k = L & 7 of matrix L >> 3 (8 features); k even in gather x,
+            // k odd in gather y (+16 B: its column window starts 8 features early)
+            const int k = lane & 7, mx = lane >> 3;
+            const uint32_t row = smem_u32(st) + ((k & 1) ? GC::GRP + 16u : 0u) + (uint32_t)(k >> 1) * GC::RS;
+            const uint32_t bv = vb0[slot] | (vb1[slot] << 16);
+            if constexpr (FW >= 32) {
+#pragma unroll
+                for (int q = 0; q < FW / 32; ++q) {
+                    uint32_t a0, a1, a2, a3;
+                    ldsm_x4_trans(a0, a1, a2, a3, row + (uint32_t)(mx * 16 + q * 64));
+                    mma_f16(acc[2 * q], a0, a1, bv);
+                    mma_f16(acc[2 * q + 1], a2, a3, bv);
+                }
+            } else {
+                uint32_t a0, a1;
+                ldsm_x2_trans(a0, a1, row + (uint32_t)((mx & 1) * 16));
+                mma_f16(acc[0], a0, a1, bv);
+            }
+        } else if constexpr (!F16 && CF::VW == 4) {
             // two k=4 halves of the 8x8 tile: rows t (k = 0..3) and t+4 (k = 4..7); each
             // LDS.128 of one row feeds the A operands of two m16 tiles directly.  All k = 0..3
             // MMAs go first so dependent accumulations sit NV*2 instructions apart.
@@ -773,6 +814,15 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
             const int64_t lr = lr0 + 2 * t + s2;
             if (!remap || lr < p.rows) {
                 const int64_t orow = remap ? (p.row_map ? (int64_t)__ldg(p.row_map + lr) : lr) : (2 * t + s2);
+                if constexpr (LDSM) {  // tile mt: features 16mt + g (c0/c1) and 16mt + 8 + g (c2/c3)
+                    float *d = base + orow * ld + g;
+#pragma unroll
+                    for (int mt = 0; mt < MT; ++mt) {
+                        st_cs1(d + 16 * mt, acc[mt][s2]);
+                        st_cs1(d + 16 * mt + 8, acc[mt][2 + s2]);
+                    }
+                    continue;
+                }
                 float *dst = base + orow * ld + VW * g;
 #pragma unroll
                 for (int j = 0; j < NV; ++j) {
@@ -876,6 +926,15 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
                 const float *src = first + (int64_t)k * p.nslices * (8 * FW);
 #pragma unroll
                 for (int s2 = 0; s2 < 2; ++s2) {
+                    if constexpr (LDSM) {
+                        const float *row = src + (2 * t + s2) * FW + g;
+#pragma unroll
+                        for (int mt = 0; mt < MT; ++mt) {
+                            acc[mt][s2] += __ldcg(row + 16 * mt);
+                            acc[mt][2 + s2] += __ldcg(row + 16 * mt + 8);
+                        }
+                        continue;
+                    }
                     const float *row = src + (2 * t + s2) * FW + VW * g;
 #pragma unroll
                     for (int j = 0; j < NV; ++j) {
@@ -957,12 +1016,12 @@ int env_int(const char *name, int dflt)
 // NM = 1: one tensor map (the full-width map when several slices exist); NM = kMaxSliceMaps:
 // one map per slice (tensor_map decides; only the default configurations instantiate it)
 template <int FW, bool F16, int WARPS, int STAGES, bool RND = false, int MINB = 1, int DIST = 1, int NM = 1,
-          bool VST = false, bool HINT = true>
+          bool VST = false, bool HINT = true, bool LDSM = false>
 accspmm_status launch_g4(const KParams &kp, const G4Maps *map, int64_t n_units, cudaStream_t stream)
 {
     using SM = G4WarpSmem<FW, F16, STAGES, VST ? 8 : kChunk, VST>;
     const size_t smem = sizeof(SM) * WARPS;
-    auto kern = spmm_bittcf_g4_kernel<FW, F16, WARPS, STAGES, RND, MINB, DIST, NM, VST, HINT>;
+    auto kern = spmm_bittcf_g4_kernel<FW, F16, WARPS, STAGES, RND, MINB, DIST, NM, VST, HINT, LDSM>;
     static int configured_device = -1;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -1024,55 +1083,58 @@ accspmm_status tensor_map(const DevicePlan &d, const KParams &kp, int FW, bool m
     return ACCSPMM_OK;
 }
 
-// Minimum resident CTAs per SM for __launch_bounds__ (caps registers per thread): the
+// Minimum resident warps per SM for __launch_bounds__ (caps registers per thread): the
 // kernel is latency-bound, so occupancy pays until the register cap starts to serialise
 // the gather/decode pipeline.  Measured on the Reddit-shaped and stencil matrices
-// (DESIGN.md §7): FW 128 10 (TF32 is then smem-bound; FP16 spills above); FW 64/32 12;
-// FW 16 16.
+// (DESIGN.md §7): FW 128 20 (TF32 is then smem-bound; FP16 spills above); FW 64/32 24;
+// FW 16 32.
 template <int FW, bool F16>
-constexpr int tuned_minb()
+constexpr int tuned_min_warps()
 {
-    return FW == 128 ? 10 : FW == 16 ? 16 : 12;
+    return FW == 128 ? 20 : FW == 16 ? 32 : 24;
 }
 
 template <int FW, bool F16>
 accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, int64_t n_units, cudaStream_t stream,
                          bool rnd)
 {
-    // Default (measured): TMA gather4, 2 warps x 2 stages per CTA, tuned launch
-    // bounds, at every width and precision.  ACCSPMM_KCFG selects other variants for A/B
-    // measurements: 20 = no launch-bounds minimum, 21 = 4 warps per CTA, 24/31/33 = minimum
-    // 10/12/16 CTAs per SM, 10-12 = register-direct gather (4, 2, 8 warps per CTA).
-    constexpr int MB = tuned_minb<FW, F16>();
+    // Default (measured): TMA gather4, one warp x 2 stages per CTA (the warp's
+    // shared-memory addresses are then CTA constants, so the TMA operands need few uniform-
+    // register moves), tuned launch bounds, one tensor map per feature slice when N > FW.
+    // FP16 takes its A fragments by ldmatrix.trans.  ACCSPMM_KCFG selects other variants for
+    // A/B measurements: 20 = 2 warps per CTA without a launch-bounds minimum (the round-1
+    // kernel), 46 = 2 warps per CTA with tuned bounds, 47 = FP16 fragments by LDS.128 + PRMT,
+    // 10-12 = register-direct gather (4, 2, 8 warps per CTA).
+    constexpr int MW = tuned_min_warps<FW, F16>();
     const int kcfg = env_int("ACCSPMM_KCFG", -1);
     if (kcfg < 0 || kcfg >= 20) {
         const G4Maps *map = nullptr;
-        const bool multi = kcfg < 0 && map_count(kp) > 1;
+        const bool multi = map_count(kp) > 1;
         accspmm_status st = tensor_map(d, kp, FW, multi, &map);
         if (st != ACCSPMM_OK) return st;
         constexpr int NM = kMaxSliceMaps;
-        if (!F16 && rnd) {  // B not pre-rounded: rho(B) applied in registers
-            if (multi) return launch_g4<FW, F16, 2, 2, true, MB, 1, NM>(kp, map, n_units, stream);
-            switch (kcfg) {
-            case 20: return launch_g4<FW, F16, 2, 2, true, 1>(kp, map, n_units, stream);
-            case 42: return launch_g4<FW, F16, 1, 2, true, 2 * MB>(kp, map, n_units, stream);
-            default: return launch_g4<FW, F16, 2, 2, true, MB>(kp, map, n_units, stream);
+        if constexpr (!F16) {
+            if (rnd) {  // B not pre-rounded: rho(B) applied in registers
+                if (kcfg == 20) return launch_g4<FW, F16, 2, 2, true, 1>(kp, map, n_units, stream);
+                if (multi) return launch_g4<FW, F16, 1, 2, true, MW, 1, NM>(kp, map, n_units, stream);
+                return launch_g4<FW, F16, 1, 2, true, MW>(kp, map, n_units, stream);
             }
         }
-        if (multi) return launch_g4<FW, F16, 2, 2, false, MB, 1, NM>(kp, map, n_units, stream);
+        constexpr bool LD = F16;  // FP16: ldmatrix.trans fragments (measured -10.5%)
         switch (kcfg) {
         case 20: return launch_g4<FW, F16, 2, 2, false, 1>(kp, map, n_units, stream);
-        case 21: return launch_g4<FW, F16, 4, 2>(kp, map, n_units, stream);
-        case 24: return launch_g4<FW, F16, 2, 2, false, 10>(kp, map, n_units, stream);
-        case 31: return launch_g4<FW, F16, 2, 2, false, 12>(kp, map, n_units, stream);
-        case 33: return launch_g4<FW, F16, 2, 2, false, 16>(kp, map, n_units, stream);
-        case 40: return launch_g4<FW, F16, 2, 2, false, MB, 1, 1, true>(kp, map, n_units, stream);
-        case 42: return launch_g4<FW, F16, 1, 2, false, 2 * MB>(kp, map, n_units, stream);
-        case 43: return launch_g4<FW, F16, 2, 2, false, MB, 1, 1, false, false>(kp, map, n_units, stream);
-        default: return launch_g4<FW, F16, 2, 2, false, MB>(kp, map, n_units, stream);
+        case 46: return launch_g4<FW, F16, 2, 2, false, MW / 2>(kp, map, n_units, stream);
+        case 47:  // FP16 fragments by LDS.128 + PRMT packing
+            if (multi) return launch_g4<FW, F16, 1, 2, false, MW, 1, NM>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 2, false, MW>(kp, map, n_units, stream);
+        default:
+            if (multi) return launch_g4<FW, F16, 1, 2, false, MW, 1, NM, false, true, LD>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 2, false, MW, 1, 1, false, true, LD>(kp, map, n_units, stream);
         }
     }
-    if (!F16 && rnd) return launch_cfg<FW, F16, 2, true>(kp, n_units, stream);
+    if constexpr (!F16) {
+        if (rnd) return launch_cfg<FW, F16, 2, true>(kp, n_units, stream);
+    }
     // register-direct flavour (kcfg 10-12: 4, 2 or 8 warps per CTA)
     switch (kcfg) {
     case 10: return launch_cfg<FW, F16, 4>(kp, n_units, stream);
