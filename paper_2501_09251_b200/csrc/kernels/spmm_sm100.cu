@@ -521,35 +521,13 @@ struct G4Cfg {
     static constexpr int STAGE_AL = 2 * GRP;
 };
 
-// A-stream chunk of the gather4 kernel: CH blocks of SparseAToB / TCLocalBit / TCOffset (plus
-// the end offset), and with VST the chunk's value range staged by cp.async (kVBytes at most;
-// values beyond it are read from global memory)
-constexpr uint32_t kVBytes = 512;
-template <int CH, bool VST>
-struct alignas(16) ChunkG4 {  // 16-byte aligned: cp.async 16 B into a2b
-    uint32_t a2b[CH * 8];
-    uint64_t mask[CH];
-    uint32_t tco[CH + 4];
-    uint32_t vbuf[VST ? kVBytes / 4 : 1];
-};
-
-template <int FW, bool F16, int STAGES, int CH = kChunk, bool VST = false>
+template <int FW, bool F16, int STAGES>
 struct G4WarpSmem {
     alignas(128) uint8_t stage[STAGES][G4Cfg<FW, F16>::STAGE_AL];
-    ChunkG4<CH, VST> ch[2];
+    ChunkSmem ch[2];
     uint64_t bar[STAGES];
 };
-static_assert(sizeof(ChunkG4<16, false>) % 16 == 0 && sizeof(ChunkG4<8, true>) % 16 == 0, "chunk alignment");
-
-__device__ __forceinline__ void tma_gather4_nohint(uint32_t dst, const CUtensorMap *map, int32_t col, int32_t r0,
-                                                   int32_t r1, int32_t r2, int32_t r3, uint32_t bar)
-{
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n"
-        ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar)
-        : "memory");
-}
+static_assert(sizeof(ChunkSmem) % 16 == 0, "chunk alignment (cp.async 16 B into a2b)");
 
 __device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap *map, int32_t col, int32_t r0, int32_t r1,
                                             int32_t r2, int32_t r3, uint32_t bar, uint64_t pol)
@@ -574,8 +552,7 @@ struct G4MapsT {
 using G4Maps = G4MapsT<kMaxSliceMaps>;
 inline int map_count(const KParams &kp) { return kp.nslices > 1 && kp.nslices <= kMaxSliceMaps ? kp.nslices : 1; }
 
-template <int FW, bool F16, int WARPS, int STAGES, bool RND, int MINB = 1, int DIST = 1, int NM = 1, bool VST = false,
-          bool HINT = true, bool LDSM_ = false>
+template <int FW, bool F16, int WARPS, int STAGES, bool RND, int MINB = 1, int NM = 1, bool LDSM_ = false>
 __global__ void __launch_bounds__(WARPS * 32, MINB)
     spmm_bittcf_g4_kernel(const KParams p, const __grid_constant__ G4MapsT<NM> maps)
 {
@@ -584,10 +561,10 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     // and the 8 row addresses of every ldmatrix phase hit 8 distinct bank groups.  The
     // accumulator layout is then m16 tile mt = features 16mt .. 16mt+15 (epilogue below).
     constexpr bool LDSM = LDSM_ && F16;
-    constexpr int CH = VST ? 8 : kChunk;  // blocks per staged chunk
+    constexpr int CH = kChunk;  // blocks per staged chunk
     using CF = Cfg<FW, F16>;
     using GC = G4Cfg<FW, F16>;
-    using SM = G4WarpSmem<FW, F16, STAGES, CH, VST>;
+    using SM = G4WarpSmem<FW, F16, STAGES>;
     using V = typename CF::V;
     constexpr int MT = CF::MT, NV = CF::NV, VW = CF::VW;
     extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -627,9 +604,10 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
             auto &c = sm.ch[(i / CH) & 1];
             const uint32_t b = b0 + i;
             const uint32_t cnt = min((uint32_t)CH, nblk - i);
-            if ((uint32_t)lane < cnt) cp_async8(smem_u32(&c.mask[lane]), p.bits + b + lane, pol_stream);
-            // VST also needs the end offset TCOffset[b + cnt] (the chunk's value range)
-            if ((uint32_t)lane < cnt + (VST ? 1u : 0u)) cp_async4(smem_u32(&c.tco[lane]), p.tco + b + lane, pol_stream);
+            if ((uint32_t)lane < cnt) {
+                cp_async8(smem_u32(&c.mask[lane]), p.bits + b + lane, pol_stream);
+                cp_async4(smem_u32(&c.tco[lane]), p.tco + b + lane, pol_stream);
+            }
             const uint4 *src4 = reinterpret_cast<const uint4 *>(p.a2b + (size_t)b * 8);
             if ((uint32_t)lane < 2 * cnt) cp_async16(smem_u32(&c.a2b[4 * lane]), src4 + lane, pol_stream);
             if (2 * CH > 32 && (uint32_t)lane + 32 < 2 * cnt)
@@ -637,26 +615,11 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
         }
         cp_async_commit();
     };
-    // VST: stage the value range of the chunk starting at block i (its TCOffsets have landed)
-    auto issue_values = [&](uint32_t i) {
-        if constexpr (VST) {
-            if (i < nblk) {
-                auto &c = sm.ch[(i / CH) & 1];
-                const uint32_t cnt = min((uint32_t)CH, nblk - i);
-                const uint32_t lo = (c.tco[0] * CF::ES) & ~3u;
-                const uint32_t hi = min(lo + kVBytes, (c.tco[cnt] * CF::ES + 3u) & ~3u);
-                const char *src = reinterpret_cast<const char *>(p.vals);
-                for (uint32_t o = lo + 4u * (uint32_t)lane; o < hi; o += 128u)
-                    cp_async4(smem_u32(reinterpret_cast<const char *>(c.vbuf) + (o - lo)), src + o, pol_stream);
-            }
-            cp_async_commit();
-        }
-    };
-
-    // Value registers of the blocks in flight: decoded and loaded DIST blocks ahead of use
-    // (a VR-slot register ring), so their L2 latency hides behind DIST block steps.
-    static_assert(DIST == 1 || DIST == 2, "value prefetch distance");
-    constexpr int VR = DIST == 1 ? 2 : 4;
+    // Value registers of the blocks in flight: decoded and loaded one block ahead of use (a
+    // 2-slot register ring).  A 4-slot ring two blocks ahead, a bulk L2 prefetch of each
+    // chunk's value range and staging values through shared memory were measured and lost
+    // (DESIGN.md §7).
+    constexpr int VR = 2;
     uint32_t vb0[VR], vb1[VR];
 
     // ---- every lane: decode this lane's two tile entries of block j, load values
@@ -668,24 +631,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
         bool p0, p1;
         const uint32_t i0 = t0 + tile_rank(mask, sh0, p0);
         const uint32_t i1 = t0 + tile_rank(mask, sh1, p1);
-        if constexpr (VST) {  // staged range first, global memory beyond it
-            const uint32_t lo = (c.tco[0] * CF::ES) & ~3u;
-            const uint32_t o0 = i0 * CF::ES - lo, o1 = i1 * CF::ES - lo;
-            const char *vb = reinterpret_cast<const char *>(c.vbuf);
-            if constexpr (!F16) {
-                const float *vp = reinterpret_cast<const float *>(p.vals);
-                vb0[slot] = p0 ? (o0 < kVBytes ? *reinterpret_cast<const uint32_t *>(vb + o0)
-                                               : __float_as_uint(__ldg(vp + i0))) : 0u;
-                vb1[slot] = p1 ? (o1 < kVBytes ? *reinterpret_cast<const uint32_t *>(vb + o1)
-                                               : __float_as_uint(__ldg(vp + i1))) : 0u;
-            } else {
-                const unsigned short *vp = reinterpret_cast<const unsigned short *>(p.vals);
-                vb0[slot] = p0 ? (o0 < kVBytes ? (uint32_t)*reinterpret_cast<const uint16_t *>(vb + o0)
-                                               : (uint32_t)__ldg(vp + i0)) : 0u;
-                vb1[slot] = p1 ? (o1 < kVBytes ? (uint32_t)*reinterpret_cast<const uint16_t *>(vb + o1)
-                                               : (uint32_t)__ldg(vp + i1)) : 0u;
-            }
-        } else if constexpr (!F16) {
+        if constexpr (!F16) {
             const float *vp = reinterpret_cast<const float *>(p.vals);
             vb0[slot] = p0 ? __float_as_uint(__ldg(vp + i0)) : 0u;
             vb1[slot] = p1 ? __float_as_uint(__ldg(vp + i1)) : 0u;
@@ -716,15 +662,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
             const CUtensorMap *tmap = &maps.m[NM > 1 ? slice : 0];
             const int32_t tcol = NM > 1 ? 0 : slice * FW;
             const int32_t tcol_y = LDSM ? tcol - 8 : tcol;
-            if constexpr (!HINT) {
-                if constexpr (!F16) {
-                    tma_gather4_nohint(st, tmap, tcol, r0, r1, r2, r3, bar);
-                    tma_gather4_nohint(st + GC::GRP, tmap, tcol, r4, r5, r6, r7, bar);
-                } else {
-                    tma_gather4_nohint(st, tmap, tcol, r0, r2, r4, r6, bar);
-                    tma_gather4_nohint(st + GC::GRP, tmap, tcol_y, r1, r3, r5, r7, bar);
-                }
-            } else if constexpr (!F16) {
+            if constexpr (!F16) {
                 tma_gather4(st, tmap, tcol, r0, r1, r2, r3, bar, pol_keep);
                 tma_gather4(st + GC::GRP, tmap, tcol, r4, r5, r6, r7, bar, pol_keep);
             } else {
@@ -855,47 +793,32 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
         }
     };
 
-    // Prologue: chunk 0 (wait) and chunk 1 in flight; values of blocks 0..DIST-1; TMA of block 0.
+    // Prologue: chunk 0 (wait) and chunk 1 in flight; values of block 0; TMA of block 0.
     issue_chunk(0);
     cp_async_wait_all();
     __syncwarp();
-    if constexpr (VST) {
-        issue_values(0);
-        cp_async_wait_all();
-        __syncwarp();
-    }
     issue_chunk(CH);
     after_block(b0);
-#pragma unroll
-    for (int d = 0; d < DIST; ++d)
-        if ((uint32_t)d < nblk) value_load((uint32_t)d, d);
+    if (nblk > 0) value_load(0u, 0);
     if (nblk > 0) issue_tma(0, 0);
-    // Block step j: TMA for j+1, values for j+DIST (at a chunk boundary first wait for that
+    // Block step j: TMA for j+1, values for j+1 (at a chunk boundary first wait for that
     // chunk and prefetch the one after), then the decode-free MMA of block j.
     static_assert(STAGES == 2, "the block step below is written for a 2-stage TMA ring");
     auto step = [&](uint32_t j, int u, bool checked) {
-        const uint32_t jt = j + 1, jv = j + DIST;
-        if (DIST == 1 && (jv & (CH - 1u)) == 0) {  // chunk (jv / CH) must have landed
+        const uint32_t jn = j + 1;
+        if ((jn & (CH - 1u)) == 0) {  // chunk (jn / CH) must have landed
             cp_async_wait_all();
             __syncwarp();
-            issue_chunk(jv + CH);
+            issue_chunk(jn + CH);
         }
-        if (VST && (jv & (CH - 1u)) == CH / 2) {  // mid-chunk: the next chunk's offsets have landed
-            cp_async_wait_all();
-            __syncwarp();
-            issue_values((jv | (CH - 1u)) + 1u);
+        if (!checked || jn < nblk) {
+            issue_tma(jn, (u + 1) & 1);
+            value_load(jn, (u + 1) & (VR - 1));
         }
-        if (!checked || jt < nblk) issue_tma(jt, (u + 1) & 1);
-        if (DIST == 2 && (jv & (CH - 1u)) == 0) {
-            cp_async_wait_all();
-            __syncwarp();
-            issue_chunk(jv + CH);
-        }
-        if (!checked || jv < nblk) value_load(jv, (u + DIST) & (VR - 1));
         consume(j, u & 1, u & (VR - 1));
         after_block(b0 + j + 1);
     };
-    const uint32_t nmain = nblk >= (uint32_t)DIST ? ((nblk - DIST) / VR) * VR : 0u;
+    const uint32_t nmain = nblk >= 1u ? ((nblk - 1u) / VR) * VR : 0u;
     uint32_t j = 0;
     for (; j < nmain; j += VR) {
 #pragma unroll
@@ -1015,13 +938,12 @@ int env_int(const char *name, int dflt)
 
 // NM = 1: one tensor map (the full-width map when several slices exist); NM = kMaxSliceMaps:
 // one map per slice (tensor_map decides; only the default configurations instantiate it)
-template <int FW, bool F16, int WARPS, int STAGES, bool RND = false, int MINB = 1, int DIST = 1, int NM = 1,
-          bool VST = false, bool HINT = true, bool LDSM = false>
+template <int FW, bool F16, int WARPS, int STAGES, bool RND = false, int MINB = 1, int NM = 1, bool LDSM = false>
 accspmm_status launch_g4(const KParams &kp, const G4Maps *map, int64_t n_units, cudaStream_t stream)
 {
-    using SM = G4WarpSmem<FW, F16, STAGES, VST ? 8 : kChunk, VST>;
+    using SM = G4WarpSmem<FW, F16, STAGES>;
     const size_t smem = sizeof(SM) * WARPS;
-    auto kern = spmm_bittcf_g4_kernel<FW, F16, WARPS, STAGES, RND, MINB, DIST, NM, VST, HINT, LDSM>;
+    auto kern = spmm_bittcf_g4_kernel<FW, F16, WARPS, STAGES, RND, MINB, NM, LDSM>;
     static int configured_device = -1;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -1116,7 +1038,7 @@ accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, 
         if constexpr (!F16) {
             if (rnd) {  // B not pre-rounded: rho(B) applied in registers
                 if (kcfg == 20) return launch_g4<FW, F16, 2, 2, true, 1>(kp, map, n_units, stream);
-                if (multi) return launch_g4<FW, F16, 1, 2, true, MW, 1, NM>(kp, map, n_units, stream);
+                if (multi) return launch_g4<FW, F16, 1, 2, true, MW, NM>(kp, map, n_units, stream);
                 return launch_g4<FW, F16, 1, 2, true, MW>(kp, map, n_units, stream);
             }
         }
@@ -1125,11 +1047,11 @@ accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, 
         case 20: return launch_g4<FW, F16, 2, 2, false, 1>(kp, map, n_units, stream);
         case 46: return launch_g4<FW, F16, 2, 2, false, MW / 2>(kp, map, n_units, stream);
         case 47:  // FP16 fragments by LDS.128 + PRMT packing
-            if (multi) return launch_g4<FW, F16, 1, 2, false, MW, 1, NM>(kp, map, n_units, stream);
+            if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM>(kp, map, n_units, stream);
             return launch_g4<FW, F16, 1, 2, false, MW>(kp, map, n_units, stream);
         default:
-            if (multi) return launch_g4<FW, F16, 1, 2, false, MW, 1, NM, false, true, LD>(kp, map, n_units, stream);
-            return launch_g4<FW, F16, 1, 2, false, MW, 1, 1, false, true, LD>(kp, map, n_units, stream);
+            if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 2, false, MW, 1, LD>(kp, map, n_units, stream);
         }
     }
     if constexpr (!F16) {

@@ -480,3 +480,23 @@ def test_permute_cols_partitions_and_device_build():
             out[rows] = G
     torch.cuda.synchronize()
     assert np.array_equal(out.cpu().numpy(), Cfull)
+
+
+@pytest.mark.parametrize("kcfg", ["20", "46", "47", "10", "11", "12"])
+@pytest.mark.parametrize("precision", PRECISIONS)
+def test_measurement_variants_stay_exact(kcfg, precision, monkeypatch):
+    """The A/B kernel variants selectable by ACCSPMM_KCFG (2 warps per CTA,
+    FP16 PRMT fragments, register-direct gather) compute the same product: integer data
+    bit-exact (split windows included), floats within tolerance, N = 64 and 256."""
+    monkeypatch.setenv("ACCSPMM_KCFG", kcfg)
+    A = gen.dcsbm(3000, 150_000, 5, 2.2, 0.2, 2000, seed=3, oversample=1.3)
+    v = gen.values_int(A.nnz, 1)
+    for N in (64, 256):
+        B = gen.dense_int(A.K, N, 2)
+        C, p = run(A, v, B, precision, balance="on", unit_cap=32)
+        assert p.info["n_split_windows"] > 0
+        assert_bit_exact(C, A, v, B, precision)
+    vf = gen.values_uniform(A.nnz, 4)
+    Bf = gen.dense_normal(A.K, 128, 5)
+    Cf, _ = run(A, vf, Bf, precision)
+    assert_within(Cf, A, vf, Bf, precision)
