@@ -1031,7 +1031,8 @@ accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, 
     const int kcfg = env_int("ACCSPMM_KCFG", -1);
     if (kcfg < 0 || kcfg >= 20) {
         const G4Maps *map = nullptr;
-        const bool multi = map_count(kp) > 1;
+        // per-slice maps only for the kernels instantiated with them (variants 20/46: one map)
+        const bool multi = map_count(kp) > 1 && kcfg != 20 && kcfg != 46;
         accspmm_status st = tensor_map(d, kp, FW, multi, &map);
         if (st != ACCSPMM_OK) return st;
         constexpr int NM = kMaxSliceMaps;

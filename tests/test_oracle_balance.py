@@ -90,3 +90,29 @@ def test_auto_cap():
     assert ob.auto_cap(0) == 32 and ob.auto_cap(10) == 32
     assert ob.auto_cap(14_000_000) == 512   # ceil(14e6 / 28416) = 493 -> 512
     assert ob.auto_cap(10 ** 10) == 4096
+
+
+@pytest.mark.parametrize("seed", range(20))
+@pytest.mark.parametrize("cap", [32, 100])
+@pytest.mark.parametrize("precision", ["tf32", "fp16"])
+def test_grouped_schedule_keeps_windows_whole(seed, cap, precision):
+    """Reading R7b (balance AUTO, IBD <= 8): whole windows only -- no unit splits a window,
+    every window appears in exactly one unit in order, groups respect the concatenation rule
+    (cost <= cap + wb unless a unit is a single window, at most WMAX windows), and a unit is
+    closed only when the next window would break that rule (greedy maximality)."""
+    rng = np.random.default_rng(300 + seed)
+    rwo = _powerlaw_rwo(rng, int(rng.integers(1, 500)))
+    units = ob.build_units(rwo, cap, False, precision, group=True)
+    ob.check_coverage(units, rwo)
+    wb = ob.wb_cost(precision)
+    nb = np.diff(rwo)
+    for k, (w0, nw, b0, b1, split, seg, nseg, slot) in enumerate(units):
+        assert split == ob.NO_SPLIT and nseg == 1 and b0 == rwo[w0] and b1 == rwo[w0 + nw]
+        cost = int(sum(nb[w0:w0 + nw])) + wb * nw
+        assert nw <= ob.WMAX and (nw == 1 or cost <= cap + wb)
+        nxt = w0 + nw
+        if k + 1 < len(units) and nb[w0:w0 + nw].max(initial=0) <= cap and nb[nxt] <= cap:
+            assert nw == ob.WMAX or cost + int(nb[nxt]) + wb > cap + wb
+    # with no window above the cap, grouping equals the balanced schedule (nothing to split)
+    small = np.concatenate([[0], np.cumsum(np.minimum(nb, cap))])
+    assert ob.build_units(small, cap, False, precision, group=True) == ob.build_units(small, cap, True, precision)

@@ -1,0 +1,7 @@
+#!/bin/bash
+cd "$GRAFT_REPO_ROOT"; mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()" > /dev/null
+timeout 1800 python -m pytest tests -m gpu -q -x -p no:cacheprovider > gpurun_out/gpu_tests_s18.log 2>&1; echo "tests rc=$?"; tail -3 gpurun_out/gpu_tests_s18.log
+timeout 1500 python tools/sweep.py --config reddit --N 128 --steps 20 --rounds 3 --out gpurun_out/sweep_s18.jsonl --variants \
+  reorder=on reorder=on,precision=fp16 reorder=on,N=64 kcfg=47,reorder=on,precision=fp16 > gpurun_out/sweep_s18.log 2>&1
+echo "sweep rc=$?"; cut -c1-130 gpurun_out/sweep_s18.log
