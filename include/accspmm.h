@@ -110,7 +110,9 @@ typedef struct {
     double ms_validate, ms_reorder, ms_build, ms_schedule, ms_upload;
     int64_t grouped;            /* 1: unbalanced plan whose whole windows are grouped per unit (AUTO) */
     int64_t cols_permuted;      /* 1: columns relabelled with the row permutation (permute_cols)      */
-    int64_t reserved[6];
+    int64_t group_cap;          /* concatenation limit of short windows (blocks): min(cap, 32) for grouped
+                                   plans under the automatic cap, else = unit_cap                    */
+    int64_t reserved[5];
 } accspmm_plan_info;
 
 /* Fills *opt with the defaults listed above.  Never fails for a non-null opt. */

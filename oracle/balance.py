@@ -58,6 +58,13 @@ def wb_cost(precision: str) -> int:
     return {"tf32": 1, "fp16": 2}[precision]
 
 
+GROUP_CAP = 32  # reading R7c: concatenation limit of grouped plans under the automatic cap
+
+
+def auto_group_cap(cap: int) -> int:
+    return max(1, min(cap, GROUP_CAP))
+
+
 def auto_cap(NB: int) -> int:
     """B200 default cap when unit_cap == 0 (reading R7): ~192 units per SM, in [32, 4096], multiple of 32."""
     c = -(-NB // (148 * 192))
@@ -65,12 +72,14 @@ def auto_cap(NB: int) -> int:
     return max(PAPER_CAP, min(4096, c))
 
 
-def build_units(rwo, cap: int, balance: bool, precision: str = "tf32", group: bool = False):
+def build_units(rwo, cap: int, balance: bool, precision: str = "tf32", group: bool = False,
+                group_cap: int | None = None):
     """Work units (w0, nw, b0, b1, split_id, seg, nseg, slot) covering every block once.
 
     Not balanced: one unit per RowWindow, or with ``group`` (the B200 reading R7b,
     DESIGN.md: balance AUTO below the IBD threshold) consecutive WHOLE windows packed into
-    one unit by the same concatenation rule, never split."""
+    one unit by the same concatenation rule, never split.  ``group_cap`` (reading R7c) bounds
+    the concatenation separately from the split cap (default: cap)."""
     rwo = np.asarray(rwo, dtype=np.int64)
     W = rwo.size - 1
     units = []
@@ -97,7 +106,7 @@ def build_units(rwo, cap: int, balance: bool, precision: str = "tf32", group: bo
             slot += nseg
         else:
             c = nb + wb
-            if cur is not None and cur[1] < WMAX and cur[4] + c <= cap + wb:
+            if cur is not None and cur[1] < WMAX and cur[4] + c <= (group_cap or cap) + wb:
                 cur[1] += 1
                 cur[3] = int(rwo[w + 1])
                 cur[4] += c

@@ -52,7 +52,8 @@ class accspmm_plan_info(ctypes.Structure):
                                                   "value_bytes", "device_bytes")]
                 + [(n, ctypes.c_double) for n in ("ms_validate", "ms_reorder", "ms_build", "ms_schedule",
                                                    "ms_upload")]
-                + [("grouped", ctypes.c_int64), ("cols_permuted", ctypes.c_int64), ("reserved", ctypes.c_int64 * 6)])
+                + [("grouped", ctypes.c_int64), ("cols_permuted", ctypes.c_int64), ("group_cap", ctypes.c_int64),
+                   ("reserved", ctypes.c_int64 * 5)])
 
     def as_dict(self) -> dict:
         return {n: getattr(self, n) for n, _ in self._fields_ if n != "reserved"}

@@ -254,11 +254,14 @@ accspmm_status accspmm_plan_create_ex(int64_t M, int64_t K, const int64_t *rowpt
     const bool balance = opt.balance == ACCSPMM_BALANCE_ON ||
                          (opt.balance == ACCSPMM_BALANCE_AUTO && ibd > kIbdThreshold);
     const int cap = opt.unit_cap > 0 ? opt.unit_cap : auto_cap(F.NB);
+    // reading R7c: grouped (unbalanced) plans concatenate only up to min(cap, 32) blocks under
+    // the automatic cap; balanced plans keep the paper's single cap for both rules
+    const int gcap = (opt.unit_cap > 0 || balance) ? cap : auto_group_cap(cap);
     // AUTO below the IBD threshold keeps windows whole but groups consecutive ones
     // into a warp's unit (reading R7b); OFF is the paper's one window per unit
     const bool group = !balance && opt.balance == ACCSPMM_BALANCE_AUTO;
-    Schedule S = build_schedule(F.rwo, cap, balance, opt.precision, group);
-    I.ibd = ibd; I.balanced = balance ? 1 : 0; I.unit_cap = cap; I.grouped = group ? 1 : 0;
+    Schedule S = build_schedule(F.rwo, cap, balance, opt.precision, group, gcap);
+    I.ibd = ibd; I.balanced = balance ? 1 : 0; I.unit_cap = cap; I.grouped = group ? 1 : 0; I.group_cap = gcap;
     I.n_units = (int64_t)S.units.size(); I.n_split_windows = S.n_split; I.n_segments = S.n_segments;
     p->units_host.resize(S.units.size() * 8);
     std::memcpy(p->units_host.data(), S.units.data(), S.units.size() * sizeof(Unit));

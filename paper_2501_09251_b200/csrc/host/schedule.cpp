@@ -11,9 +11,12 @@
 // concatenated while sum(blocks + wb) <= cap + wb (Fig. 7(b)).
 // Unbalanced plans (IBD <= 8 under ACCSPMM_BALANCE_AUTO) may still be `group`ed:
 // whole windows concatenated by the same rule, none split (reading R7b: a warp's
-// fixed per-unit cost is amortised over short windows).
+// fixed per-unit cost is amortised over short windows).  Grouped plans stop
+// concatenating at `group_cap` blocks (reading R7c: min(cap, 32) under the automatic cap):
+// long concatenated units cost 1.3-1.9x on the HBM-bound papers100M-shaped matrix.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "../internal.hpp"
 
@@ -38,8 +41,17 @@ int auto_cap(int64_t NB)
     return (int)std::max<int64_t>(kPaperCap, std::min<int64_t>(4096, c));
 }
 
-Schedule build_schedule(const std::vector<uint32_t> &rwo, int cap, bool balance, int precision, bool group)
+int auto_group_cap(int cap)
 {
+    const char *e = std::getenv("ACCSPMM_GROUP_CAP");  // A/B measurements only
+    const int g = e ? std::atoi(e) : kGroupCap;
+    return std::max(1, std::min(cap, g));
+}
+
+Schedule build_schedule(const std::vector<uint32_t> &rwo, int cap, bool balance, int precision, bool group,
+                        int group_cap)
+{
+    const int64_t gcap = group_cap > 0 ? group_cap : cap;  // concatenation limit (reading R7c)
     Schedule s;
     s.cap = cap;
     s.balanced = balance;
@@ -74,7 +86,7 @@ Schedule build_schedule(const std::vector<uint32_t> &rwo, int cap, bool balance,
             s.n_segments += nseg;
         } else {
             const int64_t c = nb + wb;
-            if (open && (int64_t)cur.nw < kWmax && cost + c <= cap + wb) {
+            if (open && (int64_t)cur.nw < kWmax && cost + c <= gcap + wb) {
                 cur.nw += 1;
                 cur.b1 = rwo[(size_t)w + 1];
                 cost += c;

@@ -14,6 +14,7 @@ constexpr uint32_t kPadLane = 0xFFFFFFFFu;  // device SparseAToB padding lane (r
 constexpr int kWmax = 31;             // windows per concatenated unit (one per lane of the window table)
 constexpr double kIbdThreshold = 8.0; // P:417 "When IBD exceeds 8"
 constexpr int kPaperCap = 32;         // P:446 "maximum threshold of 32 TC blocks per TB"
+constexpr int kGroupCap = 32;         // concatenation limit of grouped plans, automatic cap (reading R7c)
 // TF32 rho(B): a separate rounding pass over B when every B row is gathered at least this
 // many times on average (sum_w |U_w| >= kRoundReuse * K), else cvt.rna in the kernel
 constexpr int64_t kRoundReuse = 32;
@@ -67,7 +68,9 @@ int64_t count_blocks(const Csr &a, const std::vector<uint32_t> &perm);
 // host/schedule.cpp
 double compute_ibd(const std::vector<uint32_t> &rwo);
 int auto_cap(int64_t NB);
-Schedule build_schedule(const std::vector<uint32_t> &rwo, int cap, bool balance, int precision, bool group);
+Schedule build_schedule(const std::vector<uint32_t> &rwo, int cap, bool balance, int precision, bool group,
+                        int group_cap = 0);
+int auto_group_cap(int cap);  // concatenation limit under the automatic cap (reading R7c)
 
 // host/partition.cpp
 std::vector<int64_t> partition_bounds(const Csr &a, const std::vector<uint32_t> &perm, int nparts);

@@ -552,7 +552,8 @@ struct G4MapsT {
 using G4Maps = G4MapsT<kMaxSliceMaps>;
 inline int map_count(const KParams &kp) { return kp.nslices > 1 && kp.nslices <= kMaxSliceMaps ? kp.nslices : 1; }
 
-template <int FW, bool F16, int WARPS, int STAGES, bool RND, int MINB = 1, int NM = 1, bool LDSM_ = false>
+template <int FW, bool F16, int WARPS, int STAGES, bool RND, int MINB = 1, int NM = 1, bool LDSM_ = false,
+          bool K8 = false>
 __global__ void __launch_bounds__(WARPS * 32, MINB)
     spmm_bittcf_g4_kernel(const KParams p, const __grid_constant__ G4MapsT<NM> maps)
 {
@@ -717,15 +718,23 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
                                       tf32_rna_bits(y[j].w));
                 }
             }
+            if constexpr (K8) {  // one m16n8k8 per m16 tile: (x.x, x.y) k = t, (y.x, y.y) k = t + 4
 #pragma unroll
-            for (int j = 0; j < NV; ++j) {
-                mma_tf32_k4(acc[2 * j], x[j].x, x[j].y, vb0[slot]);
-                mma_tf32_k4(acc[2 * j + 1], x[j].z, x[j].w, vb0[slot]);
-            }
+                for (int j = 0; j < NV; ++j) {
+                    mma_tf32(acc[2 * j], x[j].x, x[j].y, y[j].x, y[j].y, vb0[slot], vb1[slot]);
+                    mma_tf32(acc[2 * j + 1], x[j].z, x[j].w, y[j].z, y[j].w, vb0[slot], vb1[slot]);
+                }
+            } else {
 #pragma unroll
-            for (int j = 0; j < NV; ++j) {
-                mma_tf32_k4(acc[2 * j], y[j].x, y[j].y, vb1[slot]);
-                mma_tf32_k4(acc[2 * j + 1], y[j].z, y[j].w, vb1[slot]);
+                for (int j = 0; j < NV; ++j) {
+                    mma_tf32_k4(acc[2 * j], x[j].x, x[j].y, vb0[slot]);
+                    mma_tf32_k4(acc[2 * j + 1], x[j].z, x[j].w, vb0[slot]);
+                }
+#pragma unroll
+                for (int j = 0; j < NV; ++j) {
+                    mma_tf32_k4(acc[2 * j], y[j].x, y[j].y, vb1[slot]);
+                    mma_tf32_k4(acc[2 * j + 1], y[j].z, y[j].w, vb1[slot]);
+                }
             }
         } else {
             Frag<FW, F16> fr;
@@ -783,13 +792,17 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
 #pragma unroll
         for (int m = 0; m < MT; ++m) acc[m][0] = acc[m][1] = acc[m][2] = acc[m][3] = 0.f;
     };
+    // wend = absolute block index where the current window ends; 0xFFFFFFFF once no whole
+    // window is left (split units, or after the last one): one compare per block
     uint32_t wi = 0;
-    uint32_t wend = split ? b1 : __shfl_sync(0xffffffffu, my_rwo, 1);
+    uint32_t wend = __shfl_sync(0xffffffffu, my_rwo, 1);
+    if (split || nw == 0) wend = 0xFFFFFFFFu;
     auto after_block = [&](uint32_t jnext) {
-        while (!split && wi < nw && wend == jnext) {
+        while (wend == jnext) {
             store_window(wi);
             ++wi;
-            wend = __shfl_sync(0xffffffffu, my_rwo, (int)(wi < nw ? wi + 1 : nw));
+            const uint32_t e = __shfl_sync(0xffffffffu, my_rwo, (int)(wi < nw ? wi + 1 : nw));
+            wend = wi < nw ? e : 0xFFFFFFFFu;
         }
     };
 
@@ -938,12 +951,13 @@ int env_int(const char *name, int dflt)
 
 // NM = 1: one tensor map (the full-width map when several slices exist); NM = kMaxSliceMaps:
 // one map per slice (tensor_map decides; only the default configurations instantiate it)
-template <int FW, bool F16, int WARPS, int STAGES, bool RND = false, int MINB = 1, int NM = 1, bool LDSM = false>
+template <int FW, bool F16, int WARPS, int STAGES, bool RND = false, int MINB = 1, int NM = 1, bool LDSM = false,
+          bool K8 = false>
 accspmm_status launch_g4(const KParams &kp, const G4Maps *map, int64_t n_units, cudaStream_t stream)
 {
     using SM = G4WarpSmem<FW, F16, STAGES>;
     const size_t smem = sizeof(SM) * WARPS;
-    auto kern = spmm_bittcf_g4_kernel<FW, F16, WARPS, STAGES, RND, MINB, NM, LDSM>;
+    auto kern = spmm_bittcf_g4_kernel<FW, F16, WARPS, STAGES, RND, MINB, NM, LDSM, K8>;
     static int configured_device = -1;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -1047,6 +1061,9 @@ accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, 
         switch (kcfg) {
         case 20: return launch_g4<FW, F16, 2, 2, false, 1>(kp, map, n_units, stream);
         case 46: return launch_g4<FW, F16, 2, 2, false, MW / 2>(kp, map, n_units, stream);
+        case 48:  // TF32 m16n8k8 instead of two m16n8k4
+            if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, true>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, true>(kp, map, n_units, stream);
         case 47:  // FP16 fragments by LDS.128 + PRMT packing
             if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM>(kp, map, n_units, stream);
             return launch_g4<FW, F16, 1, 2, false, MW>(kp, map, n_units, stream);

@@ -163,7 +163,10 @@ def test_schedule_bit_exact_vs_oracle(balance, cap, precision, shape):
     assert I["grouped"] == int(group)
     if shape == "road":
         assert not on or balance == "on"
-    ref = np.array(ob.build_units(rwo, expect_cap, on, precision, group=group), dtype=np.uint64).astype(np.uint32)
+    expect_gcap = expect_cap if (cap > 0 or on) else ob.auto_group_cap(expect_cap)
+    assert I["group_cap"] == expect_gcap
+    ref = np.array(ob.build_units(rwo, expect_cap, on, precision, group=group, group_cap=expect_gcap),
+                   dtype=np.uint64).astype(np.uint32)
     got = p.export_units()
     assert got.shape == ref.shape and np.array_equal(got, ref)
     ob.check_coverage([tuple(int(x) for x in u) for u in got], rwo)

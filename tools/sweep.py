@@ -41,7 +41,11 @@ def main():
         prec = kv.get("precision", "tf32")
         os.environ["ACCSPMM_KCFG"] = kv.get("kcfg", "-1")
         os.environ["ACCSPMM_FW"] = kv.get("fw", "0")
-        key = (prec, kv.get("balance", "auto"), int(kv.get("cap", 0)), kv.get("reorder", "off"))
+        if "gcap" in kv:
+            os.environ["ACCSPMM_GROUP_CAP"] = kv["gcap"]
+        else:
+            os.environ.pop("ACCSPMM_GROUP_CAP", None)
+        key = (prec, kv.get("balance", "auto"), int(kv.get("cap", 0)), kv.get("reorder", "off"), kv.get("gcap"))
         if key not in plans:
             t0 = time.perf_counter()
             plans[key] = acc.Plan(A.M, A.K, A.rowptr, A.colidx, vals, precision=prec, balance=key[1],
