@@ -140,13 +140,19 @@ std::vector<uint32_t> reorder_alg1(const Csr &a)
     // ---------------- Step I: dendrogram construction (one pass) ----------------
     std::vector<uint32_t> parent((size_t)n);
     std::iota(parent.begin(), parent.end(), 0u);
-    std::vector<double> acomm((size_t)n);
+    // per community: its degree sum a_c (Eq. 1) and the edge weight accumulated towards the
+    // vertex being visited, side by side so the merge-gain loop reads one cache line
+    struct Comm {
+        uint64_t w;
+        double a;
+    };
+    std::vector<Comm> cm((size_t)n, Comm{0, 0.0});
     std::vector<uint32_t> first_child((size_t)n, UINT32_MAX), last_child((size_t)n, UINT32_MAX),
         next_sib((size_t)n, UINT32_MAX);
     std::vector<std::vector<std::pair<uint32_t, uint32_t>>> E((size_t)n);
     std::vector<uint32_t> order((size_t)n);
     std::iota(order.begin(), order.end(), 0u);
-    for (int64_t v = 0; v < n; ++v) acomm[(size_t)v] = (double)(g.ptr[(size_t)v + 1] - g.ptr[(size_t)v]);
+    for (int64_t v = 0; v < n; ++v) cm[(size_t)v].a = (double)(g.ptr[(size_t)v + 1] - g.ptr[(size_t)v]);
     std::stable_sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) {
         return g.ptr[x + 1] - g.ptr[x] < g.ptr[y + 1] - g.ptr[y];
     });
@@ -156,7 +162,6 @@ std::vector<uint32_t> reorder_alg1(const Csr &a)
         while (parent[x] != r) { uint32_t nx = parent[x]; parent[x] = r; x = nx; }
         return r;
     };
-    std::vector<uint64_t> accw((size_t)n, 0);
     std::vector<uint32_t> touched;
     for (uint32_t v : order) {
         const int64_t deg = g.ptr[v + 1] - g.ptr[v];
@@ -165,14 +170,14 @@ std::vector<uint32_t> reorder_alg1(const Csr &a)
         auto add = [&](uint32_t x, uint32_t w) {
             uint32_t r = find(x);
             if (r == v) return;
-            if (accw[r] == 0) touched.push_back(r);
-            accw[r] += w;
+            if (cm[r].w == 0) touched.push_back(r);
+            cm[r].w += w;
         };
         for (int64_t p = g.ptr[v]; p < g.ptr[v + 1]; ++p) {
             if (p + 16 < g.ptr[v + 1]) {  // the walk is bound by random accesses: prefetch ahead
                 const uint32_t x = g.adj[(size_t)p + 16];
                 __builtin_prefetch(&parent[x]);
-                __builtin_prefetch(&accw[x], 1);
+                __builtin_prefetch(&cm[x], 1);
             }
             add(g.adj[(size_t)p], 1u);
         }
@@ -187,10 +192,10 @@ std::vector<uint32_t> reorder_alg1(const Csr &a)
         uint32_t best = UINT32_MAX;
         double best_dq = 0.0;
         for (uint32_t r : touched) {
-            double dq = 2.0 * ((double)accw[r] / m2 - acomm[r] * acomm[v] / (m2 * m2));
+            double dq = 2.0 * ((double)cm[r].w / m2 - cm[r].a * cm[v].a / (m2 * m2));
             if (best == UINT32_MAX || dq > best_dq || (dq == best_dq && r < best)) { best = r; best_dq = dq; }
-            comp.emplace_back(r, (uint32_t)accw[r]);
-            accw[r] = 0;
+            comp.emplace_back(r, (uint32_t)cm[r].w);
+            cm[r].w = 0;
         }
         E[v].clear();
         E[v].shrink_to_fit();
@@ -206,7 +211,7 @@ std::vector<uint32_t> reorder_alg1(const Csr &a)
         if (best != UINT32_MAX && best_dq > 0.0) {
             const uint32_t u = best;
             parent[v] = u;
-            acomm[u] += acomm[v];
+            cm[u].a += cm[v].a;
             // v's original edges were consumed into comp; u inherits the aggregated list
             E[u].insert(E[u].end(), comp.begin(), comp.end());
             if (first_child[u] == UINT32_MAX) first_child[u] = v; else next_sib[last_child[u]] = v;
