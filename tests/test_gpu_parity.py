@@ -500,3 +500,34 @@ def test_measurement_variants_stay_exact(kcfg, precision, monkeypatch):
     Bf = gen.dense_normal(A.K, 128, 5)
     Cf, _ = run(A, vf, Bf, precision)
     assert_within(Cf, A, vf, Bf, precision)
+
+
+@pytest.mark.parametrize("precision", PRECISIONS)
+def test_execute_is_cuda_graph_capturable(precision):
+    """After one warm-up call (workspace / scratch allocation, kernel attributes), execute
+    issues only kernel launches on the given stream: it can be captured into a CUDA graph and
+    replayed (launch overhead matters for small matrices, e.g. the DD shape at ~80 us)."""
+    import torch
+    A = gen.dcsbm(3000, 150_000, 5, 2.2, 0.2, 2000, seed=7, oversample=1.3)
+    v = gen.values_int(A.nnz, 1)
+    B0 = gen.dense_int(A.K, 128, 2)
+    p = acc.Plan(A.M, A.K, A.rowptr, A.colidx, v, precision=precision, reorder="on", balance="on", unit_cap=32)
+    Bd = to_dev_B(B0, precision)
+    C = torch.full((A.M, 128), float("nan"), device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        p.execute(Bd, C, s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    C.fill_(float("nan"))
+    torch.cuda.synchronize()
+    with torch.cuda.graph(g, stream=s):
+        p.execute(Bd, C, torch.cuda.current_stream())
+    g.replay()
+    torch.cuda.synchronize()
+    assert_bit_exact(C.cpu().numpy(), A, v, B0, precision)
+    B1 = gen.dense_int(A.K, 128, 3)
+    Bd.copy_(to_dev_B(B1, precision))
+    g.replay()
+    torch.cuda.synchronize()
+    assert_bit_exact(C.cpu().numpy(), A, v, B1, precision)
