@@ -45,6 +45,10 @@ def parse():
     ap.add_argument("--unit-cap", type=int, default=0)
     ap.add_argument("--permute-cols", action="store_true", help="symmetric reordering: relabel columns too")
     ap.add_argument("--build", default="device", choices=["host", "device"], help="BitTCF builder")
+    ap.add_argument("--allgather", default="none", choices=["none", "nccl", "fused"],
+                    help="N > 1: also time assembling the full C on every rank (NCCL all-gather + "
+                         "un-permute, or the fused epilogue into symmetric memory); reported as "
+                         "'allgather', the headline value stays the slab step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-flush", action="store_true")
@@ -208,6 +212,41 @@ def emit(out, args):
             f.write(line + "\n")
 
 
+def time_allgather(args, plan, Bd, A, stream, world, shared):
+    """N > 1 extra: full C on every rank per step, NCCL (execute + all-gather + un-permute) or
+    fused (epilogue writes into every rank's symmetric-memory C + device barrier).  Device
+    time, max over ranks; failures are reported, not raised (the slab step is the headline)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2501_09251_b200 import distributed as D
+    out = {"mode": args.allgather}
+    try:
+        steps = max(3, min(args.steps, 20))
+        if args.allgather == "fused":
+            fa = D.FusedAllGather(A.M, args.N, Bd.device)
+            run = lambda: fa.step(plan, Bd, stream)  # noqa: E731
+        else:
+            run = lambda: D.spmm_all(plan, Bd, A.M, stream)  # noqa: E731
+        for _ in range(2):
+            run()
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            run()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) / 1e3], dtype=torch.float64, device="cpu" if shared else "cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t = float(t.item())
+        out.update({"ms_per_step": t / steps * 1e3, "value": 2.0 * A.nnz * args.N * steps / t / 1e9,
+                    "unit": "GFLOP/s", "steps": steps})
+    except Exception as e:  # reported beside the headline, never a silent substitute for it
+        out["unavailable"] = repr(e)[:300]
+    return out
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -304,6 +343,10 @@ def main():
             print(json.dumps({"profile_run": True, "ms_per_step": ms_per_step, "value": value}))
         return
 
+    allgather = None
+    if world > 1 and args.allgather != "none":
+        allgather = time_allgather(args, plan, Bd, A, stream, world, shared)
+
     # warm regime: the same steps back to back, no L2 flush in between
     w0, w1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
@@ -398,7 +441,7 @@ def main():
             "plan_build": args.build,
             "warm": {"ms_per_step": warm_ms, "value": 2.0 * A.nnz * args.N / (warm_ms / 1e3) / 1e9,
                      "note": "back-to-back steps without the L2 flush (rank-local)"},
-            "plan_create_s": plan_s, "broadcast_ms": bcast_ms, "wall_s_timed_loop": wall,
+            "plan_create_s": plan_s, "broadcast_ms": bcast_ms, "allgather": allgather, "wall_s_timed_loop": wall,
             "step_ms_min": min(step_ms), "step_ms_max": max(step_ms),
         }
         emit(out, args)

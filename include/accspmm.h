@@ -150,6 +150,18 @@ accspmm_status accspmm_plan_create_ex(int64_t M, int64_t K, const int64_t *rowpt
  * (N % 16 != 0, host-only plan), OUT_OF_MEMORY, CUDA (launch failure). */
 accspmm_status accspmm_execute(const accspmm_plan *plan, const void *B, int64_t N, void *C, void *stream);
 
+/* Fused all-gather (multi-GPU, BASELINE "optional all-gather" of the C slabs): instead of
+ * writing this plan's slab, the SpMM epilogue writes every finished row, in ORIGINAL row
+ * order, into each of the n_dst full M x N float32 matrices C_all[0..n_dst) (1 <= n_dst <= 8;
+ * typically this GPU's C and its peers' C mapped through CUDA IPC / symmetric memory over
+ * NVLink, which must be accessible from the plan's device).  The gather thus overlaps the
+ * compute window by window and needs neither a collective nor the un-permute kernel; after
+ * every rank's call completed (a barrier across the ranks' streams, the caller's job) each
+ * C_all matrix holds the whole product.  Works for any plan (nparts = 1: all rows).  Errors
+ * as accspmm_execute, plus INVALID_VALUE for n_dst out of range or NULL/misaligned entries. */
+accspmm_status accspmm_execute_allgather(const accspmm_plan *plan, const void *B, int64_t N, void *const *C_all,
+                                         int32_t n_dst, void *stream);
+
 /* End-to-end variant with HOST buffers: copies B (K x N, host) to the device,
  * executes, copies C (host, same shape as accspmm_execute's C) back and
  * synchronises `stream`.  Pinned host memory gives full PCIe bandwidth. */

@@ -67,6 +67,7 @@ EXPORTED = [
     "accspmm_unpermute", "accspmm_debug_round_tf32", "accspmm_debug_decode", "accspmm_status_string",
     "accspmm_last_error", "accspmm_abi_version", "accspmm_plan_set_timing", "accspmm_plan_kernel_times",
     "accspmm_probe_l2_bandwidth", "accspmm_execute_host_batch", "accspmm_csr_transpose",
+    "accspmm_execute_allgather",
 ]
 
 
@@ -105,6 +106,7 @@ def load_library(path: str = LIB_PATH):
         "accspmm_probe_l2_bandwidth": ([I64, I32, ctypes.POINTER(ctypes.c_double)], S),
         "accspmm_execute_host_batch": ([P, P, P, I32, I64, P], S),
         "accspmm_csr_transpose": ([I64, I64, P, P, P, P, P, P], S),
+        "accspmm_execute_allgather": ([P, P, I64, P, I32, P], S),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -173,6 +175,11 @@ def accspmm_execute_host_batch(plan, B_host_ptrs, C_host_ptrs, N, stream_ptr=Non
     Bs = (ctypes.c_void_p * max(n, 1))(*B_host_ptrs)
     Cs = (ctypes.c_void_p * max(n, 1))(*C_host_ptrs)
     _check(load_library().accspmm_execute_host_batch(plan, Bs, Cs, n, int(N), stream_ptr))
+
+
+def accspmm_execute_allgather(plan, B_ptr, N, C_ptrs, stream_ptr=None):
+    arr = (ctypes.c_void_p * max(len(C_ptrs), 1))(*C_ptrs)
+    _check(load_library().accspmm_execute_allgather(plan, B_ptr, int(N), arr, len(C_ptrs), stream_ptr))
 
 
 def accspmm_plan_destroy(plan):
@@ -344,6 +351,13 @@ class Plan:
             C = torch.empty((self.out_rows, N), dtype=torch.float32, device=B.device)
         accspmm_execute(self.handle, B.data_ptr(), N, C.data_ptr(), _stream_ptr(stream))
         return C
+
+    def execute_allgather(self, B, C_all, stream=None):
+        """Fused all-gather: this plan's rows go to every matrix of C_all (full M x N float32
+        CUDA tensors, local or peer-mapped) in original row order."""
+        accspmm_execute_allgather(self.handle, B.data_ptr(), B.shape[1], [c.data_ptr() for c in C_all],
+                                  _stream_ptr(stream))
+        return C_all
 
     def execute_host(self, B_host, C_host, stream=None):
         """End to end with host buffers (numpy or pinned torch CPU tensors)."""

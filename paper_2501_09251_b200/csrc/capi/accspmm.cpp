@@ -85,7 +85,7 @@ static void free_device(accspmm_plan *p)
 {
     auto &d = p->dev;
     cudaFree(d.rwo); cudaFree(d.tco); cudaFree(d.a2b); cudaFree(d.bits); cudaFree(d.vals);
-    cudaFree(d.units); cudaFree(d.row_map); cudaFree(d.col_perm);
+    cudaFree(d.units); cudaFree(d.row_map); cudaFree(d.col_perm); cudaFree(d.orig_map);
     cudaFree(p->ws); cudaFree(p->counters); cudaFree(p->dB); cudaFree(p->dC); cudaFree(p->Br); cudaFree(p->zrow);
     cudaFree(p->dB2); cudaFree(p->dC2);
     p->dB2 = nullptr; p->dC2 = nullptr;
@@ -309,6 +309,7 @@ accspmm_status accspmm_plan_create_ex(int64_t M, int64_t K, const int64_t *rowpt
         if (st == ACCSPMM_OK) st = upload(&d.units, p->units_host, bytes);
         if (st == ACCSPMM_OK && opt.nparts == 1 && !perm.empty()) st = upload(&d.row_map, p->orig_rows, bytes);
         if (st == ACCSPMM_OK && cm) st = upload(&d.col_perm, perm, bytes);
+        if (st == ACCSPMM_OK && opt.nparts > 1) st = upload(&d.orig_map, p->orig_rows, bytes);
         if (st == ACCSPMM_OK) {
             std::vector<uint32_t> zeros(256, 0u);  // 1 KB: covers a 128-wide FP32 feature slice
             st = upload((uint32_t **)&p->zrow, zeros, bytes);
@@ -353,7 +354,8 @@ static accspmm_status ensure_workspace(const accspmm_plan *p, int64_t N)
     return ACCSPMM_OK;
 }
 
-accspmm_status accspmm_execute(const accspmm_plan *p, const void *B, int64_t N, void *C, void *stream)
+static accspmm_status execute_impl(const accspmm_plan *p, const void *B, int64_t N, void *C, float *const *dst,
+                                   int ndst, void *stream)
 {
     if (!p) return fail(ACCSPMM_ERR_INVALID_VALUE, "plan is NULL");
     if (p->opt.device < 0) return fail(ACCSPMM_ERR_UNSUPPORTED, "host-only plan cannot execute (no CPU fallback)");
@@ -395,12 +397,30 @@ accspmm_status accspmm_execute(const accspmm_plan *p, const void *B, int64_t N, 
     }
     const bool timed = p->timing && p->ev_n + 2 <= p->ev.size();
     if (timed) cudaEventRecord(p->ev[p->ev_n], (cudaStream_t)stream);
-    st = launch_spmm(p->dev, Bk, p->zrow, N, (float *)C, p->ws, p->counters, stream, in_kernel_round);
+    st = launch_spmm(p->dev, Bk, p->zrow, N, (float *)C, p->ws, p->counters, stream, in_kernel_round, dst, ndst);
     if (timed) {
         cudaEventRecord(p->ev[p->ev_n + 1], (cudaStream_t)stream);
         p->ev_n += 2;
     }
     return st;
+}
+
+accspmm_status accspmm_execute(const accspmm_plan *p, const void *B, int64_t N, void *C, void *stream)
+{
+    return execute_impl(p, B, N, C, nullptr, 0, stream);
+}
+
+accspmm_status accspmm_execute_allgather(const accspmm_plan *p, const void *B, int64_t N, void *const *C_all,
+                                         int32_t n_dst, void *stream)
+{
+    if (n_dst < 1 || n_dst > kMaxGatherDst || !C_all) return fail(ACCSPMM_ERR_INVALID_VALUE, "1 <= n_dst <= 8 required");
+    float *dst[kMaxGatherDst] = {};
+    for (int32_t k = 0; k < n_dst; ++k) {
+        if (!C_all[k] || ((uintptr_t)C_all[k] & 15))
+            return fail(ACCSPMM_ERR_INVALID_VALUE, "C_all entries must be non-NULL and 16-byte aligned");
+        dst[k] = (float *)C_all[k];
+    }
+    return execute_impl(p, B, N, dst[0], dst, n_dst, stream);
 }
 
 accspmm_status accspmm_execute_host(const accspmm_plan *p, const void *B_host, int64_t N, void *C_host, void *stream)

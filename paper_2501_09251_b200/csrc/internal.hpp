@@ -14,6 +14,7 @@ constexpr uint32_t kPadLane = 0xFFFFFFFFu;  // device SparseAToB padding lane (r
 constexpr int kWmax = 31;             // windows per concatenated unit (one per lane of the window table)
 constexpr double kIbdThreshold = 8.0; // P:417 "When IBD exceeds 8"
 constexpr int kPaperCap = 32;         // P:446 "maximum threshold of 32 TC blocks per TB"
+constexpr int kMaxGatherDst = 8;      // destinations of the fused all-gather epilogue (one per GPU)
 constexpr int kGroupCap = 32;         // concatenation limit of grouped plans, automatic cap (reading R7c)
 // TF32 rho(B): a separate rounding pass over B when every B row is gathered at least this
 // many times on average (sum_w |U_w| >= kRoundReuse * K), else cvt.rna in the kernel
@@ -88,6 +89,7 @@ struct DevicePlan {
     uint32_t *units = nullptr;     // [n_units][8]
     uint32_t *row_map = nullptr;   // slab row -> C row (nparts == 1 with a permutation), else null
     uint32_t *col_perm = nullptr;  // permute_cols: B'[i] = B[col_perm[i]] is gathered each execute
+    uint32_t *orig_map = nullptr;  // slab row -> original row (fused all-gather); = row_map when nparts == 1
     int64_t K = 0;                 // rows of B (padding lanes gather row K -> TMA zero fill)
     // cached TMA tensor maps of the last B operand (key: ptr, N, FW, dtype): one per feature
     // slice (kMaxSliceMaps at most), else one map over all N columns
@@ -116,8 +118,10 @@ void free_device_format(DeviceFormat &f);
 int pick_fw(int64_t N);
 
 // round_b: the kernel applies rho(B) in registers (B not pre-rounded)
+// dst/ndst (ndst > 0): fused all-gather epilogue instead of C (accspmm_execute_allgather)
 accspmm_status launch_spmm(const DevicePlan &p, const void *B, const void *zrow, int64_t N, float *C, float *ws,
-                           uint32_t *counters, void *stream, bool round_b);
+                           uint32_t *counters, void *stream, bool round_b, float *const *dst = nullptr,
+                           int ndst = 0);
 accspmm_status launch_round_b(const float *B, float *Br, int64_t n, void *stream);
 // B' = B[perm] row gather (K rows of row_bytes), optionally with rho = TF32 RNA (f32 rows)
 accspmm_status launch_permute_b(const void *B, void *Bp, const uint32_t *perm, int64_t K, int64_t row_bytes,

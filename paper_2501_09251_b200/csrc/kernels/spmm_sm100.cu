@@ -46,20 +46,21 @@ namespace {
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src, uint64_t pol)
+// A-stream staging copies.  No L2::cache_hint operand: with the constant-folded
+// createpolicy value ptxas (12.9) emitted one LDGSTS of a large kernel with an uninitialised
+// uniform descriptor register (desc[UR1], "illegal instruction" at run time); the policy
+// argument is kept in the signature for the call sites and ignored.
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src, uint64_t)
 {
-    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "l"(pol)
-                 : "memory");
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
 }
-__device__ __forceinline__ void cp_async8(uint32_t dst, const void *src, uint64_t pol)
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void *src, uint64_t)
 {
-    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "l"(pol)
-                 : "memory");
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src) : "memory");
 }
-__device__ __forceinline__ void cp_async4(uint32_t dst, const void *src, uint64_t pol)
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void *src, uint64_t)
 {
-    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2;\n" ::"r"(dst), "l"(src), "l"(pol)
-                 : "memory");
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dst), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
@@ -199,6 +200,11 @@ struct KParams {
     int64_t n_units;
     int32_t nslices;
     int32_t Krows;
+    // fused all-gather (accspmm_execute_allgather): every finished window row is also (only)
+    // written to dst[0..ndst) -- full M x N matrices, local or peer memory -- at orig_map[row]
+    int32_t ndst;
+    const uint32_t *__restrict__ orig_map;
+    float *dst[kMaxGatherDst];
 };
 
 template <int FW, bool F16>
@@ -754,12 +760,12 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
         }
     };
 
-    auto store_rows = [&](float *base, int64_t ld, int64_t lr0, bool remap) {
+    auto store_rows = [&](float *base, int64_t ld, int64_t lr0, bool remap, const uint32_t *rmap) {
 #pragma unroll
         for (int s2 = 0; s2 < 2; ++s2) {
             const int64_t lr = lr0 + 2 * t + s2;
             if (!remap || lr < p.rows) {
-                const int64_t orow = remap ? (p.row_map ? (int64_t)__ldg(p.row_map + lr) : lr) : (2 * t + s2);
+                const int64_t orow = remap ? (rmap ? (int64_t)__ldg(rmap + lr) : lr) : (2 * t + s2);
                 if constexpr (LDSM) {  // tile mt: features 16mt + g (c0/c1) and 16mt + 8 + g (c2/c3)
                     float *d = base + orow * ld + g;
 #pragma unroll
@@ -787,7 +793,13 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
         }
     };
     auto store_window = [&](uint32_t wi) {
-        store_rows(p.C + f0, p.N, (int64_t)(w0 + wi) * 8, true);
+        const int64_t lr0 = (int64_t)(w0 + wi) * 8;
+        if (p.ndst == 0) {
+            store_rows(p.C + f0, p.N, lr0, true, p.row_map);
+        } else {  // fused all-gather: the rows go straight to every rank's C (original order)
+#pragma unroll 1
+            for (int d = 0; d < p.ndst; ++d) store_rows(p.dst[d] + f0, p.N, lr0, true, p.orig_map);
+        }
 #pragma unroll
         for (int m = 0; m < MT; ++m) acc[m][0] = acc[m][1] = acc[m][2] = acc[m][3] = 0.f;
     };
@@ -846,7 +858,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     if (split) {
         const uint32_t sid = ub.x, seg = ub.y, nseg = ub.z, slot = ub.w;
         float *tile = p.ws + ((int64_t)slot * p.nslices + slice) * (8 * FW);
-        store_rows(tile, FW, 0, false);
+        store_rows(tile, FW, 0, false, nullptr);
         __threadfence();
         __syncwarp();
         uint32_t prev = 0;
@@ -1041,7 +1053,7 @@ accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, 
     // kernel), 46 = 2 warps per CTA with tuned bounds, 47 = FP16 fragments by LDS.128 + PRMT,
     // 10-12 = register-direct gather (4, 2, 8 warps per CTA).
     constexpr int MW = tuned_min_warps<FW, F16>();
-    const int kcfg = env_int("ACCSPMM_KCFG", -1);
+    const int kcfg = kp.ndst > 0 ? -1 : env_int("ACCSPMM_KCFG", -1);  // all-gather: default kernel
     if (kcfg < 0 || kcfg >= 20) {
         const G4Maps *map = nullptr;
         // per-slice maps only for the kernels instantiated with them (variants 20/46: one map)
@@ -1120,7 +1132,7 @@ accspmm_status launch_permute_b(const void *B, void *Bp, const uint32_t *perm, i
 }
 
 accspmm_status launch_spmm(const DevicePlan &d, const void *B, const void *zrow, int64_t N, float *C, float *ws,
-                           uint32_t *counters, void *stream, bool round_b)
+                           uint32_t *counters, void *stream, bool round_b, float *const *dst, int ndst)
 {
     if (d.rows == 0) return ACCSPMM_OK;
     const int FW = pick_fw(N);
@@ -1142,6 +1154,9 @@ accspmm_status launch_spmm(const DevicePlan &d, const void *B, const void *zrow,
     kp.n_units = d.n_units;
     kp.nslices = (int32_t)(N / FW);
     kp.Krows = (int32_t)d.K;
+    kp.ndst = ndst;
+    kp.orig_map = d.orig_map ? d.orig_map : d.row_map;
+    for (int k = 0; k < kMaxGatherDst; ++k) kp.dst[k] = k < ndst ? dst[k] : nullptr;
     cudaStream_t s = (cudaStream_t)stream;
     const bool f16 = d.precision == ACCSPMM_FP16;
     const bool r = round_b;

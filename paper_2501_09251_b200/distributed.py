@@ -7,6 +7,12 @@ broadcast once from rank 0 (NCCL over NVLink on the GPU box), each rank writes i
 C slab in reordered-row order, and the optional all-gather of padded slabs plus
 ``accspmm_unpermute`` (a device kernel) restores C in original row order.
 
+The fused alternative to that all-gather (``spmm_allgather_fused``): C lives in symmetric
+memory (torch.distributed._symmetric_memory, peer-mapped over NVLink), and every rank's SpMM
+epilogue writes its rows straight into every rank's C in original row order
+(``accspmm_execute_allgather``) -- the exchange overlaps the compute window by window, with
+no collective and no un-permute pass; a device-side barrier closes the step.
+
 This module only moves data between ranks and calls the C ABI; the SpMM and the
 un-permute run in libaccspmm's CUDA kernels.
 """
@@ -71,3 +77,31 @@ def spmm_all(plan: Plan, B, M: int, stream=None):
     C_slab = plan.execute(B, stream=stream)
     G, I = gather_slabs(C_slab, plan.export_rows())
     return unpermute(G, I, M, stream)
+
+
+class FusedAllGather:
+    """Symmetric-memory C (M x N float32) shared by the ranks of ``group`` and the peer views
+    the fused epilogue writes into.  Allocate once, reuse for every step."""
+
+    def __init__(self, M: int, N: int, device, group=None):
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+        self.group = group or dist.group.WORLD
+        self.C = symm.empty(M, N, dtype=torch.float32, device=device)
+        self.hdl = symm.rendezvous(self.C, self.group)
+        world = dist.get_world_size(self.group)
+        self.views = [self.hdl.get_buffer(r, (M, N), torch.float32) for r in range(world)]
+        self.hdl.barrier()
+
+    def step(self, plan: Plan, B, stream=None):
+        """C = A . B on every rank: this rank's rows are written into all ranks' C, then a
+        device barrier (on the current stream) waits for every rank's rows."""
+        plan.execute_allgather(B, self.views, stream)
+        self.hdl.barrier()
+        return self.C
+
+
+def spmm_allgather_fused(plan: Plan, B, M: int, group=None, stream=None):
+    """One-shot fused all-gather (allocates the symmetric C; use FusedAllGather to reuse it)."""
+    return FusedAllGather(M, B.shape[1], B.device, group).step(plan, B, stream)

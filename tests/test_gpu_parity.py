@@ -531,3 +531,26 @@ def test_execute_is_cuda_graph_capturable(precision):
     g.replay()
     torch.cuda.synchronize()
     assert_bit_exact(C.cpu().numpy(), A, v, B1, precision)
+
+
+@pytest.mark.parametrize("precision", PRECISIONS)
+@pytest.mark.parametrize("P", [1, 3])
+def test_fused_allgather_epilogue(precision, P):
+    """accspmm_execute_allgather on one GPU with several local destinations standing in for
+    the ranks' C: every part's rows land in every destination in original row order, so after
+    all P parts each destination is the whole product (integer data: bit-exact)."""
+    import torch
+    A = gen.dcsbm(4000, 200_000, 6, 2.2, 0.2, 2500, seed=2, oversample=1.3)
+    v = gen.values_int(A.nnz, 1)
+    B = gen.dense_int(A.K, 256, 2)
+    Bd = to_dev_B(B, precision)
+    dsts = [torch.full((A.M, 256), float("nan"), device="cuda") for _ in range(3)]
+    for part in range(P):
+        p = acc.Plan(A.M, A.K, A.rowptr, A.colidx, v, precision=precision, reorder="on", balance="on",
+                     unit_cap=32, part=part, nparts=P)
+        p.execute_allgather(Bd, dsts)
+    torch.cuda.synchronize()
+    for d in dsts:
+        assert_bit_exact(d.cpu().numpy(), A, v, B, precision)
+    with pytest.raises(acc.AccSpmmError):
+        acc.accspmm_execute_allgather(p.handle, Bd.data_ptr(), 256, [])

@@ -291,3 +291,14 @@ def test_permute_cols_format_is_symmetric_permutation(precision, nparts):
     # without a permutation (reorder off) the option changes nothing
     off = host_plan(A, v, precision=precision, reorder="off", permute_cols=True)
     assert off.info["cols_permuted"] == 0
+
+
+def test_sass_reads_no_unwritten_uniform_registers():
+    """Guard against a ptxas (12.9) miscompile seen in this kernel: an LDGSTS whose cache-policy
+    descriptor sat in a uniform register that no instruction wrote ('illegal instruction' at
+    run time on large units).  Every kernel of the built library is scanned (tools/check_sass_ur.py)."""
+    import subprocess
+    import sys
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "check_sass_ur.py"), acc.LIB_PATH],
+                       capture_output=True, text=True, check=True)
+    assert r.stdout.strip().endswith("kernels with unwritten uniform reads: 0"), r.stdout[-2000:]
