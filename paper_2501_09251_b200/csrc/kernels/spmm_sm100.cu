@@ -559,7 +559,7 @@ using G4Maps = G4MapsT<kMaxSliceMaps>;
 inline int map_count(const KParams &kp) { return kp.nslices > 1 && kp.nslices <= kMaxSliceMaps ? kp.nslices : 1; }
 
 template <int FW, bool F16, int WARPS, int STAGES, bool RND, int MINB = 1, int NM = 1, bool LDSM_ = false,
-          bool K8 = false>
+          bool K8 = false, int VD = 1>
 __global__ void __launch_bounds__(WARPS * 32, MINB)
     spmm_bittcf_g4_kernel(const KParams p, const __grid_constant__ G4MapsT<NM> maps)
 {
@@ -622,10 +622,11 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
         }
         cp_async_commit();
     };
-    // Value registers of the blocks in flight: decoded and loaded one block ahead of use (a
-    // 2-slot register ring).  Two blocks ahead, a bulk L2 prefetch of each chunk's value
-    // range and staging values through shared memory were measured and lost.
-    constexpr int VR = 2;
+    // Value registers of the blocks in flight: decoded and loaded VD blocks ahead of use (a
+    // VR-slot register ring).  A bulk L2 prefetch of each chunk's value range and staging
+    // values through shared memory were measured and lost.
+    static_assert(VD == 1 || VD == 2, "value distance");
+    constexpr int VR = VD == 1 ? 2 : 4;
     uint32_t vb0[VR], vb1[VR];
 
     // ---- every lane: decode this lane's two tile entries of block j, load values
@@ -824,25 +825,38 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     issue_chunk(CH);
     after_block(b0);
     if (nblk > 0) value_load(0u, 0);
+    if (VD == 2 && nblk > 1) value_load(1u, 1);
     if (nblk > 0) issue_tma(0, 0);
     // Block step j: TMA for j+1, values for j+1 (at a chunk boundary first wait for that
     // chunk and prefetch the one after), then the decode-free MMA of block j.
     static_assert(STAGES == 2, "the block step below is written for a 2-stage TMA ring");
     auto step = [&](uint32_t j, int u, bool checked) {
         const uint32_t jn = j + 1;
-        if ((jn & (CH - 1u)) == 0) {  // chunk (jn / CH) must have landed
-            cp_async_wait_all();
-            __syncwarp();
-            issue_chunk(jn + CH);
-        }
-        if (!checked || jn < nblk) {
-            issue_tma(jn, (u + 1) & 1);
-            value_load(jn, (u + 1) & (VR - 1));
+        if constexpr (VD == 1) {
+            if ((jn & (CH - 1u)) == 0) {  // chunk (jn / CH) must have landed
+                cp_async_wait_all();
+                __syncwarp();
+                issue_chunk(jn + CH);
+            }
+            if (!checked || jn < nblk) {
+                issue_tma(jn, (u + 1) & 1);
+                value_load(jn, (u + 1) & (VR - 1));
+            }
+        } else {
+            // the TMA of jn reads its row ids before chunk jv + CH may overwrite jn's buffer
+            const uint32_t jv = j + 2;
+            if (!checked || jn < nblk) issue_tma(jn, (u + 1) & 1);
+            if ((jv & (CH - 1u)) == 0) {
+                cp_async_wait_all();
+                __syncwarp();
+                issue_chunk(jv + CH);
+            }
+            if (!checked || jv < nblk) value_load(jv, (u + 2) & (VR - 1));
         }
         consume(j, u & 1, u & (VR - 1));
         after_block(b0 + j + 1);
     };
-    const uint32_t nmain = nblk >= 1u ? ((nblk - 1u) / VR) * VR : 0u;
+    const uint32_t nmain = nblk >= (uint32_t)VD ? ((nblk - VD) / VR) * VR : 0u;
     uint32_t j = 0;
     for (; j < nmain; j += VR) {
 #pragma unroll
@@ -963,12 +977,12 @@ int env_int(const char *name, int dflt)
 // NM = 1: one tensor map (the full-width map when several slices exist); NM = kMaxSliceMaps:
 // one map per slice (tensor_map decides; only the default configurations instantiate it)
 template <int FW, bool F16, int WARPS, int STAGES, bool RND = false, int MINB = 1, int NM = 1, bool LDSM = false,
-          bool K8 = false>
+          bool K8 = false, int VD = 1>
 accspmm_status launch_g4(const KParams &kp, const G4Maps *map, int64_t n_units, cudaStream_t stream)
 {
     using SM = G4WarpSmem<FW, F16, STAGES>;
     const size_t smem = sizeof(SM) * WARPS;
-    auto kern = spmm_bittcf_g4_kernel<FW, F16, WARPS, STAGES, RND, MINB, NM, LDSM, K8>;
+    auto kern = spmm_bittcf_g4_kernel<FW, F16, WARPS, STAGES, RND, MINB, NM, LDSM, K8, VD>;
     static int configured_device = -1;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -1076,6 +1090,9 @@ accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, 
         case 48:  // TF32 m16n8k8 vs two m16n8k4: the opposite of the default choice
             if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, !K8>(kp, map, n_units, stream);
             return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, !K8>(kp, map, n_units, stream);
+        case 49:  // values loaded two blocks ahead (4-slot ring)
+            if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 2>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 2>(kp, map, n_units, stream);
         case 47:  // FP16 fragments by LDS.128 + PRMT packing
             if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM>(kp, map, n_units, stream);
             return launch_g4<FW, F16, 1, 2, false, MW>(kp, map, n_units, stream);
