@@ -16,6 +16,7 @@ from .matrices import (  # noqa: F401
     road_grid,
     molecules,
     web_hosts,
+    add_hub_rows,
     sbm,
     identity,
     permutation_matrix,

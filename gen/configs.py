@@ -49,6 +49,11 @@ def _products():
     return mx.dcsbm(2_449_029, 123_718_280, 47, 2.1, 0.10, 17_481, seed=9, oversample=1.22)
 
 
+def _products_hubs():
+    # SURVEY §8(d) P adversarial variant: products-shaped plus 8 hub rows of 200K nnz each
+    return mx.add_hub_rows(_products(), 8, 200_000, seed=21)
+
+
 def _papers100m():
     # directed, out-degree lognormal(2.3, 0.8) rescaled to mean 14.55, popularity Pareto(1.2)
     return mx.powerlaw_directed(111_059_956, 14.55, seed=11)
@@ -96,6 +101,8 @@ CONFIGS = {
                  "DD-shaped union of ~284-node protein graphs ~335K nodes ~1.7M nnz (type-1)"),
     "webberkstan": Config("webberkstan", -1, (128, 256, 512), 19, 20, _webberkstan,
                           "web-BerkStan-shaped directed host-block web graph 685,230 nodes ~7.6M nnz (type-1)"),
+    "products_hubs": Config("products_hubs", 3, (128,), 9, 10, _products_hubs,
+                            "ogbn-products-shaped DC-SBM plus 8 hub rows of 200K nnz (balancer stress)"),
     "papers100m": Config("papers100m", 4, (64,), 11, 12, _papers100m,
                          "ogbn-papers100M-shaped directed power-law 111,059,956 nodes ~1.6B nnz"),
     "papers100m_small": Config("papers100m_small", 4, (64,), 11, 12, _papers100m_small,

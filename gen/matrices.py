@@ -249,6 +249,21 @@ def web_hosts(n: int, mean_deg: float, local_frac: float, seed: int, mean_host: 
     return csr_from_pairs(src, dst, n, n)
 
 
+def add_hub_rows(A: Csr, hubs: int, nnz_per_hub: int, seed: int) -> Csr:
+    """SURVEY §8(d) P adversarial variant: ``hubs`` rows (spread over the matrix) replaced by rows
+    of ``nnz_per_hub`` distinct uniformly drawn columns (not symmetrised: the load balancer's
+    worst case is one window with ~nnz_per_hub / 8 * hubs-in-window blocks)."""
+    rng = np.random.default_rng(seed)
+    hub_rows = np.sort(rng.choice(A.M, size=hubs, replace=False))
+    keep = ~np.isin(A.row_ids(), hub_rows)
+    rows = [A.row_ids()[keep]]
+    cols = [A.colidx[keep].astype(np.int64)]
+    for h in hub_rows:
+        rows.append(np.full(nnz_per_hub, h, np.int64))
+        cols.append(rng.choice(A.K, size=nnz_per_hub, replace=False).astype(np.int64))
+    return csr_from_pairs(np.concatenate(rows), np.concatenate(cols), A.M, A.K)
+
+
 def sbm(n: int, blocks: int, p_in: float, p_out: float, seed: int, shuffle: bool = True) -> Csr:
     """Symmetric 0/1 stochastic block model, no self-loops, optional label shuffle."""
     rng = np.random.default_rng(seed)

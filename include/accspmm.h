@@ -140,12 +140,15 @@ accspmm_status accspmm_plan_create_ex(int64_t M, int64_t K, const int64_t *rowpt
  * back through the permutation).  nparts > 1: C is the slab, info.rows x N, in
  * reordered row order (accspmm_plan_export_rows gives each slab row's original id).
  * Every element of C is written (empty rows get 0); there is no beta.
- * B and C are device pointers (see conventions).  For TF32 plans the call
- * launches two kernels: rho(B) into a plan-owned K x N scratch (one elementwise
- * pass; every B row is then gathered by many windows), then the SpMM kernel.
- * The first call for a given N may allocate the scratch and a split-window
- * workspace (cudaMalloc).  Concurrent executes of
- * one plan on different streams are not allowed (they share the workspace).
+ * B and C are device pointers (see conventions).  The call launches the SpMM
+ * kernel, preceded by one pass over B into a plan-owned K x N scratch when
+ * (a) the plan is TF32 and every B row is gathered >= 32 times on average
+ * (sum_w |U_w| >= 32 K): rho(B) once instead of in the kernel, or (b) the plan
+ * has permute_cols: the row gather B' = P B (fused with (a)).  The first call
+ * for a given N may allocate the scratch and a split-window workspace
+ * (cudaMalloc); later calls only launch kernels on `stream`, so they can be
+ * captured into a CUDA graph.  Concurrent executes of one plan on different
+ * streams are not allowed (they share the workspace).
  * Errors: INVALID_VALUE (null/misaligned pointers, N <= 0), UNSUPPORTED
  * (N % 16 != 0, host-only plan), OUT_OF_MEMORY, CUDA (launch failure). */
 accspmm_status accspmm_execute(const accspmm_plan *plan, const void *B, int64_t N, void *C, void *stream);

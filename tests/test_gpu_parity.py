@@ -554,3 +554,27 @@ def test_fused_allgather_epilogue(precision, P):
         assert_bit_exact(d.cpu().numpy(), A, v, B, precision)
     with pytest.raises(acc.AccSpmmError):
         acc.accspmm_execute_allgather(p.handle, Bd.data_ptr(), 256, [])
+
+
+def test_products_hub_rows_balancer_stress():
+    """SURVEY §8(d) P adversarial variant (8 rows of 200K nnz on the products shape): the hub
+    windows are split into many segments and reduced by the deterministic fixup; the hub rows
+    and a random row sample match the oracle, and balance on = balance off bitwise on the hubs
+    (integer data)."""
+    cfg, A = gen.make_config("products_hubs")
+    nnz_row = np.diff(A.rowptr)
+    hubs = np.nonzero(nnz_row >= 200_000)[0]
+    assert hubs.size == 8
+    rows = np.union1d(hubs, _sample_rows(A.M, 2000, 3))
+    v = gen.values_uniform(A.nnz, cfg.seed_A + 1)
+    B = gen.dense_normal(A.K, 128, cfg.seed_B)
+    C, p = run(A, v, B, "tf32", reorder="auto", build="device")
+    assert p.info["balanced"] == 1 and p.info["n_split_windows"] > 0
+    assert_within(C, A, v, B, "tf32", rows=rows)
+    vi = gen.values_int(A.nnz, 2)
+    Bi = gen.dense_int(A.K, 64, 3)
+    Con, _ = run(A, vi, Bi, "tf32", balance="on", build="device")
+    Coff, _ = run(A, vi, Bi, "tf32", balance="off", build="device")
+    assert np.array_equal(Con[hubs], Coff[hubs])
+    Cr, _ = oracle(A, vi, Bi, "tf32", rows=hubs)
+    assert np.array_equal(Con[hubs].astype(np.float64), Cr)
