@@ -20,7 +20,10 @@
  *     plan's device: float32 for ACCSPMM_TF32, IEEE binary16 for ACCSPMM_FP16;
  *     16-byte aligned.  C is float32, row-major, leading dimension N, 16-byte
  *     aligned, caller-owned, on the plan's device.
- *   - N must be a positive multiple of 16 (ACCSPMM_ERR_UNSUPPORTED otherwise).
+ *   - N >= 1.  The kernels run on feature widths Np = 16, 32, 64 or a multiple of
+ *     128; any other N goes through a zero-padded K x Np copy of B and a padded C
+ *     (two 2-D copies on the stream, plan-owned scratch; Np = the next such width),
+ *     so any N and any alignment of B and C is accepted there.
  *   - Streams are CUDA runtime streams passed as `void*` (cudaStream_t); NULL
  *     is the legacy default stream.
  *   - Every function returns a status; on failure a thread-local message is
@@ -46,7 +49,7 @@ typedef enum {
     ACCSPMM_OK = 0,
     ACCSPMM_ERR_INVALID_VALUE = 1,  /* null pointer, bad size, bad option, misaligned pointer     */
     ACCSPMM_ERR_INVALID_CSR = 2,    /* rowptr not monotone / colidx unsorted, duplicate, out of range */
-    ACCSPMM_ERR_UNSUPPORTED = 3,    /* N not a multiple of 16, u32 offset overflow, host-only plan  */
+    ACCSPMM_ERR_UNSUPPORTED = 3,    /* u32 offset overflow, host-only plan, fused all-gather N % 16 */
     ACCSPMM_ERR_OUT_OF_MEMORY = 4,  /* host or device allocation failed                           */
     ACCSPMM_ERR_CUDA = 5,           /* a CUDA runtime call or kernel launch failed                 */
     ACCSPMM_ERR_INTERNAL = 6
@@ -149,8 +152,8 @@ accspmm_status accspmm_plan_create_ex(int64_t M, int64_t K, const int64_t *rowpt
  * (cudaMalloc); later calls only launch kernels on `stream`, so they can be
  * captured into a CUDA graph.  Concurrent executes of one plan on different
  * streams are not allowed (they share the workspace).
- * Errors: INVALID_VALUE (null/misaligned pointers, N <= 0), UNSUPPORTED
- * (N % 16 != 0, host-only plan), OUT_OF_MEMORY, CUDA (launch failure). */
+ * Errors: INVALID_VALUE (null pointers, N <= 0, B or C not 16-byte aligned when
+ * N % 16 == 0), UNSUPPORTED (host-only plan), OUT_OF_MEMORY, CUDA (launch failure). */
 accspmm_status accspmm_execute(const accspmm_plan *plan, const void *B, int64_t N, void *C, void *stream);
 
 /* Fused all-gather (multi-GPU, BASELINE "optional all-gather" of the C slabs): instead of

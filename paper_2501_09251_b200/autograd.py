@@ -56,11 +56,9 @@ class _SpMM(torch.autograd.Function):
 
 def spmm(op: SparseOperator, B: torch.Tensor) -> torch.Tensor:
     """C = A . B (float32 C); B is K x N on the plan's device, float32 (TF32 plans) or
-    float16 (FP16 plans), N a multiple of 16."""
+    float16 (FP16 plans), any N >= 1 (N % 16 != 0 is padded inside the library)."""
     if B.dim() != 2 or B.shape[0] != op.K:
         raise ValueError(f"B must be {op.K} x N, got {tuple(B.shape)}")
-    if B.shape[1] % 16 != 0:
-        raise ValueError("N must be a multiple of 16")
     if B.dtype != op.in_dtype:
         raise TypeError(f"B must be {op.in_dtype} for a {op.precision} plan")
     if not B.is_cuda:

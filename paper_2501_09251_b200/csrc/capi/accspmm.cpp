@@ -36,6 +36,11 @@ struct accspmm_plan {
     mutable size_t Br_bytes = 0;
     // zero row read by padding lanes (>= 128 features x 4 B)
     void *zrow = nullptr;
+    // N % 16 != 0: B and C staged through zero-padded K x Np / rows x Np scratch
+    mutable void *padB = nullptr;
+    mutable size_t padB_bytes = 0;
+    mutable float *padC = nullptr;
+    mutable size_t padC_bytes = 0;
     // kernel timing ring
     mutable bool timing = false;
     mutable std::vector<cudaEvent_t> ev;
@@ -89,6 +94,8 @@ static void free_device(accspmm_plan *p)
     cudaFree(p->ws); cudaFree(p->counters); cudaFree(p->dB); cudaFree(p->dC); cudaFree(p->Br); cudaFree(p->zrow);
     cudaFree(p->dB2); cudaFree(p->dC2);
     p->dB2 = nullptr; p->dC2 = nullptr;
+    cudaFree(p->padB); cudaFree(p->padC);
+    p->padB = nullptr; p->padC = nullptr;
     if (p->s_h2d) cudaStreamDestroy(p->s_h2d);
     if (p->s_d2h) cudaStreamDestroy(p->s_d2h);
     p->s_h2d = p->s_d2h = nullptr;
@@ -355,12 +362,67 @@ static accspmm_status ensure_workspace(const accspmm_plan *p, int64_t N)
 }
 
 static accspmm_status execute_impl(const accspmm_plan *p, const void *B, int64_t N, void *C, float *const *dst,
+                                   int ndst, void *stream);
+
+// The feature width the kernels run at: a few wide slices rather than many narrow ones
+// (N = 602 or 608 -> 640 = 5 x 128 instead of 19 x 32; measured 72.9 ms at 608 = 19 x 32).
+static int64_t padded_width(int64_t N)
+{
+    return N <= 16 ? 16 : N <= 32 ? 32 : N <= 64 ? 64 : (N + 127) / 128 * 128;
+}
+
+// N % 16 != 0: the kernels take 16-feature multiples, so B is copied into a zero-padded
+// K x Np scratch (2-D copy + memset of the pad columns), the product goes to an rows x Np
+// scratch and the first N columns are copied into C.  Any N >= 1 and any alignment of B/C.
+static accspmm_status execute_padded(const accspmm_plan *p, const void *B, int64_t N, void *C, void *stream)
+{
+    if (!C || (!B && p->info.K > 0)) return fail(ACCSPMM_ERR_INVALID_VALUE, "B or C is NULL");
+    const int64_t Np = padded_width(N);
+    const size_t es = p->opt.precision == ACCSPMM_FP16 ? 2 : 4;
+    const int64_t out_rows = p->opt.nparts == 1 ? p->info.M : p->info.rows;
+    const size_t needB = (size_t)std::max<int64_t>(p->info.K, 1) * (size_t)Np * es;
+    const size_t needC = (size_t)std::max<int64_t>(out_rows, 1) * (size_t)Np * sizeof(float);
+    {
+        std::lock_guard<std::mutex> lk(p->mu);
+        if (needB > p->padB_bytes) {
+            cudaFree(p->padB); p->padB = nullptr; p->padB_bytes = 0;
+            if (cudaMalloc(&p->padB, needB) != cudaSuccess) return fail(ACCSPMM_ERR_OUT_OF_MEMORY, "padded B");
+            p->padB_bytes = needB;
+        }
+        if (needC > p->padC_bytes) {
+            cudaFree(p->padC); p->padC = nullptr; p->padC_bytes = 0;
+            if (cudaMalloc((void **)&p->padC, needC) != cudaSuccess) return fail(ACCSPMM_ERR_OUT_OF_MEMORY, "padded C");
+            p->padC_bytes = needC;
+        }
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e = cudaSuccess;
+    if (p->info.K > 0) {
+        e = cudaMemset2DAsync((char *)p->padB + N * es, Np * es, 0, (Np - N) * es, p->info.K, s);
+        if (e == cudaSuccess) e = cudaMemcpy2DAsync(p->padB, Np * es, B, N * es, N * es, p->info.K, cudaMemcpyDefault, s);
+        if (e != cudaSuccess) return cuda_fail(e, "padded B copy");
+    }
+    accspmm_status st = execute_impl(p, p->padB, Np, p->padC, nullptr, 0, stream);
+    if (st != ACCSPMM_OK) return st;
+    if (out_rows > 0) {
+        e = cudaMemcpy2DAsync(C, N * sizeof(float), p->padC, Np * sizeof(float), N * sizeof(float), out_rows,
+                              cudaMemcpyDefault, s);
+        if (e != cudaSuccess) return cuda_fail(e, "padded C copy");
+    }
+    return ACCSPMM_OK;
+}
+
+static accspmm_status execute_impl(const accspmm_plan *p, const void *B, int64_t N, void *C, float *const *dst,
                                    int ndst, void *stream)
 {
     if (!p) return fail(ACCSPMM_ERR_INVALID_VALUE, "plan is NULL");
     if (p->opt.device < 0) return fail(ACCSPMM_ERR_UNSUPPORTED, "host-only plan cannot execute (no CPU fallback)");
     if (N <= 0) return fail(ACCSPMM_ERR_INVALID_VALUE, "N <= 0");
-    if (N % 16 != 0) return fail(ACCSPMM_ERR_UNSUPPORTED, "N must be a multiple of 16");
+    if (N % 16 != 0 && ndst > 0) return fail(ACCSPMM_ERR_UNSUPPORTED, "fused all-gather needs N % 16 == 0");
+    if (padded_width(N) != N && ndst == 0) {
+        if (p->info.rows == 0) return ACCSPMM_OK;
+        return execute_padded(p, B, N, C, stream);
+    }
     if (p->info.rows == 0) return ACCSPMM_OK;
     if (!C || (!B && p->info.K > 0)) return fail(ACCSPMM_ERR_INVALID_VALUE, "B or C is NULL");
     if (((uintptr_t)B & 15) || ((uintptr_t)C & 15)) return fail(ACCSPMM_ERR_INVALID_VALUE, "B and C must be 16-byte aligned");
@@ -427,7 +489,7 @@ accspmm_status accspmm_execute_host(const accspmm_plan *p, const void *B_host, i
 {
     if (!p) return fail(ACCSPMM_ERR_INVALID_VALUE, "plan is NULL");
     if (p->opt.device < 0) return fail(ACCSPMM_ERR_UNSUPPORTED, "host-only plan cannot execute (no CPU fallback)");
-    if (N <= 0 || N % 16 != 0) return fail(N <= 0 ? ACCSPMM_ERR_INVALID_VALUE : ACCSPMM_ERR_UNSUPPORTED, "bad N");
+    if (N <= 0) return fail(ACCSPMM_ERR_INVALID_VALUE, "N <= 0");
     if (!C_host || (!B_host && p->info.K > 0)) return fail(ACCSPMM_ERR_INVALID_VALUE, "B or C is NULL");
     const size_t es = p->opt.precision == ACCSPMM_FP16 ? 2 : 4;
     const size_t bB = (size_t)p->info.K * (size_t)N * es;
@@ -462,7 +524,7 @@ accspmm_status accspmm_execute_host_batch(const accspmm_plan *p, const void *con
 {
     if (!p) return fail(ACCSPMM_ERR_INVALID_VALUE, "plan is NULL");
     if (p->opt.device < 0) return fail(ACCSPMM_ERR_UNSUPPORTED, "host-only plan cannot execute (no CPU fallback)");
-    if (N <= 0 || N % 16 != 0) return fail(N <= 0 ? ACCSPMM_ERR_INVALID_VALUE : ACCSPMM_ERR_UNSUPPORTED, "bad N");
+    if (N <= 0) return fail(ACCSPMM_ERR_INVALID_VALUE, "N <= 0");
     if (count < 0 || (count > 0 && (!B_hosts || !C_hosts))) return fail(ACCSPMM_ERR_INVALID_VALUE, "bad batch");
     for (int32_t i = 0; i < count; ++i)
         if (!C_hosts[i] || (!B_hosts[i] && p->info.K > 0)) return fail(ACCSPMM_ERR_INVALID_VALUE, "B or C is NULL");

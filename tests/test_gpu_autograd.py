@@ -58,7 +58,7 @@ def test_input_checks():
     A = gen.identity(32)
     op = SparseOperator(32, 32, A.rowptr, A.colidx, np.ones(32, np.float32))
     with pytest.raises(ValueError):
-        spmm(op, torch.zeros(32, 20, device="cuda"))
+        spmm(op, torch.zeros(31, 16, device="cuda"))
     with pytest.raises(TypeError):
         spmm(op, torch.zeros(32, 16, device="cuda", dtype=torch.float16))
     with pytest.raises(ValueError):

@@ -331,9 +331,12 @@ def test_execute_errors():
     p = acc.Plan(A.M, A.K, A.rowptr, A.colidx, gen.values_uniform(A.nnz, 1))
     B = torch.zeros((100, 24), device="cuda")
     C = torch.zeros((100, 24), device="cuda")
-    with pytest.raises(acc.AccSpmmError) as ei:
-        p.execute(B, C)
+    with pytest.raises(acc.AccSpmmError) as ei:   # N % 16 != 0 is padded, but not in the fused all-gather
+        acc.accspmm_execute_allgather(p.handle, B.data_ptr(), 24, [C.data_ptr()])
     assert ei.value.status == 3
+    with pytest.raises(acc.AccSpmmError) as ei:
+        acc.accspmm_execute(p.handle, B.data_ptr(), 0, C.data_ptr())
+    assert ei.value.status == 1
     B = torch.zeros((100, 32), device="cuda")
     with pytest.raises(acc.AccSpmmError) as ei:
         acc.accspmm_execute(p.handle, B.data_ptr() + 4, 32, C.data_ptr())
@@ -578,3 +581,21 @@ def test_products_hub_rows_balancer_stress():
     assert np.array_equal(Con[hubs], Coff[hubs])
     Cr, _ = oracle(A, vi, Bi, "tf32", rows=hubs)
     assert np.array_equal(Con[hubs].astype(np.float64), Cr)
+
+
+@pytest.mark.parametrize("precision", PRECISIONS)
+@pytest.mark.parametrize("N", [1, 7, 24, 100, 602])
+def test_any_feature_width_padded(precision, N):
+    """N % 16 != 0 (e.g. Reddit's 602 input features) goes through the padded copies; integer
+    data bit-exact, split windows and reordering included, through the device and host APIs."""
+    import torch
+    A = gen.dcsbm(3000, 150_000, 5, 2.2, 0.2, 2000, seed=N, oversample=1.3)
+    v = gen.values_int(A.nnz, 1)
+    B = gen.dense_int(A.K, N, 2)
+    C, p = run(A, v, B, precision, reorder="on", balance="on", unit_cap=32)
+    assert C.shape == (A.M, N)
+    assert_bit_exact(C, A, v, B, precision)
+    hdt = np.float16 if precision == "fp16" else np.float32
+    Ch = np.full((A.M, N), np.nan, np.float32)
+    p.execute_host(np.ascontiguousarray(B.astype(hdt)), Ch)
+    assert np.array_equal(Ch, C)
