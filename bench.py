@@ -358,6 +358,9 @@ def main():
     warm_ms = w0.elapsed_time(w1) / args.steps
 
     bm = acc.bytes_model(info, args.N)
+    # the HBM lower bound of the gather -- every distinct column's B row once
+    es_b = 2 if args.precision == "fp16" else 4
+    bm["B_compulsory"] = int(es_b * args.N * np.count_nonzero(np.bincount(A.colidx, minlength=A.K)))
     avg_s = float(np.mean(kernel_ms)) / 1e3 if len(kernel_ms) else t_local / args.steps
     peak, peak_kind = load_peaks()
     achieved = bm["total"] / avg_s / 1e9

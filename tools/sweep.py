@@ -41,6 +41,7 @@ def main():
         prec = kv.get("precision", "tf32")
         os.environ["ACCSPMM_KCFG"] = kv.get("kcfg", "-1")
         os.environ["ACCSPMM_FW"] = kv.get("fw", "0")
+        os.environ["ACCSPMM_SLICE_MAJOR"] = kv.get("sm", "1")
         if "gcap" in kv:
             os.environ["ACCSPMM_GROUP_CAP"] = kv["gcap"]
         else:
