@@ -1076,7 +1076,8 @@ accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, 
         const G4Maps *map = nullptr;
         // per-slice maps only for the kernels instantiated with them (variants 20/46: one map)
         const bool multi = map_count(kp) > 1 && kcfg != 20 && kcfg != 46;
-        accspmm_status st = tensor_map(d, kp, FW, multi, &map);
+        static const G4Maps no_maps = {};  // no TC blocks (e.g. K = 0): no TMA is ever issued
+        accspmm_status st = d.NB > 0 ? tensor_map(d, kp, FW, multi, &map) : (map = &no_maps, ACCSPMM_OK);
         if (st != ACCSPMM_OK) return st;
         constexpr int NM = kMaxSliceMaps;
         constexpr bool LD = F16;  // FP16: ldmatrix.trans fragments (measured -10.5%)

@@ -599,3 +599,19 @@ def test_any_feature_width_padded(precision, N):
     Ch = np.full((A.M, N), np.nan, np.float32)
     p.execute_host(np.ascontiguousarray(B.astype(hdt)), Ch)
     assert np.array_equal(Ch, C)
+
+
+@pytest.mark.parametrize("precision", PRECISIONS)
+def test_zero_width_inner_dimension(precision):
+    """K = 0 (B has no rows): no TC block exists, C is all zeros, including the fused all-gather."""
+    import torch
+    A = gen.Csr(21, 0, np.zeros(22, np.int64), np.zeros(0, np.int32))
+    p = acc.Plan(A.M, A.K, A.rowptr, A.colidx, np.zeros(0, np.float32), precision=precision)
+    dt = torch.float16 if precision == "fp16" else torch.float32
+    B = torch.zeros((0, 32), dtype=dt, device="cuda")
+    C = torch.full((21, 32), float("nan"), device="cuda")
+    p.execute(B, C)
+    D = torch.full((21, 32), float("nan"), device="cuda")
+    p.execute_allgather(B, [D])
+    torch.cuda.synchronize()
+    assert torch.all(C == 0) and torch.all(D == 0)
