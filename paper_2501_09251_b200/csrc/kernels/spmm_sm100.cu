@@ -7,28 +7,27 @@
 // sparse tile the right operand of m16n8k8.  TF32 inputs with
 // FP32 accumulation; an FP16 variant uses m16n8k8.f16 (BASELINE north_star).
 //
-// How it does it is designed for B200, not translated from Alg. 2:
-//   * one warp owns one work unit of the sparsity-aware schedule and
-//     one FW-wide feature slice: a run of whole RowWindows or an even segment of a
-//     long window;
-//   * the unit's compressed A stream (TCLocalBit, TCOffset, SparseAToB) is streamed
-//     in 32-block chunks by cp.async into a double-buffered per-warp shared-memory
-//     chunk (coalesced 8/4/16-byte copies, L2 evict_first);
-//   * each lane loads its part of the block's gathered B rows straight from
-//     L2/HBM into the MMA fragment registers (the paper's "B tile to registers
-//     directly") with 128-bit non-caching loads and an L2 evict_last
-//     policy; the features of the 16x8 operand are permuted so that 8 lanes read
-//     128 contiguous bytes of a B row and write 128 contiguous bytes of C;
-//     an A/B register double buffer keeps two blocks in flight per warp (the
-//     paper's least-bubble prefetch);
-//   * padding lanes of a block read a zero row instead of B[0,:];
-//   * B was rounded to TF32 (RNA) once per execute by a separate
-//     elementwise pass -- each B row is gathered by hundreds of windows, so the
-//     rounding is hoisted out of the gather instead of being repeated per block;
-//   * accumulators (8 window rows x FW features) live in registers; the epilogue
-//     stores C rows with st.global.cs through the reordering permutation (Q12);
-//   * split windows: partial tile -> workspace, the last-arriving segment (atomic
-//     counter) sums all partials in segment order (deterministic, Q18).
+// How it does it is designed for B200, not translated from Alg. 2.  The
+// default kernel is spmm_bittcf_g4_kernel:
+//   * one warp = one CTA = one work unit of the sparsity-aware schedule (a run of
+//     whole RowWindows or an even segment of a long window) x one FW-wide feature slice;
+//     the grid is slice-major when N spans several slices;
+//   * the unit's compressed A stream (TCLocalBit, TCOffset, SparseAToB) is staged 16 blocks
+//     at a time by cp.async into a double-buffered shared-memory chunk;
+//   * lane 0 gathers each block's 8 B rows with two TMA tile::gather4 requests into a
+//     2-stage mbarrier ring (padding lanes ask for row -1: zero fill); the box is
+//     32 bytes wider than the slice so the fragment loads are bank-conflict free;
+//   * every lane decodes its two tile entries from the bitmap and loads their
+//     values one block ahead; TF32 fragments come from LDS.128 (m16n8k4, or m16n8k8 at
+//     FW <= 64), FP16 fragments from ldmatrix.trans; FP32 accumulators in registers;
+//   * rho(B) (TF32 RNA) is applied once per execute by a pre-pass when B rows
+//     are reused >= 32 times, else in registers after the LDS;
+//   * the epilogue stores C rows with st.global.cs through the reordering permutation (Q12),
+//     or, for the fused all-gather, into every rank's C; split windows go through a
+//     workspace and the last-arriving segment sums the partials in segment order
+//     (deterministic, Q18).
+// spmm_bittcf_kernel (register-direct gather: each lane loads its fragment rows with
+// 128-bit non-caching loads) is kept as a measured alternative (ACCSPMM_KCFG=10..12).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_fp16.h>
