@@ -830,9 +830,43 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     if (nblk > 0) value_load(0u, 0);
     if (VD == 2 && nblk > 1) value_load(1u, 1);
     if (nblk > 0) issue_tma(0, 0);
+    if constexpr (STAGES > 2) {
+        // Deeper TMA ring (STAGES - 1 blocks of lookahead; pays where a stage is small, e.g.
+        // FP16): block step j issues the TMA of jt = j + L and the values of jn = j + 1.
+        // Chunk c + 1 is staged when jn enters chunk c (chunk c - 1's buffer is then free)
+        // and waited for when jt enters it.
+        static_assert(VD == 1 && STAGES <= 4, "multi-stage ring: one value slot ahead, <= 4 stages");
+        constexpr int L = STAGES - 1;
+        constexpr int UN = STAGES == 3 ? 6 : 4;  // unroll: a multiple of VR and of STAGES
+#pragma unroll
+        for (int d = 1; d < L; ++d)
+            if ((uint32_t)d < nblk) issue_tma((uint32_t)d, d);
+        auto stepS = [&](uint32_t j, int u, bool checked) {
+            const uint32_t jn = j + 1, jt = j + L;
+            if ((jt & (CH - 1u)) == 0) {
+                cp_async_wait_all();
+                __syncwarp();
+            }
+            if ((jn & (CH - 1u)) == 0) issue_chunk(jn + CH);
+            if (!checked || jt < nblk) issue_tma(jt, (u + L) % STAGES);
+            if (!checked || jn < nblk) value_load(jn, (u + 1) & (VR - 1));
+            consume(j, u % STAGES, u & (VR - 1));
+            after_block(b0 + j + 1);
+        };
+        const uint32_t nmainS = nblk >= (uint32_t)L ? ((nblk - L) / UN) * UN : 0u;
+        uint32_t j = 0;
+        for (; j < nmainS; j += UN) {
+#pragma unroll
+            for (int u = 0; u < UN; ++u) stepS(j + (uint32_t)u, u, false);
+        }
+        for (; j < nblk; j += UN) {
+#pragma unroll
+            for (int u = 0; u < UN; ++u)
+                if (j + (uint32_t)u < nblk) stepS(j + (uint32_t)u, u, true);
+        }
+    } else {
     // Block step j: TMA for j+1, values for j+1 (at a chunk boundary first wait for that
     // chunk and prefetch the one after), then the decode-free MMA of block j.
-    static_assert(STAGES == 2, "the block step below is written for a 2-stage TMA ring");
     auto step = [&](uint32_t j, int u, bool checked) {
         const uint32_t jn = j + 1;
         if constexpr (VD == 1) {
@@ -869,6 +903,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
 #pragma unroll
         for (int u = 0; u < VR; ++u)
             if (j + (uint32_t)u < nblk) step(j + (uint32_t)u, u, true);
+    }
     }
     cp_async_wait_all();
 
@@ -1094,6 +1129,12 @@ accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, 
         case 48:  // TF32 m16n8k8 vs two m16n8k4: the opposite of the default choice
             if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, !K8>(kp, map, n_units, stream);
             return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, !K8>(kp, map, n_units, stream);
+        case 50:  // 3-stage TMA ring
+            if (multi) return launch_g4<FW, F16, 1, 3, false, MW, NM, LD, K8>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 3, false, MW, 1, LD, K8>(kp, map, n_units, stream);
+        case 51:  // 4-stage TMA ring
+            if (multi) return launch_g4<FW, F16, 1, 4, false, MW, NM, LD, K8>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 4, false, MW, 1, LD, K8>(kp, map, n_units, stream);
         case 49:  // values loaded two blocks ahead (4-slot ring)
             if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 2>(kp, map, n_units, stream);
             return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 2>(kp, map, n_units, stream);

@@ -14,8 +14,11 @@ def main(path):
             if not m:
                 continue
             ops = [o.strip() for o in m.group(3).split(",")]
-            urs = [re.findall(r"\bUR(\d+)\b", o) for o in ops]
             op = m.group(2)
+            # "OP UPn, URm, ..." (e.g. ULOP3 with a predicate output): URm is written too
+            if len(ops) > 1 and re.fullmatch(r"U?P(\d+|T)", ops[0]) and re.fullmatch(r"UR\d+", ops[1]):
+                ops = [ops[1]] + ops[2:]
+            urs = [re.findall(r"\bUR(\d+)\b", o) for o in ops]
             if ops and urs[0] and not op.startswith(("ST", "LDGSTS", "RED", "ATOM", "UTMA", "SYNCS", "BAR", "UBLKCP", "UTMALDG", "UTMAPF")):
                 for r in urs[0]:
                     written.add(int(r))
