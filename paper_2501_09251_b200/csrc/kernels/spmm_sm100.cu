@@ -1048,8 +1048,9 @@ accspmm_status tensor_map(const DevicePlan &d, const KParams &kp, int FW, bool m
     const void *B = kp.B;
     const int64_t N = kp.N;
     const int nm = multi ? map_count(kp) : 1;
+    const int pv = env_int("ACCSPMM_L2PROMO", 3);
     const uint64_t key[4] = {(uint64_t)(uintptr_t)B, (uint64_t)N, (uint64_t)FW,
-                             (uint64_t)(d.precision + 1) | ((uint64_t)nm << 8)};
+                             (uint64_t)(d.precision + 1) | ((uint64_t)nm << 8) | ((uint64_t)pv << 16)};
     G4Maps *maps = reinterpret_cast<G4Maps *>(d.tmap);
     static_assert(sizeof(G4Maps) <= sizeof(d.tmap), "tensor-map cache too small");
     if (!(key[0] == d.tmap_key[0] && key[1] == d.tmap_key[1] && key[2] == d.tmap_key[2] && key[3] == d.tmap_key[3])) {
@@ -1064,6 +1065,12 @@ accspmm_status tensor_map(const DevicePlan &d, const KParams &kp, int FW, bool m
         }
         const bool f16 = d.precision == ACCSPMM_FP16;
         const cuuint64_t es = f16 ? 2 : 4;
+        // L2 sector promotion of the gathered rows (ACCSPMM_L2PROMO 0..3 = none/64/128/256 B
+        // for A/B measurements; default 256 B)
+        const CUtensorMapL2promotion promo = pv == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                                            : pv == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                                            : pv == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                                      : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
         for (int m = 0; m < nm; ++m) {
             cuuint64_t dims[2] = {(cuuint64_t)(nm > 1 ? FW : N), (cuuint64_t)d.K};
             cuuint64_t strides[1] = {(cuuint64_t)N * es};
@@ -1072,7 +1079,7 @@ accspmm_status tensor_map(const DevicePlan &d, const KParams &kp, int FW, bool m
             void *base = const_cast<char *>(reinterpret_cast<const char *>(B)) + (size_t)m * FW * es;
             CUresult r = encode(&maps->m[m], f16 ? CU_TENSOR_MAP_DATA_TYPE_UINT16 : CU_TENSOR_MAP_DATA_TYPE_UINT32, 2,
                                 base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                                promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
             if (r != CUDA_SUCCESS)
                 return fail(ACCSPMM_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
         }
