@@ -1,6 +1,7 @@
 // C ABI of libaccspmm (include/accspmm.h): plan lifecycle, device upload, execute.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cstdlib>
 #include <cstring>
@@ -458,12 +459,42 @@ static accspmm_status execute_impl(const accspmm_plan *p, const void *B, int64_t
         Bk = p->Br;
     }
     const bool timed = p->timing && p->ev_n + 2 <= p->ev.size();
+    // ACCSPMM_L2_PERSIST=<MiB> (measurement): mark B as an L2-persisting access-policy window
+    // for this launch only (the stream attribute is restored right after the launch)
+    const char *pe = std::getenv("ACCSPMM_L2_PERSIST");
+    const int64_t persist_mib = pe ? std::atoll(pe) : 0;
+    cudaStreamAttrValue prev{};
+    bool window = false;
+    if (persist_mib > 0 && p->info.K > 0) {
+        static int64_t limit_set = -1;
+        int dev = 0, maxp = 0, maxw = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
+        cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+        const size_t want = std::min<size_t>((size_t)persist_mib << 20, (size_t)maxp);
+        if (limit_set != (int64_t)want) {
+            cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+            limit_set = (int64_t)want;
+        }
+        const size_t es = tf32 ? 4 : 2;
+        const size_t bytes = std::min<size_t>((size_t)p->info.K * (size_t)N * es, (size_t)maxw);
+        cudaStreamGetAttribute((cudaStream_t)stream, cudaStreamAttributeAccessPolicyWindow, &prev);
+        cudaStreamAttrValue v{};
+        v.accessPolicyWindow.base_ptr = const_cast<void *>(Bk);
+        v.accessPolicyWindow.num_bytes = bytes;
+        v.accessPolicyWindow.hitRatio = std::min(1.0f, (float)want / (float)std::max<size_t>(bytes, 1));
+        v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        window = cudaStreamSetAttribute((cudaStream_t)stream, cudaStreamAttributeAccessPolicyWindow, &v) == cudaSuccess;
+        cudaGetLastError();
+    }
     if (timed) cudaEventRecord(p->ev[p->ev_n], (cudaStream_t)stream);
     st = launch_spmm(p->dev, Bk, p->zrow, N, (float *)C, p->ws, p->counters, stream, in_kernel_round, dst, ndst);
     if (timed) {
         cudaEventRecord(p->ev[p->ev_n + 1], (cudaStream_t)stream);
         p->ev_n += 2;
     }
+    if (window) cudaStreamSetAttribute((cudaStream_t)stream, cudaStreamAttributeAccessPolicyWindow, &prev);
     return st;
 }
 

@@ -43,6 +43,7 @@ def main():
         os.environ["ACCSPMM_FW"] = kv.get("fw", "0")
         os.environ["ACCSPMM_SLICE_MAJOR"] = kv.get("sm", "1")
         os.environ["ACCSPMM_L2PROMO"] = kv.get("promo", "3")
+        os.environ["ACCSPMM_L2_PERSIST"] = kv.get("persist", "0")
         if "gcap" in kv:
             os.environ["ACCSPMM_GROUP_CAP"] = kv["gcap"]
         else:
