@@ -371,7 +371,8 @@ def _sample_rows(M, n, seed):
 @pytest.mark.parametrize("name,N,precision", [
     ("reddit", 128, "tf32"), ("reddit", 128, "fp16"), ("reddit", 32, "tf32"), ("reddit", 64, "tf32"),
     ("stencil", 128, "tf32"), ("products", 128, "tf32"), ("papers100m_small", 64, "tf32"),
-    ("reddit", 256, "tf32"), ("reddit", 512, "fp16"),
+    ("reddit", 256, "tf32"), ("reddit", 512, "fp16"), ("reddit", 64, "fp16"), ("reddit", 32, "fp16"),
+    ("banded", 128, "tf32"),
     ("roadnet", 128, "tf32"), ("yeasth", 512, "tf32"), ("dd", 256, "fp16"), ("webberkstan", 128, "tf32"),
 ])
 def test_full_size_config_sampled(name, N, precision):
