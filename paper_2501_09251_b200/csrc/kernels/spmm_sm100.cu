@@ -98,6 +98,21 @@ __device__ __forceinline__ void ldg_nc(uint32_t &v, const void *p, uint64_t pol)
     asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;\n" : "=r"(v) : "l"(p), "l"(pol));
 }
 
+// value loads with an L2 256-byte prefetch: a block's values are contiguous and the next
+// blocks' follow, so one DRAM fetch serves several block steps (measurement variant)
+__device__ __forceinline__ uint32_t ldg_pf256_u32(const void *p)
+{
+    uint32_t v;
+    asm volatile("ld.global.nc.L2::256B.u32 %0, [%1];\n" : "=r"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ uint32_t ldg_pf256_u16(const void *p)
+{
+    unsigned short v;
+    asm volatile("ld.global.nc.L2::256B.u16 %0, [%1];\n" : "=h"(v) : "l"(p));
+    return (uint32_t)v;
+}
+
 __device__ __forceinline__ void mma_tf32(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
                                          uint32_t b0, uint32_t b1)
 {
@@ -559,7 +574,7 @@ using G4Maps = G4MapsT<kMaxSliceMaps>;
 inline int map_count(const KParams &kp) { return kp.nslices > 1 && kp.nslices <= kMaxSliceMaps ? kp.nslices : 1; }
 
 template <int FW, bool F16, int WARPS, int STAGES, bool RND, int MINB = 1, int NM = 1, bool LDSM_ = false,
-          bool K8 = false, int VD = 1>
+          bool K8 = false, int VD = 1, bool PF256 = false>
 __global__ void __launch_bounds__(WARPS * 32, MINB)
     spmm_bittcf_g4_kernel(const KParams p, const __grid_constant__ G4MapsT<NM> maps)
 {
@@ -641,7 +656,17 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
         bool p0, p1;
         const uint32_t i0 = t0 + tile_rank(mask, sh0, p0);
         const uint32_t i1 = t0 + tile_rank(mask, sh1, p1);
-        if constexpr (!F16) {
+        if constexpr (PF256) {
+            if constexpr (!F16) {
+                const uint32_t *vp = reinterpret_cast<const uint32_t *>(p.vals);
+                vb0[slot] = p0 ? ldg_pf256_u32(vp + i0) : 0u;
+                vb1[slot] = p1 ? ldg_pf256_u32(vp + i1) : 0u;
+            } else {
+                const unsigned short *vp = reinterpret_cast<const unsigned short *>(p.vals);
+                vb0[slot] = p0 ? ldg_pf256_u16(vp + i0) : 0u;
+                vb1[slot] = p1 ? ldg_pf256_u16(vp + i1) : 0u;
+            }
+        } else if constexpr (!F16) {
             const float *vp = reinterpret_cast<const float *>(p.vals);
             vb0[slot] = p0 ? __float_as_uint(__ldg(vp + i0)) : 0u;
             vb1[slot] = p1 ? __float_as_uint(__ldg(vp + i1)) : 0u;
@@ -1015,12 +1040,12 @@ int env_int(const char *name, int dflt)
 // NM = 1: one tensor map (the full-width map when several slices exist); NM = kMaxSliceMaps:
 // one map per slice (tensor_map decides; only the default configurations instantiate it)
 template <int FW, bool F16, int WARPS, int STAGES, bool RND = false, int MINB = 1, int NM = 1, bool LDSM = false,
-          bool K8 = false, int VD = 1>
+          bool K8 = false, int VD = 1, bool PF256 = false>
 accspmm_status launch_g4(const KParams &kp, const G4Maps *map, int64_t n_units, cudaStream_t stream)
 {
     using SM = G4WarpSmem<FW, F16, STAGES>;
     const size_t smem = sizeof(SM) * WARPS;
-    auto kern = spmm_bittcf_g4_kernel<FW, F16, WARPS, STAGES, RND, MINB, NM, LDSM, K8, VD>;
+    auto kern = spmm_bittcf_g4_kernel<FW, F16, WARPS, STAGES, RND, MINB, NM, LDSM, K8, VD, PF256>;
     static int configured_device = -1;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -1126,6 +1151,10 @@ accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, 
         if constexpr (!F16) {
             if (rnd) {  // B not pre-rounded: rho(B) applied in registers
                 if (kcfg == 20) return launch_g4<FW, F16, 2, 2, true, 1>(kp, map, n_units, stream);
+                if (kcfg == 52) {
+                    if (multi) return launch_g4<FW, F16, 1, 2, true, MW, NM, false, K8, 1, true>(kp, map, n_units, stream);
+                    return launch_g4<FW, F16, 1, 2, true, MW, 1, false, K8, 1, true>(kp, map, n_units, stream);
+                }
                 if (multi) return launch_g4<FW, F16, 1, 2, true, MW, NM, false, K8>(kp, map, n_units, stream);
                 return launch_g4<FW, F16, 1, 2, true, MW, 1, false, K8>(kp, map, n_units, stream);
             }
@@ -1136,6 +1165,9 @@ accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, 
         case 48:  // TF32 m16n8k8 vs two m16n8k4: the opposite of the default choice
             if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, !K8>(kp, map, n_units, stream);
             return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, !K8>(kp, map, n_units, stream);
+        case 52:  // value loads with an L2 256-byte prefetch
+            if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, true>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, true>(kp, map, n_units, stream);
         case 50:  // 3-stage TMA ring
             if (multi) return launch_g4<FW, F16, 1, 3, false, MW, NM, LD, K8>(kp, map, n_units, stream);
             return launch_g4<FW, F16, 1, 3, false, MW, 1, LD, K8>(kp, map, n_units, stream);
