@@ -486,12 +486,13 @@ def test_permute_cols_partitions_and_device_build():
     assert np.array_equal(out.cpu().numpy(), Cfull)
 
 
-@pytest.mark.parametrize("kcfg", ["20", "46", "47", "10", "11", "12"])
+@pytest.mark.parametrize("kcfg", ["20", "46", "47", "48", "49", "50", "51", "52", "10", "11", "12"])
 @pytest.mark.parametrize("precision", PRECISIONS)
 def test_measurement_variants_stay_exact(kcfg, precision, monkeypatch):
-    """The A/B kernel variants selectable by ACCSPMM_KCFG (2 warps per CTA,
-    FP16 PRMT fragments, register-direct gather) compute the same product: integer data
-    bit-exact (split windows included), floats within tolerance, N = 64 and 256."""
+    """Every A/B kernel variant selectable by ACCSPMM_KCFG (2 warps per CTA,
+    FP16 PRMT fragments, k4/k8 swap, values two ahead, 3/4-stage rings, L2::256B value loads,
+    register-direct gather) computes the same product: integer data bit-exact (split windows
+    included), floats within tolerance, N = 64 and 256 (per-slice maps)."""
     monkeypatch.setenv("ACCSPMM_KCFG", kcfg)
     A = gen.dcsbm(3000, 150_000, 5, 2.2, 0.2, 2000, seed=3, oversample=1.3)
     v = gen.values_int(A.nnz, 1)
