@@ -78,7 +78,7 @@ typedef enum {
 
 typedef struct {
     int32_t precision;  /* accspmm_precision; default ACCSPMM_TF32                                   */
-    int32_t reorder;    /* accspmm_reorder_mode; default ACCSPMM_REORDER_OFF                         */
+    int32_t reorder;    /* accspmm_reorder_mode; default ACCSPMM_REORDER_AUTO         */
     int32_t balance;    /* accspmm_balance_mode; default ACCSPMM_BALANCE_AUTO                        */
     int32_t unit_cap;   /* max TC blocks per work unit; 0 = automatic (>= 32, the P:446 threshold)   */
     int32_t part;       /* this rank's part in [0, nparts)                                          */

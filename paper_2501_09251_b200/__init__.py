@@ -17,7 +17,10 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libaccspmm.so")
+# ACCSPMM_LIB=variants selects the measurement build (same ABI, plus the rejected kernel variants
+# and the ACCSPMM_* A/B knobs; tools/sweep.py); the product library is libaccspmm.so
+LIB_PATH = os.path.join(_HERE, "libaccspmm_variants.so" if os.environ.get("ACCSPMM_LIB") == "variants"
+                        else "libaccspmm.so")
 
 TF32, FP16 = 0, 1
 REORDER = {"off": 0, "on": 1, "auto": 2}
@@ -303,11 +306,27 @@ def _stream_ptr(stream):
     return getattr(stream, "cuda_stream", stream)
 
 
+def _check_2d(name, X, rows, dtypes, N=None):
+    """Shape / dtype / layout checks the C ABI cannot do (it only sees pointers)."""
+    if X.ndim != 2:
+        raise ValueError(f"{name} must be 2-D, got shape {tuple(X.shape)}")
+    if X.shape[0] != rows:
+        raise ValueError(f"{name} must have {rows} rows, got {X.shape[0]}")
+    if N is not None and X.shape[1] != N:
+        raise ValueError(f"{name} must have {N} columns, got {X.shape[1]}")
+    dt = str(X.dtype).replace("torch.", "")
+    if dt not in dtypes:
+        raise TypeError(f"{name} dtype must be {dtypes[0]}, got {dt}")
+    contiguous = X.is_contiguous() if hasattr(X, "is_contiguous") else X.flags["C_CONTIGUOUS"]
+    if not contiguous:
+        raise ValueError(f"{name} must be contiguous (row-major, leading dimension = number of columns)")
+
+
 class Plan:
     """Owns one accspmm_plan.  ``execute`` takes torch CUDA tensors (B: K x N, float32 for
     TF32 / float16 for FP16) and returns / fills C (float32)."""
 
-    def __init__(self, M, K, rowptr, colidx, vals, precision="tf32", reorder="off", balance="auto",
+    def __init__(self, M, K, rowptr, colidx, vals, precision="tf32", reorder="auto", balance="auto",
                  unit_cap=0, part=0, nparts=1, device=None, build="host", permute_cols=False):
         opt = accspmm_options_default()
         opt.build = BUILD[build]
@@ -344,30 +363,65 @@ class Plan:
     def out_rows(self) -> int:
         return self.info["M"] if self.info["nparts"] == 1 else self.info["rows"]
 
+    @property
+    def _b_dtypes(self):
+        return ("float16",) if self.precision == "fp16" else ("float32",)
+
+    def _check_device(self, name, X):
+        if not getattr(X, "is_cuda", False):
+            raise ValueError(f"{name} must be a CUDA tensor (no CPU fallback; use execute_host for host buffers)")
+        if X.device.index != self.info["device"]:
+            raise ValueError(f"{name} is on cuda:{X.device.index}, the plan on cuda:{self.info['device']}")
+
+    def _check_B(self, B):
+        _check_2d("B", B, self.info["K"], self._b_dtypes)
+        self._check_device("B", B)
+
     def execute(self, B, C=None, stream=None):
         import torch
+        self._check_B(B)
         N = B.shape[1]
         if C is None:
             C = torch.empty((self.out_rows, N), dtype=torch.float32, device=B.device)
+        else:
+            _check_2d("C", C, self.out_rows, ("float32",), N)
+            self._check_device("C", C)
         accspmm_execute(self.handle, B.data_ptr(), N, C.data_ptr(), _stream_ptr(stream))
         return C
 
     def execute_allgather(self, B, C_all, stream=None):
         """Fused all-gather: this plan's rows go to every matrix of C_all (full M x N float32
         CUDA tensors, local or peer-mapped) in original row order."""
+        self._check_B(B)
+        for k, c in enumerate(C_all):
+            _check_2d(f"C_all[{k}]", c, self.info["M"], ("float32",), B.shape[1])
         accspmm_execute_allgather(self.handle, B.data_ptr(), B.shape[1], [c.data_ptr() for c in C_all],
                                   _stream_ptr(stream))
         return C_all
 
+    def _check_host(self, B_host, C_host, N=None):
+        _check_2d("B_host", B_host, self.info["K"], self._b_dtypes, N)
+        _check_2d("C_host", C_host, self.info["rows"], ("float32",), B_host.shape[1])
+        for name, X in (("B_host", B_host), ("C_host", C_host)):
+            if getattr(X, "is_cuda", False):
+                raise ValueError(f"{name} must be host memory (numpy or CPU tensor)")
+
     def execute_host(self, B_host, C_host, stream=None):
         """End to end with host buffers (numpy or pinned torch CPU tensors)."""
+        self._check_host(B_host, C_host)
         N = B_host.shape[1]
         accspmm_execute_host(self.handle, _ptr(B_host), N, _ptr(C_host), _stream_ptr(stream))
         return C_host
 
     def execute_host_batch(self, B_hosts, C_hosts, stream=None):
         """Pipelined end to end over a batch of host B / C buffers (pinned for overlap)."""
+        if len(B_hosts) != len(C_hosts):
+            raise ValueError("B and C batches differ in length")
+        if not B_hosts:
+            return C_hosts
         N = B_hosts[0].shape[1]
+        for b, c in zip(B_hosts, C_hosts):
+            self._check_host(b, c, N)
         accspmm_execute_host_batch(self.handle, [_ptr(b) for b in B_hosts], [_ptr(c) for c in C_hosts], N,
                                    _stream_ptr(stream))
         return C_hosts

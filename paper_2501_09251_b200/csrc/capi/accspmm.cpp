@@ -27,8 +27,10 @@ struct accspmm_plan {
     mutable size_t dB_bytes = 0;
     mutable float *dC = nullptr;
     mutable size_t dC_bytes = 0;
-    mutable void *dB2 = nullptr;
+    mutable void *dB2 = nullptr;      // second slots of the pipelined batch path (own sizes:
+    mutable size_t dB2_bytes = 0;     // execute_host grows only the first slots)
     mutable float *dC2 = nullptr;
+    mutable size_t dC2_bytes = 0;
     // copy-engine streams and slot events of the pipelined batch path
     mutable cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
     mutable cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_k[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
@@ -64,6 +66,26 @@ static accspmm_status cuda_fail(cudaError_t e, const char *what)
     return fail(ACCSPMM_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+// Makes `dev` current for the scope of one entry point and restores the caller's device
+// (torch keeps its own notion of the current device; a plan may live on another one).
+struct DeviceGuard {
+    int prev = -1;
+    bool ok = true;
+    explicit DeviceGuard(int dev)
+    {
+        if (dev < 0) return;
+        if (cudaGetDevice(&prev) != cudaSuccess) { prev = -1; cudaGetLastError(); }
+        if (prev != dev) ok = cudaSetDevice(dev) == cudaSuccess;
+        if (!ok) cudaGetLastError();
+    }
+    ~DeviceGuard()
+    {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+    DeviceGuard(const DeviceGuard &) = delete;
+    DeviceGuard &operator=(const DeviceGuard &) = delete;
+};
+
 static double ms_since(std::chrono::steady_clock::time_point t0)
 {
     return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
@@ -95,6 +117,7 @@ static void free_device(accspmm_plan *p)
     cudaFree(p->ws); cudaFree(p->counters); cudaFree(p->dB); cudaFree(p->dC); cudaFree(p->Br); cudaFree(p->zrow);
     cudaFree(p->dB2); cudaFree(p->dC2);
     p->dB2 = nullptr; p->dC2 = nullptr;
+    p->dB2_bytes = p->dC2_bytes = 0;
     cudaFree(p->padB); cudaFree(p->padC);
     p->padB = nullptr; p->padC = nullptr;
     if (p->s_h2d) cudaStreamDestroy(p->s_h2d);
@@ -110,6 +133,7 @@ static void free_device(accspmm_plan *p)
     p->ev.clear();
     d = DevicePlan();
     p->ws = nullptr; p->counters = nullptr; p->dB = nullptr; p->dC = nullptr; p->Br = nullptr; p->zrow = nullptr;
+    p->ws_bytes = p->counters_n = p->dB_bytes = p->dC_bytes = p->Br_bytes = p->padB_bytes = p->padC_bytes = 0;
 }
 
 }  // namespace accspmm
@@ -135,7 +159,7 @@ accspmm_status accspmm_options_default(accspmm_options *opt)
     if (!opt) return fail(ACCSPMM_ERR_INVALID_VALUE, "opt is NULL");
     std::memset(opt, 0, sizeof(*opt));
     opt->precision = ACCSPMM_TF32;
-    opt->reorder = ACCSPMM_REORDER_OFF;
+    opt->reorder = ACCSPMM_REORDER_AUTO;  // "defaults: TF32, reorder auto, balance auto"
     opt->balance = ACCSPMM_BALANCE_AUTO;
     opt->unit_cap = 0;
     opt->part = 0;
@@ -174,6 +198,9 @@ accspmm_status accspmm_plan_create_ex(int64_t M, int64_t K, const int64_t *rowpt
     if (M >= (int64_t)UINT32_MAX || K >= (int64_t)INT32_MAX)
         return fail(ACCSPMM_ERR_UNSUPPORTED, "M or K too large for 32-bit indices");
 
+    // every device call of plan creation runs on opt.device; the caller's device is restored
+    DeviceGuard guard(opt.device);
+    if (!guard.ok) return fail(ACCSPMM_ERR_CUDA, "cudaSetDevice(opt.device) failed");
     auto t0 = std::chrono::steady_clock::now();
     Csr a{M, K, rowptr, colidx};
     accspmm_status st = validate_csr(a);
@@ -231,8 +258,6 @@ accspmm_status accspmm_plan_create_ex(int64_t M, int64_t K, const int64_t *rowpt
     DeviceFormat DF;
     double ms_csr_upload = 0.0;
     if (opt.build == ACCSPMM_BUILD_DEVICE) {
-        cudaError_t e = cudaSetDevice(opt.device);
-        if (e != cudaSuccess) { delete p; return cuda_fail(e, "cudaSetDevice"); }
         st = build_format_device(a, vals, perm, r0, std::max(r0, r1), opt.precision, DF, cm);
         if (st != ACCSPMM_OK) { free_device_format(DF); delete p; return st; }
         F.W = DF.W; F.NB = DF.NB; F.nnz = DF.nnz; F.rows = DF.rows; F.sum_U = DF.sum_U;
@@ -278,8 +303,6 @@ accspmm_status accspmm_plan_create_ex(int64_t M, int64_t K, const int64_t *rowpt
     // ---- device upload ----
     t0 = std::chrono::steady_clock::now();
     if (opt.device >= 0) {
-        cudaError_t e = cudaSetDevice(opt.device);
-        if (e != cudaSuccess) { delete p; return cuda_fail(e, "cudaSetDevice"); }
         DevicePlan &d = p->dev;
         d.W = F.W; d.NB = F.NB; d.nnz = F.nnz; d.rows = F.rows; d.n_units = I.n_units;
         d.n_split = S.n_split; d.n_segments = S.n_segments; d.precision = opt.precision; d.K = K;
@@ -435,9 +458,8 @@ static accspmm_status execute_impl(const accspmm_plan *p, const void *B, int64_t
     // (reuse = sum_w |U_w| / K >= 32), else in the kernel's registers.  With permuted
     // columns the pass is a row gather B' = B[perm] (rounding fused for the TF32 pre-pass).
     const bool tf32 = p->opt.precision == ACCSPMM_TF32;
-    // ACCSPMM_ROUND_B = 1 (pass) / 2 (kernel) overrides the reuse rule for A/B measurements
-    const char *rb = std::getenv("ACCSPMM_ROUND_B");
-    const int rmode = rb ? std::atoi(rb) : 0;
+    // Knobs::round_b = 1 (pass) / 2 (kernel) overrides the reuse rule (variants build only)
+    const int rmode = knobs().round_b;
     const bool in_kernel_round = tf32 && p->info.K > 0 &&
                                  (rmode == 2 || (rmode != 1 && p->info.sum_U < kRoundReuse * p->info.K));
     const bool permute = p->dev.col_perm != nullptr && p->info.K > 0;
@@ -459,23 +481,22 @@ static accspmm_status execute_impl(const accspmm_plan *p, const void *B, int64_t
         Bk = p->Br;
     }
     const bool timed = p->timing && p->ev_n + 2 <= p->ev.size();
-    // ACCSPMM_L2_PERSIST=<MiB> (measurement): mark B as an L2-persisting access-policy window
-    // for this launch only (the stream attribute is restored right after the launch)
-    const char *pe = std::getenv("ACCSPMM_L2_PERSIST");
-    const int64_t persist_mib = pe ? std::atoll(pe) : 0;
+    // Knobs::l2_persist_mib (variants build only, measurement): mark B as an L2-persisting
+    // access-policy window for this launch; the stream attribute and the device's persisting-L2
+    // limit are both restored right after the launch
+    const int64_t persist_mib = knobs().l2_persist_mib;
     cudaStreamAttrValue prev{};
     bool window = false;
+    size_t prev_limit = 0;
+    bool limit_changed = false;
     if (persist_mib > 0 && p->info.K > 0) {
-        static int64_t limit_set = -1;
         int dev = 0, maxp = 0, maxw = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
         cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev);
         const size_t want = std::min<size_t>((size_t)persist_mib << 20, (size_t)maxp);
-        if (limit_set != (int64_t)want) {
-            cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
-            limit_set = (int64_t)want;
-        }
+        if (cudaDeviceGetLimit(&prev_limit, cudaLimitPersistingL2CacheSize) == cudaSuccess && prev_limit != want)
+            limit_changed = cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) == cudaSuccess;
         const size_t es = tf32 ? 4 : 2;
         const size_t bytes = std::min<size_t>((size_t)p->info.K * (size_t)N * es, (size_t)maxw);
         cudaStreamGetAttribute((cudaStream_t)stream, cudaStreamAttributeAccessPolicyWindow, &prev);
@@ -495,11 +516,14 @@ static accspmm_status execute_impl(const accspmm_plan *p, const void *B, int64_t
         p->ev_n += 2;
     }
     if (window) cudaStreamSetAttribute((cudaStream_t)stream, cudaStreamAttributeAccessPolicyWindow, &prev);
+    if (limit_changed) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, prev_limit);
     return st;
 }
 
 accspmm_status accspmm_execute(const accspmm_plan *p, const void *B, int64_t N, void *C, void *stream)
 {
+    if (!p) return fail(ACCSPMM_ERR_INVALID_VALUE, "plan is NULL");
+    DeviceGuard guard(p->opt.device);
     return execute_impl(p, B, N, C, nullptr, 0, stream);
 }
 
@@ -513,6 +537,8 @@ accspmm_status accspmm_execute_allgather(const accspmm_plan *p, const void *B, i
             return fail(ACCSPMM_ERR_INVALID_VALUE, "C_all entries must be non-NULL and 16-byte aligned");
         dst[k] = (float *)C_all[k];
     }
+    if (!p) return fail(ACCSPMM_ERR_INVALID_VALUE, "plan is NULL");
+    DeviceGuard guard(p->opt.device);
     return execute_impl(p, B, N, dst[0], dst, n_dst, stream);
 }
 
@@ -526,6 +552,7 @@ accspmm_status accspmm_execute_host(const accspmm_plan *p, const void *B_host, i
     const size_t bB = (size_t)p->info.K * (size_t)N * es;
     const size_t bC = (size_t)p->info.rows * (size_t)N * sizeof(float);
     cudaStream_t s = (cudaStream_t)stream;
+    DeviceGuard guard(p->opt.device);
     {
         std::lock_guard<std::mutex> lk(p->mu);
         if (bB > p->dB_bytes) {
@@ -541,7 +568,7 @@ accspmm_status accspmm_execute_host(const accspmm_plan *p, const void *B_host, i
     }
     cudaError_t e = cudaMemcpyAsync(p->dB, B_host, bB, cudaMemcpyHostToDevice, s);
     if (e != cudaSuccess) return cuda_fail(e, "H2D B");
-    accspmm_status st = accspmm_execute(p, p->dB, N, p->dC, stream);
+    accspmm_status st = execute_impl(p, p->dB, N, p->dC, nullptr, 0, stream);
     if (st != ACCSPMM_OK) return st;
     e = cudaMemcpyAsync(C_host, p->dC, bC, cudaMemcpyDeviceToHost, s);
     if (e != cudaSuccess) return cuda_fail(e, "D2H C");
@@ -564,23 +591,26 @@ accspmm_status accspmm_execute_host_batch(const accspmm_plan *p, const void *con
     const size_t bB = (size_t)p->info.K * (size_t)N * es;
     const size_t bC = (size_t)p->info.rows * (size_t)N * sizeof(float);
     cudaStream_t s = (cudaStream_t)stream;
+    DeviceGuard guard(p->opt.device);
     {
         std::lock_guard<std::mutex> lk(p->mu);
-        auto grow = [&](void **a, void **b, size_t &have, size_t need) -> bool {
-            if (need <= have && *a && *b) return true;
-            cudaFree(*a); cudaFree(*b);
-            *a = *b = nullptr;
+        // every slot carries its own size (execute_host grows only the first slots)
+        auto grow = [&](void **a, size_t &have, size_t need) -> bool {
+            if (need <= have && *a) return true;
+            cudaFree(*a);
+            *a = nullptr;
             have = 0;
-            if (cudaMalloc(a, need ? need : 16) != cudaSuccess || cudaMalloc(b, need ? need : 16) != cudaSuccess) {
-                cudaFree(*a); cudaFree(*b);
-                *a = *b = nullptr;
+            if (cudaMalloc(a, need ? need : 16) != cudaSuccess) {
+                *a = nullptr;
                 return false;
             }
             have = need;
             return true;
         };
-        if (!grow(&p->dB, &p->dB2, p->dB_bytes, bB)) return fail(ACCSPMM_ERR_OUT_OF_MEMORY, "e2e B buffers");
-        if (!grow((void **)&p->dC, (void **)&p->dC2, p->dC_bytes, bC)) return fail(ACCSPMM_ERR_OUT_OF_MEMORY, "e2e C buffers");
+        if (!grow(&p->dB, p->dB_bytes, bB) || !grow(&p->dB2, p->dB2_bytes, bB))
+            return fail(ACCSPMM_ERR_OUT_OF_MEMORY, "e2e B buffers");
+        if (!grow((void **)&p->dC, p->dC_bytes, bC) || !grow((void **)&p->dC2, p->dC2_bytes, bC))
+            return fail(ACCSPMM_ERR_OUT_OF_MEMORY, "e2e C buffers");
         if (!p->s_h2d) {
             cudaError_t e = cudaStreamCreateWithFlags(&p->s_h2d, cudaStreamNonBlocking);
             if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->s_d2h, cudaStreamNonBlocking);
@@ -609,7 +639,7 @@ accspmm_status accspmm_execute_host_batch(const accspmm_plan *p, const void *con
         if (e == cudaSuccess) e = cudaStreamWaitEvent(s, p->ev_in[k], 0);
         if (e == cudaSuccess) e = cudaStreamWaitEvent(s, p->ev_out[k], 0);  // D2H of step i-2 has read dC[k]
         if (e != cudaSuccess) return cuda_fail(e, "batch H2D");
-        accspmm_status st = accspmm_execute(p, dB[k], N, dC[k], stream);
+        accspmm_status st = execute_impl(p, dB[k], N, dC[k], nullptr, 0, stream);
         if (st != ACCSPMM_OK) return st;
         e = cudaEventRecord(p->ev_k[k], s);
         if (e == cudaSuccess) e = cudaStreamWaitEvent(p->s_d2h, p->ev_k[k], 0);
@@ -626,7 +656,10 @@ accspmm_status accspmm_execute_host_batch(const accspmm_plan *p, const void *con
 void accspmm_plan_destroy(accspmm_plan *p)
 {
     if (!p) return;
-    if (p->opt.device >= 0) free_device(p);
+    if (p->opt.device >= 0) {
+        DeviceGuard guard(p->opt.device);
+        free_device(p);
+    }
     delete p;
 }
 
@@ -643,6 +676,7 @@ accspmm_status accspmm_plan_export_format(const accspmm_plan *p, uint32_t *rwo, 
     if (!p) return fail(ACCSPMM_ERR_INVALID_VALUE, "plan is NULL");
     const auto &I = p->info;
     const bool dev = p->opt.device >= 0;
+    DeviceGuard guard(p->opt.device);
     accspmm_status st = export_array(rwo, p->host.rwo, dev ? p->dev.rwo : nullptr, (size_t)I.W + 1);
     if (st == ACCSPMM_OK) st = export_array(tco, p->host.tco, dev ? p->dev.tco : nullptr, (size_t)I.NB + 1);
     if (st == ACCSPMM_OK) {
@@ -719,6 +753,7 @@ accspmm_status accspmm_plan_set_timing(accspmm_plan *p, int32_t enable)
 {
     if (!p) return fail(ACCSPMM_ERR_INVALID_VALUE, "plan is NULL");
     if (p->opt.device < 0) return fail(ACCSPMM_ERR_UNSUPPORTED, "host-only plan");
+    DeviceGuard guard(p->opt.device);
     std::lock_guard<std::mutex> lk(p->mu);
     if (enable && p->ev.empty()) {
         p->ev.resize(8192);
@@ -770,6 +805,7 @@ accspmm_status accspmm_debug_decode(const accspmm_plan *p, float *tiles, void *s
     if (p->opt.device < 0) return fail(ACCSPMM_ERR_UNSUPPORTED, "host-only plan");
     if (p->info.NB == 0) return ACCSPMM_OK;
     if (!tiles) return fail(ACCSPMM_ERR_INVALID_VALUE, "tiles is NULL");
+    DeviceGuard guard(p->opt.device);
     return launch_decode(p->dev, tiles, stream);
 }
 

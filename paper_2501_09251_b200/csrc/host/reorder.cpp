@@ -25,8 +25,6 @@
 namespace accspmm {
 
 namespace {
-constexpr int kCandWindow = 64;  // L (default; ACCSPMM_REORDER_L overrides for experiments)
-constexpr int kHubCap = 128;     // H (default; ACCSPMM_REORDER_H overrides for experiments)
 
 int env_or(const char *name, int dflt)
 {
@@ -252,7 +250,7 @@ std::vector<uint32_t> reorder_alg1(const Csr &a)
     prv[0] = n;
     prv[(size_t)n] = n - 1;
     if (n > 0) nxt[(size_t)n - 1] = n;
-    const int L = env_or("ACCSPMM_REORDER_L", kCandWindow), H = env_or("ACCSPMM_REORDER_H", kHubCap);
+    const int L = knobs().reorder_L, H = knobs().reorder_H;  // reading R6 (variants build: sweepable)
     std::vector<char> visited((size_t)n, 0);
     std::vector<uint32_t> mark((size_t)n, 0);
     uint32_t stamp = 0;

@@ -43,8 +43,7 @@ int auto_cap(int64_t NB)
 
 int auto_group_cap(int cap)
 {
-    const char *e = std::getenv("ACCSPMM_GROUP_CAP");  // A/B measurements only
-    const int g = e ? std::atoi(e) : kGroupCap;
+    const int g = knobs().group_cap > 0 ? knobs().group_cap : kGroupCap;  // variants build: sweepable
     return std::max(1, std::min(cap, g));
 }
 

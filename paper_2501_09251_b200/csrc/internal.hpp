@@ -23,6 +23,29 @@ constexpr int64_t kRoundReuse = 32;
 // Error plumbing (thread-local message returned by accspmm_last_error).
 accspmm_status fail(accspmm_status s, const std::string &msg);
 
+// Measurement knobs for A/B sweeps (tools/sweep.py).  Only the variants build
+// (-DACCSPMM_VARIANTS -> libaccspmm_variants.so) reads them from ACCSPMM_* environment
+// variables; the product library (libaccspmm.so) never calls getenv and always uses these
+// defaults, which are the measured choices of DESIGN.md §7.
+struct Knobs {
+    int kcfg = -1;             // ACCSPMM_KCFG: kernel variant (-1 = default kernel)
+    int fw = 0;                // ACCSPMM_FW: feature-slice width override (0 = pick_fw rule)
+    int slice_major = 1;       // ACCSPMM_SLICE_MAJOR: slice-major grid when N spans several slices
+    int l2promo = 3;           // ACCSPMM_L2PROMO: TMA L2 sector promotion 0..3 = none/64/128/256 B
+    int round_b = 0;           // ACCSPMM_ROUND_B: 1 = rho(B) pre-pass, 2 = in-kernel, 0 = reuse rule
+    int64_t l2_persist_mib = 0;  // ACCSPMM_L2_PERSIST: L2 persisting window over B (MiB)
+    int group_cap = 0;         // ACCSPMM_GROUP_CAP: grouped-plan concatenation limit (0 = kGroupCap)
+    int reorder_L = 64;        // ACCSPMM_REORDER_L: Alg. 1 candidate window (reading R6)
+    int reorder_H = 128;       // ACCSPMM_REORDER_H: Alg. 1 neighbour-list cap (reading R6)
+};
+const Knobs &knobs();          // variants build: re-read on every call (sweeps flip them)
+constexpr bool kVariantsBuild =
+#ifdef ACCSPMM_VARIANTS
+    true;
+#else
+    false;
+#endif
+
 struct Csr {
     int64_t M = 0, K = 0;
     const int64_t *rowptr = nullptr;
@@ -114,7 +137,7 @@ accspmm_status build_format_device(const Csr &a, const float *vals, const std::v
 void free_device_format(DeviceFormat &f);
 
 // Feature-slice width of one warp for a given N (N % 16 == 0): the widest of 128/64/32/16
-// dividing N.  ACCSPMM_FW (16/32/64/128, must divide N) overrides it for A/B measurements.
+// dividing N.  Knobs::fw (variants build, must divide N) overrides it for A/B measurements.
 int pick_fw(int64_t N);
 
 // round_b: the kernel applies rho(B) in registers (B not pre-rounded)

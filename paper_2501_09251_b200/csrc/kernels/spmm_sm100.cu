@@ -27,7 +27,8 @@
 //     workspace and the last-arriving segment sums the partials in segment order
 //     (deterministic, Q18).
 // spmm_bittcf_kernel (register-direct gather: each lane loads its fragment rows with
-// 128-bit non-caching loads) is kept as a measured alternative (ACCSPMM_KCFG=10..12).
+// 128-bit non-caching loads) and the other measured alternatives are compiled only into the
+// variants build (-DACCSPMM_VARIANTS, libaccspmm_variants.so; ACCSPMM_KCFG selects them).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_fp16.h>
@@ -304,6 +305,9 @@ __device__ __forceinline__ void round_frag(Frag<FW, F16> &fr)
 
 // ------------------------------------------------------------------ the kernel
 
+#ifdef ACCSPMM_VARIANTS
+// Register-direct gather (variants build only): each lane loads its fragment rows with 128-bit
+// non-caching loads; bound by the LSU data pipe, it lost to gather4 at every width.
 template <int FW, bool F16, int WARPS, bool RND>
 __global__ void __launch_bounds__(WARPS * 32) spmm_bittcf_kernel(const KParams p)
 {
@@ -495,6 +499,7 @@ __global__ void __launch_bounds__(WARPS * 32) spmm_bittcf_kernel(const KParams p
         }
     }
 }
+#endif  // ACCSPMM_VARIANTS
 
 
 // ================================================================== mbarrier / TMA helpers
@@ -1018,6 +1023,7 @@ __global__ void permute_b_kernel(const uint4 *__restrict__ in, uint4 *__restrict
 
 // ------------------------------------------------------------------ launch
 
+#ifdef ACCSPMM_VARIANTS
 template <int FW, bool F16, int WARPS, bool RND = false>
 accspmm_status launch_cfg(const KParams &kp, int64_t n_units, cudaStream_t stream)
 {
@@ -1030,12 +1036,7 @@ accspmm_status launch_cfg(const KParams &kp, int64_t n_units, cudaStream_t strea
     if (e != cudaSuccess) return fail(ACCSPMM_ERR_CUDA, std::string("spmm launch: ") + cudaGetErrorString(e));
     return ACCSPMM_OK;
 }
-
-int env_int(const char *name, int dflt)
-{
-    const char *s = std::getenv(name);
-    return s ? std::atoi(s) : dflt;
-}
+#endif
 
 // NM = 1: one tensor map (the full-width map when several slices exist); NM = kMaxSliceMaps:
 // one map per slice (tensor_map decides; only the default configurations instantiate it)
@@ -1073,7 +1074,7 @@ accspmm_status tensor_map(const DevicePlan &d, const KParams &kp, int FW, bool m
     const void *B = kp.B;
     const int64_t N = kp.N;
     const int nm = multi ? map_count(kp) : 1;
-    const int pv = env_int("ACCSPMM_L2PROMO", 3);
+    const int pv = knobs().l2promo;
     const uint64_t key[4] = {(uint64_t)(uintptr_t)B, (uint64_t)N, (uint64_t)FW,
                              (uint64_t)(d.precision + 1) | ((uint64_t)nm << 8) | ((uint64_t)pv << 16)};
     G4Maps *maps = reinterpret_cast<G4Maps *>(d.tmap);
@@ -1090,8 +1091,8 @@ accspmm_status tensor_map(const DevicePlan &d, const KParams &kp, int FW, bool m
         }
         const bool f16 = d.precision == ACCSPMM_FP16;
         const cuuint64_t es = f16 ? 2 : 4;
-        // L2 sector promotion of the gathered rows (ACCSPMM_L2PROMO 0..3 = none/64/128/256 B
-        // for A/B measurements; default 256 B)
+        // L2 sector promotion of the gathered rows (Knobs::l2promo 0..3 = none/64/128/256 B
+        // for A/B measurements in the variants build; default 256 B)
         const CUtensorMapL2promotion promo = pv == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
                                             : pv == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
                                             : pv == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
@@ -1132,75 +1133,86 @@ accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, 
     // Default (measured): TMA gather4, one warp x 2 stages per CTA (the warp's
     // shared-memory addresses are then CTA constants, so the TMA operands need few uniform-
     // register moves), tuned launch bounds, one tensor map per feature slice when N > FW.
-    // FP16 takes its A fragments by ldmatrix.trans.  ACCSPMM_KCFG selects other variants for
-    // A/B measurements: 20 = 2 warps per CTA without a launch-bounds minimum (the round-1
-    // kernel), 46 = 2 warps per CTA with tuned bounds, 47 = FP16 fragments by LDS.128 + PRMT,
-    // 10-12 = register-direct gather (4, 2, 8 warps per CTA).
+    // FP16 takes its A fragments by ldmatrix.trans.
     constexpr int MW = tuned_min_warps<FW, F16>();
-    const int kcfg = kp.ndst > 0 ? -1 : env_int("ACCSPMM_KCFG", -1);  // all-gather: default kernel
+    const int kcfg = kp.ndst > 0 ? -1 : knobs().kcfg;  // all-gather: default kernel
+    const G4Maps *map = nullptr;
+    // per-slice maps only for the kernels instantiated with them (variants 20/46: one map)
+    const bool multi = map_count(kp) > 1 && kcfg != 20 && kcfg != 46;
+    static const G4Maps no_maps = {};  // no TC blocks (e.g. K = 0): no TMA is ever issued
     if (kcfg < 0 || kcfg >= 20) {
-        const G4Maps *map = nullptr;
-        // per-slice maps only for the kernels instantiated with them (variants 20/46: one map)
-        const bool multi = map_count(kp) > 1 && kcfg != 20 && kcfg != 46;
-        static const G4Maps no_maps = {};  // no TC blocks (e.g. K = 0): no TMA is ever issued
         accspmm_status st = d.NB > 0 ? tensor_map(d, kp, FW, multi, &map) : (map = &no_maps, ACCSPMM_OK);
         if (st != ACCSPMM_OK) return st;
-        constexpr int NM = kMaxSliceMaps;
-        constexpr bool LD = F16;  // FP16: ldmatrix.trans fragments (measured -10.5%)
-        constexpr bool K8 = FW <= 64;  // TF32: one m16n8k8 per tile at FW <= 64 (-6% at N = 64)
+    }
+    constexpr int NM = kMaxSliceMaps;
+    constexpr bool LD = F16;       // FP16: ldmatrix.trans fragments (measured -10.5%)
+    constexpr bool K8 = FW <= 64;  // TF32: one m16n8k8 per tile at FW <= 64 (-6% at N = 64)
+#ifdef ACCSPMM_VARIANTS
+    // Measured-and-rejected alternatives, selectable by ACCSPMM_KCFG in the variants build only
+    // (libaccspmm_variants.so): 20 = 2 warps per CTA without a launch-bounds minimum (the
+    // round-1 kernel), 46 = 2 warps per CTA with tuned bounds, 47 = FP16 fragments by LDS.128 +
+    // PRMT, 48 = the other TF32 k4/k8 choice, 49 = values two blocks ahead, 50/51 = 3/4-stage
+    // TMA ring, 52 = value loads with an L2 256-byte prefetch, 10-12 = register-direct gather.
+    if (kcfg >= 0 && kcfg < 20) {
         if constexpr (!F16) {
-            if (rnd) {  // B not pre-rounded: rho(B) applied in registers
-                if (kcfg == 20) return launch_g4<FW, F16, 2, 2, true, 1>(kp, map, n_units, stream);
-                if (kcfg == 52) {
-                    if (multi) return launch_g4<FW, F16, 1, 2, true, MW, NM, false, K8, 1, true>(kp, map, n_units, stream);
-                    return launch_g4<FW, F16, 1, 2, true, MW, 1, false, K8, 1, true>(kp, map, n_units, stream);
-                }
-                if (multi) return launch_g4<FW, F16, 1, 2, true, MW, NM, false, K8>(kp, map, n_units, stream);
-                return launch_g4<FW, F16, 1, 2, true, MW, 1, false, K8>(kp, map, n_units, stream);
-            }
+            if (rnd) return launch_cfg<FW, F16, 2, true>(kp, n_units, stream);
         }
         switch (kcfg) {
-        case 20: return launch_g4<FW, F16, 2, 2, false, 1>(kp, map, n_units, stream);
-        case 46: return launch_g4<FW, F16, 2, 2, false, MW / 2>(kp, map, n_units, stream);
-        case 48:  // TF32 m16n8k8 vs two m16n8k4: the opposite of the default choice
-            if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, !K8>(kp, map, n_units, stream);
-            return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, !K8>(kp, map, n_units, stream);
-        case 52:  // value loads with an L2 256-byte prefetch
-            if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, true>(kp, map, n_units, stream);
-            return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, true>(kp, map, n_units, stream);
-        case 50:  // 3-stage TMA ring
-            if (multi) return launch_g4<FW, F16, 1, 3, false, MW, NM, LD, K8>(kp, map, n_units, stream);
-            return launch_g4<FW, F16, 1, 3, false, MW, 1, LD, K8>(kp, map, n_units, stream);
-        case 51:  // 4-stage TMA ring
-            if (multi) return launch_g4<FW, F16, 1, 4, false, MW, NM, LD, K8>(kp, map, n_units, stream);
-            return launch_g4<FW, F16, 1, 4, false, MW, 1, LD, K8>(kp, map, n_units, stream);
-        case 49:  // values loaded two blocks ahead (4-slot ring)
-            if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 2>(kp, map, n_units, stream);
-            return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 2>(kp, map, n_units, stream);
-        case 47:  // FP16 fragments by LDS.128 + PRMT packing
-            if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM>(kp, map, n_units, stream);
-            return launch_g4<FW, F16, 1, 2, false, MW>(kp, map, n_units, stream);
-        default:
-            if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8>(kp, map, n_units, stream);
-            return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8>(kp, map, n_units, stream);
+        case 10: return launch_cfg<FW, F16, 4>(kp, n_units, stream);
+        case 12: return launch_cfg<FW, F16, 8>(kp, n_units, stream);
+        default: return launch_cfg<FW, F16, 2>(kp, n_units, stream);
         }
     }
     if constexpr (!F16) {
-        if (rnd) return launch_cfg<FW, F16, 2, true>(kp, n_units, stream);
+        if (rnd) {  // B not pre-rounded: rho(B) applied in registers
+            if (kcfg == 20) return launch_g4<FW, F16, 2, 2, true, 1>(kp, map, n_units, stream);
+            if (kcfg == 52) {
+                if (multi) return launch_g4<FW, F16, 1, 2, true, MW, NM, false, K8, 1, true>(kp, map, n_units, stream);
+                return launch_g4<FW, F16, 1, 2, true, MW, 1, false, K8, 1, true>(kp, map, n_units, stream);
+            }
+        }
     }
-    // register-direct flavour (kcfg 10-12: 4, 2 or 8 warps per CTA)
-    switch (kcfg) {
-    case 10: return launch_cfg<FW, F16, 4>(kp, n_units, stream);
-    case 12: return launch_cfg<FW, F16, 8>(kp, n_units, stream);
-    default: return launch_cfg<FW, F16, 2>(kp, n_units, stream);
+    if (!rnd) {
+        switch (kcfg) {
+        case 20: return launch_g4<FW, F16, 2, 2, false, 1>(kp, map, n_units, stream);
+        case 46: return launch_g4<FW, F16, 2, 2, false, MW / 2>(kp, map, n_units, stream);
+        case 48:
+            if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, !K8>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, !K8>(kp, map, n_units, stream);
+        case 52:
+            if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, true>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, true>(kp, map, n_units, stream);
+        case 50:
+            if (multi) return launch_g4<FW, F16, 1, 3, false, MW, NM, LD, K8>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 3, false, MW, 1, LD, K8>(kp, map, n_units, stream);
+        case 51:
+            if (multi) return launch_g4<FW, F16, 1, 4, false, MW, NM, LD, K8>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 4, false, MW, 1, LD, K8>(kp, map, n_units, stream);
+        case 49:
+            if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 2>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 2>(kp, map, n_units, stream);
+        case 47:
+            if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 2, false, MW>(kp, map, n_units, stream);
+        default: break;
+        }
     }
+#endif
+    if constexpr (!F16) {
+        if (rnd) {  // B not pre-rounded: rho(B) applied in registers
+            if (multi) return launch_g4<FW, F16, 1, 2, true, MW, NM, false, K8>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 2, true, MW, 1, false, K8>(kp, map, n_units, stream);
+        }
+    }
+    if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8>(kp, map, n_units, stream);
+    return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8>(kp, map, n_units, stream);
 }
 
 }  // namespace
 
 int pick_fw(int64_t N)
 {
-    const int f = env_int("ACCSPMM_FW", 0);
+    const int f = knobs().fw;
     if ((f == 16 || f == 32 || f == 64 || f == 128) && N % f == 0) return f;
     return N % 128 == 0 ? 128 : N % 64 == 0 ? 64 : N % 32 == 0 ? 32 : 16;
 }
@@ -1257,8 +1269,8 @@ accspmm_status launch_spmm(const DevicePlan &d, const void *B, const void *zrow,
     kp.Krows = (int32_t)d.K;
     kp.ndst = ndst;
     // slice-major grid when N spans several slices: one 128-wide slice of B at a time is the L2
-    // working set (N = 512: -13%, N = 256: -3%; ACCSPMM_SLICE_MAJOR=0 restores slice-fastest)
-    kp.slice_major = env_int("ACCSPMM_SLICE_MAJOR", 1) != 0 && kp.nslices > 1;
+    // working set (N = 512: -13%, N = 256: -3%; Knobs::slice_major = 0 restores slice-fastest)
+    kp.slice_major = knobs().slice_major != 0 && kp.nslices > 1;
     kp.orig_map = d.orig_map ? d.orig_map : d.row_map;
     for (int k = 0; k < kMaxGatherDst; ++k) kp.dst[k] = k < ndst ? dst[k] : nullptr;
     cudaStream_t s = (cudaStream_t)stream;

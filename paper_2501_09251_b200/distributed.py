@@ -72,11 +72,24 @@ def unpermute(G, ids, M: int, stream=None):
     return C
 
 
+def _stream_ctx(stream):
+    """Runs the enclosed collectives on ``stream`` (NCCL and symmetric-memory barriers are issued
+    on the current stream), so they are ordered after the SpMM launched there."""
+    import contextlib
+
+    import torch
+    if stream is None or not hasattr(stream, "cuda_stream"):
+        return contextlib.nullcontext()
+    return torch.cuda.stream(stream)
+
+
 def spmm_all(plan: Plan, B, M: int, stream=None):
-    """Execute this rank's slab and assemble the full C on every rank (all-gather + un-permute)."""
-    C_slab = plan.execute(B, stream=stream)
-    G, I = gather_slabs(C_slab, plan.export_rows())
-    return unpermute(G, I, M, stream)
+    """Execute this rank's slab and assemble the full C on every rank (all-gather + un-permute),
+    everything ordered on ``stream`` (default: the current stream)."""
+    with _stream_ctx(stream):
+        C_slab = plan.execute(B, stream=stream)
+        G, I = gather_slabs(C_slab, plan.export_rows())
+        return unpermute(G, I, M, stream)
 
 
 class FusedAllGather:
@@ -96,9 +109,14 @@ class FusedAllGather:
 
     def step(self, plan: Plan, B, stream=None):
         """C = A . B on every rank: this rank's rows are written into all ranks' C, then a
-        device barrier (on the current stream) waits for every rank's rows."""
-        plan.execute_allgather(B, self.views, stream)
-        self.hdl.barrier()
+        device barrier waits for every rank's rows.  A barrier before the epilogue writes
+        keeps a fast rank's step t+1 from overwriting a peer's C while that peer is still
+        consuming step t (write-after-read across ranks).  Both barriers and the SpMM are
+        ordered on ``stream`` (default: the current stream)."""
+        with _stream_ctx(stream):
+            self.hdl.barrier()
+            plan.execute_allgather(B, self.views, stream)
+            self.hdl.barrier()
         return self.C
 
 

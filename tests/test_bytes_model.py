@@ -12,7 +12,7 @@ from oracle import bittcf as bt
 def test_bytes_model_matches_per_unit_figures(precision, N):
     A = gen.dcsbm(2000, 80_000, 5, 2.2, 0.2, 1500, seed=2, oversample=1.3)
     v = gen.values_uniform(A.nnz, 1)
-    p = acc.Plan(A.M, A.K, A.rowptr, A.colidx, v, precision=precision, device=-1)
+    p = acc.Plan(A.M, A.K, A.rowptr, A.colidx, v, precision=precision, device=-1, reorder="off")
     F = bt.encode(A.M, A.K, A.rowptr, A.colidx)
     es = 2 if precision == "fp16" else 4
     W, NB, nnz = F["W"], F["NB"], A.nnz

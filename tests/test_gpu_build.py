@@ -28,6 +28,7 @@ def _cuda():
 
 
 def _pair(A, v, precision, **kw):
+    kw.setdefault("reorder", "off")
     ph = acc.Plan(A.M, A.K, A.rowptr, A.colidx, v, precision=precision, build="host", **kw)
     pd = acc.Plan(A.M, A.K, A.rowptr, A.colidx, v, precision=precision, build="device", **kw)
     return ph, pd

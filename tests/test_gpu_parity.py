@@ -263,7 +263,7 @@ def test_device_decode_matches_oracle_tiles(precision):
     from oracle.rounding import rho
     A = _ragged(seed=2, M=300, K=200, nnz=6000)
     v = gen.values_uniform(A.nnz, 1)
-    p = acc.Plan(A.M, A.K, A.rowptr, A.colidx, v, precision=precision)
+    p = acc.Plan(A.M, A.K, A.rowptr, A.colidx, v, precision=precision, reorder="off")
     tiles = p.debug_decode().cpu().numpy()
     F = bt.encode(A.M, A.K, A.rowptr, A.colidx, rho(v, precision))
     ref = np.zeros((F["NB"], 64), np.float32)
@@ -283,7 +283,7 @@ def test_device_plan_exports_paper_format(precision):
     from oracle.rounding import rho
     A = _ragged(seed=6, M=700, K=900, nnz=9000)
     v = gen.values_uniform(A.nnz, 2)
-    p = acc.Plan(A.M, A.K, A.rowptr, A.colidx, v, precision=precision)
+    p = acc.Plan(A.M, A.K, A.rowptr, A.colidx, v, precision=precision, reorder="off")
     F = p.export_format()
     ref = bt.encode(A.M, A.K, A.rowptr, A.colidx, rho(v, precision))
     for k in ("RowWindowOffset", "TCOffset", "SparseAToB", "TCLocalBit"):
@@ -323,6 +323,25 @@ def test_e2e_host_batch_pipeline_matches_device_path(precision):
     for c, r in zip(Ch, ref):
         assert np.array_equal(c.numpy(), r)
     acc.accspmm_execute_host_batch(p.handle, [], [], 64)  # empty batch is a no-op
+
+
+def test_e2e_mixed_host_calls_with_growing_N():
+    """ADVICE r1 repro: execute_host_batch(N=16), execute_host(N=128), execute_host_batch(N=128)
+    must regrow the second staging slots too (each slot carries its own size); every C equals
+    the oracle product of its own B."""
+    A = _ragged(seed=9)
+    v = gen.values_int(A.nnz, 1)
+    p = acc.Plan(A.M, A.K, A.rowptr, A.colidx, v, reorder="off")
+    for kind, N in (("batch", 16), ("single", 128), ("batch", 128), ("single", 256), ("batch", 256)):
+        Bs = [gen.dense_int(A.K, N, 30 + N + i) for i in range(3)]
+        Cs = [np.full((A.M, N), np.nan, np.float32) for _ in Bs]
+        if kind == "batch":
+            p.execute_host_batch(Bs, Cs)
+        else:
+            for B, C in zip(Bs, Cs):
+                p.execute_host(B, C)
+        for B, C in zip(Bs, Cs):
+            assert_bit_exact(C, A, v, B, "tf32")
 
 
 def test_execute_errors():
@@ -484,27 +503,6 @@ def test_permute_cols_partitions_and_device_build():
             out[rows] = G
     torch.cuda.synchronize()
     assert np.array_equal(out.cpu().numpy(), Cfull)
-
-
-@pytest.mark.parametrize("kcfg", ["20", "46", "47", "48", "49", "50", "51", "52", "10", "11", "12"])
-@pytest.mark.parametrize("precision", PRECISIONS)
-def test_measurement_variants_stay_exact(kcfg, precision, monkeypatch):
-    """Every A/B kernel variant selectable by ACCSPMM_KCFG (2 warps per CTA,
-    FP16 PRMT fragments, k4/k8 swap, values two ahead, 3/4-stage rings, L2::256B value loads,
-    register-direct gather) computes the same product: integer data bit-exact (split windows
-    included), floats within tolerance, N = 64 and 256 (per-slice maps)."""
-    monkeypatch.setenv("ACCSPMM_KCFG", kcfg)
-    A = gen.dcsbm(3000, 150_000, 5, 2.2, 0.2, 2000, seed=3, oversample=1.3)
-    v = gen.values_int(A.nnz, 1)
-    for N in (64, 256):
-        B = gen.dense_int(A.K, N, 2)
-        C, p = run(A, v, B, precision, balance="on", unit_cap=32)
-        assert p.info["n_split_windows"] > 0
-        assert_bit_exact(C, A, v, B, precision)
-    vf = gen.values_uniform(A.nnz, 4)
-    Bf = gen.dense_normal(A.K, 128, 5)
-    Cf, _ = run(A, vf, Bf, precision)
-    assert_within(Cf, A, vf, Bf, precision)
 
 
 @pytest.mark.parametrize("precision", PRECISIONS)

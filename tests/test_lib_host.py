@@ -26,6 +26,7 @@ def _built():
 
 def host_plan(A, vals, **kw):
     kw.setdefault("device", -1)
+    kw.setdefault("reorder", "off")   # fixtures pin the un-reordered format unless they ask
     return acc.Plan(A.M, A.K, A.rowptr, A.colidx, vals, **kw)
 
 
@@ -302,3 +303,52 @@ def test_sass_reads_no_unwritten_uniform_registers():
     r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "check_sass_ur.py"), acc.LIB_PATH],
                        capture_output=True, text=True, check=True)
     assert r.stdout.strip().endswith("kernels with unwritten uniform reads: 0"), r.stdout[-2000:]
+
+
+def test_binding_rejects_malformed_operands():
+    """Plan.execute* check shape, dtype, layout and device before handing raw pointers to the C
+    ABI (which cannot see them): a half-precision B on a TF32 plan, a transposed B or a CPU
+    tensor must raise instead of reading out of bounds or computing garbage."""
+    import torch
+    A = gen.uniform_random(40, 24, 200, seed=1)
+    v = gen.values_uniform(A.nnz, 1)
+    p = host_plan(A, v)
+    with pytest.raises(TypeError):
+        p.execute(torch.zeros((24, 16), dtype=torch.float16))
+    with pytest.raises(ValueError):
+        p.execute(torch.zeros((23, 16), dtype=torch.float32))
+    with pytest.raises(ValueError):
+        p.execute(torch.zeros((16, 24), dtype=torch.float32).t())       # not contiguous
+    with pytest.raises(ValueError):
+        p.execute(torch.zeros((24,), dtype=torch.float32))              # not 2-D
+    with pytest.raises(ValueError):
+        p.execute(torch.zeros((24, 16), dtype=torch.float32))           # host memory
+    with pytest.raises(ValueError):
+        p.execute_host(np.zeros((24, 16), np.float32), np.zeros((40, 8), np.float32))
+    with pytest.raises(TypeError):
+        p.execute_host(np.zeros((24, 16), np.float32), np.zeros((40, 16), np.float64))
+    with pytest.raises(ValueError):
+        p.execute_host_batch([np.zeros((24, 16), np.float32)], [])
+    ph = host_plan(A, v, precision="fp16")
+    with pytest.raises(TypeError):
+        ph.execute_host(np.zeros((24, 16), np.float32), np.zeros((40, 16), np.float32))
+
+
+def test_default_options_follow_the_abi_contract():
+    """plan_create defaults are TF32, reorder auto, balance auto."""
+    opt = acc.accspmm_options_default()
+    assert opt.precision == acc.TF32
+    assert opt.reorder == acc.REORDER["auto"]
+    assert opt.balance == acc.BALANCE["auto"]
+    assert opt.nparts == 1 and opt.unit_cap == 0
+
+
+def test_product_library_has_no_measurement_knobs():
+    """The product library never reads ACCSPMM_* knobs (they live in libaccspmm_variants.so)."""
+    import subprocess
+    lib = acc.LIB_PATH
+    assert lib.endswith("libaccspmm.so")
+    strings = subprocess.run(["strings", lib], capture_output=True, text=True).stdout
+    for knob in ("ACCSPMM_KCFG", "ACCSPMM_FW", "ACCSPMM_ROUND_B", "ACCSPMM_L2_PERSIST", "ACCSPMM_L2PROMO",
+                 "ACCSPMM_SLICE_MAJOR", "ACCSPMM_GROUP_CAP"):
+        assert knob not in strings, knob

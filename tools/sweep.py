@@ -10,6 +10,8 @@ import sys
 import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+# the A/B knobs and kernel variants exist only in the measurement build
+os.environ.setdefault("ACCSPMM_LIB", "variants")
 import numpy as np
 import torch
 
