@@ -16,9 +16,13 @@ Readings:
     nbrs with v" is the next L unvisited vertices in DFS order, neighbour lists
     capped at their first H entries (ascending id); ties by DFS order (P:241);
     no candidate with >= 1 common neighbour -> continue with the next DFS vertex.
-  * R6b: after a visit (whose merge decision uses all of its edges), a community
-    carries on only its EDGE_CAP heaviest community edges (ties: smaller id) --
-    a bound on the coarsening work; graphs whose lists stay short are unaffected;
+  * edge_cap (default None = Alg. 1 as printed): the library's reading R6b, where after a
+    visit (whose merge decision uses all of its edges) a community carries on only its
+    edge_cap = 256 heaviest community edges (ties: smaller id) -- a bound on the coarsening
+    work.  The oracle's default is the literal algorithm; ``edge_cap=EDGE_CAP`` reproduces
+    the library's bounded variant so tests can check the branch where it triggers
+    (tests/test_oracle_partition_reorder.py) and show it is a no-op where no list grows
+    past the cap;
   * non-square A -> identity (Q14).
 """
 from __future__ import annotations
@@ -66,8 +70,11 @@ def delta_q(w_uv: float, a_u: float, a_v: float, m2: float) -> float:
     return 2.0 * (w_uv / m2 - a_u * a_v / (m2 * m2))
 
 
-def dendrogram(adj):
-    """Alg. 1 Step I (l.1-8): returns (parent, children, roots) of the merge forest."""
+def dendrogram(adj, edge_cap: int | None = None, stats: dict | None = None):
+    """Alg. 1 Step I (l.1-8): returns (parent, children, roots) of the merge forest.
+
+    edge_cap: None = literal Alg. 1; an int = reading R6b (see the module docstring).
+    stats (optional dict): receives "truncations" = how many visits truncated a list."""
     n = len(adj)
     deg = [len(a) for a in adj]
     m2 = float(sum(deg))
@@ -97,9 +104,11 @@ def dendrogram(adj):
             dq = delta_q(acc[r], a[r], a[v], m2)
             if best < 0 or dq > best_dq:
                 best, best_dq = r, dq
-        if len(acc) > EDGE_CAP:                              # R6b
-            keep = sorted(acc.items(), key=lambda kv: (-kv[1], kv[0]))[:EDGE_CAP]
+        if edge_cap is not None and len(acc) > edge_cap:     # reading R6b (not in Alg. 1)
+            keep = sorted(acc.items(), key=lambda kv: (-kv[1], kv[0]))[:edge_cap]
             acc = dict(keep)
+            if stats is not None:
+                stats["truncations"] = stats.get("truncations", 0) + 1
         edges[v] = acc
         if best >= 0 and best_dq > 0.0:                      # l.5-7 merge v into u
             u = best
@@ -157,10 +166,12 @@ def ordering(adj, children, roots, L: int = CAND_WINDOW, H: int = HUB_CAP):
     return np.asarray(perm, dtype=np.int64)
 
 
-def reorder(M: int, K: int, rowptr, colidx, L: int = CAND_WINDOW, H: int = HUB_CAP):
-    """Algorithm 1 end to end: perm new->old (identity when M != K, Q14)."""
+def reorder(M: int, K: int, rowptr, colidx, L: int = CAND_WINDOW, H: int = HUB_CAP,
+            edge_cap: int | None = None, stats: dict | None = None):
+    """Algorithm 1 end to end: perm new->old (identity when M != K, Q14).
+    edge_cap=EDGE_CAP gives the library's reading R6b; None (default) the literal Alg. 1."""
     if M != K:
         return np.arange(M, dtype=np.int64)
     adj = affinity_graph(M, rowptr, colidx)
-    _, children, roots = dendrogram(adj)
+    _, children, roots = dendrogram(adj, edge_cap, stats)
     return ordering(adj, children, roots, L, H)

@@ -213,10 +213,74 @@ def _graphs():
 
 @pytest.mark.parametrize("idx", range(11))
 def test_reorder_matches_oracle_algorithm1(idx):
+    """No community list outgrows the R6b cap on these graphs: the library equals the literal
+    Alg. 1 of the oracle, and the oracle's bounded variant is a no-op there."""
     A = _graphs()[idx]
     got = acc.accspmm_reorder(A.M, A.rowptr, A.colidx)
+    st = {}
     ref = orr.reorder(A.M, A.K, A.rowptr, A.colidx)
+    assert np.array_equal(orr.reorder(A.M, A.K, A.rowptr, A.colidx, edge_cap=orr.EDGE_CAP, stats=st), ref)
+    assert st.get("truncations", 0) == 0
     assert np.array_equal(got.astype(np.int64), ref)
+
+
+def _shuffled(A, seed):
+    """Symmetric relabelling P A P^T (random P): hides any structure the ids carry."""
+    n = A.M
+    lab = np.random.default_rng(seed).permutation(n)
+    r = lab[A.row_ids()]
+    c = lab[A.colidx.astype(np.int64)]
+    return gen.csr_from_pairs(r, c, n, n)
+
+
+@pytest.mark.parametrize("nx", [14, 16])
+def test_reorder_edge_cap_branch_matches_oracle(nx):
+    """Reading R6b: a community carries on only its 256 heaviest community
+    edges after a visit.  On 27-point stencils of 14^3 / 16^3 vertices a community list
+    outgrows 256 (the branch triggers 1 / 3 times and changes the ordering against the literal
+    Alg. 1), and the library's permutation equals the oracle's bounded variant exactly."""
+    A = gen.stencil27(nx)
+    st = {}
+    ref = orr.reorder(A.M, A.K, A.rowptr, A.colidx, edge_cap=orr.EDGE_CAP, stats=st)
+    assert st["truncations"] >= 1
+    assert not np.array_equal(ref, orr.reorder(A.M, A.K, A.rowptr, A.colidx))   # the branch matters
+    got = acc.accspmm_reorder(A.M, A.rowptr, A.colidx).astype(np.int64)
+    assert np.array_equal(got, ref)
+
+
+def test_reorder_edge_cap_invariants_on_large_graph():
+    """Where R6b triggers, the bounded reordering is still a valid Alg. 1 ordering (the
+    invariants S:194-199 / S:572 pin both variants): a bijection, deterministic, a shuffled
+    stencil (18^3) plus a shuffled two-clique component keeps each clique contiguous, and the
+    TC-block count of the reordered shuffled stencil drops below the shuffled one."""
+    from oracle import bittcf as bt
+    S = _shuffled(gen.stencil27(18), 1)
+    k = 12
+    T = gen.two_cliques(k, seed=4)
+    n = S.M + T.M
+    r = np.concatenate([S.row_ids(), T.row_ids() + S.M])
+    c = np.concatenate([S.colidx.astype(np.int64), T.colidx.astype(np.int64) + S.M])
+    A = gen.csr_from_pairs(r, c, n, n)
+    lab = np.random.default_rng(4).permutation(2 * k)   # two_cliques(seed=4) labelling
+    clique_of = {S.M + int(lab[i]): (0 if i < k else 1) for i in range(2 * k)}
+    for cap in (None, orr.EDGE_CAP):
+        st = {}
+        perm = orr.reorder(A.M, A.K, A.rowptr, A.colidx, edge_cap=cap, stats=st)
+        assert sorted(perm.tolist()) == list(range(n))
+        assert np.array_equal(perm, orr.reorder(A.M, A.K, A.rowptr, A.colidx, edge_cap=cap))
+        seq = [clique_of[int(v)] for v in perm if int(v) in clique_of]
+        pos = [i for i, v in enumerate(perm) if int(v) in clique_of]
+        first = [p for p, q in zip(pos, seq) if q == 0]
+        second = [p for p, q in zip(pos, seq) if q == 1]
+        assert max(first) - min(first) == k - 1 and max(second) - min(second) == k - 1
+        if cap is not None:
+            assert st["truncations"] >= 1
+            assert np.array_equal(acc.accspmm_reorder(A.M, A.rowptr, A.colidx).astype(np.int64), perm)
+    pS = orr.reorder(S.M, S.K, S.rowptr, S.colidx, edge_cap=orr.EDGE_CAP)
+    inv = np.empty_like(pS)
+    inv[pS] = np.arange(S.M)
+    R = gen.csr_from_pairs(inv[S.row_ids()], S.colidx.astype(np.int64), S.M, S.M)
+    assert bt.encode(R.M, R.K, R.rowptr, R.colidx)["NB"] < bt.encode(S.M, S.K, S.rowptr, S.colidx)["NB"]
 
 
 @pytest.mark.parametrize("mode", ["on", "auto"])
@@ -352,3 +416,21 @@ def test_product_library_has_no_measurement_knobs():
     for knob in ("ACCSPMM_KCFG", "ACCSPMM_FW", "ACCSPMM_ROUND_B", "ACCSPMM_L2_PERSIST", "ACCSPMM_L2PROMO",
                  "ACCSPMM_SLICE_MAJOR", "ACCSPMM_GROUP_CAP"):
         assert knob not in strings, knob
+
+
+def test_library_schedule_equals_hand_written_paper_schedule():
+    """The library's units for unit_cap = 32 on a matrix whose windows hold
+    3, 70, 5, 40, 2, 1, 30, 64, 0, 4 TC blocks equal the units written out by hand in
+    tests/test_oracle_balance.py (row 8w of window w has 8*nb consecutive columns)."""
+    from test_oracle_balance import HAND_RWO, HAND_UNITS
+    blocks = np.diff(HAND_RWO)
+    rows, cols = [], []
+    for w, nb in enumerate(blocks):
+        for c in range(8 * int(nb)):
+            rows.append(8 * w)
+            cols.append(c)
+    A = gen.csr_from_pairs(np.array(rows), np.array(cols), 8 * len(blocks), 8 * int(blocks.max()))
+    p = host_plan(A, np.ones(A.nnz, np.float32), balance="on", unit_cap=32)
+    assert p.export_format()["RowWindowOffset"].tolist() == HAND_RWO
+    assert p.info["ibd"] == pytest.approx(23.28, abs=1e-12) and p.info["balanced"] == 1
+    assert [tuple(int(x) for x in u) for u in p.export_units()] == HAND_UNITS

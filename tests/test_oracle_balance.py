@@ -116,3 +116,37 @@ def test_grouped_schedule_keeps_windows_whole(seed, cap, precision):
     # with no window above the cap, grouping equals the balanced schedule (nothing to split)
     small = np.concatenate([[0], np.cumsum(np.minimum(nb, cap))])
     assert ob.build_units(small, cap, False, precision, group=True) == ob.build_units(small, cap, True, precision)
+
+
+# Paper-literal schedule, written out by hand (TC blocks redistributed so that
+# TBs take "nearly uniform computation time", "a maximum threshold of 32 TC blocks per TB";
+# the split of a long window is even and its segments are reduced by the cross-row
+# write-back of P:404; short windows are concatenated, reading R7 / SURVEY Q16).
+# Blocks per window: 3, 70, 5, 40, 2, 1, 30, 64, 0, 4 -> rwo below.  IBD by hand: avg 21.9,
+# |dev| = 18.9+48.1+16.9+18.1+19.9+20.9+8.1+42.1+21.9+17.9 = 232.8 -> 23.28 > 8.
+# Units (w0, nw, b0, b1, split_id, seg, nseg, slot), cap 32, TF32 (C write-back = 1 block):
+#   w0 (3 blocks) alone: the next window is split;
+#   w1 (70 > 32) -> ceil(70/32) = 3 even segments at 3 + floor(70k/3): [3,26) [26,49) [49,73);
+#   w2 (5) alone; w3 (40) -> 2 segments [78,98) [98,118);
+#   w4 + w5 (2+1 blocks, cost (2+1)+(1+1) = 5 <= 33); w6 (30) would make 5+31 = 36 > 33 -> alone;
+#   w7 (64) -> 2 segments [151,183) [183,215); w8 (empty) + w9 (4): cost 1+5 = 6.
+HAND_RWO = [0, 3, 73, 78, 118, 120, 121, 151, 215, 215, 219]
+NS = ob.NO_SPLIT
+HAND_UNITS = [
+    (0, 1, 0, 3, NS, 0, 1, 0),
+    (1, 1, 3, 26, 0, 0, 3, 0), (1, 1, 26, 49, 0, 1, 3, 1), (1, 1, 49, 73, 0, 2, 3, 2),
+    (2, 1, 73, 78, NS, 0, 1, 0),
+    (3, 1, 78, 98, 1, 0, 2, 3), (3, 1, 98, 118, 1, 1, 2, 4),
+    (4, 2, 118, 121, NS, 0, 1, 0),
+    (6, 1, 121, 151, NS, 0, 1, 0),
+    (7, 1, 151, 183, 2, 0, 2, 5), (7, 1, 183, 215, 2, 1, 2, 6),
+    (8, 2, 215, 219, NS, 0, 1, 0),
+]
+
+
+def test_paper_literal_cap32_schedule_by_hand():
+    blocks = np.diff(HAND_RWO)
+    assert ob.ibd(blocks) == pytest.approx(23.28, abs=1e-12)
+    units = ob.build_units(HAND_RWO, ob.PAPER_CAP, True, "tf32")
+    assert units == HAND_UNITS
+    assert max(b1 - b0 for (_, _, b0, b1, *_r) in units) <= 32
