@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU time of the oracle sample")
     ap.add_argument("--profile", action="store_true", help="minimal run for ncu: warmup + steps, no extras")
+    ap.add_argument("--no-ncu", action="store_true", help="skip the in-job ncu capture of the DRAM traffic")
+    ap.add_argument("--ncu-timeout", type=float, default=300.0)
+    ap.add_argument("--ncu-child", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--json-out", default=None)
     return ap.parse_args()
 
@@ -67,65 +70,170 @@ def load_peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def load_traffic(key):
-    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(p):
-        with open(p) as f:
-            d = json.load(f)
-        return d.get(key)
-    return None
-
-
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clock and clock-event (throttle) reasons of the bench GPU sampled through NVML every
+    5 ms during the timed region, plus one sample right before and one right after it, so even
+    a 50 ms region carries its own record (the recipe's nvidia-smi clocks line, B200_PROFILING.md)."""
+    PERIOD_S = 0.005
 
     def __init__(self, device_index: int):
         self.dev = device_index
-        self.proc = None
-        self.lines = []
+        self.samples = []
+        self.h = None
+        self.nv = None
+        self.error = None
+        try:
+            import pynvml as nv
+            import torch
+            nv.nvmlInit()
+            prop = torch.cuda.get_device_properties(device_index)
+            bus = "%08X:%02X:%02X.0" % (prop.pci_domain_id, prop.pci_bus_id, prop.pci_device_id)
+            self.h = nv.nvmlDeviceGetHandleByPciBusId(bus)
+            self.nv = nv
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+        except Exception as e:  # reported in the record, never fatal
+            self.error = repr(e)[:200]
+
+    def _sample(self):
+        nv = self.nv
+        try:
+            self.samples.append((nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM),
+                                 nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)))
+        except Exception as e:
+            self.error = repr(e)[:200]
+
+    def _run(self):
+        while not self.stop_flag.is_set():
+            self._sample()
+            time.sleep(self.PERIOD_S)
 
     def start(self):
-        try:
-            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                                          "-i", str(self.dev), "-lms", "200"], stdout=subprocess.PIPE,
-                                         stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-        except Exception:
-            self.proc = None
-
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+        if self.h is None:
+            return
+        self.stop_flag = threading.Event()
+        self._sample()
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
 
     def stop(self):
-        if not self.proc:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:
-            self.proc.kill()
+        if self.h is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0,
+                    "error": self.error or "NVML unavailable"}
+        self.stop_flag.set()
         self.t.join(timeout=2)
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [x.strip() for x in ln.split(",")]
-            if len(parts) < 9:
-                continue
+        self._sample()
+        nv = self.nv
+        bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+                "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap,
+                "hw_power_brake_slowdown": nv.nvmlClocksEventReasonHwPowerBrakeSlowdown}
+        reasons = sorted({n for _, r in self.samples for n, b in bits.items() if r & b})
+        sm = [float(c) for c, _ in self.samples]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": float(self.max_mhz),
+                "sm_mhz_min": min(sm) if sm else None, "reasons": reasons, "samples": len(sm),
+                "source": "NVML, every 5 ms + before/after the timed loop"}
+
+
+NCU = "/usr/local/cuda/bin/ncu"
+NCU_METRICS = ("dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_sectors_srcunit_tex_op_read.sum",
+               "gpu__time_duration.sum")
+
+
+def ncu_traffic(args, world):
+    """DRAM / L2 traffic of one SpMM launch of THIS workload, captured in this job: a child
+    bench process (same matrix, plan options, N) runs under ncu, which profiles its 3rd SpMM
+    launch (cache-control all: caches flushed before the launch, as in the timed loop).
+    Returns bytes per launch, or {"unavailable": why}."""
+    if not os.path.exists(NCU):
+        return {"unavailable": "ncu not found"}
+    cmd = [NCU, "--metrics", ",".join(NCU_METRICS), "--clock-control", "none", "--print-units", "base",
+           "-k", "regex:spmm_", "-s", "2", "-c", "1", "--csv",
+           sys.executable, os.path.abspath(__file__), "--ncu-child", "--config", args.config, "--N", str(args.N),
+           "--precision", args.precision, "--reorder", args.reorder, "--balance", args.balance,
+           "--unit-cap", str(args.unit_cap), "--build", args.build]
+    if args.permute_cols:
+        cmd.append("--permute-cols")
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK=os.environ.get("LOCAL_RANK", "0"))
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=args.ncu_timeout, env=env)
+    except Exception as e:
+        return {"unavailable": repr(e)[:200]}
+    import csv
+    import io
+    vals = {}
+    kernel = None
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith('"')]
+    for row in csv.DictReader(io.StringIO("\n".join(lines))):
+        name = row.get("Metric Name")
+        if name in NCU_METRICS:
             try:
-                sm.append(float(parts[1]))
-                mx.append(float(parts[2]))
+                vals[name] = float(row["Metric Value"].replace(",", ""))
+                kernel = row.get("Kernel Name", kernel)
             except ValueError:
-                continue
-            for n, v in zip(names, parts[5:9]):
-                if v.lower() == "active":
-                    reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                pass
+    if "dram__bytes_read.sum" not in vals:
+        return {"unavailable": f"ncu rc={r.returncode}: " + (r.stderr or r.stdout)[-300:]}
+    out = {"dram_bytes": vals["dram__bytes_read.sum"] + vals.get("dram__bytes_write.sum", 0.0),
+           "dram_read_bytes": vals["dram__bytes_read.sum"], "dram_write_bytes": vals.get("dram__bytes_write.sum"),
+           "l2_tex_read_bytes": 32.0 * vals["lts__t_sectors_srcunit_tex_op_read.sum"]
+           if "lts__t_sectors_srcunit_tex_op_read.sum" in vals else None,
+           "ncu_kernel_ns": vals.get("gpu__time_duration.sum"), "kernel": (kernel or "")[:120],
+           "how": "ncu --metrics " + ",".join(NCU_METRICS) + " on the 3rd SpMM launch of a child run of this "
+                  "workload in this job (cache-control all = cold L2, like the flushed timed loop)"}
+    return out
+
+
+def run_ncu_child(args):
+    """--ncu-child: build the same plan and execute it 3 times (ncu captures the 3rd launch)."""
+    import torch
+
+    import paper_2501_09251_b200 as acc
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    cfg, A, vals, B = make_inputs(args)
+    plan = acc.Plan(A.M, A.K, A.rowptr, A.colidx, vals, precision=args.precision, reorder=args.reorder,
+                    balance=args.balance, unit_cap=args.unit_cap, device=torch.cuda.current_device(),
+                    permute_cols=args.permute_cols, build=args.build)
+    Bd = torch.from_numpy(B).to(device="cuda", dtype=torch.float16 if args.precision == "fp16" else torch.float32)
+    C = torch.empty((plan.out_rows, args.N), dtype=torch.float32, device="cuda")
+    for _ in range(3):
+        plan.execute(Bd, C)
+    torch.cuda.synchronize()
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def single_thread_baselines(seconds: float = 2.0) -> dict:
+    """the oracle on ONE host thread for configs T (tiny, whole) and S (stencil,
+    bounded row sample), GFLOP/s = 2*nnz*N/t."""
+    import gen
+    from oracle import spmm as osp
+    from oracle.rounding import rho
+    out = {}
+    for name, N in (("tiny", 16), ("stencil", 128)):
+        cfg, A = gen.make_config(name)
+        a = rho(gen.values_uniform(A.nnz, cfg.seed_A + 1), "tf32")
+        b = rho(gen.dense_normal(A.K, N, cfg.seed_B), "tf32")
+        nnz_row = np.diff(A.rowptr)
+        rng = np.random.default_rng(0)
+        rows = np.sort(rng.choice(A.M, size=min(A.M, 2048), replace=False))
+        _, t = osp.timed_spmm(A.M, A.K, A.rowptr, A.colidx, a, b, rows=rows, nthreads=1)
+        rate = 2.0 * nnz_row[rows].sum() * N / max(t, 1e-9)
+        n = int(min(A.M, max(2048, rate * seconds / max(2.0 * nnz_row.mean() * N, 1.0))))
+        rows = np.arange(A.M) if n >= A.M else np.sort(rng.choice(A.M, size=n, replace=False))
+        _, t = osp.timed_spmm(A.M, A.K, A.rowptr, A.colidx, a, b, rows=rows, nthreads=1)
+        out[name] = {"value": 2.0 * nnz_row[rows].sum() * N / t / 1e9, "unit": "GFLOP/s", "N": N,
+                     "rows": int(rows.size), "of_rows": int(A.M), "seconds": t}
+    return out
 
 
 def make_inputs(args):
@@ -180,7 +288,7 @@ def run_reference(args, rank, world):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(args, cfg, A, world),
         "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": info["cores"], "kind": "oracle",
-                         "sample": info["sample"]},
+                         "sample": info["sample"], "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     emit(out, args)
@@ -195,13 +303,9 @@ def workload_config(args, cfg, A, world):
             "parallelism": f"rowwindow-nnz-partition x{world}"}
 
 
-def kernel_name(args):
-    """The SpMM kernel flavour the library's default dispatch picks."""
-    kcfg = int(os.environ.get("ACCSPMM_KCFG", "-1"))
-    g4 = kcfg < 0 or kcfg >= 20
-    if not g4:
-        return "spmm_bittcf_kernel (register-direct gather)"
-    return "spmm_bittcf_g4_kernel (TMA gather4, " + ("1 warp/CTA)" if kcfg < 0 else "variant %d)" % kcfg)
+def kernel_name(plan):
+    """The SpMM kernel the library's dispatch picks for this plan."""
+    return "spmm_bittcf_g4_kernel (TMA gather4 + mma.sync, 1 warp/CTA)"
 
 
 def emit(out, args):
@@ -254,6 +358,9 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         run_reference(args, rank, world)
+        return
+    if args.ncu_child:
+        run_ncu_child(args)
         return
     import torch
     import torch.distributed as dist
@@ -362,12 +469,36 @@ def main():
     es_b = 2 if args.precision == "fp16" else 4
     bm["B_compulsory"] = int(es_b * args.N * np.count_nonzero(np.bincount(A.colidx, minlength=A.K)))
     avg_s = float(np.mean(kernel_ms)) / 1e3 if len(kernel_ms) else t_local / args.steps
-    peak, peak_kind = load_peaks()
-    achieved = bm["total"] / avg_s / 1e9
-    traffic = load_traffic(f"{args.config}-N{args.N}-{args.precision}-{args.reorder}-{args.balance}-p{world}")
+    hbm_peak, peak_kind = load_peaks()
+    model_gbs = bm["total"] / avg_s / 1e9
     # L2 roofline: every model byte (gathered B rows, A stream, C) passes through L2, and on
-    # graphs whose B fits L2 the gather is served from there -- the binding resource
-    l2_peak = max(acc.accspmm_probe_l2_bandwidth(96 << 20, 100), l2_peak_before)
+    # graphs whose B fits L2 the gather is served from there
+    l2_peak_after = acc.accspmm_probe_l2_bandwidth(96 << 20, 100)
+    l2_peak = max(l2_peak_after, l2_peak_before)
+    # HBM roofline: the DRAM bytes ncu counts for one launch of this workload, captured in
+    # this job, over the same in-library launch time
+    if rank == 0 and world == 1 and not args.no_ncu:
+        traffic = ncu_traffic(args, world)
+    else:
+        traffic = {"unavailable": "--no-ncu" if args.no_ncu else "captured on single-GPU runs only (ncu replays "
+                   "kernels; never under a multi-rank command)"}
+    l2 = {"achieved": model_gbs, "peak": l2_peak, "unit": "GB/s", "frac": model_gbs / l2_peak,
+          "achieved_is": "stated bytes model (SURVEY §8(d): A_fmt + es*N*sum_w|U_w| + C) / SpMM launch time",
+          "peak_kind": "measured live in this job by accspmm_probe_l2_bandwidth (96 MiB L2-resident buffer, "
+                       "ld.global.cg from every SM, best of 4 launch shapes; max of before/after the timed loop)",
+          "peak_before": l2_peak_before, "peak_after": l2_peak_after}
+    hbm = None
+    if "dram_bytes" in traffic:
+        dram_gbs = traffic["dram_bytes"] / avg_s / 1e9
+        compulsory = bm["A_fmt"] + bm["B_compulsory"] + bm["C"]
+        hbm = {"achieved": dram_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": dram_gbs / hbm_peak,
+               "peak_kind": peak_kind + " (MEASURED_PEAKS.json hbm_gbs, copy bandwidth)",
+               "achieved_is": "ncu dram__bytes_read+write of one launch (this job) / SpMM launch time",
+               "bytes_per_launch": traffic["dram_bytes"], "compulsory_bytes": compulsory,
+               "bytes_over_compulsory": traffic["dram_bytes"] / max(compulsory, 1)}
+    # the binding resource is the one closer to its peak
+    bound = "hbm" if hbm is not None and hbm["frac"] > l2["frac"] else "l2"
+    rec = hbm if bound == "hbm" else l2
 
     # ---- end to end through the public API with pinned host buffers (H2D B + execute + D2H C)
     # Every step copies its own B from pinned host memory and its C back (separate host buffers
@@ -418,6 +549,8 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu, _ = cpu_oracle_sample(A, vals, B, args.precision, args.cpu_seconds)
+        cpu["cpu_model"] = cpu_model()
+        cpu["single_thread"] = single_thread_baselines()
 
     if rank == 0:
         out = {
@@ -425,14 +558,12 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
             "config": workload_config(args, cfg, A, world),
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                         "bytes_model_per_launch": bm, "frac_of_8TBps_spec": achieved / 8000.0,
-                         "kernel": kernel_name(args), "launch_ms": avg_s * 1e3,
-                         "kernel_share_of_step": avg_s * args.steps / t_local,
-                         "l2": {"achieved": achieved, "peak": l2_peak, "unit": "GB/s", "frac": achieved / l2_peak,
-                                "peak_kind": "measured live: accspmm_probe_l2_bandwidth (96 MiB, ld.global.cg, best "
-                                             "of 4 launch shapes, before and after the timed loop)"}},
+            "roofline": {"bound": bound, "achieved": rec["achieved"], "peak": rec["peak"], "unit": "GB/s",
+                         "frac": rec["frac"], "traffic": traffic.get("dram_bytes"), "traffic_detail": traffic,
+                         "l2": l2, "hbm": hbm, "bytes_model_per_launch": bm,
+                         "model_bytes_over_hbm_peak": model_gbs / hbm_peak,
+                         "kernel": kernel_name(plan), "launch_ms": avg_s * 1e3,
+                         "kernel_share_of_step": avg_s * args.steps / t_local},
             "cpu_baseline": cpu,
             "clocks": clk,
             "e2e": e2e,
