@@ -89,8 +89,20 @@ typedef struct {
                              it too (A' = P A P^T); every execute then gathers
                              B' = P B on the device before the SpMM (fused with the TF32 rounding
                              pass).  C is unchanged.  Default 0 (rows only, reading Q12).          */
-    int32_t reserved[7];
+    int32_t window_rows;  /* rows per RowWindow: 0 or 8 = the paper's BitTCF (8x8 tiles);
+                             16 or 32 = tall windows (reading R20: wh x 8 tiles, wh/8 u64 occupancy
+                             words per block) -- TF32 only, executed by the tcgen05 kernel.       */
+    int32_t kernel;       /* accspmm_kernel: which SpMM kernel executes the plan (default AUTO)   */
+    int32_t reserved[5];
 } accspmm_options;
+
+typedef enum {
+    ACCSPMM_KERNEL_AUTO = 0,     /* 8-row windows: mma.sync kernel; tall windows: tcgen05 kernel        */
+    ACCSPMM_KERNEL_MMA_SYNC = 1, /* TMA gather4 + warp-level mma.sync (8-row windows only)              */
+    ACCSPMM_KERNEL_TCGEN05 = 2   /* TMA gather4 + tcgen05.mma with the gathered rows in TMEM, FP32
+                                    accumulators in TMEM (TF32; any window height; N % 128 == 0 natively,
+                                    other N through the padded path)                                  */
+} accspmm_kernel;
 
 typedef struct {
     int64_t M, K, nnz;          /* the input matrix                                                 */
@@ -115,7 +127,9 @@ typedef struct {
     int64_t cols_permuted;      /* 1: columns relabelled with the row permutation (permute_cols)      */
     int64_t group_cap;          /* concatenation limit of short windows (blocks): min(cap, 32) for grouped
                                    plans under the automatic cap, else = unit_cap                    */
-    int64_t reserved[5];
+    int64_t window_rows;        /* rows per RowWindow of this plan (8 = the paper's BitTCF)           */
+    int64_t kernel;             /* accspmm_kernel the plan executes with (resolved, never AUTO)       */
+    int64_t reserved[3];
 } accspmm_plan_info;
 
 /* Fills *opt with the defaults listed above.  Never fails for a non-null opt. */
@@ -192,7 +206,8 @@ void accspmm_plan_destroy(accspmm_plan *plan);
 accspmm_status accspmm_plan_get_info(const accspmm_plan *plan, accspmm_plan_info *info);
 
 /* Copies the plan's BitTCF arrays to HOST buffers sized from accspmm_plan_info:
- * rwo u32[W+1], tco u32[NB+1], a2b u32[8*NB], bits u64[NB], vals (float32[plan_nnz]
+ * rwo u32[W+1], tco u32[NB+1], a2b u32[8*NB], bits u64[NB * window_rows/8] (window_rows/8
+ * words per block; one for the paper's 8-row windows), vals (float32[plan_nnz]
  * for TF32, uint16 bit patterns for FP16).  Any pointer may be NULL (skipped).
  * Window/block offsets are relative to this plan's slab.  Blocks the host thread. */
 accspmm_status accspmm_plan_export_format(const accspmm_plan *plan, uint32_t *rwo, uint32_t *tco, uint32_t *a2b,
@@ -218,7 +233,7 @@ accspmm_status accspmm_csr_transpose(int64_t M, int64_t K, const int64_t *rowptr
                                     const float *vals, int64_t *t_rowptr, int32_t *t_colidx, float *t_vals);
 
 /* nnz-balanced partition bounds (host): bounds int64[nparts+1] over the
- * ceil(M/8) windows of the given CSR (already in the order to be partitioned). */
+ * ceil(M/8) 8-row windows of the given CSR (already in the order to be partitioned). */
 accspmm_status accspmm_partition_bounds(int64_t M, const int64_t *rowptr, int32_t nparts, int64_t *bounds);
 
 /* Kernel timing (measurement hook).  While enabled, every execute records CUDA
@@ -237,8 +252,8 @@ accspmm_status accspmm_unpermute(const float *G, const uint32_t *orig_row, int64
 
 /* Test hooks (device).  accspmm_debug_round_tf32: out[i] = cvt.rna.tf32.f32(in[i])
  * -- the instruction the kernel applies to B.  accspmm_debug_decode: tiles
- * float32[NB][64], tile[b][r*8+c] = value of (row r, lane c) of TC block b or 0,
- * decoded on the device with the kernel's popcount rule. */
+ * float32[NB][8*wh] (wh = window_rows), tile[b][r*8+c] = value of (row r, lane c) of TC
+ * block b or 0, decoded on the device with the kernel's popcount rule. */
 accspmm_status accspmm_debug_round_tf32(const float *in, float *out, int64_t n, void *stream);
 accspmm_status accspmm_debug_decode(const accspmm_plan *plan, float *tiles, void *stream);
 

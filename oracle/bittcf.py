@@ -15,6 +15,13 @@ Readings where the paper is silent: bit k = r*8 + c, LSB = 0
 row-major, c = condensed lane (Q3); condensed columns ascending (Q4); padding
 lanes store 0 (Q5); values by ascending bit (Q6); blocks may hold 1..64 nnz
 (Q8); a ragged last window contributes no bits for missing rows (Q22).
+
+Window height ``wh`` (reading R20; default 8 = the paper's format): the
+same construction with windows of wh = 16 or 32 rows, i.e. wh x 8 tiles.  A block's
+occupancy is wh/8 u64 words, word j covering tile rows 8j..8j+7 with the paper's bit rule
+inside (bit (r mod 8)*8 + c); TCLocalBit holds the words block-major (NB*wh/8 entries);
+values ascend by tile position p = r*8 + c, so a value's index is TCOffset[b] + the
+popcount of the block's occupancy below p -- P:273 over the concatenated words.
 """
 from __future__ import annotations
 
@@ -23,17 +30,21 @@ import numpy as np
 WINDOW = 8  # P:250 "8 x 8 TC blocks", "ceil(M/8)+1 elements"
 
 
-def encode(M: int, K: int, rowptr, colidx, vals=None) -> dict:
-    """Steps 1-7 of SURVEY §8(c) C-2 "BitTCF (independent Python encoder)", vectorised."""
+def encode(M: int, K: int, rowptr, colidx, vals=None, wh: int = WINDOW) -> dict:
+    """Steps 1-7 of SURVEY §8(c) C-2 "BitTCF (independent Python encoder)", vectorised;
+    ``wh`` = rows per window (8 = the paper's; 16 / 32 = reading R20)."""
+    if wh not in (8, 16, 32):
+        raise ValueError("window height must be 8, 16 or 32")
+    nw = wh // WINDOW
     rowptr = np.asarray(rowptr, dtype=np.int64)
     colidx = np.asarray(colidx, dtype=np.int64)
     nnz = int(rowptr[-1]) if M > 0 else 0
-    # 1. W = ceil(M/8)
-    W = (M + WINDOW - 1) // WINDOW
-    # 2. window rows [8w, min(8w+8, M)): window and local row of every nnz
+    # 1. W = ceil(M/wh)
+    W = (M + wh - 1) // wh
+    # 2. window rows [wh*w, min(wh*w+wh, M)): window and local row of every nnz
     rows = np.repeat(np.arange(M, dtype=np.int64), np.diff(rowptr))
-    w_of = rows // WINDOW
-    r_of = rows % WINDOW
+    w_of = rows // wh
+    r_of = rows % wh
     # 3. U_w = sorted unique columns of the window's rows
     keys = w_of * np.int64(max(K, 1)) + colidx
     uniq, inverse = np.unique(keys, return_inverse=True)
@@ -53,21 +64,21 @@ def encode(M: int, K: int, rowptr, colidx, vals=None) -> dict:
     lane = rank % WINDOW
     a2b = np.zeros(WINDOW * NB, dtype=np.uint32)
     a2b[WINDOW * gblock + lane] = ucol.astype(np.uint32)
-    # 5. bit k = r*8 + lane of every nnz, in block gblock
+    # 5. tile position p = r*8 + lane of every nnz, in block gblock: word p // 64, bit p % 64
     nb_of = gblock[inverse]
-    bit_of = r_of * WINDOW + lane[inverse]
-    # 6. values of a block in ascending bit order
-    order = np.lexsort((bit_of, nb_of))
-    sb, sk = nb_of[order], bit_of[order]
-    bits = np.zeros(NB, dtype=np.uint64)
+    pos_of = r_of * WINDOW + lane[inverse]
+    # 6. values of a block in ascending tile position
+    order = np.lexsort((pos_of, nb_of))
+    sb, sp = nb_of[order], pos_of[order]
+    bits = np.zeros(NB * nw, dtype=np.uint64)
     counts = np.bincount(sb, minlength=NB).astype(np.int64) if NB > 0 else np.zeros(0, np.int64)
     tco = np.zeros(NB + 1, dtype=np.int64)
     np.cumsum(counts, out=tco[1:])
     if nnz > 0:
-        onehot = np.left_shift(np.uint64(1), sk.astype(np.uint64))
-        bits[:] = np.bitwise_or.reduceat(onehot, tco[:-1])
+        onehot = np.left_shift(np.uint64(1), (sp % 64).astype(np.uint64))
+        np.bitwise_or.at(bits, sb * nw + sp // 64, onehot)
     out = {
-        "M": M, "K": K, "nnz": nnz, "W": W, "NB": NB,
+        "M": M, "K": K, "nnz": nnz, "W": W, "NB": NB, "wh": wh,
         "RowWindowOffset": rwo.astype(np.uint32),
         "TCOffset": tco.astype(np.uint32),       # 7. popcount prefix sums
         "SparseAToB": a2b,
@@ -84,22 +95,26 @@ def decode(fmt: dict):
 
     Returns canonical CSR (rowptr int64, colidx int32, values or None)."""
     M, K = fmt["M"], fmt["K"]
+    wh = fmt.get("wh", WINDOW)
+    nw = wh // WINDOW
     rwo = fmt["RowWindowOffset"].astype(np.int64)
     tco = fmt["TCOffset"].astype(np.int64)
     a2b = fmt["SparseAToB"].astype(np.int64)
-    bits = fmt["TCLocalBit"].astype(np.uint64)
-    NB = bits.size
-    if np.any(tco[1:] - tco[:-1] != np.bitwise_count(bits)):
+    words = fmt["TCLocalBit"].astype(np.uint64).reshape(-1, nw)   # [NB][wh/8]
+    NB = words.shape[0]
+    if np.any(tco[1:] - tco[:-1] != np.bitwise_count(words).sum(axis=1)):
         raise ValueError("BitTCF corruption: TCOffset step != popcount(TCLocalBit)")
     win_of_block = np.searchsorted(rwo, np.arange(NB), side="right") - 1
     ks = np.arange(64, dtype=np.uint64)
-    present = ((bits[:, None] >> ks[None, :]) & np.uint64(1)).astype(bool)
-    b_idx, k_idx = np.nonzero(present)
-    below = bits[b_idx] & ((np.uint64(1) << k_idx.astype(np.uint64)) - np.uint64(1))
-    vidx = tco[b_idx] + np.bitwise_count(below).astype(np.int64)
-    r = k_idx // WINDOW
-    lane = k_idx % WINDOW
-    row = win_of_block[b_idx] * WINDOW + r
+    # present[b, p] for tile positions p = 64*word + bit
+    present = ((words[:, :, None] >> ks[None, None, :]) & np.uint64(1)).astype(bool).reshape(NB, 64 * nw)
+    b_idx, p_idx = np.nonzero(present)
+    # P:273: index = TCOffset[b] + occupancy of block b below position p
+    before = np.cumsum(present, axis=1) - present
+    vidx = tco[b_idx] + before[b_idx, p_idx].astype(np.int64)
+    r = p_idx // WINDOW
+    lane = p_idx % WINDOW
+    row = win_of_block[b_idx] * wh + r
     col = a2b[WINDOW * b_idx + lane]
     if np.any(row >= M) or np.any(col >= K):
         raise ValueError("BitTCF corruption: position out of range")

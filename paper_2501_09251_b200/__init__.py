@@ -27,6 +27,8 @@ REORDER = {"off": 0, "on": 1, "auto": 2}
 BALANCE = {"off": 0, "on": 1, "auto": 2}
 PRECISION = {"tf32": TF32, "fp16": FP16}
 BUILD = {"host": 0, "device": 1}
+KERNEL = {"auto": 0, "mma_sync": 1, "tcgen05": 2}
+KERNEL_NAME = {v: k for k, v in KERNEL.items()}
 NO_SPLIT = 0xFFFFFFFF
 
 
@@ -40,7 +42,7 @@ class accspmm_options(ctypes.Structure):
     _fields_ = [("precision", ctypes.c_int32), ("reorder", ctypes.c_int32), ("balance", ctypes.c_int32),
                 ("unit_cap", ctypes.c_int32), ("part", ctypes.c_int32), ("nparts", ctypes.c_int32),
                 ("device", ctypes.c_int32), ("build", ctypes.c_int32), ("permute_cols", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 7)]
+                ("window_rows", ctypes.c_int32), ("kernel", ctypes.c_int32), ("reserved", ctypes.c_int32 * 5)]
 
 
 _I64 = ["M", "K", "nnz", "rows", "row_begin", "window_begin", "W", "NB", "plan_nnz", "sum_U", "n_units",
@@ -56,7 +58,7 @@ class accspmm_plan_info(ctypes.Structure):
                 + [(n, ctypes.c_double) for n in ("ms_validate", "ms_reorder", "ms_build", "ms_schedule",
                                                    "ms_upload")]
                 + [("grouped", ctypes.c_int64), ("cols_permuted", ctypes.c_int64), ("group_cap", ctypes.c_int64),
-                   ("reserved", ctypes.c_int64 * 5)])
+                   ("window_rows", ctypes.c_int64), ("kernel", ctypes.c_int64), ("reserved", ctypes.c_int64 * 3)])
 
     def as_dict(self) -> dict:
         return {n: getattr(self, n) for n, _ in self._fields_ if n != "reserved"}
@@ -199,16 +201,17 @@ def accspmm_plan_get_info(plan) -> dict:
 def accspmm_plan_export_format(plan) -> dict:
     info = accspmm_plan_get_info(plan)
     W, NB, nnz = info["W"], info["NB"], info["plan_nnz"]
+    nw = info["window_rows"] // 8   # occupancy words per block (1 for the paper's 8-row windows)
     rwo = np.empty(W + 1, np.uint32)
     tco = np.empty(NB + 1, np.uint32)
     a2b = np.empty(8 * NB, np.uint32)
-    bits = np.empty(NB, np.uint64)
+    bits = np.empty(NB * nw, np.uint64)
     vals = np.empty(nnz, np.uint16 if info["precision"] == FP16 else np.float32)
     _check(load_library().accspmm_plan_export_format(plan, _ptr(rwo), _ptr(tco), _ptr(a2b), _ptr(bits), _ptr(vals)))
     if info["precision"] == FP16:
         vals = vals.view(np.float16)
     return {"RowWindowOffset": rwo, "TCOffset": tco, "SparseAToB": a2b, "TCLocalBit": bits, "values": vals,
-            "W": W, "NB": NB, "nnz": nnz}
+            "W": W, "NB": NB, "nnz": nnz, "window_rows": info["window_rows"]}
 
 
 def accspmm_plan_export_units(plan) -> np.ndarray:
@@ -327,8 +330,11 @@ class Plan:
     TF32 / float16 for FP16) and returns / fills C (float32)."""
 
     def __init__(self, M, K, rowptr, colidx, vals, precision="tf32", reorder="auto", balance="auto",
-                 unit_cap=0, part=0, nparts=1, device=None, build="host", permute_cols=False):
+                 unit_cap=0, part=0, nparts=1, device=None, build="host", permute_cols=False, window_rows=0,
+                 kernel="auto"):
         opt = accspmm_options_default()
+        opt.window_rows = int(window_rows)
+        opt.kernel = KERNEL[kernel]
         opt.build = BUILD[build]
         opt.permute_cols = int(bool(permute_cols))
         opt.precision = PRECISION[precision]
@@ -452,7 +458,7 @@ class Plan:
 
     def debug_decode(self, stream=None):
         import torch
-        tiles = torch.empty((self.info["NB"], 64), dtype=torch.float32, device="cuda")
+        tiles = torch.empty((self.info["NB"], 8 * self.info["window_rows"]), dtype=torch.float32, device="cuda")
         accspmm_debug_decode(self.handle, tiles.data_ptr(), _stream_ptr(stream))
         return tiles
 
@@ -462,7 +468,8 @@ def bytes_model(info: dict, N: int) -> dict:
     es_a = 2 if info["precision"] == FP16 else 4
     es_b = es_a
     W, NB = info["W"], info["NB"]
-    a_fmt = (4 * (W + 1) + 4 * (NB + 1) + 32 * NB + 8 * NB + es_a * info["plan_nnz"]
+    nw = info.get("window_rows", 8) // 8   # u64 occupancy words per block
+    a_fmt = (4 * (W + 1) + 4 * (NB + 1) + 32 * NB + 8 * nw * NB + es_a * info["plan_nnz"]
              + 32 * info["n_units"] + (4 * info["rows"] if info["perm_present"] and info["nparts"] == 1 else 0))
     b_model = es_b * N * info["sum_U"]
     c = 4 * info["rows"] * N

@@ -194,6 +194,17 @@ accspmm_status accspmm_plan_create_ex(int64_t M, int64_t K, const int64_t *rowpt
         return fail(ACCSPMM_ERR_INVALID_VALUE, "unknown build mode");
     if (opt.build == ACCSPMM_BUILD_DEVICE && opt.device < 0)
         return fail(ACCSPMM_ERR_UNSUPPORTED, "device build needs a device (device >= 0)");
+    // window height (reading R20): 8 = the paper's BitTCF; 16 / 32 = tall windows (tcgen05 kernel)
+    const int wh = opt.window_rows == 0 ? kWindow : opt.window_rows;
+    if (wh != 8 && wh != 16 && wh != 32) return fail(ACCSPMM_ERR_INVALID_VALUE, "window_rows must be 0, 8, 16 or 32");
+    if (opt.kernel < ACCSPMM_KERNEL_AUTO || opt.kernel > ACCSPMM_KERNEL_TCGEN05)
+        return fail(ACCSPMM_ERR_INVALID_VALUE, "unknown kernel");
+    if (wh > kWindow && opt.kernel == ACCSPMM_KERNEL_MMA_SYNC)
+        return fail(ACCSPMM_ERR_UNSUPPORTED, "the mma.sync kernel runs 8-row windows only");
+    const int kernel = (wh > kWindow || opt.kernel == ACCSPMM_KERNEL_TCGEN05) ? ACCSPMM_KERNEL_TCGEN05
+                                                                           : ACCSPMM_KERNEL_MMA_SYNC;
+    if (kernel == ACCSPMM_KERNEL_TCGEN05 && opt.precision != ACCSPMM_TF32)
+        return fail(ACCSPMM_ERR_UNSUPPORTED, "the tcgen05 kernel (and tall windows) is TF32 only");
     if (M < 0 || K < 0) return fail(ACCSPMM_ERR_INVALID_VALUE, "negative matrix dimension");
     if (M >= (int64_t)UINT32_MAX || K >= (int64_t)INT32_MAX)
         return fail(ACCSPMM_ERR_UNSUPPORTED, "M or K too large for 32-bit indices");
@@ -228,8 +239,8 @@ accspmm_status accspmm_plan_create_ex(int64_t M, int64_t K, const int64_t *rowpt
             return fail(ACCSPMM_ERR_OUT_OF_MEMORY, "reordering");
         }
         if (opt.reorder == ACCSPMM_REORDER_AUTO) {
-            int64_t nb0 = count_blocks(a, {});
-            int64_t nb1 = count_blocks(a, perm);
+            int64_t nb0 = count_blocks(a, {}, wh);
+            int64_t nb1 = count_blocks(a, perm, wh);
             I.nb_unreordered = nb0;
             if (nb1 >= nb0) perm.clear();
         }
@@ -239,13 +250,13 @@ accspmm_status accspmm_plan_create_ex(int64_t M, int64_t K, const int64_t *rowpt
 
     // ---- partition + BitTCF build ----
     t0 = std::chrono::steady_clock::now();
-    int64_t wb0 = 0, wb1 = (M + kWindow - 1) / kWindow;
+    int64_t wb0 = 0, wb1 = (M + wh - 1) / wh;
     if (opt.nparts > 1) {
-        std::vector<int64_t> b = partition_bounds(a, perm, opt.nparts);
+        std::vector<int64_t> b = partition_bounds(a, perm, opt.nparts, wh);
         wb0 = b[(size_t)opt.part];
         wb1 = b[(size_t)opt.part + 1];
     }
-    const int64_t r0 = wb0 * kWindow, r1 = std::min<int64_t>(M, wb1 * kWindow);
+    const int64_t r0 = wb0 * wh, r1 = std::min<int64_t>(M, wb1 * wh);
     // symmetric reordering (NEXT-2): column c becomes inv_perm[c]; B is gathered as B[perm]
     std::vector<uint32_t> colmap;
     if (opt.permute_cols && !perm.empty()) {
@@ -258,20 +269,23 @@ accspmm_status accspmm_plan_create_ex(int64_t M, int64_t K, const int64_t *rowpt
     DeviceFormat DF;
     double ms_csr_upload = 0.0;
     if (opt.build == ACCSPMM_BUILD_DEVICE) {
-        st = build_format_device(a, vals, perm, r0, std::max(r0, r1), opt.precision, DF, cm);
+        st = build_format_device(a, vals, perm, r0, std::max(r0, r1), opt.precision, DF, cm, wh);
         if (st != ACCSPMM_OK) { free_device_format(DF); delete p; return st; }
         F.W = DF.W; F.NB = DF.NB; F.nnz = DF.nnz; F.rows = DF.rows; F.sum_U = DF.sum_U;
         F.rwo = DF.rwo_host;
         ms_csr_upload = DF.ms_upload;
     } else {
-        st = build_format(a, vals, perm, r0, std::max(r0, r1), opt.precision, F, cm);
+        st = build_format(a, vals, perm, r0, std::max(r0, r1), opt.precision, F, cm, wh);
         if (st != ACCSPMM_OK) { delete p; return st; }
     }
     if (I.nb_unreordered < 0 && opt.nparts == 1 && perm.empty()) I.nb_unreordered = F.NB;
     I.rows = F.rows; I.row_begin = r0; I.window_begin = wb0;
     I.W = F.W; I.NB = F.NB; I.plan_nnz = F.nnz; I.sum_U = F.sum_U;
     I.mean_nnz_tc = F.NB ? (double)F.nnz / (double)F.NB : 0.0;
-    I.index_bytes = ((F.rows + 7) / 8 + 11 * F.NB + 2) * 4;
+    I.window_rows = wh;
+    I.kernel = kernel;
+    // P:253 for wh = 8; a tall window's block carries wh/8 occupancy words (2 u32 each)
+    I.index_bytes = ((F.rows + wh - 1) / wh + (9 + 2 * (wh / kWindow)) * F.NB + 2) * 4;
     I.metcf_index_bytes = ((F.rows + 7) / 8 + 1 + F.NB + 1 + 8 * F.NB) * 4 + F.nnz;
     I.csr_index_bytes = (F.rows + 1) * 4 + F.nnz * 4;
     I.value_bytes = F.nnz * (opt.precision == ACCSPMM_FP16 ? 2 : 4);
@@ -293,7 +307,7 @@ accspmm_status accspmm_plan_create_ex(int64_t M, int64_t K, const int64_t *rowpt
     // AUTO below the IBD threshold keeps windows whole but groups consecutive ones
     // into a warp's unit (reading R7b); OFF is the paper's one window per unit
     const bool group = !balance && opt.balance == ACCSPMM_BALANCE_AUTO;
-    Schedule S = build_schedule(F.rwo, cap, balance, opt.precision, group, gcap);
+    Schedule S = build_schedule(F.rwo, cap, balance, opt.precision, group, gcap, wh);
     I.ibd = ibd; I.balanced = balance ? 1 : 0; I.unit_cap = cap; I.grouped = group ? 1 : 0; I.group_cap = gcap;
     I.n_units = (int64_t)S.units.size(); I.n_split_windows = S.n_split; I.n_segments = S.n_segments;
     p->units_host.resize(S.units.size() * 8);
@@ -306,13 +320,14 @@ accspmm_status accspmm_plan_create_ex(int64_t M, int64_t K, const int64_t *rowpt
         DevicePlan &d = p->dev;
         d.W = F.W; d.NB = F.NB; d.nnz = F.nnz; d.rows = F.rows; d.n_units = I.n_units;
         d.n_split = S.n_split; d.n_segments = S.n_segments; d.precision = opt.precision; d.K = K;
+        d.wh = wh; d.kernel = kernel;
         int64_t bytes = 0;
         if (opt.build == ACCSPMM_BUILD_DEVICE) {  // format already resident: take ownership
             d.rwo = DF.rwo; d.tco = DF.tco; d.a2b = DF.a2b; d.bits = DF.bits; d.vals = DF.vals;
             DF.rwo = DF.tco = DF.a2b = nullptr; DF.bits = nullptr; DF.vals = nullptr;
             const int64_t es = opt.precision == ACCSPMM_FP16 ? 2 : 4;
-            bytes += 4 * (F.W + 1) + 4 * (F.NB + 1) + 32 * std::max<int64_t>(F.NB, 1) + 8 * std::max<int64_t>(F.NB, 1) +
-                     es * (F.nnz + 16);
+            bytes += 4 * (F.W + 1) + 4 * (F.NB + 1) + 32 * std::max<int64_t>(F.NB, 1) +
+                     8 * (wh / kWindow) * std::max<int64_t>(F.NB, 1) + es * (F.nnz + 16);
         } else {
             st = upload(&d.rwo, F.rwo, bytes);
             if (st == ACCSPMM_OK) st = upload(&d.tco, F.tco, bytes);
@@ -321,9 +336,11 @@ accspmm_status accspmm_plan_create_ex(int64_t M, int64_t K, const int64_t *rowpt
             // device copy: padding lanes (no bit in the block's column-OR) hold 0xFFFFFFFF, an
             // out-of-bounds row the TMA zero-fills; the exported paper format keeps 0
             std::vector<uint32_t> a2b_dev(F.a2b);
+            const int nwords = wh / kWindow;
 #pragma omp parallel for schedule(static)
             for (int64_t b = 0; b < F.NB; ++b) {
-                uint64_t m = F.bits[(size_t)b];
+                uint64_t m = 0;
+                for (int j = 0; j < nwords; ++j) m |= F.bits[(size_t)b * nwords + j];
                 m |= m >> 32;
                 m |= m >> 16;
                 m |= m >> 8;
@@ -349,7 +366,7 @@ accspmm_status accspmm_plan_create_ex(int64_t M, int64_t K, const int64_t *rowpt
         I.device_bytes = bytes;
         // the device holds the format now; drop the host copy
         HostFormat empty;
-        empty.W = F.W; empty.NB = F.NB; empty.nnz = F.nnz; empty.rows = F.rows; empty.sum_U = F.sum_U;
+        empty.W = F.W; empty.NB = F.NB; empty.nnz = F.nnz; empty.rows = F.rows; empty.sum_U = F.sum_U; empty.wh = wh;
         F = std::move(empty);
     }
     I.ms_upload = ms_since(t0) + ms_csr_upload;
@@ -361,8 +378,8 @@ static accspmm_status ensure_workspace(const accspmm_plan *p, int64_t N)
 {
     const auto &d = p->dev;
     if (d.n_split == 0) return ACCSPMM_OK;
-    size_t need_ws = (size_t)d.n_segments * (size_t)N * 8 * sizeof(float);
-    const int64_t fw = pick_fw(N);
+    size_t need_ws = (size_t)d.n_segments * (size_t)N * (size_t)d.wh * sizeof(float);
+    const int64_t fw = d.kernel == ACCSPMM_KERNEL_TCGEN05 ? 128 : pick_fw(N);
     size_t need_cnt = (size_t)d.n_split * (size_t)(N / fw);
     if (need_ws > p->ws_bytes) {
         cudaFree(p->ws);
@@ -390,8 +407,10 @@ static accspmm_status execute_impl(const accspmm_plan *p, const void *B, int64_t
 
 // The feature width the kernels run at: a few wide slices rather than many narrow ones
 // (N = 602 or 608 -> 640 = 5 x 128 instead of 19 x 32; measured 72.9 ms at 608 = 19 x 32).
-static int64_t padded_width(int64_t N)
+// The tcgen05 kernel runs 128-feature slices (UMMA M = 128) only.
+static int64_t padded_width(int64_t N, int kernel)
 {
+    if (kernel == ACCSPMM_KERNEL_TCGEN05) return (N + 127) / 128 * 128;
     return N <= 16 ? 16 : N <= 32 ? 32 : N <= 64 ? 64 : (N + 127) / 128 * 128;
 }
 
@@ -401,7 +420,7 @@ static int64_t padded_width(int64_t N)
 static accspmm_status execute_padded(const accspmm_plan *p, const void *B, int64_t N, void *C, void *stream)
 {
     if (!C || (!B && p->info.K > 0)) return fail(ACCSPMM_ERR_INVALID_VALUE, "B or C is NULL");
-    const int64_t Np = padded_width(N);
+    const int64_t Np = padded_width(N, p->dev.kernel);
     const size_t es = p->opt.precision == ACCSPMM_FP16 ? 2 : 4;
     const int64_t out_rows = p->opt.nparts == 1 ? p->info.M : p->info.rows;
     const size_t needB = (size_t)std::max<int64_t>(p->info.K, 1) * (size_t)Np * es;
@@ -443,7 +462,9 @@ static accspmm_status execute_impl(const accspmm_plan *p, const void *B, int64_t
     if (p->opt.device < 0) return fail(ACCSPMM_ERR_UNSUPPORTED, "host-only plan cannot execute (no CPU fallback)");
     if (N <= 0) return fail(ACCSPMM_ERR_INVALID_VALUE, "N <= 0");
     if (N % 16 != 0 && ndst > 0) return fail(ACCSPMM_ERR_UNSUPPORTED, "fused all-gather needs N % 16 == 0");
-    if (padded_width(N) != N && ndst == 0) {
+    if (ndst > 0 && p->dev.kernel == ACCSPMM_KERNEL_TCGEN05)
+        return fail(ACCSPMM_ERR_UNSUPPORTED, "fused all-gather runs on the mma.sync kernel (8-row windows) only");
+    if (padded_width(N, p->dev.kernel) != N && ndst == 0) {
         if (p->info.rows == 0) return ACCSPMM_OK;
         return execute_padded(p, B, N, C, stream);
     }
@@ -510,7 +531,10 @@ static accspmm_status execute_impl(const accspmm_plan *p, const void *B, int64_t
         cudaGetLastError();
     }
     if (timed) cudaEventRecord(p->ev[p->ev_n], (cudaStream_t)stream);
-    st = launch_spmm(p->dev, Bk, p->zrow, N, (float *)C, p->ws, p->counters, stream, in_kernel_round, dst, ndst);
+    if (p->dev.kernel == ACCSPMM_KERNEL_TCGEN05)
+        st = launch_spmm_tc05(p->dev, Bk, N, (float *)C, p->ws, p->counters, stream, in_kernel_round);
+    else
+        st = launch_spmm(p->dev, Bk, p->zrow, N, (float *)C, p->ws, p->counters, stream, in_kernel_round, dst, ndst);
     if (timed) {
         cudaEventRecord(p->ev[p->ev_n + 1], (cudaStream_t)stream);
         p->ev_n += 2;
@@ -685,7 +709,8 @@ accspmm_status accspmm_plan_export_format(const accspmm_plan *p, uint32_t *rwo, 
             for (size_t q = 0; q < (size_t)I.NB * 8; ++q)
                 if (a2b[q] == kPadLane) a2b[q] = 0u;
     }
-    if (st == ACCSPMM_OK) st = export_array(bits, p->host.bits, dev ? p->dev.bits : nullptr, (size_t)I.NB);
+    if (st == ACCSPMM_OK)
+        st = export_array(bits, p->host.bits, dev ? p->dev.bits : nullptr, (size_t)I.NB * (size_t)(I.window_rows / kWindow));
     if (st == ACCSPMM_OK) {
         if (p->opt.precision == ACCSPMM_FP16)
             st = export_array((uint16_t *)vals, p->host.v16, dev ? (const uint16_t *)p->dev.vals : nullptr,

@@ -10,6 +10,12 @@
 // reverse.  With a column map (symmetric reordering, NEXT-2) columns are relabelled
 // c -> colmap[c] before the window's condensed set is formed.  Windows are
 // independent, so every pass is an OpenMP loop over windows.
+//
+// Window height wh (reading R20): wh = 8 is the paper's format.  wh = 16 / 32
+// are the tall windows of the tcgen05 path: a window of wh rows is condensed the same way
+// into wh x 8 tiles, whose occupancy is wh/8 u64 words per block (word j = tile rows
+// 8j..8j+7, bit (r mod 8)*8 + lane inside the word), values in ascending tile position
+// r*8 + lane -- the P:273 popcount rule applied to the concatenated words.
 #include <algorithm>
 #include <cstring>
 
@@ -44,16 +50,16 @@ inline void window_columns(const Csr &a, const std::vector<uint32_t> &perm, int6
 
 }  // namespace
 
-int64_t count_blocks(const Csr &a, const std::vector<uint32_t> &perm)
+int64_t count_blocks(const Csr &a, const std::vector<uint32_t> &perm, int wh)
 {
-    const int64_t W = (a.M + kWindow - 1) / kWindow;
+    const int64_t W = (a.M + wh - 1) / wh;
     int64_t total = 0;
 #pragma omp parallel reduction(+ : total)
     {
         std::vector<int32_t> buf;
 #pragma omp for schedule(dynamic, 64)
         for (int64_t w = 0; w < W; ++w) {
-            window_columns(a, perm, w * kWindow, std::min<int64_t>(a.M, (w + 1) * kWindow), buf);
+            window_columns(a, perm, w * wh, std::min<int64_t>(a.M, (w + 1) * wh), buf);
             total += ((int64_t)buf.size() + kWindow - 1) / kWindow;
         }
     }
@@ -62,13 +68,15 @@ int64_t count_blocks(const Csr &a, const std::vector<uint32_t> &perm)
 
 accspmm_status build_format(const Csr &a, const float *vals, const std::vector<uint32_t> &perm,
                             int64_t row_begin, int64_t row_end, int precision, HostFormat &out,
-                            const uint32_t *colmap)
+                            const uint32_t *colmap, int wh)
 {
     const int64_t rows = row_end - row_begin;
-    const int64_t W = (rows + kWindow - 1) / kWindow;
+    const int64_t W = (rows + wh - 1) / wh;
+    const int nw = wh / kWindow;  // u64 occupancy words per block
     out = HostFormat();
     out.rows = rows;
     out.W = W;
+    out.wh = wh;
     std::vector<int64_t> U((size_t)W, 0);
     // pass 1: |U_w|
 #pragma omp parallel
@@ -76,7 +84,7 @@ accspmm_status build_format(const Csr &a, const float *vals, const std::vector<u
         std::vector<int32_t> buf;
 #pragma omp for schedule(dynamic, 64)
         for (int64_t w = 0; w < W; ++w) {
-            int64_t r0 = row_begin + w * kWindow, r1 = std::min(row_end, r0 + kWindow);
+            int64_t r0 = row_begin + w * wh, r1 = std::min(row_end, r0 + wh);
             window_columns(a, perm, r0, r1, buf, colmap);
             U[(size_t)w] = (int64_t)buf.size();
         }
@@ -100,7 +108,7 @@ accspmm_status build_format(const Csr &a, const float *vals, const std::vector<u
     try {
         out.rwo.resize((size_t)W + 1);
         out.a2b.assign((size_t)NB * kWindow, 0u);
-        out.bits.assign((size_t)NB, 0ull);
+        out.bits.assign((size_t)NB * nw, 0ull);
         out.tco.resize((size_t)NB + 1);
         if (precision == ACCSPMM_FP16) out.v16.resize((size_t)nnz);
         else out.v32.resize((size_t)nnz);
@@ -114,7 +122,7 @@ accspmm_status build_format(const Csr &a, const float *vals, const std::vector<u
         std::vector<int32_t> buf;
 #pragma omp for schedule(dynamic, 64)
         for (int64_t w = 0; w < W; ++w) {
-            int64_t r0 = row_begin + w * kWindow, r1 = std::min(row_end, r0 + kWindow);
+            int64_t r0 = row_begin + w * wh, r1 = std::min(row_end, r0 + wh);
             window_columns(a, perm, r0, r1, buf, colmap);
             const int64_t base = rwo64[(size_t)w];
             for (size_t q = 0; q < buf.size(); ++q) out.a2b[(size_t)base * kWindow + q] = (uint32_t)buf[q];
@@ -123,22 +131,26 @@ accspmm_status build_format(const Csr &a, const float *vals, const std::vector<u
                 const int lr = (int)(r - r0);
                 for (int64_t p = a.rowptr[o]; p < a.rowptr[o + 1]; ++p) {
                     size_t pos = (size_t)(std::lower_bound(buf.begin(), buf.end(), col_of(colmap, a.colidx[p])) - buf.begin());
-                    out.bits[(size_t)base + pos / kWindow] |= 1ull << (lr * kWindow + (int)(pos % kWindow));
+                    out.bits[((size_t)base + pos / kWindow) * nw + lr / kWindow] |=
+                        1ull << ((lr % kWindow) * kWindow + (int)(pos % kWindow));
                 }
             }
         }
     }
-    // TCOffset = popcount prefix sums
+    // TCOffset = popcount prefix sums (all words of a block)
     out.tco[0] = 0;
-    for (int64_t b = 0; b < NB; ++b)
-        out.tco[(size_t)b + 1] = out.tco[(size_t)b] + (uint32_t)__builtin_popcountll(out.bits[(size_t)b]);
+    for (int64_t b = 0; b < NB; ++b) {
+        uint32_t c = 0;
+        for (int j = 0; j < nw; ++j) c += (uint32_t)__builtin_popcountll(out.bits[(size_t)b * nw + j]);
+        out.tco[(size_t)b + 1] = out.tco[(size_t)b] + c;
+    }
     // pass 3: values, rounded with rho and placed by the popcount rule of P:273
 #pragma omp parallel
     {
         std::vector<int32_t> buf;
 #pragma omp for schedule(dynamic, 64)
         for (int64_t w = 0; w < W; ++w) {
-            int64_t r0 = row_begin + w * kWindow, r1 = std::min(row_end, r0 + kWindow);
+            int64_t r0 = row_begin + w * wh, r1 = std::min(row_end, r0 + wh);
             window_columns(a, perm, r0, r1, buf, colmap);
             const int64_t base = rwo64[(size_t)w];
             for (int64_t r = r0; r < r1; ++r) {
@@ -147,9 +159,12 @@ accspmm_status build_format(const Csr &a, const float *vals, const std::vector<u
                 for (int64_t p = a.rowptr[o]; p < a.rowptr[o + 1]; ++p) {
                     size_t pos = (size_t)(std::lower_bound(buf.begin(), buf.end(), col_of(colmap, a.colidx[p])) - buf.begin());
                     size_t b = (size_t)base + pos / kWindow;
-                    int k = lr * kWindow + (int)(pos % kWindow);
-                    uint64_t below = out.bits[b] & ((1ull << k) - 1ull);
-                    size_t idx = out.tco[b] + (size_t)__builtin_popcountll(below);
+                    const int word = lr / kWindow;
+                    int k = (lr % kWindow) * kWindow + (int)(pos % kWindow);
+                    size_t idx = out.tco[b];
+                    for (int j = 0; j < word; ++j) idx += (size_t)__builtin_popcountll(out.bits[b * nw + j]);
+                    uint64_t below = out.bits[b * nw + word] & ((1ull << k) - 1ull);
+                    idx += (size_t)__builtin_popcountll(below);
                     float v = vals ? vals[p] : 0.0f;
                     if (precision == ACCSPMM_FP16) out.v16[idx] = round_fp16_rne(v);
                     else out.v32[idx] = round_tf32_rna(v);

@@ -48,7 +48,7 @@ int auto_group_cap(int cap)
 }
 
 Schedule build_schedule(const std::vector<uint32_t> &rwo, int cap, bool balance, int precision, bool group,
-                        int group_cap)
+                        int group_cap, int wh)
 {
     const int64_t gcap = group_cap > 0 ? group_cap : cap;  // concatenation limit (reading R7c)
     Schedule s;
@@ -62,7 +62,8 @@ Schedule build_schedule(const std::vector<uint32_t> &rwo, int cap, bool balance,
             s.units.push_back({(uint32_t)w, 1u, rwo[(size_t)w], rwo[(size_t)w + 1], kNoSplit, 0u, 1u, 0u});
         return s;
     }
-    const int64_t wb = precision == ACCSPMM_FP16 ? 2 : 1;
+    // C write-back of one window in TC-block loads: wh rows x N x 4 B over 8 rows x N x es_B
+    const int64_t wb = (precision == ACCSPMM_FP16 ? 2 : 1) * (wh / kWindow);
     bool open = false;
     Unit cur{};
     int64_t cost = 0;
@@ -101,13 +102,13 @@ Schedule build_schedule(const std::vector<uint32_t> &rwo, int cap, bool balance,
     return s;
 }
 
-std::vector<int64_t> partition_bounds(const Csr &a, const std::vector<uint32_t> &perm, int nparts)
+std::vector<int64_t> partition_bounds(const Csr &a, const std::vector<uint32_t> &perm, int nparts, int wh)
 {
-    const int64_t W = (a.M + kWindow - 1) / kWindow;
+    const int64_t W = (a.M + wh - 1) / wh;
     std::vector<int64_t> pre((size_t)W + 1, 0);
     for (int64_t w = 0; w < W; ++w) {
         int64_t s = 0;
-        for (int64_t r = w * kWindow; r < std::min<int64_t>(a.M, (w + 1) * kWindow); ++r) {
+        for (int64_t r = w * wh; r < std::min<int64_t>(a.M, (w + 1) * wh); ++r) {
             int64_t o = perm.empty() ? r : (int64_t)perm[(size_t)r];
             s += a.rowptr[o + 1] - a.rowptr[o];
         }

@@ -56,10 +56,11 @@ struct Csr {
 // reordered matrix); offsets relative to the slab.
 struct HostFormat {
     int64_t W = 0, NB = 0, nnz = 0, rows = 0, sum_U = 0;
+    int wh = kWindow;            // rows per RowWindow (8 = the paper's; 16/32 tall windows, R20)
     std::vector<uint32_t> rwo;   // RowWindowOffset u32[W+1]
     std::vector<uint32_t> tco;   // TCOffset        u32[NB+1]
     std::vector<uint32_t> a2b;   // SparseAToB      u32[8 NB]
-    std::vector<uint64_t> bits;  // TCLocalBit      u64[NB]
+    std::vector<uint64_t> bits;  // TCLocalBit      u64[NB * wh/8] (wh/8 words per block)
     std::vector<float> v32;      // values (TF32-rounded) when precision == TF32
     std::vector<uint16_t> v16;   // values (FP16 bits) when precision == FP16
 };
@@ -86,18 +87,19 @@ void csr_transpose(const Csr &a, const float *vals, int64_t *t_rowptr, int32_t *
 // columns are reordered with the rows, accspmm_options.permute_cols)
 accspmm_status build_format(const Csr &a, const float *vals, const std::vector<uint32_t> &perm,
                             int64_t row_begin, int64_t row_end, int precision, HostFormat &out,
-                            const uint32_t *colmap = nullptr);
-int64_t count_blocks(const Csr &a, const std::vector<uint32_t> &perm);
+                            const uint32_t *colmap = nullptr, int wh = kWindow);
+int64_t count_blocks(const Csr &a, const std::vector<uint32_t> &perm, int wh = kWindow);
 
 // host/schedule.cpp
 double compute_ibd(const std::vector<uint32_t> &rwo);
 int auto_cap(int64_t NB);
 Schedule build_schedule(const std::vector<uint32_t> &rwo, int cap, bool balance, int precision, bool group,
-                        int group_cap = 0);
+                        int group_cap = 0, int wh = kWindow);
 int auto_group_cap(int cap);  // concatenation limit under the automatic cap (reading R7c)
 
 // host/partition.cpp
-std::vector<int64_t> partition_bounds(const Csr &a, const std::vector<uint32_t> &perm, int nparts);
+std::vector<int64_t> partition_bounds(const Csr &a, const std::vector<uint32_t> &perm, int nparts,
+                                      int wh = kWindow);
 
 // host/reorder.cpp -- Algorithm 1; returns perm new->old (identity for an edgeless graph)
 std::vector<uint32_t> reorder_alg1(const Csr &a);
@@ -106,8 +108,10 @@ std::vector<uint32_t> reorder_alg1(const Csr &a);
 struct DevicePlan {
     int64_t W = 0, NB = 0, nnz = 0, rows = 0, n_units = 0, n_split = 0, n_segments = 0;
     int precision = 0;
+    int wh = kWindow;              // rows per RowWindow (8 = paper; 16/32 tall windows, R20)
+    int kernel = ACCSPMM_KERNEL_MMA_SYNC;  // resolved accspmm_kernel
     uint32_t *rwo = nullptr, *tco = nullptr, *a2b = nullptr;
-    uint64_t *bits = nullptr;
+    uint64_t *bits = nullptr;      // [NB][wh/8]
     void *vals = nullptr;
     uint32_t *units = nullptr;     // [n_units][8]
     uint32_t *row_map = nullptr;   // slab row -> C row (nparts == 1 with a permutation), else null
@@ -125,6 +129,7 @@ struct DevicePlan {
 // host-side schedule.  On failure the caller frees what was allocated (free_device_format).
 struct DeviceFormat {
     int64_t W = 0, NB = 0, nnz = 0, rows = 0, sum_U = 0;
+    int wh = kWindow;
     uint32_t *rwo = nullptr, *tco = nullptr, *a2b = nullptr;
     uint64_t *bits = nullptr;
     void *vals = nullptr;
@@ -133,7 +138,7 @@ struct DeviceFormat {
 };
 accspmm_status build_format_device(const Csr &a, const float *vals, const std::vector<uint32_t> &perm,
                                    int64_t row_begin, int64_t row_end, int precision, DeviceFormat &out,
-                                   const uint32_t *colmap = nullptr);
+                                   const uint32_t *colmap = nullptr, int wh = kWindow);
 void free_device_format(DeviceFormat &f);
 
 // Feature-slice width of one warp for a given N (N % 16 == 0): the widest of 128/64/32/16
@@ -145,6 +150,9 @@ int pick_fw(int64_t N);
 accspmm_status launch_spmm(const DevicePlan &p, const void *B, const void *zrow, int64_t N, float *C, float *ws,
                            uint32_t *counters, void *stream, bool round_b, float *const *dst = nullptr,
                            int ndst = 0);
+// kernels/spmm_tc05_sm100.cu: the tcgen05/TMEM kernel (TF32, N % 128 == 0, any window height)
+accspmm_status launch_spmm_tc05(const DevicePlan &d, const void *B, int64_t N, float *C, float *ws, uint32_t *counters,
+                                void *stream, bool round_b);
 accspmm_status launch_round_b(const float *B, float *Br, int64_t n, void *stream);
 // B' = B[perm] row gather (K rows of row_bytes), optionally with rho = TF32 RNA (f32 rows)
 accspmm_status launch_permute_b(const void *B, void *Bp, const uint32_t *perm, int64_t K, int64_t row_bytes,

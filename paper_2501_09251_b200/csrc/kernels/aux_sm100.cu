@@ -35,15 +35,19 @@ __global__ void round_tf32_kernel(const float *__restrict__ in, float *__restric
 // tile[b][k] = value at bit k of TC block b: TCOffset[b] + popc(mask & (2^k - 1)), else 0
 template <bool F16>
 __global__ void decode_kernel(const uint64_t *__restrict__ bits, const uint32_t *__restrict__ tco,
-                              const void *__restrict__ vals, int64_t NB, float *__restrict__ tiles)
+                              const void *__restrict__ vals, int64_t NB, int nw, float *__restrict__ tiles)
 {
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < NB * 64; e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t b = e >> 6;
-        const int k = (int)(e & 63);
-        const uint64_t m = __ldg(bits + b);
+    // tile b has nw*64 positions p = r*8 + lane (r < 8*nw); word p/64, bit p%64 (reading R20)
+    const int64_t per = (int64_t)nw * 64;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < NB * per; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = e / per;
+        const int p = (int)(e - b * per);
+        const int word = p >> 6, k = p & 63;
+        const uint64_t m = __ldg(bits + b * nw + word);
         float v = 0.f;
         if ((m >> k) & 1ull) {
-            const uint32_t idx = __ldg(tco + b) + (uint32_t)__popcll(m & ((1ull << k) - 1ull));
+            uint32_t idx = __ldg(tco + b) + (uint32_t)__popcll(m & ((1ull << k) - 1ull));
+            for (int j = 0; j < word; ++j) idx += (uint32_t)__popcll(__ldg(bits + b * nw + j));
             if (F16) v = __half2float(reinterpret_cast<const __half *>(vals)[idx]);
             else v = reinterpret_cast<const float *>(vals)[idx];
         }
@@ -149,11 +153,12 @@ accspmm_status launch_round_tf32(const float *in, float *out, int64_t n, void *s
 
 accspmm_status launch_decode(const DevicePlan &p, float *tiles, void *stream)
 {
-    const int64_t n = p.NB * 64;
+    const int nw = p.wh / kWindow;
+    const int64_t n = p.NB * 64 * nw;
     if (p.precision == ACCSPMM_FP16)
-        decode_kernel<true><<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(p.bits, p.tco, p.vals, p.NB, tiles);
+        decode_kernel<true><<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(p.bits, p.tco, p.vals, p.NB, nw, tiles);
     else
-        decode_kernel<false><<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(p.bits, p.tco, p.vals, p.NB, tiles);
+        decode_kernel<false><<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(p.bits, p.tco, p.vals, p.NB, nw, tiles);
     return check_launch("decode launch");
 }
 

@@ -1,0 +1,564 @@
+// Acc-SpMM on the 5th-generation tensor cores (tcgen05 + TMEM), sm_100a -- SURVEY NEXT-1.
+//
+// What it computes is the same product as spmm_sm100.cu: every TC block of a RowWindow
+// is decoded from its occupancy bitmap with the popcount rule of P:273 and
+// multiplied against the gathered rows of B with the operands swapped: the
+// gathered B rows are the left operand (M = 128 features x K = 8 gathered rows), the decoded
+// sparse tile the right operand (K = 8 x N = window rows).  TF32 inputs, FP32 accumulation
+// (P:308).  Windows may be taller than the paper's 8 rows (reading R20: wh = 16 / 32 rows,
+// wh x 8 tiles), which cuts the dominant gathered-row bytes (Reddit-shaped, reordered:
+// sum_w |U_w| -14% at 16 rows, -28% at 32) at the price of wh/8 times the MMA work per
+// gathered row -- affordable only on tcgen05.
+//
+// Data path of one TC block (one CTA = 4 warps = one work unit x one 128-feature slice):
+//   L2 --(TMA tile::gather4, 2 per block, leader thread)--> shared stage (8 rows x 512 B)
+//      --(LDS.32: thread = feature, 8 rows)--> registers --(tcgen05.st 32x32b.x8)--> TMEM A[s]
+//   bitmap + values --(decode)--> shared B tile (K-major, no swizzle: core matrices of
+//      8 window rows x 16 B)
+//   leader: tcgen05.mma.cta_group::1.kind::tf32 D[tmem] (+)= A[tmem] . B[smem desc];
+//           tcgen05.commit -> "empty" mbarrier of the stage; at a window's end -> "acc" mbarrier
+//   window end: tcgen05.ld 32x32b (thread = feature, one column per window row) -> st.global
+// The gathered rows are MN-major (features contiguous), which UMMA reads from shared memory
+// only in the 128-byte-swizzled layout (one TMA request per 4 rows x 32 features: 8 per
+// block instead of 2); the transposition through registers into TMEM (the
+// A-from-TMEM "TS" form) keeps the gather at 2 TMA requests per block.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../internal.hpp"
+
+namespace accspmm {
+namespace {
+
+constexpr int kFW = 128;    // features per CTA slice = UMMA M
+constexpr int kCH = 16;     // TC blocks per staged A-stream chunk
+constexpr int kThreads = 128;
+constexpr int kStageBytes = 8 * kFW * 4;  // 8 gathered rows x 128 features x 4 B
+
+struct TcParams {
+    const uint32_t *__restrict__ rwo;
+    const uint32_t *__restrict__ tco;
+    const uint32_t *__restrict__ a2b;
+    const uint64_t *__restrict__ bits;
+    const float *__restrict__ vals;
+    const uint4 *__restrict__ units;
+    const uint32_t *__restrict__ row_map;
+    float *__restrict__ C;
+    float *__restrict__ ws;
+    uint32_t *__restrict__ counters;
+    int64_t N;
+    int64_t rows;
+    int64_t n_units;
+    int32_t nslices;
+    int32_t wh;         // rows per window of the plan (<= HT)
+    int32_t nw;         // occupancy words per block = wh / 8
+    int32_t slice_major;
+};
+
+template <int HT, int S>
+struct TcLayout {
+    static constexpr int NWMAX = HT / 8;
+    static constexpr int STAGE = 0;                                   // S x 4096
+    static constexpr int BTILE = STAGE + S * kStageBytes;             // S x HT x 8 x 4
+    static constexpr int A2B = BTILE + S * HT * 32;                   // 2 x CH x 8 u32
+    static constexpr int BITS = A2B + 2 * kCH * 8 * 4;                // 2 x CH x NWMAX u64
+    static constexpr int TCO = BITS + 2 * kCH * NWMAX * 8;            // 2 x CH u32
+    static constexpr int BAR = (TCO + 2 * kCH * 4 + 7) / 8 * 8;       // full[S], empty[S], acc
+    static constexpr int MISC = BAR + (2 * S + 1) * 8;                // tmem base, split flag
+    static constexpr int BYTES = MISC + 16;
+    static constexpr int TMEM_NEED = S * 8 + HT;
+    static constexpr int TMEM_COLS = TMEM_NEED <= 32 ? 32 : TMEM_NEED <= 64 ? 64 : TMEM_NEED <= 128 ? 128 : 256;
+};
+
+// ------------------------------------------------------------------ PTX helpers
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src)
+{
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void *src)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void *src)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+__device__ __forceinline__ uint64_t policy_evict_last()
+{
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
+    return p;
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase)
+{
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+        "@P1 bra DONE_%=;\n\t"
+        "bra WAIT_%=;\n\t"
+        "DONE_%=:\n\t}\n" ::"r"(bar), "r"(phase), "r"(0x989680)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap *map, int32_t col, int32_t r0, int32_t r1,
+                                            int32_t r2, int32_t r3, uint32_t bar, uint64_t pol)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;\n" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar), "l"(pol)
+        : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
+// TMEM <- registers: 32 lanes (one per thread of the warp) x 8 consecutive 32-bit columns
+__device__ __forceinline__ void tmem_st_x8(uint32_t taddr, const uint32_t (&v)[8])
+{
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n" ::"r"(taddr), "r"(v[0]),
+                 "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+
+// registers <- TMEM: 32 lanes x 16 consecutive columns
+__device__ __forceinline__ void tmem_ld_x16(uint32_t taddr, uint32_t (&v)[16], int off)
+{
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+          "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr + (uint32_t)off)
+        : "memory");
+}
+
+// D[tmem] (+)= A[tmem] . B[smem]: M = 128, N = HT, K = 8, TF32 in, FP32 accumulate
+__device__ __forceinline__ void umma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                             uint32_t accumulate)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint32_t bar)
+{
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(bar)
+                 : "memory");
+}
+
+// Shared-memory matrix descriptor of the B tile: K-major, no swizzle (canonical
+// ((8,n),2):((1,SBO),LBO) in 16-byte units): core matrix = 8 window rows x 16 B (4 TF32 of K),
+// LBO = 128 B between the two K halves, SBO = 256 B between 8-row groups; version 1 (sm_100).
+__device__ __forceinline__ uint64_t btile_desc(uint32_t saddr)
+{
+    return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)(128u >> 4) << 16) | ((uint64_t)(256u >> 4) << 32) |
+           (1ull << 46);
+}
+
+__device__ __forceinline__ uint32_t tf32_rna_bits(uint32_t x)
+{
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(__uint_as_float(x)));
+    return r;
+}
+
+// ------------------------------------------------------------------ the kernel
+
+// 8 resident CTAs per SM: TMEM (8 x 64 columns = 512) and <= 64 registers per thread
+template <int HT, int S, bool RND>
+__global__ void __launch_bounds__(kThreads, 8)
+    spmm_tc05_kernel(const TcParams p, const __grid_constant__ CUtensorMap tmap)
+{
+    using L = TcLayout<HT, S>;
+    constexpr int NWMAX = L::NWMAX;
+    constexpr int EPT = HT * 8 / kThreads;  // B-tile entries decoded per thread (1 or 2)
+    // instruction descriptor: D F32 (bit 4), A/B TF32 (bits 7, 10), K-major A and B,
+    // N >> 3 at bit 17, M >> 4 at bit 24 (M = 128)
+    constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(HT >> 3) << 17) | (8u << 24);
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t *stage = smem + L::STAGE;
+    float *btile = reinterpret_cast<float *>(smem + L::BTILE);
+    uint32_t *ch_a2b = reinterpret_cast<uint32_t *>(smem + L::A2B);
+    uint64_t *ch_bits = reinterpret_cast<uint64_t *>(smem + L::BITS);
+    uint32_t *ch_tco = reinterpret_cast<uint32_t *>(smem + L::TCO);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + L::BAR);
+    uint32_t *misc = reinterpret_cast<uint32_t *>(smem + L::MISC);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const unsigned ngrp = (unsigned)p.n_units;
+    const int slice = p.slice_major ? (int)(blockIdx.x / ngrp) : (int)(blockIdx.x % (unsigned)p.nslices);
+    const int64_t u = p.slice_major ? (int64_t)(blockIdx.x % ngrp) : (int64_t)(blockIdx.x / (unsigned)p.nslices);
+    const int64_t f0 = (int64_t)slice * kFW;
+    const int feat = warp * 32 + lane;  // this thread's feature (TMEM lane) inside the slice
+
+    const uint4 ua = __ldg(p.units + 2 * u);
+    const uint4 ub = __ldg(p.units + 2 * u + 1);
+    const uint32_t w0 = ua.x, nwin = ua.y, b0 = ua.z, b1 = ua.w;
+    const bool split = ub.x != kNoSplit;
+    const uint32_t nblk = b1 - b0;
+    const uint32_t my_rwo = (uint32_t)lane <= nwin ? __ldg(p.rwo + w0 + lane) : 0u;
+
+    auto full_bar = [&](int s) { return smem_u32(&bars[s]); };
+    auto empty_bar = [&](int s) { return smem_u32(&bars[S + s]); };
+    const uint32_t acc_bar = smem_u32(&bars[2 * S]);
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(misc)),
+                     "r"((uint32_t)L::TMEM_COLS)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+    }
+    if (tid == 0) {
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+        for (int s = 0; s < S; ++s) {
+            mbar_init(full_bar(s), 1);
+            mbar_init(empty_bar(s), 1);
+        }
+        mbar_init(acc_bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = misc[0];
+    const uint32_t tmem_d = tmem + (uint32_t)(S * 8);             // accumulator columns
+    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;          // this warp's TMEM lane quarter
+    const uint64_t pol_keep = policy_evict_last();
+
+    // ---- A-stream chunk staging (cp.async, double buffered): blocks [b0 + c*CH, +CH)
+    auto issue_chunk = [&](uint32_t c) {
+        const uint32_t i = c * kCH;
+        if (i < nblk) {
+            const int buf = c & 1;
+            const uint32_t b = b0 + i;
+            const uint32_t cnt = min((uint32_t)kCH, nblk - i);
+            if ((uint32_t)tid < 2 * cnt)
+                cp_async16(smem_u32(&ch_a2b[buf * kCH * 8 + 4 * tid]), p.a2b + (size_t)b * 8 + 4 * tid);
+            if ((uint32_t)tid < cnt * (uint32_t)p.nw)
+                cp_async8(smem_u32(&ch_bits[(buf * kCH + tid / p.nw) * NWMAX + tid % p.nw]),
+                          p.bits + (size_t)b * p.nw + tid);
+            if ((uint32_t)tid < cnt) cp_async4(smem_u32(&ch_tco[buf * kCH + tid]), p.tco + b + tid);
+        }
+        cp_async_commit();
+    };
+    // ---- leader: two gather4 of block j's 8 B rows into stage s (padding lanes: row -1, zero fill)
+    auto issue_tma = [&](uint32_t j, int s) {
+        const int buf = (j / kCH) & 1;
+        const uint32_t cs = j & (kCH - 1u);
+        const uint4 ca = *reinterpret_cast<const uint4 *>(&ch_a2b[(buf * kCH + cs) * 8]);
+        const uint4 cb = *reinterpret_cast<const uint4 *>(&ch_a2b[(buf * kCH + cs) * 8 + 4]);
+        const uint32_t bar = full_bar(s);
+        const uint32_t dst = smem_u32(stage + s * kStageBytes);
+        mbar_arrive_expect_tx(bar, (uint32_t)kStageBytes);
+        const int32_t col = (int32_t)f0;
+        tma_gather4(dst, &tmap, col, (int32_t)ca.x, (int32_t)ca.y, (int32_t)ca.z, (int32_t)ca.w, bar, pol_keep);
+        tma_gather4(dst + kStageBytes / 2, &tmap, col, (int32_t)cb.x, (int32_t)cb.y, (int32_t)cb.z, (int32_t)cb.w, bar,
+                    pol_keep);
+    };
+    // ---- every thread: its EPT B-tile entries of block j: value or 0, read ahead
+    uint32_t vreg[EPT];
+    auto value_load = [&](uint32_t j) {
+        const int buf = (j / kCH) & 1;
+        const uint32_t cs = j & (kCH - 1u);
+        const uint64_t *wb = &ch_bits[(buf * kCH + cs) * NWMAX];
+        const uint32_t t0 = ch_tco[buf * kCH + cs];
+#pragma unroll
+        for (int i = 0; i < EPT; ++i) {
+            const int e = tid + kThreads * i;
+            const int n = e >> 3, k = e & 7;   // window row n, condensed lane k
+            const int word = n >> 3, bit = (n & 7) * 8 + k;
+            uint32_t v = 0u;
+            if (n < p.wh) {
+                const uint64_t m = wb[word];
+                if ((m >> bit) & 1ull) {
+                    uint32_t idx = t0 + (uint32_t)__popcll(m & ((1ull << bit) - 1ull));
+#pragma unroll
+                    for (int q = 0; q < NWMAX - 1; ++q)
+                        if (q < word) idx += (uint32_t)__popcll(wb[q]);
+                    v = __float_as_uint(__ldg(p.vals + idx));
+                }
+            }
+            vreg[i] = v;
+        }
+    };
+
+    // ---- epilogue helpers: rows n < wh of the accumulator to C (or the split workspace);
+    // thread = feature, so every warp-wide store is one coalesced 128-byte row segment
+    auto store_rows = [&](const uint32_t (&d)[HT], int64_t lr0, float *base, int64_t ld, bool remap) {
+#pragma unroll
+        for (int n = 0; n < HT; ++n) {
+            const int64_t lr = lr0 + n;
+            if (n < p.wh) {
+                if (remap) {
+                    if (lr < p.rows) {
+                        const int64_t orow = p.row_map ? (int64_t)__ldg(p.row_map + lr) : lr;
+                        __stcs(base + orow * ld + feat, __uint_as_float(d[n]));
+                    }
+                } else {
+                    __stcg(base + (int64_t)n * ld + feat, __uint_as_float(d[n]));
+                }
+            }
+        }
+    };
+    // accumulator (after the commit of the window's last MMA) -> registers
+    auto load_acc = [&](uint32_t (&d)[HT], uint32_t phase) {
+        mbar_wait(acc_bar, phase & 1u);
+        tc_fence_after();
+        uint32_t t[16];
+#pragma unroll
+        for (int h = 0; h < HT; h += 16) {
+            tmem_ld_x16(tmem_d + lane_off, t, h);
+            tmem_wait_ld();
+#pragma unroll
+            for (int q = 0; q < 16; ++q) d[h + q] = t[q];
+        }
+        tc_fence_before();  // the next window's first MMA overwrites D after the next barrier
+    };
+    uint32_t zeros[HT];
+#pragma unroll
+    for (int q = 0; q < HT; ++q) zeros[q] = 0u;
+
+    // window bookkeeping (uniform across the CTA): wend = absolute end block of window wi
+    uint32_t wi = 0;
+    uint32_t wend = split ? b1 : __shfl_sync(0xffffffffu, my_rwo, 1);
+    uint32_t acc_phase = 0;
+    auto window_row0 = [&](uint32_t w) { return (int64_t)(w0 + w) * p.wh; };
+    // empty windows (no blocks) are zero-written; called whenever the block cursor is at jb
+    auto skip_empty = [&](uint32_t jb) {
+        while (!split && wi < nwin && wend == jb) {
+            store_rows(zeros, window_row0(wi), p.C + f0, p.N, true);
+            ++wi;
+            const uint32_t e = __shfl_sync(0xffffffffu, my_rwo, (int)(wi < nwin ? wi + 1 : nwin));
+            wend = wi < nwin ? e : 0xFFFFFFFFu;
+        }
+    };
+    skip_empty(b0);  // leading empty windows (the first window starts at rwo[w0] = b0)
+
+    // ---- prologue: chunks 0 (waited) and 1, TMA of the first S blocks, values of block 0
+    issue_chunk(0);
+    cp_async_wait_all();
+    __syncthreads();
+    issue_chunk(1);
+    if (tid == 0)
+        for (int s = 0; s < S; ++s)
+            if ((uint32_t)s < nblk) issue_tma((uint32_t)s, s);
+    if (nblk > 0) value_load(0);
+    bool first = true;  // next MMA starts a new accumulation (window or segment start)
+
+    for (uint32_t j = 0; j < nblk; ++j) {
+        const int s = (int)(j % S);
+        if (j > 0 && (j % kCH) == 0) issue_chunk(j / kCH + 1);
+        mbar_wait(full_bar(s), (j / S) & 1u);
+        if (j >= (uint32_t)S) mbar_wait(empty_bar(s), ((j / S) - 1u) & 1u);
+        tc_fence_after();
+        // gathered rows -> TMEM A[s]: this thread's feature of the 8 rows
+        {
+            const float *st = reinterpret_cast<const float *>(stage + s * kStageBytes);
+            uint32_t v[8];
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                v[r] = __float_as_uint(st[r * kFW + feat]);
+                if constexpr (RND) v[r] = tf32_rna_bits(v[r]);
+            }
+            tmem_st_x8(tmem + lane_off + (uint32_t)(s * 8), v);
+        }
+        // decoded tile -> B[s] (K-major core matrices: row n, K-half k/4, element k%4)
+        {
+            float *bt = btile + s * HT * 8;
+#pragma unroll
+            for (int i = 0; i < EPT; ++i) {
+                const int e = tid + kThreads * i;
+                const int n = e >> 3, k = e & 7;
+                bt[(n >> 3) * 64 + (k >> 2) * 32 + (n & 7) * 4 + (k & 3)] = __uint_as_float(vreg[i]);
+            }
+        }
+        tmem_wait_st();
+        fence_proxy_async_smem();
+        tc_fence_before();
+        if (((j + S) % kCH) == 0) cp_async_wait_all();  // chunk of block j + S must be resident
+        __syncthreads();
+        const uint32_t jb = b0 + j;
+        const bool last_of_window = split ? (j + 1 == nblk) : (jb + 1 == wend);
+        if (tid == 0) {
+            tc_fence_after();
+            umma_tf32_ts(tmem_d, tmem + (uint32_t)(s * 8), btile_desc(smem_u32(btile + s * HT * 8)), IDESC,
+                         first ? 0u : 1u);
+            umma_commit(empty_bar(s));
+            if (last_of_window) umma_commit(acc_bar);
+            if (j + S < nblk) issue_tma(j + S, s);
+        }
+        first = last_of_window;
+        if (j + 1 < nblk) value_load(j + 1);
+        if (last_of_window && !split) {
+            uint32_t d[HT];
+            load_acc(d, acc_phase);
+            ++acc_phase;
+            store_rows(d, window_row0(wi), p.C + f0, p.N, true);
+            ++wi;
+            const uint32_t e = __shfl_sync(0xffffffffu, my_rwo, (int)(wi < nwin ? wi + 1 : nwin));
+            wend = wi < nwin ? e : 0xFFFFFFFFu;
+            skip_empty(jb + 1);
+        }
+    }
+
+    if (split) {
+        // cross-row write-back of a split window (reading R15): partial -> workspace,
+        // the last-arriving segment sums the partials in segment order (deterministic)
+        const uint32_t sid = ub.x, seg = ub.y, nseg = ub.z, slot = ub.w;
+        const int64_t tile_elems = (int64_t)p.wh * kFW;
+        float *tile = p.ws + ((int64_t)slot * p.nslices + slice) * tile_elems;
+        uint32_t d[HT];
+        if (nblk > 0) {
+            load_acc(d, acc_phase);
+        } else {
+#pragma unroll
+            for (int q = 0; q < HT; ++q) d[q] = 0u;
+        }
+        store_rows(d, 0, tile, kFW, false);
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) misc[2] = atomicAdd(p.counters + (int64_t)sid * p.nslices + slice, 1u);
+        __syncthreads();
+        if (misc[2] == nseg - 1) {
+            __threadfence();
+            const float *firstp = p.ws + ((int64_t)(slot - seg) * p.nslices + slice) * tile_elems;
+            float acc[HT];
+#pragma unroll
+            for (int q = 0; q < HT; ++q) acc[q] = 0.f;
+            for (uint32_t k = 0; k < nseg; ++k) {
+                const float *src = firstp + (int64_t)k * p.nslices * tile_elems;
+#pragma unroll
+                for (int n = 0; n < HT; ++n)
+                    if (n < p.wh) acc[n] += __ldcg(src + (int64_t)n * kFW + feat);
+            }
+            uint32_t r[HT];
+#pragma unroll
+            for (int q = 0; q < HT; ++q) r[q] = __float_as_uint(acc[q]);
+            store_rows(r, window_row0(0), p.C + f0, p.N, true);
+            if (tid == 0) p.counters[(int64_t)sid * p.nslices + slice] = 0u;  // re-arm for the next execute
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"((uint32_t)L::TMEM_COLS)
+                     : "memory");
+}
+
+// ------------------------------------------------------------------ launch
+
+accspmm_status tensor_map_tc05(const DevicePlan &d, const void *B, int64_t N, const CUtensorMap **out)
+{
+    // key marks this kernel's map (box = exactly one 128-feature slice, no padding columns)
+    const uint64_t key[4] = {(uint64_t)(uintptr_t)B, (uint64_t)N, (uint64_t)kFW, 0x7C05ull << 32};
+    CUtensorMap *map = reinterpret_cast<CUtensorMap *>(d.tmap);
+    if (!(key[0] == d.tmap_key[0] && key[1] == d.tmap_key[1] && key[2] == d.tmap_key[2] && key[3] == d.tmap_key[3])) {
+        static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+        if (!encode) {
+            cudaDriverEntryPointQueryResult q;
+            void *fn = nullptr;
+            cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+            if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn)
+                return fail(ACCSPMM_ERR_CUDA, "cuTensorMapEncodeTiled entry point not available");
+            encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+        }
+        cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)d.K};
+        cuuint64_t strides[1] = {(cuuint64_t)N * 4};
+        cuuint32_t box[2] = {(cuuint32_t)kFW, 1u};
+        cuuint32_t estr[2] = {1u, 1u};
+        CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<void *>(B), dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS)
+            return fail(ACCSPMM_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+        for (int k = 0; k < 4; ++k) d.tmap_key[k] = key[k];
+    }
+    *out = map;
+    return ACCSPMM_OK;
+}
+
+template <int HT, int S, bool RND>
+accspmm_status launch_tc(const TcParams &tp, const CUtensorMap *map, cudaStream_t stream)
+{
+    using L = TcLayout<HT, S>;
+    auto kern = spmm_tc05_kernel<HT, S, RND>;
+    static int configured_device = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (configured_device != dev) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES);
+        if (e != cudaSuccess) return fail(ACCSPMM_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+        configured_device = dev;
+    }
+    const int64_t grid = tp.n_units * tp.nslices;
+    if (grid > 0x7FFFFFFFll) return fail(ACCSPMM_ERR_UNSUPPORTED, "grid too large");
+    kern<<<(unsigned)grid, kThreads, L::BYTES, stream>>>(tp, *map);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(ACCSPMM_ERR_CUDA, std::string("tcgen05 spmm launch: ") + cudaGetErrorString(e));
+    return ACCSPMM_OK;
+}
+
+}  // namespace
+
+accspmm_status launch_spmm_tc05(const DevicePlan &d, const void *B, int64_t N, float *C, float *ws, uint32_t *counters,
+                                void *stream, bool round_b)
+{
+    if (d.rows == 0 || d.n_units == 0) return ACCSPMM_OK;
+    if (N % kFW != 0) return fail(ACCSPMM_ERR_INTERNAL, "tcgen05 kernel needs N % 128 == 0");
+    TcParams tp;
+    tp.rwo = d.rwo;
+    tp.tco = d.tco;
+    tp.a2b = d.a2b;
+    tp.bits = d.bits;
+    tp.vals = reinterpret_cast<const float *>(d.vals);
+    tp.units = reinterpret_cast<const uint4 *>(d.units);
+    tp.row_map = d.row_map;
+    tp.C = C;
+    tp.ws = ws;
+    tp.counters = counters;
+    tp.N = N;
+    tp.rows = d.rows;
+    tp.n_units = d.n_units;
+    tp.nslices = (int32_t)(N / kFW);
+    tp.wh = d.wh;
+    tp.nw = d.wh / kWindow;
+    tp.slice_major = tp.nslices > 1 ? 1 : 0;
+    static const CUtensorMap no_map = {};
+    const CUtensorMap *map = &no_map;  // no TC blocks (K = 0): no TMA is ever issued
+    if (d.NB > 0) {
+        accspmm_status st = tensor_map_tc05(d, B, N, &map);
+        if (st != ACCSPMM_OK) return st;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    if (d.wh <= 16) return round_b ? launch_tc<16, 6, true>(tp, map, s) : launch_tc<16, 6, false>(tp, map, s);
+    return round_b ? launch_tc<32, 4, true>(tp, map, s) : launch_tc<32, 4, false>(tp, map, s);
+}
+
+}  // namespace accspmm
