@@ -330,7 +330,8 @@ accspmm_status accspmm_plan_create_ex(int64_t M, int64_t K, const int64_t *rowpt
                      8 * (wh / kWindow) * std::max<int64_t>(F.NB, 1) + es * (F.nnz + 16);
         } else {
             st = upload(&d.rwo, F.rwo, bytes);
-            if (st == ACCSPMM_OK) st = upload(&d.tco, F.tco, bytes);
+            // padding: the tcgen05 kernel bulk-copies 16-byte-aligned supersets of these arrays
+            if (st == ACCSPMM_OK) st = upload(&d.tco, F.tco, bytes, 4);
         }
         if (st == ACCSPMM_OK && opt.build != ACCSPMM_BUILD_DEVICE) {
             // device copy: padding lanes (no bit in the block's column-OR) hold 0xFFFFFFFF, an
@@ -349,7 +350,7 @@ accspmm_status accspmm_plan_create_ex(int64_t M, int64_t K, const int64_t *rowpt
             }
             st = upload(&d.a2b, a2b_dev, bytes);
         }
-        if (st == ACCSPMM_OK && opt.build != ACCSPMM_BUILD_DEVICE) st = upload(&d.bits, F.bits, bytes);
+        if (st == ACCSPMM_OK && opt.build != ACCSPMM_BUILD_DEVICE) st = upload(&d.bits, F.bits, bytes, 2);
         if (st == ACCSPMM_OK && opt.build != ACCSPMM_BUILD_DEVICE) {
             if (opt.precision == ACCSPMM_FP16) st = upload((uint16_t **)&d.vals, F.v16, bytes, 16);
             else st = upload((float **)&d.vals, F.v32, bytes, 16);

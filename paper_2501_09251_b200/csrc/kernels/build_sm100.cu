@@ -330,12 +330,14 @@ accspmm_status build_format_device(const Csr &a, const float *vals, const std::v
     // ---- 6. SparseAToB + TCLocalBit
     const size_t es = f16 ? 2 : 4;
     if (!B.ok(cudaMalloc((void **)&out.a2b, (size_t)(NB ? NB : 1) * 32), "a2b") ||
-        !B.ok(cudaMalloc((void **)&out.bits, (size_t)(NB ? NB : 1) * 8 * nwords), "bits") ||
-        !B.ok(cudaMalloc((void **)&out.tco, (size_t)(NB + 1) * 4), "tco") ||
+        // +2 words / +4 entries: the tcgen05 kernel bulk-copies 16-byte-aligned supersets
+        !B.ok(cudaMalloc((void **)&out.bits, ((size_t)(NB ? NB : 1) * nwords + 2) * 8), "bits") ||
+        !B.ok(cudaMalloc((void **)&out.tco, (size_t)(NB + 1 + 4) * 4), "tco") ||
         !B.ok(cudaMalloc(&out.vals, ((size_t)nnz + 16) * es), "vals"))
         return B.st;
     if (!B.ok(cudaMemsetAsync(out.a2b, 0xFF, (size_t)(NB ? NB : 1) * 32, B.s), "memset") ||  // kPadLane
-        !B.ok(cudaMemsetAsync(out.bits, 0, (size_t)(NB ? NB : 1) * 8 * nwords, B.s), "memset") ||
+        !B.ok(cudaMemsetAsync(out.bits, 0, ((size_t)(NB ? NB : 1) * nwords + 2) * 8, B.s), "memset") ||
+        !B.ok(cudaMemsetAsync(out.tco, 0, (size_t)(NB + 1 + 4) * 4, B.s), "memset") ||
         !B.ok(cudaMemsetAsync(out.vals, 0, ((size_t)nnz + 16) * es, B.s), "memset"))
         return B.st;
     if (nnz > 0)

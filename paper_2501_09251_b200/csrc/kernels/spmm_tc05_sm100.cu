@@ -58,20 +58,6 @@ struct TcParams {
     int32_t slice_major;
 };
 
-template <int HT, int S>
-struct TcLayout {
-    static constexpr int NWMAX = HT / 8;
-    static constexpr int STAGE = 0;                                   // S x 4096
-    static constexpr int BTILE = STAGE + S * kStageBytes;             // S x HT x 8 x 4
-    static constexpr int A2B = BTILE + S * HT * 32;                   // 2 x CH x 8 u32
-    static constexpr int BITS = A2B + 2 * kCH * 8 * 4;                // 2 x CH x NWMAX u64
-    static constexpr int TCO = BITS + 2 * kCH * NWMAX * 8;            // 2 x CH u32
-    static constexpr int BAR = (TCO + 2 * kCH * 4 + 7) / 8 * 8;       // full[S], empty[S], acc
-    static constexpr int MISC = BAR + (2 * S + 1) * 8;                // tmem base, split flag
-    static constexpr int BYTES = MISC + 16;
-    static constexpr int TMEM_NEED = S * 8 + HT;
-    static constexpr int TMEM_COLS = TMEM_NEED <= 32 ? 32 : TMEM_NEED <= 64 ? 64 : TMEM_NEED <= 128 ? 128 : 256;
-};
 
 // ------------------------------------------------------------------ PTX helpers
 
@@ -188,15 +174,59 @@ __device__ __forceinline__ uint32_t tf32_rna_bits(uint32_t x)
 }
 
 // ------------------------------------------------------------------ the kernel
+//
+// Warp roles (160 threads): warps 0-3 = transposers (thread = feature of the 128-feature
+// slice: TMEM lane quarter = warp), warp 4 lane 0 = producer (A-stream chunks and values by
+// bulk copy, B-row gathers by TMA) and MMA issuer.  They synchronise only through mbarriers:
+//   chunk_full[2]  bulk copies of a chunk's SparseAToB / TCLocalBit / TCOffset (tx bytes)
+//   vals_full[2]   bulk copy of the chunk's value range (or an overflow flag: values from L2)
+//   full_t[ST]     TMA gather of a block's 8 B rows (tx bytes)
+//   ready[SA]      4 transposer warps: A[sa] in TMEM and the decoded tile B[sa] in smem
+//   empty[SA]      tcgen05.commit: the MMA that read A[sa] / B[sa] has completed
+//   acc_full[ND]   tcgen05.commit after a window's (segment's) last MMA
+//   acc_free[ND]   4 transposer warps: accumulator read back, D may be overwritten
+// A chunk buffer is refilled only after the ready[] of the chunk's last block (every reader
+// is done with it); a gather stage only after the ready[] of the block it held.
 
-// 8 resident CTAs per SM: TMEM (8 x 64 columns = 512) and <= 64 registers per thread
-template <int HT, int S, bool RND>
-__global__ void __launch_bounds__(kThreads, 8)
+template <int HT, int ST, int SA, int ND>
+struct TcLayout {
+    static constexpr int NWMAX = HT / 8;
+    static constexpr int VCAP = 512;                                  // staged values per chunk
+    static constexpr int STAGE = 0;                                   // ST x 4096
+    static constexpr int BTILE = STAGE + ST * kStageBytes;            // SA x HT x 8 x 4
+    static constexpr int A2B = BTILE + SA * HT * 32;                  // 2 x CH x 8 u32
+    static constexpr int BITS = A2B + 2 * kCH * 8 * 4;                // 2 x (CH x NWMAX + 2) u64
+    static constexpr int BITS_BUF = kCH * NWMAX + 2;
+    static constexpr int TCO = BITS + 2 * BITS_BUF * 8;               // 2 x (CH + 8) u32
+    static constexpr int TCO_BUF = kCH + 8;
+    static constexpr int VALS = (TCO + 2 * TCO_BUF * 4 + 15) / 16 * 16;  // 2 x (VCAP + 8) f32
+    static constexpr int VALS_BUF = VCAP + 8;
+    static constexpr int BAR = VALS + 2 * VALS_BUF * 4;               // mbarriers
+    static constexpr int NBAR = 2 + 2 + ST + 2 * SA + 2 * ND;
+    static constexpr int MISC = BAR + NBAR * 8;                       // tmem base, chunk offsets
+    static constexpr int BYTES = MISC + 64;
+    static constexpr int TMEM_NEED = SA * 8 + ND * HT;
+    static constexpr int TMEM_COLS = TMEM_NEED <= 32 ? 32 : TMEM_NEED <= 64 ? 64 : TMEM_NEED <= 128 ? 128 : 256;
+};
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+
+template <int HT, int ST, int SA, int ND, bool RND>
+__global__ void __launch_bounds__(kThreads + 32, 6)
     spmm_tc05_kernel(const TcParams p, const __grid_constant__ CUtensorMap tmap)
 {
-    using L = TcLayout<HT, S>;
+    using L = TcLayout<HT, ST, SA, ND>;
     constexpr int NWMAX = L::NWMAX;
-    constexpr int EPT = HT * 8 / kThreads;  // B-tile entries decoded per thread (1 or 2)
+    constexpr int EPL = HT * 8 / kThreads;  // B-tile entries decoded per transposer thread (1 or 2)
     // instruction descriptor: D F32 (bit 4), A/B TF32 (bits 7, 10), K-major A and B,
     // N >> 3 at bit 17, M >> 4 at bit 24 (M = 128)
     constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(HT >> 3) << 17) | (8u << 24);
@@ -206,7 +236,11 @@ __global__ void __launch_bounds__(kThreads, 8)
     uint32_t *ch_a2b = reinterpret_cast<uint32_t *>(smem + L::A2B);
     uint64_t *ch_bits = reinterpret_cast<uint64_t *>(smem + L::BITS);
     uint32_t *ch_tco = reinterpret_cast<uint32_t *>(smem + L::TCO);
+    float *ch_vals = reinterpret_cast<float *>(smem + L::VALS);
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + L::BAR);
+    // misc[0] = TMEM base; misc[4 + buf] = word shift of ch_bits; misc[6 + buf] = entry shift of
+    // ch_tco; misc[8 + buf] = first value index staged (0xFFFFFFFF: overflow, values from L2);
+    // misc[12] = split-window arrival count
     uint32_t *misc = reinterpret_cast<uint32_t *>(smem + L::MISC);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -214,7 +248,6 @@ __global__ void __launch_bounds__(kThreads, 8)
     const int slice = p.slice_major ? (int)(blockIdx.x / ngrp) : (int)(blockIdx.x % (unsigned)p.nslices);
     const int64_t u = p.slice_major ? (int64_t)(blockIdx.x % ngrp) : (int64_t)(blockIdx.x / (unsigned)p.nslices);
     const int64_t f0 = (int64_t)slice * kFW;
-    const int feat = warp * 32 + lane;  // this thread's feature (TMEM lane) inside the slice
 
     const uint4 ua = __ldg(p.units + 2 * u);
     const uint4 ub = __ldg(p.units + 2 * u + 1);
@@ -223,9 +256,14 @@ __global__ void __launch_bounds__(kThreads, 8)
     const uint32_t nblk = b1 - b0;
     const uint32_t my_rwo = (uint32_t)lane <= nwin ? __ldg(p.rwo + w0 + lane) : 0u;
 
-    auto full_bar = [&](int s) { return smem_u32(&bars[s]); };
-    auto empty_bar = [&](int s) { return smem_u32(&bars[S + s]); };
-    const uint32_t acc_bar = smem_u32(&bars[2 * S]);
+    const uint32_t bar0 = smem_u32(bars);
+    auto chunk_full = [&](int b) { return bar0 + 8u * (uint32_t)b; };
+    auto vals_full = [&](int b) { return bar0 + 8u * (uint32_t)(2 + b); };
+    auto full_t = [&](int s) { return bar0 + 8u * (uint32_t)(4 + s); };
+    auto ready = [&](int s) { return bar0 + 8u * (uint32_t)(4 + ST + s); };
+    auto empty = [&](int s) { return bar0 + 8u * (uint32_t)(4 + ST + SA + s); };
+    auto acc_full = [&](int d) { return bar0 + 8u * (uint32_t)(4 + ST + 2 * SA + d); };
+    auto acc_free = [&](int d) { return bar0 + 8u * (uint32_t)(4 + ST + 2 * SA + ND + d); };
 
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(misc)),
@@ -233,82 +271,139 @@ __global__ void __launch_bounds__(kThreads, 8)
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
     }
-    if (tid == 0) {
+    if (tid == kThreads) {
         asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
-        for (int s = 0; s < S; ++s) {
-            mbar_init(full_bar(s), 1);
-            mbar_init(empty_bar(s), 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(chunk_full(b), 1);
+            mbar_init(vals_full(b), 1);
         }
-        mbar_init(acc_bar, 1);
+        for (int s = 0; s < ST; ++s) mbar_init(full_t(s), 1);
+        for (int s = 0; s < SA; ++s) {
+            mbar_init(ready(s), 4);
+            mbar_init(empty(s), 1);
+        }
+        for (int d = 0; d < ND; ++d) {
+            mbar_init(acc_full(d), 1);
+            mbar_init(acc_free(d), 4);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = misc[0];
-    const uint32_t tmem_d = tmem + (uint32_t)(S * 8);             // accumulator columns
-    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;          // this warp's TMEM lane quarter
-    const uint64_t pol_keep = policy_evict_last();
 
-    // ---- A-stream chunk staging (cp.async, double buffered): blocks [b0 + c*CH, +CH)
-    auto issue_chunk = [&](uint32_t c) {
-        const uint32_t i = c * kCH;
-        if (i < nblk) {
+    // window bookkeeping (identical in every warp): wend = absolute end block of window wi
+    auto first_wend = [&]() { return split ? b1 : __shfl_sync(0xffffffffu, my_rwo, 1); };
+
+    if (warp == 4) {
+        // ================================================= producer + MMA issuer (one thread)
+        if (lane != 0) return;
+        const uint64_t pol_keep = policy_evict_last();
+        // chunk c (blocks [c*CH, +CH)) into buffer c & 1: 16-byte-aligned supersets of the
+        // arrays by bulk copy (the allocations carry the padding)
+        auto issue_chunk = [&](uint32_t c) {
+            const uint32_t i = c * kCH;
+            if (i >= nblk) return;
             const int buf = c & 1;
             const uint32_t b = b0 + i;
             const uint32_t cnt = min((uint32_t)kCH, nblk - i);
-            if ((uint32_t)tid < 2 * cnt)
-                cp_async16(smem_u32(&ch_a2b[buf * kCH * 8 + 4 * tid]), p.a2b + (size_t)b * 8 + 4 * tid);
-            if ((uint32_t)tid < cnt * (uint32_t)p.nw)
-                cp_async8(smem_u32(&ch_bits[(buf * kCH + tid / p.nw) * NWMAX + tid % p.nw]),
-                          p.bits + (size_t)b * p.nw + tid);
-            if ((uint32_t)tid < cnt) cp_async4(smem_u32(&ch_tco[buf * kCH + tid]), p.tco + b + tid);
-        }
-        cp_async_commit();
-    };
-    // ---- leader: two gather4 of block j's 8 B rows into stage s (padding lanes: row -1, zero fill)
-    auto issue_tma = [&](uint32_t j, int s) {
-        const int buf = (j / kCH) & 1;
-        const uint32_t cs = j & (kCH - 1u);
-        const uint4 ca = *reinterpret_cast<const uint4 *>(&ch_a2b[(buf * kCH + cs) * 8]);
-        const uint4 cb = *reinterpret_cast<const uint4 *>(&ch_a2b[(buf * kCH + cs) * 8 + 4]);
-        const uint32_t bar = full_bar(s);
-        const uint32_t dst = smem_u32(stage + s * kStageBytes);
-        mbar_arrive_expect_tx(bar, (uint32_t)kStageBytes);
-        const int32_t col = (int32_t)f0;
-        tma_gather4(dst, &tmap, col, (int32_t)ca.x, (int32_t)ca.y, (int32_t)ca.z, (int32_t)ca.w, bar, pol_keep);
-        tma_gather4(dst + kStageBytes / 2, &tmap, col, (int32_t)cb.x, (int32_t)cb.y, (int32_t)cb.z, (int32_t)cb.w, bar,
-                    pol_keep);
-    };
-    // ---- every thread: its EPT B-tile entries of block j: value or 0, read ahead
-    uint32_t vreg[EPT];
-    auto value_load = [&](uint32_t j) {
-        const int buf = (j / kCH) & 1;
-        const uint32_t cs = j & (kCH - 1u);
-        const uint64_t *wb = &ch_bits[(buf * kCH + cs) * NWMAX];
-        const uint32_t t0 = ch_tco[buf * kCH + cs];
-#pragma unroll
-        for (int i = 0; i < EPT; ++i) {
-            const int e = tid + kThreads * i;
-            const int n = e >> 3, k = e & 7;   // window row n, condensed lane k
-            const int word = n >> 3, bit = (n & 7) * 8 + k;
-            uint32_t v = 0u;
-            if (n < p.wh) {
-                const uint64_t m = wb[word];
-                if ((m >> bit) & 1ull) {
-                    uint32_t idx = t0 + (uint32_t)__popcll(m & ((1ull << bit) - 1ull));
-#pragma unroll
-                    for (int q = 0; q < NWMAX - 1; ++q)
-                        if (q < word) idx += (uint32_t)__popcll(wb[q]);
-                    v = __float_as_uint(__ldg(p.vals + idx));
-                }
+            const uint32_t w_lo = (b * (uint32_t)p.nw) & ~1u, w_hi = ((b + cnt) * (uint32_t)p.nw + 1u) & ~1u;
+            const uint32_t t_lo = b & ~3u, t_hi = (b + cnt + 1u + 3u) & ~3u;
+            misc[4 + buf] = b * (uint32_t)p.nw - w_lo;
+            misc[6 + buf] = b - t_lo;
+            const uint32_t bytes = cnt * 32u + (w_hi - w_lo) * 8u + (t_hi - t_lo) * 4u;
+            mbar_arrive_expect_tx(chunk_full(buf), bytes);
+            bulk_g2s(smem_u32(ch_a2b + buf * kCH * 8), p.a2b + (size_t)b * 8, cnt * 32u, chunk_full(buf));
+            bulk_g2s(smem_u32(ch_bits + buf * L::BITS_BUF), p.bits + w_lo, (w_hi - w_lo) * 8u, chunk_full(buf));
+            bulk_g2s(smem_u32(ch_tco + buf * L::TCO_BUF), p.tco + t_lo, (t_hi - t_lo) * 4u, chunk_full(buf));
+        };
+        // values of chunk c (after its TCOffset landed): [tco[first], tco[last + 1]) superset
+        auto issue_vals = [&](uint32_t c) {
+            const uint32_t i = c * kCH;
+            if (i >= nblk) return;
+            const int buf = c & 1;
+            const uint32_t cnt = min((uint32_t)kCH, nblk - i);
+            const uint32_t *tc = ch_tco + buf * L::TCO_BUF + misc[6 + buf];
+            const uint32_t v_lo = tc[0] & ~3u, v_hi = (tc[cnt] + 3u) & ~3u;
+            if (v_hi - v_lo <= (uint32_t)L::VCAP) {
+                misc[8 + buf] = v_lo;
+                mbar_arrive_expect_tx(vals_full(buf), (v_hi - v_lo) * 4u);
+                if (v_hi > v_lo)
+                    bulk_g2s(smem_u32(ch_vals + buf * L::VALS_BUF), p.vals + v_lo, (v_hi - v_lo) * 4u, vals_full(buf));
+            } else {
+                misc[8 + buf] = 0xFFFFFFFFu;  // too many values for the stage: read from L2
+                mbar_arrive(vals_full(buf));
             }
-            vreg[i] = v;
+        };
+        auto issue_tma = [&](uint32_t j, int s) {
+            const int buf = (j / kCH) & 1;
+            const uint32_t cs = j & (kCH - 1u);
+            const uint4 ca = *reinterpret_cast<const uint4 *>(&ch_a2b[(buf * kCH + cs) * 8]);
+            const uint4 cb = *reinterpret_cast<const uint4 *>(&ch_a2b[(buf * kCH + cs) * 8 + 4]);
+            const uint32_t bar = full_t(s);
+            const uint32_t dst = smem_u32(stage + s * kStageBytes);
+            mbar_arrive_expect_tx(bar, (uint32_t)kStageBytes);
+            const int32_t col = (int32_t)f0;
+            tma_gather4(dst, &tmap, col, (int32_t)ca.x, (int32_t)ca.y, (int32_t)ca.z, (int32_t)ca.w, bar, pol_keep);
+            tma_gather4(dst + kStageBytes / 2, &tmap, col, (int32_t)cb.x, (int32_t)cb.y, (int32_t)cb.z,
+                        (int32_t)cb.w, bar, pol_keep);
+        };
+        if (nblk == 0) return;
+        // window of the block cursor (the transposers zero-write the empty ones)
+        uint32_t wi = 0, wend = split ? b1 : __ldg(p.rwo + w0 + 1);
+        auto advance = [&](uint32_t cursor) {
+            while (!split && wi < nwin && wend == cursor) {
+                ++wi;
+                wend = wi < nwin ? __ldg(p.rwo + w0 + wi + 1) : 0xFFFFFFFFu;
+            }
+        };
+        advance(b0);
+        issue_chunk(0);
+        issue_chunk(1);
+        mbar_wait(chunk_full(0), 0);
+        issue_vals(0);
+        for (int s = 0; s < ST; ++s)
+            if ((uint32_t)s < nblk) issue_tma((uint32_t)s, s);
+        bool first = true;
+        uint32_t accn = 0;  // accumulations started (window or segment)
+        for (uint32_t j = 0; j < nblk; ++j) {
+            const int sa = (int)(j % SA);
+            const uint32_t jb = b0 + j;
+            if (first && accn >= (uint32_t)ND) {  // D[accn % ND] read back by the transposers?
+                mbar_wait(acc_free(accn % ND), ((accn / ND) - 1u) & 1u);
+            }
+            mbar_wait(ready(sa), (j / SA) & 1u);
+            tc_fence_after();
+            const int dsel = (int)(accn % ND);
+            umma_tf32_ts(tmem + (uint32_t)(SA * 8 + dsel * HT), tmem + (uint32_t)(sa * 8),
+                         btile_desc(smem_u32(btile + sa * HT * 8)), IDESC, first ? 0u : 1u);
+            umma_commit(empty(sa));
+            const bool last = split ? (j + 1 == nblk) : (jb + 1 == wend);
+            if (last) {
+                umma_commit(acc_full(dsel));
+                ++accn;
+                advance(jb + 1);
+            }
+            first = last;
+            // chunk c fully consumed once the ready[] of its last block is in: refill with c + 2
+            if ((j & (kCH - 1u)) == kCH - 1u) issue_chunk(j / kCH + 2);
+            const uint32_t jt = j + ST;  // gather of block jt into the stage block j vacated
+            if (jt < nblk) {
+                if ((jt & (kCH - 1u)) == 0) {  // first block of chunk jt/CH: metadata must have landed
+                    const uint32_t c = jt / kCH;
+                    mbar_wait(chunk_full(c & 1), (c >> 1) & 1u);
+                    issue_vals(c);
+                }
+                issue_tma(jt, (int)(j % ST));
+            }
         }
-    };
+        return;
+    }
 
-    // ---- epilogue helpers: rows n < wh of the accumulator to C (or the split workspace);
-    // thread = feature, so every warp-wide store is one coalesced 128-byte row segment
+    // ===================================================== transposers (warps 0-3)
+    const int feat = warp * 32 + lane;                       // feature (TMEM lane) in the slice
+    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;  // this warp's TMEM lane quarter
     auto store_rows = [&](const uint32_t (&d)[HT], int64_t lr0, float *base, int64_t ld, bool remap) {
 #pragma unroll
         for (int n = 0; n < HT; ++n) {
@@ -317,7 +412,7 @@ __global__ void __launch_bounds__(kThreads, 8)
                 if (remap) {
                     if (lr < p.rows) {
                         const int64_t orow = p.row_map ? (int64_t)__ldg(p.row_map + lr) : lr;
-                        __stcs(base + orow * ld + feat, __uint_as_float(d[n]));
+                        __stcs(base + orow * ld + f0 + feat, __uint_as_float(d[n]));
                     }
                 } else {
                     __stcg(base + (int64_t)n * ld + feat, __uint_as_float(d[n]));
@@ -325,100 +420,95 @@ __global__ void __launch_bounds__(kThreads, 8)
             }
         }
     };
-    // accumulator (after the commit of the window's last MMA) -> registers
-    auto load_acc = [&](uint32_t (&d)[HT], uint32_t phase) {
-        mbar_wait(acc_bar, phase & 1u);
+    // accumulator D[dsel] -> registers, then release it to the MMA issuer
+    auto load_acc = [&](uint32_t (&d)[HT], int dsel, uint32_t phase) {
+        mbar_wait(acc_full(dsel), phase & 1u);
         tc_fence_after();
         uint32_t t[16];
 #pragma unroll
         for (int h = 0; h < HT; h += 16) {
-            tmem_ld_x16(tmem_d + lane_off, t, h);
+            tmem_ld_x16(tmem + lane_off + (uint32_t)(SA * 8 + dsel * HT), t, h);
             tmem_wait_ld();
 #pragma unroll
             for (int q = 0; q < 16; ++q) d[h + q] = t[q];
         }
-        tc_fence_before();  // the next window's first MMA overwrites D after the next barrier
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(acc_free(dsel));
     };
     uint32_t zeros[HT];
 #pragma unroll
     for (int q = 0; q < HT; ++q) zeros[q] = 0u;
-
-    // window bookkeeping (uniform across the CTA): wend = absolute end block of window wi
-    uint32_t wi = 0;
-    uint32_t wend = split ? b1 : __shfl_sync(0xffffffffu, my_rwo, 1);
-    uint32_t acc_phase = 0;
     auto window_row0 = [&](uint32_t w) { return (int64_t)(w0 + w) * p.wh; };
-    // empty windows (no blocks) are zero-written; called whenever the block cursor is at jb
-    auto skip_empty = [&](uint32_t jb) {
+
+    uint32_t wi = 0;
+    uint32_t wend = first_wend();
+    auto skip_empty = [&](uint32_t jb) {  // zero-write windows without blocks at cursor jb
         while (!split && wi < nwin && wend == jb) {
-            store_rows(zeros, window_row0(wi), p.C + f0, p.N, true);
+            store_rows(zeros, window_row0(wi), p.C, p.N, true);
             ++wi;
             const uint32_t e = __shfl_sync(0xffffffffu, my_rwo, (int)(wi < nwin ? wi + 1 : nwin));
             wend = wi < nwin ? e : 0xFFFFFFFFu;
         }
     };
-    skip_empty(b0);  // leading empty windows (the first window starts at rwo[w0] = b0)
-
-    // ---- prologue: chunks 0 (waited) and 1, TMA of the first S blocks, values of block 0
-    issue_chunk(0);
-    cp_async_wait_all();
-    __syncthreads();
-    issue_chunk(1);
-    if (tid == 0)
-        for (int s = 0; s < S; ++s)
-            if ((uint32_t)s < nblk) issue_tma((uint32_t)s, s);
-    if (nblk > 0) value_load(0);
-    bool first = true;  // next MMA starts a new accumulation (window or segment start)
-
+    skip_empty(b0);
+    uint32_t accn = 0;
     for (uint32_t j = 0; j < nblk; ++j) {
-        const int s = (int)(j % S);
-        if (j > 0 && (j % kCH) == 0) issue_chunk(j / kCH + 1);
-        mbar_wait(full_bar(s), (j / S) & 1u);
-        if (j >= (uint32_t)S) mbar_wait(empty_bar(s), ((j / S) - 1u) & 1u);
+        const int st = (int)(j % ST), sa = (int)(j % SA), buf = (j / kCH) & 1;
+        const uint32_t cs = j & (kCH - 1u);
+        if (cs == 0) {  // chunk metadata and values of this chunk
+            mbar_wait(chunk_full(buf), ((j / kCH) >> 1) & 1u);
+            mbar_wait(vals_full(buf), ((j / kCH) >> 1) & 1u);
+        }
+        if (j >= (uint32_t)SA) mbar_wait(empty(sa), ((j / SA) - 1u) & 1u);
         tc_fence_after();
-        // gathered rows -> TMEM A[s]: this thread's feature of the 8 rows
-        {
-            const float *st = reinterpret_cast<const float *>(stage + s * kStageBytes);
+        mbar_wait(full_t(st), (j / ST) & 1u);
+        {   // gathered rows -> TMEM A[sa]: this thread's feature of the 8 rows
+            const float *sp = reinterpret_cast<const float *>(stage + st * kStageBytes);
             uint32_t v[8];
 #pragma unroll
             for (int r = 0; r < 8; ++r) {
-                v[r] = __float_as_uint(st[r * kFW + feat]);
+                v[r] = __float_as_uint(sp[r * kFW + feat]);
                 if constexpr (RND) v[r] = tf32_rna_bits(v[r]);
             }
-            tmem_st_x8(tmem + lane_off + (uint32_t)(s * 8), v);
+            tmem_st_x8(tmem + lane_off + (uint32_t)(sa * 8), v);
         }
-        // decoded tile -> B[s] (K-major core matrices: row n, K-half k/4, element k%4)
-        {
-            float *bt = btile + s * HT * 8;
+        {   // decode of this warp's tile rows -> B[sa] (K-major core matrices)
+            const uint64_t *wb = ch_bits + buf * L::BITS_BUF + misc[4 + buf] + cs * (uint32_t)p.nw;
+            const uint32_t t0 = ch_tco[buf * L::TCO_BUF + misc[6 + buf] + cs];
+            const uint32_t vlo = misc[8 + buf];
+            float *bt = btile + sa * HT * 8;
 #pragma unroll
-            for (int i = 0; i < EPT; ++i) {
+            for (int i = 0; i < EPL; ++i) {
                 const int e = tid + kThreads * i;
-                const int n = e >> 3, k = e & 7;
-                bt[(n >> 3) * 64 + (k >> 2) * 32 + (n & 7) * 4 + (k & 3)] = __uint_as_float(vreg[i]);
+                const int n = e >> 3, k = e & 7;  // window row n, condensed lane k
+                const int word = n >> 3, bit = (n & 7) * 8 + k;
+                float v = 0.f;
+                if (n < p.wh) {
+                    const uint64_t m = wb[word];
+                    if ((m >> bit) & 1ull) {
+                        uint32_t idx = t0 + (uint32_t)__popcll(m & ((1ull << bit) - 1ull));
+#pragma unroll
+                        for (int q = 0; q < NWMAX - 1; ++q)
+                            if (q < word) idx += (uint32_t)__popcll(wb[q]);
+                        v = vlo != 0xFFFFFFFFu ? ch_vals[buf * L::VALS_BUF + (idx - vlo)] : __ldg(p.vals + idx);
+                    }
+                }
+                bt[(n >> 3) * 64 + (k >> 2) * 32 + (n & 7) * 4 + (k & 3)] = v;
             }
         }
         tmem_wait_st();
         fence_proxy_async_smem();
         tc_fence_before();
-        if (((j + S) % kCH) == 0) cp_async_wait_all();  // chunk of block j + S must be resident
-        __syncthreads();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(ready(sa));
         const uint32_t jb = b0 + j;
-        const bool last_of_window = split ? (j + 1 == nblk) : (jb + 1 == wend);
-        if (tid == 0) {
-            tc_fence_after();
-            umma_tf32_ts(tmem_d, tmem + (uint32_t)(s * 8), btile_desc(smem_u32(btile + s * HT * 8)), IDESC,
-                         first ? 0u : 1u);
-            umma_commit(empty_bar(s));
-            if (last_of_window) umma_commit(acc_bar);
-            if (j + S < nblk) issue_tma(j + S, s);
-        }
-        first = last_of_window;
-        if (j + 1 < nblk) value_load(j + 1);
-        if (last_of_window && !split) {
+        const bool last = split ? (j + 1 == nblk) : (jb + 1 == wend);
+        if (last && !split) {
             uint32_t d[HT];
-            load_acc(d, acc_phase);
-            ++acc_phase;
-            store_rows(d, window_row0(wi), p.C + f0, p.N, true);
+            load_acc(d, (int)(accn % ND), accn / ND);
+            ++accn;
+            store_rows(d, window_row0(wi), p.C, p.N, true);
             ++wi;
             const uint32_t e = __shfl_sync(0xffffffffu, my_rwo, (int)(wi < nwin ? wi + 1 : nwin));
             wend = wi < nwin ? e : 0xFFFFFFFFu;
@@ -433,18 +523,17 @@ __global__ void __launch_bounds__(kThreads, 8)
         const int64_t tile_elems = (int64_t)p.wh * kFW;
         float *tile = p.ws + ((int64_t)slot * p.nslices + slice) * tile_elems;
         uint32_t d[HT];
-        if (nblk > 0) {
-            load_acc(d, acc_phase);
-        } else {
+        if (nblk > 0) load_acc(d, 0, 0);
+        else {
 #pragma unroll
             for (int q = 0; q < HT; ++q) d[q] = 0u;
         }
         store_rows(d, 0, tile, kFW, false);
         __threadfence();
-        __syncthreads();
-        if (tid == 0) misc[2] = atomicAdd(p.counters + (int64_t)sid * p.nslices + slice, 1u);
-        __syncthreads();
-        if (misc[2] == nseg - 1) {
+        asm volatile("bar.sync 1, 128;\n" ::: "memory");
+        if (tid == 0) misc[12] = atomicAdd(p.counters + (int64_t)sid * p.nslices + slice, 1u);
+        asm volatile("bar.sync 1, 128;\n" ::: "memory");
+        if (misc[12] == nseg - 1) {
             __threadfence();
             const float *firstp = p.ws + ((int64_t)(slot - seg) * p.nslices + slice) * tile_elems;
             float acc[HT];
@@ -459,13 +548,13 @@ __global__ void __launch_bounds__(kThreads, 8)
             uint32_t r[HT];
 #pragma unroll
             for (int q = 0; q < HT; ++q) r[q] = __float_as_uint(acc[q]);
-            store_rows(r, window_row0(0), p.C + f0, p.N, true);
+            store_rows(r, window_row0(0), p.C, p.N, true);
             if (tid == 0) p.counters[(int64_t)sid * p.nslices + slice] = 0u;  // re-arm for the next execute
         }
     }
-
+    // every MMA was waited for (acc_full) before its accumulator was read: free TMEM
     tc_fence_before();
-    __syncthreads();
+    asm volatile("bar.sync 1, 128;\n" ::: "memory");
     tc_fence_after();
     if (warp == 0)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"((uint32_t)L::TMEM_COLS)
@@ -504,11 +593,11 @@ accspmm_status tensor_map_tc05(const DevicePlan &d, const void *B, int64_t N, co
     return ACCSPMM_OK;
 }
 
-template <int HT, int S, bool RND>
+template <int HT, int ST, int SA, int ND, bool RND>
 accspmm_status launch_tc(const TcParams &tp, const CUtensorMap *map, cudaStream_t stream)
 {
-    using L = TcLayout<HT, S>;
-    auto kern = spmm_tc05_kernel<HT, S, RND>;
+    using L = TcLayout<HT, ST, SA, ND>;
+    auto kern = spmm_tc05_kernel<HT, ST, SA, ND, RND>;
     static int configured_device = -1;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -519,7 +608,7 @@ accspmm_status launch_tc(const TcParams &tp, const CUtensorMap *map, cudaStream_
     }
     const int64_t grid = tp.n_units * tp.nslices;
     if (grid > 0x7FFFFFFFll) return fail(ACCSPMM_ERR_UNSUPPORTED, "grid too large");
-    kern<<<(unsigned)grid, kThreads, L::BYTES, stream>>>(tp, *map);
+    kern<<<(unsigned)grid, kThreads + 32, L::BYTES, stream>>>(tp, *map);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(ACCSPMM_ERR_CUDA, std::string("tcgen05 spmm launch: ") + cudaGetErrorString(e));
     return ACCSPMM_OK;
@@ -557,8 +646,10 @@ accspmm_status launch_spmm_tc05(const DevicePlan &d, const void *B, int64_t N, f
         if (st != ACCSPMM_OK) return st;
     }
     cudaStream_t s = (cudaStream_t)stream;
-    if (d.wh <= 16) return round_b ? launch_tc<16, 6, true>(tp, map, s) : launch_tc<16, 6, false>(tp, map, s);
-    return round_b ? launch_tc<32, 4, true>(tp, map, s) : launch_tc<32, 4, false>(tp, map, s);
+    // ring depths: ST gather stages (L2 latency), SA TMEM/B-tile stages (MMA latency), ND
+    // accumulators (epilogue overlap for short windows); TMEM 64 columns -> 8 CTAs per SM
+    if (d.wh <= 16) return round_b ? launch_tc<16, 6, 4, 2, true>(tp, map, s) : launch_tc<16, 6, 4, 2, false>(tp, map, s);
+    return round_b ? launch_tc<32, 6, 4, 1, true>(tp, map, s) : launch_tc<32, 6, 4, 1, false>(tp, map, s);
 }
 
 }  // namespace accspmm
