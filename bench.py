@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--unit-cap", type=int, default=0)
     ap.add_argument("--permute-cols", action="store_true", help="symmetric reordering: relabel columns too")
     ap.add_argument("--build", default="device", choices=["host", "device"], help="BitTCF builder")
+    ap.add_argument("--window-rows", type=int, default=0, help="rows per RowWindow: 0/8 = paper, 16/32 = tall (R20)")
+    ap.add_argument("--kernel", default="auto", choices=["auto", "mma_sync", "tcgen05"])
     ap.add_argument("--allgather", default="none", choices=["none", "nccl", "fused"],
                     help="N > 1: also time assembling the full C on every rank (NCCL all-gather + "
                          "un-permute, or the fused epilogue into symmetric memory); reported as "
@@ -151,7 +153,8 @@ def ncu_traffic(args, world):
            "-k", "regex:spmm_", "-s", "2", "-c", "1", "--csv",
            sys.executable, os.path.abspath(__file__), "--ncu-child", "--config", args.config, "--N", str(args.N),
            "--precision", args.precision, "--reorder", args.reorder, "--balance", args.balance,
-           "--unit-cap", str(args.unit_cap), "--build", args.build]
+           "--unit-cap", str(args.unit_cap), "--build", args.build, "--window-rows", str(args.window_rows),
+           "--kernel", args.kernel]
     if args.permute_cols:
         cmd.append("--permute-cols")
     env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK=os.environ.get("LOCAL_RANK", "0"))
@@ -193,7 +196,8 @@ def run_ncu_child(args):
     cfg, A, vals, B = make_inputs(args)
     plan = acc.Plan(A.M, A.K, A.rowptr, A.colidx, vals, precision=args.precision, reorder=args.reorder,
                     balance=args.balance, unit_cap=args.unit_cap, device=torch.cuda.current_device(),
-                    permute_cols=args.permute_cols, build=args.build)
+                    permute_cols=args.permute_cols, build=args.build, window_rows=args.window_rows,
+                    kernel=args.kernel)
     Bd = torch.from_numpy(B).to(device="cuda", dtype=torch.float16 if args.precision == "fp16" else torch.float32)
     C = torch.empty((plan.out_rows, args.N), dtype=torch.float32, device="cuda")
     for _ in range(3):
@@ -300,11 +304,15 @@ def workload_config(args, cfg, A, world):
             "N": args.N, "precision": args.precision, "reorder": args.reorder, "balance": args.balance,
             "permute_cols": bool(getattr(args, "permute_cols", False)),
             "l2": "none" if args.no_flush else f"flushed between timed steps ({L2_FLUSH_BYTES >> 20} MiB write)",
+            "window_rows": args.window_rows or 8, "kernel": args.kernel,
             "parallelism": f"rowwindow-nnz-partition x{world}"}
 
 
 def kernel_name(plan):
     """The SpMM kernel the library's dispatch picks for this plan."""
+    if plan.info["kernel"] == 2:
+        return ("spmm_tc05_kernel (TMA gather4 -> TMEM, tcgen05.mma kind::tf32, accumulators in TMEM; "
+                f"{plan.info['window_rows']}-row windows)")
     return "spmm_bittcf_g4_kernel (TMA gather4 + mma.sync, 1 warp/CTA)"
 
 
@@ -383,7 +391,8 @@ def main():
     t0 = time.perf_counter()
     plan = acc.Plan(A.M, A.K, A.rowptr, A.colidx, vals, precision=args.precision, reorder=args.reorder,
                     balance=args.balance, unit_cap=args.unit_cap, part=rank, nparts=world, device=local,
-                    permute_cols=args.permute_cols, build=args.build)
+                    permute_cols=args.permute_cols, build=args.build, window_rows=args.window_rows,
+                    kernel=args.kernel)
     plan_s = time.perf_counter() - t0
     info = plan.info
     tdt = torch.float16 if args.precision == "fp16" else torch.float32
