@@ -161,12 +161,13 @@ __device__ __forceinline__ uint32_t tf32_rna_bits(uint32_t x)
 // ------------------------------------------------------------------ the kernel
 //
 // Warp roles (160 threads): warps 0-3 = transposers (thread = feature of the 128-feature
-// slice: TMEM lane quarter = warp), warp 4 lane 0 = producer (A-stream chunks and values by
-// bulk copy, B-row gathers by TMA) and MMA issuer.  They synchronise only through mbarriers:
+// slice: TMEM lane quarter = warp), warp 4 = producer: its lanes decode the tile (lane = tile
+// row), lane 0 issues the A-stream chunk and value bulk copies, the B-row gathers (TMA) and
+// the MMAs.  They synchronise only through mbarriers:
 //   chunk_full[2]  bulk copies of a chunk's SparseAToB / TCLocalBit / TCOffset (tx bytes)
 //   vals_full[2]   bulk copy of the chunk's value range (or an overflow flag: values from L2)
 //   full_t[ST]     TMA gather of a block's 8 B rows (tx bytes)
-//   ready[SA]      4 transposer warps: A[sa] in TMEM and the decoded tile B[sa] in smem
+//   ready[SA]      4 transposer warps: A[sa] in TMEM (the producer decoded B[sa] itself)
 //   empty[SA]      tcgen05.commit: the MMA that read A[sa] / B[sa] has completed
 //   acc_full[ND]   tcgen05.commit after a window's (segment's) last MMA
 //   acc_free[ND]   4 transposer warps: accumulator read back, D may be overwritten
@@ -211,7 +212,6 @@ __global__ void __launch_bounds__(kThreads + 32, 6)
 {
     using L = TcLayout<HT, ST, SA, ND>;
     constexpr int NWMAX = L::NWMAX;
-    constexpr int EPL = HT * 8 / kThreads;  // B-tile entries decoded per transposer thread (1 or 2)
     // instruction descriptor: D F32 (bit 4), A/B TF32 (bits 7, 10), K-major A and B,
     // N >> 3 at bit 17, M >> 4 at bit 24 (M = 128)
     constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(HT >> 3) << 17) | (8u << 24);
@@ -282,8 +282,7 @@ __global__ void __launch_bounds__(kThreads + 32, 6)
     auto first_wend = [&]() { return split ? b1 : __shfl_sync(0xffffffffu, my_rwo, 1); };
 
     if (warp == 4) {
-        // ================================================= producer + MMA issuer (one thread)
-        if (lane != 0) return;
+        // ============================== producer warp: decode (32 lanes), MMA + copies (lane 0)
         const uint64_t pol_keep = policy_evict_last();
         // chunk c (blocks [c*CH, +CH)) into buffer c & 1: 16-byte-aligned supersets of the
         // arrays by bulk copy (the allocations carry the padding)
@@ -344,44 +343,88 @@ __global__ void __launch_bounds__(kThreads + 32, 6)
             }
         };
         advance(b0);
-        issue_chunk(0);
-        issue_chunk(1);
-        mbar_wait(chunk_full(0), 0);
-        issue_vals(0);
-        for (int s = 0; s < ST; ++s)
-            if ((uint32_t)s < nblk) issue_tma((uint32_t)s, s);
+        if (lane == 0) {
+            issue_chunk(0);
+            issue_chunk(1);
+            mbar_wait(chunk_full(0), 0);
+            issue_vals(0);
+            for (int s = 0; s < ST; ++s)
+                if ((uint32_t)s < nblk) issue_tma((uint32_t)s, s);
+        }
+        __syncwarp();
         bool first = true;
         uint32_t accn = 0;  // accumulations started (window or segment)
+        const int n = lane;  // decode: lane = tile row
         for (uint32_t j = 0; j < nblk; ++j) {
-            const int sa = (int)(j % SA);
+            const int sa = (int)(j % SA), buf = (j / kCH) & 1;
+            const uint32_t cs = j & (kCH - 1u);
             const uint32_t jb = b0 + j;
-            if (first && accn >= (uint32_t)ND) {  // D[accn % ND] read back by the transposers?
-                mbar_wait(acc_free(accn % ND), ((accn / ND) - 1u) & 1u);
+            if (cs == 0) {
+                mbar_wait(chunk_full(buf), ((j / kCH) >> 1) & 1u);
+                mbar_wait(vals_full(buf), ((j / kCH) >> 1) & 1u);
             }
-            mbar_wait(ready(sa), (j / SA) & 1u);
-            tc_fence_after();
-            const int dsel = (int)(accn % ND);
-            umma_tf32_ts(tmem + (uint32_t)(SA * 8 + dsel * HT), tmem + (uint32_t)(sa * 8),
-                         btile_desc(smem_u32(btile + sa * HT * 8)), IDESC, first ? 0u : 1u);
-            umma_commit(empty(sa));
+            if (j >= (uint32_t)SA) mbar_wait(empty(sa), ((j / SA) - 1u) & 1u);
+            // decode of tile row n: its occupancy byte, the rank of its first value
+            // (values ascend by tile position r*8 + lane, so a row's values are one run), and
+            // the row's 8 entries into B[sa] (K-major core matrices: two 16-byte halves)
+            if (n < HT) {
+                float r[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) r[k] = 0.f;
+                if (n < p.wh) {
+                    const uint64_t *wb = ch_bits + buf * L::BITS_BUF + misc[4 + buf] + cs * (uint32_t)p.nw;
+                    const int word = n >> 3, sh = (n & 7) * 8;
+                    const uint64_t m = wb[word];
+                    const uint32_t byte = (uint32_t)(m >> sh) & 0xFFu;
+                    if (byte) {
+                        uint32_t idx = ch_tco[buf * L::TCO_BUF + misc[6 + buf] + cs] +
+                                       (uint32_t)__popcll(m & ((1ull << sh) - 1ull));
+#pragma unroll
+                        for (int q = 0; q < NWMAX - 1; ++q)
+                            if (q < word) idx += (uint32_t)__popcll(wb[q]);
+                        const uint32_t vlo = misc[8 + buf];
+                        const float *vsrc = vlo != 0xFFFFFFFFu ? ch_vals + buf * L::VALS_BUF + (idx - vlo) : p.vals + idx;
+                        int c = 0;
+#pragma unroll
+                        for (int k = 0; k < 8; ++k)
+                            if ((byte >> k) & 1u) r[k] = vsrc[c++];
+                    }
+                }
+                float *bt = btile + sa * HT * 8 + (n >> 3) * 64 + (n & 7) * 4;
+                *reinterpret_cast<float4 *>(bt) = make_float4(r[0], r[1], r[2], r[3]);
+                *reinterpret_cast<float4 *>(bt + 32) = make_float4(r[4], r[5], r[6], r[7]);
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
             const bool last = split ? (j + 1 == nblk) : (jb + 1 == wend);
+            if (lane == 0) {
+                if (first && accn >= (uint32_t)ND)  // D[accn % ND] read back by the transposers?
+                    mbar_wait(acc_free(accn % ND), ((accn / ND) - 1u) & 1u);
+                mbar_wait(ready(sa), (j / SA) & 1u);
+                tc_fence_after();
+                const int dsel = (int)(accn % ND);
+                umma_tf32_ts(tmem + (uint32_t)(SA * 8 + dsel * HT), tmem + (uint32_t)(sa * 8),
+                             btile_desc(smem_u32(btile + sa * HT * 8)), IDESC, first ? 0u : 1u);
+                umma_commit(empty(sa));
+                if (last) umma_commit(acc_full(dsel));
+                // chunk c fully consumed once the ready[] of its last block is in: refill with c + 2
+                if (cs == kCH - 1u) issue_chunk(j / kCH + 2);
+                const uint32_t jt = j + ST;  // gather of block jt into the stage block j vacated
+                if (jt < nblk) {
+                    if ((jt & (kCH - 1u)) == 0) {  // first block of chunk jt/CH: metadata must have landed
+                        const uint32_t c = jt / kCH;
+                        mbar_wait(chunk_full(c & 1), (c >> 1) & 1u);
+                        issue_vals(c);
+                    }
+                    issue_tma(jt, (int)(j % ST));
+                }
+            }
+            __syncwarp();
             if (last) {
-                umma_commit(acc_full(dsel));
                 ++accn;
                 advance(jb + 1);
             }
             first = last;
-            // chunk c fully consumed once the ready[] of its last block is in: refill with c + 2
-            if ((j & (kCH - 1u)) == kCH - 1u) issue_chunk(j / kCH + 2);
-            const uint32_t jt = j + ST;  // gather of block jt into the stage block j vacated
-            if (jt < nblk) {
-                if ((jt & (kCH - 1u)) == 0) {  // first block of chunk jt/CH: metadata must have landed
-                    const uint32_t c = jt / kCH;
-                    mbar_wait(chunk_full(c & 1), (c >> 1) & 1u);
-                    issue_vals(c);
-                }
-                issue_tma(jt, (int)(j % ST));
-            }
         }
         return;
     }
@@ -439,12 +482,7 @@ __global__ void __launch_bounds__(kThreads + 32, 6)
     skip_empty(b0);
     uint32_t accn = 0;
     for (uint32_t j = 0; j < nblk; ++j) {
-        const int st = (int)(j % ST), sa = (int)(j % SA), buf = (j / kCH) & 1;
-        const uint32_t cs = j & (kCH - 1u);
-        if (cs == 0) {  // chunk metadata and values of this chunk
-            mbar_wait(chunk_full(buf), ((j / kCH) >> 1) & 1u);
-            mbar_wait(vals_full(buf), ((j / kCH) >> 1) & 1u);
-        }
+        const int st = (int)(j % ST), sa = (int)(j % SA);
         if (j >= (uint32_t)SA) mbar_wait(empty(sa), ((j / SA) - 1u) & 1u);
         tc_fence_after();
         mbar_wait(full_t(st), (j / ST) & 1u);
@@ -458,32 +496,7 @@ __global__ void __launch_bounds__(kThreads + 32, 6)
             }
             tmem_st_x8(tmem + lane_off + (uint32_t)(sa * 8), v);
         }
-        {   // decode of this warp's tile rows -> B[sa] (K-major core matrices)
-            const uint64_t *wb = ch_bits + buf * L::BITS_BUF + misc[4 + buf] + cs * (uint32_t)p.nw;
-            const uint32_t t0 = ch_tco[buf * L::TCO_BUF + misc[6 + buf] + cs];
-            const uint32_t vlo = misc[8 + buf];
-            float *bt = btile + sa * HT * 8;
-#pragma unroll
-            for (int i = 0; i < EPL; ++i) {
-                const int e = tid + kThreads * i;
-                const int n = e >> 3, k = e & 7;  // window row n, condensed lane k
-                const int word = n >> 3, bit = (n & 7) * 8 + k;
-                float v = 0.f;
-                if (n < p.wh) {
-                    const uint64_t m = wb[word];
-                    if ((m >> bit) & 1ull) {
-                        uint32_t idx = t0 + (uint32_t)__popcll(m & ((1ull << bit) - 1ull));
-#pragma unroll
-                        for (int q = 0; q < NWMAX - 1; ++q)
-                            if (q < word) idx += (uint32_t)__popcll(wb[q]);
-                        v = vlo != 0xFFFFFFFFu ? ch_vals[buf * L::VALS_BUF + (idx - vlo)] : __ldg(p.vals + idx);
-                    }
-                }
-                bt[(n >> 3) * 64 + (k >> 2) * 32 + (n & 7) * 4 + (k & 3)] = v;
-            }
-        }
         tmem_wait_st();
-        fence_proxy_async_smem();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(ready(sa));
