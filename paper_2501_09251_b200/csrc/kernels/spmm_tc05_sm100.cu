@@ -78,6 +78,36 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t byt
 {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
 }
+// Waits on an mbarrier phase.  WM = 0: try_wait with a suspend-time hint (the thread may
+// sleep until the phase completes); 1: test_wait spin (never sleeps); 2: try_wait without hint.
+template <int WM>
+__device__ __forceinline__ void mbar_wait_m(uint32_t bar, uint32_t phase)
+{
+    if constexpr (WM == 1) {
+        asm volatile(
+            "{\n\t.reg .pred P1;\n\t"
+            "WAIT_%=:\n\t"
+            "mbarrier.test_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+            "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(bar), "r"(phase)
+            : "memory");
+    } else if constexpr (WM == 2) {
+        asm volatile(
+            "{\n\t.reg .pred P1;\n\t"
+            "WAIT_%=:\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+            "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(bar), "r"(phase)
+            : "memory");
+    } else {
+        asm volatile(
+            "{\n\t.reg .pred P1;\n\t"
+            "WAIT_%=:\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+            "@P1 bra DONE_%=;\n\t"
+            "bra WAIT_%=;\n\t"
+            "DONE_%=:\n\t}\n" ::"r"(bar), "r"(phase), "r"(0x989680)
+            : "memory");
+    }
+}
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase)
 {
     asm volatile(
@@ -206,10 +236,11 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t
                  : "memory");
 }
 
-template <int HT, int ST, int SA, int ND, bool RND>
+template <int HT, int ST, int SA, int ND, bool RND, int WM = 0>
 __global__ void __launch_bounds__(kThreads + 32, 6)
     spmm_tc05_kernel(const TcParams p, const __grid_constant__ CUtensorMap tmap)
 {
+    auto mbar_wait = [](uint32_t bar, uint32_t phase) { mbar_wait_m<WM>(bar, phase); };
     using L = TcLayout<HT, ST, SA, ND>;
     constexpr int NWMAX = L::NWMAX;
     // instruction descriptor: D F32 (bit 4), A/B TF32 (bits 7, 10), K-major A and B,
@@ -591,11 +622,11 @@ accspmm_status tensor_map_tc05(const DevicePlan &d, const void *B, int64_t N, co
     return ACCSPMM_OK;
 }
 
-template <int HT, int ST, int SA, int ND, bool RND>
+template <int HT, int ST, int SA, int ND, bool RND, int WM = 0>
 accspmm_status launch_tc(const TcParams &tp, const CUtensorMap *map, cudaStream_t stream)
 {
     using L = TcLayout<HT, ST, SA, ND>;
-    auto kern = spmm_tc05_kernel<HT, ST, SA, ND, RND>;
+    auto kern = spmm_tc05_kernel<HT, ST, SA, ND, RND, WM>;
     static int configured_device = -1;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -644,6 +675,25 @@ accspmm_status launch_spmm_tc05(const DevicePlan &d, const void *B, int64_t N, f
         if (st != ACCSPMM_OK) return st;
     }
     cudaStream_t s = (cudaStream_t)stream;
+#ifdef ACCSPMM_VARIANTS
+    // measurement variants of the tcgen05 kernel (ACCSPMM_KCFG): wait flavour
+    // (60: test_wait spin, 61: try_wait without a suspend hint) and deeper TMEM rings (62/63: SA 8)
+    switch (knobs().kcfg) {
+    case 60:
+        if (d.wh <= 16) return round_b ? launch_tc<16, 6, 4, 2, true, 1>(tp, map, s) : launch_tc<16, 6, 4, 2, false, 1>(tp, map, s);
+        return round_b ? launch_tc<32, 6, 4, 1, true, 1>(tp, map, s) : launch_tc<32, 6, 4, 1, false, 1>(tp, map, s);
+    case 61:
+        if (d.wh <= 16) return round_b ? launch_tc<16, 6, 4, 2, true, 2>(tp, map, s) : launch_tc<16, 6, 4, 2, false, 2>(tp, map, s);
+        return round_b ? launch_tc<32, 6, 4, 1, true, 2>(tp, map, s) : launch_tc<32, 6, 4, 1, false, 2>(tp, map, s);
+    case 62:
+        if (d.wh <= 16) return round_b ? launch_tc<16, 8, 8, 2, true, 1>(tp, map, s) : launch_tc<16, 8, 8, 2, false, 1>(tp, map, s);
+        return round_b ? launch_tc<32, 8, 8, 1, true, 1>(tp, map, s) : launch_tc<32, 8, 8, 1, false, 1>(tp, map, s);
+    case 63:
+        if (d.wh <= 16) return round_b ? launch_tc<16, 8, 8, 2, true, 0>(tp, map, s) : launch_tc<16, 8, 8, 2, false, 0>(tp, map, s);
+        return round_b ? launch_tc<32, 8, 8, 1, true, 0>(tp, map, s) : launch_tc<32, 8, 8, 1, false, 0>(tp, map, s);
+    default: break;
+    }
+#endif
     // ring depths: ST gather stages (L2 latency), SA TMEM/B-tile stages (MMA latency), ND
     // accumulators (epilogue overlap for short windows); TMEM 64 columns -> 8 CTAs per SM
     if (d.wh <= 16) return round_b ? launch_tc<16, 6, 4, 2, true>(tp, map, s) : launch_tc<16, 6, 4, 2, false>(tp, map, s);

@@ -50,11 +50,13 @@ def main():
             os.environ["ACCSPMM_GROUP_CAP"] = kv["gcap"]
         else:
             os.environ.pop("ACCSPMM_GROUP_CAP", None)
-        key = (prec, kv.get("balance", "auto"), int(kv.get("cap", 0)), kv.get("reorder", "off"), kv.get("gcap"))
+        key = (prec, kv.get("balance", "auto"), int(kv.get("cap", 0)), kv.get("reorder", "off"), kv.get("gcap"),
+               int(kv.get("wh", 0)), kv.get("kernel", "auto"))
         if key not in plans:
             t0 = time.perf_counter()
             plans[key] = acc.Plan(A.M, A.K, A.rowptr, A.colidx, vals, precision=prec, balance=key[1],
-                                  unit_cap=key[2], reorder=key[3])
+                                  unit_cap=key[2], reorder=key[3], window_rows=key[5], kernel=key[6],
+                                  build="device")
             plans[key].create_s = time.perf_counter() - t0
         p = plans[key]
         if (prec, N) not in Bs:
