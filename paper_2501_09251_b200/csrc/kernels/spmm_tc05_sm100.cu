@@ -236,10 +236,12 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t
                  : "memory");
 }
 
-template <int HT, int ST, int SA, int ND, bool RND, int WM = 0>
+// CP = commit period: one tcgen05.commit frees CP consecutive A / B stages (CP divides SA)
+template <int HT, int ST, int SA, int ND, bool RND, int WM = 0, int CP = 1>
 __global__ void __launch_bounds__(kThreads + 32, 6)
     spmm_tc05_kernel(const TcParams p, const __grid_constant__ CUtensorMap tmap)
 {
+    static_assert(SA % CP == 0, "commit period must divide the stage count");
     auto mbar_wait = [](uint32_t bar, uint32_t phase) { mbar_wait_m<WM>(bar, phase); };
     using L = TcLayout<HT, ST, SA, ND>;
     constexpr int NWMAX = L::NWMAX;
@@ -277,7 +279,8 @@ __global__ void __launch_bounds__(kThreads + 32, 6)
     auto vals_full = [&](int b) { return bar0 + 8u * (uint32_t)(2 + b); };
     auto full_t = [&](int s) { return bar0 + 8u * (uint32_t)(4 + s); };
     auto ready = [&](int s) { return bar0 + 8u * (uint32_t)(4 + ST + s); };
-    auto empty = [&](int s) { return bar0 + 8u * (uint32_t)(4 + ST + SA + s); };
+    // empty barrier of the stage group holding block j (groups of CP stages)
+    auto empty = [&](uint32_t j) { return bar0 + 8u * (uint32_t)(4 + ST + SA + (int)((j / CP) % (SA / CP))); };
     auto acc_full = [&](int d) { return bar0 + 8u * (uint32_t)(4 + ST + 2 * SA + d); };
     auto acc_free = [&](int d) { return bar0 + 8u * (uint32_t)(4 + ST + 2 * SA + ND + d); };
 
@@ -296,7 +299,7 @@ __global__ void __launch_bounds__(kThreads + 32, 6)
         for (int s = 0; s < ST; ++s) mbar_init(full_t(s), 1);
         for (int s = 0; s < SA; ++s) {
             mbar_init(ready(s), 4);
-            mbar_init(empty(s), 1);
+            mbar_init(bar0 + 8u * (uint32_t)(4 + ST + SA + s), 1);
         }
         for (int d = 0; d < ND; ++d) {
             mbar_init(acc_full(d), 1);
@@ -394,7 +397,7 @@ __global__ void __launch_bounds__(kThreads + 32, 6)
                 mbar_wait(chunk_full(buf), ((j / kCH) >> 1) & 1u);
                 mbar_wait(vals_full(buf), ((j / kCH) >> 1) & 1u);
             }
-            if (j >= (uint32_t)SA) mbar_wait(empty(sa), ((j / SA) - 1u) & 1u);
+            if (j >= (uint32_t)SA) mbar_wait(empty(j), ((j / SA) - 1u) & 1u);
             // decode of tile row n: its occupancy byte, the rank of its first value
             // (values ascend by tile position r*8 + lane, so a row's values are one run), and
             // the row's 8 entries into B[sa] (K-major core matrices: two 16-byte halves)
@@ -436,7 +439,7 @@ __global__ void __launch_bounds__(kThreads + 32, 6)
                 const int dsel = (int)(accn % ND);
                 umma_tf32_ts(tmem + (uint32_t)(SA * 8 + dsel * HT), tmem + (uint32_t)(sa * 8),
                              btile_desc(smem_u32(btile + sa * HT * 8)), IDESC, first ? 0u : 1u);
-                umma_commit(empty(sa));
+                if ((j % CP) == CP - 1 || j + 1 == nblk) umma_commit(empty(j));
                 if (last) umma_commit(acc_full(dsel));
                 // chunk c fully consumed once the ready[] of its last block is in: refill with c + 2
                 if (cs == kCH - 1u) issue_chunk(j / kCH + 2);
@@ -514,7 +517,7 @@ __global__ void __launch_bounds__(kThreads + 32, 6)
     uint32_t accn = 0;
     for (uint32_t j = 0; j < nblk; ++j) {
         const int st = (int)(j % ST), sa = (int)(j % SA);
-        if (j >= (uint32_t)SA) mbar_wait(empty(sa), ((j / SA) - 1u) & 1u);
+        if (j >= (uint32_t)SA) mbar_wait(empty(j), ((j / SA) - 1u) & 1u);
         tc_fence_after();
         mbar_wait(full_t(st), (j / ST) & 1u);
         {   // gathered rows -> TMEM A[sa]: this thread's feature of the 8 rows
@@ -622,11 +625,11 @@ accspmm_status tensor_map_tc05(const DevicePlan &d, const void *B, int64_t N, co
     return ACCSPMM_OK;
 }
 
-template <int HT, int ST, int SA, int ND, bool RND, int WM = 0>
+template <int HT, int ST, int SA, int ND, bool RND, int WM = 0, int CP = 1>
 accspmm_status launch_tc(const TcParams &tp, const CUtensorMap *map, cudaStream_t stream)
 {
     using L = TcLayout<HT, ST, SA, ND>;
-    auto kern = spmm_tc05_kernel<HT, ST, SA, ND, RND, WM>;
+    auto kern = spmm_tc05_kernel<HT, ST, SA, ND, RND, WM, CP>;
     static int configured_device = -1;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -691,6 +694,12 @@ accspmm_status launch_spmm_tc05(const DevicePlan &d, const void *B, int64_t N, f
     case 63:
         if (d.wh <= 16) return round_b ? launch_tc<16, 8, 8, 2, true, 0>(tp, map, s) : launch_tc<16, 8, 8, 2, false, 0>(tp, map, s);
         return round_b ? launch_tc<32, 8, 8, 1, true, 0>(tp, map, s) : launch_tc<32, 8, 8, 1, false, 0>(tp, map, s);
+    case 64:  // one commit per 2 MMAs
+        if (d.wh <= 16) return round_b ? launch_tc<16, 6, 4, 2, true, 0, 2>(tp, map, s) : launch_tc<16, 6, 4, 2, false, 0, 2>(tp, map, s);
+        return round_b ? launch_tc<32, 6, 4, 1, true, 0, 2>(tp, map, s) : launch_tc<32, 6, 4, 1, false, 0, 2>(tp, map, s);
+    case 65:  // one commit per 4 MMAs, 8 stages
+        if (d.wh <= 16) return round_b ? launch_tc<16, 8, 8, 2, true, 0, 4>(tp, map, s) : launch_tc<16, 8, 8, 2, false, 0, 4>(tp, map, s);
+        return round_b ? launch_tc<32, 8, 8, 1, true, 0, 4>(tp, map, s) : launch_tc<32, 8, 8, 1, false, 0, 4>(tp, map, s);
     default: break;
     }
 #endif
