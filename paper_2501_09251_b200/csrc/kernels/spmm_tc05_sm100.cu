@@ -191,13 +191,12 @@ __device__ __forceinline__ uint32_t tf32_rna_bits(uint32_t x)
 // ------------------------------------------------------------------ the kernel
 //
 // Warp roles (160 threads): warps 0-3 = transposers (thread = feature of the 128-feature
-// slice: TMEM lane quarter = warp), warp 4 = producer: its lanes decode the tile (lane = tile
-// row), lane 0 issues the A-stream chunk and value bulk copies, the B-row gathers (TMA) and
-// the MMAs.  They synchronise only through mbarriers:
+// slice: TMEM lane quarter = warp; lanes < HT/4 also decode one tile row each), warp 4 lane 0 =
+// producer: A-stream chunk and value bulk copies, B-row gathers (TMA), MMAs.  They synchronise only through mbarriers:
 //   chunk_full[2]  bulk copies of a chunk's SparseAToB / TCLocalBit / TCOffset (tx bytes)
 //   vals_full[2]   bulk copy of the chunk's value range (or an overflow flag: values from L2)
 //   full_t[ST]     TMA gather of a block's 8 B rows (tx bytes)
-//   ready[SA]      4 transposer warps: A[sa] in TMEM (the producer decoded B[sa] itself)
+//   ready[SA]      4 transposer warps: A[sa] in TMEM and their rows of the decoded tile B[sa]
 //   empty[SA]      tcgen05.commit: the MMA that read A[sa] / B[sa] has completed
 //   acc_full[ND]   tcgen05.commit after a window's (segment's) last MMA
 //   acc_free[ND]   4 transposer warps: accumulator read back, D may be overwritten
@@ -316,7 +315,7 @@ __global__ void __launch_bounds__(kThreads + 32, 6)
     auto first_wend = [&]() { return split ? b1 : __shfl_sync(0xffffffffu, my_rwo, 1); };
 
     if (warp == 4) {
-        // ============================== producer warp: decode (32 lanes), MMA + copies (lane 0)
+        // ============================== producer (lane 0): chunk / value copies, gathers, MMAs
         const uint64_t pol_keep = policy_evict_last();
         // chunk c (blocks [c*CH, +CH)) into buffer c & 1: 16-byte-aligned supersets of the
         // arrays by bulk copy (the allocations carry the padding)
@@ -367,7 +366,7 @@ __global__ void __launch_bounds__(kThreads + 32, 6)
             tma_gather4(dst + kStageBytes / 2, &tmap, col, (int32_t)cb.x, (int32_t)cb.y, (int32_t)cb.z,
                         (int32_t)cb.w, bar, pol_keep);
         };
-        if (nblk == 0) return;
+        if (nblk == 0 || lane != 0) return;
         // window of the block cursor (the transposers zero-write the empty ones)
         uint32_t wi = 0, wend = split ? b1 : __ldg(p.rwo + w0 + 1);
         auto advance = [&](uint32_t cursor) {
@@ -377,61 +376,20 @@ __global__ void __launch_bounds__(kThreads + 32, 6)
             }
         };
         advance(b0);
-        if (lane == 0) {
-            issue_chunk(0);
-            issue_chunk(1);
-            mbar_wait(chunk_full(0), 0);
-            issue_vals(0);
-            for (int s = 0; s < ST; ++s)
-                if ((uint32_t)s < nblk) issue_tma((uint32_t)s, s);
-        }
-        __syncwarp();
+        issue_chunk(0);
+        issue_chunk(1);
+        mbar_wait(chunk_full(0), 0);
+        issue_vals(0);
+        for (int s = 0; s < ST; ++s)
+            if ((uint32_t)s < nblk) issue_tma((uint32_t)s, s);
         bool first = true;
         uint32_t accn = 0;  // accumulations started (window or segment)
-        const int n = lane;  // decode: lane = tile row
         for (uint32_t j = 0; j < nblk; ++j) {
-            const int sa = (int)(j % SA), buf = (j / kCH) & 1;
+            const int sa = (int)(j % SA);
             const uint32_t cs = j & (kCH - 1u);
             const uint32_t jb = b0 + j;
-            if (cs == 0) {
-                mbar_wait(chunk_full(buf), ((j / kCH) >> 1) & 1u);
-                mbar_wait(vals_full(buf), ((j / kCH) >> 1) & 1u);
-            }
-            if (j >= (uint32_t)SA) mbar_wait(empty(j), ((j / SA) - 1u) & 1u);
-            // decode of tile row n: its occupancy byte, the rank of its first value
-            // (values ascend by tile position r*8 + lane, so a row's values are one run), and
-            // the row's 8 entries into B[sa] (K-major core matrices: two 16-byte halves)
-            if (n < HT) {
-                float r[8];
-#pragma unroll
-                for (int k = 0; k < 8; ++k) r[k] = 0.f;
-                if (n < p.wh) {
-                    const uint64_t *wb = ch_bits + buf * L::BITS_BUF + misc[4 + buf] + cs * (uint32_t)p.nw;
-                    const int word = n >> 3, sh = (n & 7) * 8;
-                    const uint64_t m = wb[word];
-                    const uint32_t byte = (uint32_t)(m >> sh) & 0xFFu;
-                    if (byte) {
-                        uint32_t idx = ch_tco[buf * L::TCO_BUF + misc[6 + buf] + cs] +
-                                       (uint32_t)__popcll(m & ((1ull << sh) - 1ull));
-#pragma unroll
-                        for (int q = 0; q < NWMAX - 1; ++q)
-                            if (q < word) idx += (uint32_t)__popcll(wb[q]);
-                        const uint32_t vlo = misc[8 + buf];
-                        const float *vsrc = vlo != 0xFFFFFFFFu ? ch_vals + buf * L::VALS_BUF + (idx - vlo) : p.vals + idx;
-                        int c = 0;
-#pragma unroll
-                        for (int k = 0; k < 8; ++k)
-                            if ((byte >> k) & 1u) r[k] = vsrc[c++];
-                    }
-                }
-                float *bt = btile + sa * HT * 8 + (n >> 3) * 64 + (n & 7) * 4;
-                *reinterpret_cast<float4 *>(bt) = make_float4(r[0], r[1], r[2], r[3]);
-                *reinterpret_cast<float4 *>(bt + 32) = make_float4(r[4], r[5], r[6], r[7]);
-            }
-            fence_proxy_async_smem();
-            __syncwarp();
             const bool last = split ? (j + 1 == nblk) : (jb + 1 == wend);
-            if (lane == 0) {
+            {
                 if (first && accn >= (uint32_t)ND)  // D[accn % ND] read back by the transposers?
                     mbar_wait(acc_free(accn % ND), ((accn / ND) - 1u) & 1u);
                 mbar_wait(ready(sa), (j / SA) & 1u);
@@ -453,7 +411,6 @@ __global__ void __launch_bounds__(kThreads + 32, 6)
                     issue_tma(jt, (int)(j % ST));
                 }
             }
-            __syncwarp();
             if (last) {
                 ++accn;
                 advance(jb + 1);
@@ -529,6 +486,47 @@ __global__ void __launch_bounds__(kThreads + 32, 6)
                 if constexpr (RND) v[r] = tf32_rna_bits(v[r]);
             }
             tmem_st_x8(tmem + lane_off + (uint32_t)(sa * 8), v);
+        }
+        {   // decode of this warp's HT/4 tile rows (lane = row): the row's occupancy
+            // byte and the rank of its first value -- values ascend by tile position r*8 + lane,
+            // so a row's values are one contiguous run -- into B[sa] (K-major core matrices)
+            const int buf = (j / kCH) & 1;
+            const uint32_t cs = j & (kCH - 1u);
+            if (cs == 0) {
+                mbar_wait(chunk_full(buf), ((j / kCH) >> 1) & 1u);
+                mbar_wait(vals_full(buf), ((j / kCH) >> 1) & 1u);
+            }
+            constexpr int RPW = HT / 4;  // tile rows per warp
+            if (lane < RPW) {
+                const int n = warp * RPW + lane;
+                float r[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) r[k] = 0.f;
+                if (n < p.wh) {
+                    const uint64_t *wb = ch_bits + buf * L::BITS_BUF + misc[4 + buf] + cs * (uint32_t)p.nw;
+                    const int word = n >> 3, sh = (n & 7) * 8;
+                    const uint64_t m = wb[word];
+                    const uint32_t byte = (uint32_t)(m >> sh) & 0xFFu;
+                    if (byte) {
+                        uint32_t idx = ch_tco[buf * L::TCO_BUF + misc[6 + buf] + cs] +
+                                       (uint32_t)__popcll(m & ((1ull << sh) - 1ull));
+#pragma unroll
+                        for (int q = 0; q < NWMAX - 1; ++q)
+                            if (q < word) idx += (uint32_t)__popcll(wb[q]);
+                        const uint32_t vlo = misc[8 + buf];
+                        const float *vsrc =
+                            vlo != 0xFFFFFFFFu ? ch_vals + buf * L::VALS_BUF + (idx - vlo) : p.vals + idx;
+                        int c = 0;
+#pragma unroll
+                        for (int k = 0; k < 8; ++k)
+                            if ((byte >> k) & 1u) r[k] = vsrc[c++];
+                    }
+                }
+                float *bt = btile + sa * HT * 8 + (n >> 3) * 64 + (n & 7) * 4;
+                *reinterpret_cast<float4 *>(bt) = make_float4(r[0], r[1], r[2], r[3]);
+                *reinterpret_cast<float4 *>(bt + 32) = make_float4(r[4], r[5], r[6], r[7]);
+            }
+            fence_proxy_async_smem();
         }
         tmem_wait_st();
         tc_fence_before();
