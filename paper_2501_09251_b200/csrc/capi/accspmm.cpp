@@ -859,4 +859,9 @@ const char *accspmm_last_error(void) { return g_last_error.c_str(); }
 
 int32_t accspmm_abi_version(void) { return ACCSPMM_ABI_VERSION; }
 
+#ifdef ACCSPMM_VARIANTS
+// measurement hook of the variants build: per-phase cycle trace of the tcgen05 kernel (kcfg 68)
+void accspmm_debug_tc05_trace(unsigned long long *out) { accspmm::debug_tc05_trace(out); }
+#endif
+
 }  // extern "C"

@@ -154,6 +154,9 @@ accspmm_status launch_spmm(const DevicePlan &p, const void *B, const void *zrow,
 accspmm_status launch_spmm_tc05(const DevicePlan &d, const void *B, int64_t N, float *C, float *ws, uint32_t *counters,
                                 void *stream, bool round_b);
 accspmm_status launch_round_b(const float *B, float *Br, int64_t n, void *stream);
+#ifdef ACCSPMM_VARIANTS
+void debug_tc05_trace(unsigned long long *out);  // [64 CTAs][16]: producer 0-7, transposer 8-15
+#endif
 // B' = B[perm] row gather (K rows of row_bytes), optionally with rho = TF32 RNA (f32 rows)
 accspmm_status launch_permute_b(const void *B, void *Bp, const uint32_t *perm, int64_t K, int64_t row_bytes,
                                 bool round_tf32, void *stream);

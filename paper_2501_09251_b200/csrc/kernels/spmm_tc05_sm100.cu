@@ -203,6 +203,12 @@ __device__ __forceinline__ uint32_t tf32_rna_bits(uint32_t x)
 // A chunk buffer is refilled only after the ready[] of the chunk's last block (every reader
 // is done with it); a gather stage only after the ready[] of the block it held.
 
+#ifdef ACCSPMM_VARIANTS
+// phase-cycle trace of the first kTraceCtas CTAs (variants build, kcfg 68): [cta][slot]
+constexpr int kTraceCtas = 64, kTraceSlots = 16;
+__device__ unsigned long long g_tc05_trace[kTraceCtas * kTraceSlots];
+#endif
+
 template <int HT, int ST, int SA, int ND>
 struct TcLayout {
     static constexpr int NWMAX = HT / 8;
@@ -236,10 +242,21 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t
 }
 
 // CP = commit period: one tcgen05.commit frees CP consecutive A / B stages (CP divides SA)
-template <int HT, int ST, int SA, int ND, bool RND, int WM = 0, int CP = 1>
+template <int HT, int ST, int SA, int ND, bool RND, int WM = 0, int CP = 1, int REP = 1, bool TR = false>
 __global__ void __launch_bounds__(kThreads + 32, 6)
     spmm_tc05_kernel(const TcParams p, const __grid_constant__ CUtensorMap tmap)
 {
+    // TR: accumulate clock64 cycles per phase into g_tc05_trace (one transposer lane, the producer)
+    const bool trace_on = TR && blockIdx.x < 64;
+    unsigned long long tr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long tr_t = TR ? clock64() : 0;
+    auto mark = [&](int slot) {
+        if constexpr (TR) {
+            const long long t = clock64();
+            tr[slot] += (unsigned long long)(t - tr_t);
+            tr_t = t;
+        }
+    };
     static_assert(SA % CP == 0, "commit period must divide the stage count");
     auto mbar_wait = [](uint32_t bar, uint32_t phase) { mbar_wait_m<WM>(bar, phase); };
     using L = TcLayout<HT, ST, SA, ND>;
@@ -390,15 +407,24 @@ __global__ void __launch_bounds__(kThreads + 32, 6)
             const uint32_t jb = b0 + j;
             const bool last = split ? (j + 1 == nblk) : (jb + 1 == wend);
             {
+                mark(7);
                 if (first && accn >= (uint32_t)ND)  // D[accn % ND] read back by the transposers?
                     mbar_wait(acc_free(accn % ND), ((accn / ND) - 1u) & 1u);
+                mark(0);
                 mbar_wait(ready(sa), (j / SA) & 1u);
+                mark(1);
                 tc_fence_after();
                 const int dsel = (int)(accn % ND);
                 umma_tf32_ts(tmem + (uint32_t)(SA * 8 + dsel * HT), tmem + (uint32_t)(sa * 8),
                              btile_desc(smem_u32(btile + sa * HT * 8)), IDESC, first ? 0u : 1u);
+                // REP > 1 (variants build, timing probe only -- wrong results): the tensor core
+                // executes every block's MMA REP times
+                for (int rep = 1; rep < REP; ++rep)
+                    umma_tf32_ts(tmem + (uint32_t)(SA * 8 + dsel * HT), tmem + (uint32_t)(sa * 8),
+                                 btile_desc(smem_u32(btile + sa * HT * 8)), IDESC, 1u);
                 if ((j % CP) == CP - 1 || j + 1 == nblk) umma_commit(empty(j));
                 if (last) umma_commit(acc_full(dsel));
+                mark(2);
                 // chunk c fully consumed once the ready[] of its last block is in: refill with c + 2
                 if (cs == kCH - 1u) issue_chunk(j / kCH + 2);
                 const uint32_t jt = j + ST;  // gather of block jt into the stage block j vacated
@@ -410,6 +436,7 @@ __global__ void __launch_bounds__(kThreads + 32, 6)
                     }
                     issue_tma(jt, (int)(j % ST));
                 }
+                mark(3);
             }
             if (last) {
                 ++accn;
@@ -417,6 +444,10 @@ __global__ void __launch_bounds__(kThreads + 32, 6)
             }
             first = last;
         }
+#ifdef ACCSPMM_VARIANTS
+        if (trace_on)
+            for (int k = 0; k < 8; ++k) atomicAdd(&g_tc05_trace[blockIdx.x * kTraceSlots + k], tr[k]);
+#endif
         return;
     }
 
@@ -474,9 +505,12 @@ __global__ void __launch_bounds__(kThreads + 32, 6)
     uint32_t accn = 0;
     for (uint32_t j = 0; j < nblk; ++j) {
         const int st = (int)(j % ST), sa = (int)(j % SA);
+        mark(6);
         if (j >= (uint32_t)SA) mbar_wait(empty(j), ((j / SA) - 1u) & 1u);
+        mark(0);
         tc_fence_after();
         mbar_wait(full_t(st), (j / ST) & 1u);
+        mark(1);
         {   // gathered rows -> TMEM A[sa]: this thread's feature of the 8 rows
             const float *sp = reinterpret_cast<const float *>(stage + st * kStageBytes);
             uint32_t v[8];
@@ -487,6 +521,7 @@ __global__ void __launch_bounds__(kThreads + 32, 6)
             }
             tmem_st_x8(tmem + lane_off + (uint32_t)(sa * 8), v);
         }
+        mark(2);
         {   // decode of this warp's HT/4 tile rows (lane = row): the row's occupancy
             // byte and the rank of its first value -- values ascend by tile position r*8 + lane,
             // so a row's values are one contiguous run -- into B[sa] (K-major core matrices)
@@ -528,10 +563,12 @@ __global__ void __launch_bounds__(kThreads + 32, 6)
             }
             fence_proxy_async_smem();
         }
+        mark(3);
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(ready(sa));
+        mark(4);
         const uint32_t jb = b0 + j;
         const bool last = split ? (j + 1 == nblk) : (jb + 1 == wend);
         if (last && !split) {
@@ -544,7 +581,12 @@ __global__ void __launch_bounds__(kThreads + 32, 6)
             wend = wi < nwin ? e : 0xFFFFFFFFu;
             skip_empty(jb + 1);
         }
+        mark(5);
     }
+#ifdef ACCSPMM_VARIANTS
+    if (trace_on && warp == 0 && lane == 0)
+        for (int k = 0; k < 8; ++k) atomicAdd(&g_tc05_trace[blockIdx.x * kTraceSlots + 8 + k], tr[k]);
+#endif
 
     if (split) {
         // cross-row write-back of a split window (reading R15): partial -> workspace,
@@ -623,11 +665,11 @@ accspmm_status tensor_map_tc05(const DevicePlan &d, const void *B, int64_t N, co
     return ACCSPMM_OK;
 }
 
-template <int HT, int ST, int SA, int ND, bool RND, int WM = 0, int CP = 1>
+template <int HT, int ST, int SA, int ND, bool RND, int WM = 0, int CP = 1, int REP = 1, bool TR = false>
 accspmm_status launch_tc(const TcParams &tp, const CUtensorMap *map, cudaStream_t stream)
 {
     using L = TcLayout<HT, ST, SA, ND>;
-    auto kern = spmm_tc05_kernel<HT, ST, SA, ND, RND, WM, CP>;
+    auto kern = spmm_tc05_kernel<HT, ST, SA, ND, RND, WM, CP, REP, TR>;
     static int configured_device = -1;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -645,6 +687,14 @@ accspmm_status launch_tc(const TcParams &tp, const CUtensorMap *map, cudaStream_
 }
 
 }  // namespace
+
+#ifdef ACCSPMM_VARIANTS
+void debug_tc05_trace(unsigned long long *out)
+{
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, g_tc05_trace, sizeof(g_tc05_trace));
+}
+#endif
 
 accspmm_status launch_spmm_tc05(const DevicePlan &d, const void *B, int64_t N, float *C, float *ws, uint32_t *counters,
                                 void *stream, bool round_b)
@@ -698,6 +748,19 @@ accspmm_status launch_spmm_tc05(const DevicePlan &d, const void *B, int64_t N, f
     case 65:  // one commit per 4 MMAs, 8 stages
         if (d.wh <= 16) return round_b ? launch_tc<16, 8, 8, 2, true, 0, 4>(tp, map, s) : launch_tc<16, 8, 8, 2, false, 0, 4>(tp, map, s);
         return round_b ? launch_tc<32, 8, 8, 1, true, 0, 4>(tp, map, s) : launch_tc<32, 8, 8, 1, false, 0, 4>(tp, map, s);
+    case 68: {  // phase trace (g_tc05_trace; read with accspmm_debug_tc05_trace)
+        void *sym = nullptr;
+        cudaGetSymbolAddress(&sym, g_tc05_trace);
+        cudaMemsetAsync(sym, 0, sizeof(g_tc05_trace), s);
+        if (d.wh <= 16) return launch_tc<16, 6, 4, 2, false, 0, 1, 1, true>(tp, map, s);
+        return launch_tc<32, 6, 4, 1, false, 0, 1, 1, true>(tp, map, s);
+    }
+    case 66:  // timing probe: every MMA issued twice (wrong results)
+        if (d.wh <= 16) return launch_tc<16, 6, 4, 2, false, 0, 1, 2>(tp, map, s);
+        return launch_tc<32, 6, 4, 1, false, 0, 1, 2>(tp, map, s);
+    case 67:  // timing probe: every MMA issued four times (wrong results)
+        if (d.wh <= 16) return launch_tc<16, 6, 4, 2, false, 0, 1, 4>(tp, map, s);
+        return launch_tc<32, 6, 4, 1, false, 0, 1, 4>(tp, map, s);
     default: break;
     }
 #endif
