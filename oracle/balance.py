@@ -73,7 +73,7 @@ def auto_cap(NB: int) -> int:
 
 
 def build_units(rwo, cap: int, balance: bool, precision: str = "tf32", group: bool = False,
-                group_cap: int | None = None):
+                group_cap: int | None = None, wh: int = 8):
     """Work units (w0, nw, b0, b1, split_id, seg, nseg, slot) covering every block once.
 
     Not balanced: one unit per RowWindow, or with ``group`` (the B200 reading R7b,
@@ -87,7 +87,7 @@ def build_units(rwo, cap: int, balance: bool, precision: str = "tf32", group: bo
         for w in range(W):
             units.append((w, 1, int(rwo[w]), int(rwo[w + 1]), NO_SPLIT, 0, 1, 0))
         return units
-    wb = wb_cost(precision)
+    wb = wb_cost(precision) * (wh // 8)   # a window of wh rows writes wh/8 tiles' worth of C
     split_id = 0
     slot = 0
     cur = None  # [w0, nw, b0, b1, cost]

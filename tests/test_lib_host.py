@@ -434,3 +434,53 @@ def test_library_schedule_equals_hand_written_paper_schedule():
     assert p.export_format()["RowWindowOffset"].tolist() == HAND_RWO
     assert p.info["ibd"] == pytest.approx(23.28, abs=1e-12) and p.info["balanced"] == 1
     assert [tuple(int(x) for x in u) for u in p.export_units()] == HAND_UNITS
+
+
+@pytest.mark.parametrize("wh", [16, 32])
+@pytest.mark.parametrize("reorder", ["off", "on"])
+@pytest.mark.parametrize("precision", ["tf32"])
+def test_tall_window_format_and_units_bit_exact_vs_oracle(wh, reorder, precision):
+    """Reading R20: the library's tall-window plan (host builder) exports exactly the oracle's
+    wh-row encoding of the (row-permuted) matrix, and its units equal the oracle schedule with
+    the wh/8-scaled window write-back (balanced, cap 32, and grouped)."""
+    from oracle import balance as ob
+    from oracle import bittcf as bt
+    from oracle.rounding import rho
+    A = gen.dcsbm(2000, 60_000, 5, 2.2, 0.2, 1500, seed=wh, oversample=1.3)
+    v = gen.values_uniform(A.nnz, 3)
+    for balance, cap in (("on", 32), ("auto", 0)):
+        p = host_plan(A, v, precision=precision, reorder=reorder, window_rows=wh, balance=balance, unit_cap=cap)
+        assert p.info["window_rows"] == wh and p.info["kernel"] == acc.KERNEL["tcgen05"]
+        perm = p.export_rows().astype(np.int64)
+        rp, ci, vv = bt.permute_rows(A.M, A.rowptr, A.colidx, v, perm)
+        ref = bt.encode(A.M, A.K, rp, ci, rho(vv, precision), wh=wh)
+        F = p.export_format()
+        for k in ("RowWindowOffset", "TCOffset", "SparseAToB", "TCLocalBit"):
+            assert np.array_equal(F[k], ref[k].astype(F[k].dtype)), k
+        assert np.array_equal(F["values"], ref["values"])
+        assert p.info["sum_U"] == int(ref["U"].sum())
+        rwo = ref["RowWindowOffset"]
+        if p.info["balanced"]:
+            units = ob.build_units(rwo, p.info["unit_cap"], True, precision, wh=wh)
+        else:
+            units = ob.build_units(rwo, p.info["unit_cap"], False, precision, group=bool(p.info["grouped"]),
+                                   group_cap=p.info["group_cap"], wh=wh)
+        assert [tuple(int(x) for x in u) for u in p.export_units()] == [tuple(u) for u in units]
+
+
+def test_window_rows_and_kernel_option_validation():
+    A = gen.uniform_random(64, 64, 400, seed=2)
+    v = gen.values_uniform(A.nnz, 1)
+    with pytest.raises(acc.AccSpmmError) as e:
+        host_plan(A, v, window_rows=24)
+    assert e.value.status == 1                                   # INVALID_VALUE
+    with pytest.raises(acc.AccSpmmError) as e:
+        host_plan(A, v, window_rows=16, precision="fp16")        # tcgen05 path is TF32 only
+    assert e.value.status == 3
+    with pytest.raises(acc.AccSpmmError) as e:
+        host_plan(A, v, window_rows=16, kernel="mma_sync")       # mma.sync runs 8-row windows only
+    assert e.value.status == 3
+    p = host_plan(A, v)
+    assert p.info["window_rows"] == 8 and p.info["kernel"] == acc.KERNEL["mma_sync"]
+    p = host_plan(A, v, kernel="tcgen05")
+    assert p.info["window_rows"] == 8 and p.info["kernel"] == acc.KERNEL["tcgen05"]

@@ -155,3 +155,91 @@ def test_permute_rows():
         o = perm[r]
         assert np.array_equal(ci[rp[r]:rp[r + 1]], A.colidx[A.rowptr[o]:A.rowptr[o + 1]])
         assert np.array_equal(vv[rp[r]:rp[r + 1]], v[A.rowptr[o]:A.rowptr[o + 1]])
+
+
+# ----------------------------------------------------------------------- tall windows (R20)
+
+def _brute_encode_tall(A, wh):
+    """Per-window dense construction for windows of wh rows, written independently of
+    bt.encode: dense 0/1 tile of the window, condensed columns, wh/8 words per block with the
+    paper's bit rule inside each 8-row word, values in row-major tile order."""
+    nw = wh // 8
+    dense = np.zeros((A.M, A.K), bool)
+    val = np.zeros((A.M, A.K))
+    for r in range(A.M):
+        for p in range(A.rowptr[r], A.rowptr[r + 1]):
+            dense[r, A.colidx[p]] = True
+            val[r, A.colidx[p]] = p + 1.0          # value = 1 + CSR position (identifies the nnz)
+    rwo, tco, a2b, bits, vals = [0], [0], [], [], []
+    for w0 in range(0, A.M, wh):
+        win = dense[w0:w0 + wh]
+        cols = [c for c in range(A.K) if win[:, c].any()]
+        for t in range(0, len(cols), 8):
+            lane_cols = cols[t:t + 8]
+            a2b += lane_cols + [0] * (8 - len(lane_cols))
+            words = [0] * nw
+            for r in range(win.shape[0]):
+                for l, c in enumerate(lane_cols):
+                    if win[r, c]:
+                        words[r // 8] |= 1 << ((r % 8) * 8 + l)
+                        vals.append(val[w0 + r, c])
+            bits += words
+            tco.append(len(vals))
+        rwo.append(len(tco) - 1)
+    return rwo, tco, a2b, bits, vals
+
+
+@pytest.mark.parametrize("wh", [16, 32])
+@pytest.mark.parametrize("seed", range(12))
+def test_tall_windows_vectorised_equals_brute_force(wh, seed):
+    rng = np.random.default_rng(100 + seed)
+    M, K = int(rng.integers(1, 90)), int(rng.integers(1, 70))
+    A = gen.uniform_random(M, K, int(rng.integers(0, M * K // 3 + 1)), seed=seed)
+    v = np.arange(1, A.nnz + 1, dtype=np.float64)
+    F = bt.encode(A.M, A.K, A.rowptr, A.colidx, v, wh=wh)
+    rwo, tco, a2b, bits, vals = _brute_encode_tall(A, wh)
+    assert F["RowWindowOffset"].tolist() == rwo and F["TCOffset"].tolist() == tco
+    assert F["SparseAToB"].tolist() == a2b and [int(x) for x in F["TCLocalBit"]] == bits
+    assert F["values"].tolist() == vals
+
+
+@pytest.mark.parametrize("wh", [16, 32])
+@pytest.mark.parametrize("seed", range(8))
+def test_tall_windows_roundtrip_and_invariants(wh, seed):
+    rng = np.random.default_rng(seed)
+    M, K = int(rng.integers(1, 300)), int(rng.integers(1, 200))
+    A = gen.uniform_random(M, K, int(rng.integers(0, M * K // 4 + 1)), seed=seed)
+    v = gen.values_uniform(A.nnz, seed)
+    F = bt.encode(A.M, A.K, A.rowptr, A.colidx, v, wh=wh)
+    rp, ci, vv = bt.decode(F)                                   # S:324 round trip
+    assert np.array_equal(rp, A.rowptr) and np.array_equal(ci, A.colidx) and np.array_equal(vv, v)
+    words = F["TCLocalBit"].reshape(-1, wh // 8)
+    assert np.array_equal(np.diff(F["TCOffset"].astype(np.int64)), np.bitwise_count(words).sum(axis=1))
+    assert F["W"] == (M + wh - 1) // wh and F["NB"] == int(((F["U"] + 7) // 8).sum())
+    # a tall window's condensed columns are the union of its 8-row windows' (P:250 per 8 rows)
+    F8 = bt.encode(A.M, A.K, A.rowptr, A.colidx, wh=8)
+    for w in range(F["W"]):
+        cols = set(F["SparseAToB"][8 * F["RowWindowOffset"][w]: 8 * F["RowWindowOffset"][w + 1]][
+            : F["U"][w]].tolist())
+        sub = set()
+        for w8 in range(w * wh // 8, min(F8["W"], (w + 1) * wh // 8)):
+            sub |= set(F8["SparseAToB"][8 * F8["RowWindowOffset"][w8]: 8 * F8["RowWindowOffset"][w8 + 1]][
+                : F8["U"][w8]].tolist())
+        assert cols == sub
+
+
+def test_tall_window_worked_example():
+    """Hand-derived 16-row window: row 0 has columns {3, 5}, row 9 has {5, 7}.  Condensed
+    columns [3, 5, 7] -> one block, SparseAToB [3, 5, 7, 0, 0, 0, 0, 0]; word 0 (rows 0-7): row 0
+    lanes 0, 1 -> 0x3; word 1 (rows 8-15): row 9 is local row 1 there, lanes 1, 2 -> bits 9, 10
+    -> 0x600; values in tile order (0,3) (0,5) (9,5) (9,7); the value of (9,7) sits at
+    TCOffset + popc(word 0) + popc(word 1 below bit 10) = 0 + 2 + 1 = 3 (P:273 over the words)."""
+    A = gen.csr_from_pairs(np.array([0, 0, 9, 9]), np.array([3, 5, 5, 7]), 16, 8)
+    v = np.array([10.0, 20.0, 30.0, 40.0])
+    F = bt.encode(A.M, A.K, A.rowptr, A.colidx, v, wh=16)
+    assert F["NB"] == 1 and F["RowWindowOffset"].tolist() == [0, 1] and F["TCOffset"].tolist() == [0, 4]
+    assert F["SparseAToB"].tolist() == [3, 5, 7, 0, 0, 0, 0, 0]
+    assert [int(x) for x in F["TCLocalBit"]] == [0x3, 0x600]
+    assert F["values"].tolist() == [10.0, 20.0, 30.0, 40.0]
+    with pytest.raises(ValueError):
+        bt.encode(A.M, A.K, A.rowptr, A.colidx, v, wh=24)
