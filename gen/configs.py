@@ -55,8 +55,11 @@ def _products_hubs():
 
 
 def _papers100m():
-    # directed, out-degree lognormal(2.3, 0.8) rescaled to mean 14.55, popularity Pareto(1.2)
-    return mx.powerlaw_directed(111_059_956, 14.55, seed=11)
+    # directed, out-degree lognormal(2.3, 0.8), popularity Pareto(1.2).  The drawn mean is 15.37
+    # so that after per-row deduplication (hot columns collide at this scale) the matrix holds
+    # 1,613,461,269 nnz = 14.53 per row, ogbn-papers100M's ~1.616B (BASELINE configs[4]); a
+    # drawn mean of 14.55 gave 1.53B
+    return mx.powerlaw_directed(111_059_956, 15.37, seed=11)
 
 
 def _papers100m_small():

@@ -225,6 +225,17 @@ accspmm_status accspmm_plan_export_rows(const accspmm_plan *plan, uint32_t *orig
  * Returns INVALID_CSR / INVALID_VALUE as plan creation does. */
 accspmm_status accspmm_reorder(int64_t n, const int64_t *rowptr, const int32_t *colidx, uint32_t *perm_new2old);
 
+/* The deterministic parallel variant of Algorithm 1 (host; reading R21), which
+ * plan creation uses for graphs above 8M vertices: Step I in rounds of `round` vertices (in
+ * ascending degree), every vertex of a round choosing its merge target from the state at the
+ * round's start by its own edges, merges applied in round order; Step II's greedy chaining run
+ * independently on `segments` contiguous pieces of the DFS sequence with an L-candidate window.
+ * round, segments, L <= 0 select the defaults (max(4096, min(2^20, n/4096)), max(1, n/65536),
+ * 8).  The result depends only on the input and these parameters (not on the thread count).
+ * Errors as accspmm_reorder. */
+accspmm_status accspmm_reorder_parallel(int64_t n, const int64_t *rowptr, const int32_t *colidx, int64_t round,
+                                        int64_t segments, int32_t L, uint32_t *perm_new2old);
+
 /* A^T (host): the K x M transpose of the canonical CSR A as canonical CSR -- the operand
  * of the backward pass dB = A^T . dC of C = A . B.  t_rowptr int64[K+1], t_colidx
  * int32[nnz], t_vals float32[nnz] (t_vals and vals may be NULL: pattern only), caller-owned.

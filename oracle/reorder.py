@@ -166,6 +166,101 @@ def ordering(adj, children, roots, L: int = CAND_WINDOW, H: int = HUB_CAP):
     return np.asarray(perm, dtype=np.int64)
 
 
+def dendrogram_rounds(adj, round_size: int):
+    """Reading R21, Step I: Alg. 1's merge rule (l.2-8) applied in rounds of ``round_size``
+    vertices in ascending (degree, id) order.  Each vertex of a round decides from the state at
+    the round's start, counting only its own edges towards each neighbouring community; the
+    merges (dQ > 0, ties by smallest community id) are applied in round order, a target that
+    joined another community meanwhile standing for that community's root (skipped if it is
+    the deciding vertex itself)."""
+    n = len(adj)
+    deg = [len(x) for x in adj]
+    m2 = float(sum(deg))
+    parent = list(range(n))
+    a = [float(d) for d in deg]
+    children = [[] for _ in range(n)]
+
+    def find(x):
+        while parent[x] != x:
+            x = parent[x]
+        return x
+
+    order = sorted(range(n), key=lambda u: (deg[u], u))
+    for r0 in range(0, n, round_size):
+        batch = order[r0:r0 + round_size]
+        props = []
+        for v in batch:                                       # decisions: state at round start
+            best = None
+            if deg[v] > 0 and m2 > 0:
+                w = {}
+                for x in adj[v]:
+                    r = find(x)
+                    if r != v:
+                        w[r] = w.get(r, 0) + 1
+                best_dq = 0.0
+                for r in sorted(w):
+                    dq = delta_q(w[r], a[r], a[v], m2)
+                    if best is None or dq > best_dq:
+                        best, best_dq = r, dq
+                if best is not None and not best_dq > 0.0:
+                    best = None
+            props.append(best)
+        for v, r in zip(batch, props):                        # merges: round order
+            if r is None:
+                continue
+            u = find(r)
+            if u == v:
+                continue
+            parent[v] = u
+            a[u] += a[v]
+            children[u].append(v)
+    roots = [v for v in range(n) if parent[v] == v]
+    return parent, children, roots
+
+
+def ordering_segments(adj, children, roots, segments: int, L: int, H: int = HUB_CAP):
+    """Reading R21, Step II: the DFS leaf sequence cut into ``segments`` contiguous pieces of
+    ceil(n/segments) vertices; the greedy chaining of ``ordering`` runs in each piece alone."""
+    n = len(adj)
+    seq = dfs_sequence(children, roots)
+    size = -(-n // segments) if n else 0
+    capped = [x[:H] for x in adj]
+    perm = []
+    for s0 in range(0, n, max(size, 1)):
+        alive = list(seq[s0:s0 + size])
+        visited = set()
+        for v in list(alive):
+            if v in visited:
+                continue
+            visited.add(v)
+            perm.append(v)
+            alive.remove(v)
+            while alive:
+                nv = set(capped[v])
+                best, best_c = -1, 0
+                for u in alive[:L]:
+                    c = sum(1 for x in capped[u] if x in nv)
+                    if c > best_c:
+                        best, best_c = u, c
+                if best < 0:
+                    break
+                visited.add(best)
+                perm.append(best)
+                alive.remove(best)
+                v = best
+    return np.asarray(perm, dtype=np.int64)
+
+
+def reorder_parallel(M: int, K: int, rowptr, colidx, round_size: int, segments: int, L: int = 8,
+                     H: int = HUB_CAP):
+    """Reading R21 end to end (the library's variant for graphs above 8M vertices)."""
+    if M != K:
+        return np.arange(M, dtype=np.int64)
+    adj = affinity_graph(M, rowptr, colidx)
+    _, children, roots = dendrogram_rounds(adj, round_size)
+    return ordering_segments(adj, children, roots, segments, L, H)
+
+
 def reorder(M: int, K: int, rowptr, colidx, L: int = CAND_WINDOW, H: int = HUB_CAP,
             edge_cap: int | None = None, stats: dict | None = None):
     """Algorithm 1 end to end: perm new->old (identity when M != K, Q14).

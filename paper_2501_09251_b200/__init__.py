@@ -72,7 +72,7 @@ EXPORTED = [
     "accspmm_unpermute", "accspmm_debug_round_tf32", "accspmm_debug_decode", "accspmm_status_string",
     "accspmm_last_error", "accspmm_abi_version", "accspmm_plan_set_timing", "accspmm_plan_kernel_times",
     "accspmm_probe_l2_bandwidth", "accspmm_execute_host_batch", "accspmm_csr_transpose",
-    "accspmm_execute_allgather",
+    "accspmm_execute_allgather", "accspmm_reorder_parallel",
 ]
 
 
@@ -99,6 +99,7 @@ def load_library(path: str = LIB_PATH):
         "accspmm_plan_export_units": ([P, P], S),
         "accspmm_plan_export_rows": ([P, P], S),
         "accspmm_reorder": ([I64, P, P, P], S),
+        "accspmm_reorder_parallel": ([I64, P, P, I64, I64, I32, P], S),
         "accspmm_partition_bounds": ([I64, P, I32, P], S),
         "accspmm_unpermute": ([P, P, I64, I64, P, P], S),
         "accspmm_debug_round_tf32": ([P, P, I64, P], S),
@@ -234,6 +235,15 @@ def accspmm_reorder(n, rowptr, colidx) -> np.ndarray:
     colidx = np.ascontiguousarray(colidx, dtype=np.int32)
     perm = np.empty(n, np.uint32)
     _check(load_library().accspmm_reorder(int(n), _ptr(rowptr), _ptr(colidx), _ptr(perm)))
+    return perm
+
+
+def accspmm_reorder_parallel(n, rowptr, colidx, round=0, segments=0, L=0) -> np.ndarray:
+    rowptr = np.ascontiguousarray(rowptr, dtype=np.int64)
+    colidx = np.ascontiguousarray(colidx, dtype=np.int32)
+    perm = np.empty(n, np.uint32)
+    _check(load_library().accspmm_reorder_parallel(int(n), _ptr(rowptr), _ptr(colidx), int(round), int(segments),
+                                                   int(L), _ptr(perm)))
     return perm
 
 

@@ -752,6 +752,26 @@ accspmm_status accspmm_reorder(int64_t n, const int64_t *rowptr, const int32_t *
     return ACCSPMM_OK;
 }
 
+accspmm_status accspmm_reorder_parallel(int64_t n, const int64_t *rowptr, const int32_t *colidx, int64_t round,
+                                        int64_t segments, int32_t L, uint32_t *perm_new2old)
+{
+    if (n < 0 || !perm_new2old) return fail(ACCSPMM_ERR_INVALID_VALUE, "bad argument");
+    Csr a{n, n, rowptr, colidx};
+    accspmm_status st = validate_csr(a);
+    if (st != ACCSPMM_OK) return st;
+    try {
+        ParallelReorderParams pp;
+        pp.round = round;
+        pp.segments = segments;
+        pp.L = L;
+        std::vector<uint32_t> perm = reorder_alg1_parallel(a, pp);
+        std::memcpy(perm_new2old, perm.data(), perm.size() * sizeof(uint32_t));
+    } catch (const std::bad_alloc &) {
+        return fail(ACCSPMM_ERR_OUT_OF_MEMORY, "reordering");
+    }
+    return ACCSPMM_OK;
+}
+
 accspmm_status accspmm_csr_transpose(int64_t M, int64_t K, const int64_t *rowptr, const int32_t *colidx,
                                     const float *vals, int64_t *t_rowptr, int32_t *t_colidx, float *t_vals)
 {

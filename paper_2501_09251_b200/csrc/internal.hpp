@@ -101,8 +101,17 @@ int auto_group_cap(int cap);  // concatenation limit under the automatic cap (re
 std::vector<int64_t> partition_bounds(const Csr &a, const std::vector<uint32_t> &perm, int nparts,
                                       int wh = kWindow);
 
-// host/reorder.cpp -- Algorithm 1; returns perm new->old (identity for an edgeless graph)
+// host/reorder.cpp -- Algorithm 1; returns perm new->old (identity for an edgeless graph).
+// Above kParallelMinVertices the deterministic parallel variant of reading R21 runs instead.
+constexpr int64_t kParallelMinVertices = 8'000'000;
+struct ParallelReorderParams {
+    int64_t round = 0;     // vertices per dendrogram round (0: max(4096, min(2^20, n / 4096)))
+    int64_t segments = 0;  // ordering segments (0: max(1, n / 65536))
+    int L = 0;             // candidate window (0: 8)
+    ParallelReorderParams();
+};
 std::vector<uint32_t> reorder_alg1(const Csr &a);
+std::vector<uint32_t> reorder_alg1_parallel(const Csr &a, const ParallelReorderParams &pp);
 
 // kernels (device side, kernels/*.cu)
 struct DevicePlan {
