@@ -152,6 +152,16 @@ accspmm_status accspmm_plan_create(int64_t M, int64_t K, const int64_t *rowptr, 
 accspmm_status accspmm_plan_create_ex(int64_t M, int64_t K, const int64_t *rowptr, const int32_t *colidx,
                                       const float *vals, const accspmm_options *opt, accspmm_plan **out);
 
+/* As accspmm_plan_create_ex, with the Algorithm-1 permutation supplied by the caller instead
+ * of computed (perm_new2old u32[M], a bijection of [0, M), e.g. the output of accspmm_reorder
+ * or accspmm_reorder_parallel computed once and broadcast to every rank of a multi-GPU job).
+ * opt->reorder still decides: OFF ignores it, ON applies it, AUTO applies it iff it reduces
+ * the TC-block count.  Errors as accspmm_plan_create_ex, plus INVALID_VALUE for a NULL perm,
+ * a non-bijection or a non-square A. */
+accspmm_status accspmm_plan_create_perm(int64_t M, int64_t K, const int64_t *rowptr, const int32_t *colidx,
+                                        const float *vals, const accspmm_options *opt,
+                                        const uint32_t *perm_new2old, accspmm_plan **out);
+
 /* C = A . B on `stream`, asynchronously (never synchronises the host).
  * nparts == 1: C is M x N in ORIGINAL row order (reordered rows are scattered
  * back through the permutation).  nparts > 1: C is the slab, info.rows x N, in

@@ -72,7 +72,7 @@ EXPORTED = [
     "accspmm_unpermute", "accspmm_debug_round_tf32", "accspmm_debug_decode", "accspmm_status_string",
     "accspmm_last_error", "accspmm_abi_version", "accspmm_plan_set_timing", "accspmm_plan_kernel_times",
     "accspmm_probe_l2_bandwidth", "accspmm_execute_host_batch", "accspmm_csr_transpose",
-    "accspmm_execute_allgather", "accspmm_reorder_parallel",
+    "accspmm_execute_allgather", "accspmm_reorder_parallel", "accspmm_plan_create_perm",
 ]
 
 
@@ -91,6 +91,7 @@ def load_library(path: str = LIB_PATH):
         "accspmm_options_default": ([ctypes.POINTER(accspmm_options)], S),
         "accspmm_plan_create": ([I64, I64, P, P, P, ctypes.POINTER(P)], S),
         "accspmm_plan_create_ex": ([I64, I64, P, P, P, ctypes.POINTER(accspmm_options), ctypes.POINTER(P)], S),
+        "accspmm_plan_create_perm": ([I64, I64, P, P, P, ctypes.POINTER(accspmm_options), P, ctypes.POINTER(P)], S),
         "accspmm_execute": ([P, P, I64, P, P], S),
         "accspmm_execute_host": ([P, P, I64, P, P], S),
         "accspmm_plan_destroy": ([P], None),
@@ -163,6 +164,18 @@ def accspmm_plan_create_ex(M, K, rowptr, colidx, vals, opt: accspmm_options | No
     out = ctypes.c_void_p()
     _check(load_library().accspmm_plan_create_ex(int(M), int(K), _ptr(rowptr), _ptr(colidx), _ptr(vals),
                                                  ctypes.byref(opt) if opt is not None else None, ctypes.byref(out)))
+    return out.value
+
+
+def accspmm_plan_create_perm(M, K, rowptr, colidx, vals, opt: accspmm_options | None, perm):
+    rowptr = np.ascontiguousarray(rowptr, dtype=np.int64)
+    colidx = np.ascontiguousarray(colidx, dtype=np.int32)
+    vals = np.ascontiguousarray(vals, dtype=np.float32)
+    perm = np.ascontiguousarray(perm, dtype=np.uint32)
+    out = ctypes.c_void_p()
+    _check(load_library().accspmm_plan_create_perm(int(M), int(K), _ptr(rowptr), _ptr(colidx), _ptr(vals),
+                                                   ctypes.byref(opt) if opt is not None else None, _ptr(perm),
+                                                   ctypes.byref(out)))
     return out.value
 
 
@@ -341,7 +354,9 @@ class Plan:
 
     def __init__(self, M, K, rowptr, colidx, vals, precision="tf32", reorder="auto", balance="auto",
                  unit_cap=0, part=0, nparts=1, device=None, build="host", permute_cols=False, window_rows=0,
-                 kernel="auto"):
+                 kernel="auto", perm=None):
+        """perm (optional, u32[M] new -> old): an Alg. 1 permutation computed elsewhere (e.g. once
+        on rank 0 and broadcast), used instead of running the reordering again."""
         opt = accspmm_options_default()
         opt.window_rows = int(window_rows)
         opt.kernel = KERNEL[kernel]
@@ -355,7 +370,10 @@ class Plan:
         if device is not None:
             opt.device = int(device)
         self.precision = precision
-        self.handle = accspmm_plan_create_ex(M, K, rowptr, colidx, vals, opt)
+        if perm is not None:
+            self.handle = accspmm_plan_create_perm(M, K, rowptr, colidx, vals, opt, perm)
+        else:
+            self.handle = accspmm_plan_create_ex(M, K, rowptr, colidx, vals, opt)
         self.info = accspmm_plan_get_info(self.handle)
 
     def close(self):

@@ -176,8 +176,34 @@ accspmm_status accspmm_plan_create(int64_t M, int64_t K, const int64_t *rowptr, 
     return accspmm_plan_create_ex(M, K, rowptr, colidx, vals, nullptr, out);
 }
 
+static accspmm_status plan_create_impl(int64_t M, int64_t K, const int64_t *rowptr, const int32_t *colidx,
+                                       const float *vals, const accspmm_options *opt_in, const uint32_t *given_perm,
+                                       accspmm_plan **out);
+
 accspmm_status accspmm_plan_create_ex(int64_t M, int64_t K, const int64_t *rowptr, const int32_t *colidx,
                                       const float *vals, const accspmm_options *opt_in, accspmm_plan **out)
+{
+    return plan_create_impl(M, K, rowptr, colidx, vals, opt_in, nullptr, out);
+}
+
+accspmm_status accspmm_plan_create_perm(int64_t M, int64_t K, const int64_t *rowptr, const int32_t *colidx,
+                                        const float *vals, const accspmm_options *opt_in,
+                                        const uint32_t *perm_new2old, accspmm_plan **out)
+{
+    if (!perm_new2old) return fail(ACCSPMM_ERR_INVALID_VALUE, "perm is NULL");
+    if (M != K) return fail(ACCSPMM_ERR_INVALID_VALUE, "a row permutation from Alg. 1 needs a square A (Q14)");
+    std::vector<char> seen((size_t)M, 0);
+    for (int64_t r = 0; r < M; ++r) {
+        const uint32_t o = perm_new2old[r];
+        if ((int64_t)o >= M || seen[o]) return fail(ACCSPMM_ERR_INVALID_VALUE, "perm is not a bijection of [0, M)");
+        seen[o] = 1;
+    }
+    return plan_create_impl(M, K, rowptr, colidx, vals, opt_in, perm_new2old, out);
+}
+
+static accspmm_status plan_create_impl(int64_t M, int64_t K, const int64_t *rowptr, const int32_t *colidx,
+                                       const float *vals, const accspmm_options *opt_in, const uint32_t *given_perm,
+                                       accspmm_plan **out)
 {
     if (!out) return fail(ACCSPMM_ERR_INVALID_VALUE, "out is NULL");
     *out = nullptr;
@@ -233,7 +259,9 @@ accspmm_status accspmm_plan_create_ex(int64_t M, int64_t K, const int64_t *rowpt
     I.nb_unreordered = -1;
     if (opt.reorder != ACCSPMM_REORDER_OFF && M == K && M > 0) {
         try {
-            perm = reorder_alg1(a);
+            // a permutation computed once (e.g. on rank 0 and broadcast) replaces Alg. 1 here
+            if (given_perm) perm.assign(given_perm, given_perm + M);
+            else perm = reorder_alg1(a);
         } catch (const std::bad_alloc &) {
             delete p;
             return fail(ACCSPMM_ERR_OUT_OF_MEMORY, "reordering");

@@ -48,9 +48,23 @@ struct Trace {
 };
 constexpr size_t kEdgeCap = 256;  // community edges carried up a merge (reading R6b)
 
+// adjacency storage without std::vector's serial zero fill (3.2B entries on papers100M)
+struct U32Buf {
+    std::unique_ptr<uint32_t[]> p;
+    size_t n = 0;
+    void resize(size_t m)
+    {
+        p.reset(new uint32_t[m ? m : 1]);
+        n = m;
+    }
+    uint32_t &operator[](size_t i) { return p[i]; }
+    const uint32_t &operator[](size_t i) const { return p[i]; }
+    uint32_t *begin() { return p.get(); }
+};
+
 struct Graph {
     std::vector<int64_t> ptr;
-    std::vector<uint32_t> adj;
+    U32Buf adj;
 };
 
 // pattern(A or A^T) without the diagonal, as sorted unique adjacency lists.  A
@@ -165,18 +179,36 @@ Graph affinity_graph(const Csr &a)
     pairs.reset();
     std::vector<int64_t> fill;
     tr.mark("  scatter");
+    // row i = its own columns (ascending: canonical CSR) followed by the rows pointing at it,
+    // which arrive in ascending source order (buckets keep the chunk-major row order): one
+    // merge of two sorted runs with deduplication instead of a sort
     std::vector<int64_t> uniq((size_t)n, 0);
-#pragma omp parallel for schedule(dynamic, 256)
-    for (int64_t i = 0; i < n; ++i) {
-        uint32_t *b = tmp.get() + cnt[(size_t)i], *e = tmp.get() + cnt[(size_t)i + 1];
-        std::sort(b, e);
-        uniq[(size_t)i] = std::unique(b, e) - b;
+#pragma omp parallel
+    {
+        std::vector<uint32_t> buf;
+#pragma omp for schedule(dynamic, 1024)
+        for (int64_t i = 0; i < n; ++i) {
+            uint32_t *b = tmp.get() + cnt[(size_t)i], *e = tmp.get() + cnt[(size_t)i + 1];
+            const int32_t *rb = a.colidx + a.rowptr[i], *re = a.colidx + a.rowptr[i + 1];
+            const int64_t own = (re - rb) - (std::binary_search(rb, re, (int32_t)i) ? 1 : 0);  // diagonal skipped
+            uint32_t *mid = b + own;
+            buf.resize((size_t)(e - b));
+            uint32_t *o = buf.data();
+            uint32_t *x = b, *y = mid;
+            while (x < mid || y < e) {
+                uint32_t v;
+                if (y >= e || (x < mid && *x <= *y)) v = *x++; else v = *y++;
+                if (o == buf.data() || o[-1] != v) *o++ = v;
+            }
+            std::copy(buf.data(), o, b);
+            uniq[(size_t)i] = o - buf.data();
+        }
     }
     tr.mark("  sort+unique");
     for (int64_t i = 0; i < n; ++i) g.ptr[(size_t)i + 1] = g.ptr[(size_t)i] + uniq[(size_t)i];
     std::vector<int64_t>().swap(indeg);
     g.adj.resize((size_t)g.ptr[(size_t)n]);
-#pragma omp parallel for schedule(dynamic, 256)
+#pragma omp parallel for schedule(dynamic, 1024)
     for (int64_t i = 0; i < n; ++i)
         std::copy(tmp.get() + cnt[(size_t)i], tmp.get() + cnt[(size_t)i] + uniq[(size_t)i],
                   g.adj.begin() + g.ptr[(size_t)i]);

@@ -20,7 +20,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from . import Plan, accspmm_unpermute
+from . import Plan, accspmm_reorder, accspmm_unpermute
 
 PAD = -1  # row id of a padding row in a gathered slab (0xFFFFFFFF as uint32)
 
@@ -28,6 +28,22 @@ PAD = -1  # row id of a padding row in a gathered slab (0xFFFFFFFF as uint32)
 def rank_plan(M, K, rowptr, colidx, vals, rank: int, world: int, **plan_kw) -> Plan:
     """This rank's sub-plan: RowWindows [b_rank, b_rank+1) of the nnz-balanced partition."""
     return Plan(M, K, rowptr, colidx, vals, part=rank, nparts=world, **plan_kw)
+
+
+def broadcast_perm(M: int, rowptr, colidx, src: int = 0, group=None, device=None):
+    """Alg. 1 once: rank ``src`` computes the permutation (accspmm_reorder; the parallel variant
+    of reading R21 above 8M vertices) and broadcasts it, so preprocessing does not replicate the
+    reordering on every rank.  Returns u32[M] new -> old on every rank."""
+    import torch
+    import torch.distributed as dist
+    if dist.get_rank(group) == src:
+        t = torch.from_numpy(accspmm_reorder(M, rowptr, colidx).astype(np.int64))
+    else:
+        t = torch.empty(M, dtype=torch.int64)
+    if device is not None:
+        t = t.to(device)
+    dist.broadcast(t, src=src, group=group)
+    return t.cpu().numpy().astype(np.uint32)
 
 
 def broadcast_B(B, src: int = 0, group=None):

@@ -37,6 +37,14 @@ def _worker(rank, world, port, reorder, result_q):
         B = torch.from_numpy(gen.dense_normal(A.K, N, 5)) if rank == 0 else torch.zeros((A.K, N))
         D.broadcast_B(B, src=0)
         plan = D.rank_plan(A.M, A.K, A.rowptr, A.colidx, vals, rank, world, reorder=reorder, device=-1)
+        if reorder != "off":
+            # Alg. 1 once on rank 0, broadcast: the same sub-plan as reordering on every rank
+            perm = D.broadcast_perm(A.M, A.rowptr, A.colidx)
+            plan_b = D.rank_plan(A.M, A.K, A.rowptr, A.colidx, vals, rank, world, reorder=reorder, device=-1,
+                                 perm=perm)
+            assert np.array_equal(plan_b.export_rows(), plan.export_rows())
+            for k in ("RowWindowOffset", "TCOffset", "SparseAToB", "TCLocalBit"):
+                assert np.array_equal(plan_b.export_format()[k], plan.export_format()[k])
         info = plan.info
         rows = plan.export_rows()
         assert info["nparts"] == world and info["part"] == rank and len(rows) == info["rows"]

@@ -547,3 +547,24 @@ def test_parallel_reorder_invariants():
         R = gen.csr_from_pairs(inv[A.row_ids()], A.colidx.astype(np.int64), 512, 512)
         assert bt.mean_nnz_tc(bt.encode(R.M, R.K, R.rowptr, R.colidx)) > \
             bt.mean_nnz_tc(bt.encode(A.M, A.K, A.rowptr, A.colidx))
+
+
+def test_plan_create_with_supplied_permutation():
+    """accspmm_plan_create_perm: a permutation computed elsewhere gives the same plan as running
+    Alg. 1 inside plan creation; non-bijections and non-square A are rejected."""
+    A = gen.sbm(600, 12, 0.2, 0.01, seed=3)
+    v = gen.values_uniform(A.nnz, 4)
+    perm = acc.accspmm_reorder(A.M, A.rowptr, A.colidx)
+    for mode in ("on", "auto"):
+        p0 = host_plan(A, v, reorder=mode)
+        p1 = host_plan(A, v, reorder=mode, perm=perm)
+        assert np.array_equal(p0.export_rows(), p1.export_rows())
+        for k in ("RowWindowOffset", "TCOffset", "SparseAToB", "TCLocalBit", "values"):
+            assert np.array_equal(p0.export_format()[k], p1.export_format()[k])
+    bad = perm.copy()
+    bad[0] = bad[1]
+    with pytest.raises(acc.AccSpmmError):
+        host_plan(A, v, reorder="on", perm=bad)
+    R = gen.uniform_random(10, 12, 30, seed=1)
+    with pytest.raises(acc.AccSpmmError):
+        host_plan(R, gen.values_uniform(R.nnz, 1), reorder="on", perm=np.arange(10, dtype=np.uint32))
