@@ -190,7 +190,7 @@ constexpr int kChunk = 16;  // TC blocks per staged A-stream chunk
 struct ChunkSmem {
     uint32_t a2b[kChunk * 8];
     uint64_t mask[kChunk];
-    uint32_t tco[kChunk];
+    uint32_t tco[kChunk + 4];  // + TCOffset of the block after the chunk (value staging)
 };
 
 struct WarpSmem {
@@ -547,11 +547,17 @@ struct G4Cfg {
     static constexpr int STAGE_AL = 2 * GRP;
 };
 
-template <int FW, bool F16, int STAGES>
+// VST > 0: each chunk's value range (up to VST values) is staged by one bulk copy a chunk
+// ahead; the chunk metadata is then triple buffered (chunk c + 2 is in flight while the
+// values of chunk c + 1 are copied)
+template <int FW, bool F16, int STAGES, int VST = 0>
 struct G4WarpSmem {
     alignas(128) uint8_t stage[STAGES][G4Cfg<FW, F16>::STAGE_AL];
-    ChunkSmem ch[2];
+    ChunkSmem ch[VST ? 3 : 2];
+    alignas(16) uint8_t vals[VST ? 2 : 1][VST ? VST * (F16 ? 2 : 4) : 16];
+    uint32_t vlo[2];  // first staged value index per buffer (0xFFFFFFFF: over VST, values from L2)
     uint64_t bar[STAGES];
+    uint64_t vbar[2];
 };
 static_assert(sizeof(ChunkSmem) % 16 == 0, "chunk alignment (cp.async 16 B into a2b)");
 
@@ -579,10 +585,11 @@ using G4Maps = G4MapsT<kMaxSliceMaps>;
 inline int map_count(const KParams &kp) { return kp.nslices > 1 && kp.nslices <= kMaxSliceMaps ? kp.nslices : 1; }
 
 template <int FW, bool F16, int WARPS, int STAGES, bool RND, int MINB = 1, int NM = 1, bool LDSM_ = false,
-          bool K8 = false, int VD = 1, bool PF256 = false>
+          bool K8 = false, int VD = 1, int PF256 = 0, int VST = 0>
 __global__ void __launch_bounds__(WARPS * 32, MINB)
     spmm_bittcf_g4_kernel(const KParams p, const __grid_constant__ G4MapsT<NM> maps)
 {
+    static_assert(VST == 0 || (STAGES == 2 && VD == 1), "value staging: default ring only");
     // LDSM (FP16 only): A fragments by ldmatrix.trans straight from the gathered rows (no
     // PRMT packing); gather y is fetched 8 columns early so its rows sit 16 B off gather x's
     // and the 8 row addresses of every ldmatrix phase hit 8 distinct bank groups.  The
@@ -591,9 +598,10 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     constexpr int CH = kChunk;  // blocks per staged chunk
     using CF = Cfg<FW, F16>;
     using GC = G4Cfg<FW, F16>;
-    using SM = G4WarpSmem<FW, F16, STAGES>;
+    using SM = G4WarpSmem<FW, F16, STAGES, VST>;
     using V = typename CF::V;
     constexpr int MT = CF::MT, NV = CF::NV, VW = CF::VW;
+    constexpr int NCB = VST ? 3 : 2;  // chunk metadata buffers
     extern __shared__ __align__(128) uint8_t smem_raw[];
 
     const int lane = threadIdx.x & 31;
@@ -612,6 +620,10 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
                      : "memory");
 #pragma unroll
         for (int s = 0; s < STAGES; ++s) mbar_init(smem_u32(&sm.bar[s]), 1);
+        if constexpr (VST > 0) {
+            mbar_init(smem_u32(&sm.vbar[0]), 1);
+            mbar_init(smem_u32(&sm.vbar[1]), 1);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncwarp();
@@ -631,13 +643,14 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
 
     auto issue_chunk = [&](uint32_t i) {
         if (i < nblk) {
-            auto &c = sm.ch[(i / CH) & 1];
+            auto &c = sm.ch[(i / CH) % NCB];
             const uint32_t b = b0 + i;
             const uint32_t cnt = min((uint32_t)CH, nblk - i);
             if ((uint32_t)lane < cnt) {
                 cp_async8(smem_u32(&c.mask[lane]), p.bits + b + lane, pol_stream);
                 cp_async4(smem_u32(&c.tco[lane]), p.tco + b + lane, pol_stream);
             }
+            if (VST > 0 && (uint32_t)lane == cnt) cp_async4(smem_u32(&c.tco[lane]), p.tco + b + lane, pol_stream);
             const uint4 *src4 = reinterpret_cast<const uint4 *>(p.a2b + (size_t)b * 8);
             if ((uint32_t)lane < 2 * cnt) cp_async16(smem_u32(&c.a2b[4 * lane]), src4 + lane, pol_stream);
             if (2 * CH > 32 && (uint32_t)lane + 32 < 2 * cnt)
@@ -652,16 +665,55 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     constexpr int VR = VD == 1 ? 2 : 4;
     uint32_t vb0[VR], vb1[VR];
 
+    // ---- lane 0 (VST): bulk copy of chunk c's value range (16-byte-aligned superset; the
+    // value allocation carries 16 elements of padding) into value buffer c & 1
+    auto issue_vals = [&](uint32_t c) {
+        if constexpr (VST > 0) {
+            if (lane != 0 || c * CH >= nblk) return;
+            constexpr uint32_t AL = 16 / CF::ES;  // elements per 16 bytes
+            const auto &m = sm.ch[c % NCB];
+            const uint32_t cnt = min((uint32_t)CH, nblk - c * CH);
+            const uint32_t v_lo = m.tco[0] & ~(AL - 1u), v_hi = (m.tco[cnt] + AL - 1u) & ~(AL - 1u);
+            const uint32_t bar = smem_u32(&sm.vbar[c & 1]);
+            if (v_hi - v_lo <= (uint32_t)VST) {
+                sm.vlo[c & 1] = v_lo;
+                mbar_arrive_expect_tx(bar, (v_hi - v_lo) * CF::ES);
+                if (v_hi > v_lo)
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                            smem_u32(sm.vals[c & 1])),
+                        "l"(reinterpret_cast<const char *>(p.vals) + (size_t)v_lo * CF::ES), "r"((v_hi - v_lo) * CF::ES),
+                        "r"(bar)
+                        : "memory");
+            } else {
+                sm.vlo[c & 1] = 0xFFFFFFFFu;
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+            }
+        }
+    };
     // ---- every lane: decode this lane's two tile entries of block j, load values
     auto value_load = [&](uint32_t j, int slot) {
-        const auto &c = sm.ch[(j / CH) & 1];
+        const auto &c = sm.ch[(j / CH) % NCB];
         const uint32_t cs = j & (CH - 1u);
         const uint64_t mask = c.mask[cs];
         const uint32_t t0 = c.tco[cs];
         bool p0, p1;
         const uint32_t i0 = t0 + tile_rank(mask, sh0, p0);
         const uint32_t i1 = t0 + tile_rank(mask, sh1, p1);
-        if constexpr (PF256) {
+        if constexpr (PF256 == 2) {  // values with an L2 evict-first policy (measurement variant)
+            if constexpr (!F16) {
+                const uint32_t *vp = reinterpret_cast<const uint32_t *>(p.vals);
+                uint32_t x0 = 0u, x1 = 0u;
+                if (p0) ldg_nc(x0, vp + i0, pol_stream);
+                if (p1) ldg_nc(x1, vp + i1, pol_stream);
+                vb0[slot] = x0;
+                vb1[slot] = x1;
+            } else {
+                const unsigned short *vp = reinterpret_cast<const unsigned short *>(p.vals);
+                vb0[slot] = p0 ? (uint32_t)__ldg(vp + i0) : 0u;
+                vb1[slot] = p1 ? (uint32_t)__ldg(vp + i1) : 0u;
+            }
+        } else if constexpr (PF256 == 1) {
             if constexpr (!F16) {
                 const uint32_t *vp = reinterpret_cast<const uint32_t *>(p.vals);
                 vb0[slot] = p0 ? ldg_pf256_u32(vp + i0) : 0u;
@@ -670,6 +722,19 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
                 const unsigned short *vp = reinterpret_cast<const unsigned short *>(p.vals);
                 vb0[slot] = p0 ? ldg_pf256_u16(vp + i0) : 0u;
                 vb1[slot] = p1 ? ldg_pf256_u16(vp + i1) : 0u;
+            }
+        } else if constexpr (VST > 0) {  // values staged in shared memory (or from L2 on overflow)
+            const uint32_t vlo = sm.vlo[(j / CH) & 1];
+            if constexpr (!F16) {
+                const uint32_t *vs = reinterpret_cast<const uint32_t *>(sm.vals[(j / CH) & 1]);
+                const uint32_t *vp = reinterpret_cast<const uint32_t *>(p.vals);
+                vb0[slot] = p0 ? (vlo != 0xFFFFFFFFu ? vs[i0 - vlo] : __ldg(vp + i0)) : 0u;
+                vb1[slot] = p1 ? (vlo != 0xFFFFFFFFu ? vs[i1 - vlo] : __ldg(vp + i1)) : 0u;
+            } else {
+                const unsigned short *vs = reinterpret_cast<const unsigned short *>(sm.vals[(j / CH) & 1]);
+                const unsigned short *vp = reinterpret_cast<const unsigned short *>(p.vals);
+                vb0[slot] = p0 ? (uint32_t)(vlo != 0xFFFFFFFFu ? vs[i0 - vlo] : __ldg(vp + i0)) : 0u;
+                vb1[slot] = p1 ? (uint32_t)(vlo != 0xFFFFFFFFu ? vs[i1 - vlo] : __ldg(vp + i1)) : 0u;
             }
         } else if constexpr (!F16) {
             const float *vp = reinterpret_cast<const float *>(p.vals);
@@ -686,7 +751,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     // ---- lane 0: two gather4 of block j's B rows into stage s
     auto issue_tma = [&](uint32_t j, int s) {
         if (lane == 0) {
-            const auto &c = sm.ch[(j / CH) & 1];
+            const auto &c = sm.ch[(j / CH) % NCB];
             const uint32_t cs = j & (CH - 1u);
             // padding lanes hold 0xFFFFFFFF on the device (row -1): the TMA zero-fills them
             const uint4 ca = *reinterpret_cast<const uint4 *>(&c.a2b[cs * 8]);
@@ -852,10 +917,18 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     };
 
     // Prologue: chunk 0 (wait) and chunk 1 in flight; values of block 0; TMA of block 0.
+    // With value staging: chunks 0 and 1 landed, chunk 2 in flight, values of chunks 0 (waited)
+    // and 1 in flight.
     issue_chunk(0);
+    if constexpr (VST > 0) issue_chunk(CH);
     cp_async_wait_all();
     __syncwarp();
-    issue_chunk(CH);
+    issue_chunk(VST > 0 ? 2 * CH : CH);
+    if constexpr (VST > 0) {
+        issue_vals(0);
+        issue_vals(1);
+        if (nblk > 0) mbar_wait(smem_u32(&sm.vbar[0]), 0);
+    }
     after_block(b0);
     if (nblk > 0) value_load(0u, 0);
     if (VD == 2 && nblk > 1) value_load(1u, 1);
@@ -903,7 +976,14 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
             if ((jn & (CH - 1u)) == 0) {  // chunk (jn / CH) must have landed
                 cp_async_wait_all();
                 __syncwarp();
-                issue_chunk(jn + CH);
+                if constexpr (VST > 0) {  // c = jn / CH: metadata c + 2, values c + 1, wait values c
+                    const uint32_t c = jn / CH;
+                    issue_chunk(jn + 2 * CH);
+                    issue_vals(c + 1);
+                    if (jn < nblk) mbar_wait(smem_u32(&sm.vbar[c & 1]), (c >> 1) & 1u);
+                } else {
+                    issue_chunk(jn + CH);
+                }
             }
             if (!checked || jn < nblk) {
                 issue_tma(jn, (u + 1) & 1);
@@ -1041,12 +1121,12 @@ accspmm_status launch_cfg(const KParams &kp, int64_t n_units, cudaStream_t strea
 // NM = 1: one tensor map (the full-width map when several slices exist); NM = kMaxSliceMaps:
 // one map per slice (tensor_map decides; only the default configurations instantiate it)
 template <int FW, bool F16, int WARPS, int STAGES, bool RND = false, int MINB = 1, int NM = 1, bool LDSM = false,
-          bool K8 = false, int VD = 1, bool PF256 = false>
+          bool K8 = false, int VD = 1, int PF256 = 0, int VST = 0>
 accspmm_status launch_g4(const KParams &kp, const G4Maps *map, int64_t n_units, cudaStream_t stream)
 {
-    using SM = G4WarpSmem<FW, F16, STAGES>;
+    using SM = G4WarpSmem<FW, F16, STAGES, VST>;
     const size_t smem = sizeof(SM) * WARPS;
-    auto kern = spmm_bittcf_g4_kernel<FW, F16, WARPS, STAGES, RND, MINB, NM, LDSM, K8, VD, PF256>;
+    auto kern = spmm_bittcf_g4_kernel<FW, F16, WARPS, STAGES, RND, MINB, NM, LDSM, K8, VD, PF256, VST>;
     static int configured_device = -1;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -1167,8 +1247,8 @@ accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, 
         if (rnd) {  // B not pre-rounded: rho(B) applied in registers
             if (kcfg == 20) return launch_g4<FW, F16, 2, 2, true, 1>(kp, map, n_units, stream);
             if (kcfg == 52) {
-                if (multi) return launch_g4<FW, F16, 1, 2, true, MW, NM, false, K8, 1, true>(kp, map, n_units, stream);
-                return launch_g4<FW, F16, 1, 2, true, MW, 1, false, K8, 1, true>(kp, map, n_units, stream);
+                if (multi) return launch_g4<FW, F16, 1, 2, true, MW, NM, false, K8, 1, 1>(kp, map, n_units, stream);
+                return launch_g4<FW, F16, 1, 2, true, MW, 1, false, K8, 1, 1>(kp, map, n_units, stream);
             }
         }
     }
@@ -1180,8 +1260,17 @@ accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, 
             if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, !K8>(kp, map, n_units, stream);
             return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, !K8>(kp, map, n_units, stream);
         case 52:
-            if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, true>(kp, map, n_units, stream);
-            return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, true>(kp, map, n_units, stream);
+            if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 1>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 1>(kp, map, n_units, stream);
+        case 54:  // chunk values staged by bulk copy (256 per chunk buffer)
+            if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 256>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 256>(kp, map, n_units, stream);
+        case 55:  // chunk values staged by bulk copy (512 per chunk buffer)
+            if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 512>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 512>(kp, map, n_units, stream);
+        case 53:  // value loads with an L2 evict-first policy
+            if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 2>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 2>(kp, map, n_units, stream);
         case 50:
             if (multi) return launch_g4<FW, F16, 1, 3, false, MW, NM, LD, K8>(kp, map, n_units, stream);
             return launch_g4<FW, F16, 1, 3, false, MW, 1, LD, K8>(kp, map, n_units, stream);
