@@ -585,10 +585,14 @@ using G4Maps = G4MapsT<kMaxSliceMaps>;
 inline int map_count(const KParams &kp) { return kp.nslices > 1 && kp.nslices <= kMaxSliceMaps ? kp.nslices : 1; }
 
 template <int FW, bool F16, int WARPS, int STAGES, bool RND, int MINB = 1, int NM = 1, bool LDSM_ = false,
-          bool K8 = false, int VD = 1, int PF256 = 0, int VST = 0>
+          bool K8 = false, int VD = 1, int PF256 = 0, int VST = 0, bool HYB = false>
 __global__ void __launch_bounds__(WARPS * 32, MINB)
     spmm_bittcf_g4_kernel(const KParams p, const __grid_constant__ G4MapsT<NM> maps)
 {
+    // HYB: hybrid gather -- odd blocks (stage 1) are gathered by cp.async from every lane (LSU
+    // path) into the exact layout the TMA gives even blocks (stage 0), so the two request
+    // engines share the request-bound regimes (FP16, narrow N)
+    static_assert(!HYB || (STAGES == 2 && WARPS == 1), "hybrid gather: default ring only");
     static_assert(VST == 0 || (STAGES == 2 && VD == 1), "value staging: default ring only");
     // LDSM (FP16 only): A fragments by ldmatrix.trans straight from the gathered rows (no
     // PRMT packing); gather y is fetched 8 columns early so its rows sit 16 B off gather x's
@@ -619,7 +623,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
         asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&maps.m[NM > 1 ? slice : 0]))
                      : "memory");
 #pragma unroll
-        for (int s = 0; s < STAGES; ++s) mbar_init(smem_u32(&sm.bar[s]), 1);
+        for (int s = 0; s < STAGES; ++s) mbar_init(smem_u32(&sm.bar[s]), (HYB && s == 1) ? 32 : 1);
         if constexpr (VST > 0) {
             mbar_init(smem_u32(&sm.vbar[0]), 1);
             mbar_init(smem_u32(&sm.vbar[1]), 1);
@@ -749,7 +753,41 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     };
 
     // ---- lane 0: two gather4 of block j's B rows into stage s
+    // ---- HYB, all lanes: block j's 8 B rows into stage s by 16-byte cp.async, in the TMA's
+    // layout (gather x / y rows, row stride RS, FP16 y rows 16 bytes in); padding lanes are
+    // zero-filled (src-size 0); one noinc arrival per lane on the stage barrier
+    auto issue_ldgsts = [&](uint32_t j, int s) {
+        const auto &c = sm.ch[(j / CH) % NCB];
+        const uint32_t cs = j & (CH - 1u);
+        constexpr int CPR = FW * CF::ES / 16;  // 16-byte chunks per gathered row
+        const char *Bb = reinterpret_cast<const char *>(p.B) + f0 * CF::ES;
+        const int64_t rstride = p.N * CF::ES;
+        const uint32_t st = smem_u32(sm.stage[s]);
+#pragma unroll
+        for (int q0 = 0; q0 < 8 * CPR; q0 += 32) {
+            const int q = q0 + lane;
+            if (8 * CPR % 32 == 0 || q < 8 * CPR) {
+                const int r = q / CPR, cc = q % CPR;
+                const uint32_t row = c.a2b[cs * 8 + r];
+                const int gsel = F16 ? (r & 1) : (r >> 2);
+                const int slot = F16 ? (r >> 1) : (r & 3);
+                const uint32_t shift = (LDSM && gsel) ? 16u : 0u;
+                const uint32_t dst = st + (uint32_t)(gsel * GC::GRP + slot * GC::RS) + shift + (uint32_t)(cc * 16);
+                const bool pad = row == kPadLane;
+                const char *src = pad ? Bb : Bb + (int64_t)row * rstride + cc * 16;
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(pad ? 0 : 16)
+                             : "memory");
+            }
+        }
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&sm.bar[s])) : "memory");
+    };
     auto issue_tma = [&](uint32_t j, int s) {
+        if constexpr (HYB) {
+            if (s == 1) {
+                issue_ldgsts(j, s);
+                return;
+            }
+        }
         if (lane == 0) {
             const auto &c = sm.ch[(j / CH) % NCB];
             const uint32_t cs = j & (CH - 1u);
@@ -1121,12 +1159,12 @@ accspmm_status launch_cfg(const KParams &kp, int64_t n_units, cudaStream_t strea
 // NM = 1: one tensor map (the full-width map when several slices exist); NM = kMaxSliceMaps:
 // one map per slice (tensor_map decides; only the default configurations instantiate it)
 template <int FW, bool F16, int WARPS, int STAGES, bool RND = false, int MINB = 1, int NM = 1, bool LDSM = false,
-          bool K8 = false, int VD = 1, int PF256 = 0, int VST = 0>
+          bool K8 = false, int VD = 1, int PF256 = 0, int VST = 0, bool HYB = false>
 accspmm_status launch_g4(const KParams &kp, const G4Maps *map, int64_t n_units, cudaStream_t stream)
 {
     using SM = G4WarpSmem<FW, F16, STAGES, VST>;
     const size_t smem = sizeof(SM) * WARPS;
-    auto kern = spmm_bittcf_g4_kernel<FW, F16, WARPS, STAGES, RND, MINB, NM, LDSM, K8, VD, PF256, VST>;
+    auto kern = spmm_bittcf_g4_kernel<FW, F16, WARPS, STAGES, RND, MINB, NM, LDSM, K8, VD, PF256, VST, HYB>;
     static int configured_device = -1;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -1262,6 +1300,9 @@ accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, 
         case 52:
             if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 1>(kp, map, n_units, stream);
             return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 1>(kp, map, n_units, stream);
+        case 56:  // hybrid gather: odd blocks by cp.async, even blocks by TMA
+            if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 0, true>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 0, true>(kp, map, n_units, stream);
         case 54:  // chunk values staged by bulk copy (256 per chunk buffer)
             if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 256>(kp, map, n_units, stream);
             return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 256>(kp, map, n_units, stream);
