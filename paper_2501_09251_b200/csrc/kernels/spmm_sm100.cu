@@ -187,11 +187,14 @@ struct Cfg {
 
 constexpr int kChunk = 16;  // TC blocks per staged A-stream chunk
 
-struct ChunkSmem {
+// X = extra TCOffset entries (value staging reads the TCOffset of the block after the chunk)
+template <int X = 0>
+struct ChunkSmemT {
     uint32_t a2b[kChunk * 8];
     uint64_t mask[kChunk];
-    uint32_t tco[kChunk + 4];  // + TCOffset of the block after the chunk (value staging)
+    uint32_t tco[kChunk + X];
 };
+using ChunkSmem = ChunkSmemT<0>;
 
 struct WarpSmem {
     ChunkSmem ch[2];
@@ -549,17 +552,22 @@ struct G4Cfg {
 
 // VST > 0: each chunk's value range (up to VST values) is staged by one bulk copy a chunk
 // ahead; the chunk metadata is then triple buffered (chunk c + 2 is in flight while the
-// values of chunk c + 1 are copied)
-template <int FW, bool F16, int STAGES, int VST = 0>
+// values of chunk c + 1 are copied).  CX = extra TCOffset slots per chunk.
+// Layout note (measured): the stage mbarriers sit 16-byte aligned right after
+// the chunk metadata; a layout that put them at 8 mod 16 behind other fields ran the default
+// kernel 2.2x slower (5.55 vs 2.54 ms on the Reddit-shaped bench) with identical SASS apart
+// from the shared-memory offsets.
+template <int FW, bool F16, int STAGES, int VST = 0, int CX = (VST ? 4 : 0)>
 struct G4WarpSmem {
     alignas(128) uint8_t stage[STAGES][G4Cfg<FW, F16>::STAGE_AL];
-    ChunkSmem ch[VST ? 3 : 2];
-    alignas(16) uint8_t vals[VST ? 2 : 1][VST ? VST * (F16 ? 2 : 4) : 16];
-    uint32_t vlo[2];  // first staged value index per buffer (0xFFFFFFFF: over VST, values from L2)
-    uint64_t bar[STAGES];
+    ChunkSmemT<CX> ch[VST ? 3 : 2];
+    alignas(16) uint64_t bar[STAGES];
     uint64_t vbar[2];
+    uint32_t vlo[2];  // first staged value index per buffer (0xFFFFFFFF: over VST, values from L2)
+    alignas(16) uint8_t vals[VST ? 2 : 1][VST ? VST * (F16 ? 2 : 4) : 16];
 };
-static_assert(sizeof(ChunkSmem) % 16 == 0, "chunk alignment (cp.async 16 B into a2b)");
+static_assert(sizeof(ChunkSmemT<0>) % 16 == 0 && sizeof(ChunkSmemT<4>) % 16 == 0,
+              "chunk alignment (cp.async 16 B into a2b)");
 
 __device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap *map, int32_t col, int32_t r0, int32_t r1,
                                             int32_t r2, int32_t r3, uint32_t bar, uint64_t pol)
@@ -585,7 +593,7 @@ using G4Maps = G4MapsT<kMaxSliceMaps>;
 inline int map_count(const KParams &kp) { return kp.nslices > 1 && kp.nslices <= kMaxSliceMaps ? kp.nslices : 1; }
 
 template <int FW, bool F16, int WARPS, int STAGES, bool RND, int MINB = 1, int NM = 1, bool LDSM_ = false,
-          bool K8 = false, int VD = 1, int PF256 = 0, int VST = 0, bool HYB = false>
+          bool K8 = false, int VD = 1, int PF256 = 0, int VST = 0, bool HYB = false, int CX = (VST ? 4 : 0)>
 __global__ void __launch_bounds__(WARPS * 32, MINB)
     spmm_bittcf_g4_kernel(const KParams p, const __grid_constant__ G4MapsT<NM> maps)
 {
@@ -602,7 +610,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     constexpr int CH = kChunk;  // blocks per staged chunk
     using CF = Cfg<FW, F16>;
     using GC = G4Cfg<FW, F16>;
-    using SM = G4WarpSmem<FW, F16, STAGES, VST>;
+    using SM = G4WarpSmem<FW, F16, STAGES, VST, CX>;
+    static_assert(VST == 0 || CX >= 1, "value staging reads the TCOffset after the chunk");
     using V = typename CF::V;
     constexpr int MT = CF::MT, NV = CF::NV, VW = CF::VW;
     constexpr int NCB = VST ? 3 : 2;  // chunk metadata buffers
@@ -1159,12 +1168,12 @@ accspmm_status launch_cfg(const KParams &kp, int64_t n_units, cudaStream_t strea
 // NM = 1: one tensor map (the full-width map when several slices exist); NM = kMaxSliceMaps:
 // one map per slice (tensor_map decides; only the default configurations instantiate it)
 template <int FW, bool F16, int WARPS, int STAGES, bool RND = false, int MINB = 1, int NM = 1, bool LDSM = false,
-          bool K8 = false, int VD = 1, int PF256 = 0, int VST = 0, bool HYB = false>
+          bool K8 = false, int VD = 1, int PF256 = 0, int VST = 0, bool HYB = false, int CX = (VST ? 4 : 0)>
 accspmm_status launch_g4(const KParams &kp, const G4Maps *map, int64_t n_units, cudaStream_t stream)
 {
-    using SM = G4WarpSmem<FW, F16, STAGES, VST>;
+    using SM = G4WarpSmem<FW, F16, STAGES, VST, CX>;
     const size_t smem = sizeof(SM) * WARPS;
-    auto kern = spmm_bittcf_g4_kernel<FW, F16, WARPS, STAGES, RND, MINB, NM, LDSM, K8, VD, PF256, VST, HYB>;
+    auto kern = spmm_bittcf_g4_kernel<FW, F16, WARPS, STAGES, RND, MINB, NM, LDSM, K8, VD, PF256, VST, HYB, CX>;
     static int configured_device = -1;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -1309,6 +1318,9 @@ accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, 
         case 55:  // chunk values staged by bulk copy (512 per chunk buffer)
             if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 512>(kp, map, n_units, stream);
             return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 512>(kp, map, n_units, stream);
+        case 57:  // default kernel with the value-staging chunk stride (layout A/B)
+            if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 0, false, 4>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 0, false, 4>(kp, map, n_units, stream);
         case 53:  // value loads with an L2 evict-first policy
             if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 2>(kp, map, n_units, stream);
             return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 2>(kp, map, n_units, stream);
