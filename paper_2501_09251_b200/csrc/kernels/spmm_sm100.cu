@@ -34,6 +34,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <cstddef>
 #include <cstdint>
 #include <cstdlib>
 
@@ -612,6 +613,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     using GC = G4Cfg<FW, F16>;
     using SM = G4WarpSmem<FW, F16, STAGES, VST, CX>;
     static_assert(VST == 0 || CX >= 1, "value staging reads the TCOffset after the chunk");
+    static_assert(offsetof(SM, bar) % 16 == 0, "stage mbarriers 16-byte aligned (measured: 2.2x slower otherwise)");
     using V = typename CF::V;
     constexpr int MT = CF::MT, NV = CF::NV, VW = CF::VW;
     constexpr int NCB = VST ? 3 : 2;  // chunk metadata buffers
