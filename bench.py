@@ -480,9 +480,12 @@ def main():
     torch.cuda.synchronize()
     warm_ms = w0.elapsed_time(w1) / args.steps
 
-    bm = acc.bytes_model(info, args.N)
+    # bytes per B element as stored for this execute (TF32 with a pre-rounded B: the 3-byte
+    # image B3) -- the algorithmic B bytes of the bytes model
+    es_b = plan.b_bytes(args.N)
+    bm = acc.bytes_model(info, args.N, es_b)
+    bm["es_b"] = es_b
     # the HBM lower bound of the gather -- every distinct column's B row once
-    es_b = 2 if args.precision == "fp16" else 4
     bm["B_compulsory"] = int(es_b * args.N * np.count_nonzero(np.bincount(A.colidx, minlength=A.K)))
     avg_s = float(np.mean(kernel_ms)) / 1e3 if len(kernel_ms) else t_local / args.steps
     hbm_peak, peak_kind = load_peaks()

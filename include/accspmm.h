@@ -215,6 +215,14 @@ void accspmm_plan_destroy(accspmm_plan *plan);
 /* Copies plan statistics into *info. */
 accspmm_status accspmm_plan_get_info(const accspmm_plan *plan, accspmm_plan_info *info);
 
+/* Bytes per element of B as an execute at width N gathers it (SURVEY §8(d)'s es_B, the
+ * per-valid-lane B bytes of the bytes model): 2 for FP16; for TF32 3 when the pre-rounded
+ * B is stored as its 3-byte image (B3: bits 31..8 of rho(b), lossless because
+ * rho -- P:308, SURVEY Q1 -- leaves bits 12..0 zero; used when the plan's B rows are reused
+ * >= 32 times and the feature slice is 64 or 128 wide), else 4.  Host-only, no device work.
+ * INVALID_VALUE on NULL arguments or N <= 0. */
+accspmm_status accspmm_plan_b_bytes(const accspmm_plan *plan, int64_t N, int32_t *bytes_per_element);
+
 /* Copies the plan's BitTCF arrays to HOST buffers sized from accspmm_plan_info:
  * rwo u32[W+1], tco u32[NB+1], a2b u32[8*NB], bits u64[NB * window_rows/8] (window_rows/8
  * words per block; one for the paper's 8-row windows), vals (float32[plan_nnz]

@@ -72,7 +72,7 @@ EXPORTED = [
     "accspmm_unpermute", "accspmm_debug_round_tf32", "accspmm_debug_decode", "accspmm_status_string",
     "accspmm_last_error", "accspmm_abi_version", "accspmm_plan_set_timing", "accspmm_plan_kernel_times",
     "accspmm_probe_l2_bandwidth", "accspmm_execute_host_batch", "accspmm_csr_transpose",
-    "accspmm_execute_allgather", "accspmm_reorder_parallel", "accspmm_plan_create_perm",
+    "accspmm_execute_allgather", "accspmm_reorder_parallel", "accspmm_plan_create_perm", "accspmm_plan_b_bytes",
 ]
 
 
@@ -96,6 +96,7 @@ def load_library(path: str = LIB_PATH):
         "accspmm_execute_host": ([P, P, I64, P, P], S),
         "accspmm_plan_destroy": ([P], None),
         "accspmm_plan_get_info": ([P, ctypes.POINTER(accspmm_plan_info)], S),
+        "accspmm_plan_b_bytes": ([P, I64, P], S),
         "accspmm_plan_export_format": ([P, P, P, P, P, P], S),
         "accspmm_plan_export_units": ([P, P], S),
         "accspmm_plan_export_rows": ([P, P], S),
@@ -204,6 +205,13 @@ def accspmm_execute_allgather(plan, B_ptr, N, C_ptrs, stream_ptr=None):
 def accspmm_plan_destroy(plan):
     if plan:
         load_library().accspmm_plan_destroy(plan)
+
+
+def accspmm_plan_b_bytes(plan, N) -> int:
+    """Bytes per element of B an execute at width N gathers (4 FP32 rows, 3 the TF32 image B3, 2 FP16)."""
+    out = ctypes.c_int32()
+    _check(load_library().accspmm_plan_b_bytes(plan, int(N), ctypes.byref(out)))
+    return out.value
 
 
 def accspmm_plan_get_info(plan) -> dict:
@@ -475,6 +483,9 @@ class Plan:
     def kernel_times(self) -> np.ndarray:
         return accspmm_plan_kernel_times(self.handle)
 
+    def b_bytes(self, N: int) -> int:
+        return accspmm_plan_b_bytes(self.handle, N)
+
     @property
     def launches_per_execute(self) -> int:
         """SpMM kernel + (TF32 with high B-row reuse, or permuted columns) the B pre-pass --
@@ -491,10 +502,12 @@ class Plan:
         return tiles
 
 
-def bytes_model(info: dict, N: int) -> dict:
-    """SURVEY §8(d) stated bytes model for one execute: A-format + unique B rows per window + C."""
+def bytes_model(info: dict, N: int, es_b: int | None = None) -> dict:
+    """SURVEY §8(d) stated bytes model for one execute: A-format + unique B rows per window + C.
+    es_b = bytes per stored B element as the execute gathers it (Plan.b_bytes(N): 3 for the TF32
+    image B3); default the precision's element size."""
     es_a = 2 if info["precision"] == FP16 else 4
-    es_b = es_a
+    es_b = es_a if es_b is None else es_b
     W, NB = info["W"], info["NB"]
     nw = info.get("window_rows", 8) // 8   # u64 occupancy words per block
     a_fmt = (4 * (W + 1) + 4 * (NB + 1) + 32 * NB + 8 * nw * NB + es_a * info["plan_nnz"]

@@ -431,6 +431,28 @@ static accspmm_status ensure_workspace(const accspmm_plan *p, int64_t N)
     return ACCSPMM_OK;
 }
 
+// rho(B) for TF32: one elementwise pass when each B row is gathered many times
+// (reuse = sum_w |U_w| / K >= kRoundReuse), else in the kernel's registers.
+// Knobs::round_b = 1 (pass) / 2 (kernel) overrides the reuse rule (variants build only).
+static bool in_kernel_rounding(const accspmm_plan *p)
+{
+    const int rmode = knobs().round_b;
+    return p->opt.precision == ACCSPMM_TF32 && p->info.K > 0 &&
+           (rmode == 2 || (rmode != 1 && p->info.sum_U < kRoundReuse * p->info.K));
+}
+
+// Variants build, Knobs::b3 = 1 (measured, not taken: DESIGN.md §7): a pre-rounded TF32 B is
+// written as its 3-byte image (bits 31..8 of rho(b); bits 12..0 are zero) and gathered at 3/4
+// of the bytes by the mma.sync kernel's 64/128-feature slices.  The product library always
+// gathers FP32 rows (Knobs::b3 = 0).
+static bool b3_layout(const accspmm_plan *p, int64_t N, int ndst)
+{
+    return p->opt.precision == ACCSPMM_TF32 && !in_kernel_rounding(p) && p->info.K > 0 &&
+           p->dev.kernel != ACCSPMM_KERNEL_TCGEN05 && knobs().b3 != 0 &&
+           (ndst > 0 || knobs().kcfg < 0 || is_b3_variant(knobs().kcfg)) &&
+           pick_fw(N) >= 64;
+}
+
 static accspmm_status execute_impl(const accspmm_plan *p, const void *B, int64_t N, void *C, float *const *dst,
                                    int ndst, void *stream);
 
@@ -508,14 +530,12 @@ static accspmm_status execute_impl(const accspmm_plan *p, const void *B, int64_t
     // (reuse = sum_w |U_w| / K >= 32), else in the kernel's registers.  With permuted
     // columns the pass is a row gather B' = B[perm] (rounding fused for the TF32 pre-pass).
     const bool tf32 = p->opt.precision == ACCSPMM_TF32;
-    // Knobs::round_b = 1 (pass) / 2 (kernel) overrides the reuse rule (variants build only)
-    const int rmode = knobs().round_b;
-    const bool in_kernel_round = tf32 && p->info.K > 0 &&
-                                 (rmode == 2 || (rmode != 1 && p->info.sum_U < kRoundReuse * p->info.K));
+    const bool in_kernel_round = in_kernel_rounding(p);
     const bool permute = p->dev.col_perm != nullptr && p->info.K > 0;
+    const bool b3 = b3_layout(p, N, ndst);
     if (((tf32 && !in_kernel_round) || permute) && p->info.K > 0) {
         const size_t es = tf32 ? 4 : 2;
-        const size_t need = (size_t)p->info.K * (size_t)N * es;
+        const size_t need = (size_t)p->info.K * (size_t)N * (b3 ? 3 : es);
         if (need > p->Br_bytes) {
             cudaFree(p->Br);
             p->Br = nullptr;
@@ -523,7 +543,10 @@ static accspmm_status execute_impl(const accspmm_plan *p, const void *B, int64_t
             if (cudaMalloc((void **)&p->Br, need) != cudaSuccess) return fail(ACCSPMM_ERR_OUT_OF_MEMORY, "B scratch");
             p->Br_bytes = need;
         }
-        if (permute)
+        if (b3)
+            st = launch_pack_b3((const float *)B, p->Br, permute ? p->dev.col_perm : nullptr, p->info.K, N, pick_fw(N),
+                                stream);
+        else if (permute)
             st = launch_permute_b(B, p->Br, p->dev.col_perm, p->info.K, N * (int64_t)es, tf32 && !in_kernel_round, stream);
         else
             st = launch_round_b((const float *)B, p->Br, p->info.K * N, stream);
@@ -563,7 +586,7 @@ static accspmm_status execute_impl(const accspmm_plan *p, const void *B, int64_t
     if (p->dev.kernel == ACCSPMM_KERNEL_TCGEN05)
         st = launch_spmm_tc05(p->dev, Bk, N, (float *)C, p->ws, p->counters, stream, in_kernel_round);
     else
-        st = launch_spmm(p->dev, Bk, p->zrow, N, (float *)C, p->ws, p->counters, stream, in_kernel_round, dst, ndst);
+        st = launch_spmm(p->dev, Bk, p->zrow, N, (float *)C, p->ws, p->counters, stream, in_kernel_round, dst, ndst, b3);
     if (timed) {
         cudaEventRecord(p->ev[p->ev_n + 1], (cudaStream_t)stream);
         p->ev_n += 2;
@@ -720,6 +743,16 @@ accspmm_status accspmm_plan_get_info(const accspmm_plan *p, accspmm_plan_info *i
 {
     if (!p || !info) return fail(ACCSPMM_ERR_INVALID_VALUE, "NULL argument");
     *info = p->info;
+    return ACCSPMM_OK;
+}
+
+accspmm_status accspmm_plan_b_bytes(const accspmm_plan *p, int64_t N, int32_t *bytes_per_element)
+{
+    if (!p || !bytes_per_element) return fail(ACCSPMM_ERR_INVALID_VALUE, "NULL argument");
+    if (N <= 0) return fail(ACCSPMM_ERR_INVALID_VALUE, "N <= 0");
+    // widths outside 16/32/64/128k run through the padded copy at the next efficient width
+    const int64_t Np = padded_width(N, p->dev.kernel);
+    *bytes_per_element = p->opt.precision == ACCSPMM_FP16 ? 2 : (b3_layout(p, Np, 0) ? 3 : 4);
     return ACCSPMM_OK;
 }
 

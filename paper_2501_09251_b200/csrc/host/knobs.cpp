@@ -27,6 +27,7 @@ const Knobs &knobs()
     k.group_cap = (int)env_i64("ACCSPMM_GROUP_CAP", d.group_cap);
     k.reorder_L = (int)env_i64("ACCSPMM_REORDER_L", d.reorder_L);
     k.reorder_H = (int)env_i64("ACCSPMM_REORDER_H", d.reorder_H);
+    k.b3 = (int)env_i64("ACCSPMM_B3", d.b3);
     return k;
 }
 #else

@@ -37,6 +37,7 @@ struct Knobs {
     int group_cap = 0;         // ACCSPMM_GROUP_CAP: grouped-plan concatenation limit (0 = kGroupCap)
     int reorder_L = 64;        // ACCSPMM_REORDER_L: Alg. 1 candidate window (reading R6)
     int reorder_H = 128;       // ACCSPMM_REORDER_H: Alg. 1 neighbour-list cap (reading R6)
+    int b3 = 0;                // ACCSPMM_B3: 3-byte TF32 image of a pre-rounded B (measured, not taken)
 };
 const Knobs &knobs();          // variants build: re-read on every call (sweeps flip them)
 constexpr bool kVariantsBuild =
@@ -153,12 +154,19 @@ void free_device_format(DeviceFormat &f);
 // Feature-slice width of one warp for a given N (N % 16 == 0): the widest of 128/64/32/16
 // dividing N.  Knobs::fw (variants build, must divide N) overrides it for A/B measurements.
 int pick_fw(int64_t N);
+// variants build: kernel variants (Knobs::kcfg) that read the 3-byte TF32 image of B (B3)
+inline bool is_b3_variant(int kcfg) { return kcfg >= 58 && kcfg <= 61; }
 
 // round_b: the kernel applies rho(B) in registers (B not pre-rounded)
 // dst/ndst (ndst > 0): fused all-gather epilogue instead of C (accspmm_execute_allgather)
+// b3: B is the 3-byte TF32 image written by launch_pack_b3 (TF32, pre-rounded, slice of 64/128)
 accspmm_status launch_spmm(const DevicePlan &p, const void *B, const void *zrow, int64_t N, float *C, float *ws,
                            uint32_t *counters, void *stream, bool round_b, float *const *dst = nullptr,
-                           int ndst = 0);
+                           int ndst = 0, bool b3 = false);
+// rho(B) -> 3-byte TF32 image (K rows x 3N bytes, per FW slice: FW u16 high halves, FW bytes
+// 15..8), rows gathered through perm when non-null (symmetric reordering, R18)
+accspmm_status launch_pack_b3(const float *B, void *out, const uint32_t *perm, int64_t K, int64_t N, int FW,
+                              void *stream);
 // kernels/spmm_tc05_sm100.cu: the tcgen05/TMEM kernel (TF32, N % 128 == 0, any window height)
 accspmm_status launch_spmm_tc05(const DevicePlan &d, const void *B, int64_t N, float *C, float *ws, uint32_t *counters,
                                 void *stream, bool round_b);

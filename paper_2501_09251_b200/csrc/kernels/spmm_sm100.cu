@@ -540,13 +540,17 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase)
 // 8-lane phase then touches 8 distinct bank groups.  Gather 1 carries the rows of
 // fragment x (TF32 rows 0-3, FP16 rows 0,2,4,6), gather 2 those of fragment y.
 
-template <int FW, bool F16>
+// B3 (TF32 only): B is gathered from its 3-byte TF32 image (DESIGN.md §6 "B3"): per feature
+// slice, FW high halves (bits 31..16 of rho(b)) then FW bytes of bits 15..8 -- lossless, since
+// rho(b) has bits 12..0 zero -- so a gathered row is 3*FW bytes instead of 4*FW.
+template <int FW, bool F16, bool B3 = false>
 struct G4Cfg {
     using CF = Cfg<FW, F16>;
-    // box width in elements: gathered rows then sit 32 B off a 128-byte bank period, so the
-    // fragment LDS.128 of one 8-lane phase (4 rows x 2 column groups) hits 8 distinct bank groups
-    static constexpr int BOXE = FW + 32 / CF::ES;
-    static constexpr int RS = BOXE * CF::ES;                 // gathered row stride in smem
+    static_assert(!B3 || (!F16 && FW >= 64), "B3: TF32 slices of 64 or 128 features");
+    // box width: gathered rows then sit 32 B off a 128-byte bank period, so the fragment loads
+    // of one phase (LDS.128: 4 rows x 2 column groups; B3 LDS.64: 4 rows x 4) hit distinct banks
+    static constexpr int RS = B3 ? 3 * FW + 32 : (FW + 32 / CF::ES) * CF::ES;  // gathered row stride
+    static constexpr int BOXE = B3 ? RS / 2 : RS / CF::ES;  // box width in tensor-map elements
     static constexpr int GRP = (4 * RS + 127) / 128 * 128;   // one gather4 (4 rows), 128-aligned
     static constexpr int STAGE_AL = 2 * GRP;
 };
@@ -558,9 +562,9 @@ struct G4Cfg {
 // the chunk metadata; a layout that put them at 8 mod 16 behind other fields ran the default
 // kernel 2.2x slower (5.55 vs 2.54 ms on the Reddit-shaped bench) with identical SASS apart
 // from the shared-memory offsets.
-template <int FW, bool F16, int STAGES, int VST = 0, int CX = (VST ? 4 : 0)>
+template <int FW, bool F16, int STAGES, int VST = 0, int CX = (VST ? 4 : 0), bool B3 = false>
 struct G4WarpSmem {
-    alignas(128) uint8_t stage[STAGES][G4Cfg<FW, F16>::STAGE_AL];
+    alignas(128) uint8_t stage[STAGES][G4Cfg<FW, F16, B3>::STAGE_AL];
     ChunkSmemT<CX> ch[VST ? 3 : 2];
     alignas(16) uint64_t bar[STAGES];
     uint64_t vbar[2];
@@ -594,7 +598,8 @@ using G4Maps = G4MapsT<kMaxSliceMaps>;
 inline int map_count(const KParams &kp) { return kp.nslices > 1 && kp.nslices <= kMaxSliceMaps ? kp.nslices : 1; }
 
 template <int FW, bool F16, int WARPS, int STAGES, bool RND, int MINB = 1, int NM = 1, bool LDSM_ = false,
-          bool K8 = false, int VD = 1, int PF256 = 0, int VST = 0, bool HYB = false, int CX = (VST ? 4 : 0)>
+          bool K8 = false, int VD = 1, int PF256 = 0, int VST = 0, bool HYB = false, int CX = (VST ? 4 : 0),
+          bool B3 = false>
 __global__ void __launch_bounds__(WARPS * 32, MINB)
     spmm_bittcf_g4_kernel(const KParams p, const __grid_constant__ G4MapsT<NM> maps)
 {
@@ -610,12 +615,16 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     constexpr bool LDSM = LDSM_ && F16;
     constexpr int CH = kChunk;  // blocks per staged chunk
     using CF = Cfg<FW, F16>;
-    using GC = G4Cfg<FW, F16>;
-    using SM = G4WarpSmem<FW, F16, STAGES, VST, CX>;
+    using GC = G4Cfg<FW, F16, B3>;
+    using SM = G4WarpSmem<FW, F16, STAGES, VST, CX, B3>;
+    static_assert(!B3 || (!RND && !HYB && VST == 0 && !LDSM_), "B3: pre-rounded B, default ring");
     static_assert(VST == 0 || CX >= 1, "value staging reads the TCOffset after the chunk");
     static_assert(offsetof(SM, bar) % 16 == 0, "stage mbarriers 16-byte aligned (measured: 2.2x slower otherwise)");
     using V = typename CF::V;
-    constexpr int MT = CF::MT, NV = CF::NV, VW = CF::VW;
+    constexpr int MT = CF::MT;
+    // epilogue geometry: lane g owns NV vectors of VW features, vector j = features VW*(8j+g)..
+    // (B3: 8-feature groups 64j + 8g .. +7, the units of its LDS.128 of high halves)
+    constexpr int VW = B3 ? 8 : CF::VW, NV = B3 ? FW / 64 : CF::NV;
     constexpr int NCB = VST ? 3 : 2;  // chunk metadata buffers
     extern __shared__ __align__(128) uint8_t smem_raw[];
 
@@ -814,7 +823,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
             mbar_arrive_expect_tx(bar, 8u * GC::RS);
             // derived here, not held across the loop (registers are the occupancy limit)
             const CUtensorMap *tmap = &maps.m[NM > 1 ? slice : 0];
-            const int32_t tcol = NM > 1 ? 0 : slice * FW;
+            const int32_t tcol = NM > 1 ? 0 : slice * (B3 ? 3 * FW / 2 : FW);  // in map elements
             const int32_t tcol_y = LDSM ? tcol - 8 : tcol;
             if constexpr (!F16) {
                 tma_gather4(st, tmap, tcol, r0, r1, r2, r3, bar, pol_keep);
@@ -836,7 +845,37 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
         const uint8_t *st = sm.stage[s];
         const uint8_t *ra = st + t * GC::RS + CF::VB * g;
         const uint8_t *rb = st + GC::GRP + t * GC::RS + CF::VB * g;
-        if constexpr (LDSM) {
+        if constexpr (B3) {
+            // rows t (k = t, gather x) and t + 4 (gather y); per 8-feature group j: LDS.128 of the
+            // high halves + LDS.64 of the bytes 15..8; one PRMT per element rebuilds the TF32
+            // operand (byte 0 is don't-care: the tensor core reads bits 31..13 only)
+            const uint8_t *xa = st + t * GC::RS, *ya = st + GC::GRP + t * GC::RS;
+#pragma unroll
+            for (int j = 0; j < NV; ++j) {
+                const uint4 hx = *reinterpret_cast<const uint4 *>(xa + 128 * j + 16 * g);
+                const uint2 lx = *reinterpret_cast<const uint2 *>(xa + 2 * FW + 64 * j + 8 * g);
+                const uint4 hy = *reinterpret_cast<const uint4 *>(ya + 128 * j + 16 * g);
+                const uint2 ly = *reinterpret_cast<const uint2 *>(ya + 2 * FW + 64 * j + 8 * g);
+                const uint32_t hxs[4] = {hx.x, hx.y, hx.z, hx.w}, hys[4] = {hy.x, hy.y, hy.z, hy.w};
+                uint32_t xv[8], yv[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const uint32_t sel = (e & 1) ? (0x3202u | ((4u + (e & 3)) << 4)) : (0x1000u | ((4u + (e & 3)) << 4));
+                    xv[e] = __byte_perm(hxs[e >> 1], e < 4 ? lx.x : lx.y, sel);
+                    yv[e] = __byte_perm(hys[e >> 1], e < 4 ? ly.x : ly.y, sel);
+                }
+                if constexpr (K8) {  // FW = 64: one m16n8k8 per tile (k = t from x, t + 4 from y)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        mma_tf32(acc[4 * j + q], xv[2 * q], xv[2 * q + 1], yv[2 * q], yv[2 * q + 1], vb0[slot], vb1[slot]);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) mma_tf32_k4(acc[4 * j + q], xv[2 * q], xv[2 * q + 1], vb0[slot]);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) mma_tf32_k4(acc[4 * j + q], yv[2 * q], yv[2 * q + 1], vb1[slot]);
+                }
+            }
+        } else if constexpr (LDSM) {
             // lane L addresses row k = L & 7 of matrix L >> 3 (8 features); k even in gather x,
             // k odd in gather y (+16 B: its column window starts 8 features early)
             const int k = lane & 7, mx = lane >> 3;
@@ -1126,6 +1165,34 @@ __global__ void round_b_tf32_kernel(const float4 *__restrict__ in, float4 *__res
     }
 }
 
+#ifdef ACCSPMM_VARIANTS
+// rho(B) into the 3-byte TF32 image B3 (G4Cfg): output row r, feature slice s (FW wide) =
+// FW high halves (bits 31..16) then FW bytes (bits 15..8) of rho(B[src][s*FW + f]), src = perm[r]
+// with permuted columns (R18), else r.  rho(b) has bits 12..0 zero, so the image is lossless.
+// One warp per row, one float4 (4 features) per lane step.
+__global__ void pack_b3_kernel(const float4 *__restrict__ in, uint8_t *__restrict__ out, const uint32_t *__restrict__ perm,
+                               int64_t K, int64_t N, int FW)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const int64_t n4 = N / 4;
+    for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < K; r += warps) {
+        const float4 *src = in + (perm ? (int64_t)__ldg(perm + r) : r) * n4;
+        uint8_t *dst = out + r * 3 * N;
+        for (int64_t i = lane; i < n4; i += 32) {
+            const float4 v = __ldcs(src + i);
+            const uint32_t x0 = tf32_rna_bits(__float_as_uint(v.x)), x1 = tf32_rna_bits(__float_as_uint(v.y));
+            const uint32_t x2 = tf32_rna_bits(__float_as_uint(v.z)), x3 = tf32_rna_bits(__float_as_uint(v.w));
+            const int64_t f = 4 * i, sl = f / FW, fl = f - sl * FW;
+            uint8_t *o = dst + sl * 3 * FW;
+            *reinterpret_cast<uint2 *>(o + 2 * fl) = make_uint2(__byte_perm(x0, x1, 0x7632), __byte_perm(x2, x3, 0x7632));
+            *reinterpret_cast<uint32_t *>(o + 2 * FW + fl) = __byte_perm(__byte_perm(x0, x1, 0x0051), __byte_perm(x2, x3, 0x0051), 0x5410);
+        }
+    }
+}
+
+#endif  // ACCSPMM_VARIANTS
+
 // B'[i] = B[perm[i]] row gather (symmetric reordering: the plan's columns are relabelled, so
 // B is permuted once per execute), optionally fused with rho = TF32 RNA.  One warp per row,
 // 16-byte vectors (row_bytes is a multiple of 32: N % 16 == 0).
@@ -1170,12 +1237,13 @@ accspmm_status launch_cfg(const KParams &kp, int64_t n_units, cudaStream_t strea
 // NM = 1: one tensor map (the full-width map when several slices exist); NM = kMaxSliceMaps:
 // one map per slice (tensor_map decides; only the default configurations instantiate it)
 template <int FW, bool F16, int WARPS, int STAGES, bool RND = false, int MINB = 1, int NM = 1, bool LDSM = false,
-          bool K8 = false, int VD = 1, int PF256 = 0, int VST = 0, bool HYB = false, int CX = (VST ? 4 : 0)>
+          bool K8 = false, int VD = 1, int PF256 = 0, int VST = 0, bool HYB = false, int CX = (VST ? 4 : 0),
+          bool B3 = false>
 accspmm_status launch_g4(const KParams &kp, const G4Maps *map, int64_t n_units, cudaStream_t stream)
 {
-    using SM = G4WarpSmem<FW, F16, STAGES, VST, CX>;
+    using SM = G4WarpSmem<FW, F16, STAGES, VST, CX, B3>;
     const size_t smem = sizeof(SM) * WARPS;
-    auto kern = spmm_bittcf_g4_kernel<FW, F16, WARPS, STAGES, RND, MINB, NM, LDSM, K8, VD, PF256, VST, HYB, CX>;
+    auto kern = spmm_bittcf_g4_kernel<FW, F16, WARPS, STAGES, RND, MINB, NM, LDSM, K8, VD, PF256, VST, HYB, CX, B3>;
     static int configured_device = -1;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -1198,14 +1266,16 @@ accspmm_status launch_g4(const KParams &kp, const G4Maps *map, int64_t n_units, 
 
 // TMA tensor maps of B (2D: K rows x width columns, box = BOXE x 1 for gather4), cached in
 // the plan; one per feature slice when the slices fit G4Maps (see G4Maps)
-accspmm_status tensor_map(const DevicePlan &d, const KParams &kp, int FW, bool multi, const G4Maps **out)
+// b3: B is the 3-byte TF32 image (3N bytes per row, slices of 3FW bytes, u16 map elements)
+accspmm_status tensor_map(const DevicePlan &d, const KParams &kp, int FW, bool multi, bool b3, const G4Maps **out)
 {
     const void *B = kp.B;
     const int64_t N = kp.N;
     const int nm = multi ? map_count(kp) : 1;
     const int pv = knobs().l2promo;
     const uint64_t key[4] = {(uint64_t)(uintptr_t)B, (uint64_t)N, (uint64_t)FW,
-                             (uint64_t)(d.precision + 1) | ((uint64_t)nm << 8) | ((uint64_t)pv << 16)};
+                             (uint64_t)(d.precision + 1) | ((uint64_t)nm << 8) | ((uint64_t)pv << 16) |
+                                 ((uint64_t)b3 << 24)};
     G4Maps *maps = reinterpret_cast<G4Maps *>(d.tmap);
     static_assert(sizeof(G4Maps) <= sizeof(d.tmap), "tensor-map cache too small");
     if (!(key[0] == d.tmap_key[0] && key[1] == d.tmap_key[1] && key[2] == d.tmap_key[2] && key[3] == d.tmap_key[3])) {
@@ -1227,12 +1297,15 @@ accspmm_status tensor_map(const DevicePlan &d, const KParams &kp, int FW, bool m
                                             : pv == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
                                                       : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
         for (int m = 0; m < nm; ++m) {
-            cuuint64_t dims[2] = {(cuuint64_t)(nm > 1 ? FW : N), (cuuint64_t)d.K};
-            cuuint64_t strides[1] = {(cuuint64_t)N * es};
-            cuuint32_t box[2] = {(cuuint32_t)(FW + (f16 ? 16 : 8)), 1u};  // G4Cfg::BOXE
+            // B3: a row is 3N bytes = 3N/2 u16 elements, slice m starts at byte 3*FW*m
+            const cuuint64_t slice_e = b3 ? 3 * FW / 2 : FW, row_e = b3 ? 3 * N / 2 : N;
+            cuuint64_t dims[2] = {(cuuint64_t)(nm > 1 ? slice_e : row_e), (cuuint64_t)d.K};
+            cuuint64_t strides[1] = {(cuuint64_t)(b3 ? 3 * N : N * es)};
+            // G4Cfg::BOXE: the slice plus 32 bytes
+            cuuint32_t box[2] = {(cuuint32_t)(b3 ? (3 * FW + 32) / 2 : FW + (f16 ? 16 : 8)), 1u};
             cuuint32_t estr[2] = {1u, 1u};
-            void *base = const_cast<char *>(reinterpret_cast<const char *>(B)) + (size_t)m * FW * es;
-            CUresult r = encode(&maps->m[m], f16 ? CU_TENSOR_MAP_DATA_TYPE_UINT16 : CU_TENSOR_MAP_DATA_TYPE_UINT32, 2,
+            void *base = const_cast<char *>(reinterpret_cast<const char *>(B)) + (size_t)m * FW * (b3 ? 3 : es);
+            CUresult r = encode(&maps->m[m], (f16 || b3) ? CU_TENSOR_MAP_DATA_TYPE_UINT16 : CU_TENSOR_MAP_DATA_TYPE_UINT32, 2,
                                 base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                                 promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
             if (r != CUDA_SUCCESS)
@@ -1257,7 +1330,7 @@ constexpr int tuned_min_warps()
 
 template <int FW, bool F16>
 accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, int64_t n_units, cudaStream_t stream,
-                         bool rnd)
+                         bool rnd, bool b3)
 {
     // Default (measured): TMA gather4, one warp x 2 stages per CTA (the warp's
     // shared-memory addresses are then CTA constants, so the TMA operands need few uniform-
@@ -1270,12 +1343,40 @@ accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, 
     const bool multi = map_count(kp) > 1 && kcfg != 20 && kcfg != 46;
     static const G4Maps no_maps = {};  // no TC blocks (e.g. K = 0): no TMA is ever issued
     if (kcfg < 0 || kcfg >= 20) {
-        accspmm_status st = d.NB > 0 ? tensor_map(d, kp, FW, multi, &map) : (map = &no_maps, ACCSPMM_OK);
+        accspmm_status st = d.NB > 0 ? tensor_map(d, kp, FW, multi, b3, &map) : (map = &no_maps, ACCSPMM_OK);
         if (st != ACCSPMM_OK) return st;
     }
     constexpr int NM = kMaxSliceMaps;
     constexpr bool LD = F16;       // FP16: ldmatrix.trans fragments (measured -10.5%)
     constexpr bool K8 = FW <= 64;  // TF32: one m16n8k8 per tile at FW <= 64 (-6% at N = 64)
+#ifdef ACCSPMM_VARIANTS
+    if constexpr (!F16 && FW >= 64) {
+        // TF32 with a pre-rounded B gathered from its 3-byte image (G4Cfg B3; measured, not
+        // taken: DESIGN.md §7 -- the kernel is issue/latency-bound, the 24% fewer gathered
+        // bytes do not offset the 32 PRMT per block that rebuild the operands)
+        if (b3 && kcfg == 58) {  // B3 with values two blocks ahead (4-slot value ring)
+            if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, false, K8, 2, 0, 0, false, 0, true>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 2, false, MW, 1, false, K8, 2, 0, 0, false, 0, true>(kp, map, n_units, stream);
+        }
+        if (b3 && kcfg == 60) {  // B3, 3-stage TMA ring (2 blocks of lookahead), 18 warps per SM
+            if (multi) return launch_g4<FW, F16, 1, 3, false, 18, NM, false, K8, 1, 0, 0, false, 0, true>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 3, false, 18, 1, false, K8, 1, 0, 0, false, 0, true>(kp, map, n_units, stream);
+        }
+        if (b3 && kcfg == 61) {  // B3, 4-stage TMA ring (3 blocks of lookahead), 14 warps per SM
+            if (multi) return launch_g4<FW, F16, 1, 4, false, 14, NM, false, K8, 1, 0, 0, false, 0, true>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 4, false, 14, 1, false, K8, 1, 0, 0, false, 0, true>(kp, map, n_units, stream);
+        }
+        if (b3 && kcfg == 59) {  // B3 with 24 resident warps per SM (register cap 85)
+            if (multi) return launch_g4<FW, F16, 1, 2, false, 24, NM, false, K8, 1, 0, 0, false, 0, true>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 2, false, 24, 1, false, K8, 1, 0, 0, false, 0, true>(kp, map, n_units, stream);
+        }
+        if (b3) {
+            if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, false, K8, 1, 0, 0, false, 0, true>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 2, false, MW, 1, false, K8, 1, 0, 0, false, 0, true>(kp, map, n_units, stream);
+        }
+    }
+#endif
+    if (b3) return fail(ACCSPMM_ERR_INTERNAL, "B3 layout: variants build, TF32, 64/128-feature slices only");
 #ifdef ACCSPMM_VARIANTS
     // Measured-and-rejected alternatives, selectable by ACCSPMM_KCFG in the variants build only
     // (libaccspmm_variants.so): 20 = 2 warps per CTA without a launch-bounds minimum (the
@@ -1374,6 +1475,23 @@ accspmm_status launch_round_b(const float *B, float *Br, int64_t n, void *stream
     return ACCSPMM_OK;
 }
 
+accspmm_status launch_pack_b3(const float *B, void *out, const uint32_t *perm, int64_t K, int64_t N, int FW, void *stream)
+{
+#ifndef ACCSPMM_VARIANTS
+    (void)B; (void)out; (void)perm; (void)N; (void)FW; (void)stream;
+    return fail(ACCSPMM_ERR_INTERNAL, "B3 layout: variants build only");
+#else
+    if (K == 0) return ACCSPMM_OK;
+    int64_t grid = (K + 7) / 8;
+    if (grid > 148 * 16) grid = 148 * 16;
+    pack_b3_kernel<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const float4 *>(B),
+                                                                   reinterpret_cast<uint8_t *>(out), perm, K, N, FW);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(ACCSPMM_ERR_CUDA, std::string("pack_b3 launch: ") + cudaGetErrorString(e));
+    return ACCSPMM_OK;
+#endif
+}
+
 accspmm_status launch_permute_b(const void *B, void *Bp, const uint32_t *perm, int64_t K, int64_t row_bytes,
                                 bool round_tf32, void *stream)
 {
@@ -1389,7 +1507,7 @@ accspmm_status launch_permute_b(const void *B, void *Bp, const uint32_t *perm, i
 }
 
 accspmm_status launch_spmm(const DevicePlan &d, const void *B, const void *zrow, int64_t N, float *C, float *ws,
-                           uint32_t *counters, void *stream, bool round_b, float *const *dst, int ndst)
+                           uint32_t *counters, void *stream, bool round_b, float *const *dst, int ndst, bool b3)
 {
     if (d.rows == 0) return ACCSPMM_OK;
     const int FW = pick_fw(N);
@@ -1421,10 +1539,10 @@ accspmm_status launch_spmm(const DevicePlan &d, const void *B, const void *zrow,
     const bool f16 = d.precision == ACCSPMM_FP16;
     const bool r = round_b;
     switch (FW) {
-    case 128: return f16 ? launch_fw<128, true>(kp, d, B, d.n_units, s, r) : launch_fw<128, false>(kp, d, B, d.n_units, s, r);
-    case 64: return f16 ? launch_fw<64, true>(kp, d, B, d.n_units, s, r) : launch_fw<64, false>(kp, d, B, d.n_units, s, r);
-    case 32: return f16 ? launch_fw<32, true>(kp, d, B, d.n_units, s, r) : launch_fw<32, false>(kp, d, B, d.n_units, s, r);
-    default: return f16 ? launch_fw<16, true>(kp, d, B, d.n_units, s, r) : launch_fw<16, false>(kp, d, B, d.n_units, s, r);
+    case 128: return f16 ? launch_fw<128, true>(kp, d, B, d.n_units, s, r, b3) : launch_fw<128, false>(kp, d, B, d.n_units, s, r, b3);
+    case 64: return f16 ? launch_fw<64, true>(kp, d, B, d.n_units, s, r, b3) : launch_fw<64, false>(kp, d, B, d.n_units, s, r, b3);
+    case 32: return f16 ? launch_fw<32, true>(kp, d, B, d.n_units, s, r, b3) : launch_fw<32, false>(kp, d, B, d.n_units, s, r, b3);
+    default: return f16 ? launch_fw<16, true>(kp, d, B, d.n_units, s, r, b3) : launch_fw<16, false>(kp, d, B, d.n_units, s, r, b3);
     }
 }
 

@@ -16,7 +16,8 @@ import gen  # noqa: E402
 import paper_2501_09251_b200 as acc  # noqa: E402
 from gpu_util import assert_bit_exact, assert_within, run  # noqa: E402
 
-KCFGS = ["20", "46", "47", "48", "49", "50", "51", "52", "53", "54", "55", "56", "57", "10", "11", "12"]
+KCFGS = ["20", "46", "47", "48", "49", "50", "51", "52", "53", "54", "55", "56", "57", "58", "59", "60", "61", "10", "11", "12",
+         "b3"]
 
 
 def main():
@@ -27,13 +28,18 @@ def main():
     Bf = gen.dense_normal(A.K, 128, 5)
     for precision in ("tf32", "fp16"):
         for kcfg in KCFGS:
-            os.environ["ACCSPMM_KCFG"] = kcfg
+            # "b3": the default kernel reading the 3-byte TF32 image of B (ACCSPMM_B3=1); 58-61
+            # are B3 variants (the knob is on for them, off for the others)
+            os.environ["ACCSPMM_KCFG"] = "-1" if kcfg == "b3" else kcfg
+            os.environ["ACCSPMM_B3"] = "1" if kcfg in ("b3", "58", "59", "60", "61") else "0"
             res = {"kcfg": kcfg, "precision": precision, "ok": True}
             try:
                 for N in (64, 256):
                     B = gen.dense_int(A.K, N, 2)
                     C, p = run(A, v, B, precision, balance="on", unit_cap=32)
                     assert p.info["n_split_windows"] > 0
+                    if kcfg == "b3" and precision == "tf32":
+                        assert p.b_bytes(N) == 3, p.b_bytes(N)   # the B3 path really ran
                     assert_bit_exact(C, A, v, B, precision)
                 Cf, _ = run(A, vf, Bf, precision)
                 assert_within(Cf, A, vf, Bf, precision)
@@ -41,6 +47,7 @@ def main():
                 res.update(ok=False, err=repr(e)[:400])
             print(json.dumps(res), flush=True)
     os.environ.pop("ACCSPMM_KCFG", None)
+    os.environ.pop("ACCSPMM_B3", None)
     _ = np
 
 

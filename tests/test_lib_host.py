@@ -568,3 +568,18 @@ def test_plan_create_with_supplied_permutation():
     R = gen.uniform_random(10, 12, 30, seed=1)
     with pytest.raises(acc.AccSpmmError):
         host_plan(R, gen.values_uniform(R.nnz, 1), reorder="on", perm=np.arange(10, dtype=np.uint32))
+
+
+def test_plan_b_bytes_reports_stored_b_element_size():
+    """accspmm_plan_b_bytes (the es_B of the bytes model): the product library gathers FP32 rows
+    for TF32 (the 3-byte image B3 is a variants-build measurement) and FP16 rows for FP16."""
+    A = gen.uniform_random(300, 40, 3000, seed=2)       # high B-row reuse: the pre-round pass runs
+    v = gen.values_uniform(A.nnz, 3)
+    for prec, es in (("tf32", 4), ("fp16", 2)):
+        p = acc.Plan(A.M, A.K, A.rowptr, A.colidx, v, precision=prec, device=-1)
+        assert p.info["sum_U"] >= 32 * A.K
+        for N in (16, 64, 128, 602):
+            assert p.b_bytes(N) == es
+        with pytest.raises(acc.AccSpmmError):
+            p.b_bytes(0)
+        p.close()

@@ -1,7 +1,7 @@
 """Tuning sweep (GPU box): one matrix, many plan/kernel variants, CUDA-event timing per variant.
 
 usage: python tools/sweep.py --config reddit --N 128 --variants 'kcfg=0' 'kcfg=1,cap=256' ...
-variant keys: kcfg (ACCSPMM_KCFG), fw (ACCSPMM_FW), cap, balance, reorder, precision, N
+variant keys: kcfg (ACCSPMM_KCFG), fw (ACCSPMM_FW), b3 (ACCSPMM_B3), cap, balance, reorder, precision, N
 """
 import argparse
 import json
@@ -46,6 +46,7 @@ def main():
         os.environ["ACCSPMM_SLICE_MAJOR"] = kv.get("sm", "1")
         os.environ["ACCSPMM_L2PROMO"] = kv.get("promo", "3")
         os.environ["ACCSPMM_L2_PERSIST"] = kv.get("persist", "0")
+        os.environ["ACCSPMM_B3"] = kv.get("b3", "1")
         if "gcap" in kv:
             os.environ["ACCSPMM_GROUP_CAP"] = kv["gcap"]
         else:
