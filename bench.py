@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--build", default="device", choices=["host", "device"], help="BitTCF builder")
     ap.add_argument("--window-rows", type=int, default=0, help="rows per RowWindow: 0/8 = paper, 16/32 = tall (R20)")
     ap.add_argument("--kernel", default="auto", choices=["auto", "mma_sync", "tcgen05"])
+    ap.add_argument("--hot-cols", default="auto", choices=["auto", "on", "off"],
+                    help="columns relabelled by in-degree with per-block L2 hotness tags (reading R22)")
     ap.add_argument("--allgather", default="none", choices=["none", "nccl", "fused"],
                     help="N > 1: also time assembling the full C on every rank (NCCL all-gather + "
                          "un-permute, or the fused epilogue into symmetric memory); reported as "
@@ -154,7 +156,7 @@ def ncu_traffic(args, world):
            sys.executable, os.path.abspath(__file__), "--ncu-child", "--config", args.config, "--N", str(args.N),
            "--precision", args.precision, "--reorder", args.reorder, "--balance", args.balance,
            "--unit-cap", str(args.unit_cap), "--build", args.build, "--window-rows", str(args.window_rows),
-           "--kernel", args.kernel]
+           "--kernel", args.kernel, "--hot-cols", args.hot_cols]
     if args.permute_cols:
         cmd.append("--permute-cols")
     env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK=os.environ.get("LOCAL_RANK", "0"))
@@ -197,7 +199,7 @@ def run_ncu_child(args):
     plan = acc.Plan(A.M, A.K, A.rowptr, A.colidx, vals, precision=args.precision, reorder=args.reorder,
                     balance=args.balance, unit_cap=args.unit_cap, device=torch.cuda.current_device(),
                     permute_cols=args.permute_cols, build=args.build, window_rows=args.window_rows,
-                    kernel=args.kernel)
+                    kernel=args.kernel, hot_cols=args.hot_cols)
     Bd = torch.from_numpy(B).to(device="cuda", dtype=torch.float16 if args.precision == "fp16" else torch.float32)
     C = torch.empty((plan.out_rows, args.N), dtype=torch.float32, device="cuda")
     for _ in range(3):
@@ -304,7 +306,7 @@ def workload_config(args, cfg, A, world):
             "N": args.N, "precision": args.precision, "reorder": args.reorder, "balance": args.balance,
             "permute_cols": bool(getattr(args, "permute_cols", False)),
             "l2": "none" if args.no_flush else f"flushed between timed steps ({L2_FLUSH_BYTES >> 20} MiB write)",
-            "window_rows": args.window_rows or 8, "kernel": args.kernel,
+            "window_rows": args.window_rows or 8, "kernel": args.kernel, "hot_cols": args.hot_cols,
             "parallelism": f"rowwindow-nnz-partition x{world}"}
 
 
@@ -399,7 +401,7 @@ def main():
     plan = acc.Plan(A.M, A.K, A.rowptr, A.colidx, vals, precision=args.precision, reorder=args.reorder,
                     balance=args.balance, unit_cap=args.unit_cap, part=rank, nparts=world, device=local,
                     permute_cols=args.permute_cols, build=args.build, window_rows=args.window_rows,
-                    kernel=args.kernel, perm=perm)
+                    kernel=args.kernel, perm=perm, hot_cols=args.hot_cols)
     plan_s = time.perf_counter() - t0
     info = plan.info
     tdt = torch.float16 if args.precision == "fp16" else torch.float32
@@ -589,7 +591,7 @@ def main():
             "gpu_launches": args.steps * plan.launches_per_execute,
             "plan": {k: info[k] for k in ("W", "NB", "sum_U", "mean_nnz_tc", "ibd", "balanced", "grouped", "unit_cap",
                                           "n_units", "n_split_windows", "n_segments", "reorder_applied",
-                                          "cols_permuted", "ms_reorder", "ms_build", "ms_schedule", "ms_upload",
+                                          "cols_permuted", "hot_cols", "ms_reorder", "ms_build", "ms_schedule", "ms_upload",
                                           "device_bytes")},
             "plan_build": args.build,
             "warm": {"ms_per_step": warm_ms, "value": 2.0 * A.nnz * args.N / (warm_ms / 1e3) / 1e9,

@@ -86,15 +86,30 @@ typedef struct {
     int32_t device;     /* CUDA device ordinal; -1 = host-only plan (format + schedule, no upload)  */
     int32_t build;      /* accspmm_build_mode; default ACCSPMM_BUILD_HOST                            */
     int32_t permute_cols; /* 1: when a row permutation is applied (square A), relabel the columns with
-                             it too (A' = P A P^T); every execute then gathers
-                             B' = P B on the device before the SpMM (fused with the TF32 rounding
+                             it too (A' = P A P^T): windows condense their columns
+                             in the new order; the device copy of SparseAToB keeps each column's
+                             ORIGINAL id, so execute gathers B's rows directly (no B' = P B
                              pass).  C is unchanged.  Default 0 (rows only, reading Q12).          */
     int32_t window_rows;  /* rows per RowWindow: 0 or 8 = the paper's BitTCF (8x8 tiles);
                              16 or 32 = tall windows (reading R20: wh x 8 tiles, wh/8 u64 occupancy
                              words per block) -- TF32 only, executed by the tcgen05 kernel.       */
     int32_t kernel;       /* accspmm_kernel: which SpMM kernel executes the plan (default AUTO)   */
-    int32_t reserved[5];
+    int32_t hot_cols;     /* accspmm_hot_mode; reading R22 (DESIGN.md §3/§6): relabel the columns by
+                             descending in-degree so each window condenses its hottest columns
+                             first, and tag every TC block with the hotness of its first column;
+                             when B exceeds L2 the kernel then gathers hot blocks with an L2
+                             evict_last policy and the rest evict_first.  C is unchanged.  Only
+                             for 8-row windows on the mma.sync kernel, without permute_cols, and
+                             K < 2^27.  Default AUTO: on iff K >= 2^20 and the 1% most referenced
+                             of the referenced columns carry >= 10% of the plan's nnz.            */
+    int32_t reserved[4];
 } accspmm_options;
+
+typedef enum {
+    ACCSPMM_HOT_AUTO = 0,
+    ACCSPMM_HOT_ON = 1,
+    ACCSPMM_HOT_OFF = 2
+} accspmm_hot_mode;
 
 typedef enum {
     ACCSPMM_KERNEL_AUTO = 0,     /* 8-row windows: mma.sync kernel; tall windows: tcgen05 kernel        */
@@ -129,7 +144,8 @@ typedef struct {
                                    plans under the automatic cap, else = unit_cap                    */
     int64_t window_rows;        /* rows per RowWindow of this plan (8 = the paper's BitTCF)           */
     int64_t kernel;             /* accspmm_kernel the plan executes with (resolved, never AUTO)       */
-    int64_t reserved[3];
+    int64_t hot_cols;           /* 1: columns relabelled by in-degree with per-block hotness tags (R22) */
+    int64_t reserved[2];
 } accspmm_plan_info;
 
 /* Fills *opt with the defaults listed above.  Never fails for a non-null opt. */

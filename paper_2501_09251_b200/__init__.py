@@ -29,6 +29,7 @@ PRECISION = {"tf32": TF32, "fp16": FP16}
 BUILD = {"host": 0, "device": 1}
 KERNEL = {"auto": 0, "mma_sync": 1, "tcgen05": 2}
 KERNEL_NAME = {v: k for k, v in KERNEL.items()}
+HOT = {"auto": 0, "on": 1, "off": 2}
 NO_SPLIT = 0xFFFFFFFF
 
 
@@ -42,7 +43,8 @@ class accspmm_options(ctypes.Structure):
     _fields_ = [("precision", ctypes.c_int32), ("reorder", ctypes.c_int32), ("balance", ctypes.c_int32),
                 ("unit_cap", ctypes.c_int32), ("part", ctypes.c_int32), ("nparts", ctypes.c_int32),
                 ("device", ctypes.c_int32), ("build", ctypes.c_int32), ("permute_cols", ctypes.c_int32),
-                ("window_rows", ctypes.c_int32), ("kernel", ctypes.c_int32), ("reserved", ctypes.c_int32 * 5)]
+                ("window_rows", ctypes.c_int32), ("kernel", ctypes.c_int32), ("hot_cols", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 4)]
 
 
 _I64 = ["M", "K", "nnz", "rows", "row_begin", "window_begin", "W", "NB", "plan_nnz", "sum_U", "n_units",
@@ -58,7 +60,8 @@ class accspmm_plan_info(ctypes.Structure):
                 + [(n, ctypes.c_double) for n in ("ms_validate", "ms_reorder", "ms_build", "ms_schedule",
                                                    "ms_upload")]
                 + [("grouped", ctypes.c_int64), ("cols_permuted", ctypes.c_int64), ("group_cap", ctypes.c_int64),
-                   ("window_rows", ctypes.c_int64), ("kernel", ctypes.c_int64), ("reserved", ctypes.c_int64 * 3)])
+                   ("window_rows", ctypes.c_int64), ("kernel", ctypes.c_int64), ("hot_cols", ctypes.c_int64),
+                   ("reserved", ctypes.c_int64 * 2)])
 
     def as_dict(self) -> dict:
         return {n: getattr(self, n) for n, _ in self._fields_ if n != "reserved"}
@@ -362,10 +365,12 @@ class Plan:
 
     def __init__(self, M, K, rowptr, colidx, vals, precision="tf32", reorder="auto", balance="auto",
                  unit_cap=0, part=0, nparts=1, device=None, build="host", permute_cols=False, window_rows=0,
-                 kernel="auto", perm=None):
+                 kernel="auto", perm=None, hot_cols="auto"):
         """perm (optional, u32[M] new -> old): an Alg. 1 permutation computed elsewhere (e.g. once
-        on rank 0 and broadcast), used instead of running the reordering again."""
+        on rank 0 and broadcast), used instead of running the reordering again.  hot_cols:
+        auto / on / off -- columns relabelled by in-degree with per-block L2 hotness tags (R22)."""
         opt = accspmm_options_default()
+        opt.hot_cols = HOT[hot_cols]
         opt.window_rows = int(window_rows)
         opt.kernel = KERNEL[kernel]
         opt.build = BUILD[build]
@@ -488,11 +493,10 @@ class Plan:
 
     @property
     def launches_per_execute(self) -> int:
-        """SpMM kernel + (TF32 with high B-row reuse, or permuted columns) the B pre-pass --
-        mirrors accspmm_execute."""
+        """SpMM kernel + (TF32 with high B-row reuse) the rho(B) pre-pass -- mirrors
+        accspmm_execute (relabelled columns gather B's original rows: no pass)."""
         i = self.info
-        pre = (self.precision == "tf32" and i["K"] > 0 and i["sum_U"] >= 32 * i["K"]) or \
-            (i["cols_permuted"] and i["K"] > 0)
+        pre = self.precision == "tf32" and i["K"] > 0 and i["sum_U"] >= 32 * i["K"]
         return 2 if pre else 1
 
     def debug_decode(self, stream=None):

@@ -16,6 +16,7 @@ struct accspmm_plan {
     accspmm::HostFormat host;           // kept only for host-only plans
     std::vector<uint32_t> units_host;   // [n_units][8]
     std::vector<uint32_t> orig_rows;    // slab row -> original row
+    std::vector<uint32_t> colmap;       // relabelled columns (permute_cols, R22): original -> new id
     accspmm::DevicePlan dev{};
     // split-window workspace (grown on demand by execute)
     mutable float *ws = nullptr;
@@ -113,7 +114,7 @@ static void free_device(accspmm_plan *p)
 {
     auto &d = p->dev;
     cudaFree(d.rwo); cudaFree(d.tco); cudaFree(d.a2b); cudaFree(d.bits); cudaFree(d.vals);
-    cudaFree(d.units); cudaFree(d.row_map); cudaFree(d.col_perm); cudaFree(d.orig_map);
+    cudaFree(d.units); cudaFree(d.row_map); cudaFree(d.orig_map);
     cudaFree(p->ws); cudaFree(p->counters); cudaFree(p->dB); cudaFree(p->dC); cudaFree(p->Br); cudaFree(p->zrow);
     cudaFree(p->dB2); cudaFree(p->dC2);
     p->dB2 = nullptr; p->dC2 = nullptr;
@@ -225,6 +226,8 @@ static accspmm_status plan_create_impl(int64_t M, int64_t K, const int64_t *rowp
     if (wh != 8 && wh != 16 && wh != 32) return fail(ACCSPMM_ERR_INVALID_VALUE, "window_rows must be 0, 8, 16 or 32");
     if (opt.kernel < ACCSPMM_KERNEL_AUTO || opt.kernel > ACCSPMM_KERNEL_TCGEN05)
         return fail(ACCSPMM_ERR_INVALID_VALUE, "unknown kernel");
+    if (opt.hot_cols < ACCSPMM_HOT_AUTO || opt.hot_cols > ACCSPMM_HOT_OFF)
+        return fail(ACCSPMM_ERR_INVALID_VALUE, "unknown hot_cols mode");
     if (wh > kWindow && opt.kernel == ACCSPMM_KERNEL_MMA_SYNC)
         return fail(ACCSPMM_ERR_UNSUPPORTED, "the mma.sync kernel runs 8-row windows only");
     const int kernel = (wh > kWindow || opt.kernel == ACCSPMM_KERNEL_TCGEN05) ? ACCSPMM_KERNEL_TCGEN05
@@ -285,14 +288,34 @@ static accspmm_status plan_create_impl(int64_t M, int64_t K, const int64_t *rowp
         wb1 = b[(size_t)opt.part + 1];
     }
     const int64_t r0 = wb0 * wh, r1 = std::min<int64_t>(M, wb1 * wh);
-    // symmetric reordering (NEXT-2): column c becomes inv_perm[c]; B is gathered as B[perm]
-    std::vector<uint32_t> colmap;
+    // Column relabelling: the format is built on A Q^T (colmap = Q^-1: column c -> new id) and the
+    // device SparseAToB is mapped back to original ids (colorig = Q), so B is gathered as is.
+    //  * symmetric reordering (NEXT-2): Q = the row permutation;
+    //  * hot columns (reading R22): Q = columns by descending in-degree over this plan's rows
+    //    (ties by id), so every window condenses its hottest columns first.
+    std::vector<uint32_t> colmap, colorig;
     if (opt.permute_cols && !perm.empty()) {
         colmap.resize((size_t)M);
         for (int64_t r = 0; r < M; ++r) colmap[perm[(size_t)r]] = (uint32_t)r;
+        colorig = perm;
     }
+    const bool hot_ok = wh == kWindow && kernel == ACCSPMM_KERNEL_MMA_SYNC && !opt.permute_cols && K > 0 &&
+                        K <= (int64_t)kHotIdMask;
+    if (opt.hot_cols == ACCSPMM_HOT_ON && !hot_ok) {
+        delete p;
+        return fail(ACCSPMM_ERR_UNSUPPORTED, "hot_cols: 8-row windows, mma.sync kernel, no permute_cols, K < 2^27");
+    }
+    if (hot_ok && (opt.hot_cols == ACCSPMM_HOT_ON || (opt.hot_cols == ACCSPMM_HOT_AUTO && K >= kHotMinCols))) {
+        if (!hot_column_order(a, perm, r0, std::max(r0, r1), opt.hot_cols == ACCSPMM_HOT_ON, colorig)) colorig.clear();
+        if (!colorig.empty()) {
+            colmap.resize((size_t)K);
+            for (int64_t i = 0; i < K; ++i) colmap[colorig[(size_t)i]] = (uint32_t)i;
+        }
+    }
+    const bool hot = !colorig.empty() && !opt.permute_cols;
     const uint32_t *cm = colmap.empty() ? nullptr : colmap.data();
-    I.cols_permuted = cm ? 1 : 0;
+    I.cols_permuted = (cm && opt.permute_cols) ? 1 : 0;
+    I.hot_cols = hot ? 1 : 0;
     HostFormat &F = p->host;
     DeviceFormat DF;
     double ms_csr_upload = 0.0;
@@ -385,7 +408,17 @@ static accspmm_status plan_create_impl(int64_t M, int64_t K, const int64_t *rowp
         }
         if (st == ACCSPMM_OK) st = upload(&d.units, p->units_host, bytes);
         if (st == ACCSPMM_OK && opt.nparts == 1 && !perm.empty()) st = upload(&d.row_map, p->orig_rows, bytes);
-        if (st == ACCSPMM_OK && cm) st = upload(&d.col_perm, perm, bytes);
+        if (st == ACCSPMM_OK && !colorig.empty() && F.NB > 0) {
+            // device SparseAToB -> original column ids (+ hotness tags, R22)
+            uint32_t *dq = nullptr;
+            int64_t qb = 0;
+            st = upload(&dq, colorig, qb);
+            if (st == ACCSPMM_OK) st = launch_relabel_cols(d.a2b, F.NB * 8, dq, hot, nullptr);
+            if (st == ACCSPMM_OK && cudaDeviceSynchronize() != cudaSuccess) st = fail(ACCSPMM_ERR_CUDA, "relabel");
+            cudaFree(dq);
+        }
+        d.hot = hot ? 1 : 0;
+        if (st == ACCSPMM_OK && !colorig.empty()) p->colmap = std::move(colmap);  // export: original -> new id
         if (st == ACCSPMM_OK && opt.nparts > 1) st = upload(&d.orig_map, p->orig_rows, bytes);
         if (st == ACCSPMM_OK) {
             std::vector<uint32_t> zeros(256, 0u);  // 1 KB: covers a 128-wide FP32 feature slice
@@ -527,15 +560,13 @@ static accspmm_status execute_impl(const accspmm_plan *p, const void *B, int64_t
     if (st != ACCSPMM_OK) return st;
     const void *Bk = B;
     // rho(B) for TF32: one elementwise pass when each B row is gathered many times
-    // (reuse = sum_w |U_w| / K >= 32), else in the kernel's registers.  With permuted
-    // columns the pass is a row gather B' = B[perm] (rounding fused for the TF32 pre-pass).
+    // (reuse = sum_w |U_w| / K >= 32), else in the kernel's registers.  Relabelled columns
+    // (permute_cols, R22) need no pass: the device SparseAToB holds original row ids of B.
     const bool tf32 = p->opt.precision == ACCSPMM_TF32;
     const bool in_kernel_round = in_kernel_rounding(p);
-    const bool permute = p->dev.col_perm != nullptr && p->info.K > 0;
     const bool b3 = b3_layout(p, N, ndst);
-    if (((tf32 && !in_kernel_round) || permute) && p->info.K > 0) {
-        const size_t es = tf32 ? 4 : 2;
-        const size_t need = (size_t)p->info.K * (size_t)N * (b3 ? 3 : es);
+    if (tf32 && !in_kernel_round && p->info.K > 0) {
+        const size_t need = (size_t)p->info.K * (size_t)N * (b3 ? 3 : 4);
         if (need > p->Br_bytes) {
             cudaFree(p->Br);
             p->Br = nullptr;
@@ -544,10 +575,7 @@ static accspmm_status execute_impl(const accspmm_plan *p, const void *B, int64_t
             p->Br_bytes = need;
         }
         if (b3)
-            st = launch_pack_b3((const float *)B, p->Br, permute ? p->dev.col_perm : nullptr, p->info.K, N, pick_fw(N),
-                                stream);
-        else if (permute)
-            st = launch_permute_b(B, p->Br, p->dev.col_perm, p->info.K, N * (int64_t)es, tf32 && !in_kernel_round, stream);
+            st = launch_pack_b3((const float *)B, p->Br, nullptr, p->info.K, N, pick_fw(N), stream);
         else
             st = launch_round_b((const float *)B, p->Br, p->info.K * N, stream);
         if (st != ACCSPMM_OK) return st;
@@ -767,9 +795,15 @@ accspmm_status accspmm_plan_export_format(const accspmm_plan *p, uint32_t *rwo, 
     if (st == ACCSPMM_OK) st = export_array(tco, p->host.tco, dev ? p->dev.tco : nullptr, (size_t)I.NB + 1);
     if (st == ACCSPMM_OK) {
         st = export_array(a2b, p->host.a2b, dev ? p->dev.a2b : nullptr, (size_t)I.NB * 8);
-        if (st == ACCSPMM_OK && a2b && dev)  // device padding marker -> the paper format's 0
-            for (size_t q = 0; q < (size_t)I.NB * 8; ++q)
-                if (a2b[q] == kPadLane) a2b[q] = 0u;
+        // device copy -> the paper format: padding marker -> 0; relabelled columns
+        // (permute_cols, R22) hold original ids (+ hotness tags on lane 0) -> the format's new ids
+        if (st == ACCSPMM_OK && a2b && dev)
+            for (size_t q = 0; q < (size_t)I.NB * 8; ++q) {
+                uint32_t v = a2b[q];
+                if (v == kPadLane) { a2b[q] = 0u; continue; }
+                if (p->dev.hot && (q & 7) == 0) v &= kHotIdMask;
+                a2b[q] = p->colmap.empty() ? v : p->colmap[v];
+            }
     }
     if (st == ACCSPMM_OK)
         st = export_array(bits, p->host.bits, dev ? p->dev.bits : nullptr, (size_t)I.NB * (size_t)(I.window_rows / kWindow));

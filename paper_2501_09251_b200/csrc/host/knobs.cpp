@@ -28,6 +28,8 @@ const Knobs &knobs()
     k.reorder_L = (int)env_i64("ACCSPMM_REORDER_L", d.reorder_L);
     k.reorder_H = (int)env_i64("ACCSPMM_REORDER_H", d.reorder_H);
     k.b3 = (int)env_i64("ACCSPMM_B3", d.b3);
+    k.hot_bytes = env_i64("ACCSPMM_HOT_MB", d.hot_bytes >> 20) << 20;
+    k.hot_l2_bytes = env_i64("ACCSPMM_HOT_L2_MB", d.hot_l2_bytes >> 20) << 20;
     return k;
 }
 #else

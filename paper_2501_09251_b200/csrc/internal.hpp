@@ -19,6 +19,15 @@ constexpr int kGroupCap = 32;         // concatenation limit of grouped plans, a
 // TF32 rho(B): a separate rounding pass over B when every B row is gathered at least this
 // many times on average (sum_w |U_w| >= kRoundReuse * K), else cvt.rna in the kernel
 constexpr int64_t kRoundReuse = 32;
+// Hot columns (reading R22): a block's hotness tag sits in bits 31..27 of its lane-0 device
+// SparseAToB entry (column ids < 2^27); the hot set of an execute is the 2^hot_lim hottest
+// columns with 2^hot_lim * N * es <= kHotBytes, used only when B exceeds kHotL2Bytes.
+constexpr int kHotShift = 27;
+constexpr uint32_t kHotIdMask = (1u << kHotShift) - 1u;
+constexpr int64_t kHotMinCols = 1 << 20;          // AUTO: K >= 2^20 ...
+constexpr double kHotSkew = 0.10;                 // ... and the top 1% of the referenced columns carry >= 10% of nnz
+constexpr int64_t kHotBytes = 64ll << 20;         // hot set of one execute (bytes of B)
+constexpr int64_t kHotL2Bytes = 96ll << 20;       // B larger than this: hot/cold policies
 
 // Error plumbing (thread-local message returned by accspmm_last_error).
 accspmm_status fail(accspmm_status s, const std::string &msg);
@@ -38,6 +47,8 @@ struct Knobs {
     int reorder_L = 64;        // ACCSPMM_REORDER_L: Alg. 1 candidate window (reading R6)
     int reorder_H = 128;       // ACCSPMM_REORDER_H: Alg. 1 neighbour-list cap (reading R6)
     int b3 = 0;                // ACCSPMM_B3: 3-byte TF32 image of a pre-rounded B (measured, not taken)
+    int64_t hot_bytes = kHotBytes;       // ACCSPMM_HOT_MB: hot-set size of an execute (R22)
+    int64_t hot_l2_bytes = kHotL2Bytes;  // ACCSPMM_HOT_L2_MB: B size above which hot/cold policies apply
 };
 const Knobs &knobs();          // variants build: re-read on every call (sweeps flip them)
 constexpr bool kVariantsBuild =
@@ -112,6 +123,12 @@ struct ParallelReorderParams {
     ParallelReorderParams();
 };
 std::vector<uint32_t> reorder_alg1(const Csr &a);
+
+// host/hotcols.cpp -- reading R22: colorig = columns by descending in-degree over the plan's rows
+// [r0, r1) of the (reordered) matrix, ties by id.  Without force, applied (returns true) only if
+// the 1% most referenced of the referenced columns carry >= kHotSkew of those rows' nnz.
+bool hot_column_order(const Csr &a, const std::vector<uint32_t> &perm, int64_t r0, int64_t r1, bool force,
+                      std::vector<uint32_t> &colorig);
 std::vector<uint32_t> reorder_alg1_parallel(const Csr &a, const ParallelReorderParams &pp);
 
 // kernels (device side, kernels/*.cu)
@@ -125,7 +142,7 @@ struct DevicePlan {
     void *vals = nullptr;
     uint32_t *units = nullptr;     // [n_units][8]
     uint32_t *row_map = nullptr;   // slab row -> C row (nparts == 1 with a permutation), else null
-    uint32_t *col_perm = nullptr;  // permute_cols: B'[i] = B[col_perm[i]] is gathered each execute
+    int hot = 0;                   // 1: hot-column tags in the lane-0 SparseAToB entries (R22)
     uint32_t *orig_map = nullptr;  // slab row -> original row (fused all-gather); = row_map when nparts == 1
     int64_t K = 0;                 // rows of B (padding lanes gather row K -> TMA zero fill)
     // cached TMA tensor maps of the last B operand (key: ptr, N, FW, dtype): one per feature
@@ -180,6 +197,9 @@ accspmm_status launch_permute_b(const void *B, void *Bp, const uint32_t *perm, i
 accspmm_status launch_unpermute(const float *G, const uint32_t *orig_row, int64_t n_rows, int64_t N,
                                 float *C, void *stream);
 accspmm_status launch_round_tf32(const float *in, float *out, int64_t n, void *stream);
+// device SparseAToB (n entries): new column ids -> original ids colorig[], padding kept; levels:
+// the hotness tag of each block in its lane-0 entry (kHotShift)
+accspmm_status launch_relabel_cols(uint32_t *a2b, int64_t n, const uint32_t *colorig, bool levels, void *stream);
 accspmm_status launch_decode(const DevicePlan &p, float *tiles, void *stream);
 accspmm_status probe_l2_read(int64_t bytes, int iters, double *gbs);
 

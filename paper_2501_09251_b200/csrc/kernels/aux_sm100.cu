@@ -23,6 +23,23 @@ __global__ void unpermute_kernel(const float4 *__restrict__ G, const uint32_t *_
     }
 }
 
+// Device SparseAToB relabelled to ORIGINAL column ids (permute_cols, hot columns R22): entry
+// c' -> colorig[c'], padding lanes kept; with levels, lane 0 of every block also carries in bits
+// 31..27 the bit length of its new id (the block's smallest: a window's columns ascend), i.e.
+// the block's first column has new id < 2^level -- the hotness tag the kernel compares with the
+// execute's hot-set size.
+__global__ void relabel_cols_kernel(uint32_t *__restrict__ a2b, int64_t n, const uint32_t *__restrict__ colorig,
+                                    int levels)
+{
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t c = a2b[e];
+        if (c == kPadLane) continue;
+        uint32_t o = __ldg(colorig + c);
+        if (levels && (e & 7) == 0) o |= (uint32_t)(32 - __clz(c)) << kHotShift;
+        a2b[e] = o;
+    }
+}
+
 __global__ void round_tf32_kernel(const float *__restrict__ in, float *__restrict__ out, int64_t n)
 {
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
@@ -96,6 +113,17 @@ accspmm_status check_launch(const char *what)
 }
 
 }  // namespace
+
+accspmm_status launch_relabel_cols(uint32_t *a2b, int64_t n, const uint32_t *colorig, bool levels, void *stream)
+{
+    if (n == 0) return ACCSPMM_OK;
+    int64_t grid = (n + 255) / 256;
+    if (grid > 148 * 32) grid = 148 * 32;
+    relabel_cols_kernel<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(a2b, n, colorig, levels ? 1 : 0);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(ACCSPMM_ERR_CUDA, std::string("relabel launch: ") + cudaGetErrorString(e));
+    return ACCSPMM_OK;
+}
 
 accspmm_status launch_unpermute(const float *G, const uint32_t *orig_row, int64_t n_rows, int64_t N, float *C,
                                 void *stream)

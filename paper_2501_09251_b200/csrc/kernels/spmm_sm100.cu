@@ -223,6 +223,9 @@ struct KParams {
     // fused all-gather (accspmm_execute_allgather): every finished window row is also (only)
     // written to dst[0..ndst) -- full M x N matrices, local or peer memory -- at orig_map[row]
     int32_t ndst;
+    // hot columns (R22): 255 = plan without hotness tags; else lane-0 SparseAToB entries carry a
+    // tag in bits 31..27 and blocks with tag <= hot_lim gather with evict_last, the rest evict_first
+    int32_t hot_lim;
     const uint32_t *__restrict__ orig_map;
     float *dst[kMaxGatherDst];
 };
@@ -599,7 +602,7 @@ inline int map_count(const KParams &kp) { return kp.nslices > 1 && kp.nslices <=
 
 template <int FW, bool F16, int WARPS, int STAGES, bool RND, int MINB = 1, int NM = 1, bool LDSM_ = false,
           bool K8 = false, int VD = 1, int PF256 = 0, int VST = 0, bool HYB = false, int CX = (VST ? 4 : 0),
-          bool B3 = false>
+          bool B3 = false, bool DEC64 = false>
 __global__ void __launch_bounds__(WARPS * 32, MINB)
     spmm_bittcf_g4_kernel(const KParams p, const __grid_constant__ G4MapsT<NM> maps)
 {
@@ -664,6 +667,13 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     const int k0 = F16 ? g * 8 + 2 * t : g * 8 + t;
     const int k1 = F16 ? k0 + 1 : k0 + 4;
     const uint32_t sh0 = 63u - (uint32_t)k0, sh1 = 63u - (uint32_t)k1;
+    // 32-bit decode (default): k0 < k1 lie in one 32-bit half of the mask (row g's byte), so
+    // rank(k0) = popc(lo & m_lo) + popc(hi & m_hi) with lane-constant masks, and rank(k1) adds
+    // the popcount of the DK bits k0 .. k1-1 (DEC64 = the 64-bit shift form, tile_rank)
+    constexpr uint32_t DK = F16 ? 1u : 4u;
+    const uint32_t hw = (uint32_t)k0 >> 5, p0w = (uint32_t)k0 & 31u;
+    const uint32_t below = (1u << p0w) - 1u;
+    const uint32_t m_lo = hw ? 0xFFFFFFFFu : below, m_hi = hw ? below : 0u;
 
     auto issue_chunk = [&](uint32_t i) {
         if (i < nblk) {
@@ -722,8 +732,18 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
         const uint64_t mask = c.mask[cs];
         const uint32_t t0 = c.tco[cs];
         bool p0, p1;
-        const uint32_t i0 = t0 + tile_rank(mask, sh0, p0);
-        const uint32_t i1 = t0 + tile_rank(mask, sh1, p1);
+        uint32_t i0, i1;
+        if constexpr (DEC64) {
+            i0 = t0 + tile_rank(mask, sh0, p0);
+            i1 = t0 + tile_rank(mask, sh1, p1);
+        } else {
+            const uint32_t lo = (uint32_t)mask, hi = (uint32_t)(mask >> 32);
+            const uint32_t r = (hw ? hi : lo) >> p0w;  // bit 0 = position k0, bit DK = k1
+            p0 = (r & 1u) != 0u;
+            p1 = ((r >> DK) & 1u) != 0u;
+            i0 = t0 + (uint32_t)__popc(lo & m_lo) + (uint32_t)__popc(hi & m_hi);
+            i1 = i0 + (uint32_t)__popc(r & ((1u << DK) - 1u));
+        }
         if constexpr (PF256 == 2) {  // values with an L2 evict-first policy (measurement variant)
             if constexpr (!F16) {
                 const uint32_t *vp = reinterpret_cast<const uint32_t *>(p.vals);
@@ -814,7 +834,13 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
             // padding lanes hold 0xFFFFFFFF on the device (row -1): the TMA zero-fills them
             const uint4 ca = *reinterpret_cast<const uint4 *>(&c.a2b[cs * 8]);
             const uint4 cb = *reinterpret_cast<const uint4 *>(&c.a2b[cs * 8 + 4]);
-            const int32_t r0 = (int32_t)ca.x, r1 = (int32_t)ca.y, r2 = (int32_t)ca.z, r3 = (int32_t)ca.w;
+            uint32_t x0 = ca.x;
+            uint64_t pol = pol_keep;
+            if (p.hot_lim != 255) {  // hot columns (R22): the block's tag picks its L2 policy
+                if ((x0 >> kHotShift) > (uint32_t)p.hot_lim) pol = pol_stream;
+                x0 &= kHotIdMask;
+            }
+            const int32_t r0 = (int32_t)x0, r1 = (int32_t)ca.y, r2 = (int32_t)ca.z, r3 = (int32_t)ca.w;
             const int32_t r4 = (int32_t)cb.x, r5 = (int32_t)cb.y, r6 = (int32_t)cb.z, r7 = (int32_t)cb.w;
             const uint32_t bar = smem_u32(&sm.bar[s]);
             const uint32_t st = smem_u32(sm.stage[s]);
@@ -826,11 +852,11 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
             const int32_t tcol = NM > 1 ? 0 : slice * (B3 ? 3 * FW / 2 : FW);  // in map elements
             const int32_t tcol_y = LDSM ? tcol - 8 : tcol;
             if constexpr (!F16) {
-                tma_gather4(st, tmap, tcol, r0, r1, r2, r3, bar, pol_keep);
-                tma_gather4(st + GC::GRP, tmap, tcol, r4, r5, r6, r7, bar, pol_keep);
+                tma_gather4(st, tmap, tcol, r0, r1, r2, r3, bar, pol);
+                tma_gather4(st + GC::GRP, tmap, tcol, r4, r5, r6, r7, bar, pol);
             } else {
-                tma_gather4(st, tmap, tcol, r0, r2, r4, r6, bar, pol_keep);
-                tma_gather4(st + GC::GRP, tmap, tcol_y, r1, r3, r5, r7, bar, pol_keep);
+                tma_gather4(st, tmap, tcol, r0, r2, r4, r6, bar, pol);
+                tma_gather4(st + GC::GRP, tmap, tcol_y, r1, r3, r5, r7, bar, pol);
             }
         }
     };
@@ -1193,30 +1219,6 @@ __global__ void pack_b3_kernel(const float4 *__restrict__ in, uint8_t *__restric
 
 #endif  // ACCSPMM_VARIANTS
 
-// B'[i] = B[perm[i]] row gather (symmetric reordering: the plan's columns are relabelled, so
-// B is permuted once per execute), optionally fused with rho = TF32 RNA.  One warp per row,
-// 16-byte vectors (row_bytes is a multiple of 32: N % 16 == 0).
-__global__ void permute_b_kernel(const uint4 *__restrict__ in, uint4 *__restrict__ out, const uint32_t *__restrict__ perm,
-                                 int64_t K, int64_t row16, bool rnd)
-{
-    const int lane = threadIdx.x & 31;
-    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-    for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < K; r += warps) {
-        const uint4 *src = in + (int64_t)__ldg(perm + r) * row16;
-        uint4 *dst = out + r * row16;
-        for (int64_t e = lane; e < row16; e += 32) {
-            uint4 v = __ldcs(src + e);
-            if (rnd) {
-                v.x = tf32_rna_bits(v.x);
-                v.y = tf32_rna_bits(v.y);
-                v.z = tf32_rna_bits(v.z);
-                v.w = tf32_rna_bits(v.w);
-            }
-            dst[e] = v;
-        }
-    }
-}
-
 // ------------------------------------------------------------------ launch
 
 #ifdef ACCSPMM_VARIANTS
@@ -1238,12 +1240,12 @@ accspmm_status launch_cfg(const KParams &kp, int64_t n_units, cudaStream_t strea
 // one map per slice (tensor_map decides; only the default configurations instantiate it)
 template <int FW, bool F16, int WARPS, int STAGES, bool RND = false, int MINB = 1, int NM = 1, bool LDSM = false,
           bool K8 = false, int VD = 1, int PF256 = 0, int VST = 0, bool HYB = false, int CX = (VST ? 4 : 0),
-          bool B3 = false>
+          bool B3 = false, bool DEC64 = false>
 accspmm_status launch_g4(const KParams &kp, const G4Maps *map, int64_t n_units, cudaStream_t stream)
 {
     using SM = G4WarpSmem<FW, F16, STAGES, VST, CX, B3>;
     const size_t smem = sizeof(SM) * WARPS;
-    auto kern = spmm_bittcf_g4_kernel<FW, F16, WARPS, STAGES, RND, MINB, NM, LDSM, K8, VD, PF256, VST, HYB, CX, B3>;
+    auto kern = spmm_bittcf_g4_kernel<FW, F16, WARPS, STAGES, RND, MINB, NM, LDSM, K8, VD, PF256, VST, HYB, CX, B3, DEC64>;
     static int configured_device = -1;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -1337,7 +1339,8 @@ accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, 
     // register moves), tuned launch bounds, one tensor map per feature slice when N > FW.
     // FP16 takes its A fragments by ldmatrix.trans.
     constexpr int MW = tuned_min_warps<FW, F16>();
-    const int kcfg = kp.ndst > 0 ? -1 : knobs().kcfg;  // all-gather: default kernel
+    // all-gather and hot-column plans (lane-0 tags): the default kernel (or a B3 variant)
+    const int kcfg = (kp.ndst > 0 || (kp.hot_lim != 255 && !is_b3_variant(knobs().kcfg))) ? -1 : knobs().kcfg;
     const G4Maps *map = nullptr;
     // per-slice maps only for the kernels instantiated with them (variants 20/46: one map)
     const bool multi = map_count(kp) > 1 && kcfg != 20 && kcfg != 46;
@@ -1421,6 +1424,9 @@ accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, 
         case 55:  // chunk values staged by bulk copy (512 per chunk buffer)
             if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 512>(kp, map, n_units, stream);
             return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 512>(kp, map, n_units, stream);
+        case 62:  // default kernel with the 64-bit shift decode (tile_rank) instead of the 32-bit one
+            if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, true>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, true>(kp, map, n_units, stream);
         case 57:  // default kernel with the value-staging chunk stride (layout A/B)
             if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 0, false, 4>(kp, map, n_units, stream);
             return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 0, false, 4>(kp, map, n_units, stream);
@@ -1492,20 +1498,6 @@ accspmm_status launch_pack_b3(const float *B, void *out, const uint32_t *perm, i
 #endif
 }
 
-accspmm_status launch_permute_b(const void *B, void *Bp, const uint32_t *perm, int64_t K, int64_t row_bytes,
-                                bool round_tf32, void *stream)
-{
-    if (K == 0) return ACCSPMM_OK;
-    int64_t grid = (K + 7) / 8;
-    if (grid > 148 * 16) grid = 148 * 16;
-    permute_b_kernel<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const uint4 *>(B),
-                                                                     reinterpret_cast<uint4 *>(Bp), perm, K,
-                                                                     row_bytes / 16, round_tf32);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return fail(ACCSPMM_ERR_CUDA, std::string("permute launch: ") + cudaGetErrorString(e));
-    return ACCSPMM_OK;
-}
-
 accspmm_status launch_spmm(const DevicePlan &d, const void *B, const void *zrow, int64_t N, float *C, float *ws,
                            uint32_t *counters, void *stream, bool round_b, float *const *dst, int ndst, bool b3)
 {
@@ -1530,6 +1522,19 @@ accspmm_status launch_spmm(const DevicePlan &d, const void *B, const void *zrow,
     kp.nslices = (int32_t)(N / FW);
     kp.Krows = (int32_t)d.K;
     kp.ndst = ndst;
+    // hot columns (R22): with B larger than kHotL2Bytes the hot set is the 2^hot_lim hottest
+    // columns whose rows fit kHotBytes; otherwise every block keeps evict_last (hot_lim = 31)
+    kp.hot_lim = 255;
+    if (d.hot) {
+        const int64_t es = d.precision == ACCSPMM_FP16 ? 2 : 4;
+        const int64_t row = N * es, bbytes = d.K * row;
+        int lim = 31;
+        if (bbytes > knobs().hot_l2_bytes) {
+            const int64_t h = std::max<int64_t>(1, knobs().hot_bytes / row);
+            lim = 63 - __builtin_clzll((unsigned long long)h);  // 2^lim <= h
+        }
+        kp.hot_lim = lim;
+    }
     // slice-major grid when N spans several slices: one 128-wide slice of B at a time is the L2
     // working set (N = 512: -13%, N = 256: -3%; Knobs::slice_major = 0 restores slice-fastest)
     kp.slice_major = knobs().slice_major != 0 && kp.nslices > 1;

@@ -583,3 +583,70 @@ def test_plan_b_bytes_reports_stored_b_element_size():
         with pytest.raises(acc.AccSpmmError):
             p.b_bytes(0)
         p.close()
+
+
+def _hot_order(A, rows_old):
+    """Reading R22 written out: columns by descending in-degree over the given (original) rows,
+    ties by ascending id -> colorig (new -> original)."""
+    sel = np.concatenate([np.arange(A.rowptr[o], A.rowptr[o + 1]) for o in rows_old]) if len(rows_old) else \
+        np.zeros(0, np.int64)
+    deg = np.bincount(A.colidx[sel], minlength=A.K)
+    return np.lexsort((np.arange(A.K), -deg))
+
+
+@pytest.mark.parametrize("precision", ["tf32", "fp16"])
+@pytest.mark.parametrize("reorder,nparts", [("off", 1), ("on", 1), ("on", 3)])
+def test_hot_cols_format_is_column_relabelling(precision, reorder, nparts):
+    """hot_cols (reading R22): each plan holds the paper's BitTCF of its slab with the columns
+    relabelled by descending in-degree over the slab's rows (ties by id) -- encoded
+    independently by the oracle on the explicitly relabelled matrix; windows then condense their
+    hottest columns first."""
+    A = gen.powerlaw_directed(3000, 12.0, seed=3)
+    v = gen.values_uniform(A.nnz, 5)
+    full = host_plan(A, v, precision=precision, reorder=reorder, hot_cols="on")
+    perm = full.export_rows().astype(np.int64)              # slab row -> original row
+    rows_seen = 0
+    for part in range(nparts):
+        p = host_plan(A, v, precision=precision, reorder=reorder, hot_cols="on", part=part, nparts=nparts)
+        I = p.info
+        assert I["hot_cols"] == 1 and I["cols_permuted"] == 0
+        rows_old = p.export_rows().astype(np.int64)
+        colorig = _hot_order(A, rows_old)
+        newid = np.empty(A.K, np.int64)
+        newid[colorig] = np.arange(A.K)
+        r, c, vv = [], [], []
+        for i, o in enumerate(rows_old):
+            lo, hi = A.rowptr[o], A.rowptr[o + 1]
+            cc = newid[A.colidx[lo:hi]]
+            k = np.argsort(cc, kind="stable")
+            r.append(np.full(hi - lo, i))
+            c.append(cc[k])
+            vv.append(v[lo:hi][k])
+        r, c, vv = np.concatenate(r), np.concatenate(c), np.concatenate(vv)
+        sl = gen.csr_from_pairs(r, c, len(rows_old), A.K)
+        ref = bt.encode(sl.M, sl.K, sl.rowptr, sl.colidx, _rho_vals(vv, precision))
+        _check_format(p.export_format(), ref, precision)
+        rows_seen += I["rows"]
+    assert rows_seen == A.M and len(perm) == A.M
+
+
+def test_hot_cols_auto_rule_and_validation():
+    """AUTO applies R22 only for K >= 2^20 with a skewed reference distribution (the 1% most
+    referenced of the referenced columns carry >= 10% of nnz); ON is refused where the tags
+    cannot be used."""
+    K = 1 << 20
+    rng = np.random.default_rng(1)
+    rows = np.repeat(np.arange(2000), 10)
+    skew = gen.csr_from_pairs(rows, np.where(rng.random(rows.size) < 0.5, rng.integers(0, 50, rows.size),
+                                             rng.integers(0, K, rows.size)), 2000, K)
+    flat = gen.csr_from_pairs(rows, rng.integers(0, K, rows.size), 2000, K)
+    assert host_plan(skew, np.ones(skew.nnz, np.float32)).info["hot_cols"] == 1
+    assert host_plan(flat, np.ones(flat.nnz, np.float32)).info["hot_cols"] == 0
+    assert host_plan(skew, np.ones(skew.nnz, np.float32), hot_cols="off").info["hot_cols"] == 0
+    small = gen.uniform_random(300, 300, 3000, seed=2)
+    sv = np.ones(small.nnz, np.float32)
+    assert host_plan(small, sv).info["hot_cols"] == 0                       # K < 2^20
+    assert host_plan(small, sv, hot_cols="on").info["hot_cols"] == 1
+    for kw in ({"window_rows": 16}, {"permute_cols": True, "reorder": "on"}):
+        with pytest.raises(acc.AccSpmmError):
+            host_plan(small, sv, hot_cols="on", **kw)

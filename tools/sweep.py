@@ -1,7 +1,8 @@
 """Tuning sweep (GPU box): one matrix, many plan/kernel variants, CUDA-event timing per variant.
 
 usage: python tools/sweep.py --config reddit --N 128 --variants 'kcfg=0' 'kcfg=1,cap=256' ...
-variant keys: kcfg (ACCSPMM_KCFG), fw (ACCSPMM_FW), b3 (ACCSPMM_B3), cap, balance, reorder, precision, N
+variant keys: kcfg (ACCSPMM_KCFG), fw (ACCSPMM_FW), b3 (ACCSPMM_B3), hot (hot_cols plan option),
+hmb / hl2 (ACCSPMM_HOT_MB / ACCSPMM_HOT_L2_MB), cap, balance, reorder, precision, N
 """
 import argparse
 import json
@@ -46,17 +47,19 @@ def main():
         os.environ["ACCSPMM_SLICE_MAJOR"] = kv.get("sm", "1")
         os.environ["ACCSPMM_L2PROMO"] = kv.get("promo", "3")
         os.environ["ACCSPMM_L2_PERSIST"] = kv.get("persist", "0")
-        os.environ["ACCSPMM_B3"] = kv.get("b3", "1")
+        os.environ["ACCSPMM_B3"] = kv.get("b3", "0")
+        os.environ["ACCSPMM_HOT_MB"] = kv.get("hmb", "64")
+        os.environ["ACCSPMM_HOT_L2_MB"] = kv.get("hl2", "96")
         if "gcap" in kv:
             os.environ["ACCSPMM_GROUP_CAP"] = kv["gcap"]
         else:
             os.environ.pop("ACCSPMM_GROUP_CAP", None)
         key = (prec, kv.get("balance", "auto"), int(kv.get("cap", 0)), kv.get("reorder", "off"), kv.get("gcap"),
-               int(kv.get("wh", 0)), kv.get("kernel", "auto"))
+               int(kv.get("wh", 0)), kv.get("kernel", "auto"), kv.get("hot", "auto"))
         if key not in plans:
             t0 = time.perf_counter()
             plans[key] = acc.Plan(A.M, A.K, A.rowptr, A.colidx, vals, precision=prec, balance=key[1],
-                                  unit_cap=key[2], reorder=key[3], window_rows=key[5], kernel=key[6],
+                                  unit_cap=key[2], reorder=key[3], window_rows=key[5], kernel=key[6], hot_cols=key[7],
                                   build="device")
             plans[key].create_s = time.perf_counter() - t0
         p = plans[key]
@@ -86,7 +89,8 @@ def main():
              "model_GBs": bm["total"] / ms / 1e6, "NB": p.info["NB"], "sum_U": p.info["sum_U"],
              "units": p.info["n_units"], "cap": p.info["unit_cap"], "balanced": p.info["balanced"],
              "split": p.info["n_split_windows"], "reorder_ms": p.info["ms_reorder"],
-             "create_s": round(p.create_s, 2), "reorder_applied": p.info["reorder_applied"]}
+             "create_s": round(p.create_s, 2), "reorder_applied": p.info["reorder_applied"],
+             "hot_cols": p.info["hot_cols"]}
         print(json.dumps(r), flush=True)
         res.append(r)
     if a.out:
