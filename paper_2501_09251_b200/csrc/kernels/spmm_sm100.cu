@@ -47,6 +47,16 @@ namespace {
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
+// One lane of a converged warp (elect.sync).  Guarding a TMA issue with it instead of
+// lane == 0 lets the compiler issue the uniform UTMALDG once, without the per-thread ELECT loop
+// and divergent branch it emits for an arbitrary lane predicate (-~10 instructions per block).
+__device__ __forceinline__ bool elect_one()
+{
+    uint32_t pred = 0;
+    asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}\n" : "=r"(pred));
+    return pred != 0;
+}
+
 // A-stream staging copies.  No L2::cache_hint operand: with the constant-folded
 // createpolicy value ptxas (12.9) emitted one LDGSTS of a large kernel with an uninitialised
 // uniform descriptor register (desc[UR1], "illegal instruction" at run time); the policy
@@ -226,6 +236,7 @@ struct KParams {
     // hot columns (R22): 255 = plan without hotness tags; else lane-0 SparseAToB entries carry a
     // tag in bits 31..27 and blocks with tag <= hot_lim gather with evict_last, the rest evict_first
     int32_t hot_lim;
+    uint32_t id_mask;  // kHotIdMask for tagged plans, else all ones
     const uint32_t *__restrict__ orig_map;
     float *dst[kMaxGatherDst];
 };
@@ -602,7 +613,7 @@ inline int map_count(const KParams &kp) { return kp.nslices > 1 && kp.nslices <=
 
 template <int FW, bool F16, int WARPS, int STAGES, bool RND, int MINB = 1, int NM = 1, bool LDSM_ = false,
           bool K8 = false, int VD = 1, int PF256 = 0, int VST = 0, bool HYB = false, int CX = (VST ? 4 : 0),
-          bool B3 = false, bool DEC64 = false>
+          bool B3 = false, bool DEC64 = false, bool EL = true, bool HT = true>
 __global__ void __launch_bounds__(WARPS * 32, MINB)
     spmm_bittcf_g4_kernel(const KParams p, const __grid_constant__ G4MapsT<NM> maps)
 {
@@ -828,18 +839,16 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
                 return;
             }
         }
-        if (lane == 0) {
+        if (EL ? elect_one() : lane == 0) {
             const auto &c = sm.ch[(j / CH) % NCB];
             const uint32_t cs = j & (CH - 1u);
             // padding lanes hold 0xFFFFFFFF on the device (row -1): the TMA zero-fills them
             const uint4 ca = *reinterpret_cast<const uint4 *>(&c.a2b[cs * 8]);
             const uint4 cb = *reinterpret_cast<const uint4 *>(&c.a2b[cs * 8 + 4]);
-            uint32_t x0 = ca.x;
-            uint64_t pol = pol_keep;
-            if (p.hot_lim != 255) {  // hot columns (R22): the block's tag picks its L2 policy
-                if ((x0 >> kHotShift) > (uint32_t)p.hot_lim) pol = pol_stream;
-                x0 &= kHotIdMask;
-            }
+            // hot columns (R22): the block's tag picks its L2 policy (HT = false: untagged plan,
+            // instantiated without this code -- it sits on the TMA issue path of every block)
+            const uint64_t pol = HT && (ca.x >> kHotShift) > (uint32_t)p.hot_lim ? pol_stream : pol_keep;
+            const uint32_t x0 = HT ? ca.x & p.id_mask : ca.x;
             const int32_t r0 = (int32_t)x0, r1 = (int32_t)ca.y, r2 = (int32_t)ca.z, r3 = (int32_t)ca.w;
             const int32_t r4 = (int32_t)cb.x, r5 = (int32_t)cb.y, r6 = (int32_t)cb.z, r7 = (int32_t)cb.w;
             const uint32_t bar = smem_u32(&sm.bar[s]);
@@ -1240,12 +1249,12 @@ accspmm_status launch_cfg(const KParams &kp, int64_t n_units, cudaStream_t strea
 // one map per slice (tensor_map decides; only the default configurations instantiate it)
 template <int FW, bool F16, int WARPS, int STAGES, bool RND = false, int MINB = 1, int NM = 1, bool LDSM = false,
           bool K8 = false, int VD = 1, int PF256 = 0, int VST = 0, bool HYB = false, int CX = (VST ? 4 : 0),
-          bool B3 = false, bool DEC64 = false>
+          bool B3 = false, bool DEC64 = false, bool EL = true, bool HT = true>
 accspmm_status launch_g4(const KParams &kp, const G4Maps *map, int64_t n_units, cudaStream_t stream)
 {
     using SM = G4WarpSmem<FW, F16, STAGES, VST, CX, B3>;
     const size_t smem = sizeof(SM) * WARPS;
-    auto kern = spmm_bittcf_g4_kernel<FW, F16, WARPS, STAGES, RND, MINB, NM, LDSM, K8, VD, PF256, VST, HYB, CX, B3, DEC64>;
+    auto kern = spmm_bittcf_g4_kernel<FW, F16, WARPS, STAGES, RND, MINB, NM, LDSM, K8, VD, PF256, VST, HYB, CX, B3, DEC64, EL, HT>;
     static int configured_device = -1;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -1424,6 +1433,9 @@ accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, 
         case 55:  // chunk values staged by bulk copy (512 per chunk buffer)
             if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 512>(kp, map, n_units, stream);
             return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 512>(kp, map, n_units, stream);
+        case 63:  // default kernel with the TMA issued under lane == 0 instead of elect.sync
+            if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, false>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, false>(kp, map, n_units, stream);
         case 62:  // default kernel with the 64-bit shift decode (tile_rank) instead of the 32-bit one
             if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, true>(kp, map, n_units, stream);
             return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, true>(kp, map, n_units, stream);
@@ -1449,14 +1461,24 @@ accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, 
         }
     }
 #endif
+    // the default kernel, with hot-column tag handling only for tagged plans (R22)
+    const bool ht = kp.hot_lim != 255;
     if constexpr (!F16) {
         if (rnd) {  // B not pre-rounded: rho(B) applied in registers
-            if (multi) return launch_g4<FW, F16, 1, 2, true, MW, NM, false, K8>(kp, map, n_units, stream);
-            return launch_g4<FW, F16, 1, 2, true, MW, 1, false, K8>(kp, map, n_units, stream);
+            if (ht) {
+                if (multi) return launch_g4<FW, F16, 1, 2, true, MW, NM, false, K8, 1, 0, 0, false, 0, false, false, true, true>(kp, map, n_units, stream);
+                return launch_g4<FW, F16, 1, 2, true, MW, 1, false, K8, 1, 0, 0, false, 0, false, false, true, true>(kp, map, n_units, stream);
+            }
+            if (multi) return launch_g4<FW, F16, 1, 2, true, MW, NM, false, K8, 1, 0, 0, false, 0, false, false, true, false>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 2, true, MW, 1, false, K8, 1, 0, 0, false, 0, false, false, true, false>(kp, map, n_units, stream);
         }
     }
-    if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8>(kp, map, n_units, stream);
-    return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8>(kp, map, n_units, stream);
+    if (ht) {
+        if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, true, true>(kp, map, n_units, stream);
+        return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, true, true>(kp, map, n_units, stream);
+    }
+    if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, true, false>(kp, map, n_units, stream);
+    return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, true, false>(kp, map, n_units, stream);
 }
 
 }  // namespace
@@ -1525,6 +1547,7 @@ accspmm_status launch_spmm(const DevicePlan &d, const void *B, const void *zrow,
     // hot columns (R22): with B larger than kHotL2Bytes the hot set is the 2^hot_lim hottest
     // columns whose rows fit kHotBytes; otherwise every block keeps evict_last (hot_lim = 31)
     kp.hot_lim = 255;
+    kp.id_mask = d.hot ? kHotIdMask : 0xFFFFFFFFu;
     if (d.hot) {
         const int64_t es = d.precision == ACCSPMM_FP16 ? 2 : 4;
         const int64_t row = N * es, bbytes = d.K * row;

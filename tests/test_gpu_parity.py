@@ -469,9 +469,9 @@ def test_random_shapes_and_options(seed):
 @pytest.mark.parametrize("precision", PRECISIONS)
 @pytest.mark.parametrize("shape", ["graph", "road"])
 def test_permute_cols_exact(precision, shape):
-    """Symmetric reordering (permute_cols): B' = B[perm] is gathered on the
-    device (fused with the TF32 pre-round on high-reuse graphs, without it on the road grid
-    where rho(B) stays in the kernel); integer data bit-exact, floats within tolerance."""
+    """Symmetric reordering (permute_cols): the columns are relabelled with the
+    rows, the device SparseAToB keeps original ids, so no B' = B[perm] pass runs (only the TF32
+    pre-round at high reuse); integer data bit-exact, floats within tolerance."""
     if shape == "graph":
         A = gen.dcsbm(5000, 250_000, 6, 2.2, 0.15, 3000, seed=8, oversample=1.3)
     else:
@@ -479,7 +479,8 @@ def test_permute_cols_exact(precision, shape):
     v = gen.values_int(A.nnz, 1)
     B = gen.dense_int(A.K, 128, 2)
     C, p = run(A, v, B, precision, reorder="on", permute_cols=True)
-    assert p.info["cols_permuted"] == 1 and p.launches_per_execute == 2
+    pre = precision == "tf32" and p.info["sum_U"] >= 32 * A.K
+    assert p.info["cols_permuted"] == 1 and p.launches_per_execute == (2 if pre else 1)
     assert_bit_exact(C, A, v, B, precision)
     vf = gen.values_uniform(A.nnz, 3)
     Bf = gen.dense_normal(A.K, 256, 4)

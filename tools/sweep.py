@@ -2,7 +2,7 @@
 
 usage: python tools/sweep.py --config reddit --N 128 --variants 'kcfg=0' 'kcfg=1,cap=256' ...
 variant keys: kcfg (ACCSPMM_KCFG), fw (ACCSPMM_FW), b3 (ACCSPMM_B3), hot (hot_cols plan option),
-hmb / hl2 (ACCSPMM_HOT_MB / ACCSPMM_HOT_L2_MB), cap, balance, reorder, precision, N
+hmb / hl2 (ACCSPMM_HOT_MB / ACCSPMM_HOT_L2_MB), rb (ACCSPMM_ROUND_B: 1 pass, 2 in-kernel), cap, balance, reorder, precision, N
 """
 import argparse
 import json
@@ -49,6 +49,7 @@ def main():
         os.environ["ACCSPMM_L2_PERSIST"] = kv.get("persist", "0")
         os.environ["ACCSPMM_B3"] = kv.get("b3", "0")
         os.environ["ACCSPMM_HOT_MB"] = kv.get("hmb", "64")
+        os.environ["ACCSPMM_ROUND_B"] = kv.get("rb", "0")
         os.environ["ACCSPMM_HOT_L2_MB"] = kv.get("hl2", "96")
         if "gcap" in kv:
             os.environ["ACCSPMM_GROUP_CAP"] = kv["gcap"]
