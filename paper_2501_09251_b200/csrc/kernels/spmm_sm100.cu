@@ -613,7 +613,7 @@ inline int map_count(const KParams &kp) { return kp.nslices > 1 && kp.nslices <=
 
 template <int FW, bool F16, int WARPS, int STAGES, bool RND, int MINB = 1, int NM = 1, bool LDSM_ = false,
           bool K8 = false, int VD = 1, int PF256 = 0, int VST = 0, bool HYB = false, int CX = (VST ? 4 : 0),
-          bool B3 = false, bool DEC64 = false, bool EL = true, bool HT = true>
+          bool B3 = false, bool DEC64 = false, int EL = 1, bool HT = true>
 __global__ void __launch_bounds__(WARPS * 32, MINB)
     spmm_bittcf_g4_kernel(const KParams p, const __grid_constant__ G4MapsT<NM> maps)
 {
@@ -839,7 +839,11 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
                 return;
             }
         }
-        if (EL ? elect_one() : lane == 0) {
+        // EL 0: lane 0 issues; 1: an elect.sync lane issues (the body is its branch); 2: every
+        // lane computes the operands (broadcast LDS), only the arrive and the two TMA issues are
+        // predicated on the elected lane, so no divergent branch remains
+        const bool leader = EL == 0 ? lane == 0 : EL == 1 ? elect_one() : true;
+        if (leader) {
             const auto &c = sm.ch[(j / CH) % NCB];
             const uint32_t cs = j & (CH - 1u);
             // padding lanes hold 0xFFFFFFFF on the device (row -1): the TMA zero-fills them
@@ -855,17 +859,20 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
             const uint32_t st = smem_u32(sm.stage[s]);
             // no proxy fence: the stage's previous generic reads fed this warp's mma.sync,
             // which cannot issue before every lane's LDS has returned
-            mbar_arrive_expect_tx(bar, 8u * GC::RS);
+            const bool one = EL == 2 ? elect_one() : true;
+            if (one) mbar_arrive_expect_tx(bar, 8u * GC::RS);
             // derived here, not held across the loop (registers are the occupancy limit)
             const CUtensorMap *tmap = &maps.m[NM > 1 ? slice : 0];
             const int32_t tcol = NM > 1 ? 0 : slice * (B3 ? 3 * FW / 2 : FW);  // in map elements
             const int32_t tcol_y = LDSM ? tcol - 8 : tcol;
-            if constexpr (!F16) {
-                tma_gather4(st, tmap, tcol, r0, r1, r2, r3, bar, pol);
-                tma_gather4(st + GC::GRP, tmap, tcol, r4, r5, r6, r7, bar, pol);
-            } else {
-                tma_gather4(st, tmap, tcol, r0, r2, r4, r6, bar, pol);
-                tma_gather4(st + GC::GRP, tmap, tcol_y, r1, r3, r5, r7, bar, pol);
+            if (one) {
+                if constexpr (!F16) {
+                    tma_gather4(st, tmap, tcol, r0, r1, r2, r3, bar, pol);
+                    tma_gather4(st + GC::GRP, tmap, tcol, r4, r5, r6, r7, bar, pol);
+                } else {
+                    tma_gather4(st, tmap, tcol, r0, r2, r4, r6, bar, pol);
+                    tma_gather4(st + GC::GRP, tmap, tcol_y, r1, r3, r5, r7, bar, pol);
+                }
             }
         }
     };
@@ -1249,7 +1256,7 @@ accspmm_status launch_cfg(const KParams &kp, int64_t n_units, cudaStream_t strea
 // one map per slice (tensor_map decides; only the default configurations instantiate it)
 template <int FW, bool F16, int WARPS, int STAGES, bool RND = false, int MINB = 1, int NM = 1, bool LDSM = false,
           bool K8 = false, int VD = 1, int PF256 = 0, int VST = 0, bool HYB = false, int CX = (VST ? 4 : 0),
-          bool B3 = false, bool DEC64 = false, bool EL = true, bool HT = true>
+          bool B3 = false, bool DEC64 = false, int EL = 1, bool HT = true>
 accspmm_status launch_g4(const KParams &kp, const G4Maps *map, int64_t n_units, cudaStream_t stream)
 {
     using SM = G4WarpSmem<FW, F16, STAGES, VST, CX, B3>;
@@ -1434,8 +1441,11 @@ accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, 
             if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 512>(kp, map, n_units, stream);
             return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 512>(kp, map, n_units, stream);
         case 63:  // default kernel with the TMA issued under lane == 0 instead of elect.sync
-            if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, false>(kp, map, n_units, stream);
-            return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, false>(kp, map, n_units, stream);
+            if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, 0>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, 0>(kp, map, n_units, stream);
+        case 64:  // TMA operands computed by every lane, only the arrive + issues elected (EL 2)
+            if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, 2, false>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, 2, false>(kp, map, n_units, stream);
         case 62:  // default kernel with the 64-bit shift decode (tile_rank) instead of the 32-bit one
             if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, true>(kp, map, n_units, stream);
             return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, true>(kp, map, n_units, stream);
@@ -1466,19 +1476,19 @@ accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, 
     if constexpr (!F16) {
         if (rnd) {  // B not pre-rounded: rho(B) applied in registers
             if (ht) {
-                if (multi) return launch_g4<FW, F16, 1, 2, true, MW, NM, false, K8, 1, 0, 0, false, 0, false, false, true, true>(kp, map, n_units, stream);
-                return launch_g4<FW, F16, 1, 2, true, MW, 1, false, K8, 1, 0, 0, false, 0, false, false, true, true>(kp, map, n_units, stream);
+                if (multi) return launch_g4<FW, F16, 1, 2, true, MW, NM, false, K8, 1, 0, 0, false, 0, false, false, 1, true>(kp, map, n_units, stream);
+                return launch_g4<FW, F16, 1, 2, true, MW, 1, false, K8, 1, 0, 0, false, 0, false, false, 1, true>(kp, map, n_units, stream);
             }
-            if (multi) return launch_g4<FW, F16, 1, 2, true, MW, NM, false, K8, 1, 0, 0, false, 0, false, false, true, false>(kp, map, n_units, stream);
-            return launch_g4<FW, F16, 1, 2, true, MW, 1, false, K8, 1, 0, 0, false, 0, false, false, true, false>(kp, map, n_units, stream);
+            if (multi) return launch_g4<FW, F16, 1, 2, true, MW, NM, false, K8, 1, 0, 0, false, 0, false, false, 1, false>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 2, true, MW, 1, false, K8, 1, 0, 0, false, 0, false, false, 1, false>(kp, map, n_units, stream);
         }
     }
     if (ht) {
-        if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, true, true>(kp, map, n_units, stream);
-        return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, true, true>(kp, map, n_units, stream);
+        if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, 1, true>(kp, map, n_units, stream);
+        return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, true>(kp, map, n_units, stream);
     }
-    if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, true, false>(kp, map, n_units, stream);
-    return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, true, false>(kp, map, n_units, stream);
+    if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, 1, false>(kp, map, n_units, stream);
+    return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, false>(kp, map, n_units, stream);
 }
 
 }  // namespace

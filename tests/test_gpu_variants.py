@@ -5,7 +5,8 @@ library ships one kernel family per width and precision), so the check runs in a
 with ACCSPMM_LIB=variants: every ACCSPMM_KCFG variant (2 warps per CTA, FP16 PRMT fragments,
 k4/k8 swap, values two ahead, 3/4-stage rings, L2::256B value loads, value evict-first, value
 staging by bulk copy, hybrid TMA + cp.async gather, the 3-byte TF32 image of B "B3" and its
-ring/occupancy variants, register-direct gather) computes the same product -- integer data bit-exact with split windows, N = 64 and 256
+ring/occupancy variants, the 64-bit decode, lane-0 / all-lane TMA issue, hot-column plans with
+evict-first blocks at every tag level, register-direct gather) computes the same product -- integer data bit-exact with split windows, N = 64 and 256
 (per-slice maps), floats within tolerance."""
 import json
 import os
