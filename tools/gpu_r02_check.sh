@@ -10,8 +10,8 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 timeout 900 python bench.py --steps 20 --warmup 5 --json-out gpurun_out/bench_$TAG.json > gpurun_out/bench_$TAG.log 2>&1; echo "bench rc=$?"; tail -1 gpurun_out/bench_$TAG.log | cut -c1-400
 if [ "${SANITIZE:-1}" = "1" ]; then
 for tool in memcheck racecheck synccheck initcheck; do
-  timeout 1200 compute-sanitizer --tool $tool --error-exitcode 9 python -m pytest tests/test_gpu_parity.py -q -x -p no:cacheprovider \
-    -k "tiny_config or split_window_hub or padding_lanes or single_bit or empty_windows or concatenated_windows or fused_allgather or integer_bit_exact_and_balance_invariant and 64" \
+  timeout 1500 compute-sanitizer --tool $tool --error-exitcode 9 python -m pytest tests/test_gpu_parity.py tests/test_gpu_hotcols.py -q -x -p no:cacheprovider \
+    -k "tiny_config or split_window_hub or padding_lanes or single_bit or empty_windows or concatenated_windows or fused_allgather or integer_bit_exact_and_balance_invariant and 64 or hot_cols_integer_bit_exact" \
     > gpurun_out/sanitizer_${tool}_$TAG.log 2>&1
   echo "sanitizer $tool rc=$?"; tail -3 gpurun_out/sanitizer_${tool}_$TAG.log
 done
