@@ -1446,6 +1446,9 @@ accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, 
         case 64:  // TMA operands computed by every lane, only the arrive + issues elected (EL 2)
             if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, 2, false>(kp, map, n_units, stream);
             return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, 2, false>(kp, map, n_units, stream);
+        case 65:  // values two blocks ahead (4-slot value ring) on the current default (untagged)
+            if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 2, 0, 0, false, 0, false, false, 1, false>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 2, 0, 0, false, 0, false, false, 1, false>(kp, map, n_units, stream);
         case 62:  // default kernel with the 64-bit shift decode (tile_rank) instead of the 32-bit one
             if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, true>(kp, map, n_units, stream);
             return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, true>(kp, map, n_units, stream);
