@@ -613,7 +613,7 @@ inline int map_count(const KParams &kp) { return kp.nslices > 1 && kp.nslices <=
 
 template <int FW, bool F16, int WARPS, int STAGES, bool RND, int MINB = 1, int NM = 1, bool LDSM_ = false,
           bool K8 = false, int VD = 1, int PF256 = 0, int VST = 0, bool HYB = false, int CX = (VST ? 4 : 0),
-          bool B3 = false, bool DEC64 = false, int EL = 1, bool HT = true>
+          bool B3 = false, bool DEC64 = false, int EL = 1, bool HT = true, bool PIN = false>
 __global__ void __launch_bounds__(WARPS * 32, MINB)
     spmm_bittcf_g4_kernel(const KParams p, const __grid_constant__ G4MapsT<NM> maps)
 {
@@ -684,7 +684,15 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     constexpr uint32_t DK = F16 ? 1u : 4u;
     const uint32_t hw = (uint32_t)k0 >> 5, p0w = (uint32_t)k0 & 31u;
     const uint32_t below = (1u << p0w) - 1u;
-    const uint32_t m_lo = hw ? 0xFFFFFFFFu : below, m_hi = hw ? below : 0u;
+    uint32_t m_lo = hw ? 0xFFFFFFFFu : below, m_hi = hw ? below : 0u;
+    // PIN: keep the lane constants and the value base in registers (an empty asm hides their
+    // derivation, so the compiler cannot rematerialise them inside the block loop)
+    const char *vals_base = reinterpret_cast<const char *>(p.vals);
+    uint32_t frag_off = (uint32_t)(t * GC::RS + CF::VB * g);  // this lane's fragment offset in a stage
+    if constexpr (PIN) {
+        asm volatile("" : "+r"(m_lo), "+r"(m_hi), "+r"(frag_off));
+        asm volatile("" : "+l"(vals_base));
+    }
 
     auto issue_chunk = [&](uint32_t i) {
         if (i < nblk) {
@@ -792,12 +800,12 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
                 vb1[slot] = p1 ? (uint32_t)(vlo != 0xFFFFFFFFu ? vs[i1 - vlo] : __ldg(vp + i1)) : 0u;
             }
         } else if constexpr (!F16) {
-            const float *vp = reinterpret_cast<const float *>(p.vals);
+            const float *vp = reinterpret_cast<const float *>(vals_base);
             vb0[slot] = p0 ? __float_as_uint(__ldg(vp + i0)) : 0u;
             vb1[slot] = p1 ? __float_as_uint(__ldg(vp + i1)) : 0u;
         } else {
             // keep the two halves apart until the MMA: packing here would stall on the loads
-            const unsigned short *vp = reinterpret_cast<const unsigned short *>(p.vals);
+            const unsigned short *vp = reinterpret_cast<const unsigned short *>(vals_base);
             vb0[slot] = p0 ? (uint32_t)__ldg(vp + i0) : 0u;
             vb1[slot] = p1 ? (uint32_t)__ldg(vp + i1) : 0u;
         }
@@ -885,8 +893,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     auto consume = [&](uint32_t i, int s, int slot) {
         mbar_wait(smem_u32(&sm.bar[s]), (i / STAGES) & 1u);
         const uint8_t *st = sm.stage[s];
-        const uint8_t *ra = st + t * GC::RS + CF::VB * g;
-        const uint8_t *rb = st + GC::GRP + t * GC::RS + CF::VB * g;
+        const uint8_t *ra = st + frag_off;
+        const uint8_t *rb = st + GC::GRP + frag_off;
         if constexpr (B3) {
             // rows t (k = t, gather x) and t + 4 (gather y); per 8-feature group j: LDS.128 of the
             // high halves + LDS.64 of the bytes 15..8; one PRMT per element rebuilds the TF32
@@ -1256,12 +1264,12 @@ accspmm_status launch_cfg(const KParams &kp, int64_t n_units, cudaStream_t strea
 // one map per slice (tensor_map decides; only the default configurations instantiate it)
 template <int FW, bool F16, int WARPS, int STAGES, bool RND = false, int MINB = 1, int NM = 1, bool LDSM = false,
           bool K8 = false, int VD = 1, int PF256 = 0, int VST = 0, bool HYB = false, int CX = (VST ? 4 : 0),
-          bool B3 = false, bool DEC64 = false, int EL = 1, bool HT = true>
+          bool B3 = false, bool DEC64 = false, int EL = 1, bool HT = true, bool PIN = false>
 accspmm_status launch_g4(const KParams &kp, const G4Maps *map, int64_t n_units, cudaStream_t stream)
 {
     using SM = G4WarpSmem<FW, F16, STAGES, VST, CX, B3>;
     const size_t smem = sizeof(SM) * WARPS;
-    auto kern = spmm_bittcf_g4_kernel<FW, F16, WARPS, STAGES, RND, MINB, NM, LDSM, K8, VD, PF256, VST, HYB, CX, B3, DEC64, EL, HT>;
+    auto kern = spmm_bittcf_g4_kernel<FW, F16, WARPS, STAGES, RND, MINB, NM, LDSM, K8, VD, PF256, VST, HYB, CX, B3, DEC64, EL, HT, PIN>;
     static int configured_device = -1;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -1446,6 +1454,9 @@ accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, 
         case 64:  // TMA operands computed by every lane, only the arrive + issues elected (EL 2)
             if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, 2, false>(kp, map, n_units, stream);
             return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, 2, false>(kp, map, n_units, stream);
+        case 66:  // lane constants and the value base pinned in registers (no rematerialisation)
+            if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, true>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, true>(kp, map, n_units, stream);
         case 65:  // values two blocks ahead (4-slot value ring) on the current default (untagged)
             if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 2, 0, 0, false, 0, false, false, 1, false>(kp, map, n_units, stream);
             return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 2, 0, 0, false, 0, false, false, 1, false>(kp, map, n_units, stream);
