@@ -250,25 +250,35 @@ def make_inputs(args):
     return cfg, A, vals, B
 
 
+def host_threads() -> int:
+    """Every host core this process may run on.  torchrun exports OMP_NUM_THREADS=1 to its
+    workers, so the oracle's OpenMP default would time one thread under --gpus N > 1."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except (AttributeError, OSError):
+        return os.cpu_count() or 1
+
+
 def cpu_oracle_sample(A, vals, B, precision, seconds, seed=0, rounded=None):
     """The FP64 oracle as it stands, on the host cores, over a bounded random row sample
     (rho(A), rho(B) are computed once, outside the timed sample)."""
     from oracle import spmm as osp
+    nt = host_threads()
     from oracle.rounding import rho
     a, b = rounded if rounded is not None else (rho(vals, precision), rho(B, precision))
     rng = np.random.default_rng(seed)
     nnz_row = np.diff(A.rowptr)
     N = B.shape[1]
     rows = np.sort(rng.choice(A.M, size=min(A.M, 256), replace=False))
-    _, t = osp.timed_spmm(A.M, A.K, A.rowptr, A.colidx, a, b, rows=rows)
+    _, t = osp.timed_spmm(A.M, A.K, A.rowptr, A.colidx, a, b, rows=rows, nthreads=nt)
     rate = 2.0 * nnz_row[rows].sum() * N / max(t, 1e-9)
     target_flops = rate * seconds
     avg = 2.0 * nnz_row.mean() * N
     n = int(min(A.M, max(256, target_flops / max(avg, 1.0))))
     rows = np.sort(rng.choice(A.M, size=n, replace=False))
-    _, t = osp.timed_spmm(A.M, A.K, A.rowptr, A.colidx, a, b, rows=rows)
+    _, t = osp.timed_spmm(A.M, A.K, A.rowptr, A.colidx, a, b, rows=rows, nthreads=nt)
     flops = 2.0 * nnz_row[rows].sum() * N
-    return {"value": flops / t / 1e9, "unit": "GFLOP/s", "cores": osp.num_threads(), "kind": "oracle",
+    return {"value": flops / t / 1e9, "unit": "GFLOP/s", "cores": osp.num_threads(nt), "kind": "oracle",
             "sample": f"{n} of {A.M} rows (random, seed {seed}), {int(nnz_row[rows].sum())} nnz, N={N}, "
                       f"FP64 CSR triple loop, {t:.2f} s"}, t
 
