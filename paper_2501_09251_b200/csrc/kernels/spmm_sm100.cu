@@ -1454,6 +1454,12 @@ accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, 
         case 64:  // TMA operands computed by every lane, only the arrive + issues elected (EL 2)
             if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, 2, false>(kp, map, n_units, stream);
             return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, 2, false>(kp, map, n_units, stream);
+        case 68:  // 4 more resident warps per SM than the tuned launch bound (register cap lower)
+            if (multi) return launch_g4<FW, F16, 1, 2, false, MW + 4, NM, LD, K8, 1, 0, 0, false, 0, false, false, 1, false>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 2, false, MW + 4, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, false>(kp, map, n_units, stream);
+        case 69:  // 4 fewer resident warps per SM than the tuned launch bound
+            if (multi) return launch_g4<FW, F16, 1, 2, false, MW - 4, NM, LD, K8, 1, 0, 0, false, 0, false, false, 1, false>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 2, false, MW - 4, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, false>(kp, map, n_units, stream);
         case 66:  // lane constants and the value base pinned in registers (no rematerialisation)
             if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, true>(kp, map, n_units, stream);
             return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, true>(kp, map, n_units, stream);
