@@ -613,7 +613,7 @@ inline int map_count(const KParams &kp) { return kp.nslices > 1 && kp.nslices <=
 
 template <int FW, bool F16, int WARPS, int STAGES, bool RND, int MINB = 1, int NM = 1, bool LDSM_ = false,
           bool K8 = false, int VD = 1, int PF256 = 0, int VST = 0, bool HYB = false, int CX = (VST ? 4 : 0),
-          bool B3 = false, bool DEC64 = false, int EL = 1, bool HT = true, bool PIN = false>
+          bool B3 = false, bool DEC64 = false, int EL = 1, bool HT = true, bool PIN = false, bool DYN = false>
 __global__ void __launch_bounds__(WARPS * 32, MINB)
     spmm_bittcf_g4_kernel(const KParams p, const __grid_constant__ G4MapsT<NM> maps)
 {
@@ -715,8 +715,16 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     // VR-slot register ring).  A bulk L2 prefetch of each chunk's value range and staging
     // values through shared memory were measured and lost.
     static_assert(VD == 1 || VD == 2, "value distance");
-    constexpr int VR = VD == 1 ? 2 : 4;
+    // DYN (deep ring, STAGES > 2): values are loaded with the TMA of their block, STAGES - 1
+    // blocks ahead, so up to STAGES value slots are live
+    static_assert(!DYN || (STAGES > 2 && STAGES <= 4 && VST == 0 && !HYB), "deep ring: 3 or 4 stages");
+    constexpr int VR = DYN ? 4 : VD == 1 ? 2 : 4;
     uint32_t vb0[VR], vb1[VR];
+    // PF256 == 3 (measurement variant): the block's value run is loaded by one coalesced warp
+    // load (lane L: value tco + L, and tco + 32 + L when the block holds more than 32); the
+    // lane's two entries are picked by shuffles at consume time.  vix = packed local indices
+    // (bits 0-5, 6-11), presence (12, 13) and "more than 32 values" (14).
+    uint32_t vix[PF256 == 3 ? VR : 1];
 
     // ---- lane 0 (VST): bulk copy of chunk c's value range (16-byte-aligned superset; the
     // value allocation carries 16 elements of padding) into value buffer c & 1
@@ -763,7 +771,21 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
             i0 = t0 + (uint32_t)__popc(lo & m_lo) + (uint32_t)__popc(hi & m_hi);
             i1 = i0 + (uint32_t)__popc(r & ((1u << DK) - 1u));
         }
-        if constexpr (PF256 == 2) {  // values with an L2 evict-first policy (measurement variant)
+        if constexpr (PF256 == 3) {
+            const uint32_t lo = (uint32_t)mask, hi = (uint32_t)(mask >> 32);
+            const uint32_t nv = (uint32_t)__popc(lo) + (uint32_t)__popc(hi);
+            const uint32_t l0 = i0 - t0, l1 = i1 - t0;
+            vix[slot] = l0 | (l1 << 6) | ((uint32_t)p0 << 12) | ((uint32_t)p1 << 13) | ((uint32_t)(nv > 32u) << 14);
+            if constexpr (!F16) {
+                const float *vp = reinterpret_cast<const float *>(vals_base) + t0;
+                vb0[slot] = (uint32_t)lane < nv ? __float_as_uint(__ldg(vp + lane)) : 0u;
+                vb1[slot] = nv > 32u && (uint32_t)lane + 32u < nv ? __float_as_uint(__ldg(vp + 32 + lane)) : 0u;
+            } else {
+                const unsigned short *vp = reinterpret_cast<const unsigned short *>(vals_base) + t0;
+                vb0[slot] = (uint32_t)lane < nv ? (uint32_t)__ldg(vp + lane) : 0u;
+                vb1[slot] = nv > 32u && (uint32_t)lane + 32u < nv ? (uint32_t)__ldg(vp + 32 + lane) : 0u;
+            }
+        } else if constexpr (PF256 == 2) {  // values with an L2 evict-first policy (measurement variant)
             if constexpr (!F16) {
                 const uint32_t *vp = reinterpret_cast<const uint32_t *>(p.vals);
                 uint32_t x0 = 0u, x1 = 0u;
@@ -892,6 +914,19 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     // ---- consumer: wait for stage s, load the gathered-row fragments, tensor-core MMA
     auto consume = [&](uint32_t i, int s, int slot) {
         mbar_wait(smem_u32(&sm.bar[s]), (i / STAGES) & 1u);
+        if constexpr (PF256 == 3) {  // pick this lane's two values out of the warp's value run
+            const uint32_t ix = vix[slot], l0 = ix & 63u, l1 = (ix >> 6) & 63u;
+            uint32_t a0 = __shfl_sync(0xffffffffu, vb0[slot], (int)(l0 & 31u));
+            uint32_t a1 = __shfl_sync(0xffffffffu, vb0[slot], (int)(l1 & 31u));
+            if (ix & (1u << 14)) {  // warp-uniform: the block holds more than 32 values
+                const uint32_t c0 = __shfl_sync(0xffffffffu, vb1[slot], (int)(l0 & 31u));
+                const uint32_t c1 = __shfl_sync(0xffffffffu, vb1[slot], (int)(l1 & 31u));
+                a0 = l0 >= 32u ? c0 : a0;
+                a1 = l1 >= 32u ? c1 : a1;
+            }
+            vb0[slot] = (ix & (1u << 12)) ? a0 : 0u;
+            vb1[slot] = (ix & (1u << 13)) ? a1 : 0u;
+        }
         const uint8_t *st = sm.stage[s];
         const uint8_t *ra = st + frag_off;
         const uint8_t *rb = st + GC::GRP + frag_off;
@@ -1069,9 +1104,51 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     }
     after_block(b0);
     if (nblk > 0) value_load(0u, 0);
-    if (VD == 2 && nblk > 1) value_load(1u, 1);
+    if (!DYN && VD == 2 && nblk > 1) value_load(1u, 1);
     if (nblk > 0) issue_tma(0, 0);
-    if constexpr (STAGES > 2) {
+    if constexpr (DYN) {
+        // Deep ring with a run-time stage index (measurement variant): block step j issues the
+        // TMA and loads the values of jt = j + L (L = STAGES - 1), then consumes block j.  The
+        // unroll is the 4-slot value ring only (the stage rotates at run time), so the loop
+        // body stays as small as the default one.  Chunk c + 1 is staged once jt has entered
+        // chunk c: every reader of chunk c - 1's buffer (TMA issue, value decode of blocks
+        // < c * CH) has then run.
+        constexpr int L = STAGES - 1;
+#pragma unroll
+        for (int d = 1; d < L; ++d)
+            if ((uint32_t)d < nblk) {
+                issue_tma((uint32_t)d, d);
+                value_load((uint32_t)d, d);
+            }
+        int s_c = 0, s_t = L;
+        auto stepD = [&](uint32_t j, int u, bool checked) {
+            const uint32_t jt = j + L;
+            if ((jt & (CH - 1u)) == 0) {
+                cp_async_wait_all();
+                __syncwarp();
+                issue_chunk(jt + CH);
+            }
+            if (!checked || jt < nblk) {
+                issue_tma(jt, s_t);
+                value_load(jt, (u + L) & (VR - 1));
+            }
+            consume(j, s_c, u & (VR - 1));
+            after_block(b0 + j + 1);
+            s_c = s_c == STAGES - 1 ? 0 : s_c + 1;
+            s_t = s_t == STAGES - 1 ? 0 : s_t + 1;
+        };
+        const uint32_t nmainD = nblk >= (uint32_t)L ? ((nblk - L) / VR) * VR : 0u;
+        uint32_t j = 0;
+        for (; j < nmainD; j += VR) {
+#pragma unroll
+            for (int u = 0; u < VR; ++u) stepD(j + (uint32_t)u, u, false);
+        }
+        for (; j < nblk; j += VR) {
+#pragma unroll
+            for (int u = 0; u < VR; ++u)
+                if (j + (uint32_t)u < nblk) stepD(j + (uint32_t)u, u, true);
+        }
+    } else if constexpr (STAGES > 2) {
         // Deeper TMA ring (STAGES - 1 blocks of lookahead; pays where a stage is small, e.g.
         // FP16): block step j issues the TMA of jt = j + L and the values of jn = j + 1.
         // Chunk c + 1 is staged when jn enters chunk c (chunk c - 1's buffer is then free)
@@ -1264,12 +1341,12 @@ accspmm_status launch_cfg(const KParams &kp, int64_t n_units, cudaStream_t strea
 // one map per slice (tensor_map decides; only the default configurations instantiate it)
 template <int FW, bool F16, int WARPS, int STAGES, bool RND = false, int MINB = 1, int NM = 1, bool LDSM = false,
           bool K8 = false, int VD = 1, int PF256 = 0, int VST = 0, bool HYB = false, int CX = (VST ? 4 : 0),
-          bool B3 = false, bool DEC64 = false, int EL = 1, bool HT = true, bool PIN = false>
+          bool B3 = false, bool DEC64 = false, int EL = 1, bool HT = true, bool PIN = false, bool DYN = false>
 accspmm_status launch_g4(const KParams &kp, const G4Maps *map, int64_t n_units, cudaStream_t stream)
 {
     using SM = G4WarpSmem<FW, F16, STAGES, VST, CX, B3>;
     const size_t smem = sizeof(SM) * WARPS;
-    auto kern = spmm_bittcf_g4_kernel<FW, F16, WARPS, STAGES, RND, MINB, NM, LDSM, K8, VD, PF256, VST, HYB, CX, B3, DEC64, EL, HT, PIN>;
+    auto kern = spmm_bittcf_g4_kernel<FW, F16, WARPS, STAGES, RND, MINB, NM, LDSM, K8, VD, PF256, VST, HYB, CX, B3, DEC64, EL, HT, PIN, DYN>;
     static int configured_device = -1;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -1466,6 +1543,21 @@ accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, 
         case 65:  // values two blocks ahead (4-slot value ring) on the current default (untagged)
             if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 2, 0, 0, false, 0, false, false, 1, false>(kp, map, n_units, stream);
             return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 2, 0, 0, false, 0, false, false, 1, false>(kp, map, n_units, stream);
+        case 70:  // deep ring: 3 stages, TMA and values 2 blocks ahead, run-time stage index
+            if (multi) return launch_g4<FW, F16, 1, 3, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, true>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 3, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, true>(kp, map, n_units, stream);
+        case 71:  // deep ring: 4 stages, TMA and values 3 blocks ahead, run-time stage index
+            if (multi) return launch_g4<FW, F16, 1, 4, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, true>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 4, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, true>(kp, map, n_units, stream);
+        case 72:  // deep ring: 3 stages at 4 fewer resident warps (TF32 FW 128: smem for the 3rd stage)
+            if (multi) return launch_g4<FW, F16, 1, 3, false, MW - 4, NM, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, true>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 3, false, MW - 4, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, true>(kp, map, n_units, stream);
+        case 73:  // values by one coalesced warp load per block + shuffles (PF256 3)
+            if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 3, 0, false, 0, false, false, 1, false>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 3, 0, false, 0, false, false, 1, false>(kp, map, n_units, stream);
+        case 74:  // deep ring (3 stages) + coalesced values
+            if (multi) return launch_g4<FW, F16, 1, 3, false, MW, NM, LD, K8, 1, 3, 0, false, 0, false, false, 1, false, false, true>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 3, false, MW, 1, LD, K8, 1, 3, 0, false, 0, false, false, 1, false, false, true>(kp, map, n_units, stream);
         case 62:  // default kernel with the 64-bit shift decode (tile_rank) instead of the 32-bit one
             if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, true>(kp, map, n_units, stream);
             return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, true>(kp, map, n_units, stream);

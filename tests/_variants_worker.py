@@ -16,18 +16,19 @@ import gen  # noqa: E402
 import paper_2501_09251_b200 as acc  # noqa: E402
 from gpu_util import assert_bit_exact, assert_within, run  # noqa: E402
 
-KCFGS = ["20", "46", "47", "48", "49", "50", "51", "52", "53", "54", "55", "56", "57", "58", "59", "60", "61", "62", "63", "64", "65", "66", "68", "69", "10", "11", "12",
+KCFGS = ["20", "46", "47", "48", "49", "50", "51", "52", "53", "54", "55", "56", "57", "58", "59", "60", "61", "62", "63", "64", "65", "66", "68", "69", "70", "71", "72", "73", "74", "10", "11", "12",
          "b3", "hot"]
 
 
 def main():
+    kcfgs = sys.argv[1:] or KCFGS   # a subset on the command line (A/B scripts check new variants first)
     assert acc.LIB_PATH.endswith("libaccspmm_variants.so"), acc.LIB_PATH
     A = gen.dcsbm(3000, 150_000, 5, 2.2, 0.2, 2000, seed=3, oversample=1.3)
     v = gen.values_int(A.nnz, 1)
     vf = gen.values_uniform(A.nnz, 4)
     Bf = gen.dense_normal(A.K, 128, 5)
     for precision in ("tf32", "fp16"):
-        for kcfg in KCFGS:
+        for kcfg in kcfgs:
             # "b3": the default kernel reading the 3-byte TF32 image of B (ACCSPMM_B3=1); 58-61
             # are B3 variants (the knob is on for them, off for the others)
             # "hot": hot-column plans (R22) with every tag level exercised: a 1 MiB hot set and
