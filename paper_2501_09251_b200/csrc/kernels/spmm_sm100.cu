@@ -542,6 +542,34 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase)
         : "memory");
 }
 
+// WT = 0: try_wait with a suspend-time hint (the default); 1: try_wait without a hint;
+// 2: test_wait spin (never suspends) -- measurement variants of the stage wait
+template <int WT>
+__device__ __forceinline__ void mbar_wait_t(uint32_t bar, uint32_t phase)
+{
+    if constexpr (WT == 0) {
+        mbar_wait(bar, phase);
+    } else if constexpr (WT == 1) {
+        asm volatile(
+            "{\n\t.reg .pred P1;\n\t"
+            "WAIT_%=:\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+            "@P1 bra DONE_%=;\n\t"
+            "bra WAIT_%=;\n\t"
+            "DONE_%=:\n\t}\n" ::"r"(bar), "r"(phase)
+            : "memory");
+    } else {
+        asm volatile(
+            "{\n\t.reg .pred P1;\n\t"
+            "WAIT_%=:\n\t"
+            "mbarrier.test_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+            "@P1 bra DONE_%=;\n\t"
+            "bra WAIT_%=;\n\t"
+            "DONE_%=:\n\t}\n" ::"r"(bar), "r"(phase)
+            : "memory");
+    }
+}
+
 // ================================================================== v4: TMA gather4
 //
 // v3 issues 9 bulk copies per TC block and becomes TMA-request bound (~10 SM
@@ -576,11 +604,13 @@ struct G4Cfg {
 // the chunk metadata; a layout that put them at 8 mod 16 behind other fields ran the default
 // kernel 2.2x slower (5.55 vs 2.54 ms on the Reddit-shaped bench) with identical SASS apart
 // from the shared-memory offsets.
-template <int FW, bool F16, int STAGES, int VST = 0, int CX = (VST ? 4 : 0), bool B3 = false>
+// BS = barrier stride in 8-byte words (1: packed; 2: one 16-byte slot per stage barrier;
+// 16: one 128-byte line each -- measurement variants)
+template <int FW, bool F16, int STAGES, int VST = 0, int CX = (VST ? 4 : 0), bool B3 = false, int BS = 1>
 struct G4WarpSmem {
     alignas(128) uint8_t stage[STAGES][G4Cfg<FW, F16, B3>::STAGE_AL];
     ChunkSmemT<CX> ch[VST ? 3 : 2];
-    alignas(16) uint64_t bar[STAGES];
+    alignas(BS >= 16 ? 128 : 16) uint64_t bar[STAGES * BS];
     uint64_t vbar[2];
     uint32_t vlo[2];  // first staged value index per buffer (0xFFFFFFFF: over VST, values from L2)
     alignas(16) uint8_t vals[VST ? 2 : 1][VST ? VST * (F16 ? 2 : 4) : 16];
@@ -613,7 +643,8 @@ inline int map_count(const KParams &kp) { return kp.nslices > 1 && kp.nslices <=
 
 template <int FW, bool F16, int WARPS, int STAGES, bool RND, int MINB = 1, int NM = 1, bool LDSM_ = false,
           bool K8 = false, int VD = 1, int PF256 = 0, int VST = 0, bool HYB = false, int CX = (VST ? 4 : 0),
-          bool B3 = false, bool DEC64 = false, int EL = 1, bool HT = true, bool PIN = false, bool DYN = false>
+          bool B3 = false, bool DEC64 = false, int EL = 1, bool HT = true, bool PIN = false, bool DYN = false,
+          int BS = 1, int WT = 0>
 __global__ void __launch_bounds__(WARPS * 32, MINB)
     spmm_bittcf_g4_kernel(const KParams p, const __grid_constant__ G4MapsT<NM> maps)
 {
@@ -630,7 +661,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     constexpr int CH = kChunk;  // blocks per staged chunk
     using CF = Cfg<FW, F16>;
     using GC = G4Cfg<FW, F16, B3>;
-    using SM = G4WarpSmem<FW, F16, STAGES, VST, CX, B3>;
+    using SM = G4WarpSmem<FW, F16, STAGES, VST, CX, B3, BS>;
     static_assert(!B3 || (!RND && !HYB && VST == 0 && !LDSM_), "B3: pre-rounded B, default ring");
     static_assert(VST == 0 || CX >= 1, "value staging reads the TCOffset after the chunk");
     static_assert(offsetof(SM, bar) % 16 == 0, "stage mbarriers 16-byte aligned (measured: 2.2x slower otherwise)");
@@ -657,7 +688,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
         asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&maps.m[NM > 1 ? slice : 0]))
                      : "memory");
 #pragma unroll
-        for (int s = 0; s < STAGES; ++s) mbar_init(smem_u32(&sm.bar[s]), (HYB && s == 1) ? 32 : 1);
+        for (int s = 0; s < STAGES; ++s) mbar_init(smem_u32(&sm.bar[s * BS]), (HYB && s == 1) ? 32 : 1);
         if constexpr (VST > 0) {
             mbar_init(smem_u32(&sm.vbar[0]), 1);
             mbar_init(smem_u32(&sm.vbar[1]), 1);
@@ -860,7 +891,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
                              : "memory");
             }
         }
-        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&sm.bar[s])) : "memory");
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&sm.bar[s * BS])) : "memory");
     };
     auto issue_tma = [&](uint32_t j, int s) {
         if constexpr (HYB) {
@@ -885,7 +916,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
             const uint32_t x0 = HT ? ca.x & p.id_mask : ca.x;
             const int32_t r0 = (int32_t)x0, r1 = (int32_t)ca.y, r2 = (int32_t)ca.z, r3 = (int32_t)ca.w;
             const int32_t r4 = (int32_t)cb.x, r5 = (int32_t)cb.y, r6 = (int32_t)cb.z, r7 = (int32_t)cb.w;
-            const uint32_t bar = smem_u32(&sm.bar[s]);
+            const uint32_t bar = smem_u32(&sm.bar[s * BS]);
             const uint32_t st = smem_u32(sm.stage[s]);
             // no proxy fence: the stage's previous generic reads fed this warp's mma.sync,
             // which cannot issue before every lane's LDS has returned
@@ -913,7 +944,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
 
     // ---- consumer: wait for stage s, load the gathered-row fragments, tensor-core MMA
     auto consume = [&](uint32_t i, int s, int slot) {
-        mbar_wait(smem_u32(&sm.bar[s]), (i / STAGES) & 1u);
+        mbar_wait_t<WT>(smem_u32(&sm.bar[s * BS]), (i / STAGES) & 1u);
         if constexpr (PF256 == 3) {  // pick this lane's two values out of the warp's value run
             const uint32_t ix = vix[slot], l0 = ix & 63u, l1 = (ix >> 6) & 63u;
             uint32_t a0 = __shfl_sync(0xffffffffu, vb0[slot], (int)(l0 & 31u));
@@ -1341,12 +1372,13 @@ accspmm_status launch_cfg(const KParams &kp, int64_t n_units, cudaStream_t strea
 // one map per slice (tensor_map decides; only the default configurations instantiate it)
 template <int FW, bool F16, int WARPS, int STAGES, bool RND = false, int MINB = 1, int NM = 1, bool LDSM = false,
           bool K8 = false, int VD = 1, int PF256 = 0, int VST = 0, bool HYB = false, int CX = (VST ? 4 : 0),
-          bool B3 = false, bool DEC64 = false, int EL = 1, bool HT = true, bool PIN = false, bool DYN = false>
+          bool B3 = false, bool DEC64 = false, int EL = 1, bool HT = true, bool PIN = false, bool DYN = false,
+          int BS = 1, int WT = 0>
 accspmm_status launch_g4(const KParams &kp, const G4Maps *map, int64_t n_units, cudaStream_t stream)
 {
-    using SM = G4WarpSmem<FW, F16, STAGES, VST, CX, B3>;
+    using SM = G4WarpSmem<FW, F16, STAGES, VST, CX, B3, BS>;
     const size_t smem = sizeof(SM) * WARPS;
-    auto kern = spmm_bittcf_g4_kernel<FW, F16, WARPS, STAGES, RND, MINB, NM, LDSM, K8, VD, PF256, VST, HYB, CX, B3, DEC64, EL, HT, PIN, DYN>;
+    auto kern = spmm_bittcf_g4_kernel<FW, F16, WARPS, STAGES, RND, MINB, NM, LDSM, K8, VD, PF256, VST, HYB, CX, B3, DEC64, EL, HT, PIN, DYN, BS, WT>;
     static int configured_device = -1;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -1558,6 +1590,36 @@ accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, 
         case 74:  // deep ring (3 stages) + coalesced values
             if (multi) return launch_g4<FW, F16, 1, 3, false, MW, NM, LD, K8, 1, 3, 0, false, 0, false, false, 1, false, false, true>(kp, map, n_units, stream);
             return launch_g4<FW, F16, 1, 3, false, MW, 1, LD, K8, 1, 3, 0, false, 0, false, false, 1, false, false, true>(kp, map, n_units, stream);
+        case 75:  // deep ring (3 stages), one 16-byte slot per stage barrier
+            if (multi) return launch_g4<FW, F16, 1, 3, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, true, 2>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 3, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, true, 2>(kp, map, n_units, stream);
+        case 76:  // deep ring (3 stages), one 128-byte line per stage barrier
+            if (multi) return launch_g4<FW, F16, 1, 3, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, true, 16>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 3, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, true, 16>(kp, map, n_units, stream);
+        case 77:  // default kernel, one 16-byte slot per stage barrier
+            if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, false, 2>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, false, 2>(kp, map, n_units, stream);
+        case 78:  // default kernel, one 128-byte line per stage barrier
+            if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, false, 16>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, false, 16>(kp, map, n_units, stream);
+        case 79:  // default kernel, stage wait by try_wait without a suspend hint
+            if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, false, 1, 1>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, false, 1, 1>(kp, map, n_units, stream);
+        case 80:  // default kernel, stage wait by test_wait spin
+            if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, false, 1, 2>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, false, 1, 2>(kp, map, n_units, stream);
+        case 81:  // default + 16-byte barrier slots (77), try_wait without hint
+            if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, false, 2, 1>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, false, 2, 1>(kp, map, n_units, stream);
+        case 82:  // default + 16-byte barrier slots (77), test_wait spin
+            if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, false, 2, 2>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, false, 2, 2>(kp, map, n_units, stream);
+        case 83:  // deep ring (70), try_wait without hint
+            if (multi) return launch_g4<FW, F16, 1, 3, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, true, 1, 1>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 3, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, true, 1, 1>(kp, map, n_units, stream);
+        case 84:  // deep ring (70), test_wait spin
+            if (multi) return launch_g4<FW, F16, 1, 3, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, true, 1, 2>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 3, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, true, 1, 2>(kp, map, n_units, stream);
         case 62:  // default kernel with the 64-bit shift decode (tile_rank) instead of the 32-bit one
             if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, true>(kp, map, n_units, stream);
             return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, true>(kp, map, n_units, stream);
