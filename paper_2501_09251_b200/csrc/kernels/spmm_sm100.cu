@@ -37,6 +37,7 @@
 #include <cstddef>
 #include <cstdint>
 #include <cstdlib>
+#include <type_traits>
 
 #include "../internal.hpp"
 
@@ -615,6 +616,19 @@ struct G4WarpSmem {
     uint32_t vlo[2];  // first staged value index per buffer (0xFFFFFFFF: over VST, values from L2)
     alignas(16) uint8_t vals[VST ? 2 : 1][VST ? VST * (F16 ? 2 : 4) : 16];
 };
+// the same fields with the stage barriers at the head of the warp's area (BS = 0 in the kernel)
+template <int FW, bool F16, int STAGES, int VST = 0, int CX = (VST ? 4 : 0), bool B3 = false>
+struct G4WarpSmemHead {
+    alignas(128) uint64_t bar[STAGES];
+    uint64_t vbar[2];
+    uint32_t vlo[2];
+    alignas(128) uint8_t stage[STAGES][G4Cfg<FW, F16, B3>::STAGE_AL];
+    ChunkSmemT<CX> ch[VST ? 3 : 2];
+    alignas(16) uint8_t vals[VST ? 2 : 1][VST ? VST * (F16 ? 2 : 4) : 16];
+};
+template <int FW, bool F16, int STAGES, int VST, int CX, bool B3, int BS>
+using G4Smem = std::conditional_t<BS == 0, G4WarpSmemHead<FW, F16, STAGES, VST, CX, B3>,
+                                  G4WarpSmem<FW, F16, STAGES, VST, CX, B3, BS>>;
 static_assert(sizeof(ChunkSmemT<0>) % 16 == 0 && sizeof(ChunkSmemT<4>) % 16 == 0,
               "chunk alignment (cp.async 16 B into a2b)");
 
@@ -661,10 +675,11 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     constexpr int CH = kChunk;  // blocks per staged chunk
     using CF = Cfg<FW, F16>;
     using GC = G4Cfg<FW, F16, B3>;
-    using SM = G4WarpSmem<FW, F16, STAGES, VST, CX, B3, BS>;
+    using SM = G4Smem<FW, F16, STAGES, VST, CX, B3, BS>;
     static_assert(!B3 || (!RND && !HYB && VST == 0 && !LDSM_), "B3: pre-rounded B, default ring");
     static_assert(VST == 0 || CX >= 1, "value staging reads the TCOffset after the chunk");
     static_assert(offsetof(SM, bar) % 16 == 0, "stage mbarriers 16-byte aligned (measured: 2.2x slower otherwise)");
+    constexpr int BSTR = BS == 0 ? 1 : BS;  // barrier stride (BS = 0: packed, at the head)
     using V = typename CF::V;
     constexpr int MT = CF::MT;
     // epilogue geometry: lane g owns NV vectors of VW features, vector j = features VW*(8j+g)..
@@ -688,7 +703,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
         asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&maps.m[NM > 1 ? slice : 0]))
                      : "memory");
 #pragma unroll
-        for (int s = 0; s < STAGES; ++s) mbar_init(smem_u32(&sm.bar[s * BS]), (HYB && s == 1) ? 32 : 1);
+        for (int s = 0; s < STAGES; ++s) mbar_init(smem_u32(&sm.bar[s * BSTR]), (HYB && s == 1) ? 32 : 1);
         if constexpr (VST > 0) {
             mbar_init(smem_u32(&sm.vbar[0]), 1);
             mbar_init(smem_u32(&sm.vbar[1]), 1);
@@ -891,7 +906,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
                              : "memory");
             }
         }
-        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&sm.bar[s * BS])) : "memory");
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&sm.bar[s * BSTR])) : "memory");
     };
     auto issue_tma = [&](uint32_t j, int s) {
         if constexpr (HYB) {
@@ -916,7 +931,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
             const uint32_t x0 = HT ? ca.x & p.id_mask : ca.x;
             const int32_t r0 = (int32_t)x0, r1 = (int32_t)ca.y, r2 = (int32_t)ca.z, r3 = (int32_t)ca.w;
             const int32_t r4 = (int32_t)cb.x, r5 = (int32_t)cb.y, r6 = (int32_t)cb.z, r7 = (int32_t)cb.w;
-            const uint32_t bar = smem_u32(&sm.bar[s * BS]);
+            const uint32_t bar = smem_u32(&sm.bar[s * BSTR]);
             const uint32_t st = smem_u32(sm.stage[s]);
             // no proxy fence: the stage's previous generic reads fed this warp's mma.sync,
             // which cannot issue before every lane's LDS has returned
@@ -944,7 +959,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
 
     // ---- consumer: wait for stage s, load the gathered-row fragments, tensor-core MMA
     auto consume = [&](uint32_t i, int s, int slot) {
-        mbar_wait_t<WT>(smem_u32(&sm.bar[s * BS]), (i / STAGES) & 1u);
+        mbar_wait_t<WT>(smem_u32(&sm.bar[s * BSTR]), (i / STAGES) & 1u);
         if constexpr (PF256 == 3) {  // pick this lane's two values out of the warp's value run
             const uint32_t ix = vix[slot], l0 = ix & 63u, l1 = (ix >> 6) & 63u;
             uint32_t a0 = __shfl_sync(0xffffffffu, vb0[slot], (int)(l0 & 31u));
@@ -1376,7 +1391,7 @@ template <int FW, bool F16, int WARPS, int STAGES, bool RND = false, int MINB = 
           int BS = 1, int WT = 0>
 accspmm_status launch_g4(const KParams &kp, const G4Maps *map, int64_t n_units, cudaStream_t stream)
 {
-    using SM = G4WarpSmem<FW, F16, STAGES, VST, CX, B3, BS>;
+    using SM = G4Smem<FW, F16, STAGES, VST, CX, B3, BS>;
     const size_t smem = sizeof(SM) * WARPS;
     auto kern = spmm_bittcf_g4_kernel<FW, F16, WARPS, STAGES, RND, MINB, NM, LDSM, K8, VD, PF256, VST, HYB, CX, B3, DEC64, EL, HT, PIN, DYN, BS, WT>;
     static int configured_device = -1;
@@ -1620,6 +1635,12 @@ accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, 
         case 84:  // deep ring (70), test_wait spin
             if (multi) return launch_g4<FW, F16, 1, 3, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, true, 1, 2>(kp, map, n_units, stream);
             return launch_g4<FW, F16, 1, 3, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, true, 1, 2>(kp, map, n_units, stream);
+        case 85:  // default kernel, stage barriers packed at the head of the warp's area
+            if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, false, 0, 0>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, false, 0, 0>(kp, map, n_units, stream);
+        case 86:  // deep ring (70), stage barriers packed at the head
+            if (multi) return launch_g4<FW, F16, 1, 3, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, true, 0, 0>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 3, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, true, 0, 0>(kp, map, n_units, stream);
         case 62:  // default kernel with the 64-bit shift decode (tile_rank) instead of the 32-bit one
             if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, true>(kp, map, n_units, stream);
             return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, true>(kp, map, n_units, stream);
