@@ -544,9 +544,15 @@ def main():
             for i in range(e_steps):
                 plan.execute_host(Bb[i], Cb[i], stream)
         ts = timed(sync_steps)
+        io_bytes = [int(Bh[0].numel() * Bh[0].element_size()), int(Ch[0].numel() * Ch[0].element_size())]
+        if world > 1:
+            tb = torch.tensor(io_bytes, dtype=torch.int64, device="cpu" if shared else "cuda")
+            dist.all_reduce(tb)
+            io_bytes = [int(x) for x in tb.tolist()]
         e2e = {"value": 2.0 * A.nnz * args.N * e_steps / te / 1e9, "unit": "GFLOP/s",
-               "h2d_bytes_per_step": int(Bh[0].numel() * Bh[0].element_size()),
-               "d2h_bytes_per_step": int(Ch[0].numel() * Ch[0].element_size()), "steps": e_steps,
+               # whole job: every rank copies its own B in and its C slab out each step
+               "h2d_bytes_per_step": io_bytes[0], "d2h_bytes_per_step": io_bytes[1], "ranks": world,
+               "steps": e_steps,
                "ms_per_step": te / e_steps * 1e3,
                "api": "accspmm_execute_host_batch (H2D/SpMM/D2H pipelined over 2 device slots)",
                "sync_per_step": {"value": 2.0 * A.nnz * args.N * e_steps / ts / 1e9,
