@@ -309,6 +309,14 @@ accspmm_status accspmm_debug_decode(const accspmm_plan *plan, float *tiles, void
  * whose B fits there, so this is the roofline denominator of its L2 bytes (bench.py). */
 accspmm_status accspmm_probe_l2_bandwidth(int64_t bytes, int32_t iters, double *gbs);
 
+/* The same probe with a choice of request engine (device, synchronous): mode 1 = the 128-bit
+ * ld.global.cg loads above; mode 2 = TMA bulk copies (cp.async.bulk global -> shared, one
+ * issuing thread per CTA, 2-16 KB chunks through a 4-8 stage mbarrier ring: the path the
+ * SpMM kernel's gathered B rows take); mode 0 = the larger of the two.  `bytes` is rounded
+ * down to a multiple of 16 KiB.  Errors: ACCSPMM_ERR_INVALID_VALUE for bytes < 1 MiB,
+ * iters < 1, a NULL gbs or another mode; ACCSPMM_ERR_CUDA for a failed allocation/launch. */
+accspmm_status accspmm_probe_l2_bandwidth_ex(int64_t bytes, int32_t iters, int32_t mode, double *gbs);
+
 const char *accspmm_status_string(accspmm_status s);
 const char *accspmm_last_error(void);
 int32_t accspmm_abi_version(void);

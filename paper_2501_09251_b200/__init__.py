@@ -74,7 +74,7 @@ EXPORTED = [
     "accspmm_plan_export_units", "accspmm_plan_export_rows", "accspmm_reorder", "accspmm_partition_bounds",
     "accspmm_unpermute", "accspmm_debug_round_tf32", "accspmm_debug_decode", "accspmm_status_string",
     "accspmm_last_error", "accspmm_abi_version", "accspmm_plan_set_timing", "accspmm_plan_kernel_times",
-    "accspmm_probe_l2_bandwidth", "accspmm_execute_host_batch", "accspmm_csr_transpose",
+    "accspmm_probe_l2_bandwidth", "accspmm_probe_l2_bandwidth_ex", "accspmm_execute_host_batch", "accspmm_csr_transpose",
     "accspmm_execute_allgather", "accspmm_reorder_parallel", "accspmm_plan_create_perm", "accspmm_plan_b_bytes",
 ]
 
@@ -115,6 +115,7 @@ def load_library(path: str = LIB_PATH):
         "accspmm_plan_set_timing": ([P, I32], S),
         "accspmm_plan_kernel_times": ([P, P, I32, ctypes.POINTER(I32)], S),
         "accspmm_probe_l2_bandwidth": ([I64, I32, ctypes.POINTER(ctypes.c_double)], S),
+        "accspmm_probe_l2_bandwidth_ex": ([I64, I32, I32, ctypes.POINTER(ctypes.c_double)], S),
         "accspmm_execute_host_batch": ([P, P, P, I32, I64, P], S),
         "accspmm_csr_transpose": ([I64, I64, P, P, P, P, P, P], S),
         "accspmm_execute_allgather": ([P, P, I64, P, I32, P], S),
@@ -319,6 +320,13 @@ def accspmm_plan_kernel_times(plan, max_n: int = 4096) -> np.ndarray:
 def accspmm_probe_l2_bandwidth(nbytes: int = 64 << 20, iters: int = 50) -> float:
     g = ctypes.c_double()
     _check(load_library().accspmm_probe_l2_bandwidth(int(nbytes), int(iters), ctypes.byref(g)))
+    return g.value
+
+
+def accspmm_probe_l2_bandwidth_ex(nbytes: int = 64 << 20, iters: int = 50, mode: int = 0) -> float:
+    """mode 1: ld.global.cg loads, 2: TMA bulk copies, 0: the larger of the two."""
+    g = ctypes.c_double()
+    _check(load_library().accspmm_probe_l2_bandwidth_ex(int(nbytes), int(iters), int(mode), ctypes.byref(g)))
     return g.value
 
 

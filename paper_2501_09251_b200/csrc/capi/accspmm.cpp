@@ -953,7 +953,14 @@ accspmm_status accspmm_debug_decode(const accspmm_plan *p, float *tiles, void *s
 accspmm_status accspmm_probe_l2_bandwidth(int64_t bytes, int32_t iters, double *gbs)
 {
     if (bytes < (1 << 20) || iters < 1 || !gbs) return fail(ACCSPMM_ERR_INVALID_VALUE, "bad argument");
-    return probe_l2_read(bytes & ~(int64_t)15, iters, gbs);
+    return probe_l2_read(bytes & ~(int64_t)15, iters, gbs, 1);
+}
+
+accspmm_status accspmm_probe_l2_bandwidth_ex(int64_t bytes, int32_t iters, int32_t mode, double *gbs)
+{
+    if (bytes < (1 << 20) || iters < 1 || !gbs || mode < 0 || mode > 2)
+        return fail(ACCSPMM_ERR_INVALID_VALUE, "bad argument");
+    return probe_l2_read(bytes & ~(int64_t)16383, iters, gbs, mode);
 }
 
 const char *accspmm_status_string(accspmm_status s)

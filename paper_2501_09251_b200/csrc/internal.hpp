@@ -201,6 +201,6 @@ accspmm_status launch_round_tf32(const float *in, float *out, int64_t n, void *s
 // the hotness tag of each block in its lane-0 entry (kHotShift)
 accspmm_status launch_relabel_cols(uint32_t *a2b, int64_t n, const uint32_t *colorig, bool levels, void *stream);
 accspmm_status launch_decode(const DevicePlan &p, float *tiles, void *stream);
-accspmm_status probe_l2_read(int64_t bytes, int iters, double *gbs);
+accspmm_status probe_l2_read(int64_t bytes, int iters, double *gbs, int mode);  // 0 best, 1 LDG, 2 TMA
 
 }  // namespace accspmm

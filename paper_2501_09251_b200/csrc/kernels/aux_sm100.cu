@@ -100,6 +100,46 @@ __global__ void l2_read_kernel(const uint4 *__restrict__ buf, int64_t n16, int i
     if (acc == 0x9E3779B9u) sink[0] = acc;  // practically never taken; keeps the loads live
 }
 
+// L2 read-bandwidth probe through the TMA engine (the SpMM kernel's B rows arrive this way):
+// one thread per CTA streams CHUNK-byte bulk copies (cp.async.bulk global -> shared, mbarrier
+// complete_tx) of the L2-resident buffer through an ST-stage shared-memory ring.
+__device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+template <int ST, int CHUNK>
+__global__ void __launch_bounds__(32) l2_bulk_kernel(const uint8_t *__restrict__ buf, int64_t nchunks, int iters)
+{
+    extern __shared__ __align__(128) uint8_t ring[];
+    uint64_t *bar = reinterpret_cast<uint64_t *>(ring + ST * CHUNK);
+    if (threadIdx.x != 0) return;
+    for (int s = 0; s < ST; ++s)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_addr(bar + s)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    uint32_t q = 0;  // copies issued so far; copy q uses stage q % ST
+    auto wait = [&](uint32_t s, uint32_t parity) {
+        asm volatile(
+            "{\n\t.reg .pred P1;\n\t"
+            "W_%=:\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+            "@!P1 bra W_%=;\n\t}\n" ::"r"(smem_addr(bar + s)),
+            "r"(parity)
+            : "memory");
+    };
+    for (int it = 0; it < iters; ++it) {
+        for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x, ++q) {
+            const uint32_t s = q % ST;
+            if (q >= (uint32_t)ST) wait(s, ((q / ST) - 1u) & 1u);  // the stage's previous copy landed
+            const uint32_t b = smem_addr(bar + s);
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(b), "r"(CHUNK) : "memory");
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                    smem_addr(ring + s * CHUNK)),
+                "l"(buf + c * CHUNK), "r"(CHUNK), "r"(b)
+                : "memory");
+        }
+    }
+    for (uint32_t r = q > (uint32_t)ST ? q - ST : 0u; r < q; ++r) wait(r % ST, (r / ST) & 1u);  // drain
+}
+
 int grid_for(int64_t n, int threads)
 {
     int64_t g = (n + threads - 1) / threads;
@@ -134,7 +174,7 @@ accspmm_status launch_unpermute(const float *G, const uint32_t *orig_row, int64_
     return check_launch("unpermute launch");
 }
 
-accspmm_status probe_l2_read(int64_t bytes, int iters, double *gbs)
+accspmm_status probe_l2_read(int64_t bytes, int iters, double *gbs, int mode)
 {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -151,7 +191,7 @@ accspmm_status probe_l2_read(int64_t bytes, int iters, double *gbs)
     const uint4 *b16 = reinterpret_cast<const uint4 *>(buf);
     double best = 0.0;
     // the best of a few launch shapes / load depths (the probe must not under-state the peak)
-    for (int cfg = 0; cfg < 4 && e == cudaSuccess; ++cfg) {
+    for (int cfg = 0; cfg < 4 && e == cudaSuccess && mode != 2; ++cfg) {
         const unsigned grid = (unsigned)sms * (cfg & 1 ? 8 : 4);
         const int threads = cfg & 1 ? 256 : 512;
         auto kern = cfg < 2 ? l2_read_kernel<4> : l2_read_kernel<8>;
@@ -163,6 +203,28 @@ accspmm_status probe_l2_read(int64_t bytes, int iters, double *gbs)
         e = cudaEventSynchronize(e1);
         if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, e0, e1);
         if (e == cudaSuccess && ms > 0.f) best = std::max(best, (double)n16 * 16.0 * iters / (ms * 1e-3) / 1e9);
+    }
+    // TMA bulk copies (mode 0 or 2): the best of ring depths / chunk sizes / CTAs per SM
+    for (int cfg = 0; cfg < 4 && e == cudaSuccess && mode != 1; ++cfg) {
+        struct Shape { void (*k)(const uint8_t *, int64_t, int); int chunk, st, per_sm; };
+        const Shape sh[4] = {{l2_bulk_kernel<4, 16384>, 16384, 4, 3}, {l2_bulk_kernel<8, 8192>, 8192, 8, 3},
+                             {l2_bulk_kernel<4, 4096>, 4096, 4, 12}, {l2_bulk_kernel<8, 2048>, 2048, 8, 12}};
+        const Shape &x = sh[cfg];
+        const int smem = x.st * x.chunk + 128;
+        e = cudaFuncSetAttribute(x.k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) break;
+        const int64_t nchunks = bytes / x.chunk;
+        const unsigned grid = (unsigned)(sms * x.per_sm);
+        const uint8_t *b8 = reinterpret_cast<const uint8_t *>(buf);
+        x.k<<<grid, 32, smem>>>(b8, nchunks, 2);  // warm L2
+        cudaEventRecord(e0);
+        x.k<<<grid, 32, smem>>>(b8, nchunks, iters);
+        cudaEventRecord(e1);
+        float ms = 0.f;
+        e = cudaEventSynchronize(e1);
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, e0, e1);
+        if (e == cudaSuccess && ms > 0.f)
+            best = std::max(best, (double)nchunks * x.chunk * iters / (ms * 1e-3) / 1e9);
     }
     cudaFree(buf);
     cudaFree(sink);

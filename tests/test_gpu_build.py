@@ -130,3 +130,16 @@ def test_device_build_requires_device():
     A = gen.identity(16)
     with pytest.raises(acc.AccSpmmError):
         acc.Plan(A.M, A.K, A.rowptr, A.colidx, np.ones(16, np.float32), build="device", device=-1)
+
+
+@pytest.mark.gpu
+def test_l2_probe_both_engines():
+    """L2 read-bandwidth probe (the roofline denominator of bench.py): both request engines give
+    a bandwidth above the HBM copy bandwidth and below the L2's physical ceiling (a 96 MiB buffer
+    is L2-resident on the B200's 126 MB L2), and mode 0 is the larger of the two."""
+    ldg = acc.accspmm_probe_l2_bandwidth_ex(96 << 20, 20, mode=1)
+    tma = acc.accspmm_probe_l2_bandwidth_ex(96 << 20, 20, mode=2)
+    best = acc.accspmm_probe_l2_bandwidth_ex(96 << 20, 20, mode=0)
+    for g in (ldg, tma, best):
+        assert 7000.0 < g < 60000.0, (ldg, tma, best)
+    assert best >= 0.9 * max(ldg, tma), (ldg, tma, best)

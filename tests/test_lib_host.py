@@ -81,6 +81,15 @@ def test_bad_options_and_host_only_execute():
     assert ei.value.status == 3
 
 
+@pytest.mark.parametrize("args", [(0, 1, 0), (1 << 20, 0, 0), (1 << 20, 1, 3), (1 << 20, 1, -1)])
+def test_l2_probe_rejects_bad_arguments(args):
+    """The measurement hook validates before touching the device (header: bytes >= 1 MiB,
+    iters >= 1, mode 0/1/2)."""
+    with pytest.raises(acc.AccSpmmError) as ei:
+        acc.accspmm_probe_l2_bandwidth_ex(*args)
+    assert ei.value.status == 1
+
+
 def _check_format(F, ref, precision):
     assert np.array_equal(F["RowWindowOffset"], ref["RowWindowOffset"])
     assert np.array_equal(F["TCOffset"], ref["TCOffset"])
