@@ -92,7 +92,9 @@ typedef struct {
                              pass).  C is unchanged.  Default 0 (rows only, reading Q12).          */
     int32_t window_rows;  /* rows per RowWindow: 0 or 8 = the paper's BitTCF (8x8 tiles);
                              16 or 32 = tall windows (reading R20: wh x 8 tiles, wh/8 u64 occupancy
-                             words per block) -- TF32 only, executed by the tcgen05 kernel.       */
+                             words per block), executed by the tcgen05 kernel (TF32 only) unless
+                             kernel = MMA_SYNC, which runs 16-row windows (TF32 or FP16; two
+                             accumulator halves per gathered row) and rejects 32.                 */
     int32_t kernel;       /* accspmm_kernel: which SpMM kernel executes the plan (default AUTO)   */
     int32_t hot_cols;     /* accspmm_hot_mode; reading R22 (DESIGN.md §3/§6): relabel the columns by
                              descending in-degree so each window condenses its hottest columns

@@ -228,10 +228,13 @@ static accspmm_status plan_create_impl(int64_t M, int64_t K, const int64_t *rowp
         return fail(ACCSPMM_ERR_INVALID_VALUE, "unknown kernel");
     if (opt.hot_cols < ACCSPMM_HOT_AUTO || opt.hot_cols > ACCSPMM_HOT_OFF)
         return fail(ACCSPMM_ERR_INVALID_VALUE, "unknown hot_cols mode");
-    if (wh > kWindow && opt.kernel == ACCSPMM_KERNEL_MMA_SYNC)
-        return fail(ACCSPMM_ERR_UNSUPPORTED, "the mma.sync kernel runs 8-row windows only");
-    const int kernel = (wh > kWindow || opt.kernel == ACCSPMM_KERNEL_TCGEN05) ? ACCSPMM_KERNEL_TCGEN05
-                                                                           : ACCSPMM_KERNEL_MMA_SYNC;
+    if (wh > 2 * kWindow && opt.kernel == ACCSPMM_KERNEL_MMA_SYNC)
+        return fail(ACCSPMM_ERR_UNSUPPORTED, "the mma.sync kernel runs 8- or 16-row windows");
+    // tall windows default to the tcgen05 kernel; kernel = MMA_SYNC runs 16-row windows on the
+    // mma.sync kernel (two accumulator halves per gathered row)
+    const int kernel = (opt.kernel == ACCSPMM_KERNEL_TCGEN05 || (wh > kWindow && opt.kernel != ACCSPMM_KERNEL_MMA_SYNC))
+                           ? ACCSPMM_KERNEL_TCGEN05
+                           : ACCSPMM_KERNEL_MMA_SYNC;
     if (kernel == ACCSPMM_KERNEL_TCGEN05 && opt.precision != ACCSPMM_TF32)
         return fail(ACCSPMM_ERR_UNSUPPORTED, "the tcgen05 kernel (and tall windows) is TF32 only");
     if (M < 0 || K < 0) return fail(ACCSPMM_ERR_INVALID_VALUE, "negative matrix dimension");
@@ -481,7 +484,7 @@ static bool in_kernel_rounding(const accspmm_plan *p)
 static bool b3_layout(const accspmm_plan *p, int64_t N, int ndst)
 {
     return p->opt.precision == ACCSPMM_TF32 && !in_kernel_rounding(p) && p->info.K > 0 &&
-           p->dev.kernel != ACCSPMM_KERNEL_TCGEN05 && knobs().b3 != 0 &&
+           p->dev.kernel != ACCSPMM_KERNEL_TCGEN05 && p->dev.wh == kWindow && knobs().b3 != 0 &&
            (ndst > 0 || knobs().kcfg < 0 || is_b3_variant(knobs().kcfg)) &&
            pick_fw(N) >= 64;
 }

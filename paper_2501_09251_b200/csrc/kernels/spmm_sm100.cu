@@ -200,10 +200,11 @@ struct Cfg {
 constexpr int kChunk = 16;  // TC blocks per staged A-stream chunk
 
 // X = extra TCOffset entries (value staging reads the TCOffset of the block after the chunk)
-template <int X = 0>
+// NWD = occupancy words per block (1: the paper's 8-row windows; 2: 16-row windows, R20)
+template <int X = 0, int NWD = 1>
 struct ChunkSmemT {
     uint32_t a2b[kChunk * 8];
-    uint64_t mask[kChunk];
+    uint64_t mask[kChunk * NWD];
     uint32_t tco[kChunk + X];
 };
 using ChunkSmem = ChunkSmemT<0>;
@@ -607,10 +608,11 @@ struct G4Cfg {
 // from the shared-memory offsets.
 // BS = barrier stride in 8-byte words (1: packed; 2: one 16-byte slot per stage barrier;
 // 16: one 128-byte line each -- measurement variants)
-template <int FW, bool F16, int STAGES, int VST = 0, int CX = (VST ? 4 : 0), bool B3 = false, int BS = 1>
+template <int FW, bool F16, int STAGES, int VST = 0, int CX = (VST ? 4 : 0), bool B3 = false, int BS = 1,
+          int NWD = 1>
 struct G4WarpSmem {
     alignas(128) uint8_t stage[STAGES][G4Cfg<FW, F16, B3>::STAGE_AL];
-    ChunkSmemT<CX> ch[VST ? 3 : 2];
+    ChunkSmemT<CX, NWD> ch[VST ? 3 : 2];
     alignas(BS >= 16 ? 128 : 16) uint64_t bar[STAGES * BS];
     uint64_t vbar[2];
     uint32_t vlo[2];  // first staged value index per buffer (0xFFFFFFFF: over VST, values from L2)
@@ -626,10 +628,10 @@ struct G4WarpSmemHead {
     ChunkSmemT<CX> ch[VST ? 3 : 2];
     alignas(16) uint8_t vals[VST ? 2 : 1][VST ? VST * (F16 ? 2 : 4) : 16];
 };
-template <int FW, bool F16, int STAGES, int VST, int CX, bool B3, int BS>
+template <int FW, bool F16, int STAGES, int VST, int CX, bool B3, int BS, int NWD = 1>
 using G4Smem = std::conditional_t<BS == 0, G4WarpSmemHead<FW, F16, STAGES, VST, CX, B3>,
-                                  G4WarpSmem<FW, F16, STAGES, VST, CX, B3, BS>>;
-static_assert(sizeof(ChunkSmemT<0>) % 16 == 0 && sizeof(ChunkSmemT<4>) % 16 == 0,
+                                  G4WarpSmem<FW, F16, STAGES, VST, CX, B3, BS, NWD>>;
+static_assert(sizeof(ChunkSmemT<0>) % 16 == 0 && sizeof(ChunkSmemT<4>) % 16 == 0 && sizeof(ChunkSmemT<0, 2>) % 16 == 0,
               "chunk alignment (cp.async 16 B into a2b)");
 
 __device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap *map, int32_t col, int32_t r0, int32_t r1,
@@ -658,7 +660,7 @@ inline int map_count(const KParams &kp) { return kp.nslices > 1 && kp.nslices <=
 template <int FW, bool F16, int WARPS, int STAGES, bool RND, int MINB = 1, int NM = 1, bool LDSM_ = false,
           bool K8 = false, int VD = 1, int PF256 = 0, int VST = 0, bool HYB = false, int CX = (VST ? 4 : 0),
           bool B3 = false, bool DEC64 = false, int EL = 1, bool HT = true, bool PIN = false, bool DYN = false,
-          int BS = 1, int WT = 0>
+          int BS = 1, int WT = 0, int WH = 8>
 __global__ void __launch_bounds__(WARPS * 32, MINB)
     spmm_bittcf_g4_kernel(const KParams p, const __grid_constant__ G4MapsT<NM> maps)
 {
@@ -672,10 +674,17 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     // and the 8 row addresses of every ldmatrix phase hit 8 distinct bank groups.  The
     // accumulator layout is then m16 tile mt = features 16mt .. 16mt+15 (epilogue below).
     constexpr bool LDSM = LDSM_ && F16;
+    // WH = 16 (reading R20 on the mma.sync kernel): a block is a 16 x 8 tile (two occupancy
+    // words); each gathered row feeds NH = 2 accumulator halves (window rows 0-7 and 8-15), so
+    // the two gathers of a block serve twice the rows.  Default ring and value path only.
+    constexpr int NH = WH / 8;
+    static_assert(WH == 8 || (WH == 16 && STAGES == 2 && VD == 1 && PF256 == 0 && VST == 0 && !HYB && !B3 &&
+                              !DEC64 && !DYN && !HT && BS >= 1),
+                  "16-row windows: the default kernel configuration");
     constexpr int CH = kChunk;  // blocks per staged chunk
     using CF = Cfg<FW, F16>;
     using GC = G4Cfg<FW, F16, B3>;
-    using SM = G4Smem<FW, F16, STAGES, VST, CX, B3, BS>;
+    using SM = G4Smem<FW, F16, STAGES, VST, CX, B3, BS, WH / 8>;
     static_assert(!B3 || (!RND && !HYB && VST == 0 && !LDSM_), "B3: pre-rounded B, default ring");
     static_assert(VST == 0 || CX >= 1, "value staging reads the TCOffset after the chunk");
     static_assert(offsetof(SM, bar) % 16 == 0, "stage mbarriers 16-byte aligned (measured: 2.2x slower otherwise)");
@@ -746,7 +755,10 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
             const uint32_t b = b0 + i;
             const uint32_t cnt = min((uint32_t)CH, nblk - i);
             if ((uint32_t)lane < cnt) {
-                cp_async8(smem_u32(&c.mask[lane]), p.bits + b + lane, pol_stream);
+                if constexpr (NH == 1)
+                    cp_async8(smem_u32(&c.mask[lane]), p.bits + b + lane, pol_stream);
+                else
+                    cp_async16(smem_u32(&c.mask[2 * lane]), p.bits + 2 * ((size_t)b + lane), pol_stream);
                 cp_async4(smem_u32(&c.tco[lane]), p.tco + b + lane, pol_stream);
             }
             if (VST > 0 && (uint32_t)lane == cnt) cp_async4(smem_u32(&c.tco[lane]), p.tco + b + lane, pol_stream);
@@ -766,6 +778,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     static_assert(!DYN || (STAGES > 2 && STAGES <= 4 && VST == 0 && !HYB), "deep ring: 3 or 4 stages");
     constexpr int VR = DYN ? 4 : VD == 1 ? 2 : 4;
     uint32_t vb0[VR], vb1[VR];
+    uint32_t vc0[NH == 2 ? VR : 1], vc1[NH == 2 ? VR : 1];  // window rows 8-15 (WH = 16)
+    constexpr int SM1 = NH == 2 ? VR - 1 : 0;                // their slot mask
     // PF256 == 3 (measurement variant): the block's value run is loaded by one coalesced warp
     // load (lane L: value tco + L, and tco + 32 + L when the block holds more than 32); the
     // lane's two entries are picked by shuffles at consume time.  vix = packed local indices
@@ -802,7 +816,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     auto value_load = [&](uint32_t j, int slot) {
         const auto &c = sm.ch[(j / CH) % NCB];
         const uint32_t cs = j & (CH - 1u);
-        const uint64_t mask = c.mask[cs];
+        const uint64_t mask = c.mask[cs * NH];
         const uint32_t t0 = c.tco[cs];
         bool p0, p1;
         uint32_t i0, i1;
@@ -871,11 +885,31 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
             const float *vp = reinterpret_cast<const float *>(vals_base);
             vb0[slot] = p0 ? __float_as_uint(__ldg(vp + i0)) : 0u;
             vb1[slot] = p1 ? __float_as_uint(__ldg(vp + i1)) : 0u;
+            if constexpr (NH == 2) {  // word 1 (rows 8-15): its values follow all of word 0's
+                const uint64_t m1 = c.mask[cs * 2 + 1];
+                const uint32_t lo = (uint32_t)m1, hi = (uint32_t)(m1 >> 32);
+                const uint32_t r = (hw ? hi : lo) >> p0w;
+                const uint32_t j0 = t0 + (uint32_t)__popcll(mask) + (uint32_t)__popc(lo & m_lo) +
+                                    (uint32_t)__popc(hi & m_hi);
+                const uint32_t j1 = j0 + (uint32_t)__popc(r & ((1u << DK) - 1u));
+                vc0[slot & SM1] = (r & 1u) ? __float_as_uint(__ldg(vp + j0)) : 0u;
+                vc1[slot & SM1] = ((r >> DK) & 1u) ? __float_as_uint(__ldg(vp + j1)) : 0u;
+            }
         } else {
             // keep the two halves apart until the MMA: packing here would stall on the loads
             const unsigned short *vp = reinterpret_cast<const unsigned short *>(vals_base);
             vb0[slot] = p0 ? (uint32_t)__ldg(vp + i0) : 0u;
             vb1[slot] = p1 ? (uint32_t)__ldg(vp + i1) : 0u;
+            if constexpr (NH == 2) {
+                const uint64_t m1 = c.mask[cs * 2 + 1];
+                const uint32_t lo = (uint32_t)m1, hi = (uint32_t)(m1 >> 32);
+                const uint32_t r = (hw ? hi : lo) >> p0w;
+                const uint32_t j0 = t0 + (uint32_t)__popcll(mask) + (uint32_t)__popc(lo & m_lo) +
+                                    (uint32_t)__popc(hi & m_hi);
+                const uint32_t j1 = j0 + (uint32_t)__popc(r & ((1u << DK) - 1u));
+                vc0[slot & SM1] = (r & 1u) ? (uint32_t)__ldg(vp + j0) : 0u;
+                vc1[slot & SM1] = ((r >> DK) & 1u) ? (uint32_t)__ldg(vp + j1) : 0u;
+            }
         }
     };
 
@@ -954,8 +988,13 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     };
 
     float acc[MT][4];
+    float acc1[NH == 2 ? MT : 1][4];  // window rows 8-15 (WH = 16)
 #pragma unroll
     for (int m = 0; m < MT; ++m) acc[m][0] = acc[m][1] = acc[m][2] = acc[m][3] = 0.f;
+    if constexpr (NH == 2) {
+#pragma unroll
+        for (int m = 0; m < MT; ++m) acc1[m][0] = acc1[m][1] = acc1[m][2] = acc1[m][3] = 0.f;
+    }
 
     // ---- consumer: wait for stage s, load the gathered-row fragments, tensor-core MMA
     auto consume = [&](uint32_t i, int s, int slot) {
@@ -1012,6 +1051,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
             const int k = lane & 7, mx = lane >> 3;
             const uint32_t row = smem_u32(st) + ((k & 1) ? GC::GRP + 16u : 0u) + (uint32_t)(k >> 1) * GC::RS;
             const uint32_t bv = vb0[slot] | (vb1[slot] << 16);
+            const uint32_t bw = NH == 2 ? (vc0[slot & SM1] | (vc1[slot & SM1] << 16)) : 0u;
             if constexpr (FW >= 32) {
 #pragma unroll
                 for (int q = 0; q < FW / 32; ++q) {
@@ -1019,11 +1059,16 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
                     ldsm_x4_trans(a0, a1, a2, a3, row + (uint32_t)(mx * 16 + q * 64));
                     mma_f16(acc[2 * q], a0, a1, bv);
                     mma_f16(acc[2 * q + 1], a2, a3, bv);
+                    if constexpr (NH == 2) {
+                        mma_f16(acc1[2 * q], a0, a1, bw);
+                        mma_f16(acc1[2 * q + 1], a2, a3, bw);
+                    }
                 }
             } else {
                 uint32_t a0, a1;
                 ldsm_x2_trans(a0, a1, row + (uint32_t)((mx & 1) * 16));
                 mma_f16(acc[0], a0, a1, bv);
+                if constexpr (NH == 2) mma_f16(acc1[0], a0, a1, bw);
             }
         } else if constexpr (!F16 && CF::VW == 4) {
             // two k=4 halves of the 8x8 tile: rows t (k = 0..3) and t+4 (k = 4..7); each
@@ -1047,16 +1092,37 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
                     mma_tf32(acc[2 * j], x[j].x, x[j].y, y[j].x, y[j].y, vb0[slot], vb1[slot]);
                     mma_tf32(acc[2 * j + 1], x[j].z, x[j].w, y[j].z, y[j].w, vb0[slot], vb1[slot]);
                 }
+                if constexpr (NH == 2) {
+#pragma unroll
+                    for (int j = 0; j < NV; ++j) {
+                        mma_tf32(acc1[2 * j], x[j].x, x[j].y, y[j].x, y[j].y, vc0[slot & SM1], vc1[slot & SM1]);
+                        mma_tf32(acc1[2 * j + 1], x[j].z, x[j].w, y[j].z, y[j].w, vc0[slot & SM1], vc1[slot & SM1]);
+                    }
+                }
             } else {
 #pragma unroll
                 for (int j = 0; j < NV; ++j) {
                     mma_tf32_k4(acc[2 * j], x[j].x, x[j].y, vb0[slot]);
                     mma_tf32_k4(acc[2 * j + 1], x[j].z, x[j].w, vb0[slot]);
                 }
+                if constexpr (NH == 2) {
+#pragma unroll
+                    for (int j = 0; j < NV; ++j) {
+                        mma_tf32_k4(acc1[2 * j], x[j].x, x[j].y, vc0[slot & SM1]);
+                        mma_tf32_k4(acc1[2 * j + 1], x[j].z, x[j].w, vc0[slot & SM1]);
+                    }
+                }
 #pragma unroll
                 for (int j = 0; j < NV; ++j) {
                     mma_tf32_k4(acc[2 * j], y[j].x, y[j].y, vb1[slot]);
                     mma_tf32_k4(acc[2 * j + 1], y[j].z, y[j].w, vb1[slot]);
+                }
+                if constexpr (NH == 2) {
+#pragma unroll
+                    for (int j = 0; j < NV; ++j) {
+                        mma_tf32_k4(acc1[2 * j], y[j].x, y[j].y, vc1[slot & SM1]);
+                        mma_tf32_k4(acc1[2 * j + 1], y[j].z, y[j].w, vc1[slot & SM1]);
+                    }
                 }
             }
         } else {
@@ -1075,21 +1141,31 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
                 fr.b1 = vb1[slot];
             }
             mma_block<FW, F16>(acc, fr);
+            if constexpr (NH == 2) {
+                if constexpr (F16) {
+                    fr.b0 = vc0[slot & SM1] | (vc1[slot & SM1] << 16);
+                } else {
+                    fr.b0 = vc0[slot & SM1];
+                    fr.b1 = vc1[slot & SM1];
+                }
+                mma_block<FW, F16>(acc1, fr);
+            }
         }
     };
 
-    auto store_rows = [&](float *base, int64_t ld, int64_t lr0, bool remap, const uint32_t *rmap) {
+    // a = the accumulator half of window rows lr0 .. lr0 + 7 (WH = 16: acc, then acc1 at lr0 + 8)
+    auto store_rows = [&](float *base, int64_t ld, int64_t lr0, bool remap, const uint32_t *rmap, auto &a) {
 #pragma unroll
         for (int s2 = 0; s2 < 2; ++s2) {
             const int64_t lr = lr0 + 2 * t + s2;
             if (!remap || lr < p.rows) {
-                const int64_t orow = remap ? (rmap ? (int64_t)__ldg(rmap + lr) : lr) : (2 * t + s2);
+                const int64_t orow = remap ? (rmap ? (int64_t)__ldg(rmap + lr) : lr) : lr;
                 if constexpr (LDSM) {  // tile mt: features 16mt + g (c0/c1) and 16mt + 8 + g (c2/c3)
                     float *d = base + orow * ld + g;
 #pragma unroll
                     for (int mt = 0; mt < MT; ++mt) {
-                        st_cs1(d + 16 * mt, acc[mt][s2]);
-                        st_cs1(d + 16 * mt + 8, acc[mt][2 + s2]);
+                        st_cs1(d + 16 * mt, a[mt][s2]);
+                        st_cs1(d + 16 * mt + 8, a[mt][2 + s2]);
                     }
                     continue;
                 }
@@ -1098,12 +1174,12 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
                 for (int j = 0; j < NV; ++j) {
                     float *d = dst + 8 * VW * j;
                     if constexpr (VW == 2) {
-                        st_cs(d, acc[j][s2], acc[j][2 + s2]);
+                        st_cs(d, a[j][s2], a[j][2 + s2]);
                     } else {
 #pragma unroll
                         for (int q = 0; q < VW / 4; ++q) {
                             const int m0 = (VW / 2) * j + 2 * q;
-                            st_cs(d + 4 * q, acc[m0][s2], acc[m0][2 + s2], acc[m0 + 1][s2], acc[m0 + 1][2 + s2]);
+                            st_cs(d + 4 * q, a[m0][s2], a[m0][2 + s2], a[m0 + 1][s2], a[m0 + 1][2 + s2]);
                         }
                     }
                 }
@@ -1111,15 +1187,49 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
         }
     };
     auto store_window = [&](uint32_t wi) {
-        const int64_t lr0 = (int64_t)(w0 + wi) * 8;
+        const int64_t lr0 = (int64_t)(w0 + wi) * WH;
         if (p.ndst == 0) {
-            store_rows(p.C + f0, p.N, lr0, true, p.row_map);
+            store_rows(p.C + f0, p.N, lr0, true, p.row_map, acc);
+            if constexpr (NH == 2) store_rows(p.C + f0, p.N, lr0 + 8, true, p.row_map, acc1);
         } else {  // fused all-gather: the rows go straight to every rank's C (original order)
 #pragma unroll 1
-            for (int d = 0; d < p.ndst; ++d) store_rows(p.dst[d] + f0, p.N, lr0, true, p.orig_map);
+            for (int d = 0; d < p.ndst; ++d) {
+                store_rows(p.dst[d] + f0, p.N, lr0, true, p.orig_map, acc);
+                if constexpr (NH == 2) store_rows(p.dst[d] + f0, p.N, lr0 + 8, true, p.orig_map, acc1);
+            }
         }
 #pragma unroll
         for (int m = 0; m < MT; ++m) acc[m][0] = acc[m][1] = acc[m][2] = acc[m][3] = 0.f;
+        if constexpr (NH == 2) {
+#pragma unroll
+            for (int m = 0; m < MT; ++m) acc1[m][0] = acc1[m][1] = acc1[m][2] = acc1[m][3] = 0.f;
+        }
+    };
+    // split-window fixup: add one segment's partial tile (rows 0-7 of it) into accumulator a
+    auto add_tile = [&](const float *src, auto &a) {
+#pragma unroll
+        for (int s2 = 0; s2 < 2; ++s2) {
+            if constexpr (LDSM) {
+                const float *row = src + (2 * t + s2) * FW + g;
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) {
+                    a[mt][s2] += __ldcg(row + 16 * mt);
+                    a[mt][2 + s2] += __ldcg(row + 16 * mt + 8);
+                }
+                continue;
+            }
+            const float *row = src + (2 * t + s2) * FW + VW * g;
+#pragma unroll
+            for (int j = 0; j < NV; ++j) {
+#pragma unroll
+                for (int e = 0; e < VW; e += 2) {
+                    const int m = (VW / 2) * j + (e >> 1);
+                    const float2 v = __ldcg(reinterpret_cast<const float2 *>(row + 8 * VW * j + e));
+                    a[m][s2] += v.x;
+                    a[m][2 + s2] += v.y;
+                }
+            }
+        }
     };
     // wend = absolute block index where the current window ends; 0xFFFFFFFF once no whole
     // window is left (split units, or after the last one): one compare per block
@@ -1280,8 +1390,9 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
 
     if (split) {
         const uint32_t sid = ub.x, seg = ub.y, nseg = ub.z, slot = ub.w;
-        float *tile = p.ws + ((int64_t)slot * p.nslices + slice) * (8 * FW);
-        store_rows(tile, FW, 0, false, nullptr);
+        float *tile = p.ws + ((int64_t)slot * p.nslices + slice) * (WH * FW);
+        store_rows(tile, FW, 0, false, nullptr, acc);
+        if constexpr (NH == 2) store_rows(tile, FW, 8, false, nullptr, acc1);
         __threadfence();
         __syncwarp();
         uint32_t prev = 0;
@@ -1289,34 +1400,17 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
         prev = __shfl_sync(0xffffffffu, prev, 0);
         if (prev == nseg - 1) {
             __threadfence();
-            const float *first = p.ws + ((int64_t)(slot - seg) * p.nslices + slice) * (8 * FW);
+            const float *first = p.ws + ((int64_t)(slot - seg) * p.nslices + slice) * (WH * FW);
 #pragma unroll
             for (int m = 0; m < MT; ++m) acc[m][0] = acc[m][1] = acc[m][2] = acc[m][3] = 0.f;
+            if constexpr (NH == 2) {
+#pragma unroll
+                for (int m = 0; m < MT; ++m) acc1[m][0] = acc1[m][1] = acc1[m][2] = acc1[m][3] = 0.f;
+            }
             for (uint32_t k = 0; k < nseg; ++k) {
-                const float *src = first + (int64_t)k * p.nslices * (8 * FW);
-#pragma unroll
-                for (int s2 = 0; s2 < 2; ++s2) {
-                    if constexpr (LDSM) {
-                        const float *row = src + (2 * t + s2) * FW + g;
-#pragma unroll
-                        for (int mt = 0; mt < MT; ++mt) {
-                            acc[mt][s2] += __ldcg(row + 16 * mt);
-                            acc[mt][2 + s2] += __ldcg(row + 16 * mt + 8);
-                        }
-                        continue;
-                    }
-                    const float *row = src + (2 * t + s2) * FW + VW * g;
-#pragma unroll
-                    for (int j = 0; j < NV; ++j) {
-#pragma unroll
-                        for (int e = 0; e < VW; e += 2) {
-                            const int m = (VW / 2) * j + (e >> 1);
-                            const float2 v = __ldcg(reinterpret_cast<const float2 *>(row + 8 * VW * j + e));
-                            acc[m][s2] += v.x;
-                            acc[m][2 + s2] += v.y;
-                        }
-                    }
-                }
+                const float *src = first + (int64_t)k * p.nslices * (WH * FW);
+                if constexpr (NH == 2) add_tile(src + 8 * FW, acc1);
+                add_tile(src, acc);
             }
             store_window(0);
             if (lane == 0) p.counters[(int64_t)sid * p.nslices + slice] = 0u;
@@ -1388,12 +1482,12 @@ accspmm_status launch_cfg(const KParams &kp, int64_t n_units, cudaStream_t strea
 template <int FW, bool F16, int WARPS, int STAGES, bool RND = false, int MINB = 1, int NM = 1, bool LDSM = false,
           bool K8 = false, int VD = 1, int PF256 = 0, int VST = 0, bool HYB = false, int CX = (VST ? 4 : 0),
           bool B3 = false, bool DEC64 = false, int EL = 1, bool HT = true, bool PIN = false, bool DYN = false,
-          int BS = 1, int WT = 0>
+          int BS = 1, int WT = 0, int WH = 8>
 accspmm_status launch_g4(const KParams &kp, const G4Maps *map, int64_t n_units, cudaStream_t stream)
 {
-    using SM = G4Smem<FW, F16, STAGES, VST, CX, B3, BS>;
+    using SM = G4Smem<FW, F16, STAGES, VST, CX, B3, BS, WH / 8>;
     const size_t smem = sizeof(SM) * WARPS;
-    auto kern = spmm_bittcf_g4_kernel<FW, F16, WARPS, STAGES, RND, MINB, NM, LDSM, K8, VD, PF256, VST, HYB, CX, B3, DEC64, EL, HT, PIN, DYN, BS, WT>;
+    auto kern = spmm_bittcf_g4_kernel<FW, F16, WARPS, STAGES, RND, MINB, NM, LDSM, K8, VD, PF256, VST, HYB, CX, B3, DEC64, EL, HT, PIN, DYN, BS, WT, WH>;
     static int configured_device = -1;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -1528,6 +1622,19 @@ accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, 
     }
 #endif
     if (b3) return fail(ACCSPMM_ERR_INTERNAL, "B3 layout: variants build, TF32, 64/128-feature slices only");
+    if (d.wh == 16) {
+        // 16-row windows (reading R20) on this kernel: every gathered row feeds two accumulator
+        // halves, so the register cap admits fewer resident warps
+        constexpr int MW16 = FW == 128 ? 16 : FW == 64 ? 20 : 24;
+        if constexpr (!F16) {
+            if (rnd) {
+                if (multi) return launch_g4<FW, F16, 1, 2, true, MW16, NM, false, K8, 1, 0, 0, false, 0, false, false, 1, false, false, false, 1, 0, 16>(kp, map, n_units, stream);
+                return launch_g4<FW, F16, 1, 2, true, MW16, 1, false, K8, 1, 0, 0, false, 0, false, false, 1, false, false, false, 1, 0, 16>(kp, map, n_units, stream);
+            }
+        }
+        if (multi) return launch_g4<FW, F16, 1, 2, false, MW16, NM, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, false, 1, 0, 16>(kp, map, n_units, stream);
+        return launch_g4<FW, F16, 1, 2, false, MW16, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, false, 1, 0, 16>(kp, map, n_units, stream);
+    }
 #ifdef ACCSPMM_VARIANTS
     // Measured-and-rejected alternatives, selectable by ACCSPMM_KCFG in the variants build only
     // (libaccspmm_variants.so): 20 = 2 warps per CTA without a launch-bounds minimum (the

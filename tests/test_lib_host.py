@@ -487,8 +487,13 @@ def test_window_rows_and_kernel_option_validation():
         host_plan(A, v, window_rows=16, precision="fp16")        # tcgen05 path is TF32 only
     assert e.value.status == 3
     with pytest.raises(acc.AccSpmmError) as e:
-        host_plan(A, v, window_rows=16, kernel="mma_sync")       # mma.sync runs 8-row windows only
+        host_plan(A, v, window_rows=32, kernel="mma_sync")       # mma.sync runs 8- or 16-row windows
     assert e.value.status == 3
+    for precision in ("tf32", "fp16"):                           # 16-row windows on mma.sync (R20)
+        p = host_plan(A, v, window_rows=16, kernel="mma_sync", precision=precision)
+        assert p.info["window_rows"] == 16 and p.info["kernel"] == acc.KERNEL["mma_sync"]
+    p = host_plan(A, v, window_rows=16)                           # tall windows default to tcgen05
+    assert p.info["kernel"] == acc.KERNEL["tcgen05"]
     p = host_plan(A, v)
     assert p.info["window_rows"] == 8 and p.info["kernel"] == acc.KERNEL["mma_sync"]
     p = host_plan(A, v, kernel="tcgen05")
