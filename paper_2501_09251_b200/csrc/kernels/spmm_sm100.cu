@@ -660,7 +660,7 @@ inline int map_count(const KParams &kp) { return kp.nslices > 1 && kp.nslices <=
 template <int FW, bool F16, int WARPS, int STAGES, bool RND, int MINB = 1, int NM = 1, bool LDSM_ = false,
           bool K8 = false, int VD = 1, int PF256 = 0, int VST = 0, bool HYB = false, int CX = (VST ? 4 : 0),
           bool B3 = false, bool DEC64 = false, int EL = 1, bool HT = true, bool PIN = false, bool DYN = false,
-          int BS = 1, int WT = 0, int WH = 8>
+          int BS = 1, int WT = 0, int WH = 8, bool L64 = false>
 __global__ void __launch_bounds__(WARPS * 32, MINB)
     spmm_bittcf_g4_kernel(const KParams p, const __grid_constant__ G4MapsT<NM> maps)
 {
@@ -678,6 +678,13 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     // words); each gathered row feeds NH = 2 accumulator halves (window rows 0-7 and 8-15), so
     // the two gathers of a block serve twice the rows.  Default ring and value path only.
     constexpr int NH = WH / 8;
+    // L64 (TF32, FW >= 32): one m16n8k8 per m16 tile with its four A registers loaded by two
+    // LDS.64 (row t from gather x, row t + 4 from gather y) -- no register moves (the LDS.128
+    // form needs 3 MOVs per k8 MMA) and half the tensor-pipe cycles of two m16n8k4.  Gathered
+    // rows are FW + 4 elements apart (RS = 16 mod 128) and lane g's 8-byte piece tau of 32-feature
+    // chunk j sits at slot (g & 1) + 8 ((g >> 1) & 1) + 4 (g >> 2) + 2 tau, so the 16 lanes of each
+    // LDS.64 phase (4 rows x 4 pieces) hit 16 distinct 8-byte bank pairs.
+    static_assert(!L64 || (!F16 && FW >= 32 && !B3 && !HYB && VST == 0 && !LDSM_), "L64: TF32 slices >= 32");
     static_assert(WH == 8 || (WH == 16 && STAGES == 2 && VD == 1 && PF256 == 0 && VST == 0 && !HYB && !B3 &&
                               !DEC64 && !DYN && !HT && BS >= 1),
                   "16-row windows: the default kernel configuration");
@@ -685,6 +692,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     using CF = Cfg<FW, F16>;
     using GC = G4Cfg<FW, F16, B3>;
     using SM = G4Smem<FW, F16, STAGES, VST, CX, B3, BS, WH / 8>;
+    constexpr int RS = L64 ? (FW + 4) * 4 : GC::RS;
+    static_assert(!L64 || RS % 128 == 16, "L64 row stride");
     static_assert(!B3 || (!RND && !HYB && VST == 0 && !LDSM_), "B3: pre-rounded B, default ring");
     static_assert(VST == 0 || CX >= 1, "value staging reads the TCOffset after the chunk");
     static_assert(offsetof(SM, bar) % 16 == 0, "stage mbarriers 16-byte aligned (measured: 2.2x slower otherwise)");
@@ -743,7 +752,9 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     // PIN: keep the lane constants and the value base in registers (an empty asm hides their
     // derivation, so the compiler cannot rematerialise them inside the block loop)
     const char *vals_base = reinterpret_cast<const char *>(p.vals);
-    uint32_t frag_off = (uint32_t)(t * GC::RS + CF::VB * g);  // this lane's fragment offset in a stage
+    // this lane's fragment offset in a stage (L64: row t, slot of piece tau = 0)
+    const uint32_t l64_slot = (uint32_t)((g & 1) + 8 * ((g >> 1) & 1) + 4 * (g >> 2));
+    uint32_t frag_off = L64 ? (uint32_t)(t * RS + 8 * l64_slot) : (uint32_t)(t * GC::RS + CF::VB * g);
     if constexpr (PIN) {
         asm volatile("" : "+r"(m_lo), "+r"(m_hi), "+r"(frag_off));
         asm volatile("" : "+l"(vals_base));
@@ -970,7 +981,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
             // no proxy fence: the stage's previous generic reads fed this warp's mma.sync,
             // which cannot issue before every lane's LDS has returned
             const bool one = EL == 2 ? elect_one() : true;
-            if (one) mbar_arrive_expect_tx(bar, 8u * GC::RS);
+            if (one) mbar_arrive_expect_tx(bar, 8u * RS);
             // derived here, not held across the loop (registers are the occupancy limit)
             const CUtensorMap *tmap = &maps.m[NM > 1 ? slice : 0];
             const int32_t tcol = NM > 1 ? 0 : slice * (B3 ? 3 * FW / 2 : FW);  // in map elements
@@ -1015,7 +1026,24 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
         const uint8_t *st = sm.stage[s];
         const uint8_t *ra = st + frag_off;
         const uint8_t *rb = st + GC::GRP + frag_off;
-        if constexpr (B3) {
+        if constexpr (L64) {
+#pragma unroll
+            for (int j = 0; j < FW / 32; ++j) {
+#pragma unroll
+                for (int tau = 0; tau < 2; ++tau) {
+                    uint2 xa = *reinterpret_cast<const uint2 *>(ra + 128 * j + 16 * tau);
+                    uint2 ya = *reinterpret_cast<const uint2 *>(rb + 128 * j + 16 * tau);
+                    if constexpr (RND) {
+                        xa = make_uint2(tf32_rna_bits(xa.x), tf32_rna_bits(xa.y));
+                        ya = make_uint2(tf32_rna_bits(ya.x), tf32_rna_bits(ya.y));
+                    }
+                    mma_tf32(acc[2 * j + tau], xa.x, xa.y, ya.x, ya.y, vb0[slot], vb1[slot]);
+                    if constexpr (NH == 2) {
+                        mma_tf32(acc1[2 * j + tau], xa.x, xa.y, ya.x, ya.y, vc0[slot & SM1], vc1[slot & SM1]);
+                    }
+                }
+            }
+        } else if constexpr (B3) {
             // rows t (k = t, gather x) and t + 4 (gather y); per 8-feature group j: LDS.128 of the
             // high halves + LDS.64 of the bytes 15..8; one PRMT per element rebuilds the TF32
             // operand (byte 0 is don't-care: the tensor core reads bits 31..13 only)
@@ -1160,6 +1188,15 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
             const int64_t lr = lr0 + 2 * t + s2;
             if (!remap || lr < p.rows) {
                 const int64_t orow = remap ? (rmap ? (int64_t)__ldg(rmap + lr) : lr) : lr;
+                if constexpr (L64) {  // tile 2j + tau: features 32j + 2 slot(g, tau) + {0, 1}
+                    float *d = base + orow * ld + 2 * l64_slot;
+#pragma unroll
+                    for (int j = 0; j < FW / 32; ++j)
+#pragma unroll
+                        for (int tau = 0; tau < 2; ++tau)
+                            st_cs(d + 32 * j + 4 * tau, a[2 * j + tau][s2], a[2 * j + tau][2 + s2]);
+                    continue;
+                }
                 if constexpr (LDSM) {  // tile mt: features 16mt + g (c0/c1) and 16mt + 8 + g (c2/c3)
                     float *d = base + orow * ld + g;
 #pragma unroll
@@ -1209,6 +1246,18 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     auto add_tile = [&](const float *src, auto &a) {
 #pragma unroll
         for (int s2 = 0; s2 < 2; ++s2) {
+            if constexpr (L64) {
+                const float *row = src + (2 * t + s2) * FW + 2 * l64_slot;
+#pragma unroll
+                for (int j = 0; j < FW / 32; ++j)
+#pragma unroll
+                    for (int tau = 0; tau < 2; ++tau) {
+                        const float2 v = __ldcg(reinterpret_cast<const float2 *>(row + 32 * j + 4 * tau));
+                        a[2 * j + tau][s2] += v.x;
+                        a[2 * j + tau][2 + s2] += v.y;
+                    }
+                continue;
+            }
             if constexpr (LDSM) {
                 const float *row = src + (2 * t + s2) * FW + g;
 #pragma unroll
@@ -1482,12 +1531,12 @@ accspmm_status launch_cfg(const KParams &kp, int64_t n_units, cudaStream_t strea
 template <int FW, bool F16, int WARPS, int STAGES, bool RND = false, int MINB = 1, int NM = 1, bool LDSM = false,
           bool K8 = false, int VD = 1, int PF256 = 0, int VST = 0, bool HYB = false, int CX = (VST ? 4 : 0),
           bool B3 = false, bool DEC64 = false, int EL = 1, bool HT = true, bool PIN = false, bool DYN = false,
-          int BS = 1, int WT = 0, int WH = 8>
+          int BS = 1, int WT = 0, int WH = 8, bool L64 = false>
 accspmm_status launch_g4(const KParams &kp, const G4Maps *map, int64_t n_units, cudaStream_t stream)
 {
     using SM = G4Smem<FW, F16, STAGES, VST, CX, B3, BS, WH / 8>;
     const size_t smem = sizeof(SM) * WARPS;
-    auto kern = spmm_bittcf_g4_kernel<FW, F16, WARPS, STAGES, RND, MINB, NM, LDSM, K8, VD, PF256, VST, HYB, CX, B3, DEC64, EL, HT, PIN, DYN, BS, WT, WH>;
+    auto kern = spmm_bittcf_g4_kernel<FW, F16, WARPS, STAGES, RND, MINB, NM, LDSM, K8, VD, PF256, VST, HYB, CX, B3, DEC64, EL, HT, PIN, DYN, BS, WT, WH, L64>;
     static int configured_device = -1;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -1511,7 +1560,8 @@ accspmm_status launch_g4(const KParams &kp, const G4Maps *map, int64_t n_units, 
 // TMA tensor maps of B (2D: K rows x width columns, box = BOXE x 1 for gather4), cached in
 // the plan; one per feature slice when the slices fit G4Maps (see G4Maps)
 // b3: B is the 3-byte TF32 image (3N bytes per row, slices of 3FW bytes, u16 map elements)
-accspmm_status tensor_map(const DevicePlan &d, const KParams &kp, int FW, bool multi, bool b3, const G4Maps **out)
+accspmm_status tensor_map(const DevicePlan &d, const KParams &kp, int FW, bool multi, bool b3, const G4Maps **out,
+                          bool l64 = false)
 {
     const void *B = kp.B;
     const int64_t N = kp.N;
@@ -1519,7 +1569,7 @@ accspmm_status tensor_map(const DevicePlan &d, const KParams &kp, int FW, bool m
     const int pv = knobs().l2promo;
     const uint64_t key[4] = {(uint64_t)(uintptr_t)B, (uint64_t)N, (uint64_t)FW,
                              (uint64_t)(d.precision + 1) | ((uint64_t)nm << 8) | ((uint64_t)pv << 16) |
-                                 ((uint64_t)b3 << 24)};
+                                 ((uint64_t)b3 << 24) | ((uint64_t)l64 << 25)};
     G4Maps *maps = reinterpret_cast<G4Maps *>(d.tmap);
     static_assert(sizeof(G4Maps) <= sizeof(d.tmap), "tensor-map cache too small");
     if (!(key[0] == d.tmap_key[0] && key[1] == d.tmap_key[1] && key[2] == d.tmap_key[2] && key[3] == d.tmap_key[3])) {
@@ -1546,7 +1596,8 @@ accspmm_status tensor_map(const DevicePlan &d, const KParams &kp, int FW, bool m
             cuuint64_t dims[2] = {(cuuint64_t)(nm > 1 ? slice_e : row_e), (cuuint64_t)d.K};
             cuuint64_t strides[1] = {(cuuint64_t)(b3 ? 3 * N : N * es)};
             // G4Cfg::BOXE: the slice plus 32 bytes
-            cuuint32_t box[2] = {(cuuint32_t)(b3 ? (3 * FW + 32) / 2 : FW + (f16 ? 16 : 8)), 1u};
+            // (L64: the slice plus 16 bytes)
+            cuuint32_t box[2] = {(cuuint32_t)(b3 ? (3 * FW + 32) / 2 : FW + (f16 ? 16 : l64 ? 4 : 8)), 1u};
             cuuint32_t estr[2] = {1u, 1u};
             void *base = const_cast<char *>(reinterpret_cast<const char *>(B)) + (size_t)m * FW * (b3 ? 3 : es);
             CUresult r = encode(&maps->m[m], (f16 || b3) ? CU_TENSOR_MAP_DATA_TYPE_UINT16 : CU_TENSOR_MAP_DATA_TYPE_UINT32, 2,
@@ -1588,7 +1639,9 @@ accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, 
     const bool multi = map_count(kp) > 1 && kcfg != 20 && kcfg != 46;
     static const G4Maps no_maps = {};  // no TC blocks (e.g. K = 0): no TMA is ever issued
     if (kcfg < 0 || kcfg >= 20) {
-        accspmm_status st = d.NB > 0 ? tensor_map(d, kp, FW, multi, b3, &map) : (map = &no_maps, ACCSPMM_OK);
+        // L64 layout (kcfg 87/88): TF32 rows FW + 4 elements apart
+        const bool l64 = !F16 && FW >= 32 && !rnd && (kcfg == 87 || kcfg == 88) && d.wh == 8;
+        accspmm_status st = d.NB > 0 ? tensor_map(d, kp, FW, multi, b3, &map, l64) : (map = &no_maps, ACCSPMM_OK);
         if (st != ACCSPMM_OK) return st;
     }
     constexpr int NM = kMaxSliceMaps;
@@ -1748,6 +1801,20 @@ accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, 
         case 86:  // deep ring (70), stage barriers packed at the head
             if (multi) return launch_g4<FW, F16, 1, 3, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, true, 0, 0>(kp, map, n_units, stream);
             return launch_g4<FW, F16, 1, 3, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, true, 0, 0>(kp, map, n_units, stream);
+        case 87:  // TF32 FW >= 32: m16n8k8 fed by two LDS.64 per tile (L64 layout, no register moves)
+            if constexpr (!F16 && FW >= 32) {
+                if (d.wh != 8) break;
+                if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, false, 1, 0, 8, true>(kp, map, n_units, stream);
+                return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, false, 1, 0, 8, true>(kp, map, n_units, stream);
+            }
+            break;
+        case 88:  // L64 at 24 resident warps (FW 128: the k8 MMAs need fewer accumulator temporaries)
+            if constexpr (!F16 && FW >= 32) {
+                if (d.wh != 8) break;
+                if (multi) return launch_g4<FW, F16, 1, 2, false, MW + 4, NM, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, false, 1, 0, 8, true>(kp, map, n_units, stream);
+                return launch_g4<FW, F16, 1, 2, false, MW + 4, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, false, 1, 0, 8, true>(kp, map, n_units, stream);
+            }
+            break;
         case 62:  // default kernel with the 64-bit shift decode (tile_rank) instead of the 32-bit one
             if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, true>(kp, map, n_units, stream);
             return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, true>(kp, map, n_units, stream);
