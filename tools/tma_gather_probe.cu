@@ -50,10 +50,14 @@ __global__ void __launch_bounds__(32) probe_kernel(const __grid_constant__ CUten
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
     const uint32_t stage_bytes = (uint32_t)reqs * 4u * (uint32_t)box_bytes;
     // row ids from a counter hash (no dependent index loads in the issue loop)
-    uint32_t ctr = blockIdx.x * 0x9E3779B9u;
+    // per-CTA start and odd stride (a shared stride made CTA b + 1 request CTA b's rows one step
+    // later, so all SMs hit the same L2 lines at once; results before this fix understate the rate)
+    auto mix = [](uint32_t h) { h ^= h >> 16; h *= 0x7feb352du; h ^= h >> 15; h *= 0x846ca68bu; h ^= h >> 16; return h; };
+    uint32_t ctr = mix(blockIdx.x * 2u + 1u);
+    const uint32_t stride = mix(blockIdx.x ^ 0x5bd1e995u) | 1u;
     const uint32_t K = (uint32_t)nrows_idx;
     auto next_row = [&]() -> int32_t {
-        uint32_t h = (ctr += 0x9E3779B9u);
+        uint32_t h = (ctr += stride);
         h ^= h >> 16; h *= 0x7feb352du; h ^= h >> 15; h *= 0x846ca68bu; h ^= h >> 16;
         return (int32_t)__umulhi(h, K);
     };
