@@ -134,3 +134,56 @@ def test_tall_mma_full_size_reddit_sampled(precision):
     assert np.isfinite(Cg).all()
     rows = np.sort(np.random.default_rng(0).choice(A.M, 3000, replace=False))
     assert_within(Cg, A, v, B, precision, rows=rows)
+
+
+@pytest.mark.parametrize("precision", PREC)
+def test_tall_mma_fused_allgather_epilogue(precision):
+    """accspmm_execute_allgather with 16-row windows: both accumulator halves of every window go
+    to every destination in original row order (3 parts, 3 local destinations, split windows,
+    reordering; integer data bit-exact)."""
+    import torch
+    A = gen.dcsbm(4000, 200_000, 6, 2.2, 0.2, 2500, seed=3, oversample=1.3)
+    v = gen.values_int(A.nnz, 1)
+    B = gen.dense_int(A.K, 128, 2)
+    Bd = to_dev_B(B, precision)
+    dsts = [torch.full((A.M, 128), float("nan"), device="cuda") for _ in range(3)]
+    for part in range(3):
+        p = acc.Plan(A.M, A.K, A.rowptr, A.colidx, v, precision=precision, reorder="on", balance="on",
+                     unit_cap=32, part=part, nparts=3, **tall())
+        p.execute_allgather(Bd, dsts)
+    torch.cuda.synchronize()
+    for d in dsts:
+        assert_bit_exact(d.cpu().numpy(), A, v, B, precision)
+
+
+@pytest.mark.parametrize("precision", PREC)
+def test_tall_mma_cuda_graph_and_host_batch(precision):
+    """The plan replays under CUDA-graph capture and through the pipelined host batch API with
+    the same bits as a plain execute."""
+    import torch
+    A = gen.dcsbm(3000, 150_000, 5, 2.2, 0.2, 2000, seed=9, oversample=1.3)
+    v = gen.values_int(A.nnz, 1)
+    B0 = gen.dense_int(A.K, 64, 2)
+    p = acc.Plan(A.M, A.K, A.rowptr, A.colidx, v, precision=precision, reorder="on", balance="on", unit_cap=32,
+                 **tall())
+    Bd = to_dev_B(B0, precision)
+    ref = p.execute(Bd).cpu().numpy()
+    assert_bit_exact(ref, A, v, B0, precision)
+    C = torch.full((A.M, 64), float("nan"), device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        p.execute(Bd, C, s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    C.fill_(float("nan"))
+    torch.cuda.synchronize()
+    with torch.cuda.graph(g, stream=s):
+        p.execute(Bd, C, s)
+    g.replay()
+    torch.cuda.synchronize()
+    assert np.array_equal(C.cpu().numpy(), ref)
+    Bh = [Bd.cpu().pin_memory() for _ in range(3)]
+    Ch = [torch.full((A.M, 64), float("nan")).pin_memory() for _ in range(3)]
+    p.execute_host_batch(Bh, Ch)
+    for c in Ch:
+        assert np.array_equal(c.numpy(), ref)
