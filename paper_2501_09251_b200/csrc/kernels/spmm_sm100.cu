@@ -609,7 +609,7 @@ struct G4Cfg {
 // BS = barrier stride in 8-byte words (1: packed; 2: one 16-byte slot per stage barrier;
 // 16: one 128-byte line each -- measurement variants)
 template <int FW, bool F16, int STAGES, int VST = 0, int CX = (VST ? 4 : 0), bool B3 = false, int BS = 1,
-          int NWD = 1>
+          int NWD = 1, int PAD = 0>
 struct G4WarpSmem {
     alignas(128) uint8_t stage[STAGES][G4Cfg<FW, F16, B3>::STAGE_AL];
     ChunkSmemT<CX, NWD> ch[VST ? 3 : 2];
@@ -617,6 +617,7 @@ struct G4WarpSmem {
     uint64_t vbar[2];
     uint32_t vlo[2];  // first staged value index per buffer (0xFFFFFFFF: over VST, values from L2)
     alignas(16) uint8_t vals[VST ? 2 : 1][VST ? VST * (F16 ? 2 : 4) : 16];
+    uint8_t pad[PAD > 0 ? PAD : 1];  // measurement variants: per-CTA shared-memory footprint
 };
 // the same fields with the stage barriers at the head of the warp's area (BS = 0 in the kernel)
 template <int FW, bool F16, int STAGES, int VST = 0, int CX = (VST ? 4 : 0), bool B3 = false>
@@ -628,9 +629,9 @@ struct G4WarpSmemHead {
     ChunkSmemT<CX> ch[VST ? 3 : 2];
     alignas(16) uint8_t vals[VST ? 2 : 1][VST ? VST * (F16 ? 2 : 4) : 16];
 };
-template <int FW, bool F16, int STAGES, int VST, int CX, bool B3, int BS, int NWD = 1>
+template <int FW, bool F16, int STAGES, int VST, int CX, bool B3, int BS, int NWD = 1, int PAD = 0>
 using G4Smem = std::conditional_t<BS == 0, G4WarpSmemHead<FW, F16, STAGES, VST, CX, B3>,
-                                  G4WarpSmem<FW, F16, STAGES, VST, CX, B3, BS, NWD>>;
+                                  G4WarpSmem<FW, F16, STAGES, VST, CX, B3, BS, NWD, PAD>>;
 static_assert(sizeof(ChunkSmemT<0>) % 16 == 0 && sizeof(ChunkSmemT<4>) % 16 == 0 && sizeof(ChunkSmemT<0, 2>) % 16 == 0,
               "chunk alignment (cp.async 16 B into a2b)");
 
@@ -660,7 +661,7 @@ inline int map_count(const KParams &kp) { return kp.nslices > 1 && kp.nslices <=
 template <int FW, bool F16, int WARPS, int STAGES, bool RND, int MINB = 1, int NM = 1, bool LDSM_ = false,
           bool K8 = false, int VD = 1, int PF256 = 0, int VST = 0, bool HYB = false, int CX = (VST ? 4 : 0),
           bool B3 = false, bool DEC64 = false, int EL = 1, bool HT = true, bool PIN = false, bool DYN = false,
-          int BS = 1, int WT = 0, int WH = 8, bool L64 = false>
+          int BS = 1, int WT = 0, int WH = 8, bool L64 = false, int PAD = 0>
 __global__ void __launch_bounds__(WARPS * 32, MINB)
     spmm_bittcf_g4_kernel(const KParams p, const __grid_constant__ G4MapsT<NM> maps)
 {
@@ -691,7 +692,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     constexpr int CH = kChunk;  // blocks per staged chunk
     using CF = Cfg<FW, F16>;
     using GC = G4Cfg<FW, F16, B3>;
-    using SM = G4Smem<FW, F16, STAGES, VST, CX, B3, BS, WH / 8>;
+    using SM = G4Smem<FW, F16, STAGES, VST, CX, B3, BS, WH / 8, PAD>;
     constexpr int RS = L64 ? (FW + 4) * 4 : GC::RS;
     static_assert(!L64 || RS % 128 == 16, "L64 row stride");
     static_assert(!B3 || (!RND && !HYB && VST == 0 && !LDSM_), "B3: pre-rounded B, default ring");
@@ -1531,12 +1532,12 @@ accspmm_status launch_cfg(const KParams &kp, int64_t n_units, cudaStream_t strea
 template <int FW, bool F16, int WARPS, int STAGES, bool RND = false, int MINB = 1, int NM = 1, bool LDSM = false,
           bool K8 = false, int VD = 1, int PF256 = 0, int VST = 0, bool HYB = false, int CX = (VST ? 4 : 0),
           bool B3 = false, bool DEC64 = false, int EL = 1, bool HT = true, bool PIN = false, bool DYN = false,
-          int BS = 1, int WT = 0, int WH = 8, bool L64 = false>
+          int BS = 1, int WT = 0, int WH = 8, bool L64 = false, int PAD = 0>
 accspmm_status launch_g4(const KParams &kp, const G4Maps *map, int64_t n_units, cudaStream_t stream)
 {
-    using SM = G4Smem<FW, F16, STAGES, VST, CX, B3, BS, WH / 8>;
+    using SM = G4Smem<FW, F16, STAGES, VST, CX, B3, BS, WH / 8, PAD>;
     const size_t smem = sizeof(SM) * WARPS;
-    auto kern = spmm_bittcf_g4_kernel<FW, F16, WARPS, STAGES, RND, MINB, NM, LDSM, K8, VD, PF256, VST, HYB, CX, B3, DEC64, EL, HT, PIN, DYN, BS, WT, WH, L64>;
+    auto kern = spmm_bittcf_g4_kernel<FW, F16, WARPS, STAGES, RND, MINB, NM, LDSM, K8, VD, PF256, VST, HYB, CX, B3, DEC64, EL, HT, PIN, DYN, BS, WT, WH, L64, PAD>;
     static int configured_device = -1;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -1815,6 +1816,21 @@ accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, 
                 return launch_g4<FW, F16, 1, 2, false, MW + 4, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, false, 1, 0, 8, true>(kp, map, n_units, stream);
             }
             break;
+        case 90:  // deep ring (70) + 128 B of shared-memory padding per CTA
+            if (multi) return launch_g4<FW, F16, 1, 3, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, true, 1, 0, 8, false, 128>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 3, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, true, 1, 0, 8, false, 128>(kp, map, n_units, stream);
+        case 91:  // deep ring (70) + 512 B of padding per CTA
+            if (multi) return launch_g4<FW, F16, 1, 3, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, true, 1, 0, 8, false, 512>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 3, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, true, 1, 0, 8, false, 512>(kp, map, n_units, stream);
+        case 92:  // deep ring (70) + 1 KB of padding per CTA
+            if (multi) return launch_g4<FW, F16, 1, 3, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, true, 1, 0, 8, false, 1024>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 3, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, true, 1, 0, 8, false, 1024>(kp, map, n_units, stream);
+        case 93:  // default ring + 128 B of padding per CTA
+            if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, false, 1, 0, 8, false, 128>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, false, 1, 0, 8, false, 128>(kp, map, n_units, stream);
+        case 94:  // default ring + 1 KB of padding per CTA
+            if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, false, 1, 0, 8, false, 1024>(kp, map, n_units, stream);
+            return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, false, 1, 0, 8, false, 1024>(kp, map, n_units, stream);
         case 62:  // default kernel with the 64-bit shift decode (tile_rank) instead of the 32-bit one
             if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, true>(kp, map, n_units, stream);
             return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, true>(kp, map, n_units, stream);
