@@ -609,7 +609,7 @@ struct G4Cfg {
 // BS = barrier stride in 8-byte words (1: packed; 2: one 16-byte slot per stage barrier;
 // 16: one 128-byte line each -- measurement variants)
 template <int FW, bool F16, int STAGES, int VST = 0, int CX = (VST ? 4 : 0), bool B3 = false, int BS = 1,
-          int NWD = 1, int PAD = 0>
+          int NWD = 1>
 struct G4WarpSmem {
     alignas(128) uint8_t stage[STAGES][G4Cfg<FW, F16, B3>::STAGE_AL];
     ChunkSmemT<CX, NWD> ch[VST ? 3 : 2];
@@ -617,7 +617,11 @@ struct G4WarpSmem {
     uint64_t vbar[2];
     uint32_t vlo[2];  // first staged value index per buffer (0xFFFFFFFF: over VST, values from L2)
     alignas(16) uint8_t vals[VST ? 2 : 1][VST ? VST * (F16 ? 2 : 4) : 16];
-    uint8_t pad[PAD > 0 ? PAD : 1];  // measurement variants: per-CTA shared-memory footprint
+};
+// measurement variants: the same layout with PAD more bytes of per-CTA shared-memory footprint
+template <typename Base, int PAD>
+struct G4Padded : Base {
+    uint8_t pad[PAD];
 };
 // the same fields with the stage barriers at the head of the warp's area (BS = 0 in the kernel)
 template <int FW, bool F16, int STAGES, int VST = 0, int CX = (VST ? 4 : 0), bool B3 = false>
@@ -630,8 +634,10 @@ struct G4WarpSmemHead {
     alignas(16) uint8_t vals[VST ? 2 : 1][VST ? VST * (F16 ? 2 : 4) : 16];
 };
 template <int FW, bool F16, int STAGES, int VST, int CX, bool B3, int BS, int NWD = 1, int PAD = 0>
-using G4Smem = std::conditional_t<BS == 0, G4WarpSmemHead<FW, F16, STAGES, VST, CX, B3>,
-                                  G4WarpSmem<FW, F16, STAGES, VST, CX, B3, BS, NWD, PAD>>;
+using G4Smem = std::conditional_t<
+    BS == 0, G4WarpSmemHead<FW, F16, STAGES, VST, CX, B3>,
+    std::conditional_t<PAD == 0, G4WarpSmem<FW, F16, STAGES, VST, CX, B3, BS, NWD>,
+                       G4Padded<G4WarpSmem<FW, F16, STAGES, VST, CX, B3, BS, NWD>, (PAD > 0 ? PAD : 1)>>>;
 static_assert(sizeof(ChunkSmemT<0>) % 16 == 0 && sizeof(ChunkSmemT<4>) % 16 == 0 && sizeof(ChunkSmemT<0, 2>) % 16 == 0,
               "chunk alignment (cp.async 16 B into a2b)");
 
@@ -697,7 +703,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     static_assert(!L64 || RS % 128 == 16, "L64 row stride");
     static_assert(!B3 || (!RND && !HYB && VST == 0 && !LDSM_), "B3: pre-rounded B, default ring");
     static_assert(VST == 0 || CX >= 1, "value staging reads the TCOffset after the chunk");
-    static_assert(offsetof(SM, bar) % 16 == 0, "stage mbarriers 16-byte aligned (measured: 2.2x slower otherwise)");
+    using SMB = G4Smem<FW, F16, STAGES, VST, CX, B3, BS, WH / 8>;  // the layout without padding
+    static_assert(offsetof(SMB, bar) % 16 == 0, "stage mbarriers 16-byte aligned (measured: 2.2x slower otherwise)");
     constexpr int BSTR = BS == 0 ? 1 : BS;  // barrier stride (BS = 0: packed, at the head)
     using V = typename CF::V;
     constexpr int MT = CF::MT;
@@ -1640,8 +1647,8 @@ accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, 
     const bool multi = map_count(kp) > 1 && kcfg != 20 && kcfg != 46;
     static const G4Maps no_maps = {};  // no TC blocks (e.g. K = 0): no TMA is ever issued
     if (kcfg < 0 || kcfg >= 20) {
-        // L64 layout (kcfg 87/88): TF32 rows FW + 4 elements apart
-        const bool l64 = !F16 && FW >= 32 && !rnd && (kcfg == 87 || kcfg == 88) && d.wh == 8;
+        // L64 layout (kcfg 87): TF32 rows FW + 4 elements apart
+        const bool l64 = !F16 && FW >= 32 && !rnd && kcfg == 87 && d.wh == 8;
         accspmm_status st = d.NB > 0 ? tensor_map(d, kp, FW, multi, b3, &map, l64) : (map = &no_maps, ACCSPMM_OK);
         if (st != ACCSPMM_OK) return st;
     }
@@ -1754,24 +1761,9 @@ accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, 
         case 70:  // deep ring: 3 stages, TMA and values 2 blocks ahead, run-time stage index
             if (multi) return launch_g4<FW, F16, 1, 3, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, true>(kp, map, n_units, stream);
             return launch_g4<FW, F16, 1, 3, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, true>(kp, map, n_units, stream);
-        case 71:  // deep ring: 4 stages, TMA and values 3 blocks ahead, run-time stage index
-            if (multi) return launch_g4<FW, F16, 1, 4, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, true>(kp, map, n_units, stream);
-            return launch_g4<FW, F16, 1, 4, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, true>(kp, map, n_units, stream);
-        case 72:  // deep ring: 3 stages at 4 fewer resident warps (TF32 FW 128: smem for the 3rd stage)
-            if (multi) return launch_g4<FW, F16, 1, 3, false, MW - 4, NM, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, true>(kp, map, n_units, stream);
-            return launch_g4<FW, F16, 1, 3, false, MW - 4, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, true>(kp, map, n_units, stream);
         case 73:  // values by one coalesced warp load per block + shuffles (PF256 3)
             if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 3, 0, false, 0, false, false, 1, false>(kp, map, n_units, stream);
             return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 3, 0, false, 0, false, false, 1, false>(kp, map, n_units, stream);
-        case 74:  // deep ring (3 stages) + coalesced values
-            if (multi) return launch_g4<FW, F16, 1, 3, false, MW, NM, LD, K8, 1, 3, 0, false, 0, false, false, 1, false, false, true>(kp, map, n_units, stream);
-            return launch_g4<FW, F16, 1, 3, false, MW, 1, LD, K8, 1, 3, 0, false, 0, false, false, 1, false, false, true>(kp, map, n_units, stream);
-        case 75:  // deep ring (3 stages), one 16-byte slot per stage barrier
-            if (multi) return launch_g4<FW, F16, 1, 3, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, true, 2>(kp, map, n_units, stream);
-            return launch_g4<FW, F16, 1, 3, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, true, 2>(kp, map, n_units, stream);
-        case 76:  // deep ring (3 stages), one 128-byte line per stage barrier
-            if (multi) return launch_g4<FW, F16, 1, 3, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, true, 16>(kp, map, n_units, stream);
-            return launch_g4<FW, F16, 1, 3, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, true, 16>(kp, map, n_units, stream);
         case 77:  // default kernel, one 16-byte slot per stage barrier
             if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, false, 2>(kp, map, n_units, stream);
             return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, false, 2>(kp, map, n_units, stream);
@@ -1784,24 +1776,9 @@ accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, 
         case 80:  // default kernel, stage wait by test_wait spin
             if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, false, 1, 2>(kp, map, n_units, stream);
             return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, false, 1, 2>(kp, map, n_units, stream);
-        case 81:  // default + 16-byte barrier slots (77), try_wait without hint
-            if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, false, 2, 1>(kp, map, n_units, stream);
-            return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, false, 2, 1>(kp, map, n_units, stream);
-        case 82:  // default + 16-byte barrier slots (77), test_wait spin
-            if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, false, 2, 2>(kp, map, n_units, stream);
-            return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, false, 2, 2>(kp, map, n_units, stream);
-        case 83:  // deep ring (70), try_wait without hint
-            if (multi) return launch_g4<FW, F16, 1, 3, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, true, 1, 1>(kp, map, n_units, stream);
-            return launch_g4<FW, F16, 1, 3, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, true, 1, 1>(kp, map, n_units, stream);
-        case 84:  // deep ring (70), test_wait spin
-            if (multi) return launch_g4<FW, F16, 1, 3, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, true, 1, 2>(kp, map, n_units, stream);
-            return launch_g4<FW, F16, 1, 3, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, true, 1, 2>(kp, map, n_units, stream);
         case 85:  // default kernel, stage barriers packed at the head of the warp's area
             if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, false, 0, 0>(kp, map, n_units, stream);
             return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, false, 0, 0>(kp, map, n_units, stream);
-        case 86:  // deep ring (70), stage barriers packed at the head
-            if (multi) return launch_g4<FW, F16, 1, 3, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, true, 0, 0>(kp, map, n_units, stream);
-            return launch_g4<FW, F16, 1, 3, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, true, 0, 0>(kp, map, n_units, stream);
         case 87:  // TF32 FW >= 32: m16n8k8 fed by two LDS.64 per tile (L64 layout, no register moves)
             if constexpr (!F16 && FW >= 32) {
                 if (d.wh != 8) break;
@@ -1809,28 +1786,9 @@ accspmm_status launch_fw(const KParams &kp, const DevicePlan &d, const void *B, 
                 return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, false, 1, 0, 8, true>(kp, map, n_units, stream);
             }
             break;
-        case 88:  // L64 at 24 resident warps (FW 128: the k8 MMAs need fewer accumulator temporaries)
-            if constexpr (!F16 && FW >= 32) {
-                if (d.wh != 8) break;
-                if (multi) return launch_g4<FW, F16, 1, 2, false, MW + 4, NM, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, false, 1, 0, 8, true>(kp, map, n_units, stream);
-                return launch_g4<FW, F16, 1, 2, false, MW + 4, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, false, 1, 0, 8, true>(kp, map, n_units, stream);
-            }
-            break;
-        case 90:  // deep ring (70) + 128 B of shared-memory padding per CTA
-            if (multi) return launch_g4<FW, F16, 1, 3, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, true, 1, 0, 8, false, 128>(kp, map, n_units, stream);
-            return launch_g4<FW, F16, 1, 3, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, true, 1, 0, 8, false, 128>(kp, map, n_units, stream);
-        case 91:  // deep ring (70) + 512 B of padding per CTA
-            if (multi) return launch_g4<FW, F16, 1, 3, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, true, 1, 0, 8, false, 512>(kp, map, n_units, stream);
-            return launch_g4<FW, F16, 1, 3, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, true, 1, 0, 8, false, 512>(kp, map, n_units, stream);
-        case 92:  // deep ring (70) + 1 KB of padding per CTA
-            if (multi) return launch_g4<FW, F16, 1, 3, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, true, 1, 0, 8, false, 1024>(kp, map, n_units, stream);
-            return launch_g4<FW, F16, 1, 3, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, true, 1, 0, 8, false, 1024>(kp, map, n_units, stream);
         case 93:  // default ring + 128 B of padding per CTA
             if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, false, 1, 0, 8, false, 128>(kp, map, n_units, stream);
             return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, false, 1, 0, 8, false, 128>(kp, map, n_units, stream);
-        case 94:  // default ring + 1 KB of padding per CTA
-            if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, false, 1, 0, 8, false, 1024>(kp, map, n_units, stream);
-            return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, false, 1, false, false, false, 1, 0, 8, false, 1024>(kp, map, n_units, stream);
         case 62:  // default kernel with the 64-bit shift decode (tile_rank) instead of the 32-bit one
             if (multi) return launch_g4<FW, F16, 1, 2, false, MW, NM, LD, K8, 1, 0, 0, false, 0, false, true>(kp, map, n_units, stream);
             return launch_g4<FW, F16, 1, 2, false, MW, 1, LD, K8, 1, 0, 0, false, 0, false, true>(kp, map, n_units, stream);

@@ -16,7 +16,7 @@ import gen  # noqa: E402
 import paper_2501_09251_b200 as acc  # noqa: E402
 from gpu_util import assert_bit_exact, assert_within, run  # noqa: E402
 
-KCFGS = ["20", "46", "47", "48", "49", "50", "51", "52", "53", "54", "55", "56", "57", "58", "59", "60", "61", "62", "63", "64", "65", "66", "68", "69", "70", "71", "72", "73", "74", "75", "76", "77", "78", "79", "80", "81", "82", "83", "84", "85", "86", "87", "88", "90", "91", "92", "93", "94", "10", "11", "12",
+KCFGS = ["20", "46", "47", "48", "49", "50", "51", "52", "53", "54", "55", "56", "57", "58", "59", "60", "61", "62", "63", "64", "65", "66", "68", "69", "70", "73", "77", "78", "79", "80", "85", "87", "93", "10", "11", "12",
          "b3", "hot"]
 
 
